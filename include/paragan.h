@@ -1,0 +1,206 @@
+/* libparagan — C-ABI of the B200-native ParaGAN hot path.
+ *
+ * The hot path is ParaGAN's replicated, data-parallel BigGAN training
+ * iteration (arXiv 2411.03999): "the accelerators execute forward and backward
+ * passes and then synchronize gradients among other accelerators"
+ * (Sec. 3.2 Computation Model), with data parallelism as the
+ * distribution strategy (Sec. 2), D and G updated one after the
+ * other (Sec. 5.1), separate optimiser settings per network
+ * (Sec. 5.2), bf16 storage with fp32 last layers
+ * and the hardware-aware layout
+ * transformation (Sec. 4.2).  BigGAN-specific
+ * readings (hinge loss, spectral norm, cross-replica BN, topology) are listed
+ * in DESIGN.md §3.
+ *
+ * Conventions
+ *  - Every function returns a paragan_status.  Arguments are validated on the
+ *    host before anything is enqueued; device work is stream-ordered on the
+ *    caller's stream (cudaStream_t passed as void*), except the NCCL
+ *    collectives, which run on the same stream.
+ *  - "device" pointers must be CUDA device memory (16-byte aligned);
+ *    "host" pointers are ordinary host memory.
+ *  - The caller owns all buffers it passes, the workspace and the stream; the
+ *    library owns the context, its NCCL communicator and its internal events.
+ *  - One host thread per context.  After a CUDA/NCCL failure the context is
+ *    poisoned: every call but paragan_last_error / paragan_destroy returns
+ *    PARAGAN_ERR_ORDER.
+ *  - There is no CPU fallback: without a usable sm_100 device, paragan_init
+ *    returns PARAGAN_ERR_CUDA.
+ */
+#ifndef PARAGAN_H_
+#define PARAGAN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PARAGAN_ABI_VERSION 1
+
+typedef struct paragan_ctx paragan_ctx; /* opaque, library-owned */
+
+typedef enum {
+  PARAGAN_OK = 0,
+  PARAGAN_ERR_INVALID_ARG = 1, /* null / misaligned pointer, bad size */
+  PARAGAN_ERR_CONFIG = 2,      /* inconsistent configuration (SPEC exit code 2) */
+  PARAGAN_ERR_NONFINITE = 3,   /* non-finite loss or gradient: update skipped (SPEC exit code 3) */
+  PARAGAN_ERR_IO = 4,
+  PARAGAN_ERR_CUDA = 5,
+  PARAGAN_ERR_NCCL = 6,
+  PARAGAN_ERR_ORDER = 7,       /* call sequence violated, or context poisoned */
+  PARAGAN_ERR_OOM = 8          /* workspace too small */
+} paragan_status;
+
+typedef enum { PARAGAN_F32 = 0, PARAGAN_BF16 = 1 } paragan_dtype;
+typedef enum { PARAGAN_NET_D = 0, PARAGAN_NET_G = 1 } paragan_net;
+
+/* Adam hyper-parameters of one network (asymmetric policy, PAPER.md:285-307;
+ * "a slightly larger epsilon" under bf16). */
+typedef struct {
+  float lr, beta1, beta2, eps;
+} paragan_adam;
+
+/* BigGAN configuration.  The architecture is derived from (resolution, ch)
+ * exactly as DESIGN.md §3 R1 states (BigGAN channel tables; 128/256/512 and the
+ * small 16/32 test resolutions). */
+typedef struct {
+  int32_t abi_version;   /* PARAGAN_ABI_VERSION */
+  int32_t resolution;    /* 16, 32, 64, 128, 256, 512 */
+  int32_t ch;            /* channel multiplier (96 for BigGAN) */
+  int32_t n_classes;     /* 1000 for ImageNet */
+  int32_t shared_dim;    /* shared class embedding (128) */
+  int32_t z_chunk;       /* hierarchical latent chunk (20); dim_z = (blocks+1)*z_chunk */
+  int32_t attn_res;      /* resolution of the non-local block (64), 0 = none */
+  int32_t local_batch;   /* B per GPU, same for D and G */
+  int32_t d_steps_per_g; /* n_d >= 1 (step ratio) */
+  paragan_dtype compute; /* F32 = exact SIMT path; BF16 = bf16 storage + tcgen05 */
+  int32_t c_pad_image;   /* channel padding of the packed image (>= 3; 8 for BF16) */
+  paragan_adam adam_d, adam_g;
+  float sn_eps, bn_eps;
+  int32_t rank, world_size, device;
+  uint64_t seed;         /* on-device weight init (paragan_init_params) */
+} paragan_config;
+
+typedef struct {
+  float d_loss, g_loss, d_real_mean, d_fake_mean;
+  int32_t nonfinite; /* a step of this iteration skipped its update */
+  int64_t t_d, t_g;  /* Adam step counts */
+} paragan_stats;
+
+/* ------------------------------------------------------------------ setup */
+
+/* 128-byte NCCL unique id; call on rank 0 and broadcast it (torch.distributed). */
+paragan_status paragan_get_unique_id(uint8_t id[128]);
+
+/* Bytes of device workspace paragan_init needs for this config (activations,
+ * weights, optimiser state, scratch). */
+paragan_status paragan_workspace_size(const paragan_config* cfg, size_t* bytes);
+
+/* Length of the canonical flat fp32 state of one network: trainable tensors in
+ * forward-layer order (conv weights OIHW, linears [out,in], embeddings
+ * [classes,dim], each weight followed by its bias), then the spectral-norm u
+ * vectors in the same layer order. */
+paragan_status paragan_param_count(const paragan_config* cfg, paragan_net net, size_t* n_state,
+                                   size_t* n_trainable);
+
+/* Create a context on cfg->device.  id: the broadcast NCCL id (ignored when
+ * world_size == 1).  workspace: device buffer of at least
+ * paragan_workspace_size bytes, owned by the caller.  stream: cudaStream_t. */
+paragan_status paragan_init(const paragan_config* cfg, const uint8_t id[128], void* workspace, size_t ws_bytes,
+                            void* stream, paragan_ctx** out);
+
+/* Seeded on-device initialisation: N(0, 0.02) weights, zero biases, unit BN
+ * gains, attention gamma = attn_gamma, unit-norm Gaussian u vectors.  Every rank
+ * with the same seed gets the identical replica. */
+paragan_status paragan_init_params(paragan_ctx* ctx, float attn_gamma);
+
+/* Canonical flat state (host, fp32, paragan_param_count n_state floats).
+ * set resets Adam moments and step counts; get/get_grads synchronise the stream.
+ * get_grads returns the all-reduced (mean) gradient of the last step of `net`
+ * (n_trainable floats). */
+paragan_status paragan_set_params(paragan_ctx* ctx, paragan_net net, const float* host, size_t n);
+paragan_status paragan_get_params(paragan_ctx* ctx, paragan_net net, float* host, size_t n);
+paragan_status paragan_get_grads(paragan_ctx* ctx, paragan_net net, float* host, size_t n);
+
+/* --------------------------------------------------------------- hot path */
+
+/* Hardware-aware layout transformation: NCHW fp32 ->
+ * NHWC with channels zero-padded to c_pad, stored as `dst` dtype (bf16 by
+ * round-to-nearest-even).  src, dst: device.  Bit-exact.  Independent of any
+ * context.  c_pad >= c; for BF16 c_pad % 8 == 0. */
+paragan_status paragan_layout_pack(const float* src_nchw, void* dst_nhwc, paragan_dtype dst, int32_t n, int32_t c,
+                                   int32_t h, int32_t w, int32_t c_pad, void* stream);
+/* Exact inverse on the first c channels (NHWC -> NCHW fp32). */
+paragan_status paragan_layout_unpack(const void* src_nhwc, paragan_dtype src, float* dst_nchw, int32_t n, int32_t c,
+                                     int32_t h, int32_t w, int32_t c_pad, void* stream);
+
+/* One discriminator step: SN(G) -> G(z, fake_y) with
+ * cross-replica BN -> SN(D) -> D([fake; real]) (one pass over 2B images,
+ * PAPER.md:243) -> hinge L_D -> backward through D -> gradient all-reduce
+ * -> Adam(D).
+ *   real_nhwc : device, [B, R, R, c_pad_image] in the compute dtype (output of
+ *               paragan_layout_pack)
+ *   real_y, fake_y : device int32 [B];  z : device fp32 [B, dim_z]
+ *   flags     : PARAGAN_FLAG_* */
+paragan_status paragan_d_step(paragan_ctx* ctx, const void* real_nhwc, const int32_t* real_y, const float* z,
+                              const int32_t* fake_y, uint32_t flags);
+
+/* One generator step: SN(G) -> G(z, y) -> SN(D) -> D(fake) -> L_G = -mean ->
+ * backward through D (inputs only) and G -> all-reduce -> Adam(G).
+ * Returns PARAGAN_ERR_ORDER unless d_steps_per_g D steps preceded it. */
+paragan_status paragan_g_step(paragan_ctx* ctx, const float* z, const int32_t* y, uint32_t flags);
+
+/* In-place mean of the net's gradient over all ranks (NCCL all-reduce over
+ * NVLink).  d_step/g_step call it themselves unless
+ * PARAGAN_FLAG_NO_ALLREDUCE is set. */
+paragan_status paragan_allreduce_grads(paragan_ctx* ctx, paragan_net net);
+
+/* Adam on the net with its own hyper-parameters; skipped
+ * (state unchanged) when the gradient is non-finite.  Pairs with
+ * PARAGAN_FLAG_NO_UPDATE. */
+paragan_status paragan_apply_update(paragan_ctx* ctx, paragan_net net);
+
+/* Losses of the last D and G steps; synchronises the stream.  Returns
+ * PARAGAN_ERR_NONFINITE when an update was skipped since the last call. */
+paragan_status paragan_sync_stats(paragan_ctx* ctx, paragan_stats* out);
+
+/* Copy the last generated images (bf16/fp32 NHWC as D saw them) to host NCHW fp32 [B,3,R,R]. */
+paragan_status paragan_get_fakes(paragan_ctx* ctx, float* host_nchw, size_t n);
+
+/* Number of kernels this context launched since creation (bench accounting). */
+paragan_status paragan_kernel_launches(const paragan_ctx* ctx, uint64_t* n);
+
+/* Live kernel timing for the roofline report: while enabled, every tcgen05
+ * convolution launch of the step is bracketed by CUDA events on the context's
+ * stream.  profile_read (synchronises) returns, for kind 0 = implicit-GEMM
+ * fprop/dgrad kernel, 1 = wgrad (incl. its split-K reduction), the number of
+ * launches, their summed device time (ms) and their ALGORITHMIC flops
+ * (2*M*N*K with unpadded channel counts).  enable=1 also clears the record. */
+paragan_status paragan_profile(paragan_ctx* ctx, int32_t enable);
+paragan_status paragan_profile_read(paragan_ctx* ctx, int32_t kind, uint64_t* launches, double* ms, double* flops);
+
+const char* paragan_last_error(const paragan_ctx* ctx);
+paragan_status paragan_destroy(paragan_ctx* ctx);
+
+#define PARAGAN_FLAG_NO_ALLREDUCE 1u /* keep the local gradient (test hook) */
+#define PARAGAN_FLAG_NO_UPDATE 2u    /* skip Adam (test hook) */
+
+/* ------------------------------------------------------- op-level test hooks
+ * Single kernels of the path, exposed so tests can compare each with the
+ * oracle.  All pointers are device pointers; shapes as stated. */
+
+/* y[N,H,W,Cout] = conv(x[N,H,W,Cin], w[Cout][k*k][Cin]) + bias[Cout]; 3x3 pad 1 or 1x1.
+ * BF16: x, w, y bf16 (tcgen05 path, Cin % 8 == 0); F32: fp32 SIMT path. */
+paragan_status paragan_op_conv_fwd(paragan_dtype dt, const void* x, int32_t n, int32_t h, int32_t w, int32_t cin,
+                                   const void* wgt, const float* bias, int32_t cout, int32_t ksz, void* y,
+                                   void* stream);
+/* dw[Cout][k*k][Cin] (fp32) = sum_p dy[p][o] * x[p + tap][c]. */
+paragan_status paragan_op_conv_wgrad(paragan_dtype dt, const void* x, const void* dy, int32_t n, int32_t h,
+                                     int32_t w, int32_t cin, int32_t cout, int32_t ksz, float* dw, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PARAGAN_H_ */

@@ -1,0 +1,274 @@
+"""Thin ctypes binding of libparagan (include/paragan.h) — argument marshalling only.
+
+Every computation happens inside libparagan.so's CUDA kernels; this module only
+converts Python/torch arguments to pointers.  There is no CPU fallback: loading
+fails loudly when the library is missing, and paragan_init fails without an
+sm_100 device.  PyTorch is used for device memory, streams and process groups.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libparagan.so")
+
+PARAGAN_ABI_VERSION = 1
+F32, BF16 = 0, 1
+NET_D, NET_G = 0, 1
+FLAG_NO_ALLREDUCE, FLAG_NO_UPDATE = 1, 2
+STATUS = {0: "OK", 1: "INVALID_ARG", 2: "CONFIG", 3: "NONFINITE", 4: "IO", 5: "CUDA", 6: "NCCL", 7: "ORDER", 8: "OOM"}
+
+
+class Adam(C.Structure):
+    _fields_ = [("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float)]
+
+
+class Config(C.Structure):
+    _fields_ = [("abi_version", C.c_int32), ("resolution", C.c_int32), ("ch", C.c_int32),
+                ("n_classes", C.c_int32), ("shared_dim", C.c_int32), ("z_chunk", C.c_int32),
+                ("attn_res", C.c_int32), ("local_batch", C.c_int32), ("d_steps_per_g", C.c_int32),
+                ("compute", C.c_int32), ("c_pad_image", C.c_int32), ("adam_d", Adam), ("adam_g", Adam),
+                ("sn_eps", C.c_float), ("bn_eps", C.c_float), ("rank", C.c_int32), ("world_size", C.c_int32),
+                ("device", C.c_int32), ("seed", C.c_uint64)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("d_loss", C.c_float), ("g_loss", C.c_float), ("d_real_mean", C.c_float),
+                ("d_fake_mean", C.c_float), ("nonfinite", C.c_int32), ("t_d", C.c_int64), ("t_g", C.c_int64)]
+
+
+class ParaganError(RuntimeError):
+    def __init__(self, fn, status, detail=""):
+        super().__init__(f"{fn} -> PARAGAN_ERR_{STATUS.get(status, status)} {detail}".strip())
+        self.status = status
+
+
+_lib = None
+SYMBOLS = {
+    "paragan_get_unique_id": (C.c_int, [C.c_void_p]),
+    "paragan_workspace_size": (C.c_int, [C.POINTER(Config), C.POINTER(C.c_size_t)]),
+    "paragan_param_count": (C.c_int, [C.POINTER(Config), C.c_int, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]),
+    "paragan_init": (C.c_int, [C.POINTER(Config), C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p,
+                               C.POINTER(C.c_void_p)]),
+    "paragan_init_params": (C.c_int, [C.c_void_p, C.c_float]),
+    "paragan_set_params": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_size_t]),
+    "paragan_get_params": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_size_t]),
+    "paragan_get_grads": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_size_t]),
+    "paragan_layout_pack": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                      C.c_int32, C.c_void_p]),
+    "paragan_layout_unpack": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+                                        C.c_int32, C.c_int32, C.c_void_p]),
+    "paragan_d_step": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32]),
+    "paragan_g_step": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32]),
+    "paragan_allreduce_grads": (C.c_int, [C.c_void_p, C.c_int]),
+    "paragan_apply_update": (C.c_int, [C.c_void_p, C.c_int]),
+    "paragan_sync_stats": (C.c_int, [C.c_void_p, C.POINTER(Stats)]),
+    "paragan_get_fakes": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t]),
+    "paragan_kernel_launches": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64)]),
+    "paragan_profile": (C.c_int, [C.c_void_p, C.c_int32]),
+    "paragan_profile_read": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_uint64), C.POINTER(C.c_double),
+                                       C.POINTER(C.c_double)]),
+    "paragan_last_error": (C.c_char_p, [C.c_void_p]),
+    "paragan_destroy": (C.c_int, [C.c_void_p]),
+    "paragan_op_conv_fwd": (C.c_int, [C.c_int, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
+                                      C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
+    "paragan_op_conv_wgrad": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                        C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
+}
+
+
+def lib():
+    """Load libparagan.so (building it first if the sources are newer)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            from . import build
+            build.build()
+        import torch  # noqa: F401  (loads the CUDA runtime / NCCL torch ships, which the .so shares)
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in SYMBOLS.items():
+            f = getattr(L, name)
+            f.restype, f.argtypes = res, args
+        _lib = L
+    return _lib
+
+
+def _check(fn, status, ctx=None):
+    if status != 0:
+        detail = ""
+        if ctx:
+            detail = lib().paragan_last_error(ctx).decode(errors="replace")
+        raise ParaganError(fn, status, detail)
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def make_config(resolution=128, ch=96, n_classes=1000, shared_dim=128, z_chunk=20, attn_res=64, local_batch=256,
+                d_steps_per_g=1, compute=BF16, c_pad_image=8, adam_d=(2e-4, 0.0, 0.999, None),
+                adam_g=(5e-5, 0.0, 0.999, None), sn_eps=1e-12, bn_eps=1e-5, rank=0, world_size=1, device=0,
+                seed=0) -> Config:
+    """BigGAN config; Adam eps defaults to 1e-6 under bf16 and 1e-8 in fp32."""
+    eps = 1e-6 if compute == BF16 else 1e-8
+    ad = Adam(adam_d[0], adam_d[1], adam_d[2], adam_d[3] if adam_d[3] is not None else eps)
+    ag = Adam(adam_g[0], adam_g[1], adam_g[2], adam_g[3] if adam_g[3] is not None else eps)
+    return Config(PARAGAN_ABI_VERSION, resolution, ch, n_classes, shared_dim, z_chunk, attn_res, local_batch,
+                  d_steps_per_g, compute, c_pad_image, ad, ag, sn_eps, bn_eps, rank, world_size, device, seed)
+
+
+def dim_z(cfg: Config) -> int:
+    nb = {16: 2, 32: 3, 64: 4, 128: 5, 256: 6, 512: 7}[cfg.resolution]
+    return (nb + 1) * cfg.z_chunk
+
+
+def workspace_size(cfg: Config) -> int:
+    n = C.c_size_t()
+    _check("paragan_workspace_size", lib().paragan_workspace_size(C.byref(cfg), C.byref(n)))
+    return n.value
+
+
+def param_count(cfg: Config, net: int):
+    ns, nt = C.c_size_t(), C.c_size_t()
+    _check("paragan_param_count", lib().paragan_param_count(C.byref(cfg), net, C.byref(ns), C.byref(nt)))
+    return ns.value, nt.value
+
+
+def get_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    _check("paragan_get_unique_id", lib().paragan_get_unique_id(buf))
+    return bytes(buf)
+
+
+def layout_pack(src_nchw, dst_nhwc, dtype: int, c_pad: int, stream=None):
+    n, c, h, w = src_nchw.shape
+    _check("paragan_layout_pack", lib().paragan_layout_pack(_ptr(src_nchw), _ptr(dst_nhwc), dtype, n, c, h, w, c_pad,
+                                                            _stream(stream)))
+
+
+def layout_unpack(src_nhwc, dtype: int, dst_nchw, c_pad: int, stream=None):
+    n, c, h, w = dst_nchw.shape
+    _check("paragan_layout_unpack", lib().paragan_layout_unpack(_ptr(src_nhwc), dtype, _ptr(dst_nchw), n, c, h, w,
+                                                                c_pad, _stream(stream)))
+
+
+def op_conv_fwd(dtype, x, wgt, bias, cout, ksz, y, stream=None):
+    n, h, w, cin = x.shape
+    _check("paragan_op_conv_fwd", lib().paragan_op_conv_fwd(dtype, _ptr(x), n, h, w, cin, _ptr(wgt), _ptr(bias), cout,
+                                                            ksz, _ptr(y), _stream(stream)))
+
+
+def op_conv_wgrad(dtype, x, dy, cout, ksz, dw, stream=None):
+    n, h, w, cin = x.shape
+    _check("paragan_op_conv_wgrad", lib().paragan_op_conv_wgrad(dtype, _ptr(x), _ptr(dy), n, h, w, cin, cout, ksz,
+                                                                _ptr(dw), _stream(stream)))
+
+
+class Context:
+    """One rank's ParaGAN training context (paragan_init .. paragan_destroy)."""
+
+    def __init__(self, cfg: Config, nccl_id: bytes | None = None, stream=None):
+        import torch
+        self.cfg = cfg
+        self.stream = stream if stream is not None else torch.cuda.current_stream(cfg.device)
+        nbytes = workspace_size(cfg)
+        self.workspace = torch.empty(nbytes + 256, dtype=torch.uint8, device=f"cuda:{cfg.device}")
+        base = self.workspace.data_ptr()
+        off = (-base) % 256
+        self.ctx = C.c_void_p()
+        idbuf = (C.c_uint8 * 128).from_buffer_copy(nccl_id) if nccl_id else None
+        st = lib().paragan_init(C.byref(cfg), idbuf, C.c_void_p(base + off), nbytes, C.c_void_p(self.stream.cuda_stream),
+                                C.byref(self.ctx))
+        if st != 0:
+            msg = lib().paragan_last_error(self.ctx).decode() if self.ctx else ""
+            if self.ctx:
+                lib().paragan_destroy(self.ctx)
+            self.ctx = None
+            raise ParaganError("paragan_init", st, msg)
+        self.n_state_d, self.n_train_d = param_count(cfg, NET_D)
+        self.n_state_g, self.n_train_g = param_count(cfg, NET_G)
+
+    def _n(self, net, state=True):
+        if net == NET_D:
+            return self.n_state_d if state else self.n_train_d
+        return self.n_state_g if state else self.n_train_g
+
+    def init_params(self, attn_gamma=0.0):
+        _check("paragan_init_params", lib().paragan_init_params(self.ctx, attn_gamma), self.ctx)
+
+    def set_params(self, net, flat):
+        import numpy as np
+        a = np.ascontiguousarray(flat, dtype=np.float32)
+        _check("paragan_set_params", lib().paragan_set_params(self.ctx, net, a.ctypes.data, a.size), self.ctx)
+
+    def get_params(self, net):
+        import numpy as np
+        a = np.empty(self._n(net), dtype=np.float32)
+        _check("paragan_get_params", lib().paragan_get_params(self.ctx, net, a.ctypes.data, a.size), self.ctx)
+        return a
+
+    def get_grads(self, net):
+        import numpy as np
+        a = np.empty(self._n(net, False), dtype=np.float32)
+        _check("paragan_get_grads", lib().paragan_get_grads(self.ctx, net, a.ctypes.data, a.size), self.ctx)
+        return a
+
+    def get_fakes(self):
+        import numpy as np
+        r = self.cfg.resolution
+        a = np.empty((self.cfg.local_batch, 3, r, r), dtype=np.float32)
+        _check("paragan_get_fakes", lib().paragan_get_fakes(self.ctx, a.ctypes.data, a.size), self.ctx)
+        return a
+
+    def d_step(self, real_nhwc, real_y, z, fake_y, flags=0):
+        _check("paragan_d_step", lib().paragan_d_step(self.ctx, _ptr(real_nhwc), _ptr(real_y), _ptr(z), _ptr(fake_y),
+                                                      flags), self.ctx)
+
+    def g_step(self, z, y, flags=0):
+        _check("paragan_g_step", lib().paragan_g_step(self.ctx, _ptr(z), _ptr(y), flags), self.ctx)
+
+    def allreduce_grads(self, net):
+        _check("paragan_allreduce_grads", lib().paragan_allreduce_grads(self.ctx, net), self.ctx)
+
+    def apply_update(self, net):
+        _check("paragan_apply_update", lib().paragan_apply_update(self.ctx, net), self.ctx)
+
+    def sync_stats(self, raise_nonfinite=True):
+        s = Stats()
+        st = lib().paragan_sync_stats(self.ctx, C.byref(s))
+        if st == 3 and not raise_nonfinite:
+            return s
+        _check("paragan_sync_stats", st, self.ctx)
+        return s
+
+    def kernel_launches(self) -> int:
+        n = C.c_uint64()
+        _check("paragan_kernel_launches", lib().paragan_kernel_launches(self.ctx, C.byref(n)), self.ctx)
+        return n.value
+
+    def profile(self, enable: bool):
+        _check("paragan_profile", lib().paragan_profile(self.ctx, 1 if enable else 0), self.ctx)
+
+    def profile_read(self, kind: int):
+        n, ms, fl = C.c_uint64(), C.c_double(), C.c_double()
+        _check("paragan_profile_read", lib().paragan_profile_read(self.ctx, kind, C.byref(n), C.byref(ms),
+                                                                  C.byref(fl)), self.ctx)
+        return n.value, ms.value, fl.value
+
+    def close(self):
+        if self.ctx:
+            lib().paragan_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

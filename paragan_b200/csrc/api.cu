@@ -1,0 +1,211 @@
+// C-ABI entry points of libparagan (include/paragan.h).  Argument checks
+// happen here, synchronously, before anything is enqueued.
+#include <nccl.h>
+
+#include <cstring>
+#include <new>
+
+#include "../../include/paragan.h"
+#include "common.cuh"
+#include "engine.h"
+#include "kernels.h"
+#include "tc_conv.h"
+
+struct paragan_ctx {
+  pg::EngineBase* eng = nullptr;
+};
+
+using namespace pg;
+
+namespace {
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+paragan_status cuda_status(cudaError_t e) { return e == cudaSuccess ? PARAGAN_OK : PARAGAN_ERR_CUDA; }
+bool device_ok(int dev) {
+  cudaDeviceProp p;
+  if (cudaGetDeviceProperties(&p, dev) != cudaSuccess) return false;
+  return p.major == 10;   // sm_100 family (B200)
+}
+}  // namespace
+
+extern "C" {
+
+paragan_status paragan_get_unique_id(uint8_t id[128]) {
+  if (!id) return PARAGAN_ERR_INVALID_ARG;
+  ncclUniqueId u;
+  if (ncclGetUniqueId(&u) != ncclSuccess) return PARAGAN_ERR_NCCL;
+  static_assert(sizeof(u) == 128, "ncclUniqueId size");
+  std::memcpy(id, &u, 128);
+  return PARAGAN_OK;
+}
+
+paragan_status paragan_workspace_size(const paragan_config* cfg, size_t* bytes) {
+  if (!cfg || !bytes) return PARAGAN_ERR_INVALID_ARG;
+  paragan_status st;
+  EngineBase* e = make_engine(cfg, nullptr, &st);
+  if (!e) return st;
+  *bytes = e->workspace_bytes();
+  delete e;
+  return PARAGAN_OK;
+}
+
+paragan_status paragan_param_count(const paragan_config* cfg, paragan_net net, size_t* n_state, size_t* n_trainable) {
+  if (!cfg || (net != PARAGAN_NET_D && net != PARAGAN_NET_G)) return PARAGAN_ERR_INVALID_ARG;
+  paragan_status st;
+  EngineBase* e = make_engine(cfg, nullptr, &st);
+  if (!e) return st;
+  e->counts(net, n_state, n_trainable);
+  delete e;
+  return PARAGAN_OK;
+}
+
+paragan_status paragan_init(const paragan_config* cfg, const uint8_t id[128], void* workspace, size_t ws_bytes,
+                            void* stream, paragan_ctx** out) {
+  if (!cfg || !workspace || !out) return PARAGAN_ERR_INVALID_ARG;
+  if (cfg->world_size > 1 && !id) return PARAGAN_ERR_INVALID_ARG;
+  *out = nullptr;
+  if (cudaSetDevice(cfg->device) != cudaSuccess || !device_ok(cfg->device)) return PARAGAN_ERR_CUDA;
+  paragan_status st;
+  EngineBase* e = make_engine(cfg, stream, &st);
+  if (!e) return st;
+  auto* ctx = new (std::nothrow) paragan_ctx;
+  if (!ctx) {
+    delete e;
+    return PARAGAN_ERR_OOM;
+  }
+  ctx->eng = e;
+  st = e->init(id, workspace, ws_bytes);
+  *out = ctx;   // returned even on failure so last_error can explain; caller destroys
+  return st;
+}
+
+paragan_status paragan_init_params(paragan_ctx* ctx, float attn_gamma) {
+  if (!ctx || !ctx->eng) return PARAGAN_ERR_INVALID_ARG;
+  return ctx->eng->init_params(attn_gamma);
+}
+paragan_status paragan_set_params(paragan_ctx* ctx, paragan_net net, const float* host, size_t n) {
+  if (!ctx || !ctx->eng) return PARAGAN_ERR_INVALID_ARG;
+  return ctx->eng->set_params(net, host, n);
+}
+paragan_status paragan_get_params(paragan_ctx* ctx, paragan_net net, float* host, size_t n) {
+  if (!ctx || !ctx->eng) return PARAGAN_ERR_INVALID_ARG;
+  return ctx->eng->get_params(net, host, n);
+}
+paragan_status paragan_get_grads(paragan_ctx* ctx, paragan_net net, float* host, size_t n) {
+  if (!ctx || !ctx->eng) return PARAGAN_ERR_INVALID_ARG;
+  return ctx->eng->get_grads(net, host, n);
+}
+
+paragan_status paragan_layout_pack(const float* src, void* dst, paragan_dtype dt, int32_t n, int32_t c, int32_t h,
+                                   int32_t w, int32_t c_pad, void* stream) {
+  if (!src || !dst || n < 0 || c < 1 || h < 1 || w < 1 || c_pad < c) return PARAGAN_ERR_INVALID_ARG;
+  if (dt == PARAGAN_BF16 && (c_pad % 8 || !aligned16(dst))) return PARAGAN_ERR_INVALID_ARG;
+  if (n == 0) return PARAGAN_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dt == PARAGAN_BF16) return cuda_status(layout_pack<bf16>(src, static_cast<bf16*>(dst), n, c, h, w, c_pad, 0, st));
+  if (dt == PARAGAN_F32) return cuda_status(layout_pack<float>(src, static_cast<float*>(dst), n, c, h, w, c_pad, 0, st));
+  return PARAGAN_ERR_INVALID_ARG;
+}
+paragan_status paragan_layout_unpack(const void* src, paragan_dtype dt, float* dst, int32_t n, int32_t c, int32_t h,
+                                     int32_t w, int32_t c_pad, void* stream) {
+  if (!src || !dst || n < 0 || c < 1 || h < 1 || w < 1 || c_pad < c) return PARAGAN_ERR_INVALID_ARG;
+  if (n == 0) return PARAGAN_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dt == PARAGAN_BF16)
+    return cuda_status(layout_unpack<bf16>(static_cast<const bf16*>(src), dst, n, c, h, w, c_pad, st));
+  if (dt == PARAGAN_F32)
+    return cuda_status(layout_unpack<float>(static_cast<const float*>(src), dst, n, c, h, w, c_pad, st));
+  return PARAGAN_ERR_INVALID_ARG;
+}
+
+paragan_status paragan_d_step(paragan_ctx* ctx, const void* real, const int32_t* real_y, const float* z,
+                              const int32_t* fake_y, uint32_t flags) {
+  if (!ctx || !ctx->eng) return PARAGAN_ERR_INVALID_ARG;
+  return ctx->eng->d_step(real, real_y, z, fake_y, flags);
+}
+paragan_status paragan_g_step(paragan_ctx* ctx, const float* z, const int32_t* y, uint32_t flags) {
+  if (!ctx || !ctx->eng) return PARAGAN_ERR_INVALID_ARG;
+  return ctx->eng->g_step(z, y, flags);
+}
+paragan_status paragan_allreduce_grads(paragan_ctx* ctx, paragan_net net) {
+  if (!ctx || !ctx->eng || (net != PARAGAN_NET_D && net != PARAGAN_NET_G)) return PARAGAN_ERR_INVALID_ARG;
+  return ctx->eng->allreduce(net);
+}
+paragan_status paragan_apply_update(paragan_ctx* ctx, paragan_net net) {
+  if (!ctx || !ctx->eng || (net != PARAGAN_NET_D && net != PARAGAN_NET_G)) return PARAGAN_ERR_INVALID_ARG;
+  return ctx->eng->update(net);
+}
+paragan_status paragan_sync_stats(paragan_ctx* ctx, paragan_stats* out) {
+  if (!ctx || !ctx->eng) return PARAGAN_ERR_INVALID_ARG;
+  return ctx->eng->sync_stats(out);
+}
+paragan_status paragan_get_fakes(paragan_ctx* ctx, float* host, size_t n) {
+  if (!ctx || !ctx->eng) return PARAGAN_ERR_INVALID_ARG;
+  return ctx->eng->get_fakes(host, n);
+}
+paragan_status paragan_kernel_launches(const paragan_ctx* ctx, uint64_t* n) {
+  if (!ctx || !ctx->eng || !n) return PARAGAN_ERR_INVALID_ARG;
+  *n = ctx->eng->launches();
+  return PARAGAN_OK;
+}
+paragan_status paragan_profile(paragan_ctx* ctx, int32_t enable) {
+  if (!ctx || !ctx->eng) return PARAGAN_ERR_INVALID_ARG;
+  return ctx->eng->profile(enable);
+}
+paragan_status paragan_profile_read(paragan_ctx* ctx, int32_t kind, uint64_t* launches, double* ms, double* flops) {
+  if (!ctx || !ctx->eng || kind < 0 || kind > 1) return PARAGAN_ERR_INVALID_ARG;
+  return ctx->eng->profile_read(kind, launches, ms, flops);
+}
+const char* paragan_last_error(const paragan_ctx* ctx) {
+  if (!ctx || !ctx->eng) return "null context";
+  return ctx->eng->last_error();
+}
+paragan_status paragan_destroy(paragan_ctx* ctx) {
+  if (!ctx) return PARAGAN_ERR_INVALID_ARG;
+  delete ctx->eng;
+  delete ctx;
+  return PARAGAN_OK;
+}
+
+paragan_status paragan_op_conv_fwd(paragan_dtype dt, const void* x, int32_t n, int32_t h, int32_t w, int32_t cin,
+                                   const void* wgt, const float* bias, int32_t cout, int32_t ksz, void* y,
+                                   void* stream) {
+  if (!x || !wgt || !y || n < 1 || h < 1 || w < 1 || cin < 1 || cout < 1 || (ksz != 1 && ksz != 3))
+    return PARAGAN_ERR_INVALID_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dt == PARAGAN_BF16) {
+    if (cin % 8 || !aligned16(x) || !aligned16(wgt) || !aligned16(y)) return PARAGAN_ERR_INVALID_ARG;
+    TcEpilogue e;
+    e.bias = bias;
+    e.out = y;
+    return cuda_status(tc_conv_fprop(x, n, h, w, cin, wgt, cout, ksz, e, st));
+  }
+  if (dt == PARAGAN_F32)
+    return cuda_status(simt_conv_fwd<float, float, float>(static_cast<const float*>(x), n, h, w, cin,
+                                                          static_cast<const float*>(wgt), cout, ksz, bias, nullptr,
+                                                          nullptr, 0, static_cast<float*>(y), st));
+  return PARAGAN_ERR_INVALID_ARG;
+}
+
+paragan_status paragan_op_conv_wgrad(paragan_dtype dt, const void* x, const void* dy, int32_t n, int32_t h, int32_t w,
+                                     int32_t cin, int32_t cout, int32_t ksz, float* dw, void* stream) {
+  if (!x || !dy || !dw || n < 1 || h < 1 || w < 1 || cin < 1 || cout < 1 || (ksz != 1 && ksz != 3))
+    return PARAGAN_ERR_INVALID_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dt == PARAGAN_BF16) {
+    if (cin % 8 || cout % 8 || !aligned16(x) || !aligned16(dy)) return PARAGAN_ERR_INVALID_ARG;
+    const size_t out = (size_t)cout * ksz * ksz * cin;
+    const size_t scratch_n = out * 64;
+    float* scratch = nullptr;
+    if (cudaMallocAsync(reinterpret_cast<void**>(&scratch), scratch_n * sizeof(float), st) != cudaSuccess)
+      return PARAGAN_ERR_CUDA;
+    cudaError_t e = tc_conv_wgrad(x, dy, n, h, w, cin, cout, ksz, dw, 0, scratch, scratch_n, st);
+    cudaFreeAsync(scratch, st);
+    return cuda_status(e);
+  }
+  if (dt == PARAGAN_F32)
+    return cuda_status(simt_conv_wgrad<float, float>(static_cast<const float*>(x), static_cast<const float*>(dy), n, h,
+                                                     w, cin, cout, ksz, dw, 0, st));
+  return PARAGAN_ERR_INVALID_ARG;
+}
+
+}  // extern "C"

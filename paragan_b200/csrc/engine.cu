@@ -1,0 +1,1544 @@
+// BigGAN step engine.
+//
+// One Engine<T> per rank; T = float (F32 mode: exact SIMT path) or bf16 (BF16
+// mode: bf16 storage, tcgen05 convolutions, fp32 last layers as PAPER.md:202
+// prescribes).  Everything the step touches lives in the caller's workspace,
+// carved once at init by a bump arena; the step itself allocates nothing.
+//
+// Parameter storage: one flat fp32 buffer per network in canonical order
+// (include/paragan.h), except that conv weights are held OHWI ([C_out][taps]
+// [C_in], the K-major GEMM B operand) instead of OIHW; set/get convert.
+#include <cublas_v2.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "common.cuh"
+#include "engine.h"
+#include "kernels.h"
+#include "tc_conv.h"
+
+namespace pg {
+
+namespace {
+
+constexpr int kMaxPartialBlocks = 1184;  // 8 waves of 148 SMs
+
+struct Arena {
+  char* base = nullptr;
+  size_t off = 0;
+  template <class X>
+  X* get(size_t count) {
+    off = (off + 255) & ~size_t(255);
+    X* p = reinterpret_cast<X*>((base ? base : reinterpret_cast<char*>(0x100000)) + off);
+    off += count * sizeof(X);
+    return p;
+  }
+};
+
+struct PEntry {
+  std::string name;
+  std::vector<int> shape;
+  bool conv4d = false;
+  bool sn = false;
+  long long off = 0, n = 0;
+  long long u_off = -1, v_off = -1;
+  int job = -1;
+};
+
+struct Net {
+  std::vector<PEntry> E;
+  long long n = 0, nu = 0, nv = 0;
+  float *p = nullptr, *g = nullptr, *m = nullptr, *v = nullptr, *u = nullptr;
+  float *sn_v = nullptr, *sn_t = nullptr, *sn_s = nullptr, *sigma = nullptr;
+  std::vector<int> sn_entries;                // entry index per SN job
+  SnJob* jobs_d = nullptr;
+  int *b1_job = nullptr, *b1_k0 = nullptr, *b2_job = nullptr, *b2_r0 = nullptr;
+  int nb1 = 0, nb2 = 0;
+  std::vector<SnPack> pf_h, pb_h;             // fwd packs, dgrad packs
+  SnPack *pf_d = nullptr, *pb_d = nullptr;
+  long long *pf_start = nullptr, *pb_start = nullptr;
+  long long pf_blocks = 0, pb_blocks = 0;
+  int* snb_idx = nullptr;
+  float** snb_grad = nullptr;
+  long long* t_dev = nullptr;
+  int* flag = nullptr;
+  float* loss = nullptr;   // [4]
+  int add(const std::string& name, std::vector<int> shape, bool conv4d, bool sn) {
+    PEntry e;
+    e.name = name;
+    e.shape = shape;
+    e.conv4d = conv4d;
+    e.sn = sn;
+    e.n = 1;
+    for (int s : shape) e.n *= s;
+    e.off = n;
+    n += e.n;
+    E.push_back(e);
+    return (int)E.size() - 1;
+  }
+  float* P(int e) const { return p + E[e].off; }
+  float* G(int e) const { return g + E[e].off; }
+};
+
+struct ConvL {
+  int w = -1, b = -1;              // entries (b = -1: no bias)
+  int cin = 0, cin_x = 0, cout = 0, ksz = 3;
+  void* wp = nullptr;              // fprop operand [cout][taps][cin_x]
+  void* wt = nullptr;              // dgrad operand [cin_x][taps][cout]
+  bool f32 = false;                // SIMT fp32 layer (G output conv)
+};
+struct LinL {
+  int w = -1, b = -1;
+  int in = 0, out = 0;
+  float* what = nullptr;           // W / sigma (fp32) [out][in]
+};
+struct AttnL {
+  int C = 0, C8 = 0, C2 = 0, Cq = 0, Ct = 0, H = 0;
+  int th = -1, ph = -1, gg = -1, o = -1, gamma = -1;
+  void* qkv_wp = nullptr;          // [Ct][1][C]
+  void* qkv_wt = nullptr;          // [C][1][Ct]
+  ConvL oc;                        // o-conv (C2 -> C), no bias
+  // activations
+  void *qkv, *phi_p, *g_p, *P, *ov;
+  float* S;
+};
+struct GBlock {
+  int cin, cout, hin;
+  LinL g1, b1, g2, b2;
+  ConvL c1, c2, sc;
+  bool attn = false;
+  // activations (batch B)
+  void *x, *u1, *h1, *a2, *s, *out;
+  float *gain1, *bias1, *gain2, *bias2, *cond, *dcond;
+  float *mean1, *rstd1, *mean2, *rstd2;
+  double *sums1, *sums2;
+};
+struct DBlock {
+  int cin, cin_x, cout, hin, hout;
+  bool down, learn_sc, attn;
+  ConvL c1, c2, sc;
+  void *x, *rx, *c1o, *r1, *t, *xp, *s, *out;
+};
+
+int round8(int x) { return (x + 7) / 8 * 8; }
+
+struct Arch {
+  std::vector<int> gin, gout;
+  std::vector<int> din, dout, ddown;   // din[0] = -1 -> RGB
+};
+bool arch_for(int res, Arch& a) {
+  switch (res) {
+    case 16: a.gin = {4, 4}; a.gout = {4, 4}; a.din = {-1, 4, 4}; a.dout = {4, 4, 4}; a.ddown = {1, 1, 0}; return true;
+    case 32:
+      a.gin = {4, 4, 4}; a.gout = {4, 4, 4}; a.din = {-1, 4, 4, 4}; a.dout = {4, 4, 4, 4}; a.ddown = {1, 1, 0, 0};
+      return true;
+    case 64:
+      a.gin = {16, 16, 8, 4}; a.gout = {16, 8, 4, 2}; a.din = {-1, 1, 2, 4, 8}; a.dout = {1, 2, 4, 8, 16};
+      a.ddown = {1, 1, 1, 1, 0};
+      return true;
+    case 128:
+      a.gin = {16, 16, 8, 4, 2}; a.gout = {16, 8, 4, 2, 1}; a.din = {-1, 1, 2, 4, 8, 16};
+      a.dout = {1, 2, 4, 8, 16, 16}; a.ddown = {1, 1, 1, 1, 1, 0};
+      return true;
+    case 256:
+      a.gin = {16, 16, 8, 8, 4, 2}; a.gout = {16, 8, 8, 4, 2, 1}; a.din = {-1, 1, 2, 4, 8, 8, 16};
+      a.dout = {1, 2, 4, 8, 8, 16, 16}; a.ddown = {1, 1, 1, 1, 1, 1, 0};
+      return true;
+    case 512:
+      a.gin = {16, 16, 8, 8, 4, 2, 1}; a.gout = {16, 8, 8, 4, 2, 1, 1}; a.din = {-1, 1, 1, 2, 4, 8, 8, 16};
+      a.dout = {1, 1, 2, 4, 8, 8, 16, 16}; a.ddown = {1, 1, 1, 1, 1, 1, 1, 0};
+      return true;
+  }
+  return false;
+}
+
+// ---------------------------------------------------------------- cuBLAS row-major helper (attention bmm)
+cublasStatus_t gemm_rm(cublasHandle_t h, int batch, int M, int N, int K, const void* A, cudaDataType ta,
+                       long long sab, long long sam, long long sak, const void* B, cudaDataType tb, long long sbb,
+                       long long sbn, long long sbk, void* C, cudaDataType tc, long long scb, long long ldc,
+                       float beta) {
+  const cublasOperation_t opX = (sbn == 1) ? CUBLAS_OP_N : CUBLAS_OP_T;
+  const long long ldx = (sbn == 1) ? sbk : sbn;
+  const cublasOperation_t opY = (sak == 1) ? CUBLAS_OP_N : CUBLAS_OP_T;
+  const long long ldy = (sak == 1) ? sam : sak;
+  const float alpha = 1.0f;
+  return cublasGemmStridedBatchedEx(h, opX, opY, N, M, K, &alpha, B, tb, (int)ldx, sbb, A, ta, (int)ldy, sab, &beta,
+                                    C, tc, (int)ldc, scb, batch, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
+}
+
+}  // namespace
+
+#define CK(x)                                                   \
+  do {                                                          \
+    cudaError_t e_ = (x);                                       \
+    ++launches_;                                                \
+    if (e_ != cudaSuccess) return fail_cuda(e_, #x);            \
+  } while (0)
+#define CKS(x)                                                  \
+  do {                                                          \
+    paragan_status s_ = (x);                                    \
+    if (s_ != PARAGAN_OK) return s_;                            \
+  } while (0)
+
+
+// ============================================================================
+template <typename T>
+class Engine final : public EngineBase {
+  static constexpr bool kBF = std::is_same<T, bf16>::value;
+
+ public:
+  Engine(const paragan_config& c, cudaStream_t st) : cfg_(c), st_(st) {}
+  ~Engine() override {
+    if (comm_) ncclCommDestroy(comm_);
+    if (cublas_) cublasDestroy(cublas_);
+  }
+
+  // ------------------------------------------------------------------ plan
+  size_t workspace_bytes() override {
+    Arena a;
+    build(a);
+    return a.off + 4096;
+  }
+  void counts(paragan_net net, size_t* ns, size_t* nt) override {
+    if (!planned_) {
+      Arena a;
+      build(a);
+    }
+    const Net& N = net == PARAGAN_NET_D ? D_ : G_;
+    if (ns) *ns = (size_t)(N.n + N.nu);
+    if (nt) *nt = (size_t)N.n;
+  }
+
+  paragan_status init(const uint8_t* id, void* ws, size_t ws_bytes) override {
+    const size_t need = workspace_bytes();
+    if (ws_bytes < need) {
+      err_ = "workspace too small: need " + std::to_string(need);
+      return PARAGAN_ERR_OOM;
+    }
+    if (((uintptr_t)ws) & 255) return fail_arg("workspace must be 256-byte aligned");
+    Arena a;
+    a.base = static_cast<char*>(ws);
+    build(a);
+    if (cudaMemsetAsync(ws, 0, a.off, st_) != cudaSuccess) return fail_cuda(cudaGetLastError(), "memset ws");
+    if (cublasCreate(&cublas_) != CUBLAS_STATUS_SUCCESS) return fail_msg(PARAGAN_ERR_CUDA, "cublasCreate");
+    cublasSetStream(cublas_, st_);
+    paragan_status s = upload_tables();
+    if (s != PARAGAN_OK) return s;
+    if (fill_const(ones_buf_, maxc_, 1.0f, st_) != cudaSuccess) return fail_cuda(cudaGetLastError(), "ones");
+    if (cfg_.world_size > 1) {
+      ncclUniqueId uid;
+      std::memcpy(&uid, id, sizeof(uid));
+      ncclResult_t r = ncclCommInitRank(&comm_, cfg_.world_size, uid, cfg_.rank);
+      if (r != ncclSuccess) return fail_msg(PARAGAN_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    }
+    if (cudaStreamSynchronize(st_) != cudaSuccess) return fail_cuda(cudaGetLastError(), "init sync");
+    ready_ = true;
+    return PARAGAN_OK;
+  }
+
+  // ------------------------------------------------------------------ params
+  paragan_status init_params(float attn_gamma) override {
+    if (!ready_) return PARAGAN_ERR_ORDER;
+    uint64_t salt = 0;
+    for (Net* N : {&G_, &D_}) {
+      ++salt;
+      for (auto& e : N->E) {
+        float* p = N->P((int)(&e - N->E.data()));
+        const std::string& nm = e.name;
+        const bool is_bias = nm.size() >= 2 && (nm.compare(nm.size() - 2, 2, ".b") == 0 || nm == "out_bn.beta");
+        if (nm.find("gamma") != std::string::npos && nm.find("attn") != std::string::npos) {
+          CK(fill_const(p, e.n, attn_gamma, st_));
+        } else if (nm == "out_bn.gamma") {
+          CK(fill_const(p, e.n, 1.0f, st_));
+        } else if (is_bias) {
+          CK(fill_const(p, e.n, 0.0f, st_));
+        } else {
+          CK(fill_normal(p, e.n, 0.02f, cfg_.seed * 1000003ull + salt, (uint64_t)e.off, st_));
+        }
+        if (e.sn) {
+          float* u = N->u + e.u_off;
+          CK(fill_normal(u, e.shape[0], 1.0f, cfg_.seed * 7919ull + salt, (uint64_t)(1ull << 40) + e.u_off, st_));
+          CK(normalize_vec(u, e.shape[0], st_));
+        }
+      }
+      reset_opt(*N);
+    }
+    return sync_ok();
+  }
+
+  paragan_status set_params(paragan_net net, const float* host, size_t n) override {
+    if (!ready_) return PARAGAN_ERR_ORDER;
+    Net& N = net == PARAGAN_NET_D ? D_ : G_;
+    if (!host || n != (size_t)(N.n + N.nu)) return fail_arg("set_params: size mismatch");
+    // canonical -> staging (g buffer) -> internal (conv OIHW -> OHWI)
+    if (cudaMemcpyAsync(N.g, host, sizeof(float) * N.n, cudaMemcpyHostToDevice, st_) != cudaSuccess ||
+        cudaMemcpyAsync(N.u, host + N.n, sizeof(float) * N.nu, cudaMemcpyHostToDevice, st_) != cudaSuccess)
+      return fail_cuda(cudaGetLastError(), "set_params copy");
+    for (size_t i = 0; i < N.E.size(); ++i) {
+      const PEntry& e = N.E[i];
+      if (e.conv4d) {
+        CK(oihw_to_ohwi(N.g + e.off, N.p + e.off, e.shape[0], e.shape[1], e.shape[2] * e.shape[3], st_));
+      } else {
+        if (cudaMemcpyAsync(N.p + e.off, N.g + e.off, sizeof(float) * e.n, cudaMemcpyDeviceToDevice, st_))
+          return fail_cuda(cudaGetLastError(), "set_params d2d");
+      }
+    }
+    reset_opt(N);
+    return sync_ok();
+  }
+  paragan_status get_params(paragan_net net, float* host, size_t n) override {
+    if (!ready_) return PARAGAN_ERR_ORDER;
+    Net& N = net == PARAGAN_NET_D ? D_ : G_;
+    if (!host || n != (size_t)(N.n + N.nu)) return fail_arg("get_params: size mismatch");
+    return export_flat(N, N.p, host, true);
+  }
+  paragan_status get_grads(paragan_net net, float* host, size_t n) override {
+    if (!ready_) return PARAGAN_ERR_ORDER;
+    Net& N = net == PARAGAN_NET_D ? D_ : G_;
+    if (!host || n != (size_t)N.n) return fail_arg("get_grads: size mismatch");
+    return export_flat(N, N.g, host, false);
+  }
+  paragan_status get_fakes(float* host, size_t n) override {
+    if (!ready_) return PARAGAN_ERR_ORDER;
+    const size_t need = (size_t)B_ * 3 * R_ * R_;
+    if (!host || n != need) return fail_arg("get_fakes: size mismatch");
+    CK(layout_unpack<T>(static_cast<const T*>(dimg_), scratch_f_, B_, 3, R_, R_, cpad_, st_));
+    if (cudaMemcpyAsync(host, scratch_f_, need * sizeof(float), cudaMemcpyDeviceToHost, st_))
+      return fail_cuda(cudaGetLastError(), "get_fakes");
+    return sync_ok();
+  }
+
+  // ------------------------------------------------------------------ steps
+  paragan_status d_step(const void* real, const int32_t* real_y, const float* z, const int32_t* fake_y,
+                        uint32_t flags) override {
+    if (!ready_ || poisoned_) return PARAGAN_ERR_ORDER;
+    if (!real || !real_y || !z || !fake_y || ((uintptr_t)real & 15)) return fail_arg("d_step: bad pointer");
+    // SN(G) + G forward (no grad) writes fakes into D-input rows [0, B)
+    CKS(sn_forward(G_, false));
+    CKS(g_forward(z, fake_y, false));
+    // reals into rows [B, 2B) (one D pass over the concatenated batch)
+    const size_t img_bytes = (size_t)B_ * R_ * R_ * cpad_ * sizeof(T);
+    if (cudaMemcpyAsync(static_cast<char*>(dimg_) + img_bytes, real, img_bytes, cudaMemcpyDeviceToDevice, st_))
+      return fail_cuda(cudaGetLastError(), "copy reals");
+    CK(cudaMemcpyAsync(ylab_, fake_y, sizeof(int32_t) * B_, cudaMemcpyDeviceToDevice, st_));
+    CK(cudaMemcpyAsync(ylab_ + B_, real_y, sizeof(int32_t) * B_, cudaMemcpyDeviceToDevice, st_));
+    CKS(sn_forward(D_, true));
+    CKS(d_forward(2 * B_));
+    CK(hinge_loss(logits_, B_, 0, dlogits_, D_.loss, st_));
+    ++launches_;
+    CK(cudaMemsetAsync(D_.g, 0, sizeof(float) * D_.n, st_));
+    CKS(d_backward(2 * B_, true, false));
+    CKS(sn_backward_net(D_));
+    if (!(flags & PARAGAN_FLAG_NO_ALLREDUCE)) CKS(allreduce(PARAGAN_NET_D));
+    if (!(flags & PARAGAN_FLAG_NO_UPDATE)) CKS(update(PARAGAN_NET_D));
+    ++d_since_g_;
+    return PARAGAN_OK;
+  }
+
+  paragan_status g_step(const float* z, const int32_t* y, uint32_t flags) override {
+    if (!ready_ || poisoned_) return PARAGAN_ERR_ORDER;
+    if (d_since_g_ < cfg_.d_steps_per_g) {
+      err_ = "g_step before d_steps_per_g D steps";
+      return PARAGAN_ERR_ORDER;
+    }
+    if (!z || !y) return fail_arg("g_step: bad pointer");
+    CKS(sn_forward(G_, true));
+    CKS(g_forward(z, y, true));
+    CK(cudaMemcpyAsync(ylab_, y, sizeof(int32_t) * B_, cudaMemcpyDeviceToDevice, st_));
+    CKS(sn_forward(D_, true));
+    CKS(d_forward(B_));
+    CK(hinge_loss(logits_, B_, 1, dlogits_, G_.loss, st_));
+    ++launches_;
+    CK(cudaMemsetAsync(G_.g, 0, sizeof(float) * G_.n, st_));
+    CKS(d_backward(B_, false, true));   // dgrad only, down to the image
+    CKS(g_backward());
+    CKS(sn_backward_net(G_));
+    if (!(flags & PARAGAN_FLAG_NO_ALLREDUCE)) CKS(allreduce(PARAGAN_NET_G));
+    if (!(flags & PARAGAN_FLAG_NO_UPDATE)) CKS(update(PARAGAN_NET_G));
+    d_since_g_ = 0;
+    return PARAGAN_OK;
+  }
+
+  paragan_status allreduce(paragan_net net) override {
+    if (!ready_ || poisoned_) return PARAGAN_ERR_ORDER;
+    Net& N = net == PARAGAN_NET_D ? D_ : G_;
+    if (cfg_.world_size > 1) {
+      ncclResult_t r = ncclAllReduce(N.g, N.g, (size_t)N.n, ncclFloat32, ncclSum, comm_, st_);
+      if (r != ncclSuccess) return fail_msg(PARAGAN_ERR_NCCL, std::string("allreduce: ") + ncclGetErrorString(r));
+      CK(scale_f32(N.g, N.n, 1.0f / cfg_.world_size, st_));   // mean over ranks (R15)
+      ++launches_;
+    }
+    return PARAGAN_OK;
+  }
+
+  paragan_status update(paragan_net net) override {
+    if (!ready_ || poisoned_) return PARAGAN_ERR_ORDER;
+    Net& N = net == PARAGAN_NET_D ? D_ : G_;
+    const paragan_adam& h = net == PARAGAN_NET_D ? cfg_.adam_d : cfg_.adam_g;
+    CK(cudaMemsetAsync(N.flag, 0, sizeof(int), st_));
+    CK(check_finite(N.g, N.n, N.flag, st_));
+    CK(check_finite_scalar(N.loss, N.flag, st_));
+    CK(adam_flat(N.p, N.g, N.m, N.v, N.n, h.lr, h.beta1, h.beta2, h.eps, N.t_dev, 1.0f, N.flag, st_));
+    CK(adam_bookkeep(N.t_dev, N.flag, nonfinite_sticky_, st_));
+    launches_ += 4;
+    return PARAGAN_OK;
+  }
+
+  paragan_status sync_stats(paragan_stats* out) override {
+    if (!ready_) return PARAGAN_ERR_ORDER;
+    float ld[4], lg[4];
+    long long td, tg;
+    int nf;
+    if (cudaMemcpyAsync(ld, D_.loss, sizeof(ld), cudaMemcpyDeviceToHost, st_) ||
+        cudaMemcpyAsync(lg, G_.loss, sizeof(lg), cudaMemcpyDeviceToHost, st_) ||
+        cudaMemcpyAsync(&td, D_.t_dev, sizeof(td), cudaMemcpyDeviceToHost, st_) ||
+        cudaMemcpyAsync(&tg, G_.t_dev, sizeof(tg), cudaMemcpyDeviceToHost, st_) ||
+        cudaMemcpyAsync(&nf, nonfinite_sticky_, sizeof(nf), cudaMemcpyDeviceToHost, st_))
+      return fail_cuda(cudaGetLastError(), "sync_stats copy");
+    paragan_status s = sync_ok();
+    if (s != PARAGAN_OK) return s;
+    if (out) {
+      out->d_loss = ld[0];
+      out->d_real_mean = ld[1];
+      out->d_fake_mean = ld[2];
+      out->g_loss = lg[0];
+      out->nonfinite = nf;
+      out->t_d = td;
+      out->t_g = tg;
+    }
+    if (nf) {
+      cudaMemsetAsync(nonfinite_sticky_, 0, sizeof(int), st_);
+      return PARAGAN_ERR_NONFINITE;
+    }
+    return PARAGAN_OK;
+  }
+  uint64_t launches() const override { return launches_; }
+
+  // ---------------------------------------------------------------- live kernel timing (bench roofline)
+  paragan_status profile(int enable) override {
+    if (enable) {
+      for (auto& r : recs_) { ev_free_.push_back(r.a); ev_free_.push_back(r.b); }
+      recs_.clear();
+    }
+    prof_ = enable != 0;
+    return PARAGAN_OK;
+  }
+  paragan_status profile_read(int kind, uint64_t* n, double* ms, double* flops) override {
+    if (cudaStreamSynchronize(st_) != cudaSuccess) return fail_cuda(cudaGetLastError(), "profile sync");
+    uint64_t c = 0;
+    double t = 0, f = 0;
+    for (auto& r : recs_) {
+      if (r.kind != kind) continue;
+      float e = 0;
+      if (cudaEventElapsedTime(&e, r.a, r.b) != cudaSuccess) return fail_cuda(cudaGetLastError(), "event time");
+      ++c;
+      t += e;
+      f += r.flops;
+    }
+    if (n) *n = c;
+    if (ms) *ms = t;
+    if (flops) *flops = f;
+    return PARAGAN_OK;
+  }
+
+ private:
+  // ================================================================== helpers
+  paragan_status fail_cuda(cudaError_t e, const char* what) {
+    err_ = std::string(what) + ": " + cudaGetErrorString(e);
+    poisoned_ = true;
+    return PARAGAN_ERR_CUDA;
+  }
+  paragan_status fail_msg(paragan_status s, const std::string& m) {
+    err_ = m;
+    if (s == PARAGAN_ERR_CUDA || s == PARAGAN_ERR_NCCL) poisoned_ = true;
+    return s;
+  }
+  paragan_status fail_arg(const std::string& m) {
+    err_ = m;
+    return PARAGAN_ERR_INVALID_ARG;
+  }
+  paragan_status sync_ok() {
+    cudaError_t e = cudaStreamSynchronize(st_);
+    if (e != cudaSuccess) return fail_cuda(e, "stream sync");
+    return PARAGAN_OK;
+  }
+  void reset_opt(Net& N) {
+    cudaMemsetAsync(N.m, 0, sizeof(float) * N.n, st_);
+    cudaMemsetAsync(N.v, 0, sizeof(float) * N.n, st_);
+    cudaMemsetAsync(N.t_dev, 0, sizeof(long long), st_);
+  }
+  paragan_status export_flat(Net& N, const float* src, float* host, bool with_u) {
+    float* stage = scratch_f_;
+    for (const PEntry& e : N.E) {
+      if (e.conv4d) {
+        CK(ohwi_to_oihw(src + e.off, stage + e.off, e.shape[0], e.shape[1], e.shape[2] * e.shape[3], st_));
+      } else {
+        CK(cudaMemcpyAsync(stage + e.off, src + e.off, sizeof(float) * e.n, cudaMemcpyDeviceToDevice, st_));
+      }
+    }
+    if (cudaMemcpyAsync(host, stage, sizeof(float) * N.n, cudaMemcpyDeviceToHost, st_))
+      return fail_cuda(cudaGetLastError(), "export copy");
+    if (with_u && cudaMemcpyAsync(host + N.n, N.u, sizeof(float) * N.nu, cudaMemcpyDeviceToHost, st_))
+      return fail_cuda(cudaGetLastError(), "export u");
+    return sync_ok();
+  }
+
+  // ------------------------------------------------------------------ building the plan
+  ConvL conv(Net& N, const std::string& nm, int cin, int cin_x, int cout, int ksz, bool bias, bool f32 = false) {
+    ConvL c;
+    c.cin = cin;
+    c.cin_x = cin_x;
+    c.cout = cout;
+    c.ksz = ksz;
+    c.f32 = f32;
+    c.w = N.add(nm + ".w", {cout, cin, ksz, ksz}, true, true);
+    if (bias) c.b = N.add(nm + ".b", {cout}, false, false);
+    return c;
+  }
+  LinL lin(Net& N, const std::string& nm, int in, int out, bool bias, bool sn, bool wsuffix = true) {
+    LinL l;
+    l.in = in;
+    l.out = out;
+    l.w = N.add(wsuffix ? nm + ".w" : nm, {out, in}, false, sn);
+    if (bias) l.b = N.add(nm + ".b", {out}, false, false);
+    return l;
+  }
+  AttnL attn(Net& N, int C, int H) {
+    AttnL a;
+    a.C = C;
+    a.H = H;
+    a.C8 = C / 8;
+    a.C2 = C / 2;
+    a.Cq = round8(a.C8);
+    a.Ct = 2 * a.Cq + round8(a.C2);
+    a.th = N.add("attn.theta", {a.C8, C, 1, 1}, true, true);
+    a.ph = N.add("attn.phi", {a.C8, C, 1, 1}, true, true);
+    a.gg = N.add("attn.g", {a.C2, C, 1, 1}, true, true);
+    a.oc.w = N.add("attn.o", {C, a.C2, 1, 1}, true, true);
+    a.oc.cin = a.C2;
+    a.oc.cin_x = a.C2;
+    a.oc.cout = C;
+    a.oc.ksz = 1;
+    a.o = a.oc.w;
+    a.gamma = N.add("attn.gamma", {1}, false, false);
+    return a;
+  }
+
+  void build(Arena& A) {
+    G_ = Net();
+    D_ = Net();
+    gb_.clear();
+    db_.clear();
+    const int ch = cfg_.ch;
+    B_ = cfg_.local_batch;
+    R_ = cfg_.resolution;
+    cpad_ = cfg_.c_pad_image;
+    Arch ar;
+    arch_for(R_, ar);
+    const int nbg = (int)ar.gin.size();
+    zc_ = cfg_.z_chunk;
+    dimz_ = (nbg + 1) * zc_;
+    cd_ = cfg_.shared_dim + zc_;
+    // ---------------- G parameters, canonical order
+    shared_ = G_.add("shared", {cfg_.n_classes, cfg_.shared_dim}, false, false);
+    c0_ = ar.gin[0] * ch;
+    glin_ = lin(G_, "linear", zc_, 16 * c0_, true, true);
+    int h = 4;
+    for (int i = 0; i < nbg; ++i) {
+      GBlock b{};
+      b.cin = ar.gin[i] * ch;
+      b.cout = ar.gout[i] * ch;
+      b.hin = h;
+      const std::string p = "b" + std::to_string(i) + ".";
+      b.g1 = lin(G_, p + "cbn1.gain", cd_, b.cin, false, true, false);
+      b.b1 = lin(G_, p + "cbn1.bias", cd_, b.cin, false, true, false);
+      b.c1 = conv(G_, p + "conv1", b.cin, b.cin, b.cout, 3, true);
+      b.g2 = lin(G_, p + "cbn2.gain", cd_, b.cout, false, true, false);
+      b.b2 = lin(G_, p + "cbn2.bias", cd_, b.cout, false, true, false);
+      b.c2 = conv(G_, p + "conv2", b.cout, b.cout, b.cout, 3, true);
+      b.sc = conv(G_, p + "sc", b.cin, b.cin, b.cout, 1, true);
+      b.attn = (cfg_.attn_res == 2 * h);
+      if (b.attn) gattn_ = attn(G_, b.cout, 2 * h);
+      gb_.push_back(b);
+      h *= 2;
+    }
+    cl_ = ar.gout.back() * ch;
+    obn_g_ = G_.add("out_bn.gamma", {cl_}, false, false);
+    obn_b_ = G_.add("out_bn.beta", {cl_}, false, false);
+    oconv_ = conv(G_, "out_conv", cl_, cl_, 3, 3, true, true);
+    // ---------------- D parameters
+    h = R_;
+    bool placed = false;
+    for (size_t j = 0; j < ar.din.size(); ++j) {
+      DBlock b{};
+      b.cin = ar.din[j] < 0 ? 3 : ar.din[j] * ch;
+      b.cin_x = ar.din[j] < 0 ? cpad_ : b.cin;
+      b.cout = ar.dout[j] * ch;
+      b.down = ar.ddown[j] != 0;
+      b.hin = h;
+      b.hout = b.down ? h / 2 : h;
+      b.learn_sc = (b.cin != b.cout) || b.down;
+      const std::string p = "b" + std::to_string(j) + ".";
+      b.c1 = conv(D_, p + "conv1", b.cin, b.cin_x, b.cout, 3, true);
+      b.c2 = conv(D_, p + "conv2", b.cout, b.cout, b.cout, 3, true);
+      if (b.learn_sc) b.sc = conv(D_, p + "sc", b.cin, b.cin_x, b.cout, 1, true);
+      b.attn = !placed && cfg_.attn_res == b.hout;
+      placed = placed || b.attn;
+      if (b.attn) dattn_ = attn(D_, b.cout, b.hout);
+      db_.push_back(b);
+      h = b.hout;
+    }
+    cdl_ = ar.dout.back() * ch;
+    hl_ = h;
+    dlin_ = lin(D_, "linear", cdl_, 1, true, true);
+    demb_ = D_.add("embed", {cfg_.n_classes, cdl_}, false, true);
+    // u / v offsets
+    for (Net* N : {&G_, &D_}) {
+      N->nu = 0;
+      N->nv = 0;
+      N->sn_entries.clear();
+      for (auto& e : N->E)
+        if (e.sn) {
+          e.u_off = N->nu;
+          N->nu += e.shape[0];
+          e.v_off = N->nv;
+          N->nv += e.n / e.shape[0];
+          e.job = (int)N->sn_entries.size();
+          N->sn_entries.push_back((int)(&e - N->E.data()));
+        }
+    }
+    // ---------------- device memory
+    for (Net* N : {&G_, &D_}) {
+      N->p = A.get<float>(N->n);
+      N->g = A.get<float>(N->n);
+      N->m = A.get<float>(N->n);
+      N->v = A.get<float>(N->n);
+      N->u = A.get<float>(N->nu);
+      N->sn_s = A.get<float>(N->nu);
+      N->sn_v = A.get<float>(N->nv);
+      N->sn_t = A.get<float>(N->nv);
+      N->sigma = A.get<float>(2 * N->sn_entries.size());
+      N->t_dev = A.get<long long>(1);
+      N->flag = A.get<int>(1);
+      N->loss = A.get<float>(4);
+    }
+    nonfinite_sticky_ = A.get<int>(1);
+    const size_t wsz = kBF ? 2 : 4;
+    auto alloc_conv = [&](ConvL& c) {
+      const size_t nw = (size_t)c.cout * c.ksz * c.ksz * c.cin_x;
+      const size_t es = c.f32 ? 4 : wsz;
+      c.wp = A.get<char>(nw * es);
+      c.wt = A.get<char>(nw * es);
+    };
+    auto alloc_lin = [&](LinL& l) { l.what = A.get<float>((size_t)l.in * l.out); };
+    alloc_lin(glin_);
+    for (auto& b : gb_) {
+      alloc_lin(b.g1); alloc_lin(b.b1); alloc_lin(b.g2); alloc_lin(b.b2);
+      alloc_conv(b.c1); alloc_conv(b.c2); alloc_conv(b.sc);
+    }
+    alloc_conv(oconv_);
+    for (auto& b : db_) {
+      alloc_conv(b.c1); alloc_conv(b.c2);
+      if (b.learn_sc) alloc_conv(b.sc);
+    }
+    alloc_lin(dlin_);
+    demb_hat_ = A.get<float>((size_t)cfg_.n_classes * cdl_);
+    for (AttnL* at : {&gattn_, &dattn_}) {
+      if (!at->C) continue;
+      at->qkv_wp = A.get<char>((size_t)at->Ct * at->C * wsz);
+      at->qkv_wt = A.get<char>((size_t)at->Ct * at->C * wsz);
+      alloc_conv(at->oc);
+    }
+    // ---------------- activations
+    const int B = B_, B2 = 2 * B_;
+    big_ = 0;
+    auto act = [&](long long n, int h_, int w_, int c_) -> void* {
+      const long long e = n * h_ * w_ * c_;
+      big_ = std::max(big_, e);
+      return A.get<char>((size_t)e * sizeof(T));
+    };
+    zin_ = A.get<float>((size_t)B * dimz_);
+    yg_ = A.get<int32_t>(B);
+    emb_ = A.get<float>((size_t)B * cfg_.shared_dim);
+    demb_g_ = A.get<float>((size_t)B * cfg_.shared_dim);
+    h0f_ = A.get<float>((size_t)B * 16 * c0_);
+    for (auto& b : gb_) {
+      const int H = b.hin;
+      b.x = act(B, H, H, b.cin);
+      b.u1 = act(B, 2 * H, 2 * H, b.cin);
+      b.h1 = act(B, 2 * H, 2 * H, b.cout);
+      b.a2 = act(B, 2 * H, 2 * H, b.cout);
+      b.s = act(B, H, H, b.cout);
+      b.out = act(B, 2 * H, 2 * H, b.cout);
+      b.gain1 = A.get<float>((size_t)B * b.cin);
+      b.bias1 = A.get<float>((size_t)B * b.cin);
+      b.gain2 = A.get<float>((size_t)B * b.cout);
+      b.bias2 = A.get<float>((size_t)B * b.cout);
+      b.cond = A.get<float>((size_t)B * cd_);
+      b.dcond = A.get<float>((size_t)B * cd_);
+      b.mean1 = A.get<float>(b.cin);
+      b.rstd1 = A.get<float>(b.cin);
+      b.mean2 = A.get<float>(b.cout);
+      b.rstd2 = A.get<float>(b.cout);
+      b.sums1 = A.get<double>(2 * b.cin);
+      b.sums2 = A.get<double>(2 * b.cout);
+    }
+    gout_in_ = act(B, R_, R_, cl_);   // input of the output BN (= last block output or attention output)
+    aout_ = A.get<float>((size_t)B * R_ * R_ * cl_);   // fp32 output-BN activation
+    omean_ = A.get<float>(cl_);
+    orstd_ = A.get<float>(cl_);
+    osums_ = A.get<double>(2 * cl_);
+    pre_ = A.get<float>((size_t)B * R_ * R_ * 3);
+    img_ = A.get<float>((size_t)B * R_ * R_ * 3);
+    dimg_ = act(B2, R_, R_, cpad_);
+    ylab_ = A.get<int32_t>(B2);
+    for (auto& b : db_) {
+      const int H = b.hin;
+      b.x = (&b == &db_[0]) ? dimg_ : nullptr;   // set below to previous output
+      b.rx = act(B2, H, H, b.cin_x);
+      b.c1o = act(B2, H, H, b.cout);
+      b.r1 = act(B2, H, H, b.cout);
+      b.t = act(B2, H, H, b.cout);
+      b.xp = b.down ? act(B2, H / 2, H / 2, b.cin_x) : nullptr;
+      b.s = b.learn_sc ? act(B2, H, H, b.cout) : nullptr;
+      b.out = act(B2, b.hout, b.hout, b.cout);
+    }
+    for (AttnL* at : {&gattn_, &dattn_}) {
+      if (!at->C) continue;
+      const int n = (at == &gattn_) ? B : B2;
+      const long long HW = (long long)at->H * at->H, Q = HW / 4;
+      at->qkv = act(n, at->H, at->H, at->Ct);
+      at->phi_p = A.get<char>((size_t)n * Q * at->C8 * sizeof(T));
+      at->g_p = A.get<char>((size_t)n * Q * at->C2 * sizeof(T));
+      at->S = A.get<float>((size_t)n * HW * Q);
+      at->P = A.get<char>((size_t)n * HW * Q * sizeof(T));
+      at->ov = act(n, at->H, at->H, at->C2);
+      attn_out_[at == &gattn_ ? 0 : 1] = act(n, at->H, at->H, at->C);
+      big_ = std::max(big_, (long long)n * HW * Q);
+    }
+    {
+      long long mdo = 0, mdq = 0;
+      for (AttnL* at : {&gattn_, &dattn_}) {
+        if (!at->C) continue;
+        const long long n = (at == &gattn_) ? B : B2;
+        mdo = std::max(mdo, n * at->H * at->H * at->C2);
+        mdq = std::max(mdq, n * at->H * at->H * at->Ct);
+      }
+      tmp_attn_dO_ = A.get<char>((size_t)std::max(mdo, 1LL) * sizeof(T));
+      tmp_attn_dqkv_ = A.get<char>((size_t)std::max(mdq, 1LL) * sizeof(T));
+      dxp_ = A.get<char>((size_t)B2 * (R_ / 2) * (R_ / 2) * cpad_ * sizeof(T));
+    }
+    maxc_ = 8;
+    for (auto& b : gb_) maxc_ = std::max(maxc_, std::max(b.cin, b.cout));
+    for (auto& b : db_) maxc_ = std::max(maxc_, std::max(b.cin_x, b.cout));
+    ones_buf_ = A.get<float>(maxc_);
+    feat_ = A.get<float>((size_t)B2 * cdl_);
+    logits_ = A.get<float>(B2);
+    dlogits_ = A.get<float>(B2);
+    // temps: 4 gradient buffers of the largest activation, fp32 scratch
+    for (int i = 0; i < 4; ++i) tmp_[i] = A.get<char>((size_t)big_ * sizeof(T));
+    dpre_ = A.get<float>((size_t)B * R_ * R_ * 3);
+    daout_ = A.get<float>((size_t)B * R_ * R_ * cl_);
+    dh0f_ = A.get<float>((size_t)B * 16 * c0_);
+    ab_ = A.get<float>((size_t)B * 2 * maxc_);
+    bn_part_ = A.get<float>((size_t)B * 64 * 2 * maxc_);
+    dpart_ = A.get<double>((size_t)kMaxPartialBlocks * 2 * std::max(maxc_, 16 * c0_));
+    tot_ = A.get<double>(2 * maxc_);
+    size_t sf = std::max<size_t>((size_t)std::max(G_.n, D_.n), (size_t)B * 3 * R_ * R_);
+    sf = std::max<size_t>(sf, (size_t)64 << 20);
+    scratch_floats_ = sf;
+    scratch_f_ = A.get<float>(sf);
+    wg_scratch_ = A.get<float>((size_t)16 << 20);   // padded / qkv weight-gradient staging
+    dpool_ = A.get<float>((size_t)B2 * 1024 * 96);
+    // tables
+    for (Net* N : {&G_, &D_}) {
+      N->jobs_d = A.get<SnJob>(N->sn_entries.size());
+      long long nb1 = 0, nb2 = 0;
+      for (int ei : N->sn_entries) {
+        const PEntry& e = N->E[ei];
+        nb1 += ceil_div(e.n / e.shape[0], 256);
+        nb2 += ceil_div(e.shape[0], 8);
+      }
+      N->nb1 = (int)nb1;
+      N->nb2 = (int)nb2;
+      N->b1_job = A.get<int>(nb1);
+      N->b1_k0 = A.get<int>(nb1);
+      N->b2_job = A.get<int>(nb2);
+      N->b2_r0 = A.get<int>(nb2);
+      N->snb_idx = A.get<int>(N->sn_entries.size());
+      N->snb_grad = A.get<float*>(N->sn_entries.size());
+      N->pf_d = A.get<SnPack>(64 + N->sn_entries.size() * 2);
+      N->pb_d = A.get<SnPack>(64 + N->sn_entries.size() * 2);
+      N->pf_start = A.get<long long>(64 + N->sn_entries.size() * 2);
+      N->pb_start = A.get<long long>(64 + N->sn_entries.size() * 2);
+    }
+    // chain D block inputs
+    void* prev = dimg_;
+    for (auto& b : db_) {
+      b.x = prev;
+      prev = b.out;
+      if (b.attn) prev = attn_out_[1];
+    }
+    planned_ = true;
+  }
+
+  // SN job tables and pack lists (host -> device once)
+  paragan_status upload_tables() {
+    for (Net* N : {&G_, &D_}) {
+      std::vector<SnJob> jobs;
+      std::vector<int> b1j, b1k, b2j, b2r, sidx;
+      std::vector<float*> sgrad;
+      for (int ei : N->sn_entries) {
+        const PEntry& e = N->E[ei];
+        SnJob j;
+        j.w = N->p + e.off;
+        j.u = N->u + e.u_off;
+        j.v = N->sn_v + e.v_off;
+        j.t = N->sn_t + e.v_off;
+        j.s = N->sn_s + e.u_off;
+        j.sigma = N->sigma + 2 * e.job;
+        j.rows = e.shape[0];
+        j.K = (int)(e.n / e.shape[0]);
+        const int ji = (int)jobs.size();
+        for (int k = 0; k < j.K; k += 256) { b1j.push_back(ji); b1k.push_back(k); }
+        for (int r = 0; r < j.rows; r += 8) { b2j.push_back(ji); b2r.push_back(r); }
+        sidx.push_back(ji);
+        sgrad.push_back(N->g + e.off);
+        jobs.push_back(j);
+      }
+      CK(cudaMemcpyAsync(N->jobs_d, jobs.data(), jobs.size() * sizeof(SnJob), cudaMemcpyHostToDevice, st_));
+      CK(cudaMemcpyAsync(N->b1_job, b1j.data(), b1j.size() * sizeof(int), cudaMemcpyHostToDevice, st_));
+      CK(cudaMemcpyAsync(N->b1_k0, b1k.data(), b1k.size() * sizeof(int), cudaMemcpyHostToDevice, st_));
+      CK(cudaMemcpyAsync(N->b2_job, b2j.data(), b2j.size() * sizeof(int), cudaMemcpyHostToDevice, st_));
+      CK(cudaMemcpyAsync(N->b2_r0, b2r.data(), b2r.size() * sizeof(int), cudaMemcpyHostToDevice, st_));
+      CK(cudaMemcpyAsync(N->snb_idx, sidx.data(), sidx.size() * sizeof(int), cudaMemcpyHostToDevice, st_));
+      CK(cudaMemcpyAsync(N->snb_grad, sgrad.data(), sgrad.size() * sizeof(float*), cudaMemcpyHostToDevice, st_));
+      jobs_h_[N == &G_ ? 0 : 1] = jobs;
+    }
+    // pack lists
+    auto sig = [&](Net& N, int e) { return N.sigma + 2 * N.E[e].job; };
+    auto add_conv = [&](Net& N, const ConvL& c) {
+      SnPack f{};
+      f.w = N.P(c.w);
+      f.sigma = sig(N, c.w);
+      f.dst = c.wp;
+      f.rows = c.cout;
+      f.taps = c.ksz * c.ksz;
+      f.cin = c.cin;
+      f.mode = 0;
+      f.dst_bf16 = (kBF && !c.f32) ? 1 : 0;
+      f.dst_row_offset = 0;
+      f.dst_rows = c.cout;
+      f.dst_cin = c.cin_x;
+      N.pf_h.push_back(f);
+      SnPack b = f;
+      b.dst = c.wt;
+      b.mode = 1;
+      N.pb_h.push_back(b);
+    };
+    auto add_lin = [&](Net& N, const LinL& l) {
+      SnPack f{};
+      f.w = N.P(l.w);
+      f.sigma = sig(N, l.w);
+      f.dst = l.what;
+      f.rows = l.out;
+      f.taps = 1;
+      f.cin = l.in;
+      f.mode = 0;
+      f.dst_bf16 = 0;
+      f.dst_rows = l.out;
+      f.dst_cin = l.in;
+      N.pf_h.push_back(f);
+    };
+    auto add_attn = [&](Net& N, AttnL& a) {
+      const int rows[3] = {a.C8, a.C8, a.C2}, offs[3] = {0, a.Cq, 2 * a.Cq}, es[3] = {a.th, a.ph, a.gg};
+      for (int k = 0; k < 3; ++k) {
+        SnPack f{};
+        f.w = N.P(es[k]);
+        f.sigma = sig(N, es[k]);
+        f.dst = a.qkv_wp;
+        f.rows = rows[k];
+        f.taps = 1;
+        f.cin = a.C;
+        f.mode = 0;
+        f.dst_bf16 = kBF ? 1 : 0;
+        f.dst_row_offset = offs[k];
+        f.dst_rows = a.Ct;
+        f.dst_cin = a.C;
+        N.pf_h.push_back(f);
+        SnPack b = f;
+        b.dst = a.qkv_wt;
+        b.mode = 1;
+        N.pb_h.push_back(b);
+      }
+      add_conv(N, a.oc);
+    };
+    G_.pf_h.clear(); G_.pb_h.clear(); D_.pf_h.clear(); D_.pb_h.clear();
+    add_lin(G_, glin_);
+    for (auto& b : gb_) {
+      add_lin(G_, b.g1); add_lin(G_, b.b1); add_lin(G_, b.g2); add_lin(G_, b.b2);
+      add_conv(G_, b.c1); add_conv(G_, b.c2); add_conv(G_, b.sc);
+    }
+    if (gattn_.C) add_attn(G_, gattn_);
+    add_conv(G_, oconv_);
+    for (auto& b : db_) {
+      add_conv(D_, b.c1); add_conv(D_, b.c2);
+      if (b.learn_sc) add_conv(D_, b.sc);
+    }
+    if (dattn_.C) add_attn(D_, dattn_);
+    add_lin(D_, dlin_);
+    {
+      LinL e;
+      e.w = demb_;
+      e.in = cdl_;
+      e.out = cfg_.n_classes;
+      e.what = demb_hat_;
+      add_lin(D_, e);
+    }
+    for (Net* N : {&G_, &D_}) {
+      for (int pass = 0; pass < 2; ++pass) {
+        auto& lst = pass == 0 ? N->pf_h : N->pb_h;
+        std::vector<long long> st;
+        long long acc = 0;
+        for (auto& j : lst) {
+          st.push_back(acc);
+          acc += ceil_div((long long)j.rows * j.taps * j.cin, 256);
+        }
+        (pass == 0 ? N->pf_blocks : N->pb_blocks) = acc;
+        CK(cudaMemcpyAsync(pass == 0 ? N->pf_d : N->pb_d, lst.data(), lst.size() * sizeof(SnPack),
+                           cudaMemcpyHostToDevice, st_));
+        CK(cudaMemcpyAsync(pass == 0 ? N->pf_start : N->pb_start, st.data(), st.size() * sizeof(long long),
+                           cudaMemcpyHostToDevice, st_));
+      }
+    }
+    return sync_ok();
+  }
+
+  // ------------------------------------------------------------------ SN forward (A2)
+  paragan_status sn_forward(Net& N, bool need_dgrad) {
+    CK(sn_power(N.jobs_d, (int)N.sn_entries.size(), N.b1_job, N.b1_k0, N.nb1, N.b2_job, N.b2_r0, N.nb2, st_));
+    launches_ += 2;
+    CK(sn_pack(N.pf_d, N.pf_start, (int)N.pf_h.size(), N.pf_blocks, st_));
+    if (need_dgrad) CK(sn_pack(N.pb_d, N.pb_start, (int)N.pb_h.size(), N.pb_blocks, st_));
+    return PARAGAN_OK;
+  }
+  paragan_status sn_backward_net(Net& N) {
+    CK(sn_backward(N.jobs_d, N.snb_idx, (int)N.sn_entries.size(), N.snb_grad, nullptr, st_));
+    return PARAGAN_OK;
+  }
+
+  struct ProfRec {
+    int kind;
+    double flops;
+    cudaEvent_t a, b;
+  };
+  cudaEvent_t ev_get() {
+    if (!ev_free_.empty()) {
+      cudaEvent_t e = ev_free_.back();
+      ev_free_.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+  // brackets one launch with events when profiling; kind 0 = tcgen05 fprop/dgrad, 1 = tcgen05 wgrad
+  template <class F>
+  cudaError_t timed(int kind, double flops, F&& f) {
+    if (!prof_) return f();
+    ProfRec r{kind, flops, ev_get(), ev_get()};
+    cudaEventRecord(r.a, st_);
+    cudaError_t e = f();
+    cudaEventRecord(r.b, st_);
+    recs_.push_back(r);
+    return e;
+  }
+
+  // ------------------------------------------------------------------ conv dispatch
+  paragan_status conv_fwd(const void* x, int n, int H, const ConvL& c, void* y, const float* bias,
+                          const void* res, int res_mode, const float* alpha = nullptr) {
+    if constexpr (kBF) {
+      if (!c.f32) {
+        TcEpilogue e;
+        e.bias = bias;
+        e.alpha = alpha;
+        e.residual = res;
+        e.res_mode = res ? res_mode : 0;
+        e.out = y;
+        const double fl = 2.0 * n * H * H * (double)c.cout * c.ksz * c.ksz * c.cin;
+        CK(timed(0, fl, [&] { return tc_conv_fprop(x, n, H, H, c.cin_x, c.wp, c.cout, c.ksz, e, st_); }));
+        return PARAGAN_OK;
+      }
+    }
+    CK((simt_conv_fwd<float, float, float>(static_cast<const float*>(x), n, H, H, c.cin_x,
+                                           static_cast<const float*>(c.wp), c.cout, c.ksz, bias, alpha,
+                                           static_cast<const float*>(res), res_mode, static_cast<float*>(y), st_)));
+    return PARAGAN_OK;
+  }
+  // dx[n,H,H,cin_x] = alpha * dgrad(dy) (+ add)
+  paragan_status conv_dgrad(const void* dy, int n, int H, const ConvL& c, void* dx, const void* add,
+                            const float* alpha = nullptr) {
+    if constexpr (kBF) {
+      if (!c.f32) {
+        TcEpilogue e;
+        e.alpha = alpha;
+        e.residual = add;
+        e.res_mode = add ? 1 : 0;
+        e.out = dx;
+        const double fl = 2.0 * n * H * H * (double)c.cout * c.ksz * c.ksz * c.cin;
+        CK(timed(0, fl, [&] { return tc_conv_fprop(dy, n, H, H, c.cout, c.wt, c.cin_x, c.ksz, e, st_); }));
+        return PARAGAN_OK;
+      }
+    }
+    CK((simt_conv_fwd<float, float, float>(static_cast<const float*>(dy), n, H, H, c.cout,
+                                           static_cast<const float*>(c.wt), c.cin_x, c.ksz, nullptr, alpha,
+                                           static_cast<const float*>(add), add ? 1 : 0, static_cast<float*>(dx),
+                                           st_)));
+    return PARAGAN_OK;
+  }
+  // dW (into the net's grad slot, OHWI) = wgrad(x, dy)
+  paragan_status conv_wgrad(Net& N, const void* x, const void* dy, int n, int H, const ConvL& c) {
+    float* dst = N.G(c.w);
+    const bool pad = c.cin_x != c.cin;
+    float* out = pad ? wg_scratch_ : dst;
+    if constexpr (kBF) {
+      if (!c.f32) {
+        const double fl = 2.0 * n * H * H * (double)c.cout * c.ksz * c.ksz * c.cin;
+        CK(timed(1, fl, [&] {
+          return tc_conv_wgrad(x, dy, n, H, H, c.cin_x, c.cout, c.ksz, out, 0, scratch_f_, scratch_floats_, st_);
+        }));
+        if (pad) CK(copy_rows_cols(out, c.cin_x, (long long)c.cout * c.ksz * c.ksz, c.cin, dst, c.cin, 0, st_));
+        return PARAGAN_OK;
+      }
+    }
+    CK((simt_conv_wgrad<float, float>(static_cast<const float*>(x), static_cast<const float*>(dy), n, H, H, c.cin_x,
+                                      c.cout, c.ksz, out, 0, st_)));
+    if (pad) CK(copy_rows_cols(out, c.cin_x, (long long)c.cout * c.ksz * c.ksz, c.cin, dst, c.cin, 0, st_));
+    return PARAGAN_OK;
+  }
+  paragan_status bias_grad(Net& N, const ConvL& c, const void* dy, long long M) {
+    if (c.b < 0) return PARAGAN_OK;
+    CK(col_sum<T>(static_cast<const T*>(dy), M, c.cout, dpart_, kMaxPartialBlocks, N.G(c.b), 0, st_));
+    return PARAGAN_OK;
+  }
+  paragan_status bgemm(int batch, int M, int N, int K, const void* A, long long sab, long long sam, long long sak,
+                       const void* Bm, long long sbb, long long sbn, long long sbk, void* C, bool c_f32, long long scb,
+                       long long ldc) {
+    if constexpr (kBF) {
+      cublasStatus_t s = gemm_rm(cublas_, batch, M, N, K, A, CUDA_R_16BF, sab, sam, sak, Bm, CUDA_R_16BF, sbb, sbn, sbk,
+                                 C, c_f32 ? CUDA_R_32F : CUDA_R_16BF, scb, ldc, 0.0f);
+      ++launches_;
+      if (s != CUBLAS_STATUS_SUCCESS) return fail_msg(PARAGAN_ERR_CUDA, "cublas gemm " + std::to_string((int)s));
+      return PARAGAN_OK;
+    } else {
+      (void)c_f32;
+      CK(gemm_f32_batched(batch, M, N, K, static_cast<const float*>(A), sab, sam, sak, static_cast<const float*>(Bm),
+                          sbb, sbn, sbk, static_cast<float*>(C), scb, ldc, 0.0f, st_));
+      return PARAGAN_OK;
+    }
+  }
+  // cross-replica BN statistics (A4): local sums -> NCCL all-reduce -> mean / rstd
+  paragan_status bn_forward_stats(const void* x, long long M, int C, double* sums, float* mean, float* rstd) {
+    CK(bn_stats<T>(static_cast<const T*>(x), M, C, dpart_, kMaxPartialBlocks, sums, st_));
+    ++launches_;
+    if (cfg_.world_size > 1) {
+      ncclResult_t r = ncclAllReduce(sums, sums, 2 * C, ncclFloat64, ncclSum, comm_, st_);
+      if (r != ncclSuccess) return fail_msg(PARAGAN_ERR_NCCL, std::string("bn allreduce: ") + ncclGetErrorString(r));
+    }
+    CK(bn_finalize(sums, C, (double)M * cfg_.world_size, cfg_.bn_eps, mean, rstd, st_));
+    return PARAGAN_OK;
+  }
+  paragan_status allreduce_small(double* p, int n) {
+    if (cfg_.world_size > 1) {
+      ncclResult_t r = ncclAllReduce(p, p, n, ncclFloat64, ncclSum, comm_, st_);
+      if (r != ncclSuccess) return fail_msg(PARAGAN_ERR_NCCL, std::string("allreduce: ") + ncclGetErrorString(r));
+    }
+    return PARAGAN_OK;
+  }
+  void* tmp(int i) { return tmp_[i]; }
+
+  // ------------------------------------------------------------------ G forward (A3, A4, A5, A6)
+  paragan_status g_forward(const float* z, const int32_t* y, bool train) {
+    (void)train;
+    const int B = B_;
+    CK(cudaMemcpyAsync(zin_, z, sizeof(float) * B * dimz_, cudaMemcpyDeviceToDevice, st_));
+    CK(cudaMemcpyAsync(yg_, y, sizeof(int32_t) * B, cudaMemcpyDeviceToDevice, st_));
+    CK(gather_rows(G_.P(shared_), yg_, B, cfg_.shared_dim, emb_, cfg_.shared_dim, st_));
+    // linear z0 -> [B, 4, 4, C0]  (R10: NHWC view of the 16*C0 vector)
+    CK(gemm_f32(B, 16 * c0_, zc_, zin_, dimz_, 1, glin_.what, zc_, 1, h0f_, 16 * c0_, 0.0f, G_.P(glin_.b), st_));
+    CK(convert_f32<T>(h0f_, static_cast<T*>(gb_[0].x), (long long)B * 16 * c0_, st_));
+    for (size_t i = 0; i < gb_.size(); ++i) {
+      GBlock& b = gb_[i];
+      const int H = b.hin, H2 = 2 * H;
+      // cond_i = [shared[y] | z_{i+1}]  (R11)
+      CK(copy_cols(emb_, cfg_.shared_dim, B, cfg_.shared_dim, b.cond, cd_, st_));
+      CK(copy_cols(zin_ + (i + 1) * zc_, dimz_, B, zc_, b.cond + cfg_.shared_dim, cd_, st_));
+      CK(gemm_f32(B, b.cin, cd_, b.cond, cd_, 1, b.g1.what, cd_, 1, b.gain1, b.cin, 0.0f, nullptr, st_));
+      CK(gemm_f32(B, b.cin, cd_, b.cond, cd_, 1, b.b1.what, cd_, 1, b.bias1, b.cin, 0.0f, nullptr, st_));
+      CK(gemm_f32(B, b.cout, cd_, b.cond, cd_, 1, b.g2.what, cd_, 1, b.gain2, b.cout, 0.0f, nullptr, st_));
+      CK(gemm_f32(B, b.cout, cd_, b.cond, cd_, 1, b.b2.what, cd_, 1, b.bias2, b.cout, 0.0f, nullptr, st_));
+      // CBN1 -> ReLU -> up x2 (fused)
+      CKS(bn_forward_stats(b.x, (long long)B * H * H, b.cin, b.sums1, b.mean1, b.rstd1));
+      CK((bn_apply_relu<T, T>(static_cast<const T*>(b.x), B, H, H, b.cin, b.mean1, b.rstd1, b.gain1, b.bias1, nullptr,
+                              nullptr, static_cast<T*>(b.u1), true, st_)));
+      CKS(conv_fwd(b.u1, B, H2, b.c1, b.h1, G_.P(b.c1.b), nullptr, 0));
+      CKS(bn_forward_stats(b.h1, (long long)B * H2 * H2, b.cout, b.sums2, b.mean2, b.rstd2));
+      CK((bn_apply_relu<T, T>(static_cast<const T*>(b.h1), B, H2, H2, b.cout, b.mean2, b.rstd2, b.gain2, b.bias2,
+                              nullptr, nullptr, static_cast<T*>(b.a2), false, st_)));
+      // skip 1x1 before the upsample (commutes), added by conv2's epilogue with x2 nearest indexing
+      CKS(conv_fwd(b.x, B, H, b.sc, b.s, G_.P(b.sc.b), nullptr, 0));
+      void* out = b.out;
+      CKS(conv_fwd(b.a2, B, H2, b.c2, out, G_.P(b.c2.b), b.s, 2));
+      if (b.attn) {
+        CKS(attn_forward(G_, gattn_, out, B, attn_out_[0]));
+        out = attn_out_[0];
+      }
+      void* next = (i + 1 < gb_.size()) ? gb_[i + 1].x : gout_in_;
+      CK(cudaMemcpyAsync(next, out, sizeof(T) * (size_t)B * H2 * H2 * b.cout, cudaMemcpyDeviceToDevice, st_));
+    }
+    // output layer in fp32: BN -> ReLU -> conv3x3 (96 -> 3) -> tanh
+    const long long M = (long long)B * R_ * R_;
+    CKS(bn_forward_stats(gout_in_, M, cl_, osums_, omean_, orstd_));
+    CK((bn_apply_relu<T, float>(static_cast<const T*>(gout_in_), B, R_, R_, cl_, omean_, orstd_, nullptr, nullptr,
+                                G_.P(obn_g_), G_.P(obn_b_), aout_, false, st_)));
+    CK((simt_conv_fwd<float, float, float>(aout_, B, R_, R_, cl_, static_cast<const float*>(oconv_.wp), 3, 3,
+                                           G_.P(oconv_.b), nullptr, nullptr, 0, pre_, st_)));
+    CK(tanh_to_image<T>(pre_, img_, static_cast<T*>(dimg_), M, cpad_, st_));
+    return PARAGAN_OK;
+  }
+
+  // ------------------------------------------------------------------ attention (A6)
+  paragan_status attn_forward(Net& N, AttnL& a, const void* x, int n, void* out) {
+    const int H = a.H;
+    const long long HW = (long long)H * H, Q = HW / 4;
+    {
+      TcEpilogue e;
+      e.out = a.qkv;
+      if constexpr (kBF) {
+        CK(tc_conv_fprop(x, n, H, H, a.C, a.qkv_wp, a.Ct, 1, e, st_));
+      } else {
+        CK((simt_conv_fwd<float, float, float>(static_cast<const float*>(x), n, H, H, a.C,
+                                               static_cast<const float*>(a.qkv_wp), a.Ct, 1, nullptr, nullptr, nullptr,
+                                               0, static_cast<float*>(a.qkv), st_)));
+      }
+    }
+    const T* qkv = static_cast<const T*>(a.qkv);
+    CK(maxpool2_split<T>(qkv, n, H, H, a.Ct, a.Cq, a.C8, static_cast<T*>(a.phi_p), nullptr, st_));
+    CK(maxpool2_split<T>(qkv, n, H, H, a.Ct, 2 * a.Cq, a.C2, static_cast<T*>(a.g_p), nullptr, st_));
+    // S = theta phi^T  [n][HW][Q] fp32
+    CKS(bgemm(n, (int)HW, (int)Q, a.C8, qkv, HW * a.Ct, a.Ct, 1, a.phi_p, Q * a.C8, a.C8, 1, a.S, true, HW * Q, Q));
+    CK(softmax_rows<T>(a.S, n * HW, (int)Q, static_cast<T*>(a.P), st_));
+    // o = beta g  [n][HW][C2]
+    CKS(bgemm(n, (int)HW, a.C2, (int)Q, a.P, HW * Q, Q, 1, a.g_p, Q * a.C2, 1, a.C2, a.ov, !kBF, HW * a.C2, a.C2));
+    // out = x + gamma * conv1x1(o)
+    CKS(conv_fwd(a.ov, n, H, a.oc, out, nullptr, x, 1, N.P(a.gamma)));
+    return PARAGAN_OK;
+  }
+  // dout -> dx (= dout + attention path), weight grads when want_w
+  paragan_status attn_backward(Net& N, AttnL& a, const void* x, int n, const void* dout, void* dx, bool want_w) {
+    const int H = a.H;
+    const long long HW = (long long)H * H, Q = HW / 4;
+    const long long M = n * HW;
+    void* dO = tmp_attn_dO_;
+    void* dqkv = tmp_attn_dqkv_;
+    if (want_w) {
+      // G_o = wgrad(o, dout) unscaled; dgamma = <W_o/sigma, G_o>; dW_o_hat = gamma * G_o
+      float* go = N.G(a.oc.w);
+      CKS(conv_wgrad(N, a.ov, dout, n, H, a.oc));
+      const int job = N.E[a.oc.w].job;
+      CK(dot_f32(N.P(a.oc.w), go, (long long)a.C * a.C2, N.G(a.gamma), 0, st_));
+      CK(scale_dev(N.G(a.gamma), 1, N.sigma + 2 * job + 1, st_));
+      CK(scale_dev(go, (long long)a.C * a.C2, N.P(a.gamma), st_));
+    }
+    CKS(conv_dgrad(dout, n, H, a.oc, dO, nullptr, N.P(a.gamma)));   // dO = gamma * W_o^T dout
+    float* dP = a.S;   // reuse S
+    // dgp = P^T dO  [n][Q][C2] fp32 ; dP = dO gp^T [n][HW][Q] fp32
+    float* dgp = dpool_;
+    CKS(bgemm(n, (int)Q, a.C2, (int)HW, a.P, HW * Q, 1, Q, dO, HW * a.C2, 1, a.C2, dgp, true, Q * a.C2, a.C2));
+    CKS(bgemm(n, (int)HW, (int)Q, a.C2, dO, HW * a.C2, a.C2, 1, a.g_p, Q * a.C2, a.C2, 1, dP, true, HW * Q, Q));
+    CK(softmax_bwd_rows<T>(static_cast<const T*>(a.P), dP, M, (int)Q, static_cast<T*>(a.P), st_));  // P <- dS
+    const void* dS = a.P;
+    CK(cudaMemsetAsync(dqkv, 0, sizeof(T) * (size_t)M * a.Ct, st_));
+    // dtheta = dS phi_p -> dqkv[:, 0:C8]
+    CKS(bgemm(n, (int)HW, a.C8, (int)Q, dS, HW * Q, Q, 1, a.phi_p, Q * a.C8, 1, a.C8, dqkv, false, HW * a.Ct, a.Ct));
+    // dphi_p = dS^T theta [n][Q][C8] fp32
+    float* dph = dpool_ + (size_t)n * Q * a.C2;
+    CKS(bgemm(n, (int)Q, a.C8, (int)HW, dS, HW * Q, 1, Q, a.qkv, HW * a.Ct, 1, a.Ct, dph, true, Q * a.C8, a.C8));
+    CK(maxpool2_split_bwd<T>(static_cast<const T*>(a.qkv), n, H, H, a.Ct, a.Cq, a.C8, dph, static_cast<T*>(dqkv), st_));
+    CK(maxpool2_split_bwd<T>(static_cast<const T*>(a.qkv), n, H, H, a.Ct, 2 * a.Cq, a.C2, dgp, static_cast<T*>(dqkv),
+                             st_));
+    // dx = dout + W_qkv^T dqkv
+    ConvL q;
+    q.cin = a.C;
+    q.cin_x = a.C;
+    q.cout = a.Ct;
+    q.ksz = 1;
+    q.wp = a.qkv_wp;
+    q.wt = a.qkv_wt;
+    CKS(conv_dgrad(dqkv, n, H, q, dx, dout));
+    if (want_w) {
+      // wgrad of the packed qkv conv, then scatter the real rows to theta / phi / g
+      if constexpr (kBF) {
+        CK(tc_conv_wgrad(x, dqkv, n, H, H, a.C, a.Ct, 1, wg_scratch_, 0, scratch_f_, scratch_floats_, st_));
+      } else {
+        CK((simt_conv_wgrad<float, float>(static_cast<const float*>(x), static_cast<const float*>(dqkv), n, H, H, a.C,
+                                          a.Ct, 1, wg_scratch_, 0, st_)));
+      }
+      CK(copy_rows_cols(wg_scratch_, a.C, a.C8, a.C, N.G(a.th), a.C, 0, st_));
+      CK(copy_rows_cols(wg_scratch_ + (size_t)a.Cq * a.C, a.C, a.C8, a.C, N.G(a.ph), a.C, 0, st_));
+      CK(copy_rows_cols(wg_scratch_ + (size_t)2 * a.Cq * a.C, a.C, a.C2, a.C, N.G(a.gg), a.C, 0, st_));
+    }
+    return PARAGAN_OK;
+  }
+
+  // ------------------------------------------------------------------ D forward (A7)
+  paragan_status d_forward(int n) {
+    for (size_t j = 0; j < db_.size(); ++j) {
+      DBlock& b = db_[j];
+      const int H = b.hin, Ho = b.hout;
+      const long long Mi = (long long)n * H * H;
+      const void* cin = b.x;
+      if (j > 0) {
+        CK(relu_copy<T>(static_cast<const T*>(b.x), static_cast<T*>(b.rx), Mi * b.cin_x, st_));
+        cin = b.rx;
+      }
+      CKS(conv_fwd(cin, n, H, b.c1, b.c1o, D_.P(b.c1.b), nullptr, 0));
+      CK(relu_copy<T>(static_cast<const T*>(b.c1o), static_cast<T*>(b.r1), Mi * b.cout, st_));
+      if (j == 0 && b.down) {
+        // skip: avgpool the image, then 1x1 conv (block 0 has no pre-activation)
+        CK(avgpool2<T>(static_cast<const T*>(b.x), n, H, H, b.cin_x, b.cin_x, nullptr, static_cast<T*>(b.xp), st_));
+        CKS(conv_fwd(b.xp, n, Ho, b.sc, b.s, D_.P(b.sc.b), nullptr, 0));
+        CKS(conv_fwd(b.r1, n, H, b.c2, b.t, D_.P(b.c2.b), nullptr, 0));
+        CK(avgpool2<T>(static_cast<const T*>(b.t), n, H, H, b.cout, b.cout, static_cast<const T*>(b.s),
+                       static_cast<T*>(b.out), st_));
+      } else {
+        const void* skip = b.x;
+        if (b.learn_sc) {
+          CKS(conv_fwd(b.x, n, H, b.sc, b.s, D_.P(b.sc.b), nullptr, 0));
+          skip = b.s;
+        }
+        if (b.down) {
+          CKS(conv_fwd(b.r1, n, H, b.c2, b.t, D_.P(b.c2.b), skip, 1));
+          CK(avgpool2<T>(static_cast<const T*>(b.t), n, H, H, b.cout, b.cout, nullptr, static_cast<T*>(b.out), st_));
+        } else {
+          CKS(conv_fwd(b.r1, n, H, b.c2, b.out, D_.P(b.c2.b), skip, 1));
+        }
+      }
+      if (b.attn) CKS(attn_forward(D_, dattn_, b.out, n, attn_out_[1]));
+    }
+    const DBlock& last = db_.back();
+    const void* hlast = last.attn ? attn_out_[1] : last.out;
+    CK(d_head_fwd<T>(static_cast<const T*>(hlast), n, hl_ * hl_, cdl_, dlin_.what, D_.P(dlin_.b), demb_hat_, ylab_,
+                     feat_, logits_, st_));
+    return PARAGAN_OK;
+  }
+
+  // ------------------------------------------------------------------ D backward (A8-A11)
+  // want_w: weight grads (D step); want_dimg: gradient down to the image (G step)
+  paragan_status d_backward(int n, bool want_w, bool want_dimg) {
+    const DBlock& last = db_.back();
+    const void* hlast = last.attn ? attn_out_[1] : last.out;
+    void* cur = tmp(0);   // gradient w.r.t. the current block output
+    CK(d_head_bwd<T>(static_cast<const T*>(hlast), n, hl_ * hl_, cdl_, dlin_.what, demb_hat_, ylab_, feat_, dlogits_,
+                     static_cast<T*>(cur), D_.G(dlin_.w), D_.G(dlin_.b), D_.G(demb_), cfg_.n_classes, want_w, st_));
+    int ic = 0;   // index of cur in tmp_
+    auto other = [&](int a_, int b_ = -1, int c_ = -1) {
+      for (int k = 0; k < 4; ++k)
+        if (k != a_ && k != b_ && k != c_) return k;
+      return -1;
+    };
+    for (int j = (int)db_.size() - 1; j >= 0; --j) {
+      DBlock& b = db_[j];
+      const int H = b.hin, Ho = b.hout;
+      const long long Mi = (long long)n * H * H;
+      if (b.attn) {
+        const int k = other(ic);
+        CKS(attn_backward(D_, dattn_, b.out, n, cur, tmp(k), want_w));
+        ic = k;
+        cur = tmp(k);
+      }
+      // dt: gradient at the conv2 output (full res)
+      int it;
+      void* dt;
+      if (b.down) {
+        it = other(ic);
+        dt = tmp(it);
+        CK(avgpool2_bwd<T>(static_cast<const T*>(cur), n, H, H, b.cout, nullptr, static_cast<T*>(dt), b.cout, st_));
+      } else {
+        it = ic;
+        dt = cur;
+      }
+      // conv2 backward
+      const int ir1 = other(ic, it);
+      void* dr1 = tmp(ir1);
+      CKS(conv_dgrad(dt, n, H, b.c2, dr1, nullptr));
+      if (want_w) {
+        CKS(conv_wgrad(D_, b.r1, dt, n, H, b.c2));
+        CKS(bias_grad(D_, b.c2, dt, Mi));
+      }
+      // skip branch
+      const bool need_dx = (j > 0) || want_dimg;
+      int isk = -1;
+      void* dskip = nullptr;
+      if (j == 0 && b.down) {
+        // s = sc(avgpool(x)) at half res; its gradient is cur (half res)
+        if (want_w) {
+          CKS(conv_wgrad(D_, b.xp, cur, n, Ho, b.sc));
+          CKS(bias_grad(D_, b.sc, cur, (long long)n * Ho * Ho));
+        }
+        if (need_dx) {
+          isk = other(ic, it, ir1);
+          // dxp (half res) into the tail of tmp(isk), then avgpool adjoint into tmp(isk) head
+          void* dxp = dxp_;
+          CKS(conv_dgrad(cur, n, Ho, b.sc, dxp, nullptr));
+          CK(avgpool2_bwd<T>(static_cast<const T*>(dxp), n, H, H, b.cin_x, nullptr, static_cast<T*>(tmp(isk)),
+                             b.cin_x, st_));
+          dskip = tmp(isk);
+        }
+      } else if (b.learn_sc) {
+        if (want_w) {
+          CKS(conv_wgrad(D_, b.x, dt, n, H, b.sc));
+          CKS(bias_grad(D_, b.sc, dt, Mi));
+        }
+        if (need_dx) {
+          isk = other(ic, it, ir1);
+          CKS(conv_dgrad(dt, n, H, b.sc, tmp(isk), nullptr));
+          dskip = tmp(isk);
+        }
+      } else {
+        dskip = dt;   // identity skip
+        isk = it;
+      }
+      // relu between conv1 and conv2: dc1 = dr1 * [c1 > 0] (in place)
+      CK(relu_bwd<T>(static_cast<const T*>(dr1), static_cast<const T*>(b.r1), nullptr, static_cast<T*>(dr1),
+                     Mi * b.cout, st_));
+      const void* cin = (j > 0) ? b.rx : b.x;
+      if (want_w) {
+        CKS(conv_wgrad(D_, cin, dr1, n, H, b.c1));
+        CKS(bias_grad(D_, b.c1, dr1, Mi));
+      }
+      if (!need_dx) break;
+      // dx = relu'(x) * dgrad(conv1) + dskip   (block 0: no pre-activation)
+      int ix = -1;
+      for (int k = 0; k < 4; ++k)
+        if (k != ir1 && k != isk) { ix = k; break; }
+      void* dx = tmp(ix);
+      if (j > 0) {
+        CKS(conv_dgrad(dr1, n, H, b.c1, dx, nullptr));
+        CK(relu_bwd<T>(static_cast<const T*>(dx), static_cast<const T*>(b.x), static_cast<const T*>(dskip),
+                       static_cast<T*>(dx), Mi * b.cin_x, st_));
+      } else {
+        CKS(conv_dgrad(dr1, n, H, b.c1, dx, dskip));
+      }
+      cur = dx;
+      ic = ix;
+    }
+    dimg_grad_ = want_dimg ? cur : nullptr;
+    dimg_idx_ = ic;
+    return PARAGAN_OK;
+  }
+
+  // ------------------------------------------------------------------ G backward (A9-A11)
+  paragan_status g_backward() {
+    const int B = B_;
+    const long long M = (long long)B * R_ * R_;
+    // tanh' and the fp32 output conv
+    CK(tanh_bwd<T>(static_cast<const T*>(dimg_grad_), cpad_, img_, dpre_, M, st_));
+    CK((simt_conv_wgrad<float, float>(aout_, dpre_, B, R_, R_, cl_, 3, 3, G_.G(oconv_.w), 0, st_)));
+    CK(col_sum<float>(dpre_, M, 3, dpart_, kMaxPartialBlocks, G_.G(oconv_.b), 0, st_));
+    CK((simt_conv_fwd<float, float, float>(dpre_, B, R_, R_, 3, static_cast<const float*>(oconv_.wt), cl_, 3, nullptr,
+                                           nullptr, nullptr, 0, daout_, st_)));
+    // output BN backward (plain BN, learned gamma/beta)
+    int ic = (dimg_idx_ + 1) % 4;
+    void* cur = tmp(ic);
+    CK((bn_bwd_reduce<T, float>(static_cast<const T*>(gout_in_), daout_, B, R_, R_, cl_, omean_, orstd_, nullptr,
+                                nullptr, G_.P(obn_g_), G_.P(obn_b_), false, bn_part_, bn_chunks(R_ * R_), ab_, st_)));
+    // dgamma[c] = sum_n Bv[n][c], dbeta[c] = sum_n A[n][c]: channel totals with unit gain
+    CK(bn_bwd_totals(ab_, B, cl_, nullptr, ones_(cl_), tot_, st_));
+    CK(to_f32_from_d(tot_, G_.G(obn_b_), cl_));
+    CK(to_f32_from_d(tot_ + cl_, G_.G(obn_g_), cl_));
+    CK(bn_bwd_totals(ab_, B, cl_, nullptr, G_.P(obn_g_), tot_, st_));
+    CKS(allreduce_small(tot_, 2 * cl_));
+    CK((bn_bwd_apply<T, float, T>(static_cast<const T*>(gout_in_), daout_, B, R_, R_, cl_, omean_, orstd_, nullptr,
+                                  nullptr, G_.P(obn_g_), G_.P(obn_b_), false, tot_, (double)M * cfg_.world_size,
+                                  nullptr, static_cast<T*>(cur), st_)));
+    for (int i = (int)gb_.size() - 1; i >= 0; --i) {
+      GBlock& b = gb_[i];
+      const int H = b.hin, H2 = 2 * H;
+      const long long Mlo = (long long)B * H * H, Mhi = (long long)B * H2 * H2;
+      if (b.attn) {
+        const int k = (ic + 1) % 4;
+        CKS(attn_backward(G_, gattn_, b.out, B, cur, tmp(k), true));
+        ic = k;
+        cur = tmp(k);
+      }
+      const int i_a2 = (ic + 1) % 4, i_ds = (ic + 2) % 4, i_dxs = (ic + 3) % 4;
+      // conv2
+      CKS(conv_dgrad(cur, B, H2, b.c2, tmp(i_a2), nullptr));
+      CKS(conv_wgrad(G_, b.a2, cur, B, H2, b.c2));
+      CKS(bias_grad(G_, b.c2, cur, Mhi));
+      // skip: out += up2(s) -> ds = 2x2 sum of dout
+      CK(up2_bwd<T>(static_cast<const T*>(cur), B, H, H, b.cout, static_cast<T*>(tmp(i_ds)), st_));
+      CKS(conv_wgrad(G_, b.x, tmp(i_ds), B, H, b.sc));
+      CKS(bias_grad(G_, b.sc, tmp(i_ds), Mlo));
+      CKS(conv_dgrad(tmp(i_ds), B, H, b.sc, tmp(i_dxs), nullptr));
+      // CBN2 backward: da2 -> dh1 (into cur's buffer)
+      CKS(cbn_backward(b.h1, tmp(i_a2), B, H2, b.cout, b.mean2, b.rstd2, b.gain2, b.bias2, false, nullptr, cur,
+                       b.g2, b.b2, b.cond, b.dcond, true));
+      // conv1 on the upsampled activation
+      CKS(conv_wgrad(G_, b.u1, cur, B, H2, b.c1));
+      CKS(bias_grad(G_, b.c1, cur, Mhi));
+      CKS(conv_dgrad(cur, B, H2, b.c1, tmp(i_a2), nullptr));
+      // CBN1 backward through the upsample (2x2 sum), plus the skip gradient
+      CKS(cbn_backward(b.x, tmp(i_a2), B, H, b.cin, b.mean1, b.rstd1, b.gain1, b.bias1, true, tmp(i_dxs), tmp(i_ds),
+                       b.g1, b.b1, b.cond, b.dcond, false));
+      // cond -> shared embedding gradient (first shared_dim columns)
+      CK(scatter_add_rows(b.dcond, cd_, yg_, B, cfg_.shared_dim, G_.G(shared_), st_));
+      ic = i_ds;
+      cur = tmp(ic);
+    }
+    // G linear: h0 = z0 W^T + b
+    CK(to_f32<T>(static_cast<const T*>(cur), dh0f_, (long long)B * 16 * c0_, st_));
+    CK(gemm_f32(16 * c0_, zc_, B, dh0f_, 1, 16 * c0_, zin_, 1, dimz_, G_.G(glin_.w), zc_, 0.0f, nullptr, st_));
+    CK(col_sum<float>(dh0f_, B, 16 * c0_, dpart_, kMaxPartialBlocks, G_.G(glin_.b), 0, st_));
+    return PARAGAN_OK;
+  }
+  // conditional BN backward; writes dx (+ add), per-sample gain/bias grads into the CBN linears and dcond
+  paragan_status cbn_backward(const void* x, const void* dy, int n, int H, int C, const float* mean, const float* rstd,
+                              const float* gain, const float* bias, bool up2, const void* add, void* dx,
+                              const LinL& lg, const LinL& lb, const float* cond, float* dcond, bool first) {
+    CK((bn_bwd_reduce<T, T>(static_cast<const T*>(x), static_cast<const T*>(dy), n, H, H, C, mean, rstd, gain, bias,
+                            nullptr, nullptr, up2, bn_part_, bn_chunks(H * H), ab_, st_)));
+    CK(bn_bwd_totals(ab_, n, C, gain, nullptr, tot_, st_));
+    CKS(allreduce_small(tot_, 2 * C));
+    CK((bn_bwd_apply<T, T, T>(static_cast<const T*>(x), static_cast<const T*>(dy), n, H, H, C, mean, rstd, gain, bias,
+                              nullptr, nullptr, up2, tot_, (double)n * H * H * cfg_.world_size,
+                              static_cast<const T*>(add), static_cast<T*>(dx), st_)));
+    // AB[n][0:C] = dbias (sum g0), AB[n][C:2C] = dgain (sum g0 * x_hat)
+    const float* dbias = ab_;
+    const float* dgain = ab_ + C;
+    const int ld = 2 * C;
+    // dW_gain[c][k] = sum_n dgain[n][c] cond[n][k]; same for bias
+    CK(gemm_f32(C, cd_, n, dgain, 1, ld, cond, 1, cd_, G_.G(lg.w), cd_, 0.0f, nullptr, st_));
+    CK(gemm_f32(C, cd_, n, dbias, 1, ld, cond, 1, cd_, G_.G(lb.w), cd_, 0.0f, nullptr, st_));
+    // dcond[n][k] (+)= sum_c dgain[n][c] What[c][k] + dbias[n][c] Bhat[c][k]
+    CK(gemm_f32(n, cd_, C, dgain, ld, 1, lg.what, 1, cd_, dcond, cd_, first ? 0.0f : 1.0f, nullptr, st_));
+    CK(gemm_f32(n, cd_, C, dbias, ld, 1, lb.what, 1, cd_, dcond, cd_, 1.0f, nullptr, st_));
+    return PARAGAN_OK;
+  }
+  int bn_chunks(long long hw) const {
+    long long c = (hw + 1023) / 1024;
+    if (c < 1) c = 1;
+    if (c > 64) c = 64;
+    return (int)c;
+  }
+  const float* ones_(int C) {
+    (void)C;
+    return ones_buf_;
+  }
+  cudaError_t to_f32_from_d(const double* s, float* d, int n) {
+    // tiny: copy through host-free kernel path (reuse convert via scratch)
+    return d2f(s, d, n, st_);
+  }
+  static cudaError_t d2f(const double* s, float* d, int n, cudaStream_t st);
+
+  // ------------------------------------------------------------------ state
+  paragan_config cfg_;
+  cudaStream_t st_;
+  ncclComm_t comm_ = nullptr;
+  cublasHandle_t cublas_ = nullptr;
+  bool ready_ = false, poisoned_ = false, planned_ = false, ones_ready_ = false;
+  int d_since_g_ = 0;
+  uint64_t launches_ = 0;
+  Net G_, D_;
+  std::vector<SnJob> jobs_h_[2];
+  int B_ = 0, R_ = 0, cpad_ = 0, zc_ = 0, dimz_ = 0, cd_ = 0, c0_ = 0, cl_ = 0, cdl_ = 0, hl_ = 0;
+  int shared_ = -1, obn_g_ = -1, obn_b_ = -1, demb_ = -1;
+  LinL glin_, dlin_;
+  ConvL oconv_;
+  std::vector<GBlock> gb_;
+  std::vector<DBlock> db_;
+  AttnL gattn_, dattn_;
+  void* attn_out_[2] = {nullptr, nullptr};
+  long long big_ = 0;
+  void* tmp_[4] = {};
+  void* tmp_attn_dO_ = nullptr;
+  void* dxp_ = nullptr;
+  bool prof_ = false;
+  std::vector<ProfRec> recs_;
+  std::vector<cudaEvent_t> ev_free_;
+  float* ones_buf_ = nullptr;
+  int maxc_ = 8;
+  void* tmp_attn_dqkv_ = nullptr;
+  float *zin_ = nullptr, *emb_ = nullptr, *demb_g_ = nullptr, *h0f_ = nullptr, *dh0f_ = nullptr;
+  int32_t *yg_ = nullptr, *ylab_ = nullptr;
+  void* gout_in_ = nullptr;
+  float *aout_ = nullptr, *daout_ = nullptr, *omean_ = nullptr, *orstd_ = nullptr, *pre_ = nullptr, *img_ = nullptr,
+        *dpre_ = nullptr;
+  double* osums_ = nullptr;
+  void* dimg_ = nullptr;
+  void* dimg_grad_ = nullptr;
+  int dimg_idx_ = 0;
+  float* demb_hat_ = nullptr;
+  float *feat_ = nullptr, *logits_ = nullptr, *dlogits_ = nullptr;
+  float *ab_ = nullptr, *bn_part_ = nullptr;
+  double *dpart_ = nullptr, *tot_ = nullptr;
+  float *scratch_f_ = nullptr, *wg_scratch_ = nullptr, *dpool_ = nullptr;
+  size_t scratch_floats_ = 0;
+  int* nonfinite_sticky_ = nullptr;
+#undef CK
+#undef CKS
+};
+
+namespace {
+__global__ void k_d2f(const double* s, float* d, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) d[i] = (float)s[i];
+}
+}  // namespace
+template <typename T>
+cudaError_t Engine<T>::d2f(const double* s, float* d, int n, cudaStream_t st) {
+  k_d2f<<<(n + 255) / 256, 256, 0, st>>>(s, d, n);
+  return cudaGetLastError();
+}
+
+paragan_status validate_config(const paragan_config* c) {
+  if (!c) return PARAGAN_ERR_INVALID_ARG;
+  if (c->abi_version != PARAGAN_ABI_VERSION) return PARAGAN_ERR_CONFIG;
+  Arch a;
+  if (!arch_for(c->resolution, a)) return PARAGAN_ERR_CONFIG;
+  if (c->ch < 1 || c->n_classes < 1 || c->shared_dim < 1 || c->z_chunk < 1 || c->local_batch < 1 ||
+      c->d_steps_per_g < 1 || c->world_size < 1 || c->rank < 0 || c->rank >= c->world_size)
+    return PARAGAN_ERR_CONFIG;
+  if (c->compute != PARAGAN_F32 && c->compute != PARAGAN_BF16) return PARAGAN_ERR_CONFIG;
+  if (c->c_pad_image < 3 || c->c_pad_image % 8) return PARAGAN_ERR_CONFIG;
+  // every BN / tensor-core channel count must be a multiple of 8 (16-byte NHWC pixel rows)
+  for (int m : a.gin) if ((m * c->ch) % 8) return PARAGAN_ERR_CONFIG;
+  for (int m : a.gout) if ((m * c->ch) % 8 || (m * c->ch) / 8 > 256) return PARAGAN_ERR_CONFIG;
+  for (size_t j = 1; j < a.din.size(); ++j) if ((a.din[j] * c->ch) % 8) return PARAGAN_ERR_CONFIG;
+  if (c->attn_res) {
+    bool ok = false;
+    for (int h = 8; h <= c->resolution; h *= 2) ok |= (h == c->attn_res);
+    if (!ok) return PARAGAN_ERR_CONFIG;
+    // attention channel C must give C/2 % 8 == 0
+    for (size_t i = 0; i < a.gout.size(); ++i)
+      if ((8 << i) == c->attn_res && ((a.gout[i] * c->ch) / 2) % 8) return PARAGAN_ERR_CONFIG;
+  }
+  if (!(c->sn_eps > 0) || !(c->bn_eps > 0)) return PARAGAN_ERR_CONFIG;
+  return PARAGAN_OK;
+}
+
+EngineBase* make_engine(const paragan_config* cfg, void* stream, paragan_status* st) {
+  *st = validate_config(cfg);
+  if (*st != PARAGAN_OK) return nullptr;
+  if (cfg->compute == PARAGAN_BF16) return new Engine<bf16>(*cfg, static_cast<cudaStream_t>(stream));
+  return new Engine<float>(*cfg, static_cast<cudaStream_t>(stream));
+}
+
+}  // namespace pg

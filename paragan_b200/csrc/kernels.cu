@@ -1,0 +1,1504 @@
+// Memory-bound and SIMT kernels of libparagan (see kernels.h for contracts).
+// Access pattern rules (B200): NHWC activations are read/written with one
+// thread per 8-channel group of a pixel (16-byte vectors for bf16), grids are
+// sized in multiples of the 148 SMs, reductions are warp-shuffle + shared
+// memory with fp64 cross-block accumulation in a fixed order (deterministic).
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace pg {
+
+namespace {
+
+inline int grid_for(long long n, int threads, int max_waves = 8) {
+  long long b = (n + threads - 1) / threads;
+  long long cap = (long long)kNumSMs * max_waves;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+template <typename T> struct Vec8;
+template <> struct Vec8<float> {
+  __device__ static void load(const float* p, float (&v)[8]) {
+    float4 a = reinterpret_cast<const float4*>(p)[0], b = reinterpret_cast<const float4*>(p)[1];
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  }
+  __device__ static void store(float* p, const float (&v)[8]) {
+    reinterpret_cast<float4*>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
+    reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
+  }
+};
+template <> struct Vec8<bf16> {
+  __device__ static void load(const bf16* p, float (&v)[8]) {
+    uint4 u = *reinterpret_cast<const uint4*>(p);
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float2 f = __bfloat1622float2(h[j]);
+      v[2 * j] = f.x;
+      v[2 * j + 1] = f.y;
+    }
+  }
+  __device__ static void store(bf16* p, const float (&v)[8]) {
+    uint4 u;
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) h[j] = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+    *reinterpret_cast<uint4*>(p) = u;
+  }
+};
+
+// ===================================================================== layout
+template <typename TD>
+__global__ void k_pack(const float* __restrict__ src, TD* __restrict__ dst, int n, int c, int h, int w, int cp) {
+  const long long total = (long long)n * h * w * cp;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int k = (int)(i % cp);
+    long long p = i / cp;
+    const int x = (int)(p % w);
+    p /= w;
+    const int y = (int)(p % h);
+    const int b = (int)(p / h);
+    float v = 0.0f;
+    if (k < c) v = src[(((long long)b * c + k) * h + y) * w + x];
+    dst[i] = from_f<TD>(v);
+  }
+}
+template <typename TS>
+__global__ void k_unpack(const TS* __restrict__ src, float* __restrict__ dst, int n, int c, int h, int w, int cp) {
+  const long long total = (long long)n * c * h * w;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int x = (int)(i % w);
+    long long p = i / w;
+    const int y = (int)(p % h);
+    p /= h;
+    const int k = (int)(p % c);
+    const int b = (int)(p / c);
+    dst[i] = to_f<TS>(src[(((long long)b * h + y) * w + x) * cp + k]);
+  }
+}
+
+// ===================================================================== small GEMM
+// 64x64 tile, 256 threads, 4x4 per thread, K chunk 16
+template <typename TC>
+__global__ void __launch_bounds__(256) k_gemm(int M, int N, int K, const float* __restrict__ A, long long sab,
+                                              long long sam, long long sak, const float* __restrict__ B, long long sbb,
+                                              long long sbn, long long sbk, TC* __restrict__ C, long long scb,
+                                              long long ldc, float beta, const float* __restrict__ bias) {
+  __shared__ float As[16][65];
+  __shared__ float Bs[16][65];
+  const int b = blockIdx.z;
+  A += b * sab;
+  B += b * sbb;
+  C += b * scb;
+  const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += 16) {
+    for (int i = tid; i < 1024; i += 256) {
+      int mm, kk;
+      if (sak == 1) { mm = i >> 4; kk = i & 15; } else { kk = i >> 6; mm = i & 63; }
+      const int m = m0 + mm, k = k0 + kk;
+      As[kk][mm] = (m < M && k < K) ? A[m * sam + k * sak] : 0.0f;
+      int nn, kb;
+      if (sbk == 1) { nn = i >> 4; kb = i & 15; } else { kb = i >> 6; nn = i & 63; }
+      const int n = n0 + nn, k2 = k0 + kb;
+      Bs[kb][nn] = (n < N && k2 < K) ? B[n * sbn + k2 * sbk] : 0.0f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      float a[4], bb[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bb[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], bb[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int m = m0 + ty * 4 + i;
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int n = n0 + tx * 4 + j;
+      if (n >= N) continue;
+      float v = acc[i][j];
+      if (bias) v += bias[n];
+      TC* cp = C + m * ldc + n;
+      if (beta != 0.0f) v += beta * to_f<TC>(*cp);
+      *cp = from_f<TC>(v);
+    }
+  }
+}
+
+// ===================================================================== gathers
+__global__ void k_gather_rows(const float* __restrict__ table, const int32_t* __restrict__ idx, int n, int dim,
+                              float* __restrict__ out, int ldo) {
+  const long long total = (long long)n * dim;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(i / dim), j = (int)(i % dim);
+    out[(long long)r * ldo + j] = table[(long long)idx[r] * dim + j];
+  }
+}
+__global__ void k_copy_cols(const float* __restrict__ src, int lds, int n, int cols, float* __restrict__ dst,
+                            int ldd) {
+  const long long total = (long long)n * cols;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(i / cols), j = (int)(i % cols);
+    dst[(long long)r * ldd + j] = src[(long long)r * lds + j];
+  }
+}
+__global__ void k_scatter_add_rows(const float* __restrict__ src, int lds, const int32_t* __restrict__ idx, int n,
+                                   int dim, float* __restrict__ dtable) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= dim) return;
+  for (int i = 0; i < n; ++i) dtable[(long long)idx[i] * dim + j] += src[(long long)i * lds + j];
+}
+template <typename TD>
+__global__ void k_convert(const float* __restrict__ s, TD* __restrict__ d, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    d[i] = from_f<TD>(s[i]);
+}
+template <typename TS>
+__global__ void k_to_f32(const TS* __restrict__ s, float* __restrict__ d, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    d[i] = to_f<TS>(s[i]);
+}
+
+// ===================================================================== BN statistics
+// block: 256 threads = R rows x G groups (8 channels each); each block covers a
+// contiguous pixel range; per-thread fp32 partials, block combine in fp64.
+template <typename T>
+__global__ void __launch_bounds__(256) k_bn_stats(const T* __restrict__ x, long long M, int C,
+                                                  double* __restrict__ partial, long long pix_per_blk) {
+  extern __shared__ double sh[];  // [R][2C] doubles
+  const int G = C >> 3;
+  const int R = 256 / G;
+  const int tid = threadIdx.x;
+  const int g = tid % G, r = tid / G;
+  const long long p0 = (long long)blockIdx.x * pix_per_blk;
+  const long long p1 = min(M, p0 + pix_per_blk);
+  float s[8] = {}, q[8] = {};
+  if (r < R) {
+    for (long long p = p0 + r; p < p1; p += R) {
+      float v[8];
+      Vec8<T>::load(x + p * C + g * 8, v);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        s[j] += v[j];
+        q[j] = fmaf(v[j], v[j], q[j]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      sh[r * 2 * C + g * 8 + j] = s[j];
+      sh[r * 2 * C + C + g * 8 + j] = q[j];
+    }
+  }
+  __syncthreads();
+  for (int c = tid; c < 2 * C; c += 256) {
+    double a = 0.0;
+    for (int rr = 0; rr < R; ++rr) a += sh[rr * 2 * C + c];
+    partial[(long long)blockIdx.x * 2 * C + c] = a;
+  }
+}
+__global__ void k_reduce_partials(const double* __restrict__ partial, int nblk, int width, double* __restrict__ out) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < width; c += gridDim.x * blockDim.x) {
+    double a = 0.0;
+    for (int b = 0; b < nblk; ++b) a += partial[(long long)b * width + c];
+    out[c] = a;
+  }
+}
+__global__ void k_bn_finalize(const double* __restrict__ sums, int C, double count, float eps,
+                              float* __restrict__ mean, float* __restrict__ rstd) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  const double mu = sums[c] / count;
+  double var = sums[C + c] / count - mu * mu;
+  if (var < 0) var = 0;
+  mean[c] = (float)mu;
+  rstd[c] = (float)(1.0 / sqrt(var + (double)eps));
+}
+
+// per (pixel, 8-channel group): gain/bias factors
+struct BnAffine {
+  const float* gain;   // [N][C] (conditional: factor 1 + gain)
+  const float* bias;   // [N][C]
+  const float* gamma;  // [C]    (plain BN)
+  const float* beta;   // [C]
+  __device__ __forceinline__ void get(int n, int c, int C, float& g, float& b) const {
+    if (gain) {
+      g = 1.0f + gain[(long long)n * C + c];
+      b = bias[(long long)n * C + c];
+    } else {
+      g = gamma[c];
+      b = beta[c];
+    }
+  }
+};
+
+template <typename TI, typename TO>
+__global__ void k_bn_apply_relu(const TI* __restrict__ x, int N, int H, int W, int C, const float* __restrict__ mean,
+                                const float* __restrict__ rstd, BnAffine af, TO* __restrict__ y, int up2) {
+  const int G = C >> 3;
+  const long long total = (long long)N * H * W * G;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int g = (int)(i % G);
+    const long long p = i / G;
+    const int n = (int)(p / ((long long)H * W));
+    float v[8];
+    Vec8<TI>::load(x + p * C + g * 8, v);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int c = g * 8 + j;
+      float ga, be;
+      af.get(n, c, C, ga, be);
+      const float t = (v[j] - mean[c]) * rstd[c] * ga + be;
+      v[j] = t > 0.0f ? t : 0.0f;
+    }
+    if (!up2) {
+      Vec8<TO>::store(y + p * C + g * 8, v);
+    } else {
+      const int rem = (int)(p - (long long)n * H * W);
+      const int h = rem / W, w = rem - (rem / W) * W;
+      const long long W2 = 2 * W;
+      const long long base = ((long long)n * 2 * H + 2 * h) * W2 + 2 * w;
+      Vec8<TO>::store(y + (base)*C + g * 8, v);
+      Vec8<TO>::store(y + (base + 1) * C + g * 8, v);
+      Vec8<TO>::store(y + (base + W2) * C + g * 8, v);
+      Vec8<TO>::store(y + (base + W2 + 1) * C + g * 8, v);
+    }
+  }
+}
+
+// g0 (gradient w.r.t. the affine output z = x_hat*g + b, through relu) at pixel p
+template <typename TG>
+__device__ __forceinline__ void load_dy(const TG* dy, long long p, int n, int H, int W, int C, int g, int up2,
+                                        float (&d)[8]) {
+  if (!up2) {
+    Vec8<TG>::load(dy + p * C + g * 8, d);
+  } else {
+    const int rem = (int)(p - (long long)n * H * W);
+    const int h = rem / W, w = rem - (rem / W) * W;
+    const long long W2 = 2 * W;
+    const long long base = ((long long)n * 2 * H + 2 * h) * W2 + 2 * w;
+    float a[8], b[8], c[8], e[8];
+    Vec8<TG>::load(dy + base * C + g * 8, a);
+    Vec8<TG>::load(dy + (base + 1) * C + g * 8, b);
+    Vec8<TG>::load(dy + (base + W2) * C + g * 8, c);
+    Vec8<TG>::load(dy + (base + W2 + 1) * C + g * 8, e);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) d[j] = (a[j] + b[j]) + (c[j] + e[j]);
+  }
+}
+
+// grid: (chunks, N); each block sums over its chunk of sample n's pixels
+template <typename TI, typename TG>
+__global__ void __launch_bounds__(256) k_bn_bwd_reduce(const TI* __restrict__ x, const TG* __restrict__ dy, int N,
+                                                       int H, int W, int C, const float* __restrict__ mean,
+                                                       const float* __restrict__ rstd, BnAffine af, int up2,
+                                                       float* __restrict__ partial, int chunks) {
+  extern __shared__ float shf[];  // [R][2C]
+  const int G = C >> 3;
+  const int R = 256 / G;
+  const int tid = threadIdx.x;
+  const int g = tid % G, r = tid / G;
+  const int n = blockIdx.y;
+  const long long HW = (long long)H * W;
+  const long long per = (HW + chunks - 1) / chunks;
+  const long long q0 = blockIdx.x * per, q1 = min(HW, q0 + per);
+  float sa[8] = {}, sb[8] = {};
+  if (r < R) {
+    float ga[8], be[8], mu[8], rs[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      af.get(n, g * 8 + j, C, ga[j], be[j]);
+      mu[j] = mean[g * 8 + j];
+      rs[j] = rstd[g * 8 + j];
+    }
+    for (long long q = q0 + r; q < q1; q += R) {
+      const long long p = (long long)n * HW + q;
+      float v[8], d[8];
+      Vec8<TI>::load(x + p * C + g * 8, v);
+      load_dy<TG>(dy, p, n, H, W, C, g, up2, d);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float xh = (v[j] - mu[j]) * rs[j];
+        const float z = xh * ga[j] + be[j];
+        const float g0 = z > 0.0f ? d[j] : 0.0f;
+        sa[j] += g0;
+        sb[j] = fmaf(g0, xh, sb[j]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      shf[r * 2 * C + g * 8 + j] = sa[j];
+      shf[r * 2 * C + C + g * 8 + j] = sb[j];
+    }
+  }
+  __syncthreads();
+  for (int c = tid; c < 2 * C; c += 256) {
+    float a = 0.0f;
+    for (int rr = 0; rr < R; ++rr) a += shf[rr * 2 * C + c];
+    partial[((long long)n * chunks + blockIdx.x) * 2 * C + c] = a;
+  }
+}
+__global__ void k_bn_bwd_fold(const float* __restrict__ partial, int N, int chunks, int C, float* __restrict__ AB) {
+  const long long total = (long long)N * 2 * C;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int n = (int)(i / (2 * C)), c = (int)(i % (2 * C));
+    double a = 0.0;
+    for (int k = 0; k < chunks; ++k) a += partial[((long long)n * chunks + k) * 2 * C + c];
+    AB[i] = (float)a;
+  }
+}
+__global__ void k_bn_bwd_totals(const float* __restrict__ AB, int N, int C, const float* __restrict__ gain,
+                                const float* __restrict__ gamma, double* __restrict__ tot) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  double t0 = 0.0, t1 = 0.0;
+  for (int n = 0; n < N; ++n) {
+    const double g = gain ? 1.0 + (double)gain[(long long)n * C + c] : (double)gamma[c];
+    t0 += g * AB[(long long)n * 2 * C + c];
+    t1 += g * AB[(long long)n * 2 * C + C + c];
+  }
+  tot[c] = t0;
+  tot[C + c] = t1;
+}
+template <typename TI, typename TG, typename TO>
+__global__ void k_bn_bwd_apply(const TI* __restrict__ x, const TG* __restrict__ dy, int N, int H, int W, int C,
+                               const float* __restrict__ mean, const float* __restrict__ rstd, BnAffine af, int up2,
+                               const double* __restrict__ tot, double count, const TO* __restrict__ add,
+                               TO* __restrict__ dx) {
+  const int G = C >> 3;
+  const long long total = (long long)N * H * W * G;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int g = (int)(i % G);
+    const long long p = i / G;
+    const int n = (int)(p / ((long long)H * W));
+    float v[8], d[8], o[8];
+    Vec8<TI>::load(x + p * C + g * 8, v);
+    load_dy<TG>(dy, p, n, H, W, C, g, up2, d);
+    float ad[8];
+    if (add) Vec8<TO>::load(add + p * C + g * 8, ad);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int c = g * 8 + j;
+      float ga, be;
+      af.get(n, c, C, ga, be);
+      const float xh = (v[j] - mean[c]) * rstd[c];
+      const float z = xh * ga + be;
+      const float g0 = z > 0.0f ? d[j] : 0.0f;
+      const float mg = (float)(tot[c] / count), mgx = (float)(tot[C + c] / count);
+      o[j] = rstd[c] * (ga * g0 - mg - xh * mgx);
+      if (add) o[j] += ad[j];
+    }
+    Vec8<TO>::store(dx + p * C + g * 8, o);
+  }
+}
+
+// ===================================================================== elementwise
+template <typename T>
+__global__ void k_relu_copy(const T* __restrict__ x, T* __restrict__ y, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const float v = to_f<T>(x[i]);
+    y[i] = from_f<T>(v > 0.0f ? v : 0.0f);
+  }
+}
+template <typename T>
+__global__ void k_relu_bwd(const T* __restrict__ dy, const T* __restrict__ ref, const T* __restrict__ add,
+                           T* __restrict__ dx, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    float v = to_f<T>(ref[i]) > 0.0f ? to_f<T>(dy[i]) : 0.0f;
+    if (add) v += to_f<T>(add[i]);
+    dx[i] = from_f<T>(v);
+  }
+}
+// out pixel (n, ho, wo), channel c:  ((x00 + x01) + (x10 + x11)) * 0.25 (+ add)
+template <typename T>
+__global__ void k_avgpool2(const T* __restrict__ x, int N, int H, int W, int C, int ldx, const T* __restrict__ add,
+                           T* __restrict__ y) {
+  const int Ho = H >> 1, Wo = W >> 1;
+  const long long total = (long long)N * Ho * Wo * C;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(i % C);
+    long long p = i / C;
+    const int wo = (int)(p % Wo);
+    p /= Wo;
+    const int ho = (int)(p % Ho);
+    const int n = (int)(p / Ho);
+    const long long b = ((long long)n * H + 2 * ho) * W + 2 * wo;
+    const float s = (to_f<T>(x[b * ldx + c]) + to_f<T>(x[(b + 1) * ldx + c])) +
+                    (to_f<T>(x[(b + W) * ldx + c]) + to_f<T>(x[(b + W + 1) * ldx + c]));
+    float v = s * 0.25f;
+    if (add) v += to_f<T>(add[i]);
+    y[i] = from_f<T>(v);
+  }
+}
+template <typename T>
+__global__ void k_avgpool2_bwd(const T* __restrict__ dy, int N, int H, int W, int C, const T* __restrict__ add,
+                               T* __restrict__ dx, int lddx) {
+  const long long total = (long long)N * H * W * C;
+  const int Ho = H >> 1, Wo = W >> 1;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(i % C);
+    long long p = i / C;
+    const int w = (int)(p % W);
+    p /= W;
+    const int h = (int)(p % H);
+    const int n = (int)(p / H);
+    float v = 0.25f * to_f<T>(dy[(((long long)n * Ho + (h >> 1)) * Wo + (w >> 1)) * C + c]);
+    const long long o = (((long long)n * H + h) * W + w);
+    if (add) v += to_f<T>(add[o * C + c]);
+    dx[o * lddx + c] = from_f<T>(v);
+  }
+}
+template <typename T>
+__global__ void k_up2_bwd(const T* __restrict__ dy, int N, int H, int W, int C, T* __restrict__ dx) {
+  const long long total = (long long)N * H * W * C;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(i % C);
+    long long p = i / C;
+    const int w = (int)(p % W);
+    p /= W;
+    const int h = (int)(p % H);
+    const int n = (int)(p / H);
+    const long long W2 = 2 * W;
+    const long long b = ((long long)n * 2 * H + 2 * h) * W2 + 2 * w;
+    const float s = (to_f<T>(dy[b * C + c]) + to_f<T>(dy[(b + 1) * C + c])) +
+                    (to_f<T>(dy[(b + W2) * C + c]) + to_f<T>(dy[(b + W2 + 1) * C + c]));
+    dx[i] = from_f<T>(s);
+  }
+}
+// column sums with 8-channel vectors when C % 8 == 0, scalar otherwise
+template <typename T>
+__global__ void __launch_bounds__(256) k_col_sum(const T* __restrict__ x, long long M, int C,
+                                                 double* __restrict__ partial, long long pix_per_blk) {
+  extern __shared__ double sh[];  // [256]
+  const long long p0 = (long long)blockIdx.x * pix_per_blk;
+  const long long p1 = min(M, p0 + pix_per_blk);
+  for (int c0 = 0; c0 < C; c0 += 32) {
+    // 8 rows of 32 channels
+    const int c = c0 + (threadIdx.x & 31);
+    const int r = threadIdx.x >> 5;
+    float s = 0.0f;
+    if (c < C)
+      for (long long p = p0 + r; p < p1; p += 8) s += to_f<T>(x[p * C + c]);
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    if (threadIdx.x < 32 && c < C) {
+      double a = 0.0;
+      for (int k = 0; k < 8; ++k) a += sh[k * 32 + threadIdx.x];
+      partial[(long long)blockIdx.x * C + c] = a;
+    }
+    __syncthreads();
+  }
+}
+__global__ void k_reduce_partials_f32(const double* __restrict__ partial, int nblk, int width, float* __restrict__ out,
+                                      int accumulate) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < width; c += gridDim.x * blockDim.x) {
+    double a = accumulate ? (double)out[c] : 0.0;
+    for (int b = 0; b < nblk; ++b) a += partial[(long long)b * width + c];
+    out[c] = (float)a;
+  }
+}
+
+// ===================================================================== G output / tanh
+template <typename T>
+__global__ void k_tanh_to_image(const float* __restrict__ pre, float* __restrict__ img, T* __restrict__ dst,
+                                long long M, int cp) {
+  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < M; p += (long long)gridDim.x * blockDim.x) {
+    for (int k = 0; k < cp; ++k) {
+      float v = 0.0f;
+      if (k < 3) {
+        v = tanhf(pre[p * 3 + k]);
+        img[p * 3 + k] = v;
+      }
+      dst[p * cp + k] = from_f<T>(v);
+    }
+  }
+}
+template <typename T>
+__global__ void k_tanh_bwd(const T* __restrict__ dimg, int cp, const float* __restrict__ img, float* __restrict__ dpre,
+                           long long M) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < M * 3;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long p = i / 3;
+    const int k = (int)(i % 3);
+    const float y = img[i];
+    dpre[i] = to_f<T>(dimg[p * cp + k]) * (1.0f - y * y);
+  }
+}
+
+// ===================================================================== SIMT conv
+// y tile: TM pixels x TN output channels; K = taps x Cin in chunks of 8 channels
+template <typename TI, typename TW, typename TO, int TM, int TN, int RM, int RN>
+__global__ void __launch_bounds__(256) k_simt_conv(const TI* __restrict__ x, int N, int H, int W, int Cin,
+                                                   const TW* __restrict__ w, int Cout, int ksz,
+                                                   const float* __restrict__ bias, const float* __restrict__ alpha,
+                                                   const TO* __restrict__ res, int res_mode, TO* __restrict__ y) {
+  constexpr int KC = 8;
+  __shared__ float As[KC][TM + 1];
+  __shared__ float Bs[KC][TN + 1];
+  const long long M = (long long)N * H * W;
+  const long long m0 = (long long)blockIdx.x * TM;
+  const int n0 = blockIdx.y * TN;
+  const int tid = threadIdx.x;
+  constexpr int TX = TN / RN;   // threads along N
+  const int tx = tid % TX, ty = tid / TX;
+  const int taps = ksz * ksz, pad = ksz >> 1;
+  float acc[RM][RN] = {};
+  for (int tap = 0; tap < taps; ++tap) {
+    const int dy = tap / ksz - pad, dx = tap % ksz - pad;
+    for (int c0 = 0; c0 < Cin; c0 += KC) {
+      for (int i = tid; i < TM * KC; i += 256) {
+        const int mm = i / KC, kk = i % KC;
+        const long long m = m0 + mm;
+        float v = 0.0f;
+        const int c = c0 + kk;
+        if (m < M && c < Cin) {
+          const int n = (int)(m / ((long long)H * W));
+          const int r = (int)(m - (long long)n * H * W);
+          const int h = r / W + dy, ww = r % W + dx;
+          if (h >= 0 && h < H && ww >= 0 && ww < W) v = to_f<TI>(x[(((long long)n * H + h) * W + ww) * Cin + c]);
+        }
+        As[kk][mm] = v;
+      }
+      for (int i = tid; i < TN * KC; i += 256) {
+        const int nn = i / KC, kk = i % KC;
+        const int o = n0 + nn, c = c0 + kk;
+        Bs[kk][nn] = (o < Cout && c < Cin) ? to_f<TW>(w[((long long)o * taps + tap) * Cin + c]) : 0.0f;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int kk = 0; kk < KC; ++kk) {
+        float a[RM], b[RN];
+#pragma unroll
+        for (int i = 0; i < RM; ++i) a[i] = As[kk][ty * RM + i];
+#pragma unroll
+        for (int j = 0; j < RN; ++j) b[j] = Bs[kk][tx * RN + j];
+#pragma unroll
+        for (int i = 0; i < RM; ++i)
+#pragma unroll
+          for (int j = 0; j < RN; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+      }
+      __syncthreads();
+    }
+  }
+  const float al = alpha ? *alpha : 1.0f;
+#pragma unroll
+  for (int i = 0; i < RM; ++i) {
+    const long long m = m0 + ty * RM + i;
+    if (m >= M) continue;
+    long long rb = m * Cout;
+    if (res && res_mode == 2) {
+      const int n = (int)(m / ((long long)H * W));
+      const int r = (int)(m - (long long)n * H * W);
+      const int h = r / W, ww = r % W;
+      rb = (((long long)n * (H >> 1) + (h >> 1)) * (W >> 1) + (ww >> 1)) * Cout;
+    }
+#pragma unroll
+    for (int j = 0; j < RN; ++j) {
+      const int o = n0 + tx * RN + j;
+      if (o >= Cout) continue;
+      float v = acc[i][j] * al;
+      if (bias) v += bias[o];
+      if (res) v += to_f<TO>(res[rb + o]);
+      y[m * Cout + o] = from_f<TO>(v);
+    }
+  }
+}
+
+// wgrad: block tile T_O x T_C over (o, c) for one tap; pixel range split over blockIdx.z;
+// 256 threads = (T_O/RO) x (T_C/RC), each RO x RC outputs
+template <typename TI, typename TG, int T_O, int T_C, int RO, int RC>
+__global__ void __launch_bounds__(256) k_simt_wgrad(const TI* __restrict__ x, const TG* __restrict__ dy, int N, int H,
+                                                    int W, int Cin, int Cout, int ksz, float* __restrict__ dw,
+                                                    long long pix_per_split) {
+  constexpr int KP = 16;
+  constexpr int TXC = T_C / RC;   // threads along c
+  __shared__ float As[KP][T_O + 1];
+  __shared__ float Bs[KP][T_C + 1];
+  const int taps = ksz * ksz, pad = ksz >> 1;
+  const int cblocks = (Cin + T_C - 1) / T_C;
+  const int tap = blockIdx.y / cblocks, cb = blockIdx.y % cblocks;
+  const int o0 = blockIdx.x * T_O, c0 = cb * T_C;
+  const int dyy = tap / ksz - pad, dxx = tap % ksz - pad;
+  const long long M = (long long)N * H * W;
+  const long long p0 = (long long)blockIdx.z * pix_per_split, p1 = min(M, p0 + pix_per_split);
+  const int tid = threadIdx.x, tx = tid % TXC, ty = tid / TXC;
+  float acc[RO][RC] = {};
+  for (long long pb = p0; pb < p1; pb += KP) {
+    for (int i = tid; i < KP * T_O; i += 256) {
+      const int kk = i / T_O, oo = i % T_O;
+      const long long p = pb + kk;
+      const int o = o0 + oo;
+      As[kk][oo] = (p < p1 && o < Cout) ? to_f<TG>(dy[p * Cout + o]) : 0.0f;
+    }
+    for (int i = tid; i < KP * T_C; i += 256) {
+      const int kk = i / T_C, cc = i % T_C;
+      const long long p = pb + kk;
+      const int c = c0 + cc;
+      float v = 0.0f;
+      if (p < p1 && c < Cin) {
+        const int n = (int)(p / ((long long)H * W));
+        const int r = (int)(p - (long long)n * H * W);
+        const int h = r / W + dyy, ww = r % W + dxx;
+        if (h >= 0 && h < H && ww >= 0 && ww < W) v = to_f<TI>(x[(((long long)n * H + h) * W + ww) * Cin + c]);
+      }
+      Bs[kk][cc] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < KP; ++kk) {
+      float a[RO], b[RC];
+#pragma unroll
+      for (int i = 0; i < RO; ++i) a[i] = As[kk][ty * RO + i];
+#pragma unroll
+      for (int j = 0; j < RC; ++j) b[j] = Bs[kk][tx * RC + j];
+#pragma unroll
+      for (int i = 0; i < RO; ++i)
+#pragma unroll
+        for (int j = 0; j < RC; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < RO; ++i) {
+    const int o = o0 + ty * RO + i;
+    if (o >= Cout) continue;
+#pragma unroll
+    for (int j = 0; j < RC; ++j) {
+      const int c = c0 + tx * RC + j;
+      if (c >= Cin) continue;
+      atomicAdd(&dw[((long long)o * taps + tap) * Cin + c], acc[i][j]);
+    }
+  }
+}
+
+// ===================================================================== D head / hinge
+template <typename T>
+__global__ void k_d_head_fwd(const T* __restrict__ h, int HW, int C, const float* __restrict__ w_lin,
+                             const float* __restrict__ b_lin, const float* __restrict__ embed,
+                             const int32_t* __restrict__ y, float* __restrict__ feat, float* __restrict__ logits) {
+  const int n = blockIdx.x;
+  __shared__ double red[32];
+  double part = 0.0;
+  const float* e = embed + (long long)y[n] * C;
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    float s = 0.0f;
+    for (int q = 0; q < HW; ++q) {
+      const float v = to_f<T>(h[((long long)n * HW + q) * C + c]);
+      s += v > 0.0f ? v : 0.0f;
+    }
+    feat[(long long)n * C + c] = s;
+    part += (double)s * ((double)w_lin[c] + (double)e[c]);
+  }
+  part = warp_sum_d(part);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) a += red[i];
+    logits[n] = (float)(a + (double)b_lin[0]);
+  }
+}
+__global__ void k_hinge(const float* __restrict__ logits, int B, int mode, float* __restrict__ dl,
+                        float* __restrict__ out) {
+  // single block
+  __shared__ double s_loss, s_real, s_fake;
+  __shared__ int s_bad;
+  if (threadIdx.x == 0) { s_loss = 0; s_real = 0; s_fake = 0; s_bad = 0; }
+  __syncthreads();
+  const int total = mode == 0 ? 2 * B : B;
+  for (int i = threadIdx.x; i < total; i += blockDim.x) {
+    const float l = logits[i];
+    if (!isfinite(l)) atomicOr(&s_bad, 1);
+    double lo;
+    float d;
+    if (mode == 0) {
+      if (i < B) {  // fake: relu(1 + l)
+        lo = 1.0 + l > 0 ? 1.0 + l : 0.0;
+        d = (1.0f + l > 0.0f) ? 1.0f / B : 0.0f;
+        atomicAdd(&s_fake, (double)l);
+      } else {      // real: relu(1 - l)
+        lo = 1.0 - l > 0 ? 1.0 - l : 0.0;
+        d = (1.0f - l > 0.0f) ? -1.0f / B : 0.0f;
+        atomicAdd(&s_real, (double)l);
+      }
+    } else {
+      lo = -(double)l;
+      d = -1.0f / B;
+      atomicAdd(&s_fake, (double)l);
+    }
+    dl[i] = d;
+    atomicAdd(&s_loss, lo);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    out[0] = (float)(s_loss / B);
+    out[1] = (float)(s_real / B);
+    out[2] = (float)(s_fake / B);
+    out[3] = s_bad ? 1.0f : 0.0f;
+  }
+}
+template <typename T>
+__global__ void k_d_head_bwd_dh(const T* __restrict__ h, int N, int HW, int C, const float* __restrict__ w_lin,
+                                const float* __restrict__ embed, const int32_t* __restrict__ y,
+                                const float* __restrict__ dl, T* __restrict__ dh) {
+  const long long total = (long long)N * HW * C;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(i % C);
+    const int n = (int)(i / ((long long)HW * C));
+    const float df = dl[n] * (w_lin[c] + embed[(long long)y[n] * C + c]);
+    dh[i] = from_f<T>(to_f<T>(h[i]) > 0.0f ? df : 0.0f);
+  }
+}
+__global__ void k_d_head_bwd_w(int N, int C, const float* __restrict__ feat, const float* __restrict__ dl,
+                               const int32_t* __restrict__ y, float* __restrict__ dw_lin, float* __restrict__ db_lin,
+                               float* __restrict__ dembed) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < C) {
+    double a = 0.0;
+    for (int n = 0; n < N; ++n) {
+      const float g = dl[n] * feat[(long long)n * C + c];
+      a += g;
+      dembed[(long long)y[n] * C + c] += g;  // sequential over n: deterministic
+    }
+    dw_lin[c] = (float)a;
+  }
+  if (c == 0) {
+    double s = 0.0;
+    for (int n = 0; n < N; ++n) s += dl[n];
+    db_lin[0] = (float)s;
+  }
+}
+
+// ===================================================================== attention helpers
+template <typename T>
+__global__ void k_maxpool2_split(const T* __restrict__ x, int N, int H, int W, int ldx, int c_off, int C,
+                                 T* __restrict__ pooled, T* __restrict__ pooledT) {
+  const int Ho = H >> 1, Wo = W >> 1, Q = Ho * Wo;
+  const long long total = (long long)N * Q * C;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(i % C);
+    const long long pq = i / C;
+    const int q = (int)(pq % Q);
+    const int n = (int)(pq / Q);
+    const int ho = q / Wo, wo = q % Wo;
+    const long long b = ((long long)n * H + 2 * ho) * W + 2 * wo;
+    const float a0 = to_f<T>(x[b * ldx + c_off + c]), a1 = to_f<T>(x[(b + 1) * ldx + c_off + c]);
+    const float a2 = to_f<T>(x[(b + W) * ldx + c_off + c]), a3 = to_f<T>(x[(b + W + 1) * ldx + c_off + c]);
+    const float m = fmaxf(fmaxf(a0, a1), fmaxf(a2, a3));
+    pooled[i] = from_f<T>(m);
+    if (pooledT) pooledT[((long long)n * C + c) * Q + q] = from_f<T>(m);
+  }
+}
+template <typename T>
+__global__ void k_maxpool2_split_bwd(const T* __restrict__ x, int N, int H, int W, int ldx, int c_off, int C,
+                                     const float* __restrict__ dp, T* __restrict__ dx) {
+  const int Ho = H >> 1, Wo = W >> 1, Q = Ho * Wo;
+  const long long total = (long long)N * Q * C;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(i % C);
+    const long long pq = i / C;
+    const int q = (int)(pq % Q);
+    const int n = (int)(pq / Q);
+    const int ho = q / Wo, wo = q % Wo;
+    const long long b = ((long long)n * H + 2 * ho) * W + 2 * wo;
+    const long long idx[4] = {b, b + 1, b + W, b + W + 1};
+    // first maximum in row-major scan wins (R7)
+    int arg = 0;
+    float best = to_f<T>(x[idx[0] * ldx + c_off + c]);
+    for (int k = 1; k < 4; ++k) {
+      const float v = to_f<T>(x[idx[k] * ldx + c_off + c]);
+      if (v > best) { best = v; arg = k; }
+    }
+    const float g = dp[i];
+    for (int k = 0; k < 4; ++k) dx[idx[k] * ldx + c_off + c] = from_f<T>(k == arg ? g : 0.0f);
+  }
+}
+// one warp per row
+template <typename T>
+__global__ void k_softmax_rows(const float* __restrict__ S, long long rows, int cols, T* __restrict__ P) {
+  const long long row = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const float* s = S + row * cols;
+  float mx = -INFINITY;
+  for (int j = lane; j < cols; j += 32) mx = fmaxf(mx, s[j]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  float sum = 0.0f;
+  for (int j = lane; j < cols; j += 32) sum += __expf(s[j] - mx);
+  sum = warp_sum(sum);
+  const float inv = 1.0f / sum;
+  for (int j = lane; j < cols; j += 32) P[row * cols + j] = from_f<T>(__expf(s[j] - mx) * inv);
+}
+template <typename T>
+__global__ void k_softmax_bwd_rows(const T* __restrict__ P, const float* __restrict__ dP, long long rows, int cols,
+                                   T* __restrict__ dS) {
+  const long long row = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  float dot = 0.0f;
+  for (int j = lane; j < cols; j += 32) dot += to_f<T>(P[row * cols + j]) * dP[row * cols + j];
+  dot = warp_sum(dot);
+  for (int j = lane; j < cols; j += 32) {
+    const float p = to_f<T>(P[row * cols + j]);
+    dS[row * cols + j] = from_f<T>(p * (dP[row * cols + j] - dot));
+  }
+}
+
+// ===================================================================== SN
+// pass 1: t[k] = sum_r W[r][k] u[r]   (block = 256 columns of one job)
+__global__ void __launch_bounds__(256) k_sn_wtu(const SnJob* __restrict__ jobs, const int* __restrict__ blk_job,
+                                                const int* __restrict__ blk_k0) {
+  const SnJob j = jobs[blk_job[blockIdx.x]];
+  const int k = blk_k0[blockIdx.x] + threadIdx.x;
+  if (k >= j.K) return;
+  float a = 0.0f;
+  for (int r = 0; r < j.rows; ++r) a = fmaf(j.w[(long long)r * j.K + k], j.u[r], a);
+  j.t[k] = a;
+}
+// pass 2: s[r] = sum_k W[r][k] t[k] / ||t||   (block = 8 rows, one warp per row)
+__global__ void __launch_bounds__(256) k_sn_wv(const SnJob* __restrict__ jobs, const int* __restrict__ blk_job,
+                                               const int* __restrict__ blk_r0) {
+  const SnJob j = jobs[blk_job[blockIdx.x]];
+  __shared__ float red[8];
+  __shared__ float s_inv;
+  // ||t|| (every block recomputes it: K <= 14k floats from L2)
+  float q = 0.0f;
+  for (int k = threadIdx.x; k < j.K; k += 256) q = fmaf(j.t[k], j.t[k], q);
+  q = warp_sum(q);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = q;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float a = 0.0f;
+    for (int i = 0; i < 8; ++i) a += red[i];
+    s_inv = 1.0f / fmaxf(sqrtf(a), 1e-12f);
+  }
+  __syncthreads();
+  const float inv = s_inv;
+  const int r = blk_r0[blockIdx.x] + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (blk_r0[blockIdx.x] == 0) {  // one block per job writes v
+    for (int k = threadIdx.x; k < j.K; k += 256) j.v[k] = j.t[k] * inv;
+  }
+  if (r >= j.rows) return;
+  float a = 0.0f;
+  for (int k = lane; k < j.K; k += 32) a = fmaf(j.w[(long long)r * j.K + k], j.t[k], a);
+  a = warp_sum(a);
+  if (lane == 0) j.s[r] = a * inv;
+}
+// pass 3: sigma = ||s||, u = s / ||s||   (one block per job)
+__global__ void k_sn_finish(const SnJob* __restrict__ jobs) {
+  const SnJob j = jobs[blockIdx.x];
+  __shared__ float red[8];
+  __shared__ float s_n;
+  float q = 0.0f;
+  for (int r = threadIdx.x; r < j.rows; r += 256) q = fmaf(j.s[r], j.s[r], q);
+  q = warp_sum(q);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = q;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float a = 0.0f;
+    for (int i = 0; i < 8; ++i) a += red[i];
+    s_n = sqrtf(a);
+    j.sigma[0] = s_n;   // sigma = u'^T W v = ||W v||
+    j.sigma[1] = 1.0f / s_n;
+  }
+  __syncthreads();
+  const float inv = 1.0f / fmaxf(s_n, 1e-12f);
+  for (int r = threadIdx.x; r < j.rows; r += 256) j.u[r] = j.s[r] * inv;
+}
+__global__ void __launch_bounds__(256) k_sn_pack(const SnPack* __restrict__ jobs, const long long* __restrict__ blk_start,
+                                                 int n_jobs) {
+  // find job by binary search over block starts
+  int lo = 0, hi = n_jobs - 1;
+  const long long b = blockIdx.x;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (blk_start[mid] <= b) lo = mid; else hi = mid - 1;
+  }
+  const SnPack J = jobs[lo];
+  const long long n = (long long)J.rows * J.taps * J.cin;
+  const long long i = (b - blk_start[lo]) * 256 + threadIdx.x;
+  if (i >= n) return;
+  const float v = J.w[i] * J.sigma[1];
+  const int c = (int)(i % J.cin);
+  const long long rt = i / J.cin;
+  const int t = (int)(rt % J.taps);
+  const int o = (int)(rt / J.taps);
+  long long d;
+  if (J.mode == 1) {  // dgrad layout [cin][taps-1-t][rows]
+    d = ((long long)c * J.taps + (J.taps - 1 - t)) * J.dst_rows + (o + J.dst_row_offset);
+  } else {
+    d = ((long long)(o + J.dst_row_offset) * J.taps + t) * J.dst_cin + c;
+  }
+  if (J.dst_bf16) reinterpret_cast<bf16*>(J.dst)[d] = __float2bfloat16_rn(v);
+  else reinterpret_cast<float*>(J.dst)[d] = v;
+}
+// SN backward: one block per weight (pass a: <g, W>; pass b: g = (g - <g,W>/sigma u v^T)/sigma)
+__global__ void __launch_bounds__(1024) k_sn_bwd(const SnJob* __restrict__ jobs, const int* __restrict__ idx,
+                                                 float* const* __restrict__ grads) {
+  const SnJob j = jobs[idx[blockIdx.x]];
+  float* g = grads[blockIdx.x];
+  const long long n = (long long)j.rows * j.K;
+  __shared__ double red[32];
+  __shared__ float s_c;
+  double a = 0.0;
+  for (long long i = threadIdx.x; i < n; i += blockDim.x) a += (double)g[i] * (double)j.w[i];
+  a = warp_sum_d(a);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
+    // <G, W_hat> = <G, W>/sigma ; coefficient of u v^T in dW is <G, W_hat>/sigma
+    s_c = (float)(t * (double)j.sigma[1] * (double)j.sigma[1]);
+  }
+  __syncthreads();
+  const float c = s_c, inv = j.sigma[1];
+  for (long long i = threadIdx.x; i < n; i += blockDim.x) {
+    const int r = (int)(i / j.K), k = (int)(i % j.K);
+    g[i] = g[i] * inv - c * j.u[r] * j.v[k];
+  }
+}
+
+// ===================================================================== Adam / finite / init
+__global__ void k_check_finite(const float* __restrict__ g, long long n, int* flag) {
+  int bad = 0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    bad |= !isfinite(g[i]);
+  bad = __syncthreads_or(bad);
+  if (bad && threadIdx.x == 0) atomicOr(flag, 1);
+}
+__global__ void k_check_finite_scalar(const float* loss, int* flag) {
+  if (!isfinite(loss[0]) || loss[3] != 0.0f) atomicOr(flag, 1);
+}
+__global__ void k_adam(float* __restrict__ w, const float* __restrict__ g, float* __restrict__ m, float* __restrict__ v,
+                       long long n, float lr, float b1, float b2, float eps, const long long* __restrict__ t_dev,
+                       float gscale, const int* __restrict__ flag) {
+  if (*flag) return;
+  const double t = (double)(*t_dev + 1);
+  const float bc1 = (float)(1.0 - pow((double)b1, t)), bc2 = (float)(1.0 - pow((double)b2, t));
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const float gi = g[i] * gscale;
+    const float mi = b1 * m[i] + (1.0f - b1) * gi;
+    const float vi = b2 * v[i] + (1.0f - b2) * gi * gi;
+    m[i] = mi;
+    v[i] = vi;
+    w[i] -= lr * (mi / bc1) / (sqrtf(vi / bc2) + eps);
+  }
+}
+__global__ void k_adam_bookkeep(long long* t_dev, const int* flag, int* sticky) {
+  if (*flag) *sticky = 1;
+  else *t_dev += 1;
+}
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__global__ void k_fill_normal(float* p, long long n, float std, uint64_t seed, uint64_t off) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const uint64_t h = mix64(seed ^ mix64(off + (uint64_t)i));
+    const double u1 = ((h >> 11) + 1.0) * (1.0 / 9007199254740993.0);
+    const double u2 = (mix64(h) >> 11) * (1.0 / 9007199254740992.0);
+    p[i] = (float)(std * sqrt(-2.0 * log(u1)) * cos(6.283185307179586 * u2));
+  }
+}
+__global__ void k_fill_const(float* p, long long n, float v) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+__global__ void k_normalize(float* p, int n) {
+  __shared__ double red[32];
+  double a = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) a += (double)p[i] * p[i];
+  a = warp_sum_d(a);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
+    red[0] = t;
+  }
+  __syncthreads();
+  const float inv = (float)(1.0 / sqrt(red[0]));
+  for (int i = threadIdx.x; i < n; i += blockDim.x) p[i] *= inv;
+}
+__global__ void k_oihw_ohwi(const float* __restrict__ s, float* __restrict__ d, int O, int I, int taps, int to_ohwi) {
+  const long long n = (long long)O * I * taps;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    // i indexes OIHW: o, c, t
+    const int t = (int)(i % taps);
+    const long long oc = i / taps;
+    const int c = (int)(oc % I);
+    const int o = (int)(oc / I);
+    const long long j = ((long long)o * taps + t) * I + c;   // OHWI
+    if (to_ohwi) d[j] = s[i];
+    else d[i] = s[j];
+  }
+}
+__global__ void k_scale_dev(float* p, long long n, const float* s) {
+  const float f = *s;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    p[i] *= f;
+}
+__global__ void k_dot(const float* __restrict__ a, const float* __restrict__ b, long long n, float* out, int acc) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (long long i = threadIdx.x; i < n; i += blockDim.x) s += (double)a[i] * (double)b[i];
+  s = warp_sum_d(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
+    out[0] = (float)(acc ? (double)out[0] + t : t);
+  }
+}
+__global__ void k_copy_rows_cols(const float* __restrict__ src, long long lds, long long rows, int cols,
+                                 float* __restrict__ dst, long long ldd, int acc) {
+  const long long total = rows * cols;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / cols;
+    const int j = (int)(i % cols);
+    const float v = src[r * lds + j];
+    dst[r * ldd + j] = acc ? dst[r * ldd + j] + v : v;
+  }
+}
+__global__ void k_scale(float* p, long long n, float s) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    p[i] *= s;
+}
+
+}  // namespace
+
+// ============================================================================ launchers
+template <typename TD>
+cudaError_t layout_pack(const float* src, TD* dst, int n, int c, int h, int w, int c_pad, long long off,
+                        cudaStream_t st) {
+  const long long total = (long long)n * h * w * c_pad;
+  k_pack<TD><<<grid_for(total, 256), 256, 0, st>>>(src, dst + off, n, c, h, w, c_pad);
+  return cudaGetLastError();
+}
+template <typename TS>
+cudaError_t layout_unpack(const TS* src, float* dst, int n, int c, int h, int w, int c_pad, cudaStream_t st) {
+  const long long total = (long long)n * h * w * c;
+  k_unpack<TS><<<grid_for(total, 256), 256, 0, st>>>(src, dst, n, c, h, w, c_pad);
+  return cudaGetLastError();
+}
+template cudaError_t layout_pack<float>(const float*, float*, int, int, int, int, int, long long, cudaStream_t);
+template cudaError_t layout_pack<bf16>(const float*, bf16*, int, int, int, int, int, long long, cudaStream_t);
+template cudaError_t layout_unpack<float>(const float*, float*, int, int, int, int, int, cudaStream_t);
+template cudaError_t layout_unpack<bf16>(const bf16*, float*, int, int, int, int, int, cudaStream_t);
+
+cudaError_t gemm_f32(int M, int N, int K, const float* A, long long sam, long long sak, const float* B, long long sbn,
+                     long long sbk, float* C, long long ldc, float beta, const float* bias, cudaStream_t st) {
+  if (M <= 0 || N <= 0) return cudaSuccess;
+  dim3 g(ceil_div(N, 64), ceil_div(M, 64), 1);
+  k_gemm<float><<<g, 256, 0, st>>>(M, N, K, A, 0, sam, sak, B, 0, sbn, sbk, C, 0, ldc, beta, bias);
+  return cudaGetLastError();
+}
+cudaError_t gemm_f32_batched(int batch, int M, int N, int K, const float* A, long long sab, long long sam,
+                             long long sak, const float* B, long long sbb, long long sbn, long long sbk, float* C,
+                             long long scb, long long ldc, float beta, cudaStream_t st) {
+  dim3 g(ceil_div(N, 64), ceil_div(M, 64), batch);
+  k_gemm<float><<<g, 256, 0, st>>>(M, N, K, A, sab, sam, sak, B, sbb, sbn, sbk, C, scb, ldc, beta, nullptr);
+  return cudaGetLastError();
+}
+
+template <typename TD>
+cudaError_t convert_f32(const float* s, TD* d, long long n, cudaStream_t st) {
+  k_convert<TD><<<grid_for(n, 256), 256, 0, st>>>(s, d, n);
+  return cudaGetLastError();
+}
+template cudaError_t convert_f32<float>(const float*, float*, long long, cudaStream_t);
+template cudaError_t convert_f32<bf16>(const float*, bf16*, long long, cudaStream_t);
+template <typename TS>
+cudaError_t to_f32(const TS* s, float* d, long long n, cudaStream_t st) {
+  k_to_f32<TS><<<grid_for(n, 256), 256, 0, st>>>(s, d, n);
+  return cudaGetLastError();
+}
+template cudaError_t to_f32<float>(const float*, float*, long long, cudaStream_t);
+template cudaError_t to_f32<bf16>(const bf16*, float*, long long, cudaStream_t);
+
+cudaError_t gather_rows(const float* table, const int32_t* idx, int n, int dim, float* out, int ldo, cudaStream_t st) {
+  k_gather_rows<<<grid_for((long long)n * dim, 256), 256, 0, st>>>(table, idx, n, dim, out, ldo);
+  return cudaGetLastError();
+}
+cudaError_t copy_cols(const float* src, int lds, int n, int cols, float* dst, int ldd, cudaStream_t st) {
+  k_copy_cols<<<grid_for((long long)n * cols, 256), 256, 0, st>>>(src, lds, n, cols, dst, ldd);
+  return cudaGetLastError();
+}
+cudaError_t scatter_add_rows(const float* src, int lds, const int32_t* idx, int n, int dim, float* dtable,
+                             cudaStream_t st) {
+  k_scatter_add_rows<<<ceil_div(dim, 128), 128, 0, st>>>(src, lds, idx, n, dim, dtable);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t bn_stats(const T* x, long long M, int C, double* partial, int max_blocks, double* sums, cudaStream_t st) {
+  if (C % 8 || C / 8 > 256) return cudaErrorInvalidValue;
+  int nblk = (int)((M + 511) / 512);
+  if (nblk > max_blocks) nblk = max_blocks;
+  const long long per = (M + nblk - 1) / nblk;
+  const int R = 256 / (C / 8);
+  const size_t sm = (size_t)R * 2 * C * sizeof(double);
+  if (sm > 48 * 1024) PG_CUDA(cudaFuncSetAttribute(k_bn_stats<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  k_bn_stats<T><<<nblk, 256, sm, st>>>(x, M, C, partial, per);
+  PG_LAUNCH_CHECK();
+  k_reduce_partials<<<ceil_div(2 * C, 256), 256, 0, st>>>(partial, nblk, 2 * C, sums);
+  return cudaGetLastError();
+}
+template cudaError_t bn_stats<float>(const float*, long long, int, double*, int, double*, cudaStream_t);
+template cudaError_t bn_stats<bf16>(const bf16*, long long, int, double*, int, double*, cudaStream_t);
+
+cudaError_t bn_finalize(const double* sums, int C, double count, float eps, float* mean, float* rstd, cudaStream_t st) {
+  k_bn_finalize<<<ceil_div(C, 256), 256, 0, st>>>(sums, C, count, eps, mean, rstd);
+  return cudaGetLastError();
+}
+
+template <typename TI, typename TO>
+cudaError_t bn_apply_relu(const TI* x, int N, int H, int W, int C, const float* mean, const float* rstd,
+                          const float* gain, const float* bias, const float* gamma, const float* beta, TO* y, bool up2,
+                          cudaStream_t st) {
+  const long long total = (long long)N * H * W * (C / 8);
+  k_bn_apply_relu<TI, TO><<<grid_for(total, 256), 256, 0, st>>>(x, N, H, W, C, mean, rstd,
+                                                                BnAffine{gain, bias, gamma, beta}, y, up2 ? 1 : 0);
+  return cudaGetLastError();
+}
+template cudaError_t bn_apply_relu<float, float>(const float*, int, int, int, int, const float*, const float*,
+                                                 const float*, const float*, const float*, const float*, float*, bool,
+                                                 cudaStream_t);
+template cudaError_t bn_apply_relu<bf16, bf16>(const bf16*, int, int, int, int, const float*, const float*,
+                                               const float*, const float*, const float*, const float*, bf16*, bool,
+                                               cudaStream_t);
+template cudaError_t bn_apply_relu<bf16, float>(const bf16*, int, int, int, int, const float*, const float*,
+                                                const float*, const float*, const float*, const float*, float*, bool,
+                                                cudaStream_t);
+
+template <typename TI, typename TG>
+cudaError_t bn_bwd_reduce(const TI* x, const TG* dy, int N, int H, int W, int C, const float* mean, const float* rstd,
+                          const float* gain, const float* bias, const float* gamma, const float* beta, bool up2,
+                          float* partial, int chunks, float* AB, cudaStream_t st) {
+  if (C % 8 || C / 8 > 256) return cudaErrorInvalidValue;
+  const int R = 256 / (C / 8);
+  const size_t sm = (size_t)R * 2 * C * sizeof(float);
+  if (sm > 48 * 1024)
+    PG_CUDA(cudaFuncSetAttribute(k_bn_bwd_reduce<TI, TG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  dim3 g(chunks, N);
+  k_bn_bwd_reduce<TI, TG><<<g, 256, sm, st>>>(x, dy, N, H, W, C, mean, rstd, BnAffine{gain, bias, gamma, beta},
+                                              up2 ? 1 : 0, partial, chunks);
+  PG_LAUNCH_CHECK();
+  k_bn_bwd_fold<<<grid_for((long long)N * 2 * C, 256), 256, 0, st>>>(partial, N, chunks, C, AB);
+  return cudaGetLastError();
+}
+template cudaError_t bn_bwd_reduce<float, float>(const float*, const float*, int, int, int, int, const float*,
+                                                 const float*, const float*, const float*, const float*, const float*,
+                                                 bool, float*, int, float*, cudaStream_t);
+template cudaError_t bn_bwd_reduce<bf16, bf16>(const bf16*, const bf16*, int, int, int, int, const float*, const float*,
+                                               const float*, const float*, const float*, const float*, bool, float*, int,
+                                               float*, cudaStream_t);
+template cudaError_t bn_bwd_reduce<bf16, float>(const bf16*, const float*, int, int, int, int, const float*,
+                                                const float*, const float*, const float*, const float*, const float*,
+                                                bool, float*, int, float*, cudaStream_t);
+
+cudaError_t bn_bwd_totals(const float* AB, int N, int C, const float* gain, const float* gamma, double* tot,
+                          cudaStream_t st) {
+  k_bn_bwd_totals<<<ceil_div(C, 128), 128, 0, st>>>(AB, N, C, gain, gamma, tot);
+  return cudaGetLastError();
+}
+
+template <typename TI, typename TG, typename TO>
+cudaError_t bn_bwd_apply(const TI* x, const TG* dy, int N, int H, int W, int C, const float* mean, const float* rstd,
+                         const float* gain, const float* bias, const float* gamma, const float* beta, bool up2,
+                         const double* tot, double count, const TO* add, TO* dx, cudaStream_t st) {
+  const long long total = (long long)N * H * W * (C / 8);
+  k_bn_bwd_apply<TI, TG, TO><<<grid_for(total, 256), 256, 0, st>>>(
+      x, dy, N, H, W, C, mean, rstd, BnAffine{gain, bias, gamma, beta}, up2 ? 1 : 0, tot, count, add, dx);
+  return cudaGetLastError();
+}
+template cudaError_t bn_bwd_apply<float, float, float>(const float*, const float*, int, int, int, int, const float*,
+                                                       const float*, const float*, const float*, const float*,
+                                                       const float*, bool, const double*, double, const float*, float*,
+                                                       cudaStream_t);
+template cudaError_t bn_bwd_apply<bf16, bf16, bf16>(const bf16*, const bf16*, int, int, int, int, const float*,
+                                                    const float*, const float*, const float*, const float*,
+                                                    const float*, bool, const double*, double, const bf16*, bf16*,
+                                                    cudaStream_t);
+template cudaError_t bn_bwd_apply<bf16, float, bf16>(const bf16*, const float*, int, int, int, int, const float*,
+                                                     const float*, const float*, const float*, const float*,
+                                                     const float*, bool, const double*, double, const bf16*, bf16*,
+                                                     cudaStream_t);
+
+#define PG_INST_T(T)                                                                                               \
+  template cudaError_t relu_copy<T>(const T*, T*, long long, cudaStream_t);                                        \
+  template cudaError_t relu_bwd<T>(const T*, const T*, const T*, T*, long long, cudaStream_t);                     \
+  template cudaError_t avgpool2<T>(const T*, int, int, int, int, int, const T*, T*, cudaStream_t);                 \
+  template cudaError_t avgpool2_bwd<T>(const T*, int, int, int, int, const T*, T*, int, cudaStream_t);             \
+  template cudaError_t up2_bwd<T>(const T*, int, int, int, int, T*, cudaStream_t);                                 \
+  template cudaError_t col_sum<T>(const T*, long long, int, double*, int, float*, int, cudaStream_t);              \
+  template cudaError_t tanh_to_image<T>(const float*, float*, T*, long long, int, cudaStream_t);                   \
+  template cudaError_t tanh_bwd<T>(const T*, int, const float*, float*, long long, cudaStream_t);                  \
+  template cudaError_t d_head_fwd<T>(const T*, int, int, int, const float*, const float*, const float*,            \
+                                     const int32_t*, float*, float*, cudaStream_t);                                \
+  template cudaError_t d_head_bwd<T>(const T*, int, int, int, const float*, const float*, const int32_t*,          \
+                                     const float*, const float*, T*, float*, float*, float*, int, bool,            \
+                                     cudaStream_t);                                                                \
+  template cudaError_t maxpool2_split<T>(const T*, int, int, int, int, int, int, T*, T*, cudaStream_t);            \
+  template cudaError_t maxpool2_split_bwd<T>(const T*, int, int, int, int, int, int, const float*, T*,             \
+                                             cudaStream_t);                                                        \
+  template cudaError_t softmax_rows<T>(const float*, long long, int, T*, cudaStream_t);                            \
+  template cudaError_t softmax_bwd_rows<T>(const T*, const float*, long long, int, T*, cudaStream_t);
+
+template <typename T>
+cudaError_t relu_copy(const T* x, T* y, long long n, cudaStream_t st) {
+  k_relu_copy<T><<<grid_for(n, 256), 256, 0, st>>>(x, y, n);
+  return cudaGetLastError();
+}
+template <typename T>
+cudaError_t relu_bwd(const T* dy, const T* ref, const T* add, T* dx, long long n, cudaStream_t st) {
+  k_relu_bwd<T><<<grid_for(n, 256), 256, 0, st>>>(dy, ref, add, dx, n);
+  return cudaGetLastError();
+}
+template <typename T>
+cudaError_t avgpool2(const T* x, int N, int H, int W, int C, int ldx, const T* add, T* y, cudaStream_t st) {
+  const long long total = (long long)N * (H / 2) * (W / 2) * C;
+  k_avgpool2<T><<<grid_for(total, 256), 256, 0, st>>>(x, N, H, W, C, ldx, add, y);
+  return cudaGetLastError();
+}
+template <typename T>
+cudaError_t avgpool2_bwd(const T* dy, int N, int H, int W, int C, const T* add, T* dx, int lddx, cudaStream_t st) {
+  const long long total = (long long)N * H * W * C;
+  k_avgpool2_bwd<T><<<grid_for(total, 256), 256, 0, st>>>(dy, N, H, W, C, add, dx, lddx);
+  return cudaGetLastError();
+}
+template <typename T>
+cudaError_t up2_bwd(const T* dy, int N, int H, int W, int C, T* dx, cudaStream_t st) {
+  const long long total = (long long)N * H * W * C;
+  k_up2_bwd<T><<<grid_for(total, 256), 256, 0, st>>>(dy, N, H, W, C, dx);
+  return cudaGetLastError();
+}
+template <typename T>
+cudaError_t col_sum(const T* dy, long long M, int C, double* partial, int max_blocks, float* db, int accumulate,
+                    cudaStream_t st) {
+  int nblk = (int)((M + 1023) / 1024);
+  if (nblk > max_blocks) nblk = max_blocks;
+  const long long per = (M + nblk - 1) / nblk;
+  k_col_sum<T><<<nblk, 256, 256 * sizeof(double), st>>>(dy, M, C, partial, per);
+  PG_LAUNCH_CHECK();
+  k_reduce_partials_f32<<<ceil_div(C, 256), 256, 0, st>>>(partial, nblk, C, db, accumulate);
+  return cudaGetLastError();
+}
+template <typename T>
+cudaError_t tanh_to_image(const float* pre, float* img, T* dst, long long M, int c_pad, cudaStream_t st) {
+  k_tanh_to_image<T><<<grid_for(M, 256), 256, 0, st>>>(pre, img, dst, M, c_pad);
+  return cudaGetLastError();
+}
+template <typename T>
+cudaError_t tanh_bwd(const T* dimg, int c_pad, const float* img, float* dpre, long long M, cudaStream_t st) {
+  k_tanh_bwd<T><<<grid_for(M * 3, 256), 256, 0, st>>>(dimg, c_pad, img, dpre, M);
+  return cudaGetLastError();
+}
+template <typename T>
+cudaError_t d_head_fwd(const T* h, int N, int HW, int C, const float* w_lin, const float* b_lin, const float* embed,
+                       const int32_t* y, float* feat, float* logits, cudaStream_t st) {
+  k_d_head_fwd<T><<<N, 256, 0, st>>>(h, HW, C, w_lin, b_lin, embed, y, feat, logits);
+  return cudaGetLastError();
+}
+cudaError_t hinge_loss(const float* logits, int B, int mode, float* dlogits, float* loss_out, cudaStream_t st) {
+  k_hinge<<<1, 256, 0, st>>>(logits, B, mode, dlogits, loss_out);
+  return cudaGetLastError();
+}
+template <typename T>
+cudaError_t d_head_bwd(const T* h, int N, int HW, int C, const float* w_lin, const float* embed, const int32_t* y,
+                       const float* feat, const float* dlogits, T* dh, float* dw_lin, float* db_lin, float* dembed,
+                       int n_classes, bool want_wgrad, cudaStream_t st) {
+  (void)n_classes;
+  const long long total = (long long)N * HW * C;
+  k_d_head_bwd_dh<T><<<grid_for(total, 256), 256, 0, st>>>(h, N, HW, C, w_lin, embed, y, dlogits, dh);
+  PG_LAUNCH_CHECK();
+  if (want_wgrad) {
+    k_d_head_bwd_w<<<ceil_div(C, 128), 128, 0, st>>>(N, C, feat, dlogits, y, dw_lin, db_lin, dembed);
+    PG_LAUNCH_CHECK();
+  }
+  return cudaSuccess;
+}
+template <typename T>
+cudaError_t maxpool2_split(const T* x, int N, int H, int W, int ldx, int c_off, int C, T* pooled, T* pooledT,
+                           cudaStream_t st) {
+  const long long total = (long long)N * (H / 2) * (W / 2) * C;
+  k_maxpool2_split<T><<<grid_for(total, 256), 256, 0, st>>>(x, N, H, W, ldx, c_off, C, pooled, pooledT);
+  return cudaGetLastError();
+}
+template <typename T>
+cudaError_t maxpool2_split_bwd(const T* x, int N, int H, int W, int ldx, int c_off, int C, const float* dpooled, T* dx,
+                               cudaStream_t st) {
+  const long long total = (long long)N * (H / 2) * (W / 2) * C;
+  k_maxpool2_split_bwd<T><<<grid_for(total, 256), 256, 0, st>>>(x, N, H, W, ldx, c_off, C, dpooled, dx);
+  return cudaGetLastError();
+}
+template <typename T>
+cudaError_t softmax_rows(const float* S, long long rows, int cols, T* P, cudaStream_t st) {
+  k_softmax_rows<T><<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(S, rows, cols, P);
+  return cudaGetLastError();
+}
+template <typename T>
+cudaError_t softmax_bwd_rows(const T* P, const float* dP, long long rows, int cols, T* dS, cudaStream_t st) {
+  k_softmax_bwd_rows<T><<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(P, dP, rows, cols, dS);
+  return cudaGetLastError();
+}
+PG_INST_T(float)
+PG_INST_T(bf16)
+
+template <typename TI, typename TW, typename TO>
+cudaError_t simt_conv_fwd(const TI* x, int N, int H, int W, int Cin, const TW* w, int Cout, int ksz, const float* bias,
+                          const float* alpha, const TO* residual, int res_mode, TO* y, cudaStream_t st) {
+  const long long M = (long long)N * H * W;
+  if (Cout <= 8) {
+    dim3 g(ceil_div(M, 256), ceil_div(Cout, 4));
+    k_simt_conv<TI, TW, TO, 256, 4, 1, 4><<<g, 256, 0, st>>>(x, N, H, W, Cin, w, Cout, ksz, bias, alpha, residual,
+                                                             res_mode, y);
+  } else {
+    dim3 g(ceil_div(M, 64), ceil_div(Cout, 64));
+    k_simt_conv<TI, TW, TO, 64, 64, 4, 4><<<g, 256, 0, st>>>(x, N, H, W, Cin, w, Cout, ksz, bias, alpha, residual,
+                                                             res_mode, y);
+  }
+  return cudaGetLastError();
+}
+template cudaError_t simt_conv_fwd<float, float, float>(const float*, int, int, int, int, const float*, int, int,
+                                                        const float*, const float*, const float*, int, float*,
+                                                        cudaStream_t);
+
+template <typename TI, typename TG>
+cudaError_t simt_conv_wgrad(const TI* x, const TG* dy, int N, int H, int W, int Cin, int Cout, int ksz, float* dw,
+                            int accumulate, cudaStream_t st) {
+  const long long M = (long long)N * H * W;
+  const int taps = ksz * ksz;
+  if (!accumulate) PG_CUDA(cudaMemsetAsync(dw, 0, sizeof(float) * (size_t)Cout * taps * Cin, st));
+  const bool small = Cout <= 4;
+  const int TO = small ? 4 : 64, TC = small ? 256 : 64;
+  const int cblocks = ceil_div(Cin, TC);
+  const int tiles = ceil_div(Cout, TO) * taps * cblocks;
+  int splits = ceil_div(4 * kNumSMs, tiles);
+  const long long max_splits = (M + 255) / 256;
+  if (splits > max_splits) splits = (int)max_splits;
+  if (splits < 1) splits = 1;
+  const long long per = ((M + splits - 1) / splits + 15) / 16 * 16;
+  splits = (int)((M + per - 1) / per);
+  dim3 g(ceil_div(Cout, TO), taps * cblocks, splits);
+  if (small)
+    k_simt_wgrad<TI, TG, 4, 256, 1, 4><<<g, 256, 0, st>>>(x, dy, N, H, W, Cin, Cout, ksz, dw, per);
+  else
+    k_simt_wgrad<TI, TG, 64, 64, 4, 4><<<g, 256, 0, st>>>(x, dy, N, H, W, Cin, Cout, ksz, dw, per);
+  return cudaGetLastError();
+}
+template cudaError_t simt_conv_wgrad<float, float>(const float*, const float*, int, int, int, int, int, int, float*,
+                                                   int, cudaStream_t);
+
+cudaError_t sn_power(const SnJob* jobs, int n_jobs, const int* blk_job, const int* blk_k0, int n_blk1,
+                     const int* blk2_job, const int* blk2_r0, int n_blk2, cudaStream_t st) {
+  k_sn_wtu<<<n_blk1, 256, 0, st>>>(jobs, blk_job, blk_k0);
+  PG_LAUNCH_CHECK();
+  k_sn_wv<<<n_blk2, 256, 0, st>>>(jobs, blk2_job, blk2_r0);
+  PG_LAUNCH_CHECK();
+  k_sn_finish<<<n_jobs, 256, 0, st>>>(jobs);
+  return cudaGetLastError();
+}
+cudaError_t sn_pack(const SnPack* jobs, const long long* blk_start, int n_jobs, long long total_blocks,
+                    cudaStream_t st) {
+  k_sn_pack<<<(unsigned)total_blocks, 256, 0, st>>>(jobs, blk_start, n_jobs);
+  return cudaGetLastError();
+}
+cudaError_t sn_backward(const SnJob* jobs, const int* idx, int n, float* const* grads, double* scratch,
+                        cudaStream_t st) {
+  (void)scratch;
+  k_sn_bwd<<<n, 1024, 0, st>>>(jobs, idx, grads);
+  return cudaGetLastError();
+}
+
+cudaError_t check_finite(const float* g, long long n, int* flag, cudaStream_t st) {
+  k_check_finite<<<grid_for(n, 256, 4), 256, 0, st>>>(g, n, flag);
+  return cudaGetLastError();
+}
+cudaError_t check_finite_scalar(const float* loss, int* flag, cudaStream_t st) {
+  k_check_finite_scalar<<<1, 1, 0, st>>>(loss, flag);
+  return cudaGetLastError();
+}
+cudaError_t adam_flat(float* w, const float* g, float* m, float* v, long long n, float lr, float b1, float b2,
+                      float eps, const long long* t_dev, float gscale, const int* flag, cudaStream_t st) {
+  k_adam<<<grid_for(n, 256, 4), 256, 0, st>>>(w, g, m, v, n, lr, b1, b2, eps, t_dev, gscale, flag);
+  return cudaGetLastError();
+}
+cudaError_t adam_bookkeep(long long* t_dev, const int* flag, int* sticky, cudaStream_t st) {
+  k_adam_bookkeep<<<1, 1, 0, st>>>(t_dev, flag, sticky);
+  return cudaGetLastError();
+}
+cudaError_t fill_normal(float* p, long long n, float std, uint64_t seed, uint64_t off, cudaStream_t st) {
+  k_fill_normal<<<grid_for(n, 256), 256, 0, st>>>(p, n, std, seed, off);
+  return cudaGetLastError();
+}
+cudaError_t fill_const(float* p, long long n, float v, cudaStream_t st) {
+  k_fill_const<<<grid_for(n, 256), 256, 0, st>>>(p, n, v);
+  return cudaGetLastError();
+}
+cudaError_t normalize_vec(float* p, int n, cudaStream_t st) {
+  k_normalize<<<1, 1024, 0, st>>>(p, n);
+  return cudaGetLastError();
+}
+cudaError_t oihw_to_ohwi(const float* s, float* d, int O, int I, int taps, cudaStream_t st) {
+  k_oihw_ohwi<<<grid_for((long long)O * I * taps, 256), 256, 0, st>>>(s, d, O, I, taps, 1);
+  return cudaGetLastError();
+}
+cudaError_t ohwi_to_oihw(const float* s, float* d, int O, int I, int taps, cudaStream_t st) {
+  k_oihw_ohwi<<<grid_for((long long)O * I * taps, 256), 256, 0, st>>>(s, d, O, I, taps, 0);
+  return cudaGetLastError();
+}
+cudaError_t scale_dev(float* p, long long n, const float* s, cudaStream_t st) {
+  k_scale_dev<<<grid_for(n, 256), 256, 0, st>>>(p, n, s);
+  return cudaGetLastError();
+}
+cudaError_t dot_f32(const float* a, const float* b, long long n, float* out, int accumulate, cudaStream_t st) {
+  k_dot<<<1, 1024, 0, st>>>(a, b, n, out, accumulate);
+  return cudaGetLastError();
+}
+cudaError_t copy_rows_cols(const float* src, long long lds, long long rows, int cols, float* dst, long long ldd,
+                           int accumulate, cudaStream_t st) {
+  k_copy_rows_cols<<<grid_for(rows * cols, 256), 256, 0, st>>>(src, lds, rows, cols, dst, ldd, accumulate);
+  return cudaGetLastError();
+}
+cudaError_t scale_f32(float* p, long long n, float s, cudaStream_t st) {
+  k_scale<<<grid_for(n, 256), 256, 0, st>>>(p, n, s);
+  return cudaGetLastError();
+}
+
+}  // namespace pg

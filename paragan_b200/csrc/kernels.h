@@ -1,0 +1,190 @@
+// Launchers of the memory-bound and SIMT kernels of libparagan.  Storage
+// type T is float (F32 mode) or bf16 (BF16 mode); arithmetic is fp32, global
+// reductions are accumulated in fp64.  Activations are NHWC, [M = N*H*W][C].
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace pg {
+
+// ---------------- layout (A1)
+template <typename TD>
+cudaError_t layout_pack(const float* src, TD* dst, int n, int c, int h, int w, int c_pad, long long dst_batch_offset,
+                        cudaStream_t st);
+template <typename TS>
+cudaError_t layout_unpack(const TS* src, float* dst, int n, int c, int h, int w, int c_pad, cudaStream_t st);
+
+// ---------------- small fp32 GEMM: C[m][n] = beta*C + sum_k A(m,k) B(n,k) (+ bias[n])
+// A(m,k) = A[m*sam + k*sak]; B(n,k) = B[n*sbn + k*sbk]; C[m*ldc + n]
+cudaError_t gemm_f32(int M, int N, int K, const float* A, long long sam, long long sak, const float* B,
+                     long long sbn, long long sbk, float* C, long long ldc, float beta, const float* bias,
+                     cudaStream_t st);
+
+// ---------------- conversion / gathers
+template <typename TD>
+cudaError_t convert_f32(const float* src, TD* dst, long long n, cudaStream_t st);
+template <typename TS>
+cudaError_t to_f32(const TS* src, float* dst, long long n, cudaStream_t st);
+cudaError_t gather_rows(const float* table, const int32_t* idx, int n, int dim, float* out, int ldo, cudaStream_t st);
+cudaError_t copy_cols(const float* src, int lds, int n, int cols, float* dst, int ldd, cudaStream_t st);
+// dtable[idx[i]][j] += src[i*lds + j]; deterministic (sequential over i per column)
+cudaError_t scatter_add_rows(const float* src, int lds, const int32_t* idx, int n, int dim, float* dtable,
+                             cudaStream_t st);
+
+// ---------------- batch norm (A4, A11)
+// partial sums over pixel blocks -> sums[2C] (fp64: sum x, sum x^2)
+template <typename T>
+cudaError_t bn_stats(const T* x, long long M, int C, double* partial, int max_blocks, double* sums, cudaStream_t st);
+// sums (all-reduced) -> mean, rstd (fp32)
+cudaError_t bn_finalize(const double* sums, int C, double count, float eps, float* mean, float* rstd,
+                        cudaStream_t st);
+// y = relu(x_hat * g + b), g = 1 + gain[n][c] (conditional) or gamma[c]; b = bias[n][c] or beta[c];
+// up2: write each output pixel to its 2x2 block of a [N,2H,2W,C] tensor
+template <typename TI, typename TO>
+cudaError_t bn_apply_relu(const TI* x, int N, int H, int W, int C, const float* mean, const float* rstd,
+                          const float* gain, const float* bias, const float* gamma, const float* beta, TO* y, bool up2,
+                          cudaStream_t st);
+// backward, pass 1: per sample sums A[n][c] = sum g0, Bv[n][c] = sum g0*x_hat (g0 = dy * relu')
+// dy is [N,2H,2W,C] when up2 (summed over each 2x2 block)
+template <typename TI, typename TG>
+cudaError_t bn_bwd_reduce(const TI* x, const TG* dy, int N, int H, int W, int C, const float* mean, const float* rstd,
+                          const float* gain, const float* bias, const float* gamma, const float* beta, bool up2,
+                          float* partial, int chunks, float* AB, cudaStream_t st);
+// channel totals tot[2C] = sum_n g[n][c]*A[n][c], sum_n g[n][c]*Bv[n][c]  (fp64)
+cudaError_t bn_bwd_totals(const float* AB, int N, int C, const float* gain, const float* gamma, double* tot,
+                          cudaStream_t st);
+// pass 2: dx = rstd*(g*g0 - tot0/cnt - x_hat*tot1/cnt) (+ add)
+template <typename TI, typename TG, typename TO>
+cudaError_t bn_bwd_apply(const TI* x, const TG* dy, int N, int H, int W, int C, const float* mean, const float* rstd,
+                         const float* gain, const float* bias, const float* gamma, const float* beta, bool up2,
+                         const double* tot, double count, const TO* add, TO* dx, cudaStream_t st);
+
+// ---------------- elementwise / resampling (A7, A11)
+template <typename T>
+cudaError_t relu_copy(const T* x, T* y, long long n, cudaStream_t st);
+// dx = dy * [ref > 0] (+ add)
+template <typename T>
+cudaError_t relu_bwd(const T* dy, const T* ref, const T* add, T* dx, long long n, cudaStream_t st);
+// y[N,H/2,W/2,C] = avgpool2(x) (+ add[N,H/2,W/2,C])
+template <typename T>
+cudaError_t avgpool2(const T* x, int N, int H, int W, int C, int ldx, const T* add, T* y, cudaStream_t st);
+// dx[N,H,W,C] = 0.25 * dy[n,h/2,w/2,c]   (avgpool adjoint); optional add (same shape as dx)
+template <typename T>
+cudaError_t avgpool2_bwd(const T* dy, int N, int H, int W, int C, const T* add, T* dx, int lddx, cudaStream_t st);
+// dx[N,H,W,C] = sum of the 2x2 block of dy[N,2H,2W,C]   (nearest-upsample adjoint)
+template <typename T>
+cudaError_t up2_bwd(const T* dy, int N, int H, int W, int C, T* dx, cudaStream_t st);
+// column sums: db[c] (+)= sum_m dy[m][c]   (bias gradients; fp64 partials, fixed order)
+template <typename T>
+cudaError_t col_sum(const T* dy, long long M, int C, double* partial, int max_blocks, float* db, int accumulate,
+                    cudaStream_t st);
+
+// ---------------- G output layer (fp32) and image buffer
+// img = tanh(pre[M][3]); writes fp32 img and T copy into dst[M][c_pad] (pad channels zero)
+template <typename T>
+cudaError_t tanh_to_image(const float* pre, float* img, T* dst, long long M, int c_pad, cudaStream_t st);
+// dpre[m][k] = dimg[m][k] * (1 - img^2), k < 3
+template <typename T>
+cudaError_t tanh_bwd(const T* dimg, int c_pad, const float* img, float* dpre, long long M, cudaStream_t st);
+
+// ---------------- SIMT convolution (F32 path; G output conv in both modes)
+// y[m][o] = alpha*sum + bias[o] + residual; w[Cout][k*k][Cin]
+template <typename TI, typename TW, typename TO>
+cudaError_t simt_conv_fwd(const TI* x, int N, int H, int W, int Cin, const TW* w, int Cout, int ksz,
+                          const float* bias, const float* alpha, const TO* residual, int res_mode, TO* y,
+                          cudaStream_t st);
+// dw[o][tap][c] (+)= sum_m dy[m][o] * x[m+tap][c]   (fp32, atomics across pixel splits)
+template <typename TI, typename TG>
+cudaError_t simt_conv_wgrad(const TI* x, const TG* dy, int N, int H, int W, int Cin, int Cout, int ksz, float* dw,
+                            int accumulate, cudaStream_t st);
+
+// ---------------- discriminator head + hinge loss (A7, A8), fp32
+template <typename T>
+cudaError_t d_head_fwd(const T* h, int N, int HW, int C, const float* w_lin, const float* b_lin, const float* embed,
+                       const int32_t* y, float* feat, float* logits, cudaStream_t st);
+// mode 0: D loss over [fake(B); real(B)]; mode 1: G loss over B fakes.  Writes loss[0..3]
+// (loss, mean real logit, mean fake logit, nonfinite) and dlogits (local-mean scaling 1/B).
+cudaError_t hinge_loss(const float* logits, int B, int mode, float* dlogits, float* loss_out, cudaStream_t st);
+// backward: dfeat = dl*(w + E[y]); dh = dfeat * [h > 0]; grads of w, b, E (if want_wgrad)
+template <typename T>
+cudaError_t d_head_bwd(const T* h, int N, int HW, int C, const float* w_lin, const float* embed, const int32_t* y,
+                       const float* feat, const float* dlogits, T* dh, float* dw_lin, float* db_lin, float* dembed,
+                       int n_classes, bool want_wgrad, cudaStream_t st);
+
+// ---------------- attention (A6)
+// pooled[n][hw/4][c] = max over 2x2 of x[n][.][c_off + c] (ld = ldx); also transposed copy pooledT[n][c][hw/4]
+template <typename T>
+cudaError_t maxpool2_split(const T* x, int N, int H, int W, int ldx, int c_off, int C, T* pooled, T* pooledT,
+                           cudaStream_t st);
+// dx[n][h][w][c_off+c] = dpooled at the argmax of each 2x2 block (others 0); dpooled given [n][hw/4][c] (fp32)
+template <typename T>
+cudaError_t maxpool2_split_bwd(const T* x, int N, int H, int W, int ldx, int c_off, int C, const float* dpooled,
+                               T* dx, cudaStream_t st);
+// P = softmax rows of S [rows][cols] fp32 -> T
+template <typename T>
+cudaError_t softmax_rows(const float* S, long long rows, int cols, T* P, cudaStream_t st);
+// dS = P * (dP - rowsum(dP * P))  (fp32 dP, T P) -> T
+template <typename T>
+cudaError_t softmax_bwd_rows(const T* P, const float* dP, long long rows, int cols, T* dS, cudaStream_t st);
+// batched SIMT GEMM for the F32 path: C[b][m][n] = sum_k A[b](m,k) B[b](n,k)
+cudaError_t gemm_f32_batched(int batch, int M, int N, int K, const float* A, long long sab, long long sam,
+                             long long sak, const float* B, long long sbb, long long sbn, long long sbk, float* C,
+                             long long scb, long long ldc, float beta, cudaStream_t st);
+
+// ---------------- spectral norm (A2) and Adam (A13)
+struct SnJob {
+  const float* w;   // [rows][K] fp32 master
+  float* u;         // [rows] (updated in place)
+  float* v;         // [K] out
+  float* t;         // [K] scratch (W^T u)
+  float* s;         // [rows] scratch (W v)
+  float* sigma;     // [2]: sigma, 1/sigma
+  int rows, K;
+};
+struct SnPack {     // one packed copy of W/sigma
+  const float* w;
+  const float* sigma;
+  void* dst;        // bf16 or fp32
+  int rows, taps, cin;  // W is [rows][taps][cin]
+  int mode;         // 0: dst[o + row_off][t][c] (row stride taps*dst_cin); 1: dgrad dst[c][taps-1-t][o + row_off]
+  int dst_bf16;
+  int dst_row_offset;  // sub-block placement (qkv packing)
+  int dst_rows;        // mode 1: total rows (row stride of the transposed layout)
+  int dst_cin;         // mode 0: padded input channels (>= cin; pads left untouched = 0)
+};
+cudaError_t sn_power(const SnJob* jobs_dev, int n_jobs, const int* blk_job_dev, const int* blk_k0_dev, int n_blk1,
+                     const int* blk2_job_dev, const int* blk2_r0_dev, int n_blk2, cudaStream_t st);
+cudaError_t sn_pack(const SnPack* jobs_dev, const long long* blk_start_dev, int n_jobs, long long total_blocks,
+                    cudaStream_t st);
+// SN backward for one weight: g <- (g - <g, W/sigma> u v^T) / sigma
+cudaError_t sn_backward(const SnJob* jobs_dev, const int* idx_dev, int n, float* const* grads_dev, double* scratch,
+                        cudaStream_t st);
+
+// flag[0] |= any non-finite in g
+cudaError_t check_finite(const float* g, long long n, int* flag, cudaStream_t st);
+cudaError_t check_finite_scalar(const float* loss, int* flag, cudaStream_t st);
+// Adam over a flat buffer; g scaled by gscale (1/world); skipped when *flag != 0
+cudaError_t adam_flat(float* w, const float* g, float* m, float* v, long long n, float lr, float b1, float b2,
+                      float eps, const long long* t_dev, float gscale, const int* flag, cudaStream_t st);
+cudaError_t adam_bookkeep(long long* t_dev, const int* flag, int* nonfinite_sticky, cudaStream_t st);
+
+// seeded on-device init: counter-based Gaussian (Box-Muller over a 64-bit hash)
+cudaError_t fill_normal(float* p, long long n, float std, uint64_t seed, uint64_t offset, cudaStream_t st);
+cudaError_t fill_const(float* p, long long n, float v, cudaStream_t st);
+cudaError_t normalize_vec(float* p, int n, cudaStream_t st);
+
+// conversions between canonical OIHW and internal OHWI master layout
+cudaError_t oihw_to_ohwi(const float* src, float* dst, int O, int I, int taps, cudaStream_t st);
+cudaError_t ohwi_to_oihw(const float* src, float* dst, int O, int I, int taps, cudaStream_t st);
+cudaError_t scale_f32(float* p, long long n, float s, cudaStream_t st);
+// p[i] *= *s (device scalar)
+cudaError_t scale_dev(float* p, long long n, const float* s, cudaStream_t st);
+// out[0] (+)= sum_i a[i]*b[i]  (fp64 accumulation, single block)
+cudaError_t dot_f32(const float* a, const float* b, long long n, float* out, int accumulate, cudaStream_t st);
+// dst[r*ldd + j] (+)= src[r*lds + j] for j < cols
+cudaError_t copy_rows_cols(const float* src, long long lds, long long rows, int cols, float* dst, long long ldd,
+                           int accumulate, cudaStream_t st);
+
+}  // namespace pg

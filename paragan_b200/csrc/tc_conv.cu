@@ -1,0 +1,583 @@
+// tcgen05 implicit-GEMM convolution for sm_100a.
+//
+// Activations are NHWC bf16 ("hardware-aware layout").  A
+// 3x3 / 1x1 stride-1 'same' convolution is a GEMM over M = N*H*W output
+// pixels, N = C_out, K = taps * C_in.  No im2col is materialised: the A tile
+// of one K-block (one filter tap x 64 input channels) is a single 4-D TMA box
+// {64 ch, bw, bh, bn} of the input at coordinates shifted by the tap offset;
+// TMA's out-of-bounds zero fill *is* the zero padding, per image and per edge.
+//
+//   fprop : A = X (K-major), B = W^  [C_out][taps][C_in]          -> Y
+//   dgrad : A = dY (K-major), B = W^T [C_in][taps'][C_out] (flip) -> dX
+//   wgrad : A = dY (MN-major, M = C_out), B = X shifted (MN-major,
+//           N = C_in of one tap), K = pixels, split-K with fp32 partials
+//
+// Warp roles (192 threads, 1 CTA/SM, persistent over tiles):
+//   warp 0 lane 0 : TMA producer over a STAGES-deep smem ring (mbarriers)
+//   warp 1        : TMEM allocation; lane 0 issues tcgen05.mma and commits
+//   warps 2..5    : epilogue, TMEM -> registers -> global (bias / residual /
+//                   scale fused), double-buffered accumulators in TMEM so the
+//                   epilogue of tile i overlaps the main loop of tile i+1.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+#include "tc_conv.h"
+#include "tc_ptx.cuh"
+
+namespace pg {
+
+namespace {
+
+constexpr int kTileM = 128;
+constexpr uint32_t kAtomBytes = 128 * 128;   // 128 rows x 128 B (64 bf16)
+constexpr int kSmemBudget = 200 * 1024;
+
+template <int BN>
+struct FpropCfg {
+  static constexpr uint32_t A_BYTES = kAtomBytes;
+  static constexpr uint32_t B_BYTES = BN * 128;
+  static constexpr int STAGES_RAW = kSmemBudget / (A_BYTES + B_BYTES);
+  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
+  static constexpr uint32_t TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
+                                        : (2 * BN <= 256) ? 256 : 512;
+  static constexpr size_t SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + 256;
+};
+
+template <int BN>
+struct WgradCfg {
+  static constexpr int NB = (BN + 63) / 64;           // 64-wide MN atoms of B
+  static constexpr uint32_t A_BYTES = 2 * kAtomBytes;  // M = 128 output channels
+  static constexpr uint32_t B_BYTES = NB * kAtomBytes;
+  static constexpr int STAGES_RAW = kSmemBudget / (A_BYTES + B_BYTES);
+  static constexpr int STAGES = STAGES_RAW > 6 ? 6 : STAGES_RAW;
+  static constexpr uint32_t TMEM_COLS = (BN <= 32) ? 32 : (BN <= 64) ? 64 : (BN <= 128) ? 128 : 256;
+  static constexpr size_t SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + 256;
+};
+
+__device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
+  uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  return reinterpret_cast<uint8_t*>((a + 1023) & ~uintptr_t(1023));
+}
+
+// pixel index -> (n, h, w) origin of a 128-pixel tile
+__device__ __forceinline__ void pix_origin(int p0, int H, int W, int& n0, int& h0, int& w0) {
+  int hw = H * W;
+  n0 = p0 / hw;
+  int r = p0 - n0 * hw;
+  h0 = r / W;
+  w0 = r - h0 * W;
+}
+
+__device__ __forceinline__ void store_row32_bf16(bf16* dst, const float (&v)[32]) {
+  uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint4 u;
+    uint32_t* w = reinterpret_cast<uint32_t*>(&u);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      __nv_bfloat162 t = __floats2bfloat162_rn(v[q * 8 + 2 * j], v[q * 8 + 2 * j + 1]);
+      w[j] = *reinterpret_cast<uint32_t*>(&t);
+    }
+    d[q] = u;
+  }
+}
+
+__device__ __forceinline__ void load_row32_bf16(const bf16* src, float (&r)[32]) {
+  const uint4* s = reinterpret_cast<const uint4*>(src);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint4 u = s[q];
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float2 f = __bfloat1622float2(h[j]);
+      r[q * 8 + 2 * j] = f.x;
+      r[q * 8 + 2 * j + 1] = f.y;
+    }
+  }
+}
+
+// ===========================================================================
+// fprop / dgrad kernel
+// ===========================================================================
+template <int BN>
+__global__ void __launch_bounds__(192, 1)
+    k_conv_fprop(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                 const TcFpropArgs a) {
+  using C = FpropCfg<BN>;
+  constexpr int STAGES = C::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * C::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * C::B_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    tc::tma_prefetch(&tmA);
+    tc::tma_prefetch(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&tfull[b], 1);
+      tc::mbar_init(&tempty[b], 128);
+    }
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tmem_slot, C::TMEM_COLS);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const int num_tiles = a.m_tiles * a.n_tiles;
+  const int num_kb = a.taps * a.c_chunks;
+  const int pad = a.ksz >> 1;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int mt = tile / a.n_tiles, nt = tile - mt * a.n_tiles;
+        int n0, h0, w0;
+        pix_origin(mt * kTileM, a.H, a.W, n0, h0, w0);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          const int tap = kb / a.c_chunks, cc = kb - tap * a.c_chunks;
+          const int dy = tap / a.ksz - pad, dx = tap % a.ksz - pad;
+          tc::mbar_wait(&empty[stage], phase ^ 1);
+          tc::mbar_expect_tx(&full[stage], C::A_BYTES + C::B_BYTES);
+          tc::tma_load_4d(sA + stage * C::A_BYTES, &tmA, &full[stage], cc * 64, w0 + dx, h0 + dy, n0);
+          tc::tma_load_3d(sB + stage * C::B_BYTES, &tmB, &full[stage], cc * 64, tap, nt * BN);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = tc::idesc_bf16(kTileM, BN, false, false);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+        const int buf = it & 1;
+        tc::mbar_wait(&tempty[buf], ((it >> 1) & 1) ^ 1);
+        tc::tc_fence_after();
+        const uint32_t d_tmem = tmem + buf * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          tc::mbar_wait(&full[stage], phase);
+          tc::tc_fence_after();
+          const uint32_t a_base = tc::smem_u32(sA + stage * C::A_BYTES);
+          const uint32_t b_base = tc::smem_u32(sB + stage * C::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint64_t ad = tc::sdesc_sw128(a_base + k * 32, 16, 1024);
+            const uint64_t bd = tc::sdesc_sw128(b_base + k * 32, 16, 1024);
+            tc::mma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0);
+          }
+          tc::mma_commit(&empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        tc::mma_commit(&tfull[buf]);
+      }
+    }
+  } else {
+    // ------------------------------------------------ epilogue warps 2..5
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const float alpha = a.alpha ? *a.alpha : 1.0f;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      const int buf = it & 1;
+      const int mt = tile / a.n_tiles, nt = tile - mt * a.n_tiles;
+      tc::mbar_wait(&tfull[buf], (it >> 1) & 1);
+      tc::tc_fence_after();
+      const long long m = (long long)mt * kTileM + row;
+      const bool valid = m < a.M;
+      long long rbase = 0;
+      if (valid && a.residual) {
+        if (a.res_mode == 2) {   // residual stored at half resolution (nearest x2 upsample)
+          const int hw = a.H * a.W;
+          const int n = (int)(m / hw);
+          const int r = (int)(m - (long long)n * hw);
+          const int h = r / a.W, w = r - h * a.W;
+          rbase = ((long long)(n * (a.H >> 1) + (h >> 1)) * (a.W >> 1) + (w >> 1)) * a.ldr;
+        } else {
+          rbase = m * a.ldr;
+        }
+      }
+#pragma unroll 1
+      for (int cb = 0; cb < BN; cb += 32) {
+        float v[32];
+        tc::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + buf * BN + cb, v);
+        const int col0 = nt * BN + cb;
+        if (!valid || col0 >= a.Cout) continue;
+        const bool full32 = (col0 + 32 <= a.Cout);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] *= alpha;
+        if (a.bias) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (full32 || col0 + j < a.Cout) v[j] += a.bias[col0 + j];
+        }
+        if (a.residual) {
+          const bf16* rp = reinterpret_cast<const bf16*>(a.residual) + rbase + col0;
+          if (full32) {
+            float r[32];
+            load_row32_bf16(rp, r);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] += r[j];
+          } else {
+            for (int j = 0; j < 32 && col0 + j < a.Cout; ++j) v[j] += __bfloat162float(rp[j]);
+          }
+        }
+        if (a.out_f32) {
+          float* op = reinterpret_cast<float*>(a.out) + m * a.ldo + col0;
+          if (full32) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(op + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+          } else {
+            for (int j = 0; j < 32 && col0 + j < a.Cout; ++j) op[j] = v[j];
+          }
+        } else {
+          bf16* op = reinterpret_cast<bf16*>(a.out) + m * a.ldo + col0;
+          if (full32) {
+            store_row32_bf16(op, v);
+          } else {
+            for (int j = 0; j < 32 && col0 + j < a.Cout; ++j) op[j] = __float2bfloat16_rn(v[j]);
+          }
+        }
+      }
+      tc::tc_fence_before();
+      tc::mbar_arrive(&tempty[buf]);
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tmem, C::TMEM_COLS);
+}
+
+// ===========================================================================
+// wgrad kernel: dW[o][tap][c] = sum_p dY[p][o] * X[p + delta_tap][c]
+// ===========================================================================
+template <int BN>
+__global__ void __launch_bounds__(192, 1)
+    k_conv_wgrad(const __grid_constant__ CUtensorMap tmDY, const __grid_constant__ CUtensorMap tmX,
+                 const TcWgradArgs a) {
+  using C = WgradCfg<BN>;
+  constexpr int STAGES = C::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * C::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * C::B_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    tc::tma_prefetch(&tmDY);
+    tc::tma_prefetch(&tmX);
+    for (int s = 0; s < STAGES; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    tc::mbar_init(&tfull[0], 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tmem_slot, C::TMEM_COLS);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  // work unit -> (m tile over C_out, n tile over (tap, C_in block), split)
+  int u = blockIdx.x;
+  const int split = u % a.splits;
+  u /= a.splits;
+  const int nt = u % a.n_tiles;
+  const int mt = u / a.n_tiles;
+  const int tap = nt / a.c_blocks, cb = nt - tap * a.c_blocks;
+  const int pad = a.ksz >> 1;
+  const int dy = tap / a.ksz - pad, dx = tap % a.ksz - pad;
+  const int kb0 = split * a.kb_per_split;
+  const int kb1 = min(a.total_kb, kb0 + a.kb_per_split);
+  const int o0 = mt * 128, c0 = cb * BN;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        int n0, h0, w0;
+        pix_origin(kb * kTileM, a.H, a.W, n0, h0, w0);
+        tc::mbar_wait(&empty[stage], phase ^ 1);
+        tc::mbar_expect_tx(&full[stage], C::A_BYTES + C::B_BYTES);
+        uint8_t* da = sA + stage * C::A_BYTES;
+        tc::tma_load_4d(da, &tmDY, &full[stage], o0, w0, h0, n0);
+        tc::tma_load_4d(da + kAtomBytes, &tmDY, &full[stage], o0 + 64, w0, h0, n0);
+        uint8_t* db = sB + stage * C::B_BYTES;
+#pragma unroll
+        for (int j = 0; j < C::NB; ++j)
+          tc::tma_load_4d(db + j * kAtomBytes, &tmX, &full[stage], c0 + 64 * j, w0 + dx, h0 + dy, n0);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = tc::idesc_bf16(128, BN, true, true);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        tc::mbar_wait(&full[stage], phase);
+        tc::tc_fence_after();
+        const uint32_t a_base = tc::smem_u32(sA + stage * C::A_BYTES);
+        const uint32_t b_base = tc::smem_u32(sB + stage * C::B_BYTES);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {   // 8 x K=16 pixels; each K=16 step = two 8-row groups = 2048 B
+          const uint64_t ad = tc::sdesc_sw128(a_base + k * 2048, kAtomBytes, 1024);
+          const uint64_t bd = tc::sdesc_sw128(b_base + k * 2048, kAtomBytes, 1024);
+          tc::mma_bf16(tmem, ad, bd, idesc, (kb != kb0) || (k != 0));
+        }
+        tc::mma_commit(&empty[stage]);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+      tc::mma_commit(&tfull[0]);
+    }
+  } else {
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    tc::mbar_wait(&tfull[0], 0);
+    tc::tc_fence_after();
+    const int o = o0 + row;
+#pragma unroll 1
+    for (int cbk = 0; cbk < BN; cbk += 32) {
+      float v[32];
+      tc::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + cbk, v);
+      const int col0 = c0 + cbk;
+      if (o >= a.Cout || col0 >= a.Cin) continue;
+      float* op = a.out + (((long long)split * a.Cout + o) * a.taps + tap) * a.Cin + col0;
+      if (col0 + 32 <= a.Cin && (a.Cin & 3) == 0) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(op + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+      } else {
+        for (int j = 0; j < 32 && col0 + j < a.Cin; ++j) op[j] = v[j];
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tmem, C::TMEM_COLS);
+}
+
+// deterministic split-K reduction: dst[i] (+)= sum_s part[s][i] in split order
+__global__ void k_split_reduce(const float* __restrict__ part, float* __restrict__ dst, long long n, int splits,
+                               int accumulate) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (; i < n; i += stride) {
+    float s = accumulate ? dst[i] : 0.0f;
+    for (int k = 0; k < splits; ++k) s += part[(long long)k * n + i];
+    dst[i] = s;
+  }
+}
+
+// ------------------------------------------------------------------ host side
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+cudaError_t get_encoder() {
+  if (g_encode) return cudaSuccess;
+  cudaDriverEntryPointQueryResult qr;
+  PG_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&g_encode), cudaEnableDefault,
+                                  &qr));
+  if (qr != cudaDriverEntryPointSuccess || !g_encode) return cudaErrorNotSupported;
+  return cudaSuccess;
+}
+
+void tile_box(int N, int H, int W, int& bw, int& bh, int& bn) {
+  bw = W < 128 ? W : 128;
+  bh = H < 128 / bw ? H : 128 / bw;
+  bn = 128 / (bw * bh);
+  (void)N;
+}
+
+cudaError_t act_map(CUtensorMap* m, const void* base, int N, int H, int W, int C) {
+  PG_CUDA(get_encoder());
+  int bw, bh, bn;
+  tile_box(N, H, W, bw, bh, bn);
+  cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
+  cuuint64_t strides[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
+  cuuint32_t box[4] = {64, (cuuint32_t)bw, (cuuint32_t)bh, (cuuint32_t)bn};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+cudaError_t weight_map(CUtensorMap* m, const void* base, int rows, int taps, int C, int box_rows) {
+  PG_CUDA(get_encoder());
+  cuuint64_t dims[3] = {(cuuint64_t)C, (cuuint64_t)taps, (cuuint64_t)rows};
+  cuuint64_t strides[2] = {(cuuint64_t)C * 2, (cuuint64_t)taps * C * 2};
+  cuuint32_t box[3] = {64, 1, (cuuint32_t)box_rows};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+template <int BN>
+cudaError_t launch_fprop_bn(const CUtensorMap& ma, const CUtensorMap& mb, const TcFpropArgs& a, int num_sms,
+                            cudaStream_t st) {
+  using C = FpropCfg<BN>;
+  static bool attr = false;
+  if (!attr) {
+    PG_CUDA(cudaFuncSetAttribute(k_conv_fprop<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    attr = true;
+  }
+  const int tiles = a.m_tiles * a.n_tiles;
+  const int grid = tiles < num_sms ? tiles : num_sms;
+  k_conv_fprop<BN><<<grid, 192, C::SMEM, st>>>(ma, mb, a);
+  return cudaGetLastError();
+}
+
+template <int BN>
+cudaError_t launch_wgrad_bn(const CUtensorMap& ma, const CUtensorMap& mb, const TcWgradArgs& a, cudaStream_t st) {
+  using C = WgradCfg<BN>;
+  static bool attr = false;
+  if (!attr) {
+    PG_CUDA(cudaFuncSetAttribute(k_conv_wgrad<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    attr = true;
+  }
+  const int units = a.m_tiles * a.n_tiles * a.splits;
+  k_conv_wgrad<BN><<<units, 192, C::SMEM, st>>>(ma, mb, a);
+  return cudaGetLastError();
+}
+
+int pick_bn(int cout) {
+  if (cout % 256 == 0) return 256;
+  if (cout % 192 == 0) return 192;
+  if (cout % 128 == 0) return 128;
+  if (cout == 96) return 96;
+  if (cout <= 32) return 32;
+  if (cout <= 64) return 64;
+  if (cout <= 96) return 96;
+  return 128;
+}
+
+}  // namespace
+
+int tc_fprop_bn(int cout) { return pick_bn(cout); }
+
+cudaError_t tc_conv_fprop(const void* x, int N, int H, int W, int Cin, const void* wpack, int Cout, int ksz,
+                          const TcEpilogue& epi, cudaStream_t st) {
+  if (Cin % 8 || ((uintptr_t)x & 15) || ((uintptr_t)wpack & 15)) return cudaErrorInvalidValue;
+  CUtensorMap ma, mb;
+  const int bn = pick_bn(Cout);
+  PG_CUDA(act_map(&ma, x, N, H, W, Cin));
+  PG_CUDA(weight_map(&mb, wpack, Cout, ksz * ksz, Cin, bn));
+  TcFpropArgs a{};
+  a.M = (long long)N * H * W;
+  a.H = H;
+  a.W = W;
+  a.ksz = ksz;
+  a.taps = ksz * ksz;
+  a.c_chunks = ceil_div(Cin, 64);
+  a.Cout = Cout;
+  a.m_tiles = ceil_div(a.M, kTileM);
+  a.n_tiles = ceil_div(Cout, bn);
+  a.bias = epi.bias;
+  a.alpha = epi.alpha;
+  a.residual = epi.residual;
+  a.res_mode = epi.res_mode;
+  a.ldr = epi.ldr ? epi.ldr : Cout;
+  a.out = epi.out;
+  a.out_f32 = epi.out_f32;
+  a.ldo = epi.ldo ? epi.ldo : Cout;
+  const int sms = kNumSMs;
+  switch (bn) {
+    case 32: return launch_fprop_bn<32>(ma, mb, a, sms, st);
+    case 64: return launch_fprop_bn<64>(ma, mb, a, sms, st);
+    case 96: return launch_fprop_bn<96>(ma, mb, a, sms, st);
+    case 128: return launch_fprop_bn<128>(ma, mb, a, sms, st);
+    case 192: return launch_fprop_bn<192>(ma, mb, a, sms, st);
+    default: return launch_fprop_bn<256>(ma, mb, a, sms, st);
+  }
+}
+
+size_t tc_wgrad_workspace_floats(int N, int H, int W, int Cin, int Cout, int ksz) {
+  // upper bound used by the engine to size its split-K scratch
+  (void)N; (void)H; (void)W;
+  return (size_t)32 * Cout * ksz * ksz * Cin;
+}
+
+cudaError_t tc_conv_wgrad(const void* x, const void* dy, int N, int H, int W, int Cin, int Cout, int ksz,
+                          float* dw, int accumulate, float* scratch, size_t scratch_floats, cudaStream_t st) {
+  if (Cin % 8 || Cout % 8 || ((uintptr_t)x & 15) || ((uintptr_t)dy & 15)) return cudaErrorInvalidValue;
+  int bn;
+  if (Cin % 256 == 0) bn = 256;
+  else if (Cin % 192 == 0) bn = 192;
+  else if (Cin % 128 == 0) bn = 128;
+  else if (Cin <= 32) bn = 32;
+  else if (Cin <= 64) bn = 64;
+  else if (Cin <= 96) bn = 96;
+  else bn = 128;
+  CUtensorMap mdy, mx;
+  PG_CUDA(act_map(&mdy, dy, N, H, W, Cout));
+  PG_CUDA(act_map(&mx, x, N, H, W, Cin));
+  TcWgradArgs a{};
+  a.H = H;
+  a.W = W;
+  a.ksz = ksz;
+  a.taps = ksz * ksz;
+  a.Cin = Cin;
+  a.Cout = Cout;
+  a.c_blocks = ceil_div(Cin, bn);
+  a.m_tiles = ceil_div(Cout, 128);
+  a.n_tiles = a.taps * a.c_blocks;
+  a.total_kb = ceil_div((long long)N * H * W, kTileM);
+  const int tiles = a.m_tiles * a.n_tiles;
+  // split K so that tiles * splits covers the SMs ~2x, with >= 4 K-blocks per split
+  int splits = (2 * kNumSMs + tiles - 1) / tiles;
+  if (splits > a.total_kb / 4) splits = a.total_kb / 4;
+  if (splits < 1) splits = 1;
+  const size_t out_floats = (size_t)Cout * a.taps * Cin;
+  const bool direct = (splits == 1 && !accumulate);
+  if (!direct) {
+    while (splits > 1 && (size_t)splits * out_floats > scratch_floats) --splits;
+    if ((size_t)splits * out_floats > scratch_floats) return cudaErrorMemoryAllocation;
+  }
+  a.kb_per_split = ceil_div(a.total_kb, splits);
+  a.splits = ceil_div(a.total_kb, a.kb_per_split);
+  a.out = direct ? dw : scratch;
+  cudaError_t e;
+  switch (bn) {
+    case 32: e = launch_wgrad_bn<32>(mdy, mx, a, st); break;
+    case 64: e = launch_wgrad_bn<64>(mdy, mx, a, st); break;
+    case 96: e = launch_wgrad_bn<96>(mdy, mx, a, st); break;
+    case 128: e = launch_wgrad_bn<128>(mdy, mx, a, st); break;
+    case 192: e = launch_wgrad_bn<192>(mdy, mx, a, st); break;
+    default: e = launch_wgrad_bn<256>(mdy, mx, a, st); break;
+  }
+  PG_CUDA(e);
+  if (!direct) {
+    const long long n = (long long)out_floats;
+    int blocks = ceil_div(n, 256);
+    if (blocks > 4 * kNumSMs) blocks = 4 * kNumSMs;
+    k_split_reduce<<<blocks, 256, 0, st>>>(scratch, dw, n, a.splits, accumulate);
+    PG_LAUNCH_CHECK();
+  }
+  return cudaSuccess;
+}
+
+}  // namespace pg

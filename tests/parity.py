@@ -1,0 +1,112 @@
+"""Helpers for step-level parity: run one ParaGAN iteration on the oracle and on
+the CUDA path (through the C-ABI) from the same seeded inputs, and compare
+tensor by tensor (SURVEY §8(c) "Comparison rules")."""
+from __future__ import annotations
+
+import numpy as np
+
+from oracle import biggan as bg
+from paragan_b200 import inputs
+
+
+def oracle_config(res, ch, attn, n_classes, shared_dim, z_chunk, n_d=1, bf16=False):
+    eps = 1e-6 if bf16 else 1e-8
+    return bg.Config(resolution=res, ch=ch, attn_res=attn, n_classes=n_classes, shared_dim=shared_dim,
+                     z_chunk=z_chunk, d_steps_per_g=n_d, bf16=bf16,
+                     adam_d=bg.AdamHP(2e-4, 0.0, 0.999, eps), adam_g=bg.AdamHP(5e-5, 0.0, 0.999, eps))
+
+
+def make_inputs(ocfg, B, seed, n_d=1, gamma=0.1):
+    """Global-batch inputs: initial states and n_d D batches + 1 G batch (R18)."""
+    gs, ds = bg.g_param_specs(ocfg), bg.d_param_specs(ocfg)
+    g0 = inputs.init_params(gs, seed, inputs.ROLE_PARAMS_G, attn_gamma=gamma)
+    d0 = inputs.init_params(ds, seed, inputs.ROLE_PARAMS_D, attn_gamma=gamma)
+    dbs = []
+    for k in range(n_d):
+        real, ry = inputs.real_batch(seed, k, B, ocfg.resolution, ocfg.n_classes)
+        z, fy = inputs.latent_batch(seed, inputs.ROLE_Z_D, k, B, ocfg.dim_z, ocfg.n_classes)
+        dbs.append((real, ry, z, fy))
+    zg, yg = inputs.latent_batch(seed, inputs.ROLE_Z_G, 0, B, ocfg.dim_z, ocfg.n_classes)
+    return gs, ds, g0, d0, dbs, (zg, yg)
+
+
+def run_oracle(ocfg, gs, ds, g0, d0, dbs, gb):
+    G = bg.NetState.from_flat(gs, g0)
+    D = bg.NetState.from_flat(ds, d0)
+    out = bg.iteration(ocfg, G, D, dbs, gb)
+    return dict(d_loss=out["d"][-1]["loss"], g_loss=out["g"]["loss"], d_grads=out["d"][-1]["grads"],
+                g_grads=out["g"]["grads"], g_state=G.flat(), d_state=D.flat(), fake=out["g"]["fake"],
+                d_logits=out["d"][-1]["logits"], g_logits=out["g"]["logits"])
+
+
+def run_gpu(cfg, g0, d0, dbs, gb, rank=0, world=1, nccl_id=None, ctx=None):
+    """One iteration through the C-ABI on this rank's shard of the global batch."""
+    import torch
+    from paragan_b200 import api
+    dev = f"cuda:{cfg.device}"
+    own = ctx is None
+    if own:
+        ctx = api.Context(cfg, nccl_id)
+    ctx.set_params(api.NET_G, g0)
+    ctx.set_params(api.NET_D, d0)
+    tdt = torch.bfloat16 if cfg.compute == api.BF16 else torch.float32
+    R = cfg.resolution
+    for real, ry, z, fy in dbs:
+        real = inputs.shard(real, rank, world)
+        rp = torch.empty((real.shape[0], R, R, cfg.c_pad_image), dtype=tdt, device=dev)
+        api.layout_pack(torch.from_numpy(real).to(dev), rp, cfg.compute, cfg.c_pad_image)
+        ctx.d_step(rp, torch.from_numpy(inputs.shard(ry, rank, world)).to(dev),
+                   torch.from_numpy(inputs.shard(z, rank, world)).to(dev),
+                   torch.from_numpy(inputs.shard(fy, rank, world)).to(dev))
+    zg, yg = gb
+    ctx.g_step(torch.from_numpy(inputs.shard(zg, rank, world)).to(dev),
+               torch.from_numpy(inputs.shard(yg, rank, world)).to(dev))
+    st = ctx.sync_stats(raise_nonfinite=False)
+    res = dict(d_loss=st.d_loss, g_loss=st.g_loss, d_grads=ctx.get_grads(api.NET_D), g_grads=ctx.get_grads(api.NET_G),
+               g_state=ctx.get_params(api.NET_G), d_state=ctx.get_params(api.NET_D), fake=ctx.get_fakes(),
+               stats=st, launches=ctx.kernel_launches())
+    if own:
+        ctx.close()
+    return res
+
+
+def rel(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def compare_tensors(specs, got, want, tol, floor_frac=1e-3, with_u=False):
+    """Per tensor: ||got - want|| <= tol * ||want|| + floor, floor = floor_frac * tol * RMS-norm scale of
+    the whole vector (tensors whose exact value is ~0, e.g. a bias feeding BN, fall to the floor)."""
+    got = np.asarray(got, np.float64)
+    want = np.asarray(want, np.float64)
+    scale = np.linalg.norm(want) / np.sqrt(max(want.size, 1))
+    bad, worst, o = [], {}, 0
+    for s in specs:
+        n = int(np.prod(s.shape))
+        g, w = got[o:o + n], want[o:o + n]
+        o += n
+        err = np.linalg.norm(g - w)
+        lim = tol * np.linalg.norm(w) + floor_frac * tol * scale * np.sqrt(n)
+        worst[s.name] = err / max(np.linalg.norm(w), 1e-30)
+        if not err <= lim:
+            bad.append((s.name, float(err), float(lim), worst[s.name]))
+    if with_u:
+        for s in specs:
+            if s.sn:
+                n = s.shape[0]
+                g, w = got[o:o + n], want[o:o + n]
+                o += n
+                e = np.linalg.norm(g - w) / max(np.linalg.norm(w), 1e-30)
+                worst["u:" + s.name] = e
+                if e > tol:
+                    bad.append(("u:" + s.name, float(e), tol, e))
+    return bad, worst
+
+
+def adam_sign_agreement(p0, p1_got, p1_want, n):
+    dg = np.asarray(p1_got[:n], np.float64) - p0[:n]
+    dw = np.asarray(p1_want[:n], np.float64) - p0[:n]
+    m = dw != 0
+    return float(np.mean(np.sign(dg[m]) == np.sign(dw[m]))) if m.any() else 1.0

@@ -1,0 +1,63 @@
+"""C-ABI boundary on CPU: the library loads, exports every symbol include/paragan.h
+declares, validates configs, and its parameter layout agrees with the oracle's
+independently written one (no GPU needed: these calls do not touch CUDA)."""
+import os
+import re
+
+import pytest
+
+from oracle import biggan as bg
+from paragan_b200 import api
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    with open(os.path.join(ROOT, "include", "paragan.h")) as f:
+        src = f.read()
+    return sorted(set(re.findall(r"\b(paragan_[a-z_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    L = api.lib()
+    names = _declared()
+    assert "paragan_d_step" in names and "paragan_layout_pack" in names
+    for n in names:
+        assert hasattr(L, n), n
+    assert set(names) <= set(api.SYMBOLS), set(names) - set(api.SYMBOLS)
+
+
+@pytest.mark.parametrize("res,ch,attn", [(128, 96, 64), (32, 8, 16), (16, 8, 8), (256, 96, 64), (512, 96, 64),
+                                         (64, 16, 32)])
+def test_param_layout_matches_oracle(res, ch, attn):
+    ocfg = bg.Config(resolution=res, ch=ch, attn_res=attn)
+    cfg = api.make_config(resolution=res, ch=ch, attn_res=attn, local_batch=2)
+    for net, specs in ((api.NET_G, bg.g_param_specs(ocfg)), (api.NET_D, bg.d_param_specs(ocfg))):
+        ns, nt = api.param_count(cfg, net)
+        assert nt == bg.n_trainable(specs)
+        assert ns == bg.n_state(specs)
+
+
+def test_biggan128_total_is_paper_count():
+    cfg = api.make_config()
+    tot = api.param_count(cfg, api.NET_G)[1] + api.param_count(cfg, api.NET_D)[1]
+    assert tot == 158_416_358   # "158.42M"
+
+
+def test_config_validation():
+    bad = [dict(resolution=100), dict(ch=3), dict(local_batch=0), dict(d_steps_per_g=0), dict(c_pad_image=4),
+           dict(rank=2, world_size=2), dict(attn_res=48)]
+    for kw in bad:
+        cfg = api.make_config(**kw)
+        with pytest.raises(api.ParaganError) as e:
+            api.workspace_size(cfg)
+        assert e.value.status == 2, kw
+    cfg = api.make_config()
+    cfg.abi_version = 99
+    with pytest.raises(api.ParaganError):
+        api.workspace_size(cfg)
+
+
+def test_workspace_fits_b200_at_paper_config():
+    n = api.workspace_size(api.make_config(local_batch=256))
+    assert 1e9 < n < 170e9

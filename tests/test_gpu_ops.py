@@ -1,0 +1,146 @@
+"""Kernel-level parity through the C-ABI: layout pack (bit-exact), tcgen05 conv
+fprop/dgrad-shaped/wgrad on integer-valued inputs (bit-exact: every partial sum is
+an exact fp32 integer) and on random inputs, SIMT fp32 conv."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import ops
+from paragan_b200 import api
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+
+def _bf16_np(a):
+    return torch.from_numpy(np.asarray(a, np.float32)).to(torch.bfloat16)
+
+
+@pytest.mark.parametrize("n,c,h,w,cp", [(2, 3, 5, 7, 8), (4, 3, 128, 128, 8), (1, 3, 1, 1, 8), (3, 5, 9, 4, 16)])
+def test_layout_pack_bit_exact(n, c, h, w, cp):
+    rng = np.random.default_rng(n * 100 + h)
+    x = rng.uniform(-1, 1, size=(n, c, h, w)).astype(np.float32)
+    x.flat[0] = 0.5 + 2 ** -9          # a bf16 tie (rounds to even)
+    xs = torch.from_numpy(x).to(DEV)
+    for dt, tdt in ((api.BF16, torch.bfloat16), (api.F32, torch.float32)):
+        y = torch.full((n, h, w, cp), 7.0, dtype=tdt, device=DEV)   # pads must be overwritten with 0
+        api.layout_pack(xs, y, dt, cp)
+        torch.cuda.synchronize()
+        want = ops.layout_pack(x, cp, dt == api.BF16)
+        got = y.float().cpu().numpy()
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+        back = torch.empty((n, c, h, w), dtype=torch.float32, device=DEV)
+        api.layout_unpack(y, dt, back, cp)
+        torch.cuda.synchronize()
+        assert np.array_equal(back.cpu().numpy(), ops.layout_unpack(want, c))
+
+
+def test_layout_pack_rejects_bad_args():
+    x = torch.zeros((1, 3, 4, 4), device=DEV)
+    y = torch.zeros((1, 4, 4, 4), dtype=torch.bfloat16, device=DEV)
+    with pytest.raises(api.ParaganError) as e:
+        api.layout_pack(x, y, api.BF16, 4)     # bf16 needs c_pad % 8 == 0
+    assert e.value.status == 1
+
+
+CONV_SHAPES = [  # n, h, w, cin, cout, k
+    (2, 8, 8, 64, 128, 3),
+    (3, 16, 16, 96, 96, 3),      # 96-channel tail chunk
+    (1, 4, 4, 8, 32, 3),         # M < 128 (ragged single tile), tiny C
+    (2, 128, 128, 8, 96, 3),     # RGB-padded first D layer geometry
+    (1, 32, 256, 16, 16, 3),     # W > 128: row-segment tiles
+    (5, 32, 32, 192, 384, 1),    # 1x1
+    (2, 64, 64, 192, 24, 1),     # attention-sized N tail
+    (3, 8, 8, 1536, 256, 3),     # deep layer, several K chunks
+    (1, 12, 12, 32, 48, 3),      # M not a multiple of 128
+]
+
+
+def _int_inputs(rng, n, h, w, cin, cout, k):
+    x = rng.integers(-2, 3, size=(n, h, w, cin)).astype(np.float32)
+    wt = rng.integers(-1, 2, size=(cout, k * k, cin)).astype(np.float32)
+    b = rng.integers(-3, 4, size=(cout,)).astype(np.float32)
+    return x, wt, b
+
+
+def _oracle_conv(x_nhwc, w_otc, b, k):
+    x = torch.from_numpy(x_nhwc).double().permute(0, 3, 1, 2)
+    cout, _, cin = w_otc.shape
+    w = torch.from_numpy(w_otc).double().reshape(cout, k, k, cin).permute(0, 3, 1, 2)
+    y = ops.conv2d(x, w, torch.from_numpy(b).double() if b is not None else None)
+    return y.permute(0, 2, 3, 1).numpy()
+
+
+@pytest.mark.parametrize("shape", CONV_SHAPES)
+def test_tc_conv_fprop_integer_exact(shape):
+    n, h, w, cin, cout, k = shape
+    rng = np.random.default_rng(hash(shape) % 2**32)
+    x, wt, b = _int_inputs(rng, n, h, w, cin, cout, k)
+    want = ops.bf16_round(torch.from_numpy(_oracle_conv(x, wt, b, k))).float().numpy()
+    xd, wd = _bf16_np(x).to(DEV), _bf16_np(wt).to(DEV)
+    bd = torch.from_numpy(b).to(DEV)
+    y = torch.full((n, h, w, cout), float("nan"), dtype=torch.bfloat16, device=DEV)
+    api.op_conv_fwd(api.BF16, xd, wd, bd, cout, k, y)
+    torch.cuda.synchronize()
+    got = y.float().cpu().numpy()
+    assert np.array_equal(got, want), np.argwhere(got != want)[:5]
+
+
+@pytest.mark.parametrize("shape", CONV_SHAPES)
+def test_tc_conv_wgrad_integer_exact(shape):
+    n, h, w, cin, cout, k = shape
+    if cout % 8:
+        pytest.skip("wgrad needs C_out % 8")
+    rng = np.random.default_rng(hash(shape) % 2**31 + 1)
+    x = rng.integers(-2, 3, size=(n, h, w, cin)).astype(np.float32)
+    dy = rng.integers(-2, 3, size=(n, h, w, cout)).astype(np.float32)
+    # oracle: dW = d/dW <conv(x, W), dy>  (autograd of the plain conv)
+    xt = torch.from_numpy(x).double().permute(0, 3, 1, 2)
+    wv = torch.zeros(cout, cin, k, k, dtype=torch.float64, requires_grad=True)
+    (gw,) = torch.autograd.grad((ops.conv2d(xt, wv, None) * torch.from_numpy(dy).double().permute(0, 3, 1, 2)).sum(), wv)
+    want = gw.permute(0, 2, 3, 1).reshape(cout, k * k, cin).numpy().astype(np.float32)
+    assert np.abs(want).max() < 2 ** 24
+    dw = torch.full((cout, k * k, cin), float("nan"), dtype=torch.float32, device=DEV)
+    api.op_conv_wgrad(api.BF16, _bf16_np(x).to(DEV), _bf16_np(dy).to(DEV), cout, k, dw)
+    torch.cuda.synchronize()
+    got = dw.cpu().numpy()
+    assert np.array_equal(got, want), np.argwhere(got != want)[:5]
+
+
+@pytest.mark.parametrize("shape", CONV_SHAPES[:4])
+def test_tc_conv_random_within_bf16_accumulation_error(shape):
+    n, h, w, cin, cout, k = shape
+    rng = np.random.default_rng(7)
+    x = ops.bf16_round(torch.from_numpy(rng.standard_normal((n, h, w, cin)).astype(np.float32))).float().numpy()
+    wt = ops.bf16_round(torch.from_numpy(rng.standard_normal((cout, k * k, cin)).astype(np.float32) * 0.05)).float().numpy()
+    want = _oracle_conv(x, wt, None, k)
+    y = torch.empty((n, h, w, cout), dtype=torch.bfloat16, device=DEV)
+    api.op_conv_fwd(api.BF16, _bf16_np(x).to(DEV), _bf16_np(wt).to(DEV), None, cout, k, y)
+    torch.cuda.synchronize()
+    got = y.float().cpu().numpy()
+    # only the final bf16 rounding (2^-9 relative) plus fp32 accumulation
+    err = np.linalg.norm(got - want) / np.linalg.norm(want)
+    assert err < 4e-3
+
+
+@pytest.mark.parametrize("shape", [(2, 8, 8, 16, 24, 3), (1, 5, 7, 3, 8, 3), (2, 6, 6, 96, 3, 3), (3, 4, 4, 40, 70, 1)])
+def test_simt_conv_f32(shape):
+    n, h, w, cin, cout, k = shape
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((n, h, w, cin)).astype(np.float32)
+    wt = rng.standard_normal((cout, k * k, cin)).astype(np.float32)
+    b = rng.standard_normal(cout).astype(np.float32)
+    want = _oracle_conv(x, wt, b, k)
+    y = torch.empty((n, h, w, cout), dtype=torch.float32, device=DEV)
+    api.op_conv_fwd(api.F32, torch.from_numpy(x).to(DEV), torch.from_numpy(wt).to(DEV), torch.from_numpy(b).to(DEV),
+                    cout, k, y)
+    dy = rng.standard_normal((n, h, w, cout)).astype(np.float32)
+    dw = torch.empty((cout, k * k, cin), dtype=torch.float32, device=DEV)
+    api.op_conv_wgrad(api.F32, torch.from_numpy(x).to(DEV), torch.from_numpy(dy).to(DEV), cout, k, dw)
+    torch.cuda.synchronize()
+    assert np.linalg.norm(y.cpu().numpy() - want) <= 1e-5 * np.linalg.norm(want)
+    xt = torch.from_numpy(x).double().permute(0, 3, 1, 2)
+    wv = torch.zeros(cout, cin, k, k, dtype=torch.float64, requires_grad=True)
+    (gw,) = torch.autograd.grad((ops.conv2d(xt, wv, None) * torch.from_numpy(dy).double().permute(0, 3, 1, 2)).sum(), wv)
+    wantw = gw.permute(0, 2, 3, 1).reshape(cout, k * k, cin).numpy()
+    assert np.linalg.norm(dw.cpu().numpy() - wantw) <= 1e-5 * np.linalg.norm(wantw)
