@@ -294,18 +294,17 @@ def d_forward(cfg: Config, sn: _SN, x: torch.Tensor, y: torch.Tensor) -> torch.T
         pre = f"b{j}."
         a = h if j == 0 else q(torch.relu(h), bf)
         a = q(ops.conv2d(a, _qw(sn, pre + "conv1.w"), p[pre + "conv1.b"]), bf)
-        a = ops.conv2d(q(torch.relu(a), bf), _qw(sn, pre + "conv2.w"), p[pre + "conv2.b"])
-        if dn:
-            a = ops.avgpool2(q(a, bf))
-        if ci != co or dn:
-            if j == 0:   # block 0 (no pre-activation): pool, then 1x1 conv
-                s = ops.conv2d(q(ops.avgpool2(h), bf), _qw(sn, pre + "sc.w"), p[pre + "sc.b"])
-            else:        # later blocks: 1x1 conv, then pool
-                s = ops.avgpool2(q(ops.conv2d(h, _qw(sn, pre + "sc.w"), p[pre + "sc.b"]), bf)) if dn \
-                    else ops.conv2d(h, _qw(sn, pre + "sc.w"), p[pre + "sc.b"])
+        c2 = ops.conv2d(q(torch.relu(a), bf), _qw(sn, pre + "conv2.w"), p[pre + "conv2.b"])
+        learn = ci != co or dn
+        if dn and j == 0:
+            # block 0 (no pre-activation): pool the image, then the 1x1 skip conv (R7)
+            s = q(ops.conv2d(q(ops.avgpool2(h), bf), _qw(sn, pre + "sc.w"), p[pre + "sc.b"]), bf)
+            h = q(ops.avgpool2(q(c2, bf)) + s, bf)
         else:
-            s = h
-        h = q(a + s, bf)
+            # later blocks: 1x1 skip conv, residual add, then pool (= pool of each branch, R7)
+            s = q(ops.conv2d(h, _qw(sn, pre + "sc.w"), p[pre + "sc.b"]), bf) if learn else h
+            t = q(c2 + s, bf)
+            h = q(ops.avgpool2(t), bf) if dn else t
         if att:
             h = _attention(cfg, sn, "attn.", h)
     feat = torch.relu(h).sum(dim=(2, 3))                       # fp32 head from here
@@ -377,7 +376,7 @@ def d_step(cfg: Config, G: NetState, D: NetState, real, real_y, z, fake_y, updat
     grads = {n: (g if g is not None else torch.zeros_like(dparams[n])).detach() for n, g in zip(names, gl)}
     D.params = {k: v.detach() for k, v in dparams.items()}
     ok = _adam(D, grads, cfg.adam_d) if update else True
-    return dict(loss=float(loss), logits=logits.detach().numpy(), fake=fake.detach().numpy(),
+    return dict(loss=float(loss.detach()), logits=logits.detach().numpy(), fake=fake.detach().numpy(),
                 grads=D.grad_flat(grads), applied=ok,
                 sigma_g=dict(sng.sigma), sigma_d=dict(snd.sigma),
                 d_real_mean=float(l_real.mean()), d_fake_mean=float(l_fake.mean()))
@@ -399,7 +398,7 @@ def g_step(cfg: Config, G: NetState, D: NetState, z, y, update: bool = True) -> 
     grads = {n: (g if g is not None else torch.zeros_like(gparams[n])).detach() for n, g in zip(names, gl)}
     G.params = {k: v.detach() for k, v in gparams.items()}
     ok = _adam(G, grads, cfg.adam_g) if update else True
-    return dict(loss=float(loss), logits=logits.detach().numpy(), fake=fake.detach().numpy(),
+    return dict(loss=float(loss.detach()), logits=logits.detach().numpy(), fake=fake.detach().numpy(),
                 grads=G.grad_flat(grads), applied=ok, sigma_g=dict(sng.sigma), sigma_d=dict(snd.sigma))
 
 
