@@ -233,7 +233,8 @@ class _SN:
         self.vectors[name] = (u_new, v)
         self.sigma[name] = sigma.detach().clone()
         w_hat = wt / sigma
-        return ops.bf16_round(w_hat) + (w_hat - w_hat.detach()) if (mma and self.bf16) else w_hat
+        # straight-through: the value is the bf16 operand, the gradient is d/dW_hat (fp32)
+        return ops.bf16_round(w_hat.detach()) + (w_hat - w_hat.detach()) if (mma and self.bf16) else w_hat
 
 
 def _qw(sn: _SN, name: str) -> torch.Tensor:

@@ -173,7 +173,8 @@ paragan_status paragan_op_conv_fwd(paragan_dtype dt, const void* x, int32_t n, i
     return PARAGAN_ERR_INVALID_ARG;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (dt == PARAGAN_BF16) {
-    if (cin % 8 || !aligned16(x) || !aligned16(wgt) || !aligned16(y)) return PARAGAN_ERR_INVALID_ARG;
+    if (cin % 8 || !aligned16(x) || !aligned16(wgt) || !aligned16(y) || !tc_geometry_ok(h, w))
+      return PARAGAN_ERR_INVALID_ARG;
     TcEpilogue e;
     e.bias = bias;
     e.out = y;
@@ -192,7 +193,7 @@ paragan_status paragan_op_conv_wgrad(paragan_dtype dt, const void* x, const void
     return PARAGAN_ERR_INVALID_ARG;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (dt == PARAGAN_BF16) {
-    if (cin % 8 || cout % 8 || !aligned16(x) || !aligned16(dy)) return PARAGAN_ERR_INVALID_ARG;
+    if (cin % 8 || cout % 8 || !aligned16(x) || !aligned16(dy) || !tc_geometry_ok(h, w)) return PARAGAN_ERR_INVALID_ARG;
     const size_t out = (size_t)cout * ksz * ksz * cin;
     const size_t scratch_n = out * 64;
     float* scratch = nullptr;

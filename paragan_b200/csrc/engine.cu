@@ -670,7 +670,7 @@ class Engine final : public EngineBase {
     h0f_ = A.get<float>((size_t)B * 16 * c0_);
     for (auto& b : gb_) {
       const int H = b.hin;
-      b.x = act(B, H, H, b.cin);
+      b.x = (&b == &gb_[0]) ? act(B, H, H, b.cin) : nullptr;   // later blocks read the previous output in place
       b.u1 = act(B, 2 * H, 2 * H, b.cin);
       b.h1 = act(B, 2 * H, 2 * H, b.cout);
       b.a2 = act(B, 2 * H, 2 * H, b.cout);
@@ -689,7 +689,6 @@ class Engine final : public EngineBase {
       b.sums1 = A.get<double>(2 * b.cin);
       b.sums2 = A.get<double>(2 * b.cout);
     }
-    gout_in_ = act(B, R_, R_, cl_);   // input of the output BN (= last block output or attention output)
     aout_ = A.get<float>((size_t)B * R_ * R_ * cl_);   // fp32 output-BN activation
     omean_ = A.get<float>(cl_);
     orstd_ = A.get<float>(cl_);
@@ -778,6 +777,9 @@ class Engine final : public EngineBase {
       N->pf_start = A.get<long long>(64 + N->sn_entries.size() * 2);
       N->pb_start = A.get<long long>(64 + N->sn_entries.size() * 2);
     }
+    // chain G block inputs (block i+1 reads block i's output, or the attention output, in place)
+    for (size_t i = 1; i < gb_.size(); ++i) gb_[i].x = gb_[i - 1].attn ? attn_out_[0] : gb_[i - 1].out;
+    gout_in_ = gb_.back().attn ? attn_out_[0] : gb_.back().out;
     // chain D block inputs
     void* prev = dimg_;
     for (auto& b : db_) {
@@ -1099,8 +1101,6 @@ class Engine final : public EngineBase {
         CKS(attn_forward(G_, gattn_, out, B, attn_out_[0]));
         out = attn_out_[0];
       }
-      void* next = (i + 1 < gb_.size()) ? gb_[i + 1].x : gout_in_;
-      CK(cudaMemcpyAsync(next, out, sizeof(T) * (size_t)B * H2 * H2 * b.cout, cudaMemcpyDeviceToDevice, st_));
     }
     // output layer in fp32: BN -> ReLU -> conv3x3 (96 -> 3) -> tanh
     const long long M = (long long)B * R_ * R_;

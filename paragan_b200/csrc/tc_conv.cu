@@ -475,13 +475,26 @@ int pick_bn(int cout) {
   return 128;
 }
 
+// The 128-pixel M tile must be one TMA box {bw, bh, bn} in pixel order:
+// W a power of two, and either W >= 128 (row segments) or whole rows that tile H
+// (or whole images when H*W < 128).
+bool tileable(int H, int W) {
+  auto pow2 = [](int v) { return v > 0 && (v & (v - 1)) == 0; };
+  if (!pow2(W) || H < 1) return false;
+  if (W >= 128) return true;
+  const int rows = 128 / W;
+  if (H >= rows) return H % rows == 0;
+  return pow2(H);
+}
+
 }  // namespace
 
 int tc_fprop_bn(int cout) { return pick_bn(cout); }
+bool tc_geometry_ok(int H, int W) { return tileable(H, W); }
 
 cudaError_t tc_conv_fprop(const void* x, int N, int H, int W, int Cin, const void* wpack, int Cout, int ksz,
                           const TcEpilogue& epi, cudaStream_t st) {
-  if (Cin % 8 || ((uintptr_t)x & 15) || ((uintptr_t)wpack & 15)) return cudaErrorInvalidValue;
+  if (Cin % 8 || ((uintptr_t)x & 15) || ((uintptr_t)wpack & 15) || !tileable(H, W)) return cudaErrorInvalidValue;
   CUtensorMap ma, mb;
   const int bn = pick_bn(Cout);
   PG_CUDA(act_map(&ma, x, N, H, W, Cin));
@@ -523,7 +536,8 @@ size_t tc_wgrad_workspace_floats(int N, int H, int W, int Cin, int Cout, int ksz
 
 cudaError_t tc_conv_wgrad(const void* x, const void* dy, int N, int H, int W, int Cin, int Cout, int ksz,
                           float* dw, int accumulate, float* scratch, size_t scratch_floats, cudaStream_t st) {
-  if (Cin % 8 || Cout % 8 || ((uintptr_t)x & 15) || ((uintptr_t)dy & 15)) return cudaErrorInvalidValue;
+  if (Cin % 8 || Cout % 8 || ((uintptr_t)x & 15) || ((uintptr_t)dy & 15) || !tileable(H, W))
+    return cudaErrorInvalidValue;
   int bn;
   if (Cin % 256 == 0) bn = 256;
   else if (Cin % 192 == 0) bn = 192;

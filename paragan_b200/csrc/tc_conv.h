@@ -45,5 +45,7 @@ cudaError_t tc_conv_wgrad(const void* x, const void* dy, int N, int H, int W, in
 
 size_t tc_wgrad_workspace_floats(int N, int H, int W, int Cin, int Cout, int ksz);
 int tc_fprop_bn(int cout);
+// true when an H x W image tiles into 128-pixel TMA boxes (see tc_conv.cu)
+bool tc_geometry_ok(int H, int W);
 
 }  // namespace pg

@@ -35,6 +35,15 @@ def test_layout_pack_bit_exact(n, c, h, w, cp):
         assert np.array_equal(back.cpu().numpy(), ops.layout_unpack(want, c))
 
 
+def test_tc_conv_rejects_untileable_geometry():
+    x = torch.zeros((1, 12, 12, 32), dtype=torch.bfloat16, device=DEV)
+    w = torch.zeros((48, 9, 32), dtype=torch.bfloat16, device=DEV)
+    y = torch.zeros((1, 12, 12, 48), dtype=torch.bfloat16, device=DEV)
+    with pytest.raises(api.ParaganError) as e:
+        api.op_conv_fwd(api.BF16, x, w, None, 48, 3, y)
+    assert e.value.status == 1
+
+
 def test_layout_pack_rejects_bad_args():
     x = torch.zeros((1, 3, 4, 4), device=DEV)
     y = torch.zeros((1, 4, 4, 4), dtype=torch.bfloat16, device=DEV)
@@ -52,7 +61,8 @@ CONV_SHAPES = [  # n, h, w, cin, cout, k
     (5, 32, 32, 192, 384, 1),    # 1x1
     (2, 64, 64, 192, 24, 1),     # attention-sized N tail
     (3, 8, 8, 1536, 256, 3),     # deep layer, several K chunks
-    (1, 12, 12, 32, 48, 3),      # M not a multiple of 128
+    (3, 8, 8, 32, 48, 3),        # M = 192: ragged last tile
+    (1, 2, 2, 16, 16, 1),        # M = 4
 ]
 
 
