@@ -366,7 +366,7 @@ __global__ void __launch_bounds__(192, 1)
       const int col0 = c0 + cbk;
       if (o >= a.Cout || col0 >= a.Cin) continue;
       float* op = a.out + (((long long)split * a.Cout + o) * a.taps + tap) * a.Cin + col0;
-      if (col0 + 32 <= a.Cin && (a.Cin & 3) == 0) {
+      if (col0 + 32 <= a.Cin && ((reinterpret_cast<uintptr_t>(op) & 15) == 0)) {
 #pragma unroll
         for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(op + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
       } else {

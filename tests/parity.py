@@ -105,8 +105,30 @@ def compare_tensors(specs, got, want, tol, floor_frac=1e-2, with_u=False):
     return bad, worst
 
 
-def adam_sign_agreement(p0, p1_got, p1_want, n):
+def compare_state(specs, got, want, g_oracle, tol, g_rel, with_u=True):
+    """Updated weights.  Adam's first step is ~ -lr * sign(g), so an element whose exact
+    gradient is below the arithmetic's noise (|g| < g_rel * RMS(g), e.g. a bias feeding a
+    BN) has an indeterminate update sign; those elements are excluded here and counted by
+    adam_sign_agreement instead (SURVEY §8(c) comparison rules)."""
+    got = np.asarray(got, np.float64)
+    want = np.asarray(want, np.float64)
+    g = np.asarray(g_oracle, np.float64)
+    n_tr = g.size
+    thr = g_rel * np.sqrt(np.mean(g ** 2))
+    keep = np.abs(g) >= thr
+    got_t = np.where(keep, got[:n_tr], want[:n_tr])
+    merged = np.concatenate([got_t, got[n_tr:]])
+    bad, worst = compare_tensors(specs, merged, want, tol, with_u=with_u)
+    return bad, worst, float(1.0 - keep.mean())
+
+
+def adam_sign_agreement(p0, p1_got, p1_want, n, g_oracle=None, g_rel=0.0):
+    """Fraction of updates with the oracle's sign, over elements whose exact gradient is
+    above the noise threshold g_rel * RMS(g) (the rest have no determinate sign)."""
     dg = np.asarray(p1_got[:n], np.float64) - p0[:n]
     dw = np.asarray(p1_want[:n], np.float64) - p0[:n]
     m = dw != 0
+    if g_oracle is not None:
+        g = np.asarray(g_oracle, np.float64)
+        m &= np.abs(g) >= g_rel * np.sqrt(np.mean(g ** 2))
     return float(np.mean(np.sign(dg[m]) == np.sign(dw[m]))) if m.any() else 1.0

@@ -1,0 +1,56 @@
+"""Per-tensor parity report of one iteration: CUDA path vs the oracle (bf16-emulating
+and plain fp64).  Diagnostic tool; tests/test_gpu_step.py holds the pass/fail bars.
+
+    python tools/parity_report.py [--res 32 --ch 4 --attn 16 --classes 10 --shared 16 --zc 4 --batch 4 --bf16]
+"""
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--res", type=int, default=32)
+    ap.add_argument("--ch", type=int, default=4)
+    ap.add_argument("--attn", type=int, default=16)
+    ap.add_argument("--classes", type=int, default=10)
+    ap.add_argument("--shared", type=int, default=16)
+    ap.add_argument("--zc", type=int, default=4)
+    ap.add_argument("--batch", type=int, default=4)
+    ap.add_argument("--seed", type=int, default=23)
+    ap.add_argument("--bf16", action="store_true")
+    a = ap.parse_args()
+    import numpy as np
+    from paragan_b200 import api
+    from tests import parity as P
+    compute = api.BF16 if a.bf16 else api.F32
+    cfg = api.make_config(resolution=a.res, ch=a.ch, attn_res=a.attn, n_classes=a.classes, shared_dim=a.shared,
+                          z_chunk=a.zc, local_batch=a.batch, compute=compute)
+    res = {}
+    for emu in ([True, False] if a.bf16 else [False]):
+        o = P.oracle_config(a.res, a.ch, a.attn, a.classes, a.shared, a.zc, bf16=emu)
+        gs, ds, g0, d0, dbs, gb = P.make_inputs(o, a.batch, a.seed)
+        res[emu] = P.run_oracle(o, gs, ds, g0, d0, dbs, gb)
+    got = P.run_gpu(cfg, g0, d0, dbs, gb)
+    print(f"losses gpu d={got['d_loss']:.6f} g={got['g_loss']:.6f}; oracle " +
+          " ".join(f"[emu={k}] d={v['d_loss']:.6f} g={v['g_loss']:.6f}" for k, v in res.items()))
+    for key, specs in (("d_grads", ds), ("g_grads", gs)):
+        print(f"\n{key}: tensor | rel err vs " + " | ".join(f"emu={k}" for k in res) + " | emu vs plain")
+        o = 0
+        for s in specs:
+            n = int(np.prod(s.shape))
+            row = []
+            for k in res:
+                row.append(P.rel(got[key][o:o + n], res[k][key][o:o + n]))
+            extra = ""
+            if len(res) == 2:
+                extra = f" | {P.rel(res[True][key][o:o + n], res[False][key][o:o + n]):.2e}"
+            print(f"  {s.name:22s} " + " ".join(f"{r:.2e}" for r in row) + extra)
+            o += n
+
+
+if __name__ == "__main__":
+    main()
