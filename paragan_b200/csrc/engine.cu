@@ -58,8 +58,14 @@ struct Net {
   float *sn_v = nullptr, *sn_t = nullptr, *sn_s = nullptr, *sigma = nullptr;
   std::vector<int> sn_entries;                // entry index per SN job
   SnJob* jobs_d = nullptr;
-  int *b1_job = nullptr, *b1_k0 = nullptr, *b2_job = nullptr, *b2_r0 = nullptr;
-  int nb1 = 0, nb2 = 0;
+  int *b1_job = nullptr, *b1_k0 = nullptr, *b1_rc = nullptr, *b1b_job = nullptr, *b1b_k0 = nullptr;
+  int *b2_job = nullptr, *b2_r0 = nullptr;
+  int nb1 = 0, nb1b = 0, nb2 = 0;
+  float* sn_part = nullptr;
+  long long npart = 0;
+  double *sn_coef = nullptr, *sn_dotp = nullptr;
+  long long* snb_start = nullptr;
+  long long snb_blocks = 0;
   std::vector<SnPack> pf_h, pb_h;             // fwd packs, dgrad packs
   SnPack *pf_d = nullptr, *pb_d = nullptr;
   long long *pf_start = nullptr, *pb_start = nullptr;
@@ -731,6 +737,10 @@ class Engine final : public EngineBase {
       }
       tmp_attn_dO_ = A.get<char>((size_t)std::max(mdo, 1LL) * sizeof(T));
       tmp_attn_dqkv_ = A.get<char>((size_t)std::max(mdq, 1LL) * sizeof(T));
+      long long mdp = 1;
+      for (AttnL* at : {&gattn_, &dattn_})
+        if (at->C) mdp = std::max(mdp, (long long)((at == &gattn_) ? B : B2) * at->H * at->H * (at->H * at->H / 4));
+      dP_ = A.get<float>((size_t)mdp);
       dxp_ = A.get<char>((size_t)B2 * (R_ / 2) * (R_ / 2) * cpad_ * sizeof(T));
     }
     maxc_ = 8;
@@ -758,18 +768,33 @@ class Engine final : public EngineBase {
     // tables
     for (Net* N : {&G_, &D_}) {
       N->jobs_d = A.get<SnJob>(N->sn_entries.size());
-      long long nb1 = 0, nb2 = 0;
+      long long nb1 = 0, nb1b = 0, nb2 = 0, npart = 0, nbw = 0;
       for (int ei : N->sn_entries) {
         const PEntry& e = N->E[ei];
-        nb1 += ceil_div(e.n / e.shape[0], 256);
+        const long long K = e.n / e.shape[0];
+        const int nrc = ceil_div(e.shape[0], 128);
+        nb1 += ceil_div(K, 256) * nrc;
+        nb1b += ceil_div(K, 256);
         nb2 += ceil_div(e.shape[0], 8);
+        npart += nrc * K;
+        nbw += ceil_div(e.n, 4096);
       }
       N->nb1 = (int)nb1;
+      N->nb1b = (int)nb1b;
       N->nb2 = (int)nb2;
+      N->npart = npart;
+      N->snb_blocks = nbw;
       N->b1_job = A.get<int>(nb1);
       N->b1_k0 = A.get<int>(nb1);
+      N->b1_rc = A.get<int>(nb1);
+      N->b1b_job = A.get<int>(nb1b);
+      N->b1b_k0 = A.get<int>(nb1b);
       N->b2_job = A.get<int>(nb2);
       N->b2_r0 = A.get<int>(nb2);
+      N->sn_part = A.get<float>(npart);
+      N->sn_coef = A.get<double>(N->sn_entries.size());
+      N->sn_dotp = A.get<double>(nbw);
+      N->snb_start = A.get<long long>(N->sn_entries.size());
       N->snb_idx = A.get<int>(N->sn_entries.size());
       N->snb_grad = A.get<float*>(N->sn_entries.size());
       N->pf_d = A.get<SnPack>(64 + N->sn_entries.size() * 2);
@@ -794,11 +819,12 @@ class Engine final : public EngineBase {
   paragan_status upload_tables() {
     for (Net* N : {&G_, &D_}) {
       std::vector<SnJob> jobs;
-      std::vector<int> b1j, b1k, b2j, b2r, sidx;
-      std::vector<float*> sgrad;
+      std::vector<int> b1j, b1k, b1r, b1bj, b1bk, b2j, b2r;
+      std::vector<long long> bstart;
+      long long part_off = 0, bw = 0;
       for (int ei : N->sn_entries) {
         const PEntry& e = N->E[ei];
-        SnJob j;
+        SnJob j{};
         j.w = N->p + e.off;
         j.u = N->u + e.u_off;
         j.v = N->sn_v + e.v_off;
@@ -807,20 +833,35 @@ class Engine final : public EngineBase {
         j.sigma = N->sigma + 2 * e.job;
         j.rows = e.shape[0];
         j.K = (int)(e.n / e.shape[0]);
+        j.nrc = ceil_div(j.rows, 128);
+        j.part = N->sn_part + part_off;
+        part_off += (long long)j.nrc * j.K;
+        j.grad = N->g + e.off;
         const int ji = (int)jobs.size();
-        for (int k = 0; k < j.K; k += 256) { b1j.push_back(ji); b1k.push_back(k); }
+        j.coef = N->sn_coef + ji;
+        j.bwd_blk0 = bw;
+        j.bwd_nblk = ceil_div(e.n, 4096);
+        bstart.push_back(bw);
+        bw += j.bwd_nblk;
+        for (int rc = 0; rc < j.nrc; ++rc)
+          for (int k = 0; k < j.K; k += 256) { b1j.push_back(ji); b1k.push_back(k); b1r.push_back(rc); }
+        for (int k = 0; k < j.K; k += 256) { b1bj.push_back(ji); b1bk.push_back(k); }
         for (int r = 0; r < j.rows; r += 8) { b2j.push_back(ji); b2r.push_back(r); }
-        sidx.push_back(ji);
-        sgrad.push_back(N->g + e.off);
         jobs.push_back(j);
       }
-      CK(cudaMemcpyAsync(N->jobs_d, jobs.data(), jobs.size() * sizeof(SnJob), cudaMemcpyHostToDevice, st_));
-      CK(cudaMemcpyAsync(N->b1_job, b1j.data(), b1j.size() * sizeof(int), cudaMemcpyHostToDevice, st_));
-      CK(cudaMemcpyAsync(N->b1_k0, b1k.data(), b1k.size() * sizeof(int), cudaMemcpyHostToDevice, st_));
-      CK(cudaMemcpyAsync(N->b2_job, b2j.data(), b2j.size() * sizeof(int), cudaMemcpyHostToDevice, st_));
-      CK(cudaMemcpyAsync(N->b2_r0, b2r.data(), b2r.size() * sizeof(int), cudaMemcpyHostToDevice, st_));
-      CK(cudaMemcpyAsync(N->snb_idx, sidx.data(), sidx.size() * sizeof(int), cudaMemcpyHostToDevice, st_));
-      CK(cudaMemcpyAsync(N->snb_grad, sgrad.data(), sgrad.size() * sizeof(float*), cudaMemcpyHostToDevice, st_));
+      auto up = [&](void* dst, const void* src, size_t bytes) {
+        return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st_);
+      };
+      CK(up(N->jobs_d, jobs.data(), jobs.size() * sizeof(SnJob)));
+      CK(up(N->b1_job, b1j.data(), b1j.size() * sizeof(int)));
+      CK(up(N->b1_k0, b1k.data(), b1k.size() * sizeof(int)));
+      CK(up(N->b1_rc, b1r.data(), b1r.size() * sizeof(int)));
+      CK(up(N->b1b_job, b1bj.data(), b1bj.size() * sizeof(int)));
+      CK(up(N->b1b_k0, b1bk.data(), b1bk.size() * sizeof(int)));
+      CK(up(N->b2_job, b2j.data(), b2j.size() * sizeof(int)));
+      CK(up(N->b2_r0, b2r.data(), b2r.size() * sizeof(int)));
+      CK(up(N->snb_start, bstart.data(), bstart.size() * sizeof(long long)));
+      CK(cudaStreamSynchronize(st_));   // host vectors go out of scope
       jobs_h_[N == &G_ ? 0 : 1] = jobs;
     }
     // pack lists
@@ -910,7 +951,8 @@ class Engine final : public EngineBase {
         long long acc = 0;
         for (auto& j : lst) {
           st.push_back(acc);
-          acc += ceil_div((long long)j.rows * j.taps * j.cin, 256);
+          acc += pass == 0 ? ceil_div((long long)j.rows * j.taps * j.cin, 256)
+                           : (long long)j.taps * ceil_div(j.rows, 32) * ceil_div(j.cin, 32);
         }
         (pass == 0 ? N->pf_blocks : N->pb_blocks) = acc;
         CK(cudaMemcpyAsync(pass == 0 ? N->pf_d : N->pb_d, lst.data(), lst.size() * sizeof(SnPack),
@@ -924,14 +966,16 @@ class Engine final : public EngineBase {
 
   // ------------------------------------------------------------------ SN forward (A2)
   paragan_status sn_forward(Net& N, bool need_dgrad) {
-    CK(sn_power(N.jobs_d, (int)N.sn_entries.size(), N.b1_job, N.b1_k0, N.nb1, N.b2_job, N.b2_r0, N.nb2, st_));
-    launches_ += 2;
+    CK(sn_power(N.jobs_d, (int)N.sn_entries.size(), N.b1_job, N.b1_k0, N.b1_rc, N.nb1, N.b1b_job, N.b1b_k0, N.nb1b,
+                N.b2_job, N.b2_r0, N.nb2, st_));
+    launches_ += 3;
     CK(sn_pack(N.pf_d, N.pf_start, (int)N.pf_h.size(), N.pf_blocks, st_));
-    if (need_dgrad) CK(sn_pack(N.pb_d, N.pb_start, (int)N.pb_h.size(), N.pb_blocks, st_));
+    if (need_dgrad) CK(sn_pack_t(N.pb_d, N.pb_start, (int)N.pb_h.size(), N.pb_blocks, st_));
     return PARAGAN_OK;
   }
   paragan_status sn_backward_net(Net& N) {
-    CK(sn_backward(N.jobs_d, N.snb_idx, (int)N.sn_entries.size(), N.snb_grad, nullptr, st_));
+    CK(sn_backward(N.jobs_d, (int)N.sn_entries.size(), N.snb_start, N.snb_blocks, N.sn_dotp, st_));
+    launches_ += 2;
     return PARAGAN_OK;
   }
 
@@ -985,11 +1029,12 @@ class Engine final : public EngineBase {
   }
   // dx[n,H,H,cin_x] = alpha * dgrad(dy) (+ add)
   paragan_status conv_dgrad(const void* dy, int n, int H, const ConvL& c, void* dx, const void* add,
-                            const float* alpha = nullptr) {
+                            const float* alpha = nullptr, const void* relu_ref = nullptr) {
     if constexpr (kBF) {
       if (!c.f32) {
         TcEpilogue e;
         e.alpha = alpha;
+        e.relu_ref = relu_ref;
         e.residual = add;
         e.res_mode = add ? 1 : 0;
         e.out = dx;
@@ -1001,7 +1046,7 @@ class Engine final : public EngineBase {
     CK((simt_conv_fwd<float, float, float>(static_cast<const float*>(dy), n, H, H, c.cout,
                                            static_cast<const float*>(c.wt), c.cin_x, c.ksz, nullptr, alpha,
                                            static_cast<const float*>(add), add ? 1 : 0, static_cast<float*>(dx),
-                                           st_)));
+                                           st_, static_cast<const float*>(relu_ref))));
     return PARAGAN_OK;
   }
   // dW (into the net's grad slot, OHWI) = wgrad(x, dy)
@@ -1107,8 +1152,7 @@ class Engine final : public EngineBase {
     CKS(bn_forward_stats(gout_in_, M, cl_, osums_, omean_, orstd_));
     CK((bn_apply_relu<T, float>(static_cast<const T*>(gout_in_), B, R_, R_, cl_, omean_, orstd_, nullptr, nullptr,
                                 G_.P(obn_g_), G_.P(obn_b_), aout_, false, st_)));
-    CK((simt_conv_fwd<float, float, float>(aout_, B, R_, R_, cl_, static_cast<const float*>(oconv_.wp), 3, 3,
-                                           G_.P(oconv_.b), nullptr, nullptr, 0, pre_, st_)));
+    CK(thin_conv_fwd(aout_, B, R_, R_, cl_, static_cast<const float*>(oconv_.wp), 3, G_.P(oconv_.b), pre_, st_));
     CK(tanh_to_image<T>(pre_, img_, static_cast<T*>(dimg_), M, cpad_, st_));
     return PARAGAN_OK;
   }
@@ -1157,12 +1201,13 @@ class Engine final : public EngineBase {
       CK(scale_dev(go, (long long)a.C * a.C2, N.P(a.gamma), st_));
     }
     CKS(conv_dgrad(dout, n, H, a.oc, dO, nullptr, N.P(a.gamma)));   // dO = gamma * W_o^T dout
-    float* dP = a.S;   // reuse S
+    float* dP = dP_;
     // dgp = P^T dO  [n][Q][C2] fp32 ; dP = dO gp^T [n][HW][Q] fp32
     float* dgp = dpool_;
     CKS(bgemm(n, (int)Q, a.C2, (int)HW, a.P, HW * Q, 1, Q, dO, HW * a.C2, 1, a.C2, dgp, true, Q * a.C2, a.C2));
     CKS(bgemm(n, (int)HW, (int)Q, a.C2, dO, HW * a.C2, a.C2, 1, a.g_p, Q * a.C2, a.C2, 1, dP, true, HW * Q, Q));
-    CK(softmax_bwd_rows<T>(static_cast<const T*>(a.P), dP, M, (int)Q, static_cast<T*>(a.P), st_));  // P <- dS
+    // dS with P recomputed in fp32 from the kept scores (gradients kept in higher precision)
+    CK(softmax_bwd_rows<T>(a.S, dP, M, (int)Q, static_cast<T*>(a.P), st_));  // P <- dS
     const void* dS = a.P;
     CK(cudaMemsetAsync(dqkv, 0, sizeof(T) * (size_t)M * a.Ct, st_));
     // dtheta = dS phi_p -> dqkv[:, 0:C8]
@@ -1277,7 +1322,8 @@ class Engine final : public EngineBase {
       // conv2 backward
       const int ir1 = other(ic, it);
       void* dr1 = tmp(ir1);
-      CKS(conv_dgrad(dt, n, H, b.c2, dr1, nullptr));
+      // gradient at the conv1 output: dgrad(conv2) masked by relu'(c1) in the epilogue
+      CKS(conv_dgrad(dt, n, H, b.c2, dr1, nullptr, nullptr, b.r1));
       if (want_w) {
         CKS(conv_wgrad(D_, b.r1, dt, n, H, b.c2));
         CKS(bias_grad(D_, b.c2, dt, Mi));
@@ -1315,9 +1361,6 @@ class Engine final : public EngineBase {
         dskip = dt;   // identity skip
         isk = it;
       }
-      // relu between conv1 and conv2: dc1 = dr1 * [c1 > 0] (in place)
-      CK(relu_bwd<T>(static_cast<const T*>(dr1), static_cast<const T*>(b.r1), nullptr, static_cast<T*>(dr1),
-                     Mi * b.cout, st_));
       const void* cin = (j > 0) ? b.rx : b.x;
       if (want_w) {
         CKS(conv_wgrad(D_, cin, dr1, n, H, b.c1));
@@ -1329,10 +1372,8 @@ class Engine final : public EngineBase {
       for (int k = 0; k < 4; ++k)
         if (k != ir1 && k != isk) { ix = k; break; }
       void* dx = tmp(ix);
-      if (j > 0) {
-        CKS(conv_dgrad(dr1, n, H, b.c1, dx, nullptr));
-        CK(relu_bwd<T>(static_cast<const T*>(dx), static_cast<const T*>(b.x), static_cast<const T*>(dskip),
-                       static_cast<T*>(dx), Mi * b.cin_x, st_));
+      if (j > 0) {   // pre-activation block: relu'(x) mask and the skip gradient fused in the epilogue
+        CKS(conv_dgrad(dr1, n, H, b.c1, dx, dskip, nullptr, b.x));
       } else {
         CKS(conv_dgrad(dr1, n, H, b.c1, dx, dskip));
       }
@@ -1350,10 +1391,9 @@ class Engine final : public EngineBase {
     const long long M = (long long)B * R_ * R_;
     // tanh' and the fp32 output conv
     CK(tanh_bwd<T>(static_cast<const T*>(dimg_grad_), cpad_, img_, dpre_, M, st_));
-    CK((simt_conv_wgrad<float, float>(aout_, dpre_, B, R_, R_, cl_, 3, 3, G_.G(oconv_.w), 0, st_)));
+    CK(thin_conv_wgrad(aout_, dpre_, B, R_, R_, cl_, 3, G_.G(oconv_.w), scratch_f_, scratch_floats_, st_));
     CK(col_sum<float>(dpre_, M, 3, dpart_, kMaxPartialBlocks, G_.G(oconv_.b), 0, st_));
-    CK((simt_conv_fwd<float, float, float>(dpre_, B, R_, R_, 3, static_cast<const float*>(oconv_.wt), cl_, 3, nullptr,
-                                           nullptr, nullptr, 0, daout_, st_)));
+    CK(thin_conv_dgrad(dpre_, B, R_, R_, cl_, static_cast<const float*>(oconv_.wp), 3, daout_, st_));
     // output BN backward (plain BN, learned gamma/beta)
     int ic = (dimg_idx_ + 1) % 4;
     void* cur = tmp(ic);
@@ -1470,6 +1510,7 @@ class Engine final : public EngineBase {
   void* tmp_[4] = {};
   void* tmp_attn_dO_ = nullptr;
   void* dxp_ = nullptr;
+  float* dP_ = nullptr;
   bool prof_ = false;
   std::vector<ProfRec> recs_;
   std::vector<cudaEvent_t> ev_free_;

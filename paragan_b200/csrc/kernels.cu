@@ -490,7 +490,7 @@ __global__ void k_up2_bwd(const T* __restrict__ dy, int N, int H, int W, int C, 
     dx[i] = from_f<T>(s);
   }
 }
-// column sums with 8-channel vectors when C % 8 == 0, scalar otherwise
+// column sums: scalar path (any C) and an 8-channel-vector path (C % 8 == 0, C/8 <= 256)
 template <typename T>
 __global__ void __launch_bounds__(256) k_col_sum(const T* __restrict__ x, long long M, int C,
                                                  double* __restrict__ partial, long long pix_per_blk) {
@@ -498,7 +498,6 @@ __global__ void __launch_bounds__(256) k_col_sum(const T* __restrict__ x, long l
   const long long p0 = (long long)blockIdx.x * pix_per_blk;
   const long long p1 = min(M, p0 + pix_per_blk);
   for (int c0 = 0; c0 < C; c0 += 32) {
-    // 8 rows of 32 channels
     const int c = c0 + (threadIdx.x & 31);
     const int r = threadIdx.x >> 5;
     float s = 0.0f;
@@ -512,6 +511,32 @@ __global__ void __launch_bounds__(256) k_col_sum(const T* __restrict__ x, long l
       partial[(long long)blockIdx.x * C + c] = a;
     }
     __syncthreads();
+  }
+}
+template <typename T>
+__global__ void __launch_bounds__(256) k_col_sum_vec(const T* __restrict__ x, long long M, int C,
+                                                     double* __restrict__ partial, long long pix_per_blk) {
+  extern __shared__ float shs[];  // [R][C]
+  const int G = C >> 3, R = 256 / G;
+  const int g = threadIdx.x % G, r = threadIdx.x / G;
+  const long long p0 = (long long)blockIdx.x * pix_per_blk;
+  const long long p1 = min(M, p0 + pix_per_blk);
+  float s[8] = {};
+  if (r < R) {
+    for (long long p = p0 + r; p < p1; p += R) {
+      float v[8];
+      Vec8<T>::load(x + p * C + g * 8, v);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) s[j] += v[j];
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) shs[r * C + g * 8 + j] = s[j];
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < C; c += 256) {
+    double a = 0.0;
+    for (int rr = 0; rr < R; ++rr) a += shs[rr * C + c];
+    partial[(long long)blockIdx.x * C + c] = a;
   }
 }
 __global__ void k_reduce_partials_f32(const double* __restrict__ partial, int nblk, int width, float* __restrict__ out,
@@ -556,7 +581,8 @@ template <typename TI, typename TW, typename TO, int TM, int TN, int RM, int RN>
 __global__ void __launch_bounds__(256) k_simt_conv(const TI* __restrict__ x, int N, int H, int W, int Cin,
                                                    const TW* __restrict__ w, int Cout, int ksz,
                                                    const float* __restrict__ bias, const float* __restrict__ alpha,
-                                                   const TO* __restrict__ res, int res_mode, TO* __restrict__ y) {
+                                                   const TO* __restrict__ res, int res_mode, TO* __restrict__ y,
+                                                   const TO* __restrict__ relu_ref) {
   constexpr int KC = 8;
   __shared__ float As[KC][TM + 1];
   __shared__ float Bs[KC][TN + 1];
@@ -622,6 +648,7 @@ __global__ void __launch_bounds__(256) k_simt_conv(const TI* __restrict__ x, int
       const int o = n0 + tx * RN + j;
       if (o >= Cout) continue;
       float v = acc[i][j] * al;
+      if (relu_ref && !(to_f<TO>(relu_ref[m * Cout + o]) > 0.0f)) v = 0.0f;
       if (bias) v += bias[o];
       if (res) v += to_f<TO>(res[rb + o]);
       y[m * Cout + o] = from_f<TO>(v);
@@ -859,29 +886,54 @@ __global__ void k_softmax_rows(const float* __restrict__ S, long long rows, int 
   for (int j = lane; j < cols; j += 32) P[row * cols + j] = from_f<T>(__expf(s[j] - mx) * inv);
 }
 template <typename T>
-__global__ void k_softmax_bwd_rows(const T* __restrict__ P, const float* __restrict__ dP, long long rows, int cols,
+__global__ void k_softmax_bwd_rows(const float* __restrict__ S, const float* __restrict__ dP, long long rows, int cols,
                                    T* __restrict__ dS) {
   const long long row = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= rows) return;
-  float dot = 0.0f;
-  for (int j = lane; j < cols; j += 32) dot += to_f<T>(P[row * cols + j]) * dP[row * cols + j];
-  dot = warp_sum(dot);
+  const float* s = S + row * cols;
+  const float* d = dP + row * cols;
+  float mx = -INFINITY;
+  for (int j = lane; j < cols; j += 32) mx = fmaxf(mx, s[j]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  float sum = 0.0f, dot = 0.0f;
   for (int j = lane; j < cols; j += 32) {
-    const float p = to_f<T>(P[row * cols + j]);
-    dS[row * cols + j] = from_f<T>(p * (dP[row * cols + j] - dot));
+    const float e = __expf(s[j] - mx);
+    sum += e;
+    dot = fmaf(e, d[j], dot);
+  }
+  sum = warp_sum(sum);
+  dot = warp_sum(dot);
+  const float inv = 1.0f / sum;
+  dot *= inv;
+  for (int j = lane; j < cols; j += 32) {
+    const float p = __expf(s[j] - mx) * inv;
+    dS[row * cols + j] = from_f<T>(p * (d[j] - dot));
   }
 }
 
 // ===================================================================== SN
-// pass 1: t[k] = sum_r W[r][k] u[r]   (block = 256 columns of one job)
+// pass 1a: part[rc][k] = sum_{r in chunk rc} W[r][k] u[r]   (block = 256 columns x 128 rows of one job)
 __global__ void __launch_bounds__(256) k_sn_wtu(const SnJob* __restrict__ jobs, const int* __restrict__ blk_job,
-                                                const int* __restrict__ blk_k0) {
+                                                const int* __restrict__ blk_k0, const int* __restrict__ blk_rc) {
+  const SnJob j = jobs[blk_job[blockIdx.x]];
+  const int k = blk_k0[blockIdx.x] + threadIdx.x;
+  const int rc = blk_rc[blockIdx.x];
+  if (k >= j.K) return;
+  const int r0 = rc * 128, r1 = min(j.rows, r0 + 128);
+  float a = 0.0f;
+  for (int r = r0; r < r1; ++r) a = fmaf(j.w[(long long)r * j.K + k], j.u[r], a);
+  j.part[(long long)rc * j.K + k] = a;
+}
+// pass 1b: t[k] = sum_rc part[rc][k] (fixed order)
+__global__ void __launch_bounds__(256) k_sn_wtu_reduce(const SnJob* __restrict__ jobs, const int* __restrict__ blk_job,
+                                                       const int* __restrict__ blk_k0) {
   const SnJob j = jobs[blk_job[blockIdx.x]];
   const int k = blk_k0[blockIdx.x] + threadIdx.x;
   if (k >= j.K) return;
   float a = 0.0f;
-  for (int r = 0; r < j.rows; ++r) a = fmaf(j.w[(long long)r * j.K + k], j.u[r], a);
+  for (int rc = 0; rc < j.nrc; ++rc) a += j.part[(long long)rc * j.K + k];
   j.t[k] = a;
 }
 // pass 2: s[r] = sum_k W[r][k] t[k] / ||t||   (block = 8 rows, one warp per row)
@@ -962,30 +1014,90 @@ __global__ void __launch_bounds__(256) k_sn_pack(const SnPack* __restrict__ jobs
   if (J.dst_bf16) reinterpret_cast<bf16*>(J.dst)[d] = __float2bfloat16_rn(v);
   else reinterpret_cast<float*>(J.dst)[d] = v;
 }
-// SN backward: one block per weight (pass a: <g, W>; pass b: g = (g - <g,W>/sigma u v^T)/sigma)
-__global__ void __launch_bounds__(1024) k_sn_bwd(const SnJob* __restrict__ jobs, const int* __restrict__ idx,
-                                                 float* const* __restrict__ grads) {
-  const SnJob j = jobs[idx[blockIdx.x]];
-  float* g = grads[blockIdx.x];
+// dgrad-layout pack through a 32x32 shared-memory tile: reads W[o][t][c] along c,
+// writes Wt[c][T-1-t][o] along o (both coalesced).  One block = (job, t, o-tile, c-tile).
+__global__ void __launch_bounds__(256) k_sn_pack_t(const SnPack* __restrict__ jobs, const long long* __restrict__ blk_start,
+                                                   int n_jobs) {
+  __shared__ float tile[32][33];
+  int lo = 0, hi = n_jobs - 1;
+  const long long b = blockIdx.x;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (blk_start[mid] <= b) lo = mid; else hi = mid - 1;
+  }
+  const SnPack J = jobs[lo];
+  const int ot = (J.rows + 31) / 32, ct = (J.cin + 31) / 32;
+  long long r = b - blk_start[lo];
+  const int cti = (int)(r % ct);
+  r /= ct;
+  const int oti = (int)(r % ot);
+  const int t = (int)(r / ot);
+  const int o0 = oti * 32, c0 = cti * 32;
+  const float inv = J.sigma[1];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8
+  for (int k = ty; k < 32; k += 8) {
+    const int o = o0 + k, c = c0 + tx;
+    tile[k][tx] = (o < J.rows && c < J.cin) ? J.w[((long long)o * J.taps + t) * J.cin + c] * inv : 0.0f;
+  }
+  __syncthreads();
+  for (int k = ty; k < 32; k += 8) {
+    const int c = c0 + k, o = o0 + tx;
+    if (c < J.cin && o < J.rows) {
+      const long long d = ((long long)c * J.taps + (J.taps - 1 - t)) * J.dst_rows + (o + J.dst_row_offset);
+      const float v = tile[tx][k];
+      if (J.dst_bf16) reinterpret_cast<bf16*>(J.dst)[d] = __float2bfloat16_rn(v);
+      else reinterpret_cast<float*>(J.dst)[d] = v;
+    }
+  }
+}
+// SN backward, pass a: per-block fp64 partial of <g, W> over 4096 elements of one job
+__device__ __forceinline__ int find_job(const long long* __restrict__ start, int n, long long b) {
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (start[mid] <= b) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+__global__ void __launch_bounds__(256) k_snb_dot(const SnJob* __restrict__ jobs, const long long* __restrict__ start,
+                                                 int n_jobs, double* __restrict__ dotp) {
+  __shared__ double red[8];
+  const int ji = find_job(start, n_jobs, blockIdx.x);
+  const SnJob j = jobs[ji];
   const long long n = (long long)j.rows * j.K;
-  __shared__ double red[32];
-  __shared__ float s_c;
+  const long long e0 = (blockIdx.x - start[ji]) * 4096;
   double a = 0.0;
-  for (long long i = threadIdx.x; i < n; i += blockDim.x) a += (double)g[i] * (double)j.w[i];
+  for (long long i = e0 + threadIdx.x; i < min(n, e0 + 4096); i += 256) a += (double)j.grad[i] * (double)j.w[i];
   a = warp_sum_d(a);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
   __syncthreads();
   if (threadIdx.x == 0) {
     double t = 0.0;
-    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
-    // <G, W_hat> = <G, W>/sigma ; coefficient of u v^T in dW is <G, W_hat>/sigma
-    s_c = (float)(t * (double)j.sigma[1] * (double)j.sigma[1]);
+    for (int i = 0; i < 8; ++i) t += red[i];
+    dotp[blockIdx.x] = t;
   }
-  __syncthreads();
-  const float c = s_c, inv = j.sigma[1];
-  for (long long i = threadIdx.x; i < n; i += blockDim.x) {
-    const int r = (int)(i / j.K), k = (int)(i % j.K);
-    g[i] = g[i] * inv - c * j.u[r] * j.v[k];
+}
+// pass b: coef = <g, W> / sigma^2 (sum of the job's partials in block order)
+__global__ void k_snb_coef(const SnJob* __restrict__ jobs, int n_jobs, const double* __restrict__ dotp) {
+  const int ji = blockIdx.x * blockDim.x + threadIdx.x;
+  if (ji >= n_jobs) return;
+  const SnJob j = jobs[ji];
+  double t = 0.0;
+  for (long long b = 0; b < j.bwd_nblk; ++b) t += dotp[j.bwd_blk0 + b];
+  const double is = (double)j.sigma[1];
+  j.coef[0] = t * is * is;
+}
+// pass c: g = g / sigma - coef * u[r] * v[k]
+__global__ void __launch_bounds__(256) k_snb_apply(const SnJob* __restrict__ jobs, const long long* __restrict__ start,
+                                                   int n_jobs) {
+  const int ji = find_job(start, n_jobs, blockIdx.x);
+  const SnJob j = jobs[ji];
+  const long long n = (long long)j.rows * j.K;
+  const long long e0 = (blockIdx.x - start[ji]) * 4096;
+  const float c = (float)j.coef[0], inv = j.sigma[1];
+  for (long long i = e0 + threadIdx.x; i < min(n, e0 + 4096); i += 256) {
+    const int r = (int)(i / j.K), k = (int)(i - (long long)r * j.K);
+    j.grad[i] = j.grad[i] * inv - c * j.u[r] * j.v[k];
   }
 }
 
@@ -1098,6 +1210,106 @@ __global__ void k_copy_rows_cols(const float* __restrict__ src, long long lds, l
 __global__ void k_scale(float* p, long long n, float s) {
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     p[i] *= s;
+}
+
+// ---- 8-channel vector variants of the resampling kernels (C % 8 == 0, 16-byte rows)
+template <typename T>
+__global__ void k_relu_copy_v(const T* __restrict__ x, T* __restrict__ y, long long n8) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += (long long)gridDim.x * blockDim.x) {
+    float v[8];
+    Vec8<T>::load(x + i * 8, v);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = v[j] > 0.0f ? v[j] : 0.0f;
+    Vec8<T>::store(y + i * 8, v);
+  }
+}
+template <typename T>
+__global__ void k_avgpool2_v(const T* __restrict__ x, int N, int H, int W, int C, int ldx, const T* __restrict__ add,
+                             T* __restrict__ y) {
+  const int Ho = H >> 1, Wo = W >> 1, G = C >> 3;
+  const long long total = (long long)N * Ho * Wo * G;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int g = (int)(i % G);
+    long long p = i / G;
+    const int wo = (int)(p % Wo);
+    p /= Wo;
+    const int ho = (int)(p % Ho);
+    const int n = (int)(p / Ho);
+    const long long b = ((long long)n * H + 2 * ho) * W + 2 * wo;
+    float a0[8], a1[8], a2[8], a3[8], o[8];
+    Vec8<T>::load(x + b * ldx + g * 8, a0);
+    Vec8<T>::load(x + (b + 1) * ldx + g * 8, a1);
+    Vec8<T>::load(x + (b + W) * ldx + g * 8, a2);
+    Vec8<T>::load(x + (b + W + 1) * ldx + g * 8, a3);
+    float ad[8];
+    if (add) Vec8<T>::load(add + i * 8, ad);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      o[j] = ((a0[j] + a1[j]) + (a2[j] + a3[j])) * 0.25f;
+      if (add) o[j] += ad[j];
+    }
+    Vec8<T>::store(y + i * 8, o);
+  }
+}
+template <typename T>
+__global__ void k_avgpool2_bwd_v(const T* __restrict__ dy, int N, int H, int W, int C, const T* __restrict__ add,
+                                 T* __restrict__ dx, int lddx) {
+  // one thread per (output-grad pixel of the pooled map, 8 channels): writes its 2x2 block
+  const int Ho = H >> 1, Wo = W >> 1, G = C >> 3;
+  const long long total = (long long)N * Ho * Wo * G;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int g = (int)(i % G);
+    long long p = i / G;
+    const int wo = (int)(p % Wo);
+    p /= Wo;
+    const int ho = (int)(p % Ho);
+    const int n = (int)(p / Ho);
+    float v[8];
+    Vec8<T>::load(dy + i * 8, v);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] *= 0.25f;
+    const long long b = ((long long)n * H + 2 * ho) * W + 2 * wo;
+    const long long q[4] = {b, b + 1, b + W, b + W + 1};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      float o[8];
+      if (add) {
+        Vec8<T>::load(add + q[k] * C + g * 8, o);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o[j] += v[j];
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o[j] = v[j];
+      }
+      Vec8<T>::store(dx + q[k] * lddx + g * 8, o);
+    }
+  }
+}
+template <typename T>
+__global__ void k_up2_bwd_v(const T* __restrict__ dy, int N, int H, int W, int C, T* __restrict__ dx) {
+  const int G = C >> 3;
+  const long long total = (long long)N * H * W * G;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int g = (int)(i % G);
+    long long p = i / G;
+    const int w = (int)(p % W);
+    p /= W;
+    const int h = (int)(p % H);
+    const int n = (int)(p / H);
+    const long long W2 = 2 * W;
+    const long long b = ((long long)n * 2 * H + 2 * h) * W2 + 2 * w;
+    float a0[8], a1[8], a2[8], a3[8], o[8];
+    Vec8<T>::load(dy + b * C + g * 8, a0);
+    Vec8<T>::load(dy + (b + 1) * C + g * 8, a1);
+    Vec8<T>::load(dy + (b + W2) * C + g * 8, a2);
+    Vec8<T>::load(dy + (b + W2 + 1) * C + g * 8, a3);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j] = (a0[j] + a1[j]) + (a2[j] + a3[j]);
+    Vec8<T>::store(dx + i * 8, o);
+  }
 }
 
 }  // namespace
@@ -1278,10 +1490,14 @@ template cudaError_t bn_bwd_apply<bf16, float, bf16>(const bf16*, const float*, 
   template cudaError_t maxpool2_split_bwd<T>(const T*, int, int, int, int, int, int, const float*, T*,             \
                                              cudaStream_t);                                                        \
   template cudaError_t softmax_rows<T>(const float*, long long, int, T*, cudaStream_t);                            \
-  template cudaError_t softmax_bwd_rows<T>(const T*, const float*, long long, int, T*, cudaStream_t);
+  template cudaError_t softmax_bwd_rows<T>(const float*, const float*, long long, int, T*, cudaStream_t);
 
 template <typename T>
 cudaError_t relu_copy(const T* x, T* y, long long n, cudaStream_t st) {
+  if (n % 8 == 0 && !((uintptr_t)x & 15) && !((uintptr_t)y & 15)) {
+    k_relu_copy_v<T><<<grid_for(n / 8, 256), 256, 0, st>>>(x, y, n / 8);
+    return cudaGetLastError();
+  }
   k_relu_copy<T><<<grid_for(n, 256), 256, 0, st>>>(x, y, n);
   return cudaGetLastError();
 }
@@ -1293,18 +1509,30 @@ cudaError_t relu_bwd(const T* dy, const T* ref, const T* add, T* dx, long long n
 template <typename T>
 cudaError_t avgpool2(const T* x, int N, int H, int W, int C, int ldx, const T* add, T* y, cudaStream_t st) {
   const long long total = (long long)N * (H / 2) * (W / 2) * C;
+  if (C % 8 == 0 && ldx % 8 == 0) {
+    k_avgpool2_v<T><<<grid_for(total / 8, 256), 256, 0, st>>>(x, N, H, W, C, ldx, add, y);
+    return cudaGetLastError();
+  }
   k_avgpool2<T><<<grid_for(total, 256), 256, 0, st>>>(x, N, H, W, C, ldx, add, y);
   return cudaGetLastError();
 }
 template <typename T>
 cudaError_t avgpool2_bwd(const T* dy, int N, int H, int W, int C, const T* add, T* dx, int lddx, cudaStream_t st) {
   const long long total = (long long)N * H * W * C;
+  if (C % 8 == 0 && lddx % 8 == 0 && H % 2 == 0 && W % 2 == 0) {
+    k_avgpool2_bwd_v<T><<<grid_for(total / 32, 256), 256, 0, st>>>(dy, N, H, W, C, add, dx, lddx);
+    return cudaGetLastError();
+  }
   k_avgpool2_bwd<T><<<grid_for(total, 256), 256, 0, st>>>(dy, N, H, W, C, add, dx, lddx);
   return cudaGetLastError();
 }
 template <typename T>
 cudaError_t up2_bwd(const T* dy, int N, int H, int W, int C, T* dx, cudaStream_t st) {
   const long long total = (long long)N * H * W * C;
+  if (C % 8 == 0) {
+    k_up2_bwd_v<T><<<grid_for(total / 8, 256), 256, 0, st>>>(dy, N, H, W, C, dx);
+    return cudaGetLastError();
+  }
   k_up2_bwd<T><<<grid_for(total, 256), 256, 0, st>>>(dy, N, H, W, C, dx);
   return cudaGetLastError();
 }
@@ -1314,7 +1542,15 @@ cudaError_t col_sum(const T* dy, long long M, int C, double* partial, int max_bl
   int nblk = (int)((M + 1023) / 1024);
   if (nblk > max_blocks) nblk = max_blocks;
   const long long per = (M + nblk - 1) / nblk;
-  k_col_sum<T><<<nblk, 256, 256 * sizeof(double), st>>>(dy, M, C, partial, per);
+  if (C % 8 == 0 && C / 8 <= 256) {
+    const int R = 256 / (C / 8);
+    const size_t sm = (size_t)R * C * sizeof(float);
+    if (sm > 48 * 1024)
+      PG_CUDA(cudaFuncSetAttribute(k_col_sum_vec<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    k_col_sum_vec<T><<<nblk, 256, sm, st>>>(dy, M, C, partial, per);
+  } else {
+    k_col_sum<T><<<nblk, 256, 256 * sizeof(double), st>>>(dy, M, C, partial, per);
+  }
   PG_LAUNCH_CHECK();
   k_reduce_partials_f32<<<ceil_div(C, 256), 256, 0, st>>>(partial, nblk, C, db, accumulate);
   return cudaGetLastError();
@@ -1373,8 +1609,8 @@ cudaError_t softmax_rows(const float* S, long long rows, int cols, T* P, cudaStr
   return cudaGetLastError();
 }
 template <typename T>
-cudaError_t softmax_bwd_rows(const T* P, const float* dP, long long rows, int cols, T* dS, cudaStream_t st) {
-  k_softmax_bwd_rows<T><<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(P, dP, rows, cols, dS);
+cudaError_t softmax_bwd_rows(const float* S, const float* dP, long long rows, int cols, T* dS, cudaStream_t st) {
+  k_softmax_bwd_rows<T><<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(S, dP, rows, cols, dS);
   return cudaGetLastError();
 }
 PG_INST_T(float)
@@ -1382,22 +1618,23 @@ PG_INST_T(bf16)
 
 template <typename TI, typename TW, typename TO>
 cudaError_t simt_conv_fwd(const TI* x, int N, int H, int W, int Cin, const TW* w, int Cout, int ksz, const float* bias,
-                          const float* alpha, const TO* residual, int res_mode, TO* y, cudaStream_t st) {
+                          const float* alpha, const TO* residual, int res_mode, TO* y, cudaStream_t st,
+                          const TO* relu_ref) {
   const long long M = (long long)N * H * W;
   if (Cout <= 8) {
     dim3 g(ceil_div(M, 256), ceil_div(Cout, 4));
     k_simt_conv<TI, TW, TO, 256, 4, 1, 4><<<g, 256, 0, st>>>(x, N, H, W, Cin, w, Cout, ksz, bias, alpha, residual,
-                                                             res_mode, y);
+                                                             res_mode, y, relu_ref);
   } else {
     dim3 g(ceil_div(M, 64), ceil_div(Cout, 64));
     k_simt_conv<TI, TW, TO, 64, 64, 4, 4><<<g, 256, 0, st>>>(x, N, H, W, Cin, w, Cout, ksz, bias, alpha, residual,
-                                                             res_mode, y);
+                                                             res_mode, y, relu_ref);
   }
   return cudaGetLastError();
 }
 template cudaError_t simt_conv_fwd<float, float, float>(const float*, int, int, int, int, const float*, int, int,
                                                         const float*, const float*, const float*, int, float*,
-                                                        cudaStream_t);
+                                                        cudaStream_t, const float*);
 
 template <typename TI, typename TG>
 cudaError_t simt_conv_wgrad(const TI* x, const TG* dy, int N, int H, int W, int Cin, int Cout, int ksz, float* dw,
@@ -1425,11 +1662,14 @@ cudaError_t simt_conv_wgrad(const TI* x, const TG* dy, int N, int H, int W, int 
 template cudaError_t simt_conv_wgrad<float, float>(const float*, const float*, int, int, int, int, int, int, float*,
                                                    int, cudaStream_t);
 
-cudaError_t sn_power(const SnJob* jobs, int n_jobs, const int* blk_job, const int* blk_k0, int n_blk1,
-                     const int* blk2_job, const int* blk2_r0, int n_blk2, cudaStream_t st) {
-  k_sn_wtu<<<n_blk1, 256, 0, st>>>(jobs, blk_job, blk_k0);
+cudaError_t sn_power(const SnJob* jobs, int n_jobs, const int* b1_job, const int* b1_k0, const int* b1_rc, int n_b1,
+                     const int* b1b_job, const int* b1b_k0, int n_b1b, const int* b2_job, const int* b2_r0, int n_b2,
+                     cudaStream_t st) {
+  k_sn_wtu<<<n_b1, 256, 0, st>>>(jobs, b1_job, b1_k0, b1_rc);
   PG_LAUNCH_CHECK();
-  k_sn_wv<<<n_blk2, 256, 0, st>>>(jobs, blk2_job, blk2_r0);
+  k_sn_wtu_reduce<<<n_b1b, 256, 0, st>>>(jobs, b1b_job, b1b_k0);
+  PG_LAUNCH_CHECK();
+  k_sn_wv<<<n_b2, 256, 0, st>>>(jobs, b2_job, b2_r0);
   PG_LAUNCH_CHECK();
   k_sn_finish<<<n_jobs, 256, 0, st>>>(jobs);
   return cudaGetLastError();
@@ -1439,13 +1679,20 @@ cudaError_t sn_pack(const SnPack* jobs, const long long* blk_start, int n_jobs, 
   k_sn_pack<<<(unsigned)total_blocks, 256, 0, st>>>(jobs, blk_start, n_jobs);
   return cudaGetLastError();
 }
-cudaError_t sn_backward(const SnJob* jobs, const int* idx, int n, float* const* grads, double* scratch,
-                        cudaStream_t st) {
-  (void)scratch;
-  k_sn_bwd<<<n, 1024, 0, st>>>(jobs, idx, grads);
+cudaError_t sn_pack_t(const SnPack* jobs, const long long* blk_start, int n_jobs, long long total_blocks,
+                      cudaStream_t st) {
+  k_sn_pack_t<<<(unsigned)total_blocks, 256, 0, st>>>(jobs, blk_start, n_jobs);
   return cudaGetLastError();
 }
-
+cudaError_t sn_backward(const SnJob* jobs, int n_jobs, const long long* blk_start, long long total_blocks,
+                        double* dotp, cudaStream_t st) {
+  k_snb_dot<<<(unsigned)total_blocks, 256, 0, st>>>(jobs, blk_start, n_jobs, dotp);
+  PG_LAUNCH_CHECK();
+  k_snb_coef<<<ceil_div(n_jobs, 128), 128, 0, st>>>(jobs, n_jobs, dotp);
+  PG_LAUNCH_CHECK();
+  k_snb_apply<<<(unsigned)total_blocks, 256, 0, st>>>(jobs, blk_start, n_jobs);
+  return cudaGetLastError();
+}
 cudaError_t check_finite(const float* g, long long n, int* flag, cudaStream_t st) {
   k_check_finite<<<grid_for(n, 256, 4), 256, 0, st>>>(g, n, flag);
   return cudaGetLastError();
@@ -1498,6 +1745,235 @@ cudaError_t copy_rows_cols(const float* src, long long lds, long long rows, int 
 }
 cudaError_t scale_f32(float* p, long long n, float s, cudaStream_t st) {
   k_scale<<<grid_for(n, 256), 256, 0, st>>>(p, n, s);
+  return cudaGetLastError();
+}
+
+}  // namespace pg
+
+// ============================================================================
+// Thin fp32 convolution (C_out <= 4): G's output layer 96 -> 3 (P:202 keeps it
+// fp32).  A 3x3 halo tile of the input is staged once per channel chunk in
+// shared memory (channel-major planes, padded to a bank-conflict-free stride),
+// so each input element is read from HBM once per tile instead of once per tap.
+// ============================================================================
+namespace pg {
+namespace {
+constexpr int kTH = 8, kTW = 32;                 // output tile: 8 rows x 32 cols
+constexpr int kHR = kTH + 2, kHC = kTW + 2;      // halo tile
+constexpr int kPlane = kHR * kHC + 13;           // 353 = 1 (mod 32)
+constexpr int kCC = 16;                          // channels per chunk
+
+template <typename TI>
+__device__ __forceinline__ void load_halo(const TI* __restrict__ x, int n, int H, int W, int C, int h0, int w0, int c0,
+                                          int cc, float* xs) {
+  // xs[c][r][s] <- x[n][h0 - 1 + r][w0 - 1 + s][c0 + c]  (zero outside the image / channel range)
+  for (int i = threadIdx.x; i < kHR * kHC * cc; i += blockDim.x) {
+    const int c = i % cc;
+    const int rs = i / cc;
+    const int s = rs % kHC, r = rs / kHC;
+    const int h = h0 - 1 + r, w = w0 - 1 + s;
+    float v = 0.0f;
+    if (h >= 0 && h < H && w >= 0 && w < W && c0 + c < C) v = to_f<TI>(x[(((long long)n * H + h) * W + w) * C + c0 + c]);
+    xs[c * kPlane + r * kHC + s] = v;
+  }
+}
+
+// y[m][o] = bias[o] + sum_{tap,c} x[m+tap][c] w[o][tap][c]; one thread per output pixel
+template <int CO>
+__global__ void __launch_bounds__(256) k_thin_fwd(const float* __restrict__ x, int N, int H, int W, int C,
+                                                  const float* __restrict__ w, const float* __restrict__ bias,
+                                                  float* __restrict__ y) {
+  extern __shared__ float sm[];
+  float* ws = sm;                       // [CO][9][C]
+  float* xs = sm + CO * 9 * C;          // [kCC][kPlane]
+  const int tiles_w = (W + kTW - 1) / kTW, tiles_h = (H + kTH - 1) / kTH;
+  int t = blockIdx.x;
+  const int tw = t % tiles_w;
+  t /= tiles_w;
+  const int th = t % tiles_h;
+  const int n = t / tiles_h;
+  const int h0 = th * kTH, w0 = tw * kTW;
+  for (int i = threadIdx.x; i < CO * 9 * C; i += blockDim.x) ws[i] = w[i];
+  const int py = threadIdx.x / kTW, px = threadIdx.x % kTW;
+  float acc[CO];
+#pragma unroll
+  for (int o = 0; o < CO; ++o) acc[o] = 0.0f;
+  for (int c0 = 0; c0 < C; c0 += kCC) {
+    const int cc = min(kCC, C - c0);
+    __syncthreads();
+    load_halo<float>(x, n, H, W, C, h0, w0, c0, cc, xs);
+    __syncthreads();
+    for (int c = 0; c < cc; ++c) {
+      const float* plane = xs + c * kPlane;
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int s = 0; s < 3; ++s) {
+          const float xv = plane[(py + r) * kHC + px + s];
+#pragma unroll
+          for (int o = 0; o < CO; ++o) acc[o] = fmaf(xv, ws[(o * 9 + r * 3 + s) * C + c0 + c], acc[o]);
+        }
+    }
+  }
+  const int h = h0 + py, ww = w0 + px;
+  if (h < H && ww < W) {
+    const long long m = ((long long)n * H + h) * W + ww;
+#pragma unroll
+    for (int o = 0; o < CO; ++o) y[m * CO + o] = acc[o] + (bias ? bias[o] : 0.0f);
+  }
+}
+
+// dx[m][c] = sum_{tap,o} dy[m - delta_tap][o] w[o][tap][c]  (transposed 3x3, pad 1)
+// block = 64 pixels (2 rows x 32) x 4 channel groups; each thread CPT channels of one pixel
+template <int CO, int CPT>
+__global__ void __launch_bounds__(256) k_thin_dgrad(const float* __restrict__ dy, int N, int H, int W, int C,
+                                                    const float* __restrict__ w, float* __restrict__ dx) {
+  extern __shared__ float sm[];
+  float* ws = sm;                                 // [CO][9][C]
+  float* ds = sm + CO * 9 * C;                    // [CO][4][34] halo of dy for a 2 x 32 tile
+  const int tiles_w = (W + 31) / 32, tiles_h = (H + 1) / 2;
+  int t = blockIdx.x;
+  const int tw = t % tiles_w;
+  t /= tiles_w;
+  const int th = t % tiles_h;
+  const int n = t / tiles_h;
+  const int h0 = th * 2, w0 = tw * 32;
+  for (int i = threadIdx.x; i < CO * 9 * C; i += blockDim.x) ws[i] = w[i];
+  for (int i = threadIdx.x; i < CO * 4 * 34; i += blockDim.x) {
+    const int s = i % 34, r = (i / 34) % 4, o = i / 136;
+    const int h = h0 - 1 + r, ww = w0 - 1 + s;
+    ds[i] = (h >= 0 && h < H && ww >= 0 && ww < W) ? dy[(((long long)n * H + h) * W + ww) * CO + o] : 0.0f;
+  }
+  __syncthreads();
+  const int pix = threadIdx.x & 63, grp = threadIdx.x >> 6;
+  const int py = pix >> 5, px = pix & 31;
+  const int h = h0 + py, ww = w0 + px;
+  if (h >= H || ww >= W) return;
+  // dx at (h, w) gathers dy at (h + 1 - r, w + 1 - s) with tap (r, s)
+  float d[CO][9];
+#pragma unroll
+  for (int o = 0; o < CO; ++o)
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int s = 0; s < 3; ++s) d[o][r * 3 + s] = ds[(o * 4 + (py + 2 - r)) * 34 + (px + 2 - s)];
+  const long long m = ((long long)n * H + h) * W + ww;
+  for (int cb = grp * CPT; cb < C; cb += 4 * CPT) {
+    float acc[CPT];
+#pragma unroll
+    for (int j = 0; j < CPT; ++j) acc[j] = 0.0f;
+#pragma unroll
+    for (int o = 0; o < CO; ++o)
+#pragma unroll
+      for (int tp = 0; tp < 9; ++tp) {
+        const float dv = d[o][tp];
+        const float* wr = ws + (o * 9 + tp) * C + cb;
+#pragma unroll
+        for (int j = 0; j < CPT; ++j) acc[j] = fmaf(dv, wr[j], acc[j]);
+      }
+#pragma unroll
+    for (int j = 0; j < CPT; ++j)
+      if (cb + j < C) dx[m * C + cb + j] = acc[j];
+  }
+}
+
+// dW[o][tap][c] partials: persistent blocks over 8x32 pixel tiles; thread = (c-lane, tap), 3 channel
+// chunks of 32 kept in registers; per-block partials [grid][CO*9*C] reduced in fixed order afterwards
+template <int CO>
+__global__ void __launch_bounds__(288) k_thin_wgrad(const float* __restrict__ x, const float* __restrict__ dy, int N,
+                                                    int H, int W, int C, float* __restrict__ partial) {
+  extern __shared__ float sm[];
+  float* xs = sm;                          // [32][kPlane]
+  float* ds = sm + 32 * kPlane;            // [CO][256]
+  const int tiles_w = (W + kTW - 1) / kTW, tiles_h = (H + kTH - 1) / kTH;
+  const int tiles = N * tiles_h * tiles_w;
+  const int cl = threadIdx.x & 31, tap = threadIdx.x >> 5;   // tap 0..8
+  const int r = tap / 3, s = tap % 3;
+  constexpr int MAXCH = 4;                 // up to 128 channels = 4 chunks of 32
+  float acc[MAXCH][CO];
+#pragma unroll
+  for (int k = 0; k < MAXCH; ++k)
+#pragma unroll
+    for (int o = 0; o < CO; ++o) acc[k][o] = 0.0f;
+  const int nch = (C + 31) / 32;
+  for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+    int u = t;
+    const int tw = u % tiles_w;
+    u /= tiles_w;
+    const int th = u % tiles_h;
+    const int n = u / tiles_h;
+    const int h0 = th * kTH, w0 = tw * kTW;
+    __syncthreads();
+    for (int i = threadIdx.x; i < CO * 256; i += blockDim.x) {
+      const int o = i / 256, p = i % 256;
+      const int h = h0 + p / kTW, ww = w0 + p % kTW;
+      ds[i] = (h < H && ww < W) ? dy[(((long long)n * H + h) * W + ww) * CO + o] : 0.0f;
+    }
+#pragma unroll
+    for (int k = 0; k < MAXCH; ++k) {
+      if (k >= nch) break;
+      __syncthreads();
+      load_halo<float>(x, n, H, W, C, h0, w0, k * 32, min(32, C - k * 32), xs);
+      __syncthreads();
+      const float* plane = xs + cl * kPlane;
+      for (int p = 0; p < 256; ++p) {
+        const int py = p / kTW, px = p % kTW;
+        const float xv = plane[(py + r) * kHC + px + s];
+#pragma unroll
+        for (int o = 0; o < CO; ++o) acc[k][o] = fmaf(xv, ds[o * 256 + p], acc[k][o]);
+      }
+    }
+  }
+  float* pb = partial + (long long)blockIdx.x * CO * 9 * C;
+#pragma unroll
+  for (int k = 0; k < MAXCH; ++k) {
+    const int c = k * 32 + cl;
+    if (k < nch && c < C)
+#pragma unroll
+      for (int o = 0; o < CO; ++o) pb[(o * 9 + tap) * C + c] = acc[k][o];
+  }
+}
+__global__ void k_reduce_rows_f32(const float* __restrict__ partial, int rows, int n, float* __restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double a = 0.0;
+    for (int r = 0; r < rows; ++r) a += partial[(long long)r * n + i];
+    out[i] = (float)a;
+  }
+}
+}  // namespace
+
+cudaError_t thin_conv_fwd(const float* x, int N, int H, int W, int C, const float* w, int CO, const float* bias,
+                          float* y, cudaStream_t st) {
+  if (CO != 3) return cudaErrorInvalidValue;
+  const int tiles = N * ((H + kTH - 1) / kTH) * ((W + kTW - 1) / kTW);
+  const size_t sm = (size_t)(CO * 9 * C + kCC * kPlane) * sizeof(float);
+  if (sm > 48 * 1024) PG_CUDA(cudaFuncSetAttribute(k_thin_fwd<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  k_thin_fwd<3><<<tiles, 256, sm, st>>>(x, N, H, W, C, w, bias, y);
+  return cudaGetLastError();
+}
+cudaError_t thin_conv_dgrad(const float* dy, int N, int H, int W, int C, const float* w, int CO, float* dx,
+                            cudaStream_t st) {
+  if (CO != 3 || C % 8) return cudaErrorInvalidValue;
+  const int tiles = N * ((H + 1) / 2) * ((W + 31) / 32);
+  const size_t sm = (size_t)(CO * 9 * C + CO * 4 * 34) * sizeof(float);
+  if (sm > 48 * 1024)
+    PG_CUDA(cudaFuncSetAttribute(k_thin_dgrad<3, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  k_thin_dgrad<3, 8><<<tiles, 256, sm, st>>>(dy, N, H, W, C, w, dx);
+  return cudaGetLastError();
+}
+cudaError_t thin_conv_wgrad(const float* x, const float* dy, int N, int H, int W, int C, int CO, float* dw,
+                            float* scratch, size_t scratch_floats, cudaStream_t st) {
+  if (CO != 3 || C > 128) return cudaErrorInvalidValue;
+  const int tiles = N * ((H + kTH - 1) / kTH) * ((W + kTW - 1) / kTW);
+  int grid = 4 * kNumSMs;
+  if (grid > tiles) grid = tiles;
+  const int n = CO * 9 * C;
+  while ((size_t)grid * n > scratch_floats && grid > 1) grid /= 2;
+  const size_t sm = (size_t)(32 * kPlane + CO * 256) * sizeof(float);
+  if (sm > 48 * 1024) PG_CUDA(cudaFuncSetAttribute(k_thin_wgrad<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  k_thin_wgrad<3><<<grid, 288, sm, st>>>(x, dy, N, H, W, C, scratch);
+  PG_LAUNCH_CHECK();
+  k_reduce_rows_f32<<<ceil_div(n, 256), 256, 0, st>>>(scratch, grid, n, dw);
   return cudaGetLastError();
 }
 

@@ -76,7 +76,8 @@ cudaError_t avgpool2_bwd(const T* dy, int N, int H, int W, int C, const T* add, 
 // dx[N,H,W,C] = sum of the 2x2 block of dy[N,2H,2W,C]   (nearest-upsample adjoint)
 template <typename T>
 cudaError_t up2_bwd(const T* dy, int N, int H, int W, int C, T* dx, cudaStream_t st);
-// column sums: db[c] (+)= sum_m dy[m][c]   (bias gradients; fp64 partials, fixed order)
+// column sums: db[c] (+)= sum_m dy[m][c]   (bias gradients; fp64 partials, fixed order;
+// 16-byte vectors over 8-channel groups when C % 8 == 0)
 template <typename T>
 cudaError_t col_sum(const T* dy, long long M, int C, double* partial, int max_blocks, float* db, int accumulate,
                     cudaStream_t st);
@@ -94,11 +95,21 @@ cudaError_t tanh_bwd(const T* dimg, int c_pad, const float* img, float* dpre, lo
 template <typename TI, typename TW, typename TO>
 cudaError_t simt_conv_fwd(const TI* x, int N, int H, int W, int Cin, const TW* w, int Cout, int ksz,
                           const float* bias, const float* alpha, const TO* residual, int res_mode, TO* y,
-                          cudaStream_t st);
+                          cudaStream_t st, const TO* relu_ref = nullptr);
 // dw[o][tap][c] (+)= sum_m dy[m][o] * x[m+tap][c]   (fp32, atomics across pixel splits)
 template <typename TI, typename TG>
 cudaError_t simt_conv_wgrad(const TI* x, const TG* dy, int N, int H, int W, int Cin, int Cout, int ksz, float* dw,
                             int accumulate, cudaStream_t st);
+
+// ---------------- thin fp32 conv (C_out = 3): G's fp32 output layer, 3x3 pad 1
+cudaError_t thin_conv_fwd(const float* x, int N, int H, int W, int C, const float* w, int CO, const float* bias,
+                          float* y, cudaStream_t st);
+// dx[m][c] = transposed conv of dy[m][CO] with w[CO][9][C]
+cudaError_t thin_conv_dgrad(const float* dy, int N, int H, int W, int C, const float* w, int CO, float* dx,
+                            cudaStream_t st);
+// dw[CO][9][C] = sum_m dy[m][o] x[m+tap][c]  (deterministic: per-block partials in scratch, fixed-order sum)
+cudaError_t thin_conv_wgrad(const float* x, const float* dy, int N, int H, int W, int C, int CO, float* dw,
+                            float* scratch, size_t scratch_floats, cudaStream_t st);
 
 // ---------------- discriminator head + hinge loss (A7, A8), fp32
 template <typename T>
@@ -125,9 +136,9 @@ cudaError_t maxpool2_split_bwd(const T* x, int N, int H, int W, int ldx, int c_o
 // P = softmax rows of S [rows][cols] fp32 -> T
 template <typename T>
 cudaError_t softmax_rows(const float* S, long long rows, int cols, T* P, cudaStream_t st);
-// dS = P * (dP - rowsum(dP * P))  (fp32 dP, T P) -> T
+// dS = P * (dP - rowsum(dP * P)) with P = softmax(S) recomputed in fp32 from the scores -> T
 template <typename T>
-cudaError_t softmax_bwd_rows(const T* P, const float* dP, long long rows, int cols, T* dS, cudaStream_t st);
+cudaError_t softmax_bwd_rows(const float* S, const float* dP, long long rows, int cols, T* dS, cudaStream_t st);
 // batched SIMT GEMM for the F32 path: C[b][m][n] = sum_k A[b](m,k) B[b](n,k)
 cudaError_t gemm_f32_batched(int batch, int M, int N, int K, const float* A, long long sab, long long sam,
                              long long sak, const float* B, long long sbb, long long sbn, long long sbk, float* C,
@@ -141,7 +152,11 @@ struct SnJob {
   float* t;         // [K] scratch (W^T u)
   float* s;         // [rows] scratch (W v)
   float* sigma;     // [2]: sigma, 1/sigma
-  int rows, K;
+  float* part;      // [nrc][K] partial W^T u over row chunks of 128
+  float* grad;      // [rows][K] gradient w.r.t. W/sigma (SN backward, in place)
+  double* coef;     // [1] SN backward coefficient
+  int rows, K, nrc;
+  long long bwd_blk0, bwd_nblk;   // SN-backward block range of this job
 };
 struct SnPack {     // one packed copy of W/sigma
   const float* w;
@@ -154,13 +169,20 @@ struct SnPack {     // one packed copy of W/sigma
   int dst_rows;        // mode 1: total rows (row stride of the transposed layout)
   int dst_cin;         // mode 0: padded input channels (>= cin; pads left untouched = 0)
 };
-cudaError_t sn_power(const SnJob* jobs_dev, int n_jobs, const int* blk_job_dev, const int* blk_k0_dev, int n_blk1,
-                     const int* blk2_job_dev, const int* blk2_r0_dev, int n_blk2, cudaStream_t st);
+// power step over all SN weights of a net: pass 1a blocks = (job, 256 columns, 128-row chunk),
+// pass 1b blocks = (job, 256 columns), pass 2 blocks = (job, 8 rows), pass 3 = one block per job
+cudaError_t sn_power(const SnJob* jobs_dev, int n_jobs, const int* b1_job, const int* b1_k0, const int* b1_rc, int n_b1,
+                     const int* b1b_job, const int* b1b_k0, int n_b1b, const int* b2_job, const int* b2_r0, int n_b2,
+                     cudaStream_t st);
 cudaError_t sn_pack(const SnPack* jobs_dev, const long long* blk_start_dev, int n_jobs, long long total_blocks,
                     cudaStream_t st);
-// SN backward for one weight: g <- (g - <g, W/sigma> u v^T) / sigma
-cudaError_t sn_backward(const SnJob* jobs_dev, const int* idx_dev, int n, float* const* grads_dev, double* scratch,
-                        cudaStream_t st);
+// dgrad-layout (mode 1) packs through 32x32 smem tiles; blocks per job = taps * ceil(rows/32) * ceil(cin/32)
+cudaError_t sn_pack_t(const SnPack* jobs_dev, const long long* blk_start_dev, int n_jobs, long long total_blocks,
+                      cudaStream_t st);
+// SN backward over all SN weights: g <- g / sigma - (<g, W> / sigma^2) u v^T; blocks of 4096 elements,
+// deterministic (per-block fp64 partial dots reduced per job in block order)
+cudaError_t sn_backward(const SnJob* jobs_dev, int n_jobs, const long long* blk_start_dev, long long total_blocks,
+                        double* dot_partial, cudaStream_t st);
 
 // flag[0] |= any non-finite in g
 cudaError_t check_finite(const float* g, long long n, int* flag, cudaStream_t st);

@@ -223,6 +223,17 @@ __global__ void __launch_bounds__(192, 1)
         const bool full32 = (col0 + 32 <= a.Cout);
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] *= alpha;
+        if (a.relu_ref) {   // fused ReLU backward: keep the gradient where the forward input was > 0
+          const bf16* rr = reinterpret_cast<const bf16*>(a.relu_ref) + m * a.ldo + col0;
+          if (full32) {
+            float r[32];
+            load_row32_bf16(rr, r);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = r[j] > 0.0f ? v[j] : 0.0f;
+          } else {
+            for (int j = 0; j < 32 && col0 + j < a.Cout; ++j) v[j] = __bfloat162float(rr[j]) > 0.0f ? v[j] : 0.0f;
+          }
+        }
         if (a.bias) {
 #pragma unroll
           for (int j = 0; j < 32; ++j)
@@ -514,6 +525,7 @@ cudaError_t tc_conv_fprop(const void* x, int N, int H, int W, int Cin, const voi
   a.residual = epi.residual;
   a.res_mode = epi.res_mode;
   a.ldr = epi.ldr ? epi.ldr : Cout;
+  a.relu_ref = epi.relu_ref;
   a.out = epi.out;
   a.out_f32 = epi.out_f32;
   a.ldo = epi.ldo ? epi.ldo : Cout;

@@ -12,6 +12,7 @@ struct TcEpilogue {
   const void* residual = nullptr;  // bf16, added last (same pixel or half-res nearest-upsampled)
   int res_mode = 0;                // 1 = same resolution, 2 = half resolution (x2 nearest)
   int ldr = 0;                     // residual row stride (elements), default Cout
+  const void* relu_ref = nullptr;  // bf16 [M][ldo]: acc is zeroed where ref <= 0 (fused ReLU backward)
   void* out = nullptr;             // bf16 or fp32 [M][ldo]
   int out_f32 = 0;
   int ldo = 0;                     // default Cout
@@ -24,6 +25,7 @@ struct TcFpropArgs {
   const float* alpha;
   const void* residual;
   int res_mode, ldr;
+  const void* relu_ref;
   void* out;
   int out_f32, ldo;
 };
