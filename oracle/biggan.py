@@ -29,7 +29,7 @@ import numpy as np
 import torch
 
 from . import ops
-from .ops import F64, q
+from .ops import F64, q, qg, qv
 
 # ---------------------------------------------------------------------------
 # Architecture (reading R1; BigGAN-PyTorch G_arch / D_arch channel multipliers)
@@ -258,13 +258,14 @@ def g_forward(cfg: Config, sn: _SN, z: torch.Tensor, y: torch.Tensor) -> torch.T
         g1 = cond @ sn.w(pre + "cbn1.gain").t()
         b1 = cond @ sn.w(pre + "cbn1.bias").t()
         x = h
-        a = q(torch.relu(ops.cbn(x, g1, b1, cfg.bn_eps)), bf)
-        a = ops.up2(a)
+        a = qv(torch.relu(ops.cbn(x, g1, b1, cfg.bn_eps)), bf)
+        a = qg(ops.up2(a), bf)                       # the conv input's gradient is stored at full resolution
         a = q(ops.conv2d(a, _qw(sn, pre + "conv1.w"), p[pre + "conv1.b"]), bf)
         g2 = cond @ sn.w(pre + "cbn2.gain").t()
         b2 = cond @ sn.w(pre + "cbn2.bias").t()
         a = q(torch.relu(ops.cbn(a, g2, b2, cfg.bn_eps)), bf)
-        s = q(ops.conv2d(x, _qw(sn, pre + "sc.w"), p[pre + "sc.b"]), bf)  # skip before upsample (commutes)
+        # skip 1x1 before the upsample (commutes); its input gradient is a separately stored partial
+        s = q(ops.conv2d(qg(x, bf), _qw(sn, pre + "sc.w"), p[pre + "sc.b"]), bf)
         h = q(ops.conv2d(a, _qw(sn, pre + "conv2.w"), p[pre + "conv2.b"]) + ops.up2(s), bf)
         if att:
             h = _attention(cfg, sn, "attn.", h)
@@ -274,13 +275,16 @@ def g_forward(cfg: Config, sn: _SN, z: torch.Tensor, y: torch.Tensor) -> torch.T
 
 
 def _attention(cfg: Config, sn: _SN, pre: str, x: torch.Tensor) -> torch.Tensor:
-    """Non-local block with the bf16 storage points of R14 (scores/softmax in fp32)."""
+    """Non-local block with the bf16 storage points of R14: theta/phi/g conv outputs, the
+    softmax output and beta*g stored bf16; scores, their softmax and dP in fp32; dS and the
+    theta/phi/g/o gradients stored bf16."""
     bf = cfg.bf16
     n, c, h, w = x.shape
     theta = q(ops.conv2d(x, _qw(sn, pre + "theta"), None), bf).reshape(n, -1, h * w)
-    phi = q(ops.maxpool2(ops.conv2d(x, _qw(sn, pre + "phi"), None)), bf).reshape(n, -1, h * w // 4)
-    g = q(ops.maxpool2(ops.conv2d(x, _qw(sn, pre + "g"), None)), bf).reshape(n, -1, h * w // 4)
-    beta = q(torch.softmax(torch.bmm(theta.transpose(1, 2), phi), dim=-1), bf)
+    phi = ops.maxpool2(q(ops.conv2d(x, _qw(sn, pre + "phi"), None), bf)).reshape(n, -1, h * w // 4)
+    g = ops.maxpool2(q(ops.conv2d(x, _qw(sn, pre + "g"), None), bf)).reshape(n, -1, h * w // 4)
+    scores = qg(torch.bmm(theta.transpose(1, 2), phi), bf)
+    beta = qv(torch.softmax(scores, dim=-1), bf)
     o = q(torch.bmm(g, beta.transpose(1, 2)).reshape(n, -1, h, w), bf)
     return q(x + sn.params[pre + "gamma"] * ops.conv2d(o, _qw(sn, pre + "o"), None), bf)
 
@@ -293,7 +297,7 @@ def d_forward(cfg: Config, sn: _SN, x: torch.Tensor, y: torch.Tensor) -> torch.T
     blocks = d_blocks(cfg)
     for j, (ci, co, _, dn, att) in enumerate(blocks):
         pre = f"b{j}."
-        a = h if j == 0 else q(torch.relu(h), bf)
+        a = h if j == 0 else qv(torch.relu(h), bf)
         a = q(ops.conv2d(a, _qw(sn, pre + "conv1.w"), p[pre + "conv1.b"]), bf)
         c2 = ops.conv2d(q(torch.relu(a), bf), _qw(sn, pre + "conv2.w"), p[pre + "conv2.b"])
         learn = ci != co or dn
@@ -302,8 +306,9 @@ def d_forward(cfg: Config, sn: _SN, x: torch.Tensor, y: torch.Tensor) -> torch.T
             s = q(ops.conv2d(q(ops.avgpool2(h), bf), _qw(sn, pre + "sc.w"), p[pre + "sc.b"]), bf)
             h = q(ops.avgpool2(q(c2, bf)) + s, bf)
         else:
-            # later blocks: 1x1 skip conv, residual add, then pool (= pool of each branch, R7)
-            s = q(ops.conv2d(h, _qw(sn, pre + "sc.w"), p[pre + "sc.b"]), bf) if learn else h
+            # later blocks: 1x1 skip conv, residual add, then pool (= pool of each branch, R7);
+            # the skip conv's input gradient is a separately stored partial
+            s = q(ops.conv2d(qg(h, bf), _qw(sn, pre + "sc.w"), p[pre + "sc.b"]), bf) if learn else h
             t = q(c2 + s, bf)
             h = q(ops.avgpool2(t), bf) if dn else t
         if att:

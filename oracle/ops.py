@@ -38,9 +38,43 @@ class _Q(torch.autograd.Function):
         return bf16_round(g)
 
 
+class _QV(torch.autograd.Function):
+    """Rounds the stored value to bf16; the gradient flowing back is not a stored tensor."""
+
+    @staticmethod
+    def forward(ctx, x):
+        return bf16_round(x)
+
+    @staticmethod
+    def backward(ctx, g):
+        return g
+
+
+class _QG(torch.autograd.Function):
+    """Identity value; the gradient w.r.t. this tensor is stored in bf16."""
+
+    @staticmethod
+    def forward(ctx, x):
+        return x.clone()
+
+    @staticmethod
+    def backward(ctx, g):
+        return bf16_round(g)
+
+
 def q(x: torch.Tensor, on: bool) -> torch.Tensor:
     """Storage point: bf16 round-trip of value and gradient when ``on``."""
     return _Q.apply(x) if on else x
+
+
+def qv(x: torch.Tensor, on: bool) -> torch.Tensor:
+    """Value-only storage point (the gradient of this tensor is kept in fp32)."""
+    return _QV.apply(x) if on else x
+
+
+def qg(x: torch.Tensor, on: bool) -> torch.Tensor:
+    """Gradient-only storage point (e.g. a branch's partial gradient written in bf16)."""
+    return _QG.apply(x) if on else x
 
 
 # ---------------------------------------------------------------------------

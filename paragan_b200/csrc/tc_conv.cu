@@ -177,8 +177,11 @@ __global__ void __launch_bounds__(192, 1)
           tc::tc_fence_after();
           const uint32_t a_base = tc::smem_u32(sA + stage * C::A_BYTES);
           const uint32_t b_base = tc::smem_u32(sB + stage * C::B_BYTES);
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
+          // the last channel chunk may hold fewer than 64 real channels (e.g. 96 = 64 + 32, or the
+          // 8-channel RGB image): issue only the K=16 steps that cover them
+          const int cc = kb % a.c_chunks;
+          const int ksteps = (cc == a.c_chunks - 1) ? a.last_ksteps : 4;
+          for (int k = 0; k < ksteps; ++k) {
             const uint64_t ad = tc::sdesc_sw128(a_base + k * 32, 16, 1024);
             const uint64_t bd = tc::sdesc_sw128(b_base + k * 32, 16, 1024);
             tc::mma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0);
@@ -517,6 +520,7 @@ cudaError_t tc_conv_fprop(const void* x, int N, int H, int W, int Cin, const voi
   a.ksz = ksz;
   a.taps = ksz * ksz;
   a.c_chunks = ceil_div(Cin, 64);
+  a.last_ksteps = ceil_div(Cin - (a.c_chunks - 1) * 64, 16);
   a.Cout = Cout;
   a.m_tiles = ceil_div(a.M, kTileM);
   a.n_tiles = ceil_div(Cout, bn);

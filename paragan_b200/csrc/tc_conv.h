@@ -20,7 +20,7 @@ struct TcEpilogue {
 
 struct TcFpropArgs {
   long long M;
-  int H, W, ksz, taps, c_chunks, Cout, m_tiles, n_tiles;
+  int H, W, ksz, taps, c_chunks, last_ksteps, Cout, m_tiles, n_tiles;
   const float* bias;
   const float* alpha;
   const void* residual;
