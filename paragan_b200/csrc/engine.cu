@@ -128,8 +128,9 @@ struct GBlock {
 struct DBlock {
   int cin, cin_x, cout, hin, hout;
   bool down, learn_sc, attn;
-  ConvL c1, c2, sc;
-  void *x, *rx, *c1o, *r1, *t, *xp, *s, *out;
+  bool im2col = false;   // first layer as a K = 27 (-> 32) GEMM over an im2col of the image
+  ConvL c1, c2, sc, c1x;
+  void *x, *rx, *c1o, *r1, *t, *xp, *s, *out, *xi;
 };
 
 int round8(int x) { return (x + 7) / 8 * 8; }
@@ -592,6 +593,13 @@ class Engine final : public EngineBase {
       b.learn_sc = (b.cin != b.cout) || b.down;
       const std::string p = "b" + std::to_string(j) + ".";
       b.c1 = conv(D_, p + "conv1", b.cin, b.cin_x, b.cout, 3, true);
+      if (kBF && ar.din[j] < 0) {
+        b.im2col = true;
+        b.c1x = b.c1;
+        b.c1x.cin = 27;
+        b.c1x.cin_x = 32;
+        b.c1x.ksz = 1;
+      }
       b.c2 = conv(D_, p + "conv2", b.cout, b.cout, b.cout, 3, true);
       if (b.learn_sc) b.sc = conv(D_, p + "sc", b.cin, b.cin_x, b.cout, 1, true);
       b.attn = !placed && cfg_.attn_res == b.hout;
@@ -650,7 +658,8 @@ class Engine final : public EngineBase {
     }
     alloc_conv(oconv_);
     for (auto& b : db_) {
-      alloc_conv(b.c1); alloc_conv(b.c2);
+      if (b.im2col) alloc_conv(b.c1x); else alloc_conv(b.c1);
+      alloc_conv(b.c2);
       if (b.learn_sc) alloc_conv(b.sc);
     }
     alloc_lin(dlin_);
@@ -713,6 +722,7 @@ class Engine final : public EngineBase {
       b.xp = b.down ? act(B2, H / 2, H / 2, b.cin_x) : nullptr;
       b.s = b.learn_sc ? act(B2, H, H, b.cout) : nullptr;
       b.out = act(B2, b.hout, b.hout, b.cout);
+      b.xi = b.im2col ? act(B2, H, H, 32) : nullptr;
     }
     for (AttnL* at : {&gattn_, &dattn_}) {
       if (!at->C) continue;
@@ -931,7 +941,8 @@ class Engine final : public EngineBase {
     if (gattn_.C) add_attn(G_, gattn_);
     add_conv(G_, oconv_);
     for (auto& b : db_) {
-      add_conv(D_, b.c1); add_conv(D_, b.c2);
+      add_conv(D_, b.im2col ? b.c1x : b.c1);
+      add_conv(D_, b.c2);
       if (b.learn_sc) add_conv(D_, b.sc);
     }
     if (dattn_.C) add_attn(D_, dattn_);
@@ -1253,7 +1264,12 @@ class Engine final : public EngineBase {
         CK(relu_copy<T>(static_cast<const T*>(b.x), static_cast<T*>(b.rx), Mi * b.cin_x, st_));
         cin = b.rx;
       }
-      CKS(conv_fwd(cin, n, H, b.c1, b.c1o, D_.P(b.c1.b), nullptr, 0));
+      if (b.im2col) {
+        CK(im2col3<T>(static_cast<const T*>(b.x), n, H, H, b.cin_x, static_cast<T*>(b.xi), st_));
+        CKS(conv_fwd(b.xi, n, H, b.c1x, b.c1o, D_.P(b.c1.b), nullptr, 0));
+      } else {
+        CKS(conv_fwd(cin, n, H, b.c1, b.c1o, D_.P(b.c1.b), nullptr, 0));
+      }
       CK(relu_copy<T>(static_cast<const T*>(b.c1o), static_cast<T*>(b.r1), Mi * b.cout, st_));
       if (j == 0 && b.down) {
         // skip: avgpool the image, then 1x1 conv (block 0 has no pre-activation)
@@ -1363,7 +1379,8 @@ class Engine final : public EngineBase {
       }
       const void* cin = (j > 0) ? b.rx : b.x;
       if (want_w) {
-        CKS(conv_wgrad(D_, cin, dr1, n, H, b.c1));
+        if (b.im2col) CKS(conv_wgrad(D_, b.xi, dr1, n, H, b.c1x));
+        else CKS(conv_wgrad(D_, cin, dr1, n, H, b.c1));
         CKS(bias_grad(D_, b.c1, dr1, Mi));
       }
       if (!need_dx) break;
@@ -1374,6 +1391,11 @@ class Engine final : public EngineBase {
       void* dx = tmp(ix);
       if (j > 0) {   // pre-activation block: relu'(x) mask and the skip gradient fused in the epilogue
         CKS(conv_dgrad(dr1, n, H, b.c1, dx, dskip, nullptr, b.x));
+      } else if (b.im2col) {
+        // dgrad into the im2col buffer (no longer needed), then its adjoint (col2im) + skip gradient
+        CKS(conv_dgrad(dr1, n, H, b.c1x, b.xi, nullptr));
+        CK(col2im3<T>(static_cast<const T*>(b.xi), n, H, H, b.cin_x, static_cast<const T*>(dskip), static_cast<T*>(dx),
+                      st_));
       } else {
         CKS(conv_dgrad(dr1, n, H, b.c1, dx, dskip));
       }

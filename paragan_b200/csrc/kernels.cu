@@ -1978,3 +1978,89 @@ cudaError_t thin_conv_wgrad(const float* x, const float* dy, int N, int H, int W
 }
 
 }  // namespace pg
+
+// ============================================================================
+// First D layer as a K = 27 (padded to 32) GEMM: im2col of the 3-channel image
+// and its adjoint.  out[p][tap*3 + c] = x[p + delta_tap][c] (zero padding), 0 for k >= 27.
+// ============================================================================
+namespace pg {
+namespace {
+template <typename T>
+__global__ void k_im2col3(const T* __restrict__ x, int N, int H, int W, int cx, T* __restrict__ out) {
+  const long long total = (long long)N * H * W;
+  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < total; p += (long long)gridDim.x * blockDim.x) {
+    const int w = (int)(p % W);
+    const long long q = p / W;
+    const int h = (int)(q % H);
+    const int n = (int)(q / H);
+    float v[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) v[k] = 0.0f;
+#pragma unroll
+    for (int t = 0; t < 9; ++t) {
+      const int hh = h + t / 3 - 1, ww = w + t % 3 - 1;
+      if (hh >= 0 && hh < H && ww >= 0 && ww < W) {
+        const T* src = x + (((long long)n * H + hh) * W + ww) * cx;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) v[t * 3 + c] = to_f<T>(src[c]);
+      }
+    }
+    T* dst = out + p * 32;
+#pragma unroll
+    for (int k = 0; k < 32; k += 8) {
+      float u[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) u[j] = v[k + j];
+      Vec8<T>::store(dst + k, u);
+    }
+  }
+}
+// dx[p][c] = sum_tap dxi[p - delta_tap][tap*3 + c] (+ add[p][c]); channels 3..cx-1 = add or 0
+template <typename T>
+__global__ void k_col2im3(const T* __restrict__ dxi, int N, int H, int W, int cx, const T* __restrict__ add,
+                          T* __restrict__ dx) {
+  const long long total = (long long)N * H * W;
+  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < total; p += (long long)gridDim.x * blockDim.x) {
+    const int w = (int)(p % W);
+    const long long q = p / W;
+    const int h = (int)(q % H);
+    const int n = (int)(q / H);
+    float acc[3] = {0.0f, 0.0f, 0.0f};
+#pragma unroll
+    for (int t = 0; t < 9; ++t) {
+      // x[p] feeds output pixel p - delta_tap through slot tap
+      const int hh = h - (t / 3 - 1), ww = w - (t % 3 - 1);
+      if (hh >= 0 && hh < H && ww >= 0 && ww < W) {
+        const T* src = dxi + (((long long)n * H + hh) * W + ww) * 32 + t * 3;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) acc[c] += to_f<T>(src[c]);
+      }
+    }
+    for (int c = 0; c < cx; ++c) {
+      float v = c < 3 ? acc[c] : 0.0f;
+      if (add) v += to_f<T>(add[p * cx + c]);
+      dx[p * cx + c] = from_f<T>(v);
+    }
+  }
+}
+}  // namespace
+
+template <typename T>
+cudaError_t im2col3(const T* x, int N, int H, int W, int cx, T* out, cudaStream_t st) {
+  const long long total = (long long)N * H * W;
+  k_im2col3<T><<<(unsigned)std::min<long long>((total + 255) / 256, 8LL * kNumSMs), 256, 0, st>>>(x, N, H, W, cx, out);
+  return cudaGetLastError();
+}
+template <typename T>
+cudaError_t col2im3(const T* dxi, int N, int H, int W, int cx, const T* add, T* dx, cudaStream_t st) {
+  const long long total = (long long)N * H * W;
+  k_col2im3<T><<<(unsigned)std::min<long long>((total + 255) / 256, 8LL * kNumSMs), 256, 0, st>>>(dxi, N, H, W, cx, add,
+                                                                                                  dx);
+  return cudaGetLastError();
+}
+template cudaError_t im2col3<bf16>(const bf16*, int, int, int, int, bf16*, cudaStream_t);
+template cudaError_t col2im3<bf16>(const bf16*, int, int, int, int, const bf16*, bf16*, cudaStream_t);
+template cudaError_t im2col3<float>(const float*, int, int, int, int, float*, cudaStream_t);
+template cudaError_t col2im3<float>(const float*, int, int, int, int, const float*, float*, cudaStream_t);
+
+}  // namespace pg

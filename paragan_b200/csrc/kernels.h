@@ -3,6 +3,7 @@
 // reductions are accumulated in fp64.  Activations are NHWC, [M = N*H*W][C].
 #pragma once
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <cstdint>
 
 #include "common.cuh"
@@ -100,6 +101,12 @@ cudaError_t simt_conv_fwd(const TI* x, int N, int H, int W, int Cin, const TW* w
 template <typename TI, typename TG>
 cudaError_t simt_conv_wgrad(const TI* x, const TG* dy, int N, int H, int W, int Cin, int Cout, int ksz, float* dw,
                             int accumulate, cudaStream_t st);
+
+// ---------------- first D layer as a K=27 GEMM: xi[p][tap*3+c] (K padded to 32) and its adjoint
+template <typename T>
+cudaError_t im2col3(const T* x, int N, int H, int W, int cx, T* out, cudaStream_t st);
+template <typename T>
+cudaError_t col2im3(const T* dxi, int N, int H, int W, int cx, const T* add, T* dx, cudaStream_t st);
 
 // ---------------- thin fp32 conv (C_out = 3): G's fp32 output layer, 3x3 pad 1
 cudaError_t thin_conv_fwd(const float* x, int N, int H, int W, int C, const float* w, int CO, const float* bias,

@@ -73,6 +73,14 @@ def test_step_parity_bf16_micro():
     _check(ocfg, cfg, 4, seed=23, tol=2e-2, sign_min=0.95)
 
 
+def test_step_parity_f32_biggan128_b2():
+    """Every BigGAN-128 shape (channel padding, attention at 64^2 with C/8 = 12 -> 16, 4x4 head)
+    through the exact fp32 path at 1e-4."""
+    ocfg = P.oracle_config(128, 96, 64, 1000, 128, 20, bf16=False)
+    cfg = api.make_config(local_batch=2, compute=api.F32)
+    _check(ocfg, cfg, 2, seed=24, tol=1e-4, sign_min=0.999)
+
+
 def test_step_parity_bf16_biggan128_b2():
     ocfg = P.oracle_config(128, 96, 64, 1000, 128, 20, bf16=True)
     cfg = api.make_config(local_batch=2, compute=api.BF16)

@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--batch", type=int, default=4)
     ap.add_argument("--seed", type=int, default=23)
     ap.add_argument("--bf16", action="store_true")
+    ap.add_argument("--summary", action="store_true")
     a = ap.parse_args()
     import numpy as np
     from paragan_b200 import api
@@ -35,8 +36,15 @@ def main():
         gs, ds, g0, d0, dbs, gb = P.make_inputs(o, a.batch, a.seed)
         res[emu] = P.run_oracle(o, gs, ds, g0, d0, dbs, gb)
     got = P.run_gpu(cfg, g0, d0, dbs, gb)
+    first = next(iter(res.values()))
+    print("oracle D logits", np.round(first["d_logits"], 4), "G logits", np.round(first["g_logits"], 4))
     print(f"losses gpu d={got['d_loss']:.6f} g={got['g_loss']:.6f}; oracle " +
           " ".join(f"[emu={k}] d={v['d_loss']:.6f} g={v['g_loss']:.6f}" for k, v in res.items()))
+    print("fake rel err vs " + " ".join(f"emu={k}: {P.rel(got['fake'], v['fake']):.2e}" for k, v in res.items()))
+    print("d_grads global " + " ".join(f"emu={k}: {P.rel(got['d_grads'], v['d_grads']):.2e}" for k, v in res.items()))
+    print("g_grads global " + " ".join(f"emu={k}: {P.rel(got['g_grads'], v['g_grads']):.2e}" for k, v in res.items()))
+    if a.summary:
+        return
     for key, specs in (("d_grads", ds), ("g_grads", gs)):
         print(f"\n{key}: tensor | rel err vs " + " | ".join(f"emu={k}" for k in res) + " | emu vs plain")
         o = 0
