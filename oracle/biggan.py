@@ -360,9 +360,11 @@ def pack_real(cfg: Config, real_nchw: np.ndarray) -> torch.Tensor:
     return ops.bf16_round(x) if cfg.bf16 else x
 
 
-def d_step(cfg: Config, G: NetState, D: NetState, real, real_y, z, fake_y, update: bool = True) -> dict:
+def d_step(cfg: Config, G: NetState, D: NetState, real, real_y, z, fake_y, update: bool = True,
+           fake_override=None) -> dict:
     """One D step: SN(G), G forward (no grad), SN(D), D([fake; real]),
-    hinge L_D, backward through D, Adam on D."""
+    hinge L_D, backward through D, Adam on D.  ``fake_override`` (test hook) replaces the
+    generated images so D's own arithmetic can be compared in isolation."""
     real = pack_real(cfg, real)
     real_y = torch.as_tensor(np.asarray(real_y), dtype=torch.long)
     fake_y = torch.as_tensor(np.asarray(fake_y), dtype=torch.long)
@@ -370,6 +372,8 @@ def d_step(cfg: Config, G: NetState, D: NetState, real, real_y, z, fake_y, updat
     sng = _SN(G.specs, G.params, G.us, cfg.sn_eps, cfg.bf16)
     with torch.no_grad():
         fake = g_forward(cfg, sng, z, fake_y)
+    if fake_override is not None:
+        fake = torch.as_tensor(np.asarray(fake_override, dtype=np.float64))
     fake = q(fake, cfg.bf16)
     dparams = {k: v.detach().requires_grad_(True) for k, v in D.params.items()}
     snd = _SN(D.specs, dparams, D.us, cfg.sn_eps, cfg.bf16)

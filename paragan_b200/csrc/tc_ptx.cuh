@@ -115,6 +115,13 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr, uint32_t lbo_byt
   return d;
 }
 
+// Same, with the matrix base offset field (bits 49-51): the row phase of a start address
+// that is not aligned to the 1024-byte swizzle repeat.
+__device__ __forceinline__ uint64_t sdesc_sw128_off(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes,
+                                                    uint32_t base_off) {
+  return sdesc_sw128(saddr, lbo_bytes, sbo_bytes) | ((uint64_t)(base_off & 7) << 49);
+}
+
 // Instruction descriptor: kind::f16, A/B = bf16, D = fp32, dense.
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn_major, bool b_mn_major) {
   return (1u << 4)                      // D format fp32

@@ -63,6 +63,9 @@ CONV_SHAPES = [  # n, h, w, cin, cout, k
     (3, 8, 8, 1536, 256, 3),     # deep layer, several K chunks
     (3, 8, 8, 32, 48, 3),        # M = 192: ragged last tile
     (1, 2, 2, 16, 16, 1),        # M = 4
+    (2, 4, 128, 96, 96, 3),      # halo-tile kernel (W % 128 == 0): 96 = 64 + 32 channels
+    (1, 3, 256, 64, 192, 3),     # halo-tile kernel, two tiles per row
+    (2, 2, 128, 192, 96, 3),     # halo-tile kernel, top and bottom rows out of the image
 ]
 
 

@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--seed", type=int, default=23)
     ap.add_argument("--bf16", action="store_true")
     ap.add_argument("--summary", action="store_true")
+    ap.add_argument("--d-only", action="store_true", help="D step alone, oracle fed the GPU's fake images")
     a = ap.parse_args()
     import numpy as np
     from paragan_b200 import api
@@ -30,6 +31,32 @@ def main():
     compute = api.BF16 if a.bf16 else api.F32
     cfg = api.make_config(resolution=a.res, ch=a.ch, attn_res=a.attn, n_classes=a.classes, shared_dim=a.shared,
                           z_chunk=a.zc, local_batch=a.batch, compute=compute)
+    if a.d_only:
+        import torch
+        from oracle import biggan as bg
+        o = P.oracle_config(a.res, a.ch, a.attn, a.classes, a.shared, a.zc, bf16=a.bf16)
+        gs, ds, g0, d0, dbs, gb = P.make_inputs(o, a.batch, a.seed)
+        ctx = api.Context(cfg)
+        ctx.set_params(api.NET_G, g0)
+        ctx.set_params(api.NET_D, d0)
+        real, ry, z, fy = dbs[0]
+        tdt = torch.bfloat16 if a.bf16 else torch.float32
+        rp = torch.empty((a.batch, a.res, a.res, 8), dtype=tdt, device="cuda:0")
+        api.layout_pack(torch.from_numpy(real).cuda(), rp, compute, 8)
+        ctx.d_step(rp, torch.from_numpy(ry).cuda(), torch.from_numpy(z).cuda(), torch.from_numpy(fy).cuda(),
+                   flags=api.FLAG_NO_UPDATE)
+        st = ctx.sync_stats(raise_nonfinite=False)
+        fk = ctx.get_fakes()
+        gd = ctx.get_grads(api.NET_D)
+        G = bg.NetState.from_flat(gs, g0)
+        D = bg.NetState.from_flat(ds, d0)
+        want = bg.d_step(o, G, D, real, ry, z, fy, update=False, fake_override=fk)
+        wfree = bg.d_step(o, bg.NetState.from_flat(gs, g0), bg.NetState.from_flat(ds, d0), real, ry, z, fy,
+                          update=False)
+        print(f"D-only: loss gpu {st.d_loss:.7f} oracle(gpu fakes) {want['loss']:.7f}; fake err {P.rel(fk, wfree['fake']):.2e}")
+        print(f"D-only grads vs oracle on the GPU's fakes: {P.rel(gd, want['grads']):.2e}; "
+              f"vs oracle's own fakes: {P.rel(gd, wfree['grads']):.2e}")
+        return
     res = {}
     for emu in ([True, False] if a.bf16 else [False]):
         o = P.oracle_config(a.res, a.ch, a.attn, a.classes, a.shared, a.zc, bf16=emu)
