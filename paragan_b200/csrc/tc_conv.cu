@@ -33,7 +33,9 @@ namespace {
 
 constexpr int kTileM = 128;
 constexpr uint32_t kAtomBytes = 128 * 128;   // 128 rows x 128 B (64 bf16)
-constexpr int kSmemBudget = 200 * 1024;
+// 227 KB per CTA minus alignment slack, barriers and the 2 x 16 KB epilogue staging tiles
+constexpr uint32_t kStageBytes = 128 * 128;   // one [128 rows][64 bf16] SW128 output tile
+constexpr int kSmemBudget = 232448 - 1024 - 2 * (int)kStageBytes - 1024;
 
 template <int BN>
 struct FpropCfg {
@@ -43,7 +45,7 @@ struct FpropCfg {
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr uint32_t TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
                                         : (2 * BN <= 256) ? 256 : 512;
-  static constexpr size_t SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + 256;
+  static constexpr size_t SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + 2 * kStageBytes + 512;
 };
 
 template <int BN>
@@ -51,7 +53,7 @@ struct WgradCfg {
   static constexpr int NB = (BN + 63) / 64;           // 64-wide MN atoms of B
   static constexpr uint32_t A_BYTES = 2 * kAtomBytes;  // M = 128 output channels
   static constexpr uint32_t B_BYTES = NB * kAtomBytes;
-  static constexpr int STAGES_RAW = kSmemBudget / (A_BYTES + B_BYTES);
+  static constexpr int STAGES_RAW = (232448 - 2048) / (A_BYTES + B_BYTES);
   static constexpr int STAGES = STAGES_RAW > 6 ? 6 : STAGES_RAW;
   static constexpr uint32_t TMEM_COLS = (BN <= 32) ? 32 : (BN <= 64) ? 64 : (BN <= 128) ? 128 : 256;
   static constexpr size_t SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + 256;
@@ -101,16 +103,20 @@ __device__ __forceinline__ void load_row32_bf16(const bf16* src, float (&r)[32])
   }
 }
 
-// Epilogue warps 2..5: TMEM -> registers -> global with bias / gamma scale / ReLU-backward
-// mask / residual (same or half resolution) fused and a single rounding.
+// Epilogue warps 2..5: TMEM -> registers (thread = output row) with bias / gamma scale /
+// ReLU-backward mask / residual (same or half resolution) fused and a single rounding.
+// bf16 outputs go through two 16 KB shared-memory tiles in the SW128 layout (row r's 16-byte
+// chunk j at chunk j ^ (r & 7): conflict-free) and leave as 64-column TMA bulk stores
+// (full lines, rows >= M and columns >= C_out clipped by the tensor map).
 template <int BN>
-__device__ __forceinline__ void epilogue_loop(const TcFpropArgs& a, uint32_t tmem, uint64_t* tfull, uint64_t* tempty,
-                                              int num_tiles) {
+__device__ __forceinline__ void epilogue_loop(const TcFpropArgs& a, const CUtensorMap* tmO, uint8_t* stage,
+                                              uint32_t tmem, uint64_t* tfull, uint64_t* tempty, int num_tiles) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = warp & 3;
   const int row = q * 32 + lane;
+  const bool leader = (threadIdx.x == 64);
   const float alpha = a.alpha ? *a.alpha : 1.0f;
-  int it = 0;
+  int it = 0, sg = 0;
   for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
     const int buf = it & 1;
     const int mt = tile / a.n_tiles, nt = tile - mt * a.n_tiles;
@@ -131,61 +137,99 @@ __device__ __forceinline__ void epilogue_loop(const TcFpropArgs& a, uint32_t tme
       }
     }
 #pragma unroll 1
-    for (int cb = 0; cb < BN; cb += 32) {
-      float v[32];
-      tc::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + buf * BN + cb, v);
-      const int col0 = nt * BN + cb;
-      if (!valid || col0 >= a.Cout) continue;
-      const bool full32 = (col0 + 32 <= a.Cout);
+    for (int g = 0; g < BN; g += 64) {
+      uint8_t* st = stage + (sg & 1) * kStageBytes;
+      if (a.tma_store) {
+        if (leader) tc::bulk_wait_read<1>();   // the store issued from this buffer two groups ago has read it
+        tc::named_bar(1, 128);
+      }
+#pragma unroll 1
+      for (int cb = g; cb < g + 64 && cb < BN; cb += 32) {
+        float v[32];
+        tc::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + buf * BN + cb, v);
+        const int col0 = nt * BN + cb;
+        const bool live = valid && col0 < a.Cout;
+        const bool full32 = (col0 + 32 <= a.Cout);
+        if (live) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] *= alpha;
-      if (a.relu_ref) {   // fused ReLU backward: keep the gradient where the forward input was > 0
-        const bf16* rr = reinterpret_cast<const bf16*>(a.relu_ref) + m * a.ldo + col0;
-        if (full32) {
-          float r[32];
-          load_row32_bf16(rr, r);
+          for (int j = 0; j < 32; ++j) v[j] *= alpha;
+          if (a.relu_ref) {   // fused ReLU backward: keep the gradient where the forward input was > 0
+            const bf16* rr = reinterpret_cast<const bf16*>(a.relu_ref) + m * a.ldo + col0;
+            if (full32) {
+              float r[32];
+              load_row32_bf16(rr, r);
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = r[j] > 0.0f ? v[j] : 0.0f;
-        } else {
-          for (int j = 0; j < 32 && col0 + j < a.Cout; ++j) v[j] = __bfloat162float(rr[j]) > 0.0f ? v[j] : 0.0f;
+              for (int j = 0; j < 32; ++j) v[j] = r[j] > 0.0f ? v[j] : 0.0f;
+            } else {
+              for (int j = 0; j < 32 && col0 + j < a.Cout; ++j) v[j] = __bfloat162float(rr[j]) > 0.0f ? v[j] : 0.0f;
+            }
+          }
+          if (a.bias) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (full32 || col0 + j < a.Cout) v[j] += a.bias[col0 + j];
+          }
+          if (a.residual) {
+            const bf16* rp = reinterpret_cast<const bf16*>(a.residual) + rbase + col0;
+            if (full32) {
+              float r[32];
+              load_row32_bf16(rp, r);
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] += r[j];
+            } else {
+              for (int j = 0; j < 32 && col0 + j < a.Cout; ++j) v[j] += __bfloat162float(rp[j]);
+            }
+          }
+        }
+        if (a.tma_store) {
+          // 4 x 16-byte chunks of this row into the swizzled staging tile
+          const int c0 = (cb - g) >> 3;
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq) {
+            uint4 u;
+            uint32_t* w = reinterpret_cast<uint32_t*>(&u);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              __nv_bfloat162 t2 = __floats2bfloat162_rn(v[qq * 8 + 2 * j], v[qq * 8 + 2 * j + 1]);
+              w[j] = *reinterpret_cast<uint32_t*>(&t2);
+            }
+            const int chunk = (c0 + qq) ^ (row & 7);
+            *reinterpret_cast<uint4*>(st + row * 128 + chunk * 16) = u;
+          }
+        } else if (live) {
+          if (a.out_f32) {
+            float* op = reinterpret_cast<float*>(a.out) + m * a.ldo + col0;
+            if (full32) {
+#pragma unroll
+              for (int j = 0; j < 32; j += 4)
+                *reinterpret_cast<float4*>(op + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+            } else {
+              for (int j = 0; j < 32 && col0 + j < a.Cout; ++j) op[j] = v[j];
+            }
+          } else {
+            bf16* op = reinterpret_cast<bf16*>(a.out) + m * a.ldo + col0;
+            if (full32) {
+              store_row32_bf16(op, v);
+            } else {
+              for (int j = 0; j < 32 && col0 + j < a.Cout; ++j) op[j] = __float2bfloat16_rn(v[j]);
+            }
+          }
         }
       }
-      if (a.bias) {
-#pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (full32 || col0 + j < a.Cout) v[j] += a.bias[col0 + j];
-      }
-      if (a.residual) {
-        const bf16* rp = reinterpret_cast<const bf16*>(a.residual) + rbase + col0;
-        if (full32) {
-          float r[32];
-          load_row32_bf16(rp, r);
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] += r[j];
-        } else {
-          for (int j = 0; j < 32 && col0 + j < a.Cout; ++j) v[j] += __bfloat162float(rp[j]);
+      if (a.tma_store) {
+        tc::fence_async_smem();
+        tc::named_bar(1, 128);
+        if (leader) {
+          tc::tma_store_2d(tmO, st, nt * BN + g, mt * kTileM);
+          tc::bulk_commit();
         }
-      }
-      if (a.out_f32) {
-        float* op = reinterpret_cast<float*>(a.out) + m * a.ldo + col0;
-        if (full32) {
-#pragma unroll
-          for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(op + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-        } else {
-          for (int j = 0; j < 32 && col0 + j < a.Cout; ++j) op[j] = v[j];
-        }
-      } else {
-        bf16* op = reinterpret_cast<bf16*>(a.out) + m * a.ldo + col0;
-        if (full32) {
-          store_row32_bf16(op, v);
-        } else {
-          for (int j = 0; j < 32 && col0 + j < a.Cout; ++j) op[j] = __float2bfloat16_rn(v[j]);
-        }
+        ++sg;
       }
     }
     tc::tc_fence_before();
     tc::mbar_arrive(&tempty[buf]);
   }
+  if (a.tma_store && leader) tc::bulk_wait_all();
 }
 
 // ===========================================================================
@@ -194,14 +238,15 @@ __device__ __forceinline__ void epilogue_loop(const TcFpropArgs& a, uint32_t tme
 template <int BN>
 __global__ void __launch_bounds__(192, 1)
     k_conv_fprop(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                 const TcFpropArgs a) {
+                 const __grid_constant__ CUtensorMap tmO, const TcFpropArgs a) {
   using C = FpropCfg<BN>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * C::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * C::B_BYTES);
+  uint8_t* sO = sB + STAGES * C::B_BYTES;            // 2 epilogue staging tiles
+  uint64_t* full = reinterpret_cast<uint64_t*>(sO + 2 * kStageBytes);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -282,7 +327,7 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else {
-    epilogue_loop<BN>(a, tmem, tfull, tempty, num_tiles);
+    epilogue_loop<BN>(a, &tmO, sO, tmem, tfull, tempty, num_tiles);
   }
   tc::tc_fence_before();
   __syncthreads();
@@ -404,39 +449,46 @@ __global__ void __launch_bounds__(192, 1)
 }
 
 // ===========================================================================
-// fprop / dgrad, 3x3, W % 128 == 0: halo-tile variant.  One M tile = 128 pixels of one
-// image row; per 64-channel chunk ONE TMA box {64, 130, 3, 1} (3 input rows x 130 columns,
-// zero-filled outside the image) is staged, and the 9 taps read it through descriptors
-// whose start address is shifted by (r * 130 + s) rows — the A operand is loaded once
-// per chunk instead of once per tap (2.95x less L2->SMEM traffic for A).
+// fprop / dgrad, 3x3: halo variants.  The A operand of the 9 taps is staged in
+// "units" that several taps share, each tap reading its unit through a descriptor
+// whose start address is shifted by whole 128-byte pixel rows (the SW128 swizzle is
+// a function of the absolute smem address, so any row offset is valid — verified
+// bit-exact, base-offset field 0):
+//   MODE 0 (W % 128 == 0, tile = 128 pixels of one row): one unit per 64-channel
+//          chunk = box {64, 130, 3, 1}; tap (r, s) starts at row r*130 + s
+//          (2.95x less A traffic than one box per tap);
+//   MODE 1 (16 <= W <= 64, tile = 128/W whole rows): three units per chunk, one per
+//          filter column s = box {64, W, 128/W + 2, 1} shifted by s - 1; tap (r, s)
+//          starts at row r*W of unit s (1.5x / 2x / 2.4x less A traffic at W = 64/32/16).
 // ===========================================================================
-constexpr uint32_t kHaloRows = 3 * 130;
-constexpr uint32_t kHaloBytes = ((kHaloRows * 128 + 1023) / 1024) * 1024;
-
-template <int BN>
+template <int BN, int MODE>
 struct HaloCfg {
+  static constexpr uint32_t UNIT_BYTES = MODE == 0 ? 50176 : 32768;   // 390 rows / (128/W + 2) * W rows
+  static constexpr int NA = MODE == 0 ? 2 : 3;
   static constexpr uint32_t B_BYTES = BN * 128;
-  static constexpr int STAGES_RAW = (kSmemBudget - 2 * (int)kHaloBytes) / (int)B_BYTES;
+  static constexpr int STAGES_RAW = (kSmemBudget - NA * (int)UNIT_BYTES) / (int)B_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr uint32_t TMEM_COLS = FpropCfg<BN>::TMEM_COLS;
-  static constexpr size_t SMEM = 1024 + 2 * kHaloBytes + STAGES * B_BYTES + 256;
+  static constexpr size_t SMEM = 1024 + NA * UNIT_BYTES + STAGES * B_BYTES + 2 * kStageBytes + 512;
 };
 
-template <int BN>
+template <int BN, int MODE>
 __global__ void __launch_bounds__(192, 1)
     k_conv_fprop_halo(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                      const TcFpropArgs a, const int use_base_off) {
-  using C = HaloCfg<BN>;
-  constexpr int STAGES = C::STAGES;
+                      const __grid_constant__ CUtensorMap tmO, const TcFpropArgs a, const uint32_t unit_tx) {
+  using C = HaloCfg<BN, MODE>;
+  constexpr int STAGES = C::STAGES, NA = C::NA;
+  constexpr int UNITS = MODE == 0 ? 1 : 3, TAPS_PER_UNIT = MODE == 0 ? 9 : 3;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  uint8_t* sH = smem;                                  // 2 halo buffers
-  uint8_t* sB = smem + 2 * kHaloBytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * C::B_BYTES);
+  uint8_t* sH = smem;
+  uint8_t* sB = smem + NA * C::UNIT_BYTES;
+  uint8_t* sO = sB + STAGES * C::B_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sO + 2 * kStageBytes);
   uint64_t* empty = full + STAGES;
   uint64_t* hfull = empty + STAGES;
-  uint64_t* hempty = hfull + 2;
-  uint64_t* tfull = hempty + 2;
+  uint64_t* hempty = hfull + NA;
+  uint64_t* tfull = hempty + NA;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -448,9 +500,11 @@ __global__ void __launch_bounds__(192, 1)
       tc::mbar_init(&full[s], 1);
       tc::mbar_init(&empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NA; ++b) {
       tc::mbar_init(&hfull[b], 1);
       tc::mbar_init(&hempty[b], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&tfull[b], 1);
       tc::mbar_init(&tempty[b], 128);
     }
@@ -472,16 +526,20 @@ __global__ void __launch_bounds__(192, 1)
         int n0, h0, w0;
         pix_origin(mt * kTileM, a.H, a.W, n0, h0, w0);
         for (int cc = 0; cc < a.c_chunks; ++cc) {
-          tc::mbar_wait(&hempty[hs], hphase ^ 1);
-          tc::mbar_expect_tx(&hfull[hs], kHaloRows * 128);
-          tc::tma_load_4d(sH + hs * kHaloBytes, &tmA, &hfull[hs], cc * 64, w0 - 1, h0 - 1, n0);
-          for (int tap = 0; tap < 9; ++tap) {
-            tc::mbar_wait(&empty[stage], phase ^ 1);
-            tc::mbar_expect_tx(&full[stage], C::B_BYTES);
-            tc::tma_load_3d(sB + stage * C::B_BYTES, &tmB, &full[stage], cc * 64, tap, nt * BN);
-            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          for (int u = 0; u < UNITS; ++u) {
+            tc::mbar_wait(&hempty[hs], hphase ^ 1);
+            tc::mbar_expect_tx(&hfull[hs], unit_tx);
+            tc::tma_load_4d(sH + hs * C::UNIT_BYTES, &tmA, &hfull[hs], cc * 64, w0 - 1 + (MODE == 0 ? 0 : u), h0 - 1,
+                            n0);
+            for (int j = 0; j < TAPS_PER_UNIT; ++j) {
+              const int tap = MODE == 0 ? j : j * 3 + u;
+              tc::mbar_wait(&empty[stage], phase ^ 1);
+              tc::mbar_expect_tx(&full[stage], C::B_BYTES);
+              tc::tma_load_3d(sB + stage * C::B_BYTES, &tmB, &full[stage], cc * 64, tap, nt * BN);
+              if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            }
+            if (++hs == NA) { hs = 0; hphase ^= 1; }
           }
-          if (++hs == 2) { hs = 0; hphase ^= 1; }
         }
       }
     }
@@ -496,33 +554,37 @@ __global__ void __launch_bounds__(192, 1)
         tc::mbar_wait(&tempty[buf], ((it >> 1) & 1) ^ 1);
         tc::tc_fence_after();
         const uint32_t d_tmem = tmem + buf * BN;
+        bool first = true;
         for (int cc = 0; cc < a.c_chunks; ++cc) {
-          tc::mbar_wait(&hfull[hs], hphase);
-          tc::tc_fence_after();
-          const uint32_t h_base = tc::smem_u32(sH + hs * kHaloBytes);
           const int ksteps = (cc == a.c_chunks - 1) ? a.last_ksteps : 4;
-          for (int tap = 0; tap < 9; ++tap) {
-            tc::mbar_wait(&full[stage], phase);
+          for (int u = 0; u < UNITS; ++u) {
+            tc::mbar_wait(&hfull[hs], hphase);
             tc::tc_fence_after();
-            const uint32_t row = (uint32_t)((tap / 3) * 130 + (tap % 3));
-            const uint32_t a_base = h_base + row * 128;
-            const uint32_t b_base = tc::smem_u32(sB + stage * C::B_BYTES);
-            for (int k = 0; k < ksteps; ++k) {
-              const uint64_t ad = tc::sdesc_sw128_off(a_base + k * 32, 16, 1024, use_base_off ? (row & 7) : 0);
-              const uint64_t bd = tc::sdesc_sw128(b_base + k * 32, 16, 1024);
-              tc::mma_bf16(d_tmem, ad, bd, idesc, (cc | tap | k) != 0);
+            const uint32_t h_base = tc::smem_u32(sH + hs * C::UNIT_BYTES);
+            for (int j = 0; j < TAPS_PER_UNIT; ++j) {
+              tc::mbar_wait(&full[stage], phase);
+              tc::tc_fence_after();
+              const uint32_t row = MODE == 0 ? (uint32_t)((j / 3) * 130 + (j % 3)) : (uint32_t)(j * a.W);
+              const uint32_t a_base = h_base + row * 128;
+              const uint32_t b_base = tc::smem_u32(sB + stage * C::B_BYTES);
+              for (int k = 0; k < ksteps; ++k) {
+                const uint64_t ad = tc::sdesc_sw128(a_base + k * 32, 16, 1024);
+                const uint64_t bd = tc::sdesc_sw128(b_base + k * 32, 16, 1024);
+                tc::mma_bf16(d_tmem, ad, bd, idesc, first ? 0u : 1u);
+                first = false;
+              }
+              tc::mma_commit(&empty[stage]);
+              if (++stage == STAGES) { stage = 0; phase ^= 1; }
             }
-            tc::mma_commit(&empty[stage]);
-            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            tc::mma_commit(&hempty[hs]);
+            if (++hs == NA) { hs = 0; hphase ^= 1; }
           }
-          tc::mma_commit(&hempty[hs]);
-          if (++hs == 2) { hs = 0; hphase ^= 1; }
         }
         tc::mma_commit(&tfull[buf]);
       }
     }
   } else {
-    epilogue_loop<BN>(a, tmem, tfull, tempty, num_tiles);
+    epilogue_loop<BN>(a, &tmO, sO, tmem, tfull, tempty, num_tiles);
   }
   tc::tc_fence_before();
   __syncthreads();
@@ -586,9 +648,21 @@ cudaError_t weight_map(CUtensorMap* m, const void* base, int rows, int taps, int
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+cudaError_t out_map(CUtensorMap* m, const void* base, long long M, int C, int ld) {
+  PG_CUDA(get_encoder());
+  cuuint64_t dims[2] = {(cuuint64_t)C, (cuuint64_t)M};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {64, 128};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 template <int BN>
-cudaError_t launch_fprop_bn(const CUtensorMap& ma, const CUtensorMap& mb, const TcFpropArgs& a, int num_sms,
-                            cudaStream_t st) {
+cudaError_t launch_fprop_bn(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo, const TcFpropArgs& a,
+                            int num_sms, cudaStream_t st) {
   using C = FpropCfg<BN>;
   static bool attr = false;
   if (!attr) {
@@ -597,15 +671,15 @@ cudaError_t launch_fprop_bn(const CUtensorMap& ma, const CUtensorMap& mb, const 
   }
   const int tiles = a.m_tiles * a.n_tiles;
   const int grid = tiles < num_sms ? tiles : num_sms;
-  k_conv_fprop<BN><<<grid, 192, C::SMEM, st>>>(ma, mb, a);
+  k_conv_fprop<BN><<<grid, 192, C::SMEM, st>>>(ma, mb, mo, a);
   return cudaGetLastError();
 }
 
-cudaError_t halo_map(CUtensorMap* m, const void* base, int N, int H, int W, int C) {
+cudaError_t halo_map(CUtensorMap* m, const void* base, int N, int H, int W, int C, int bw, int bh) {
   PG_CUDA(get_encoder());
   cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
   cuuint64_t strides[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
-  cuuint32_t box[4] = {64, 130, 3, 1};
+  cuuint32_t box[4] = {64, (cuuint32_t)bw, (cuuint32_t)bh, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -613,19 +687,33 @@ cudaError_t halo_map(CUtensorMap* m, const void* base, int N, int H, int W, int 
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-template <int BN>
-cudaError_t launch_halo_bn(const CUtensorMap& ma, const CUtensorMap& mb, const TcFpropArgs& a, int boff,
-                           cudaStream_t st) {
-  using C = HaloCfg<BN>;
+template <int BN, int MODE>
+cudaError_t launch_halo_bn(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo, const TcFpropArgs& a,
+                           uint32_t unit_tx, cudaStream_t st) {
+  using C = HaloCfg<BN, MODE>;
   static bool attr = false;
   if (!attr) {
-    PG_CUDA(cudaFuncSetAttribute(k_conv_fprop_halo<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    PG_CUDA(cudaFuncSetAttribute(k_conv_fprop_halo<BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)C::SMEM));
     attr = true;
   }
   const int tiles = a.m_tiles * a.n_tiles;
   const int grid = tiles < kNumSMs ? tiles : kNumSMs;
-  k_conv_fprop_halo<BN><<<grid, 192, C::SMEM, st>>>(ma, mb, a, boff);
+  k_conv_fprop_halo<BN, MODE><<<grid, 192, C::SMEM, st>>>(ma, mb, mo, a, unit_tx);
   return cudaGetLastError();
+}
+
+template <int MODE>
+cudaError_t launch_halo(int bn, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo,
+                        const TcFpropArgs& a, uint32_t unit_tx, cudaStream_t st) {
+  switch (bn) {
+    case 32: return launch_halo_bn<32, MODE>(ma, mb, mo, a, unit_tx, st);
+    case 64: return launch_halo_bn<64, MODE>(ma, mb, mo, a, unit_tx, st);
+    case 96: return launch_halo_bn<96, MODE>(ma, mb, mo, a, unit_tx, st);
+    case 128: return launch_halo_bn<128, MODE>(ma, mb, mo, a, unit_tx, st);
+    case 192: return launch_halo_bn<192, MODE>(ma, mb, mo, a, unit_tx, st);
+    default: return launch_halo_bn<256, MODE>(ma, mb, mo, a, unit_tx, st);
+  }
 }
 
 int env_int(const char* name, int dflt) {
@@ -702,26 +790,30 @@ cudaError_t tc_conv_fprop(const void* x, int N, int H, int W, int Cin, const voi
   a.out_f32 = epi.out_f32;
   a.ldo = epi.ldo ? epi.ldo : Cout;
   const int sms = kNumSMs;
-  static const int halo_on = env_int("PARAGAN_HALO", 1), halo_boff = env_int("PARAGAN_HALO_BOFF", 0);
+  static const int halo_on = env_int("PARAGAN_HALO", 1), tma_st = env_int("PARAGAN_TMA_STORE", 1);
+  CUtensorMap mo;
+  a.tma_store = tma_st && !a.out_f32 && (bn % 64 == 0 || a.n_tiles == 1) && a.ldo % 8 == 0 &&
+                !((uintptr_t)epi.out & 15);
+  if (a.tma_store) PG_CUDA(out_map(&mo, epi.out, a.M, Cout, a.ldo));
+  else mo = mb;   // unused
   if (halo_on && ksz == 3 && W % 128 == 0) {
     CUtensorMap mh;
-    PG_CUDA(halo_map(&mh, x, N, H, W, Cin));
-    switch (bn) {
-      case 32: return launch_halo_bn<32>(mh, mb, a, halo_boff, st);
-      case 64: return launch_halo_bn<64>(mh, mb, a, halo_boff, st);
-      case 96: return launch_halo_bn<96>(mh, mb, a, halo_boff, st);
-      case 128: return launch_halo_bn<128>(mh, mb, a, halo_boff, st);
-      case 192: return launch_halo_bn<192>(mh, mb, a, halo_boff, st);
-      default: return launch_halo_bn<256>(mh, mb, a, halo_boff, st);
-    }
+    PG_CUDA(halo_map(&mh, x, N, H, W, Cin, 130, 3));
+    return launch_halo<0>(bn, mh, mb, mo, a, 390u * 128u, st);
+  }
+  if (halo_on && ksz == 3 && W >= 16 && W <= 64 && H % (128 / W) == 0) {
+    const int rows = 128 / W + 2;
+    CUtensorMap mh;
+    PG_CUDA(halo_map(&mh, x, N, H, W, Cin, W, rows));
+    return launch_halo<1>(bn, mh, mb, mo, a, (uint32_t)(rows * W * 128), st);
   }
   switch (bn) {
-    case 32: return launch_fprop_bn<32>(ma, mb, a, sms, st);
-    case 64: return launch_fprop_bn<64>(ma, mb, a, sms, st);
-    case 96: return launch_fprop_bn<96>(ma, mb, a, sms, st);
-    case 128: return launch_fprop_bn<128>(ma, mb, a, sms, st);
-    case 192: return launch_fprop_bn<192>(ma, mb, a, sms, st);
-    default: return launch_fprop_bn<256>(ma, mb, a, sms, st);
+    case 32: return launch_fprop_bn<32>(ma, mb, mo, a, sms, st);
+    case 64: return launch_fprop_bn<64>(ma, mb, mo, a, sms, st);
+    case 96: return launch_fprop_bn<96>(ma, mb, mo, a, sms, st);
+    case 128: return launch_fprop_bn<128>(ma, mb, mo, a, sms, st);
+    case 192: return launch_fprop_bn<192>(ma, mb, mo, a, sms, st);
+    default: return launch_fprop_bn<256>(ma, mb, mo, a, sms, st);
   }
 }
 

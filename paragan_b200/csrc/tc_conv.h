@@ -28,6 +28,7 @@ struct TcFpropArgs {
   const void* relu_ref;
   void* out;
   int out_f32, ldo;
+  int tma_store;   // epilogue writes through SW128 staging tiles + TMA bulk stores
 };
 
 struct TcWgradArgs {

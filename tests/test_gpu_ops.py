@@ -66,6 +66,9 @@ CONV_SHAPES = [  # n, h, w, cin, cout, k
     (2, 4, 128, 96, 96, 3),      # halo-tile kernel (W % 128 == 0): 96 = 64 + 32 channels
     (1, 3, 256, 64, 192, 3),     # halo-tile kernel, two tiles per row
     (2, 2, 128, 192, 96, 3),     # halo-tile kernel, top and bottom rows out of the image
+    (2, 64, 64, 96, 192, 3),     # column-shifted halo units, W = 64 (2 rows per tile)
+    (2, 32, 32, 192, 96, 3),     # column-shifted halo units, W = 32
+    (1, 16, 16, 8, 32, 3),       # column-shifted halo units, W = 16, one K step
 ]
 
 
