@@ -768,7 +768,7 @@ class Engine final : public EngineBase {
     ab_ = A.get<float>((size_t)B * 2 * maxc_);
     bn_part_ = A.get<float>((size_t)B * 64 * 2 * maxc_);
     dpart_ = A.get<double>((size_t)kMaxPartialBlocks * 2 * std::max(maxc_, 16 * c0_));
-    tot_ = A.get<double>(2 * maxc_);
+    tot_ = A.get<double>(4 * maxc_);   // fp64 channel sums + fp32 means (bn_bwd_apply)
     size_t sf = std::max<size_t>((size_t)std::max(G_.n, D_.n), (size_t)B * 3 * R_ * R_);
     sf = std::max<size_t>(sf, (size_t)64 << 20);
     scratch_floats_ = sf;

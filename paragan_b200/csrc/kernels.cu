@@ -217,11 +217,13 @@ __global__ void __launch_bounds__(256) k_bn_stats(const T* __restrict__ x, long 
   }
 }
 __global__ void k_reduce_partials(const double* __restrict__ partial, int nblk, int width, double* __restrict__ out) {
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < width; c += gridDim.x * blockDim.x) {
-    double a = 0.0;
-    for (int b = 0; b < nblk; ++b) a += partial[(long long)b * width + c];
-    out[c] = a;
-  }
+  const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (c >= width) return;
+  double a = 0.0;
+  for (int b = lane; b < nblk; b += 32) a += partial[(long long)b * width + c];
+  a = warp_sum_d(a);
+  if (lane == 0) out[c] = a;
 }
 __global__ void k_bn_finalize(const double* __restrict__ sums, int C, double count, float eps,
                               float* __restrict__ mean, float* __restrict__ rstd) {
@@ -249,6 +251,22 @@ struct BnAffine {
       b = beta[c];
     }
   }
+  // 8 consecutive channels c0..c0+7 (c0 % 8 == 0, 16-byte aligned rows)
+  __device__ __forceinline__ void get8(int n, int c0, int C, float (&g)[8], float (&b)[8]) const {
+    if (gain) {
+      ld8(gain + (long long)n * C + c0, g);
+      ld8(bias + (long long)n * C + c0, b);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) g[j] += 1.0f;
+    } else {
+      ld8(gamma + c0, g);
+      ld8(beta + c0, b);
+    }
+  }
+  __device__ __forceinline__ static void ld8(const float* p, float (&v)[8]) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(p)), b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  }
 };
 
 template <typename TI, typename TO>
@@ -261,14 +279,14 @@ __global__ void k_bn_apply_relu(const TI* __restrict__ x, int N, int H, int W, i
     const int g = (int)(i % G);
     const long long p = i / G;
     const int n = (int)(p / ((long long)H * W));
-    float v[8];
+    float v[8], ga[8], be[8], mu[8], rs[8];
     Vec8<TI>::load(x + p * C + g * 8, v);
+    af.get8(n, g * 8, C, ga, be);
+    BnAffine::ld8(mean + g * 8, mu);
+    BnAffine::ld8(rstd + g * 8, rs);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const int c = g * 8 + j;
-      float ga, be;
-      af.get(n, c, C, ga, be);
-      const float t = (v[j] - mean[c]) * rstd[c] * ga + be;
+      const float t = (v[j] - mu[j]) * rs[j] * ga[j] + be[j];
       v[j] = t > 0.0f ? t : 0.0f;
     }
     if (!up2) {
@@ -325,12 +343,9 @@ __global__ void __launch_bounds__(256) k_bn_bwd_reduce(const TI* __restrict__ x,
   float sa[8] = {}, sb[8] = {};
   if (r < R) {
     float ga[8], be[8], mu[8], rs[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      af.get(n, g * 8 + j, C, ga[j], be[j]);
-      mu[j] = mean[g * 8 + j];
-      rs[j] = rstd[g * 8 + j];
-    }
+    af.get8(n, g * 8, C, ga, be);
+    BnAffine::ld8(mean + g * 8, mu);
+    BnAffine::ld8(rstd + g * 8, rs);
     for (long long q = q0 + r; q < q1; q += R) {
       const long long p = (long long)n * HW + q;
       float v[8], d[8];
@@ -384,8 +399,8 @@ __global__ void k_bn_bwd_totals(const float* __restrict__ AB, int N, int C, cons
 template <typename TI, typename TG, typename TO>
 __global__ void k_bn_bwd_apply(const TI* __restrict__ x, const TG* __restrict__ dy, int N, int H, int W, int C,
                                const float* __restrict__ mean, const float* __restrict__ rstd, BnAffine af, int up2,
-                               const double* __restrict__ tot, double count, const TO* __restrict__ add,
-                               TO* __restrict__ dx) {
+                               const float* __restrict__ mgrad, const TO* __restrict__ add, TO* __restrict__ dx) {
+  // mgrad[c] = mean over the global batch of g * g0, mgrad[C + c] = mean of g * g0 * x_hat
   const int G = C >> 3;
   const long long total = (long long)N * H * W * G;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
@@ -393,25 +408,31 @@ __global__ void k_bn_bwd_apply(const TI* __restrict__ x, const TG* __restrict__ 
     const int g = (int)(i % G);
     const long long p = i / G;
     const int n = (int)(p / ((long long)H * W));
-    float v[8], d[8], o[8];
+    float v[8], d[8], o[8], ga[8], be[8], mu[8], rs[8], mg[8], mgx[8];
     Vec8<TI>::load(x + p * C + g * 8, v);
     load_dy<TG>(dy, p, n, H, W, C, g, up2, d);
+    af.get8(n, g * 8, C, ga, be);
+    BnAffine::ld8(mean + g * 8, mu);
+    BnAffine::ld8(rstd + g * 8, rs);
+    BnAffine::ld8(mgrad + g * 8, mg);
+    BnAffine::ld8(mgrad + C + g * 8, mgx);
     float ad[8];
     if (add) Vec8<TO>::load(add + p * C + g * 8, ad);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const int c = g * 8 + j;
-      float ga, be;
-      af.get(n, c, C, ga, be);
-      const float xh = (v[j] - mean[c]) * rstd[c];
-      const float z = xh * ga + be;
+      const float xh = (v[j] - mu[j]) * rs[j];
+      const float z = xh * ga[j] + be[j];
       const float g0 = z > 0.0f ? d[j] : 0.0f;
-      const float mg = (float)(tot[c] / count), mgx = (float)(tot[C + c] / count);
-      o[j] = rstd[c] * (ga * g0 - mg - xh * mgx);
+      o[j] = rs[j] * (ga[j] * g0 - mg[j] - xh * mgx[j]);
       if (add) o[j] += ad[j];
     }
     Vec8<TO>::store(dx + p * C + g * 8, o);
   }
+}
+__global__ void k_bn_bwd_means(const double* __restrict__ tot, int C, double count, float* __restrict__ mgrad) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= 2 * C) return;
+  mgrad[c] = (float)(tot[c] / count);
 }
 
 // ===================================================================== elementwise
@@ -513,6 +534,28 @@ __global__ void __launch_bounds__(256) k_col_sum(const T* __restrict__ x, long l
     __syncthreads();
   }
 }
+// C <= 8: thread-private sums of all channels over a strided pixel range, block combine in fp64
+template <typename T>
+__global__ void __launch_bounds__(256) k_col_sum_small(const T* __restrict__ x, long long M, int C,
+                                                       double* __restrict__ partial, long long pix_per_blk) {
+  __shared__ double sh[8][33];
+  const long long p0 = (long long)blockIdx.x * pix_per_blk;
+  const long long p1 = min(M, p0 + pix_per_blk);
+  float s[8] = {};
+  for (long long p = p0 + threadIdx.x; p < p1; p += blockDim.x)
+    for (int c = 0; c < C; ++c) s[c] += to_f<T>(x[p * C + c]);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int c = 0; c < C; ++c) {
+    const double v = warp_sum_d((double)s[c]);
+    if (lane == 0) sh[c][wid] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < C) {
+    double a = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) a += sh[threadIdx.x][w];
+    partial[(long long)blockIdx.x * C + threadIdx.x] = a;
+  }
+}
 template <typename T>
 __global__ void __launch_bounds__(256) k_col_sum_vec(const T* __restrict__ x, long long M, int C,
                                                      double* __restrict__ partial, long long pix_per_blk) {
@@ -523,7 +566,17 @@ __global__ void __launch_bounds__(256) k_col_sum_vec(const T* __restrict__ x, lo
   const long long p1 = min(M, p0 + pix_per_blk);
   float s[8] = {};
   if (r < R) {
-    for (long long p = p0 + r; p < p1; p += R) {
+    long long p = p0 + r;
+    for (; p + 3 * R < p1; p += 4 * R) {   // four independent 16-byte loads in flight
+      float v0[8], v1[8], v2[8], v3[8];
+      Vec8<T>::load(x + p * C + g * 8, v0);
+      Vec8<T>::load(x + (p + R) * C + g * 8, v1);
+      Vec8<T>::load(x + (p + 2 * R) * C + g * 8, v2);
+      Vec8<T>::load(x + (p + 3 * R) * C + g * 8, v3);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) s[j] += (v0[j] + v1[j]) + (v2[j] + v3[j]);
+    }
+    for (; p < p1; p += R) {
       float v[8];
       Vec8<T>::load(x + p * C + g * 8, v);
 #pragma unroll
@@ -541,11 +594,14 @@ __global__ void __launch_bounds__(256) k_col_sum_vec(const T* __restrict__ x, lo
 }
 __global__ void k_reduce_partials_f32(const double* __restrict__ partial, int nblk, int width, float* __restrict__ out,
                                       int accumulate) {
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < width; c += gridDim.x * blockDim.x) {
-    double a = accumulate ? (double)out[c] : 0.0;
-    for (int b = 0; b < nblk; ++b) a += partial[(long long)b * width + c];
-    out[c] = (float)a;
-  }
+  // one warp per column: lane l sums blocks l, l+32, ... then a fixed shuffle tree (deterministic)
+  const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (c >= width) return;
+  double a = 0.0;
+  for (int b = lane; b < nblk; b += 32) a += partial[(long long)b * width + c];
+  a = warp_sum_d(a);
+  if (lane == 0) out[c] = (float)(accumulate ? (double)out[c] + a : a);
 }
 
 // ===================================================================== G output / tanh
@@ -1388,7 +1444,7 @@ cudaError_t bn_stats(const T* x, long long M, int C, double* partial, int max_bl
   if (sm > 48 * 1024) PG_CUDA(cudaFuncSetAttribute(k_bn_stats<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   k_bn_stats<T><<<nblk, 256, sm, st>>>(x, M, C, partial, per);
   PG_LAUNCH_CHECK();
-  k_reduce_partials<<<ceil_div(2 * C, 256), 256, 0, st>>>(partial, nblk, 2 * C, sums);
+  k_reduce_partials<<<ceil_div(2 * C, 8), 256, 0, st>>>(partial, nblk, 2 * C, sums);
   return cudaGetLastError();
 }
 template cudaError_t bn_stats<float>(const float*, long long, int, double*, int, double*, cudaStream_t);
@@ -1454,9 +1510,13 @@ template <typename TI, typename TG, typename TO>
 cudaError_t bn_bwd_apply(const TI* x, const TG* dy, int N, int H, int W, int C, const float* mean, const float* rstd,
                          const float* gain, const float* bias, const float* gamma, const float* beta, bool up2,
                          const double* tot, double count, const TO* add, TO* dx, cudaStream_t st) {
+  // tot (all-reduced channel sums, fp64) -> per-channel means in fp32, kept in the tail of tot's buffer
+  float* mgrad = reinterpret_cast<float*>(const_cast<double*>(tot) + 2 * C);
+  k_bn_bwd_means<<<ceil_div(2 * C, 256), 256, 0, st>>>(tot, C, count, mgrad);
+  PG_LAUNCH_CHECK();
   const long long total = (long long)N * H * W * (C / 8);
   k_bn_bwd_apply<TI, TG, TO><<<grid_for(total, 256), 256, 0, st>>>(
-      x, dy, N, H, W, C, mean, rstd, BnAffine{gain, bias, gamma, beta}, up2 ? 1 : 0, tot, count, add, dx);
+      x, dy, N, H, W, C, mean, rstd, BnAffine{gain, bias, gamma, beta}, up2 ? 1 : 0, mgrad, add, dx);
   return cudaGetLastError();
 }
 template cudaError_t bn_bwd_apply<float, float, float>(const float*, const float*, int, int, int, int, const float*,
@@ -1542,7 +1602,9 @@ cudaError_t col_sum(const T* dy, long long M, int C, double* partial, int max_bl
   int nblk = (int)((M + 1023) / 1024);
   if (nblk > max_blocks) nblk = max_blocks;
   const long long per = (M + nblk - 1) / nblk;
-  if (C % 8 == 0 && C / 8 <= 256) {
+  if (C <= 8) {
+    k_col_sum_small<T><<<nblk, 256, 0, st>>>(dy, M, C, partial, per);
+  } else if (C % 8 == 0 && C / 8 <= 256) {
     const int R = 256 / (C / 8);
     const size_t sm = (size_t)R * C * sizeof(float);
     if (sm > 48 * 1024)
@@ -1552,7 +1614,7 @@ cudaError_t col_sum(const T* dy, long long M, int C, double* partial, int max_bl
     k_col_sum<T><<<nblk, 256, 256 * sizeof(double), st>>>(dy, M, C, partial, per);
   }
   PG_LAUNCH_CHECK();
-  k_reduce_partials_f32<<<ceil_div(C, 256), 256, 0, st>>>(partial, nblk, C, db, accumulate);
+  k_reduce_partials_f32<<<ceil_div(C, 8), 256, 0, st>>>(partial, nblk, C, db, accumulate);
   return cudaGetLastError();
 }
 template <typename T>
