@@ -1206,9 +1206,12 @@ class Engine final : public EngineBase {
       // G_o = wgrad(o, dout) unscaled; dgamma = <W_o/sigma, G_o>; dW_o_hat = gamma * G_o
       float* go = N.G(a.oc.w);
       CKS(conv_wgrad(N, a.ov, dout, n, H, a.oc));
-      const int job = N.E[a.oc.w].job;
-      CK(dot_f32(N.P(a.oc.w), go, (long long)a.C * a.C2, N.G(a.gamma), 0, st_));
-      CK(scale_dev(N.G(a.gamma), 1, N.sigma + 2 * job + 1, st_));
+      // dgamma against the very operand the forward used (W_o/sigma as packed, bf16 in BF16 mode)
+      if constexpr (kBF) {
+        CK(dot_bf16_f32(static_cast<const bf16*>(a.oc.wp), go, (long long)a.C * a.C2, N.G(a.gamma), 0, st_));
+      } else {
+        CK(dot_f32(static_cast<const float*>(a.oc.wp), go, (long long)a.C * a.C2, N.G(a.gamma), 0, st_));
+      }
       CK(scale_dev(go, (long long)a.C * a.C2, N.P(a.gamma), st_));
     }
     CKS(conv_dgrad(dout, n, H, a.oc, dO, nullptr, N.P(a.gamma)));   // dO = gamma * W_o^T dout

@@ -263,9 +263,15 @@ struct BnAffine {
       ld8(beta + c0, b);
     }
   }
+  // 8 floats; vector loads when 16-byte aligned (parameter slots inside the flat buffer may not be)
   __device__ __forceinline__ static void ld8(const float* p, float (&v)[8]) {
-    const float4 a = __ldg(reinterpret_cast<const float4*>(p)), b = __ldg(reinterpret_cast<const float4*>(p) + 1);
-    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+      const float4 a = __ldg(reinterpret_cast<const float4*>(p)), b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = __ldg(p + j);
+    }
   }
 };
 
@@ -1239,10 +1245,11 @@ __global__ void k_scale_dev(float* p, long long n, const float* s) {
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     p[i] *= f;
 }
-__global__ void k_dot(const float* __restrict__ a, const float* __restrict__ b, long long n, float* out, int acc) {
+template <typename TA>
+__global__ void k_dot(const TA* __restrict__ a, const float* __restrict__ b, long long n, float* out, int acc) {
   __shared__ double red[32];
   double s = 0.0;
-  for (long long i = threadIdx.x; i < n; i += blockDim.x) s += (double)a[i] * (double)b[i];
+  for (long long i = threadIdx.x; i < n; i += blockDim.x) s += (double)to_f<TA>(a[i]) * (double)b[i];
   s = warp_sum_d(s);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
   __syncthreads();
@@ -1797,7 +1804,11 @@ cudaError_t scale_dev(float* p, long long n, const float* s, cudaStream_t st) {
   return cudaGetLastError();
 }
 cudaError_t dot_f32(const float* a, const float* b, long long n, float* out, int accumulate, cudaStream_t st) {
-  k_dot<<<1, 1024, 0, st>>>(a, b, n, out, accumulate);
+  k_dot<float><<<1, 1024, 0, st>>>(a, b, n, out, accumulate);
+  return cudaGetLastError();
+}
+cudaError_t dot_bf16_f32(const bf16* a, const float* b, long long n, float* out, int accumulate, cudaStream_t st) {
+  k_dot<bf16><<<1, 1024, 0, st>>>(a, b, n, out, accumulate);
   return cudaGetLastError();
 }
 cudaError_t copy_rows_cols(const float* src, long long lds, long long rows, int cols, float* dst, long long ldd,

@@ -212,6 +212,7 @@ cudaError_t scale_f32(float* p, long long n, float s, cudaStream_t st);
 cudaError_t scale_dev(float* p, long long n, const float* s, cudaStream_t st);
 // out[0] (+)= sum_i a[i]*b[i]  (fp64 accumulation, single block)
 cudaError_t dot_f32(const float* a, const float* b, long long n, float* out, int accumulate, cudaStream_t st);
+cudaError_t dot_bf16_f32(const bf16* a, const float* b, long long n, float* out, int accumulate, cudaStream_t st);
 // dst[r*ldd + j] (+)= src[r*lds + j] for j < cols
 cudaError_t copy_rows_cols(const float* src, long long lds, long long rows, int cols, float* dst, long long ldd,
                            int accumulate, cudaStream_t st);
