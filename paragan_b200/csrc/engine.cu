@@ -339,6 +339,7 @@ class Engine final : public EngineBase {
     CKS(d_forward(2 * B_));
     CK(hinge_loss(logits_, B_, 0, dlogits_, D_.loss, st_));
     ++launches_;
+    CKS(allreduce_loss(D_.loss));
     CK(cudaMemsetAsync(D_.g, 0, sizeof(float) * D_.n, st_));
     CKS(d_backward(2 * B_, true, false));
     CKS(sn_backward_net(D_));
@@ -362,6 +363,7 @@ class Engine final : public EngineBase {
     CKS(d_forward(B_));
     CK(hinge_loss(logits_, B_, 1, dlogits_, G_.loss, st_));
     ++launches_;
+    CKS(allreduce_loss(G_.loss));
     CK(cudaMemsetAsync(G_.g, 0, sizeof(float) * G_.n, st_));
     CKS(d_backward(B_, false, true));   // dgrad only, down to the image
     CKS(g_backward());
@@ -411,10 +413,11 @@ class Engine final : public EngineBase {
     paragan_status s = sync_ok();
     if (s != PARAGAN_OK) return s;
     if (out) {
-      out->d_loss = ld[0];
-      out->d_real_mean = ld[1];
-      out->d_fake_mean = ld[2];
-      out->g_loss = lg[0];
+      const float inv = 1.0f / cfg_.world_size;
+      out->d_loss = ld[0] * inv;
+      out->d_real_mean = ld[1] * inv;
+      out->d_fake_mean = ld[2] * inv;
+      out->g_loss = lg[0] * inv;
       out->nonfinite = nf;
       out->t_d = td;
       out->t_g = tg;
@@ -1110,6 +1113,15 @@ class Engine final : public EngineBase {
       if (r != ncclSuccess) return fail_msg(PARAGAN_ERR_NCCL, std::string("bn allreduce: ") + ncclGetErrorString(r));
     }
     CK(bn_finalize(sums, C, (double)M * cfg_.world_size, cfg_.bn_eps, mean, rstd, st_));
+    return PARAGAN_OK;
+  }
+  // losses / logit means are local means: sum over ranks here, / world_size in sync_stats (R15);
+  // the non-finite flag (loss[3]) becomes the number of ranks that saw one
+  paragan_status allreduce_loss(float* loss4) {
+    if (cfg_.world_size > 1) {
+      ncclResult_t r = ncclAllReduce(loss4, loss4, 4, ncclFloat32, ncclSum, comm_, st_);
+      if (r != ncclSuccess) return fail_msg(PARAGAN_ERR_NCCL, std::string("loss allreduce: ") + ncclGetErrorString(r));
+    }
     return PARAGAN_OK;
   }
   paragan_status allreduce_small(double* p, int n) {

@@ -242,15 +242,6 @@ struct BnAffine {
   const float* bias;   // [N][C]
   const float* gamma;  // [C]    (plain BN)
   const float* beta;   // [C]
-  __device__ __forceinline__ void get(int n, int c, int C, float& g, float& b) const {
-    if (gain) {
-      g = 1.0f + gain[(long long)n * C + c];
-      b = bias[(long long)n * C + c];
-    } else {
-      g = gamma[c];
-      b = beta[c];
-    }
-  }
   // 8 consecutive channels c0..c0+7 (c0 % 8 == 0, 16-byte aligned rows)
   __device__ __forceinline__ void get8(int n, int c0, int C, float (&g)[8], float (&b)[8]) const {
     if (gain) {
