@@ -269,13 +269,14 @@ struct BnAffine {
 template <typename TI, typename TO>
 __global__ void k_bn_apply_relu(const TI* __restrict__ x, int N, int H, int W, int C, const float* __restrict__ mean,
                                 const float* __restrict__ rstd, BnAffine af, TO* __restrict__ y, int up2) {
-  const int G = C >> 3;
-  const long long total = (long long)N * H * W * G;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int g = (int)(i % G);
-    const long long p = i / G;
-    const int n = (int)(p / ((long long)H * W));
+  // 32-bit index arithmetic (every tensor here has < 2^31 elements): 64-bit div/mod dominated the loop
+  const unsigned G = C >> 3, HW = (unsigned)(H * W);
+  const unsigned total = (unsigned)N * HW * G;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const unsigned g = i % G;
+    const unsigned pp = i / G;
+    const long long p = pp;
+    const int n = (int)(pp / HW);
     float v[8], ga[8], be[8], mu[8], rs[8];
     Vec8<TI>::load(x + p * C + g * 8, v);
     af.get8(n, g * 8, C, ga, be);
@@ -289,8 +290,8 @@ __global__ void k_bn_apply_relu(const TI* __restrict__ x, int N, int H, int W, i
     if (!up2) {
       Vec8<TO>::store(y + p * C + g * 8, v);
     } else {
-      const int rem = (int)(p - (long long)n * H * W);
-      const int h = rem / W, w = rem - (rem / W) * W;
+      const unsigned rem = pp - (unsigned)n * HW;
+      const int h = (int)(rem / (unsigned)W), w = (int)(rem - (unsigned)h * W);
       const long long W2 = 2 * W;
       const long long base = ((long long)n * 2 * H + 2 * h) * W2 + 2 * w;
       Vec8<TO>::store(y + (base)*C + g * 8, v);
@@ -308,8 +309,8 @@ __device__ __forceinline__ void load_dy(const TG* dy, long long p, int n, int H,
   if (!up2) {
     Vec8<TG>::load(dy + p * C + g * 8, d);
   } else {
-    const int rem = (int)(p - (long long)n * H * W);
-    const int h = rem / W, w = rem - (rem / W) * W;
+    const unsigned rem = (unsigned)p - (unsigned)n * (unsigned)(H * W);
+    const int h = (int)(rem / (unsigned)W), w = (int)(rem - (unsigned)h * W);
     const long long W2 = 2 * W;
     const long long base = ((long long)n * 2 * H + 2 * h) * W2 + 2 * w;
     float a[8], b[8], c[8], e[8];
@@ -398,13 +399,12 @@ __global__ void k_bn_bwd_apply(const TI* __restrict__ x, const TG* __restrict__ 
                                const float* __restrict__ mean, const float* __restrict__ rstd, BnAffine af, int up2,
                                const float* __restrict__ mgrad, const TO* __restrict__ add, TO* __restrict__ dx) {
   // mgrad[c] = mean over the global batch of g * g0, mgrad[C + c] = mean of g * g0 * x_hat
-  const int G = C >> 3;
-  const long long total = (long long)N * H * W * G;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int g = (int)(i % G);
+  const unsigned G = C >> 3, HW = (unsigned)(H * W);
+  const unsigned total = (unsigned)N * HW * G;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const unsigned g = i % G;
     const long long p = i / G;
-    const int n = (int)(p / ((long long)H * W));
+    const int n = (int)((unsigned)p / HW);
     float v[8], d[8], o[8], ga[8], be[8], mu[8], rs[8], mg[8], mgx[8];
     Vec8<TI>::load(x + p * C + g * 8, v);
     load_dy<TG>(dy, p, n, H, W, C, g, up2, d);
@@ -1280,16 +1280,15 @@ __global__ void k_relu_copy_v(const T* __restrict__ x, T* __restrict__ y, long l
 template <typename T>
 __global__ void k_avgpool2_v(const T* __restrict__ x, int N, int H, int W, int C, int ldx, const T* __restrict__ add,
                              T* __restrict__ y) {
-  const int Ho = H >> 1, Wo = W >> 1, G = C >> 3;
-  const long long total = (long long)N * Ho * Wo * G;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int g = (int)(i % G);
-    long long p = i / G;
-    const int wo = (int)(p % Wo);
+  const unsigned Ho = H >> 1, Wo = W >> 1, G = C >> 3;
+  const unsigned total = (unsigned)N * Ho * Wo * G;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const unsigned g = i % G;
+    unsigned p = i / G;
+    const unsigned wo = p % Wo;
     p /= Wo;
-    const int ho = (int)(p % Ho);
-    const int n = (int)(p / Ho);
+    const unsigned ho = p % Ho;
+    const unsigned n = p / Ho;
     const long long b = ((long long)n * H + 2 * ho) * W + 2 * wo;
     float a0[8], a1[8], a2[8], a3[8], o[8];
     Vec8<T>::load(x + b * ldx + g * 8, a0);
@@ -1297,31 +1296,30 @@ __global__ void k_avgpool2_v(const T* __restrict__ x, int N, int H, int W, int C
     Vec8<T>::load(x + (b + W) * ldx + g * 8, a2);
     Vec8<T>::load(x + (b + W + 1) * ldx + g * 8, a3);
     float ad[8];
-    if (add) Vec8<T>::load(add + i * 8, ad);
+    if (add) Vec8<T>::load(add + (long long)i * 8, ad);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       o[j] = ((a0[j] + a1[j]) + (a2[j] + a3[j])) * 0.25f;
       if (add) o[j] += ad[j];
     }
-    Vec8<T>::store(y + i * 8, o);
+    Vec8<T>::store(y + (long long)i * 8, o);
   }
 }
 template <typename T>
 __global__ void k_avgpool2_bwd_v(const T* __restrict__ dy, int N, int H, int W, int C, const T* __restrict__ add,
                                  T* __restrict__ dx, int lddx) {
   // one thread per (output-grad pixel of the pooled map, 8 channels): writes its 2x2 block
-  const int Ho = H >> 1, Wo = W >> 1, G = C >> 3;
-  const long long total = (long long)N * Ho * Wo * G;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int g = (int)(i % G);
-    long long p = i / G;
-    const int wo = (int)(p % Wo);
+  const unsigned Ho = H >> 1, Wo = W >> 1, G = C >> 3;
+  const unsigned total = (unsigned)N * Ho * Wo * G;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const unsigned g = i % G;
+    unsigned p = i / G;
+    const unsigned wo = p % Wo;
     p /= Wo;
-    const int ho = (int)(p % Ho);
-    const int n = (int)(p / Ho);
+    const unsigned ho = p % Ho;
+    const unsigned n = p / Ho;
     float v[8];
-    Vec8<T>::load(dy + i * 8, v);
+    Vec8<T>::load(dy + (long long)i * 8, v);
 #pragma unroll
     for (int j = 0; j < 8; ++j) v[j] *= 0.25f;
     const long long b = ((long long)n * H + 2 * ho) * W + 2 * wo;
@@ -1343,16 +1341,15 @@ __global__ void k_avgpool2_bwd_v(const T* __restrict__ dy, int N, int H, int W, 
 }
 template <typename T>
 __global__ void k_up2_bwd_v(const T* __restrict__ dy, int N, int H, int W, int C, T* __restrict__ dx) {
-  const int G = C >> 3;
-  const long long total = (long long)N * H * W * G;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int g = (int)(i % G);
-    long long p = i / G;
-    const int w = (int)(p % W);
-    p /= W;
-    const int h = (int)(p % H);
-    const int n = (int)(p / H);
+  const unsigned G = C >> 3;
+  const unsigned total = (unsigned)N * H * W * G;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const unsigned g = i % G;
+    unsigned p = i / G;
+    const unsigned w = p % (unsigned)W;
+    p /= (unsigned)W;
+    const unsigned h = p % (unsigned)H;
+    const unsigned n = p / (unsigned)H;
     const long long W2 = 2 * W;
     const long long b = ((long long)n * 2 * H + 2 * h) * W2 + 2 * w;
     float a0[8], a1[8], a2[8], a3[8], o[8];
@@ -1362,7 +1359,7 @@ __global__ void k_up2_bwd_v(const T* __restrict__ dy, int N, int H, int W, int C
     Vec8<T>::load(dy + (b + W2 + 1) * C + g * 8, a3);
 #pragma unroll
     for (int j = 0; j < 8; ++j) o[j] = (a0[j] + a1[j]) + (a2[j] + a3[j]);
-    Vec8<T>::store(dx + i * 8, o);
+    Vec8<T>::store(dx + (long long)i * 8, o);
   }
 }
 
