@@ -108,18 +108,26 @@ __device__ __forceinline__ void load_row32_bf16(const bf16* src, float (&r)[32])
 // bf16 outputs go through two 16 KB shared-memory tiles in the SW128 layout (row r's 16-byte
 // chunk j at chunk j ^ (r & 7): conflict-free) and leave as 64-column TMA bulk stores
 // (full lines, rows >= M and columns >= C_out clipped by the tensor map).
-template <int BN>
+// CG = 2: tiles are CTA-pair tiles (M = 256); this CTA owns M rows [rank * 128, rank * 128 + 128)
+// and releases the accumulator on the leader CTA's barrier.
+template <int BN, int CG = 1>
 __device__ __forceinline__ void epilogue_loop(const TcFpropArgs& a, const CUtensorMap* tmO, uint8_t* stage,
-                                              uint32_t tmem, uint64_t* tfull, uint64_t* tempty, int num_tiles) {
+                                              uint32_t tmem, uint64_t* tfull, uint64_t* tempty, int num_tiles,
+                                              int tile0 = -1, int tile_step = 0, int rank = 0) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = warp & 3;
   const int row = q * 32 + lane;
   const bool leader = (threadIdx.x == 64);
   const float alpha = a.alpha ? *a.alpha : 1.0f;
+  if (tile0 < 0) {
+    tile0 = blockIdx.x;
+    tile_step = gridDim.x;
+  }
   int it = 0, sg = 0;
-  for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+  for (int tile = tile0; tile < num_tiles; tile += tile_step, ++it) {
     const int buf = it & 1;
-    const int mt = tile / a.n_tiles, nt = tile - mt * a.n_tiles;
+    const int nt = tile % a.n_tiles;
+    const int mt = CG == 2 ? (tile / a.n_tiles) * 2 + rank : tile / a.n_tiles;
     tc::mbar_wait(&tfull[buf], (it >> 1) & 1);
     tc::tc_fence_after();
     const long long m = (long long)mt * kTileM + row;
@@ -227,7 +235,8 @@ __device__ __forceinline__ void epilogue_loop(const TcFpropArgs& a, const CUtens
       }
     }
     tc::tc_fence_before();
-    tc::mbar_arrive(&tempty[buf]);
+    if (CG == 2) tc::mbar_arrive_cluster(tc::map_to_rank(&tempty[buf], 0));
+    else tc::mbar_arrive(&tempty[buf]);
   }
   if (a.tma_store && leader) tc::bulk_wait_all();
 }
@@ -591,6 +600,161 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 1) tc::tmem_dealloc(tmem, C::TMEM_COLS);
 }
 
+// ===========================================================================
+// CTA-pair (cta_group::2) fprop / dgrad.  Two CTAs of a cluster share one M = 256 x BN
+// tile: each stages its own 128 pixel rows of A and HALF of the B tile (BN/2 weight rows),
+// the leader issues tcgen05.mma.cta_group::2 over both CTAs' shared memory, and each
+// CTA's TMEM holds its 128 accumulator rows.  Per SM this halves the B traffic at the
+// same MMA rate.  A is staged in "units" as in the halo kernels; MODE 2 is the plain
+// one-box-per-tap layout (any geometry).
+// ===========================================================================
+template <int BN, int MODE>
+struct Cg2Cfg {
+  static constexpr uint32_t UNIT_BYTES = MODE == 0 ? 50176 : (MODE == 1 ? 32768 : kAtomBytes);
+  static constexpr int NA = MODE == 0 ? 2 : (MODE == 1 ? 3 : 4);
+  static constexpr uint32_t B_BYTES = (BN / 2) * 128;
+  static constexpr int STAGES_RAW = (kSmemBudget - NA * (int)UNIT_BYTES) / (int)B_BYTES;
+  static constexpr int STAGES = STAGES_RAW > 12 ? 12 : STAGES_RAW;
+  static constexpr uint32_t TMEM_COLS = FpropCfg<BN>::TMEM_COLS;
+  static constexpr size_t SMEM = 1024 + NA * UNIT_BYTES + STAGES * B_BYTES + 2 * kStageBytes + 512;
+};
+
+template <int BN, int MODE>
+__global__ void __launch_bounds__(192, 1)
+    k_conv_fprop_cg2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const __grid_constant__ CUtensorMap tmO, const TcFpropArgs a, const uint32_t unit_tx) {
+  using C = Cg2Cfg<BN, MODE>;
+  constexpr int STAGES = C::STAGES, NA = C::NA;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint8_t* sH = smem;
+  uint8_t* sB = smem + NA * C::UNIT_BYTES;
+  uint8_t* sO = sB + STAGES * C::B_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sO + 2 * kStageBytes);
+  uint64_t* empty = full + STAGES;
+  uint64_t* hfull = empty + STAGES;
+  uint64_t* hempty = hfull + NA;
+  uint64_t* tfull = hempty + NA;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = tc::cluster_rank();
+  const bool is_leader = rank == 0;
+  if (warp == 0 && lane == 0) {
+    tc::tma_prefetch(&tmA);
+    tc::tma_prefetch(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < NA; ++b) {
+      tc::mbar_init(&hfull[b], 1);
+      tc::mbar_init(&hempty[b], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&tfull[b], 1);
+      tc::mbar_init(&tempty[b], 256);   // both CTAs' epilogue threads (leader's copy is the one used)
+    }
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc_cg2(tmem_slot, C::TMEM_COLS);
+  tc::tc_fence_before();
+  tc::cluster_sync();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int mpairs = (a.m_tiles + 1) / 2;
+  const int num_tiles = mpairs * a.n_tiles;
+  const int cid = (int)tc::cluster_id_x(), ncl = (int)tc::num_clusters_x();
+  constexpr int UNITS_PER_CHUNK_FIXED = MODE == 0 ? 1 : (MODE == 1 ? 3 : 0);
+  const int units_per_chunk = MODE == 2 ? a.taps : UNITS_PER_CHUNK_FIXED;
+  const int taps_per_unit = MODE == 0 ? 9 : (MODE == 1 ? 3 : 1);
+  const int pad = a.ksz >> 1;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0, hs = 0;
+      uint32_t phase = 0, hphase = 0;
+      for (int tile = cid; tile < num_tiles; tile += ncl) {
+        const int nt = tile % a.n_tiles;
+        const int mt = (tile / a.n_tiles) * 2 + (int)rank;
+        int n0, h0, w0;
+        pix_origin(mt * kTileM, a.H, a.W, n0, h0, w0);
+        for (int cc = 0; cc < a.c_chunks; ++cc) {
+          for (int u = 0; u < units_per_chunk; ++u) {
+            tc::mbar_wait(&hempty[hs], hphase ^ 1);
+            const uint32_t hbar = tc::map_to_rank(&hfull[hs], 0);
+            if (is_leader) tc::mbar_expect_tx(&hfull[hs], 2 * unit_tx);
+            if (MODE == 0) {
+              tc::tma_load_4d_cg2(sH + hs * C::UNIT_BYTES, &tmA, hbar, cc * 64, w0 - 1, h0 - 1, n0);
+            } else if (MODE == 1) {
+              tc::tma_load_4d_cg2(sH + hs * C::UNIT_BYTES, &tmA, hbar, cc * 64, w0 - 1 + u, h0 - 1, n0);
+            } else {
+              const int dy = u / a.ksz - pad, dx = u % a.ksz - pad;
+              tc::tma_load_4d_cg2(sH + hs * C::UNIT_BYTES, &tmA, hbar, cc * 64, w0 + dx, h0 + dy, n0);
+            }
+            for (int j = 0; j < taps_per_unit; ++j) {
+              const int tap = MODE == 0 ? j : (MODE == 1 ? j * 3 + u : u);
+              tc::mbar_wait(&empty[stage], phase ^ 1);
+              const uint32_t fbar = tc::map_to_rank(&full[stage], 0);
+              if (is_leader) tc::mbar_expect_tx(&full[stage], 2 * C::B_BYTES);
+              tc::tma_load_3d_cg2(sB + stage * C::B_BYTES, &tmB, fbar, cc * 64, tap, nt * BN + (int)rank * (BN / 2));
+              if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            }
+            if (++hs == NA) { hs = 0; hphase ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && is_leader) {
+      constexpr uint32_t idesc = tc::idesc_bf16(256, BN, false, false);
+      int stage = 0, hs = 0;
+      uint32_t phase = 0, hphase = 0;
+      int it = 0;
+      for (int tile = cid; tile < num_tiles; tile += ncl, ++it) {
+        const int buf = it & 1;
+        tc::mbar_wait(&tempty[buf], ((it >> 1) & 1) ^ 1);
+        tc::tc_fence_after();
+        const uint32_t d_tmem = tmem + buf * BN;
+        bool first = true;
+        for (int cc = 0; cc < a.c_chunks; ++cc) {
+          const int ksteps = (cc == a.c_chunks - 1) ? a.last_ksteps : 4;
+          for (int u = 0; u < units_per_chunk; ++u) {
+            tc::mbar_wait(&hfull[hs], hphase);
+            tc::tc_fence_after();
+            const uint32_t h_base = tc::smem_u32(sH + hs * C::UNIT_BYTES);
+            for (int j = 0; j < taps_per_unit; ++j) {
+              tc::mbar_wait(&full[stage], phase);
+              tc::tc_fence_after();
+              const uint32_t row =
+                  MODE == 0 ? (uint32_t)((j / 3) * 130 + (j % 3)) : (MODE == 1 ? (uint32_t)(j * a.W) : 0u);
+              const uint32_t a_base = h_base + row * 128;
+              const uint32_t b_base = tc::smem_u32(sB + stage * C::B_BYTES);
+              for (int k = 0; k < ksteps; ++k) {
+                const uint64_t ad = tc::sdesc_sw128(a_base + k * 32, 16, 1024);
+                const uint64_t bd = tc::sdesc_sw128(b_base + k * 32, 16, 1024);
+                tc::mma_bf16_cg2(d_tmem, ad, bd, idesc, first ? 0u : 1u);
+                first = false;
+              }
+              tc::mma_commit_cg2(&empty[stage], 3);
+              if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            }
+            tc::mma_commit_cg2(&hempty[hs], 3);
+            if (++hs == NA) { hs = 0; hphase ^= 1; }
+          }
+        }
+        tc::mma_commit_cg2(&tfull[buf], 3);
+      }
+    }
+  } else {
+    epilogue_loop<BN, 2>(a, &tmO, sO, tmem, tfull, tempty, num_tiles, cid, ncl, (int)rank);
+  }
+  tc::tc_fence_before();
+  tc::cluster_sync();
+  if (warp == 1) tc::tmem_dealloc_cg2(tmem, C::TMEM_COLS);
+}
+
 // deterministic split-K reduction: dst[i] (+)= sum_s part[s][i] in split order
 __global__ void k_split_reduce(const float* __restrict__ part, float* __restrict__ dst, long long n, int splits,
                                int accumulate) {
@@ -716,6 +880,46 @@ cudaError_t launch_halo(int bn, const CUtensorMap& ma, const CUtensorMap& mb, co
   }
 }
 
+template <int BN, int MODE>
+cudaError_t launch_cg2_bn(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo, const TcFpropArgs& a,
+                          uint32_t unit_tx, cudaStream_t st) {
+  using C = Cg2Cfg<BN, MODE>;
+  static bool attr = false;
+  if (!attr) {
+    PG_CUDA(cudaFuncSetAttribute(k_conv_fprop_cg2<BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)C::SMEM));
+    attr = true;
+  }
+  const int tiles = ((a.m_tiles + 1) / 2) * a.n_tiles;
+  int clusters = tiles < kNumSMs / 2 ? tiles : kNumSMs / 2;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * clusters, 1, 1);
+  cfg.blockDim = dim3(192, 1, 1);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeClusterDimension;
+  attrs[0].val.clusterDim.x = 2;
+  attrs[0].val.clusterDim.y = 1;
+  attrs[0].val.clusterDim.z = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_conv_fprop_cg2<BN, MODE>, ma, mb, mo, a, unit_tx);
+}
+
+template <int MODE>
+cudaError_t launch_cg2(int bn, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo,
+                       const TcFpropArgs& a, uint32_t unit_tx, cudaStream_t st) {
+  switch (bn) {
+    case 32: return launch_cg2_bn<32, MODE>(ma, mb, mo, a, unit_tx, st);
+    case 64: return launch_cg2_bn<64, MODE>(ma, mb, mo, a, unit_tx, st);
+    case 96: return launch_cg2_bn<96, MODE>(ma, mb, mo, a, unit_tx, st);
+    case 128: return launch_cg2_bn<128, MODE>(ma, mb, mo, a, unit_tx, st);
+    case 192: return launch_cg2_bn<192, MODE>(ma, mb, mo, a, unit_tx, st);
+    default: return launch_cg2_bn<256, MODE>(ma, mb, mo, a, unit_tx, st);
+  }
+}
+
 int env_int(const char* name, int dflt) {
   const char* v = getenv(name);
   return v ? atoi(v) : dflt;
@@ -790,12 +994,29 @@ cudaError_t tc_conv_fprop(const void* x, int N, int H, int W, int Cin, const voi
   a.out_f32 = epi.out_f32;
   a.ldo = epi.ldo ? epi.ldo : Cout;
   const int sms = kNumSMs;
-  static const int halo_on = env_int("PARAGAN_HALO", 1), tma_st = env_int("PARAGAN_TMA_STORE", 1);
+  static const int halo_on = env_int("PARAGAN_HALO", 1), tma_st = env_int("PARAGAN_TMA_STORE", 1),
+                   cg2_on = env_int("PARAGAN_CG2", 1);
   CUtensorMap mo;
   a.tma_store = tma_st && !a.out_f32 && (bn % 64 == 0 || a.n_tiles == 1) && a.ldo % 8 == 0 &&
                 !((uintptr_t)epi.out & 15);
   if (a.tma_store) PG_CUDA(out_map(&mo, epi.out, a.M, Cout, a.ldo));
   else mo = mb;   // unused
+  if (cg2_on && a.tma_store && a.m_tiles >= 2) {
+    CUtensorMap mb2;
+    PG_CUDA(weight_map(&mb2, wpack, Cout, ksz * ksz, Cin, bn / 2));
+    if (halo_on && ksz == 3 && W % 128 == 0) {
+      CUtensorMap mh;
+      PG_CUDA(halo_map(&mh, x, N, H, W, Cin, 130, 3));
+      return launch_cg2<0>(bn, mh, mb2, mo, a, 390u * 128u, st);
+    }
+    if (halo_on && ksz == 3 && W >= 16 && W <= 64 && H % (128 / W) == 0) {
+      const int rows = 128 / W + 2;
+      CUtensorMap mh;
+      PG_CUDA(halo_map(&mh, x, N, H, W, Cin, W, rows));
+      return launch_cg2<1>(bn, mh, mb2, mo, a, (uint32_t)(rows * W * 128), st);
+    }
+    return launch_cg2<2>(bn, ma, mb2, mo, a, kAtomBytes, st);
+  }
   if (halo_on && ksz == 3 && W % 128 == 0) {
     CUtensorMap mh;
     PG_CUDA(halo_map(&mh, x, N, H, W, Cin, 130, 3));

@@ -69,6 +69,8 @@ CONV_SHAPES = [  # n, h, w, cin, cout, k
     (2, 64, 64, 96, 192, 3),     # column-shifted halo units, W = 64 (2 rows per tile)
     (2, 32, 32, 192, 96, 3),     # column-shifted halo units, W = 32
     (1, 16, 16, 8, 32, 3),       # column-shifted halo units, W = 16, one K step
+    (5, 8, 8, 64, 128, 3),       # odd number of M tiles (CTA-pair kernel: last pair half empty)
+    (4, 8, 8, 1536, 1536, 3),    # CTA pairs with several N tiles
 ]
 
 
