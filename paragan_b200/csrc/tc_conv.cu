@@ -35,7 +35,10 @@ constexpr int kTileM = 128;
 constexpr uint32_t kAtomBytes = 128 * 128;   // 128 rows x 128 B (64 bf16)
 // 227 KB per CTA minus alignment slack, barriers and the 2 x 16 KB epilogue staging tiles
 constexpr uint32_t kStageBytes = 128 * 128;   // one [128 rows][64 bf16] SW128 output tile
-constexpr int kSmemBudget = 232448 - 1024 - 2 * (int)kStageBytes - 1024;
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = 64 + 32 * kEpiWarps;   // producer warp, MMA warp, 8 epilogue warps
+constexpr int kMaxBiasSmem = 2048;              // floats of bias staged in shared memory
+constexpr int kSmemBudget = 232448 - 1024 - 2 * (int)kStageBytes - 1024 - 4 * kMaxBiasSmem;
 
 template <int BN>
 struct FpropCfg {
@@ -45,7 +48,7 @@ struct FpropCfg {
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr uint32_t TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
                                         : (2 * BN <= 256) ? 256 : 512;
-  static constexpr size_t SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + 2 * kStageBytes + 512;
+  static constexpr size_t SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + 2 * kStageBytes + 512 + 4 * kMaxBiasSmem;
 };
 
 template <int BN>
@@ -103,27 +106,51 @@ __device__ __forceinline__ void load_row32_bf16(const bf16* src, float (&r)[32])
   }
 }
 
-// Epilogue warps 2..5: TMEM -> registers (thread = output row) with bias / gamma scale /
-// ReLU-backward mask / residual (same or half resolution) fused and a single rounding.
-// bf16 outputs go through two 16 KB shared-memory tiles in the SW128 layout (row r's 16-byte
-// chunk j at chunk j ^ (r & 7): conflict-free) and leave as 64-column TMA bulk stores
-// (full lines, rows >= M and columns >= C_out clipped by the tensor map).
+// Epilogue: 8 warps (2..9), two per TMEM lane quadrant (warp w may only read lanes
+// 32*(w%4)..+31); half h = (w-2)/4 takes the 64-column groups g with g % 2 == h.  Thread =
+// output row.  bias / gamma scale / ReLU-backward mask / residual (same or half resolution)
+// are fused before a single rounding; the bias vector is staged in shared memory once.
+// bf16 outputs go through one 16 KB SW128 staging tile per half (row r's 16-byte chunk j at
+// j ^ (r & 7): conflict-free) and leave as 64-column TMA bulk stores (rows >= M and columns
+// >= C_out clipped by the tensor map).
+
+__device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float* r) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    float2 f = __bfloat1622float2(h[j]);
+    r[2 * j] = f.x;
+    r[2 * j + 1] = f.y;
+  }
+}
+
 // CG = 2: tiles are CTA-pair tiles (M = 256); this CTA owns M rows [rank * 128, rank * 128 + 128)
 // and releases the accumulator on the leader CTA's barrier.
 template <int BN, int CG = 1>
 __device__ __forceinline__ void epilogue_loop(const TcFpropArgs& a, const CUtensorMap* tmO, uint8_t* stage,
-                                              uint32_t tmem, uint64_t* tfull, uint64_t* tempty, int num_tiles,
-                                              int tile0 = -1, int tile_step = 0, int rank = 0) {
+                                              float* sbias, uint32_t tmem, uint64_t* tfull, uint64_t* tempty,
+                                              int num_tiles, int tile0 = -1, int tile_step = 0, int rank = 0) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = warp & 3;
+  const int half = (warp - 2) >> 2;
   const int row = q * 32 + lane;
-  const bool leader = (threadIdx.x == 64);
+  const int etid = threadIdx.x - 64;                    // 0..255
+  const bool leader = (etid & 127) == 0;                // one store-issuing thread per half
   const float alpha = a.alpha ? *a.alpha : 1.0f;
+  const bool scale = a.alpha != nullptr;
+  // bias -> shared memory (all epilogue threads; named barrier over the 256 of them)
+  const bool bias_smem = a.bias && a.Cout <= kMaxBiasSmem;
+  if (bias_smem) {
+    for (int c = etid; c < a.Cout; c += 32 * kEpiWarps) sbias[c] = a.bias[c];
+  }
+  tc::named_bar(3, 32 * kEpiWarps);
   if (tile0 < 0) {
     tile0 = blockIdx.x;
     tile_step = gridDim.x;
   }
-  int it = 0, sg = 0;
+  uint8_t* st = stage + half * kStageBytes;
+  int it = 0;
+  bool pending = false;
   for (int tile = tile0; tile < num_tiles; tile += tile_step, ++it) {
     const int buf = it & 1;
     const int nt = tile % a.n_tiles;
@@ -145,47 +172,83 @@ __device__ __forceinline__ void epilogue_loop(const TcFpropArgs& a, const CUtens
       }
     }
 #pragma unroll 1
-    for (int g = 0; g < BN; g += 64) {
-      uint8_t* st = stage + (sg & 1) * kStageBytes;
+    for (int g = half * 64; g < BN; g += 128) {
       if (a.tma_store) {
-        if (leader) tc::bulk_wait_read<1>();   // the store issued from this buffer two groups ago has read it
-        tc::named_bar(1, 128);
+        if (leader && pending) tc::bulk_wait_read<0>();   // this half's previous store has read the tile
+        tc::named_bar(1 + half, 128);
       }
 #pragma unroll 1
       for (int cb = g; cb < g + 64 && cb < BN; cb += 32) {
         float v[32];
         tc::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + buf * BN + cb, v);
         const int col0 = nt * BN + cb;
-        const bool live = valid && col0 < a.Cout;
-        const bool full32 = (col0 + 32 <= a.Cout);
-        if (live) {
+        if (valid && col0 + 32 <= a.Cout) {
+          // ---- full 32-column chunk: straight-line, vectorised
+          if (scale) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] *= alpha;
-          if (a.relu_ref) {   // fused ReLU backward: keep the gradient where the forward input was > 0
-            const bf16* rr = reinterpret_cast<const bf16*>(a.relu_ref) + m * a.ldo + col0;
-            if (full32) {
-              float r[32];
-              load_row32_bf16(rr, r);
+            for (int j = 0; j < 32; ++j) v[j] *= alpha;
+          }
+          if (a.relu_ref) {
+            const uint4* rr = reinterpret_cast<const uint4*>(reinterpret_cast<const bf16*>(a.relu_ref) + m * a.ldo + col0);
 #pragma unroll
-              for (int j = 0; j < 32; ++j) v[j] = r[j] > 0.0f ? v[j] : 0.0f;
-            } else {
-              for (int j = 0; j < 32 && col0 + j < a.Cout; ++j) v[j] = __bfloat162float(rr[j]) > 0.0f ? v[j] : 0.0f;
+            for (int qq = 0; qq < 4; ++qq) {
+              float r[8];
+              bf16x8_to_f32(rr[qq], r);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) v[qq * 8 + j] = r[j] > 0.0f ? v[qq * 8 + j] : 0.0f;
             }
           }
           if (a.bias) {
+            if (bias_smem) {
+              const float4* b4 = reinterpret_cast<const float4*>(sbias + col0);
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (full32 || col0 + j < a.Cout) v[j] += a.bias[col0 + j];
+              for (int j = 0; j < 8; ++j) {
+                const float4 b = b4[j];
+                v[4 * j] += b.x;
+                v[4 * j + 1] += b.y;
+                v[4 * j + 2] += b.z;
+                v[4 * j + 3] += b.w;
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] += __ldg(a.bias + col0 + j);
+            }
           }
           if (a.residual) {
-            const bf16* rp = reinterpret_cast<const bf16*>(a.residual) + rbase + col0;
-            if (full32) {
-              float r[32];
-              load_row32_bf16(rp, r);
+            const uint4* rp = reinterpret_cast<const uint4*>(reinterpret_cast<const bf16*>(a.residual) + rbase + col0);
 #pragma unroll
-              for (int j = 0; j < 32; ++j) v[j] += r[j];
+            for (int qq = 0; qq < 4; ++qq) {
+              float r[8];
+              bf16x8_to_f32(rp[qq], r);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) v[qq * 8 + j] += r[j];
+            }
+          }
+          if (!a.tma_store) {
+            if (a.out_f32) {
+              float* op = reinterpret_cast<float*>(a.out) + m * a.ldo + col0;
+#pragma unroll
+              for (int j = 0; j < 32; j += 4)
+                *reinterpret_cast<float4*>(op + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
             } else {
-              for (int j = 0; j < 32 && col0 + j < a.Cout; ++j) v[j] += __bfloat162float(rp[j]);
+              store_row32_bf16(reinterpret_cast<bf16*>(a.out) + m * a.ldo + col0, v);
+            }
+          }
+        } else if (valid && col0 < a.Cout) {
+          // ---- ragged tail (C_out not a multiple of 32): masked, compile-time indices only
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int c = col0 + j;
+            const bool ok = c < a.Cout;
+            float t = v[j] * alpha;
+            if (a.relu_ref && ok)
+              t = __bfloat162float(reinterpret_cast<const bf16*>(a.relu_ref)[m * a.ldo + c]) > 0.0f ? t : 0.0f;
+            if (a.bias && ok) t += __ldg(a.bias + c);
+            if (a.residual && ok) t += __bfloat162float(reinterpret_cast<const bf16*>(a.residual)[rbase + c]);
+            v[j] = t;
+            if (!a.tma_store && ok) {
+              if (a.out_f32) reinterpret_cast<float*>(a.out)[m * a.ldo + c] = t;
+              else reinterpret_cast<bf16*>(a.out)[m * a.ldo + c] = __float2bfloat16_rn(t);
             }
           }
         }
@@ -204,34 +267,16 @@ __device__ __forceinline__ void epilogue_loop(const TcFpropArgs& a, const CUtens
             const int chunk = (c0 + qq) ^ (row & 7);
             *reinterpret_cast<uint4*>(st + row * 128 + chunk * 16) = u;
           }
-        } else if (live) {
-          if (a.out_f32) {
-            float* op = reinterpret_cast<float*>(a.out) + m * a.ldo + col0;
-            if (full32) {
-#pragma unroll
-              for (int j = 0; j < 32; j += 4)
-                *reinterpret_cast<float4*>(op + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-            } else {
-              for (int j = 0; j < 32 && col0 + j < a.Cout; ++j) op[j] = v[j];
-            }
-          } else {
-            bf16* op = reinterpret_cast<bf16*>(a.out) + m * a.ldo + col0;
-            if (full32) {
-              store_row32_bf16(op, v);
-            } else {
-              for (int j = 0; j < 32 && col0 + j < a.Cout; ++j) op[j] = __float2bfloat16_rn(v[j]);
-            }
-          }
         }
       }
       if (a.tma_store) {
         tc::fence_async_smem();
-        tc::named_bar(1, 128);
+        tc::named_bar(1 + half, 128);
         if (leader) {
           tc::tma_store_2d(tmO, st, nt * BN + g, mt * kTileM);
           tc::bulk_commit();
+          pending = true;
         }
-        ++sg;
       }
     }
     tc::tc_fence_before();
@@ -245,7 +290,7 @@ __device__ __forceinline__ void epilogue_loop(const TcFpropArgs& a, const CUtens
 // fprop / dgrad kernel
 // ===========================================================================
 template <int BN>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(kThreads, 1)
     k_conv_fprop(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const __grid_constant__ CUtensorMap tmO, const TcFpropArgs a) {
   using C = FpropCfg<BN>;
@@ -260,6 +305,7 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* sbias = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(tmem_slot + 4) + 15) & ~uintptr_t(15));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
@@ -271,7 +317,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&tfull[b], 1);
-      tc::mbar_init(&tempty[b], 128);
+      tc::mbar_init(&tempty[b], 32 * kEpiWarps);
     }
     tc::fence_barrier_init();
   }
@@ -336,7 +382,7 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else {
-    epilogue_loop<BN>(a, &tmO, sO, tmem, tfull, tempty, num_tiles);
+    epilogue_loop<BN>(a, &tmO, sO, sbias, tmem, tfull, tempty, num_tiles);
   }
   tc::tc_fence_before();
   __syncthreads();
@@ -478,11 +524,11 @@ struct HaloCfg {
   static constexpr int STAGES_RAW = (kSmemBudget - NA * (int)UNIT_BYTES) / (int)B_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr uint32_t TMEM_COLS = FpropCfg<BN>::TMEM_COLS;
-  static constexpr size_t SMEM = 1024 + NA * UNIT_BYTES + STAGES * B_BYTES + 2 * kStageBytes + 512;
+  static constexpr size_t SMEM = 1024 + NA * UNIT_BYTES + STAGES * B_BYTES + 2 * kStageBytes + 512 + 4 * kMaxBiasSmem;
 };
 
 template <int BN, int MODE>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(kThreads, 1)
     k_conv_fprop_halo(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const __grid_constant__ CUtensorMap tmO, const TcFpropArgs a, const uint32_t unit_tx) {
   using C = HaloCfg<BN, MODE>;
@@ -500,6 +546,7 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* tfull = hempty + NA;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* sbias = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(tmem_slot + 4) + 15) & ~uintptr_t(15));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
@@ -515,7 +562,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&tfull[b], 1);
-      tc::mbar_init(&tempty[b], 128);
+      tc::mbar_init(&tempty[b], 32 * kEpiWarps);
     }
     tc::fence_barrier_init();
   }
@@ -593,7 +640,7 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else {
-    epilogue_loop<BN>(a, &tmO, sO, tmem, tfull, tempty, num_tiles);
+    epilogue_loop<BN>(a, &tmO, sO, sbias, tmem, tfull, tempty, num_tiles);
   }
   tc::tc_fence_before();
   __syncthreads();
@@ -616,11 +663,11 @@ struct Cg2Cfg {
   static constexpr int STAGES_RAW = (kSmemBudget - NA * (int)UNIT_BYTES) / (int)B_BYTES;
   static constexpr int STAGES = STAGES_RAW > 12 ? 12 : STAGES_RAW;
   static constexpr uint32_t TMEM_COLS = FpropCfg<BN>::TMEM_COLS;
-  static constexpr size_t SMEM = 1024 + NA * UNIT_BYTES + STAGES * B_BYTES + 2 * kStageBytes + 512;
+  static constexpr size_t SMEM = 1024 + NA * UNIT_BYTES + STAGES * B_BYTES + 2 * kStageBytes + 512 + 4 * kMaxBiasSmem;
 };
 
 template <int BN, int MODE>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(kThreads, 1)
     k_conv_fprop_cg2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmO, const TcFpropArgs a, const uint32_t unit_tx) {
   using C = Cg2Cfg<BN, MODE>;
@@ -637,6 +684,7 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* tfull = hempty + NA;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* sbias = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(tmem_slot + 4) + 15) & ~uintptr_t(15));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = tc::cluster_rank();
@@ -654,7 +702,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&tfull[b], 1);
-      tc::mbar_init(&tempty[b], 256);   // both CTAs' epilogue threads (leader's copy is the one used)
+      tc::mbar_init(&tempty[b], 2 * 32 * kEpiWarps);   // both CTAs' epilogue threads (leader's copy is used)
     }
     tc::fence_barrier_init();
   }
@@ -729,14 +777,14 @@ __global__ void __launch_bounds__(192, 1)
               tc::tc_fence_after();
               const uint32_t row =
                   MODE == 0 ? (uint32_t)((j / 3) * 130 + (j % 3)) : (MODE == 1 ? (uint32_t)(j * a.W) : 0u);
-              const uint32_t a_base = h_base + row * 128;
-              const uint32_t b_base = tc::smem_u32(sB + stage * C::B_BYTES);
-              for (int k = 0; k < ksteps; ++k) {
-                const uint64_t ad = tc::sdesc_sw128(a_base + k * 32, 16, 1024);
-                const uint64_t bd = tc::sdesc_sw128(b_base + k * 32, 16, 1024);
-                tc::mma_bf16_cg2(d_tmem, ad, bd, idesc, first ? 0u : 1u);
-                first = false;
-              }
+              // descriptors advance by 32 bytes (= 2 in the >>4 address field) per K=16 step
+              const uint64_t ad0 = tc::sdesc_sw128(h_base + row * 128, 16, 1024);
+              const uint64_t bd0 = tc::sdesc_sw128(tc::smem_u32(sB + stage * C::B_BYTES), 16, 1024);
+              tc::mma_bf16_cg2(d_tmem, ad0, bd0, idesc, first ? 0u : 1u);
+              first = false;
+              if (ksteps > 1) tc::mma_bf16_cg2(d_tmem, ad0 + 2, bd0 + 2, idesc, 1u);
+              if (ksteps > 2) tc::mma_bf16_cg2(d_tmem, ad0 + 4, bd0 + 4, idesc, 1u);
+              if (ksteps > 3) tc::mma_bf16_cg2(d_tmem, ad0 + 6, bd0 + 6, idesc, 1u);
               tc::mma_commit_cg2(&empty[stage], 3);
               if (++stage == STAGES) { stage = 0; phase ^= 1; }
             }
@@ -748,7 +796,7 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else {
-    epilogue_loop<BN, 2>(a, &tmO, sO, tmem, tfull, tempty, num_tiles, cid, ncl, (int)rank);
+    epilogue_loop<BN, 2>(a, &tmO, sO, sbias, tmem, tfull, tempty, num_tiles, cid, ncl, (int)rank);
   }
   tc::tc_fence_before();
   tc::cluster_sync();
@@ -835,7 +883,7 @@ cudaError_t launch_fprop_bn(const CUtensorMap& ma, const CUtensorMap& mb, const 
   }
   const int tiles = a.m_tiles * a.n_tiles;
   const int grid = tiles < num_sms ? tiles : num_sms;
-  k_conv_fprop<BN><<<grid, 192, C::SMEM, st>>>(ma, mb, mo, a);
+  k_conv_fprop<BN><<<grid, kThreads, C::SMEM, st>>>(ma, mb, mo, a);
   return cudaGetLastError();
 }
 
@@ -863,7 +911,7 @@ cudaError_t launch_halo_bn(const CUtensorMap& ma, const CUtensorMap& mb, const C
   }
   const int tiles = a.m_tiles * a.n_tiles;
   const int grid = tiles < kNumSMs ? tiles : kNumSMs;
-  k_conv_fprop_halo<BN, MODE><<<grid, 192, C::SMEM, st>>>(ma, mb, mo, a, unit_tx);
+  k_conv_fprop_halo<BN, MODE><<<grid, kThreads, C::SMEM, st>>>(ma, mb, mo, a, unit_tx);
   return cudaGetLastError();
 }
 
@@ -894,7 +942,7 @@ cudaError_t launch_cg2_bn(const CUtensorMap& ma, const CUtensorMap& mb, const CU
   int clusters = tiles < kNumSMs / 2 ? tiles : kNumSMs / 2;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * clusters, 1, 1);
-  cfg.blockDim = dim3(192, 1, 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = st;
   cudaLaunchAttribute attrs[1];
