@@ -91,21 +91,6 @@ __device__ __forceinline__ void store_row32_bf16(bf16* dst, const float (&v)[32]
   }
 }
 
-__device__ __forceinline__ void load_row32_bf16(const bf16* src, float (&r)[32]) {
-  const uint4* s = reinterpret_cast<const uint4*>(src);
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    uint4 u = s[q];
-    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      float2 f = __bfloat1622float2(h[j]);
-      r[q * 8 + 2 * j] = f.x;
-      r[q * 8 + 2 * j + 1] = f.y;
-    }
-  }
-}
-
 // Epilogue: 8 warps (2..9), two per TMEM lane quadrant (warp w may only read lanes
 // 32*(w%4)..+31); half h = (w-2)/4 takes the 64-column groups g with g % 2 == h.  Thread =
 // output row.  bias / gamma scale / ReLU-backward mask / residual (same or half resolution)
@@ -494,7 +479,9 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
         for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(op + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
       } else {
-        for (int j = 0; j < 32 && col0 + j < a.Cin; ++j) op[j] = v[j];
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (col0 + j < a.Cin) op[j] = v[j];
       }
     }
   }
