@@ -200,6 +200,27 @@ paragan_status paragan_op_conv_fwd(paragan_dtype dt, const void* x, int32_t n, i
 paragan_status paragan_op_conv_wgrad(paragan_dtype dt, const void* x, const void* dy, int32_t n, int32_t h,
                                      int32_t w, int32_t cin, int32_t cout, int32_t ksz, float* dw, void* stream);
 
+/* Fused attention core of the non-local block (BigGAN's self-attention,
+ * reading R8 — beta = softmax_rows(theta^T phi) without a 1/sqrt(d) scale, o = beta g).
+ * BF16 only (tcgen05).  Per image of hw pixels and q = hw/4 pooled keys:
+ *   qkv  bf16 [n][hw][ct]  theta = channels [0, cq)   (cq = 16 or 32; channels beyond C/8 zero)
+ *   phi  bf16 [n][q][cq]   max-pooled phi;  gp bf16 [n][q][c2] max-pooled g (c2 % 16 == 0, <= 128)
+ *   o    bf16 [n][hw][c2]  = beta gp with beta rounded to bf16 (R14);  o32 fp32 the same before the
+ *        final rounding (may be NULL);  lse fp32 [n][hw] = log sum_j exp(s_ij)
+ * hw and q must be multiples of 128; all pointers device, 16-byte aligned, caller-owned.
+ * Returns PARAGAN_ERR_INVALID_ARG for shapes outside that set. */
+paragan_status paragan_op_attn_fwd(const void* qkv, const void* phi, const void* gp, int32_t n, int32_t hw,
+                                   int32_t cq, int32_t c2, int32_t ct, void* o, float* o32, float* lse,
+                                   void* stream);
+/* Backward of the same: from dO bf16 [n][hw][c2], o32 and lse of the forward,
+ *   dS = beta (dP - rowsum(dO o32)),  dP = dO gp^T (fp32, beta recomputed in fp32),
+ *   dtheta = bf16(dS) phi -> bf16 into dqkv [n][hw][ct] channels [0, cq) (other channels untouched),
+ *   dphi fp32 [n][q][cq] = bf16(dS)^T theta,  dgp fp32 [n][q][c2] = bf16(beta)^T dO.
+ * Sums are taken in a fixed order (bit-reproducible). */
+paragan_status paragan_op_attn_bwd(const void* qkv, const void* phi, const void* gp, const void* dO,
+                                   const float* o32, const float* lse, int32_t n, int32_t hw, int32_t cq,
+                                   int32_t c2, int32_t ct, void* dqkv, float* dphi, float* dgp, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

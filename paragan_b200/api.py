@@ -75,6 +75,11 @@ SYMBOLS = {
                                       C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
     "paragan_op_conv_wgrad": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                         C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
+    "paragan_op_attn_fwd": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                      C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "paragan_op_attn_bwd": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                      C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
+                                      C.c_void_p, C.c_void_p]),
 }
 
 
@@ -169,6 +174,20 @@ def op_conv_wgrad(dtype, x, dy, cout, ksz, dw, stream=None):
     n, h, w, cin = x.shape
     _check("paragan_op_conv_wgrad", lib().paragan_op_conv_wgrad(dtype, _ptr(x), _ptr(dy), n, h, w, cin, cout, ksz,
                                                                 _ptr(dw), _stream(stream)))
+
+
+def op_attn_fwd(qkv, phi, gp, cq, c2, o, o32, lse, stream=None):
+    """qkv [n][hw][ct], phi [n][hw/4][cq], gp [n][hw/4][c2] (bf16) -> o, o32 (or None), lse."""
+    n, hw, ct = qkv.shape
+    _check("paragan_op_attn_fwd", lib().paragan_op_attn_fwd(_ptr(qkv), _ptr(phi), _ptr(gp), n, hw, cq, c2, ct, _ptr(o),
+                                                            _ptr(o32), _ptr(lse), _stream(stream)))
+
+
+def op_attn_bwd(qkv, phi, gp, dO, o32, lse, cq, c2, dqkv, dphi, dgp, stream=None):
+    n, hw, ct = qkv.shape
+    _check("paragan_op_attn_bwd", lib().paragan_op_attn_bwd(_ptr(qkv), _ptr(phi), _ptr(gp), _ptr(dO), _ptr(o32),
+                                                            _ptr(lse), n, hw, cq, c2, ct, _ptr(dqkv), _ptr(dphi),
+                                                            _ptr(dgp), _stream(stream)))
 
 
 class Context:

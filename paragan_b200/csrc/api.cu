@@ -9,6 +9,7 @@
 #include "common.cuh"
 #include "engine.h"
 #include "kernels.h"
+#include "tc_attn.h"
 #include "tc_conv.h"
 
 struct paragan_ctx {
@@ -207,6 +208,77 @@ paragan_status paragan_op_conv_wgrad(paragan_dtype dt, const void* x, const void
     return cuda_status(simt_conv_wgrad<float, float>(static_cast<const float*>(x), static_cast<const float*>(dy), n, h,
                                                      w, cin, cout, ksz, dw, 0, st));
   return PARAGAN_ERR_INVALID_ARG;
+}
+
+paragan_status paragan_op_attn_fwd(const void* qkv, const void* phi, const void* gp, int32_t n, int32_t hw,
+                                   int32_t cq, int32_t c2, int32_t ct, void* o, float* o32, float* lse,
+                                   void* stream) {
+  if (!qkv || !phi || !gp || !o || !lse || n < 1 || hw % 4 || ct < 2 * cq + c2 || ct % 8 ||
+      !tc_attn_ok(hw, hw / 4, cq, c2) || !aligned16(qkv) || !aligned16(phi) || !aligned16(gp) || !aligned16(o) ||
+      (o32 && !aligned16(o32)))
+    return PARAGAN_ERR_INVALID_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  void* gT = nullptr;
+  if (cudaMallocAsync(&gT, (size_t)n * (hw / 4) * c2 * 2, st) != cudaSuccess) return PARAGAN_ERR_CUDA;
+  TcAttnArgs a{};
+  a.n = n;
+  a.HW = hw;
+  a.Q = hw / 4;
+  a.Cq = cq;
+  a.C2 = c2;
+  a.Ct = ct;
+  a.qkv = qkv;
+  a.phi = phi;
+  a.gp = gp;
+  a.gT = gT;
+  a.o = o;
+  a.o32 = o32;
+  a.lse = lse;
+  cudaError_t e = attn_transpose(gp, n, a.Q, c2, gT, st);
+  if (e == cudaSuccess) e = tc_attn_fwd(a, st);
+  cudaFreeAsync(gT, st);
+  return cuda_status(e);
+}
+
+paragan_status paragan_op_attn_bwd(const void* qkv, const void* phi, const void* gp, const void* dO,
+                                   const float* o32, const float* lse, int32_t n, int32_t hw, int32_t cq,
+                                   int32_t c2, int32_t ct, void* dqkv, float* dphi, float* dgp, void* stream) {
+  if (!qkv || !phi || !gp || !dO || !o32 || !lse || !dqkv || !dphi || !dgp || n < 1 || hw % 4 ||
+      ct < 2 * cq + c2 || ct % 8 || !tc_attn_ok(hw, hw / 4, cq, c2) || !aligned16(qkv) || !aligned16(phi) ||
+      !aligned16(gp) || !aligned16(dO) || !aligned16(dqkv) || !aligned16(dphi) || !aligned16(dgp))
+    return PARAGAN_ERR_INVALID_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int nkb = hw / 4 / 128;
+  float *D = nullptr, *part = nullptr;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&D), (size_t)n * hw * sizeof(float), st) != cudaSuccess)
+    return PARAGAN_ERR_CUDA;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&part), (size_t)nkb * n * hw * cq * sizeof(float), st) !=
+      cudaSuccess) {
+    cudaFreeAsync(D, st);
+    return PARAGAN_ERR_CUDA;
+  }
+  TcAttnArgs a{};
+  a.n = n;
+  a.HW = hw;
+  a.Q = hw / 4;
+  a.Cq = cq;
+  a.C2 = c2;
+  a.Ct = ct;
+  a.qkv = qkv;
+  a.phi = phi;
+  a.gp = gp;
+  a.lse = const_cast<float*>(lse);
+  a.dO = dO;
+  a.Dr = D;
+  a.dgp = dgp;
+  a.dphi = dphi;
+  a.dth_part = part;
+  cudaError_t e = attn_rowdot(dO, o32, (long long)n * hw, c2, D, st);
+  if (e == cudaSuccess) e = tc_attn_bwd(a, st);
+  if (e == cudaSuccess) e = attn_dtheta_reduce(part, nkb, (long long)n * hw, cq, dqkv, ct, st);
+  cudaFreeAsync(part, st);
+  cudaFreeAsync(D, st);
+  return cuda_status(e);
 }
 
 }  // extern "C"

@@ -20,6 +20,7 @@
 
 #include "common.cuh"
 #include "engine.h"
+#include "tc_attn.h"
 #include "kernels.h"
 #include "tc_conv.h"
 
@@ -113,6 +114,10 @@ struct AttnL {
   // activations
   void *qkv, *phi_p, *g_p, *P, *ov;
   float* S;
+  // fused tcgen05 path (BF16, tc_attn_ok): S / P never materialised
+  bool fused = false;
+  void* gT = nullptr;              // pooled g transposed [n][C2][Q]
+  float *o32 = nullptr, *lse = nullptr, *Dr = nullptr;
 };
 struct GBlock {
   int cin, cout, hin;
@@ -134,6 +139,7 @@ struct DBlock {
 };
 
 int round8(int x) { return (x + 7) / 8 * 8; }
+int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
 struct Arch {
   std::vector<int> gin, gout;
@@ -525,7 +531,7 @@ class Engine final : public EngineBase {
     a.H = H;
     a.C8 = C / 8;
     a.C2 = C / 2;
-    a.Cq = round8(a.C8);
+    a.Cq = round_up(a.C8, 16);   // K steps of the tensor-core MMA are 16 wide
     a.Ct = 2 * a.Cq + round8(a.C2);
     a.th = N.add("attn.theta", {a.C8, C, 1, 1}, true, true);
     a.ph = N.add("attn.phi", {a.C8, C, 1, 1}, true, true);
@@ -732,14 +738,27 @@ class Engine final : public EngineBase {
       const int n = (at == &gattn_) ? B : B2;
       const long long HW = (long long)at->H * at->H, Q = HW / 4;
       at->qkv = act(n, at->H, at->H, at->Ct);
-      at->phi_p = A.get<char>((size_t)n * Q * at->C8 * sizeof(T));
+      at->phi_p = A.get<char>((size_t)n * Q * at->Cq * sizeof(T));
       at->g_p = A.get<char>((size_t)n * Q * at->C2 * sizeof(T));
-      at->S = A.get<float>((size_t)n * HW * Q);
-      at->P = A.get<char>((size_t)n * HW * Q * sizeof(T));
       at->ov = act(n, at->H, at->H, at->C2);
       attn_out_[at == &gattn_ ? 0 : 1] = act(n, at->H, at->H, at->C);
-      big_ = std::max(big_, (long long)n * HW * Q);
+      at->fused = kBF && std::getenv("PARAGAN_ATTN_UNFUSED") == nullptr &&
+                  tc_attn_ok((int)HW, (int)Q, at->Cq, at->C2);
+      if (at->fused) {
+        at->gT = A.get<char>((size_t)n * Q * at->C2 * sizeof(T));
+        at->o32 = A.get<float>((size_t)n * HW * at->C2);
+        at->lse = A.get<float>((size_t)n * HW);
+        at->Dr = A.get<float>((size_t)n * HW);
+        dth_part_floats_ = std::max(dth_part_floats_, (size_t)((Q / 128) * n * HW * at->Cq));
+      } else {
+        at->S = A.get<float>((size_t)n * HW * Q);
+        at->P = A.get<char>((size_t)n * HW * Q * sizeof(T));
+        big_ = std::max(big_, (long long)n * HW * Q);
+        unfused_dp_ = std::max(unfused_dp_, (long long)n * HW * Q);
+      }
+      dpool_floats_ = std::max(dpool_floats_, (size_t)(n * Q * (at->C2 + at->Cq)));
     }
+    if (dth_part_floats_) dth_part_ = A.get<float>(dth_part_floats_);
     {
       long long mdo = 0, mdq = 0;
       for (AttnL* at : {&gattn_, &dattn_}) {
@@ -750,10 +769,7 @@ class Engine final : public EngineBase {
       }
       tmp_attn_dO_ = A.get<char>((size_t)std::max(mdo, 1LL) * sizeof(T));
       tmp_attn_dqkv_ = A.get<char>((size_t)std::max(mdq, 1LL) * sizeof(T));
-      long long mdp = 1;
-      for (AttnL* at : {&gattn_, &dattn_})
-        if (at->C) mdp = std::max(mdp, (long long)((at == &gattn_) ? B : B2) * at->H * at->H * (at->H * at->H / 4));
-      dP_ = A.get<float>((size_t)mdp);
+      dP_ = A.get<float>((size_t)std::max(unfused_dp_, 1LL));
       dxp_ = A.get<char>((size_t)B2 * (R_ / 2) * (R_ / 2) * cpad_ * sizeof(T));
     }
     maxc_ = 8;
@@ -777,7 +793,7 @@ class Engine final : public EngineBase {
     scratch_floats_ = sf;
     scratch_f_ = A.get<float>(sf);
     wg_scratch_ = A.get<float>((size_t)16 << 20);   // padded / qkv weight-gradient staging
-    dpool_ = A.get<float>((size_t)B2 * 1024 * 96);
+    dpool_ = A.get<float>(std::max<size_t>(dpool_floats_, 1));
     // tables
     for (Net* N : {&G_, &D_}) {
       N->jobs_d = A.get<SnJob>(N->sn_entries.size());
@@ -1181,6 +1197,24 @@ class Engine final : public EngineBase {
   }
 
   // ------------------------------------------------------------------ attention (A6)
+  TcAttnArgs attn_args(const AttnL& a, int n) {
+    TcAttnArgs t{};
+    t.n = n;
+    t.HW = a.H * a.H;
+    t.Q = t.HW / 4;
+    t.Cq = a.Cq;
+    t.C2 = a.C2;
+    t.Ct = a.Ct;
+    t.qkv = a.qkv;
+    t.phi = a.phi_p;
+    t.gp = a.g_p;
+    t.gT = a.gT;
+    t.o = a.ov;
+    t.o32 = a.o32;
+    t.lse = a.lse;
+    t.Dr = a.Dr;
+    return t;
+  }
   paragan_status attn_forward(Net& N, AttnL& a, const void* x, int n, void* out) {
     const int H = a.H;
     const long long HW = (long long)H * H, Q = HW / 4;
@@ -1196,13 +1230,20 @@ class Engine final : public EngineBase {
       }
     }
     const T* qkv = static_cast<const T*>(a.qkv);
-    CK(maxpool2_split<T>(qkv, n, H, H, a.Ct, a.Cq, a.C8, static_cast<T*>(a.phi_p), nullptr, st_));
+    // pooled phi keeps the zero channels C/8..Cq (the theta / phi rows of the packed weight beyond C/8 are zero)
+    CK(maxpool2_split<T>(qkv, n, H, H, a.Ct, a.Cq, a.Cq, static_cast<T*>(a.phi_p), nullptr, st_));
     CK(maxpool2_split<T>(qkv, n, H, H, a.Ct, 2 * a.Cq, a.C2, static_cast<T*>(a.g_p), nullptr, st_));
-    // S = theta phi^T  [n][HW][Q] fp32
-    CKS(bgemm(n, (int)HW, (int)Q, a.C8, qkv, HW * a.Ct, a.Ct, 1, a.phi_p, Q * a.C8, a.C8, 1, a.S, true, HW * Q, Q));
-    CK(softmax_rows<T>(a.S, n * HW, (int)Q, static_cast<T*>(a.P), st_));
-    // o = beta g  [n][HW][C2]
-    CKS(bgemm(n, (int)HW, a.C2, (int)Q, a.P, HW * Q, Q, 1, a.g_p, Q * a.C2, 1, a.C2, a.ov, !kBF, HW * a.C2, a.C2));
+    if (a.fused) {
+      CK(attn_transpose(a.g_p, n, (int)Q, a.C2, a.gT, st_));
+      TcAttnArgs t = attn_args(a, n);
+      CK(tc_attn_fwd(t, st_));
+    } else {
+      // S = theta phi^T  [n][HW][Q] fp32
+      CKS(bgemm(n, (int)HW, (int)Q, a.Cq, qkv, HW * a.Ct, a.Ct, 1, a.phi_p, Q * a.Cq, a.Cq, 1, a.S, true, HW * Q, Q));
+      CK(softmax_rows<T>(a.S, n * HW, (int)Q, static_cast<T*>(a.P), st_));
+      // o = beta g  [n][HW][C2]
+      CKS(bgemm(n, (int)HW, a.C2, (int)Q, a.P, HW * Q, Q, 1, a.g_p, Q * a.C2, 1, a.C2, a.ov, !kBF, HW * a.C2, a.C2));
+    }
     // out = x + gamma * conv1x1(o)
     CKS(conv_fwd(a.ov, n, H, a.oc, out, nullptr, x, 1, N.P(a.gamma)));
     return PARAGAN_OK;
@@ -1227,6 +1268,24 @@ class Engine final : public EngineBase {
       CK(scale_dev(go, (long long)a.C * a.C2, N.P(a.gamma), st_));
     }
     CKS(conv_dgrad(dout, n, H, a.oc, dO, nullptr, N.P(a.gamma)));   // dO = gamma * W_o^T dout
+    if (a.fused) {
+      float* dgp = dpool_;
+      float* dph = dpool_ + (size_t)n * Q * a.C2;
+      CK(attn_rowdot(dO, a.o32, M, a.C2, a.Dr, st_));
+      TcAttnArgs t = attn_args(a, n);
+      t.dO = dO;
+      t.dgp = dgp;
+      t.dphi = dph;
+      t.dth_part = dth_part_;
+      CK(tc_attn_bwd(t, st_));
+      // every channel of dqkv is written below: theta [0,Cq), phi [Cq,2Cq), g [2Cq,2Cq+C2)
+      CK(attn_dtheta_reduce(dth_part_, (int)(Q / 128), M, a.Cq, dqkv, a.Ct, st_));
+      CK(maxpool2_split_bwd<T>(static_cast<const T*>(a.qkv), n, H, H, a.Ct, a.Cq, a.Cq, dph, static_cast<T*>(dqkv),
+                               st_));
+      CK(maxpool2_split_bwd<T>(static_cast<const T*>(a.qkv), n, H, H, a.Ct, 2 * a.Cq, a.C2, dgp,
+                               static_cast<T*>(dqkv), st_));
+      return attn_qkv_backward(N, a, x, n, dout, dx, dqkv, want_w);
+    }
     float* dP = dP_;
     // dgp = P^T dO  [n][Q][C2] fp32 ; dP = dO gp^T [n][HW][Q] fp32
     float* dgp = dpool_;
@@ -1236,15 +1295,20 @@ class Engine final : public EngineBase {
     CK(softmax_bwd_rows<T>(a.S, dP, M, (int)Q, static_cast<T*>(a.P), st_));  // P <- dS
     const void* dS = a.P;
     CK(cudaMemsetAsync(dqkv, 0, sizeof(T) * (size_t)M * a.Ct, st_));
-    // dtheta = dS phi_p -> dqkv[:, 0:C8]
-    CKS(bgemm(n, (int)HW, a.C8, (int)Q, dS, HW * Q, Q, 1, a.phi_p, Q * a.C8, 1, a.C8, dqkv, false, HW * a.Ct, a.Ct));
-    // dphi_p = dS^T theta [n][Q][C8] fp32
+    // dtheta = dS phi_p -> dqkv[:, 0:Cq]
+    CKS(bgemm(n, (int)HW, a.Cq, (int)Q, dS, HW * Q, Q, 1, a.phi_p, Q * a.Cq, 1, a.Cq, dqkv, false, HW * a.Ct, a.Ct));
+    // dphi_p = dS^T theta [n][Q][Cq] fp32
     float* dph = dpool_ + (size_t)n * Q * a.C2;
-    CKS(bgemm(n, (int)Q, a.C8, (int)HW, dS, HW * Q, 1, Q, a.qkv, HW * a.Ct, 1, a.Ct, dph, true, Q * a.C8, a.C8));
-    CK(maxpool2_split_bwd<T>(static_cast<const T*>(a.qkv), n, H, H, a.Ct, a.Cq, a.C8, dph, static_cast<T*>(dqkv), st_));
+    CKS(bgemm(n, (int)Q, a.Cq, (int)HW, dS, HW * Q, 1, Q, a.qkv, HW * a.Ct, 1, a.Ct, dph, true, Q * a.Cq, a.Cq));
+    CK(maxpool2_split_bwd<T>(static_cast<const T*>(a.qkv), n, H, H, a.Ct, a.Cq, a.Cq, dph, static_cast<T*>(dqkv), st_));
     CK(maxpool2_split_bwd<T>(static_cast<const T*>(a.qkv), n, H, H, a.Ct, 2 * a.Cq, a.C2, dgp, static_cast<T*>(dqkv),
                              st_));
-    // dx = dout + W_qkv^T dqkv
+    return attn_qkv_backward(N, a, x, n, dout, dx, dqkv, want_w);
+  }
+  // dx = dout + W_qkv^T dqkv; the theta / phi / g weight gradients
+  paragan_status attn_qkv_backward(Net& N, AttnL& a, const void* x, int n, const void* dout, void* dx, void* dqkv,
+                                   bool want_w) {
+    const int H = a.H;
     ConvL q;
     q.cin = a.C;
     q.cin_x = a.C;
@@ -1548,6 +1612,9 @@ class Engine final : public EngineBase {
   void* tmp_attn_dO_ = nullptr;
   void* dxp_ = nullptr;
   float* dP_ = nullptr;
+  float* dth_part_ = nullptr;
+  size_t dth_part_floats_ = 0, dpool_floats_ = 0;
+  long long unfused_dp_ = 0;
   bool prof_ = false;
   std::vector<ProfRec> recs_;
   std::vector<cudaEvent_t> ev_free_;

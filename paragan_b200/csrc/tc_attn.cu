@@ -1,0 +1,621 @@
+// Fused tcgen05 attention for the BigGAN non-local block (reading
+// R8: beta = softmax_rows(theta^T phi) with no 1/sqrt(d) scale, o = beta g).
+//
+// The [HW x Q] score matrix of an image (4096 x 1024 at 64x64) never reaches HBM:
+//
+//   forward  — one CTA per (image, 128-query tile).  Pass 1 streams 128-key chunks
+//              of phi, S = theta phi^T lands in TMEM, the softmax warps keep a running
+//              row max / sum.  Pass 2 recomputes each S chunk, writes
+//              P = exp(S - m) / l as bf16 into a SW128 smem tile (the storage point of
+//              R14) and the MMA warp accumulates O += P g in TMEM.  Outputs: o (bf16),
+//              o32 (fp32, optional) and lse = m + log l per row.
+//   backward — one CTA per (image, 128-key block), looping over the query tiles:
+//              S^T and dP^T = g dO^T in TMEM, P = exp(S - lse) recomputed in fp32,
+//              dS = P (dP - D) with D = rowsum(dO * o32) (= rowsum(dP * P)), then
+//                dg   += P^T dO      (TMEM accumulator, per key)
+//                dphi += dS^T theta  (TMEM accumulator, per key)
+//                dtheta_part = dS phi (per query tile; one fp32 partial per key block,
+//                                      summed in a fixed order by the caller)
+//              so every reduction is deterministic.
+//
+// Operands are staged by TMA with 128-byte swizzle; the MMA reads the P / dS tiles
+// both K-major (P^T dO, dS^T theta) and MN-major (dS phi).
+#include "tc_attn.h"
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+#include "tc_ptx.cuh"
+
+namespace pg {
+namespace {
+
+constexpr int kT = 128;                 // query rows per tile = keys per chunk
+constexpr uint32_t kAtom = 16384;       // 128 rows x 128 B, one SW128 operand atom
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr int kFwdKStages = 3, kFwdVStages = 2;
+constexpr int kFwdThreads = 192;        // w0 TMA, w1 MMA, w2-5 softmax / epilogue
+constexpr int kBwdThreads = 320;        // w0 TMA, w1 MMA, w2-9 softmax / epilogue
+constexpr uint32_t kBwdStageBytes = 3 * kAtom + 1024;   // theta, dO (2 atoms), lse + D
+
+__device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
+  uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  return reinterpret_cast<uint8_t*>((a + 1023) & ~uintptr_t(1023));
+}
+
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// 16-byte chunk c (0..7) of row r of a K-major SW128 atom
+__device__ __forceinline__ void st_sw128(uint8_t* atom, int r, int c, uint4 v) {
+  *reinterpret_cast<uint4*>(atom + r * 128 + ((c ^ (r & 7)) << 4)) = v;
+}
+
+__device__ __forceinline__ uint64_t kdesc(const void* p) {   // K-major operand
+  return tc::sdesc_sw128(tc::smem_u32(p), 16, 1024);
+}
+__device__ __forceinline__ uint64_t mndesc(const void* p) {  // MN-major operand, 64-wide atoms kAtom apart
+  return tc::sdesc_sw128(tc::smem_u32(p), kAtom, 1024);
+}
+
+// ===========================================================================
+// forward
+// ===========================================================================
+__global__ void __launch_bounds__(kFwdThreads, 1)
+    k_attn_fwd(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+               const __grid_constant__ CUtensorMap tmV, const TcAttnArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  const int C2 = a.C2;
+  const uint32_t v_bytes = 2u * C2 * 128;       // two boxes [C2][64 keys]
+  uint8_t* sQ = smem;
+  uint8_t* sK = sQ + kAtom;
+  uint8_t* sP = sK + kFwdKStages * kAtom;       // 2 buffers x 2 atoms
+  uint8_t* sV = sP + 4 * kAtom;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + kFwdVStages * v_bytes);
+  uint64_t* qfull = bars;
+  uint64_t* kfull = bars + 1;
+  uint64_t* kempty = kfull + kFwdKStages;
+  uint64_t* vfull = kempty + kFwdKStages;
+  uint64_t* vempty = vfull + kFwdVStages;
+  uint64_t* sfull = vempty + kFwdVStages;
+  uint64_t* sempty = sfull + 2;
+  uint64_t* pfull = sempty + 2;
+  uint64_t* pempty = pfull + 2;
+  uint64_t* ofull = pempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ofull + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    tc::tma_prefetch(&tmQ);
+    tc::tma_prefetch(&tmK);
+    tc::tma_prefetch(&tmV);
+    tc::mbar_init(qfull, 1);
+    for (int s = 0; s < kFwdKStages; ++s) {
+      tc::mbar_init(&kfull[s], 1);
+      tc::mbar_init(&kempty[s], 1);
+    }
+    for (int s = 0; s < kFwdVStages; ++s) {
+      tc::mbar_init(&vfull[s], 1);
+      tc::mbar_init(&vempty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      tc::mbar_init(&sfull[s], 1);
+      tc::mbar_init(&sempty[s], 128);
+      tc::mbar_init(&pfull[s], 128);
+      tc::mbar_init(&pempty[s], 1);
+    }
+    tc::mbar_init(ofull, 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;   // S buffers at columns 0 / 128, O at 256
+
+  const int tiles_per_img = a.HW / kT;
+  const int b = blockIdx.x / tiles_per_img;
+  const int q0 = (blockIdx.x - b * tiles_per_img) * kT;
+  const int NC = a.Q / kT;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      tc::mbar_expect_tx(qfull, kAtom);
+      tc::tma_load_3d(sQ, &tmQ, qfull, 0, q0, b);
+      int ks = 0, vs = 0;
+      uint32_t kph = 0, vph = 0;
+      for (int u = 0; u < 2 * NC; ++u) {
+        const int c = u < NC ? u : u - NC;
+        tc::mbar_wait(&kempty[ks], kph ^ 1);
+        tc::mbar_expect_tx(&kfull[ks], kAtom);
+        tc::tma_load_3d(sK + ks * kAtom, &tmK, &kfull[ks], 0, c * kT, b);
+        if (++ks == kFwdKStages) { ks = 0; kph ^= 1; }
+        if (u >= NC) {
+          tc::mbar_wait(&vempty[vs], vph ^ 1);
+          tc::mbar_expect_tx(&vfull[vs], v_bytes);
+          uint8_t* dv = sV + vs * v_bytes;
+          tc::tma_load_3d(dv, &tmV, &vfull[vs], c * kT, 0, b);
+          tc::tma_load_3d(dv + C2 * 128, &tmV, &vfull[vs], c * kT + 64, 0, b);
+          if (++vs == kFwdVStages) { vs = 0; vph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idS = tc::idesc_bf16(kT, kT, false, false);
+      const uint32_t idO = tc::idesc_bf16(kT, C2, false, false);
+      const int ksteps = a.Cq / 16;
+      int ks = 0, vs = 0;
+      uint32_t kph = 0, vph = 0;
+      tc::mbar_wait(qfull, 0);
+      tc::tc_fence_after();
+      auto issue_s = [&](int u) {
+        const int sb = u & 1;
+        tc::mbar_wait(&sempty[sb], ((u >> 1) & 1) ^ 1);
+        tc::mbar_wait(&kfull[ks], kph);
+        tc::tc_fence_after();
+        for (int k = 0; k < ksteps; ++k)
+          tc::mma_bf16(tmem + sb * kT, kdesc(sQ + k * 32), kdesc(sK + ks * kAtom + k * 32), idS, k > 0);
+        tc::mma_commit(&kempty[ks]);
+        tc::mma_commit(&sfull[sb]);
+        if (++ks == kFwdKStages) { ks = 0; kph ^= 1; }
+      };
+      for (int u = 0; u < NC; ++u) issue_s(u);
+      issue_s(NC);
+      for (int c = 0; c < NC; ++c) {
+        if (c + 1 < NC) issue_s(NC + c + 1);
+        const int pb = c & 1;
+        tc::mbar_wait(&pfull[pb], (c >> 1) & 1);
+        tc::mbar_wait(&vfull[vs], vph);
+        tc::tc_fence_after();
+        const uint8_t* p = sP + pb * 2 * kAtom;
+        const uint8_t* v = sV + vs * v_bytes;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          tc::mma_bf16(tmem + 256, kdesc(p + (k >> 2) * kAtom + (k & 3) * 32),
+                       kdesc(v + (k >> 2) * C2 * 128 + (k & 3) * 32), idO, (c | k) != 0);
+        tc::mma_commit(&pempty[pb]);
+        tc::mma_commit(&vempty[vs]);
+        if (++vs == kFwdVStages) { vs = 0; vph ^= 1; }
+      }
+      tc::mma_commit(ofull);
+    }
+  } else {
+    const int qd = warp & 3;
+    const int row = qd * 32 + lane;
+    const uint32_t lrow = tmem + ((uint32_t)(qd * 32) << 16);
+    float m = -INFINITY, l = 0.0f;
+    // pass 1: running max / sum of exp over the key chunks
+    for (int u = 0; u < NC; ++u) {
+      const int sb = u & 1;
+      tc::mbar_wait(&sfull[sb], (u >> 1) & 1);
+      tc::tc_fence_after();
+#pragma unroll 1
+      for (int g = 0; g < 4; ++g) {
+        float v[32];
+        tc::tmem_ld32(lrow + sb * kT + g * 32, v);
+        float mx = v[0];
+#pragma unroll
+        for (int j = 1; j < 32; ++j) mx = fmaxf(mx, v[j]);
+        const float mn = fmaxf(m, mx);
+        const float ml = mn * kLog2e;
+        float s = 0.0f;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) s += tc::ex2(fmaf(v[j], kLog2e, -ml));
+        l = l * tc::ex2((m - mn) * kLog2e) + s;
+        m = mn;
+      }
+      tc::tc_fence_before();
+      tc::mbar_arrive(&sempty[sb]);
+    }
+    // pass 2: P = exp(S - m) / l -> bf16 smem tile for the P g MMA
+    const float ml = m * kLog2e, inv_l = 1.0f / l;
+    for (int c = 0; c < NC; ++c) {
+      const int u = NC + c, sb = u & 1, pb = c & 1;
+      tc::mbar_wait(&sfull[sb], (u >> 1) & 1);
+      tc::mbar_wait(&pempty[pb], ((c >> 1) & 1) ^ 1);
+      tc::tc_fence_after();
+      uint8_t* p = sP + pb * 2 * kAtom;
+#pragma unroll 1
+      for (int g = 0; g < 4; ++g) {
+        float v[32];
+        tc::tmem_ld32(lrow + sb * kT + g * 32, v);
+        uint8_t* atom = p + (g >> 1) * kAtom;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          float e[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) e[i] = tc::ex2(fmaf(v[j * 8 + i], kLog2e, -ml)) * inv_l;
+          st_sw128(atom, row, (g & 1) * 4 + j,
+                   make_uint4(pack2(e[0], e[1]), pack2(e[2], e[3]), pack2(e[4], e[5]), pack2(e[6], e[7])));
+        }
+      }
+      tc::tc_fence_before();
+      tc::mbar_arrive(&sempty[sb]);
+      tc::fence_async_smem();
+      tc::mbar_arrive(&pfull[pb]);
+    }
+    // epilogue: O (TMEM cols 256..) -> bf16 (+ fp32), lse
+    tc::mbar_wait(ofull, 0);
+    tc::tc_fence_after();
+    const long long grow = (long long)b * a.HW + q0 + row;
+    bf16* op = static_cast<bf16*>(a.o) + grow * C2;
+    float* op32 = a.o32 ? a.o32 + grow * C2 : nullptr;
+#pragma unroll 1
+    for (int cb = 0; cb < C2; cb += 32) {
+      float v[32];
+      tc::tmem_ld32(lrow + 256 + cb, v);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (cb + j * 8 < C2) {
+          *reinterpret_cast<uint4*>(op + cb + j * 8) =
+              make_uint4(pack2(v[j * 8], v[j * 8 + 1]), pack2(v[j * 8 + 2], v[j * 8 + 3]),
+                         pack2(v[j * 8 + 4], v[j * 8 + 5]), pack2(v[j * 8 + 6], v[j * 8 + 7]));
+          if (op32) {
+            *reinterpret_cast<float4*>(op32 + cb + j * 8) =
+                make_float4(v[j * 8], v[j * 8 + 1], v[j * 8 + 2], v[j * 8 + 3]);
+            *reinterpret_cast<float4*>(op32 + cb + j * 8 + 4) =
+                make_float4(v[j * 8 + 4], v[j * 8 + 5], v[j * 8 + 6], v[j * 8 + 7]);
+          }
+        }
+      }
+    }
+    a.lse[grow] = m + logf(l);
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tmem, 512);
+}
+
+// ===========================================================================
+// backward (key-block outer loop)
+// ===========================================================================
+__global__ void __launch_bounds__(kBwdThreads, 1)
+    k_attn_bwd(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+               const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmO,
+               const TcAttnArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  const int C2 = a.C2, Cq = a.Cq;
+  const int g_atoms = C2 > 64 ? 2 : 1;
+  uint8_t* sPhi = smem;                       // [128 keys][64]   1 atom
+  uint8_t* sG = sPhi + kAtom;                 // [128 keys][128]  2 atoms
+  uint8_t* sPT = sG + 2 * kAtom;              // P^T  [128 keys][128 q] 2 atoms
+  uint8_t* sDS = sPT + 2 * kAtom;             // dS^T [128 keys][128 q] 2 atoms
+  uint8_t* sStage = sDS + 2 * kAtom;          // 2 x {theta atom, dO 2 atoms, lse[128], D[128]}
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sStage + 2 * kBwdStageBytes);
+  uint64_t* kvfull = bars;
+  uint64_t* qfull = bars + 1;      // [2]
+  uint64_t* qempty = bars + 3;     // [2]
+  uint64_t* sfull = bars + 5;
+  uint64_t* sempty = bars + 6;
+  uint64_t* pfull = bars + 7;
+  uint64_t* pempty = bars + 8;
+  uint64_t* dtfull = bars + 9;     // [2]
+  uint64_t* dtempty = bars + 11;   // [2]
+  uint64_t* accfull = bars + 13;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    tc::tma_prefetch(&tmQ);
+    tc::tma_prefetch(&tmK);
+    tc::tma_prefetch(&tmG);
+    tc::tma_prefetch(&tmO);
+    tc::mbar_init(kvfull, 1);
+    for (int s = 0; s < 2; ++s) {
+      tc::mbar_init(&qfull[s], 1);
+      tc::mbar_init(&qempty[s], 1);
+      tc::mbar_init(&dtfull[s], 1);
+      tc::mbar_init(&dtempty[s], 256);
+    }
+    tc::mbar_init(sfull, 1);
+    tc::mbar_init(sempty, 256);
+    tc::mbar_init(pfull, 256);
+    tc::mbar_init(pempty, 1);
+    tc::mbar_init(accfull, 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  // TMEM columns: S^T 0..127, dP^T 128..255, dg 256.., dphi 384.., dtheta partial 448 / 480
+  const uint32_t tmem = *tmem_slot;
+  constexpr uint32_t cS = 0, cDP = 128, cDG = 256, cDPH = 384, cDT = 448;
+
+  const int NC = a.Q / kT;
+  const int b = blockIdx.x / NC;
+  const int kb = blockIdx.x - b * NC;
+  const int T = a.HW / kT;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      tc::mbar_expect_tx(kvfull, (1 + g_atoms) * kAtom);
+      tc::tma_load_3d(sPhi, &tmK, kvfull, 0, kb * kT, b);
+      tc::tma_load_3d(sG, &tmG, kvfull, 0, kb * kT, b);
+      if (g_atoms == 2) tc::tma_load_3d(sG + kAtom, &tmG, kvfull, 64, kb * kT, b);
+      for (int t = 0; t < T; ++t) {
+        const int st = t & 1;
+        tc::mbar_wait(&qempty[st], ((t >> 1) & 1) ^ 1);
+        uint8_t* sb = sStage + st * kBwdStageBytes;
+        tc::mbar_expect_tx(&qfull[st], (1 + g_atoms) * kAtom + 1024);
+        tc::tma_load_3d(sb, &tmQ, &qfull[st], 0, t * kT, b);
+        tc::tma_load_3d(sb + kAtom, &tmO, &qfull[st], 0, t * kT, b);
+        if (g_atoms == 2) tc::tma_load_3d(sb + 2 * kAtom, &tmO, &qfull[st], 64, t * kT, b);
+        const long long r0 = (long long)b * a.HW + t * kT;
+        tc::bulk_load_1d(sb + 3 * kAtom, a.lse + r0, 512, &qfull[st]);
+        tc::bulk_load_1d(sb + 3 * kAtom + 512, a.Dr + r0, 512, &qfull[st]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idS = tc::idesc_bf16(kT, kT, false, false);
+      const uint32_t idDG = tc::idesc_bf16(kT, C2, false, true);
+      const uint32_t idDPH = tc::idesc_bf16(kT, Cq, false, true);
+      const uint32_t idDT = tc::idesc_bf16(kT, Cq, true, true);
+      const int qsteps = Cq / 16, gsteps = C2 / 16;
+      tc::mbar_wait(kvfull, 0);
+      auto issue_s = [&](int t) {
+        const int st = t & 1;
+        tc::mbar_wait(&qfull[st], (t >> 1) & 1);
+        tc::mbar_wait(sempty, (t & 1) ^ 1);
+        tc::tc_fence_after();
+        const uint8_t* sb = sStage + st * kBwdStageBytes;
+        for (int k = 0; k < qsteps; ++k)
+          tc::mma_bf16(tmem + cS, kdesc(sPhi + k * 32), kdesc(sb + k * 32), idS, k > 0);
+        for (int k = 0; k < gsteps; ++k) {
+          const uint32_t off = (k >> 2) * kAtom + (k & 3) * 32;
+          tc::mma_bf16(tmem + cDP, kdesc(sG + off), kdesc(sb + kAtom + off), idS, k > 0);
+        }
+        tc::mma_commit(sfull);
+      };
+      issue_s(0);
+      for (int t = 0; t < T; ++t) {
+        if (t + 1 < T) issue_s(t + 1);
+        const int st = t & 1;
+        const uint8_t* sb = sStage + st * kBwdStageBytes;
+        tc::mbar_wait(pfull, t & 1);
+        tc::mbar_wait(&dtempty[st], ((t >> 1) & 1) ^ 1);
+        tc::tc_fence_after();
+#pragma unroll 1
+        for (int k = 0; k < 8; ++k) {   // K = 128 queries in steps of 16
+          const uint32_t koff = (k >> 2) * kAtom + (k & 3) * 32;
+          tc::mma_bf16(tmem + cDG, kdesc(sPT + koff), mndesc(sb + kAtom + k * 2048), idDG, (t | k) != 0);
+          tc::mma_bf16(tmem + cDPH, kdesc(sDS + koff), mndesc(sb + k * 2048), idDPH, (t | k) != 0);
+        }
+#pragma unroll 1
+        for (int k = 0; k < 8; ++k)     // K = 128 keys in steps of 16
+          tc::mma_bf16(tmem + cDT + st * 32, mndesc(sDS + k * 2048), mndesc(sPhi + k * 2048), idDT, k > 0);
+        tc::mma_commit(pempty);
+        tc::mma_commit(&qempty[st]);
+        tc::mma_commit(&dtfull[st]);
+      }
+      tc::mma_commit(accfull);
+    }
+  } else {
+    const int qd = warp & 3;
+    const int h = (warp - 2) >> 2;           // which 64 of the 128 columns
+    const int row = qd * 32 + lane;          // key row (S^T, dP^T, dg, dphi) / query row (dtheta)
+    const uint32_t lrow = tmem + ((uint32_t)(qd * 32) << 16);
+    float* part_base = a.dth_part + ((long long)kb * a.n + b) * a.HW * Cq;
+    auto drain_dt = [&](int t) {   // dtheta partial of tile t -> global
+      const int st = t & 1;
+      tc::mbar_wait(&dtfull[st], (t >> 1) & 1);
+      tc::tc_fence_after();
+      if (h * 16 < Cq) {
+        float v[16];
+        tc::tmem_ld16(lrow + cDT + st * 32 + h * 16, v);
+        float* dst = part_base + ((long long)t * kT + row) * Cq + h * 16;
+#pragma unroll
+        for (int j = 0; j < 16; j += 4) *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+      }
+      tc::tc_fence_before();
+      tc::mbar_arrive(&dtempty[st]);
+    };
+    for (int t = 0; t < T; ++t) {
+      const int st = t & 1;
+      const uint8_t* sb = sStage + st * kBwdStageBytes;
+      const float* sl = reinterpret_cast<const float*>(sb + 3 * kAtom) + h * 64;
+      const float* sd = reinterpret_cast<const float*>(sb + 3 * kAtom + 512) + h * 64;
+      tc::mbar_wait(sfull, t & 1);
+      tc::mbar_wait(&qfull[st], (t >> 1) & 1);   // lse / D of this tile are in smem
+      tc::tc_fence_after();
+      float s[64], dp[64];
+      tc::tmem_ld32(lrow + cS + h * 64, *reinterpret_cast<float(*)[32]>(s));
+      tc::tmem_ld32(lrow + cS + h * 64 + 32, *reinterpret_cast<float(*)[32]>(s + 32));
+      tc::tmem_ld32(lrow + cDP + h * 64, *reinterpret_cast<float(*)[32]>(dp));
+      tc::tmem_ld32(lrow + cDP + h * 64 + 32, *reinterpret_cast<float(*)[32]>(dp + 32));
+      tc::tc_fence_before();
+      tc::mbar_arrive(sempty);
+      // P recomputed in fp32 from the scores; dS = P (dP - D)
+#pragma unroll
+      for (int j = 0; j < 64; ++j) {
+        const float p = tc::ex2(fmaf(s[j], kLog2e, -sl[j] * kLog2e));
+        dp[j] = p * (dp[j] - sd[j]);
+        s[j] = p;
+      }
+      tc::mbar_wait(pempty, (t & 1) ^ 1);
+      uint8_t* pa = sPT + h * kAtom;
+      uint8_t* da = sDS + h * kAtom;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        st_sw128(pa, row, c,
+                 make_uint4(pack2(s[c * 8], s[c * 8 + 1]), pack2(s[c * 8 + 2], s[c * 8 + 3]),
+                            pack2(s[c * 8 + 4], s[c * 8 + 5]), pack2(s[c * 8 + 6], s[c * 8 + 7])));
+        st_sw128(da, row, c,
+                 make_uint4(pack2(dp[c * 8], dp[c * 8 + 1]), pack2(dp[c * 8 + 2], dp[c * 8 + 3]),
+                            pack2(dp[c * 8 + 4], dp[c * 8 + 5]), pack2(dp[c * 8 + 6], dp[c * 8 + 7])));
+      }
+      tc::fence_async_smem();
+      tc::mbar_arrive(pfull);
+      if (t > 0) drain_dt(t - 1);
+    }
+    drain_dt(T - 1);
+    // per-key accumulators -> global fp32
+    tc::mbar_wait(accfull, 0);
+    tc::tc_fence_after();
+    const long long krow = (long long)b * a.Q + kb * kT + row;
+    float* dg = a.dgp + krow * C2;
+#pragma unroll 1
+    for (int cb = h * 64; cb < C2 && cb < h * 64 + 64; cb += 32) {
+      float v[32];
+      tc::tmem_ld32(lrow + cDG + cb, v);
+#pragma unroll
+      for (int j = 0; j < 32; j += 4)
+        if (cb + j < C2) *reinterpret_cast<float4*>(dg + cb + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+    }
+    if (h * 16 < Cq) {
+      float v[16];
+      tc::tmem_ld16(lrow + cDPH + h * 16, v);
+      float* dph = a.dphi + krow * Cq + h * 16;
+#pragma unroll
+      for (int j = 0; j < 16; j += 4) *reinterpret_cast<float4*>(dph + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tmem, 512);
+}
+
+// ------------------------------------------------------------------ host side
+PFN_cuTensorMapEncodeTiled_v12000 g_enc = nullptr;
+
+cudaError_t encoder() {
+  if (g_enc) return cudaSuccess;
+  cudaDriverEntryPointQueryResult qr;
+  PG_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&g_enc), cudaEnableDefault,
+                                  &qr));
+  if (qr != cudaDriverEntryPointSuccess || !g_enc) return cudaErrorNotSupported;
+  return cudaSuccess;
+}
+
+// 3-D bf16 map over [d2][d1][d0] (d0 contiguous), box {b0, b1, 1}, 128-byte swizzle
+cudaError_t map3(CUtensorMap* m, const void* base, long long d0, long long d1, long long d2, int b0, int b1) {
+  PG_CUDA(encoder());
+  cuuint64_t dims[3] = {(cuuint64_t)d0, (cuuint64_t)d1, (cuuint64_t)d2};
+  cuuint64_t strides[2] = {(cuuint64_t)d0 * 2, (cuuint64_t)(d0 * d1 * 2)};
+  cuuint32_t box[3] = {(cuuint32_t)b0, (cuuint32_t)b1, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = g_enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+size_t fwd_smem(int C2) { return 1024 + (1 + kFwdKStages + 4) * kAtom + kFwdVStages * 2u * C2 * 128 + 256; }
+size_t bwd_smem() { return 1024 + 7 * kAtom + 2 * kBwdStageBytes + 256; }
+
+}  // namespace
+
+bool tc_attn_ok(int HW, int Q, int Cq, int C2) {
+  return HW % kT == 0 && Q % kT == 0 && (Cq == 16 || Cq == 32) && C2 % 16 == 0 && C2 >= 16 && C2 <= 128;
+}
+
+cudaError_t tc_attn_fwd(const TcAttnArgs& a, cudaStream_t st) {
+  if (!tc_attn_ok(a.HW, a.Q, a.Cq, a.C2) || a.Ct % 8) return cudaErrorInvalidValue;
+  CUtensorMap mq, mk, mv;
+  PG_CUDA(map3(&mq, a.qkv, a.Ct, a.HW, a.n, 64, kT));
+  PG_CUDA(map3(&mk, a.phi, a.Cq, a.Q, a.n, 64, kT));
+  PG_CUDA(map3(&mv, a.gT, a.Q, a.C2, a.n, 64, a.C2));
+  const size_t smem = fwd_smem(a.C2);
+  PG_CUDA(cudaFuncSetAttribute(k_attn_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_attn_fwd<<<a.n * (a.HW / kT), kFwdThreads, smem, st>>>(mq, mk, mv, a);
+  return cudaGetLastError();
+}
+
+cudaError_t tc_attn_bwd(const TcAttnArgs& a, cudaStream_t st) {
+  if (!tc_attn_ok(a.HW, a.Q, a.Cq, a.C2) || a.Ct % 8) return cudaErrorInvalidValue;
+  CUtensorMap mq, mk, mg, mo;
+  PG_CUDA(map3(&mq, a.qkv, a.Ct, a.HW, a.n, 64, kT));
+  PG_CUDA(map3(&mk, a.phi, a.Cq, a.Q, a.n, 64, kT));
+  PG_CUDA(map3(&mg, a.gp, a.C2, a.Q, a.n, 64, kT));
+  PG_CUDA(map3(&mo, a.dO, a.C2, a.HW, a.n, 64, kT));
+  const size_t smem = bwd_smem();
+  PG_CUDA(cudaFuncSetAttribute(k_attn_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_attn_bwd<<<a.n * (a.Q / kT), kBwdThreads, smem, st>>>(mq, mk, mg, mo, a);
+  return cudaGetLastError();
+}
+
+namespace {
+__global__ void k_attn_transpose(const bf16* __restrict__ in, int Q, int C, bf16* __restrict__ out) {
+  __shared__ bf16 tile[32][33];
+  const int b = blockIdx.z;
+  const int q0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+  const bf16* src = in + (long long)b * Q * C;
+  bf16* dst = out + (long long)b * Q * C;
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int q = q0 + i, c = c0 + threadIdx.x;
+    if (q < Q && c < C) tile[i][threadIdx.x] = src[(long long)q * C + c];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int c = c0 + i, q = q0 + threadIdx.x;
+    if (q < Q && c < C) dst[(long long)c * Q + q] = tile[threadIdx.x][i];
+  }
+}
+
+__global__ void k_attn_rowdot(const bf16* __restrict__ dO, const float* __restrict__ o32, long long rows, int C,
+                              float* __restrict__ D) {
+  const long long r = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  float s = 0.0f;
+  for (int c = lane; c < C; c += 32) s += __bfloat162float(dO[r * C + c]) * o32[r * C + c];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) D[r] = s;
+}
+
+__global__ void k_attn_dtheta_reduce(const float* __restrict__ part, int nkb, long long rows, int Cq,
+                                     bf16* __restrict__ dqkv, int ld) {
+  const long long n4 = rows * (Cq / 4);
+  const long long stride = rows * Cq;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / (Cq / 4);
+    const int c = (int)(i - r * (Cq / 4)) * 4;
+    float4 acc = *reinterpret_cast<const float4*>(part + r * Cq + c);
+    for (int k = 1; k < nkb; ++k) {
+      const float4 v = *reinterpret_cast<const float4*>(part + k * stride + r * Cq + c);
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    }
+    __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x, acc.y), hi = __floats2bfloat162_rn(acc.z, acc.w);
+    uint2 pk;
+    pk.x = *reinterpret_cast<uint32_t*>(&lo);
+    pk.y = *reinterpret_cast<uint32_t*>(&hi);
+    *reinterpret_cast<uint2*>(dqkv + r * ld + c) = pk;
+  }
+}
+}  // namespace
+
+cudaError_t attn_transpose(const void* gp, int n, int Q, int C, void* gT, cudaStream_t st) {
+  dim3 grid((Q + 31) / 32, (C + 31) / 32, n);
+  k_attn_transpose<<<grid, dim3(32, 8), 0, st>>>(static_cast<const bf16*>(gp), Q, C, static_cast<bf16*>(gT));
+  return cudaGetLastError();
+}
+
+cudaError_t attn_rowdot(const void* dO, const float* o32, long long rows, int C, float* D, cudaStream_t st) {
+  const long long blocks = (rows + 7) / 8;
+  k_attn_rowdot<<<(unsigned)blocks, 256, 0, st>>>(static_cast<const bf16*>(dO), o32, rows, C, D);
+  return cudaGetLastError();
+}
+
+cudaError_t attn_dtheta_reduce(const float* part, int nkb, long long rows, int Cq, void* dqkv, int ld,
+                               cudaStream_t st) {
+  if (Cq % 4 || ld % 4 || ((uintptr_t)dqkv & 7)) return cudaErrorInvalidValue;
+  const long long n4 = rows * (Cq / 4);
+  long long blocks = (n4 + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k_attn_dtheta_reduce<<<(unsigned)blocks, 256, 0, st>>>(part, nkb, rows, Cq, static_cast<bf16*>(dqkv), ld);
+  return cudaGetLastError();
+}
+
+}  // namespace pg

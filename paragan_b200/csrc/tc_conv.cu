@@ -409,10 +409,12 @@ __global__ void __launch_bounds__(192, 1)
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  // work unit -> (m tile over C_out, n tile over (tap, C_in block), split)
-  int u = blockIdx.x;
-  const int split = u % a.splits;
-  u /= a.splits;
+  // work unit -> (split, m tile over C_out, n tile over (tap, C_in block)); the split (pixel
+  // range) is the slowest index so that the CTAs resident together read the same dY / X
+  // pixels for all taps and channel blocks (L2 reuse instead of one DRAM pass per tap)
+  const int tiles = a.m_tiles * a.n_tiles;
+  const int split = blockIdx.x / tiles;
+  const int u = blockIdx.x - split * tiles;
   const int nt = u % a.n_tiles;
   const int mt = u / a.n_tiles;
   const int tap = nt / a.c_blocks, cb = nt - tap * a.c_blocks;
