@@ -3,12 +3,14 @@
 //
 // The [HW x Q] score matrix of an image (4096 x 1024 at 64x64) never reaches HBM:
 //
-//   forward  — one CTA per (image, 128-query tile).  Pass 1 streams 128-key chunks
-//              of phi, S = theta phi^T lands in TMEM, the softmax warps keep a running
-//              row max / sum.  Pass 2 recomputes each S chunk, writes
-//              P = exp(S - m) / l as bf16 into a SW128 smem tile (the storage point of
-//              R14) and the MMA warp accumulates O += P g in TMEM.  Outputs: o (bf16),
-//              o32 (fp32, optional) and lse = m + log l per row.
+//   forward  — persistent CTAs walk the (image, 128-query tile) list.  Pass 1 streams
+//              128-key chunks of phi, S = theta phi^T lands in TMEM and the softmax
+//              warps take the row max m (no exponentials).  Pass 2 recomputes each S
+//              chunk, writes P~ = exp(S - m) <= 1 as bf16 into a SW128 smem tile and sums
+//              l = sum P~ in fp32, while the MMA warp accumulates O += P~ g in TMEM; the
+//              epilogue scales by 1/l (reading R21: the bf16 storage point of beta is taken
+//              before the normalisation).  Outputs: o (bf16), o32 (fp32, optional) and
+//              lse = m + log l per row.
 //   backward — one CTA per (image, 128-key block), looping over the query tiles:
 //              S^T and dP^T = g dO^T in TMEM, P = exp(S - lse) recomputed in fp32,
 //              dS = P (dP - D) with D = rowsum(dO * o32) (= rowsum(dP * P)), then
@@ -36,9 +38,9 @@ constexpr int kT = 128;                 // query rows per tile = keys per chunk
 constexpr uint32_t kAtom = 16384;       // 128 rows x 128 B, one SW128 operand atom
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr int kFwdKStages = 3, kFwdVStages = 2;
-constexpr int kFwdThreads = 192;        // w0 TMA, w1 MMA, w2-5 softmax / epilogue
+constexpr int kFwdThreads = 320;        // w0 TMA, w1 MMA, w2-9 softmax / epilogue
+constexpr int kSoftThreads = 256;
 constexpr int kBwdThreads = 320;        // w0 TMA, w1 MMA, w2-9 softmax / epilogue
-constexpr uint32_t kBwdStageBytes = 3 * kAtom + 1024;   // theta, dO (2 atoms), lse + D
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
   uintptr_t a = reinterpret_cast<uintptr_t>(p);
@@ -63,7 +65,7 @@ __device__ __forceinline__ uint64_t mndesc(const void* p) {  // MN-major operand
 }
 
 // ===========================================================================
-// forward
+// forward (persistent: one CTA per SM walks the (image, query tile) list)
 // ===========================================================================
 __global__ void __launch_bounds__(kFwdThreads, 1)
     k_attn_fwd(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -76,9 +78,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   uint8_t* sK = sQ + kAtom;
   uint8_t* sP = sK + kFwdKStages * kAtom;       // 2 buffers x 2 atoms
   uint8_t* sV = sP + 4 * kAtom;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + kFwdVStages * v_bytes);
+  float* red = reinterpret_cast<float*>(sV + kFwdVStages * v_bytes);   // [2 tiles][2 halves][128] row max
+  uint64_t* bars = reinterpret_cast<uint64_t*>(red + 2 * 2 * kT);
   uint64_t* qfull = bars;
-  uint64_t* kfull = bars + 1;
+  uint64_t* qempty = bars + 1;
+  uint64_t* kfull = bars + 2;
   uint64_t* kempty = kfull + kFwdKStages;
   uint64_t* vfull = kempty + kFwdKStages;
   uint64_t* vempty = vfull + kFwdVStages;
@@ -87,7 +91,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   uint64_t* pfull = sempty + 2;
   uint64_t* pempty = pfull + 2;
   uint64_t* ofull = pempty + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ofull + 1);
+  uint64_t* oempty = ofull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(oempty + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
@@ -95,6 +100,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     tc::tma_prefetch(&tmK);
     tc::tma_prefetch(&tmV);
     tc::mbar_init(qfull, 1);
+    tc::mbar_init(qempty, 1);
     for (int s = 0; s < kFwdKStages; ++s) {
       tc::mbar_init(&kfull[s], 1);
       tc::mbar_init(&kempty[s], 1);
@@ -105,11 +111,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       tc::mbar_init(&sfull[s], 1);
-      tc::mbar_init(&sempty[s], 128);
-      tc::mbar_init(&pfull[s], 128);
+      tc::mbar_init(&sempty[s], kSoftThreads);
+      tc::mbar_init(&pfull[s], kSoftThreads);
       tc::mbar_init(&pempty[s], 1);
     }
     tc::mbar_init(ofull, 1);
+    tc::mbar_init(oempty, kSoftThreads);
     tc::fence_barrier_init();
   }
   if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
@@ -119,29 +126,33 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const uint32_t tmem = *tmem_slot;   // S buffers at columns 0 / 128, O at 256
 
   const int tiles_per_img = a.HW / kT;
-  const int b = blockIdx.x / tiles_per_img;
-  const int q0 = (blockIdx.x - b * tiles_per_img) * kT;
+  const int num_tiles = a.n * tiles_per_img;
   const int NC = a.Q / kT;
 
   if (warp == 0) {
     if (lane == 0) {
-      tc::mbar_expect_tx(qfull, kAtom);
-      tc::tma_load_3d(sQ, &tmQ, qfull, 0, q0, b);
-      int ks = 0, vs = 0;
+      int ks = 0, vs = 0, it = 0;
       uint32_t kph = 0, vph = 0;
-      for (int u = 0; u < 2 * NC; ++u) {
-        const int c = u < NC ? u : u - NC;
-        tc::mbar_wait(&kempty[ks], kph ^ 1);
-        tc::mbar_expect_tx(&kfull[ks], kAtom);
-        tc::tma_load_3d(sK + ks * kAtom, &tmK, &kfull[ks], 0, c * kT, b);
-        if (++ks == kFwdKStages) { ks = 0; kph ^= 1; }
-        if (u >= NC) {
-          tc::mbar_wait(&vempty[vs], vph ^ 1);
-          tc::mbar_expect_tx(&vfull[vs], v_bytes);
-          uint8_t* dv = sV + vs * v_bytes;
-          tc::tma_load_3d(dv, &tmV, &vfull[vs], c * kT, 0, b);
-          tc::tma_load_3d(dv + C2 * 128, &tmV, &vfull[vs], c * kT + 64, 0, b);
-          if (++vs == kFwdVStages) { vs = 0; vph ^= 1; }
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+        const int b = tile / tiles_per_img;
+        const int q0 = (tile - b * tiles_per_img) * kT;
+        tc::mbar_wait(qempty, (it & 1) ^ 1);
+        tc::mbar_expect_tx(qfull, kAtom);
+        tc::tma_load_3d(sQ, &tmQ, qfull, 0, q0, b);
+        for (int u = 0; u < 2 * NC; ++u) {
+          const int c = u < NC ? u : u - NC;
+          tc::mbar_wait(&kempty[ks], kph ^ 1);
+          tc::mbar_expect_tx(&kfull[ks], kAtom);
+          tc::tma_load_3d(sK + ks * kAtom, &tmK, &kfull[ks], 0, c * kT, b);
+          if (++ks == kFwdKStages) { ks = 0; kph ^= 1; }
+          if (u >= NC) {
+            tc::mbar_wait(&vempty[vs], vph ^ 1);
+            tc::mbar_expect_tx(&vfull[vs], v_bytes);
+            uint8_t* dv = sV + vs * v_bytes;
+            tc::tma_load_3d(dv, &tmV, &vfull[vs], c * kT, 0, b);
+            tc::tma_load_3d(dv + C2 * 128, &tmV, &vfull[vs], c * kT + 64, 0, b);
+            if (++vs == kFwdVStages) { vs = 0; vph ^= 1; }
+          }
         }
       }
     }
@@ -150,122 +161,146 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       const uint32_t idS = tc::idesc_bf16(kT, kT, false, false);
       const uint32_t idO = tc::idesc_bf16(kT, C2, false, false);
       const int ksteps = a.Cq / 16;
-      int ks = 0, vs = 0;
+      int ks = 0, vs = 0, it = 0;
       uint32_t kph = 0, vph = 0;
-      tc::mbar_wait(qfull, 0);
-      tc::tc_fence_after();
-      auto issue_s = [&](int u) {
-        const int sb = u & 1;
-        tc::mbar_wait(&sempty[sb], ((u >> 1) & 1) ^ 1);
+      uint32_t su = 0, pc = 0;   // running S-buffer use / P-buffer use counters
+      auto issue_s = [&](bool last) {
+        const int sb = su & 1;
+        tc::mbar_wait(&sempty[sb], ((su >> 1) & 1) ^ 1);
         tc::mbar_wait(&kfull[ks], kph);
         tc::tc_fence_after();
         for (int k = 0; k < ksteps; ++k)
           tc::mma_bf16(tmem + sb * kT, kdesc(sQ + k * 32), kdesc(sK + ks * kAtom + k * 32), idS, k > 0);
         tc::mma_commit(&kempty[ks]);
         tc::mma_commit(&sfull[sb]);
+        if (last) tc::mma_commit(qempty);
         if (++ks == kFwdKStages) { ks = 0; kph ^= 1; }
+        ++su;
       };
-      for (int u = 0; u < NC; ++u) issue_s(u);
-      issue_s(NC);
-      for (int c = 0; c < NC; ++c) {
-        if (c + 1 < NC) issue_s(NC + c + 1);
-        const int pb = c & 1;
-        tc::mbar_wait(&pfull[pb], (c >> 1) & 1);
-        tc::mbar_wait(&vfull[vs], vph);
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+        tc::mbar_wait(qfull, it & 1);
         tc::tc_fence_after();
-        const uint8_t* p = sP + pb * 2 * kAtom;
-        const uint8_t* v = sV + vs * v_bytes;
+        for (int u = 0; u < NC; ++u) issue_s(false);
+        issue_s(NC == 1);
+        tc::mbar_wait(oempty, (it & 1) ^ 1);   // the previous tile's O has been read out
+        for (int c = 0; c < NC; ++c) {
+          if (c + 1 < NC) issue_s(c + 2 == NC);
+          const int pb = pc & 1;
+          tc::mbar_wait(&pfull[pb], (pc >> 1) & 1);
+          tc::mbar_wait(&vfull[vs], vph);
+          tc::tc_fence_after();
+          const uint8_t* p = sP + pb * 2 * kAtom;
+          const uint8_t* v = sV + vs * v_bytes;
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-          tc::mma_bf16(tmem + 256, kdesc(p + (k >> 2) * kAtom + (k & 3) * 32),
-                       kdesc(v + (k >> 2) * C2 * 128 + (k & 3) * 32), idO, (c | k) != 0);
-        tc::mma_commit(&pempty[pb]);
-        tc::mma_commit(&vempty[vs]);
-        if (++vs == kFwdVStages) { vs = 0; vph ^= 1; }
+          for (int k = 0; k < 8; ++k)
+            tc::mma_bf16(tmem + 256, kdesc(p + (k >> 2) * kAtom + (k & 3) * 32),
+                         kdesc(v + (k >> 2) * C2 * 128 + (k & 3) * 32), idO, (c | k) != 0);
+          tc::mma_commit(&pempty[pb]);
+          tc::mma_commit(&vempty[vs]);
+          if (++vs == kFwdVStages) { vs = 0; vph ^= 1; }
+          ++pc;
+        }
+        tc::mma_commit(ofull);
       }
-      tc::mma_commit(ofull);
     }
   } else {
+    // 8 softmax warps: TMEM lane quadrant qd = warp % 4, half h = 64 of the 128 columns of a chunk
     const int qd = warp & 3;
+    const int h = (warp - 2) >> 2;
     const int row = qd * 32 + lane;
     const uint32_t lrow = tmem + ((uint32_t)(qd * 32) << 16);
-    float m = -INFINITY, l = 0.0f;
-    // pass 1: running max / sum of exp over the key chunks
-    for (int u = 0; u < NC; ++u) {
-      const int sb = u & 1;
-      tc::mbar_wait(&sfull[sb], (u >> 1) & 1);
-      tc::tc_fence_after();
-#pragma unroll 1
-      for (int g = 0; g < 4; ++g) {
-        float v[32];
-        tc::tmem_ld32(lrow + sb * kT + g * 32, v);
-        float mx = v[0];
+    uint32_t su = 0, pc = 0;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      const int b = tile / tiles_per_img;
+      const int q0 = (tile - b * tiles_per_img) * kT;
+      // pass 1: row max (no exponentials)
+      float m = -INFINITY;
+      for (int u = 0; u < NC; ++u, ++su) {
+        const int sb = su & 1;
+        tc::mbar_wait(&sfull[sb], (su >> 1) & 1);
+        tc::tc_fence_after();
+        float v[32], w[32];
+        tc::tmem_ld32(lrow + sb * kT + h * 64, v);
+        tc::tmem_ld32(lrow + sb * kT + h * 64 + 32, w);
+        tc::tc_fence_before();
+        tc::mbar_arrive(&sempty[sb]);
 #pragma unroll
-        for (int j = 1; j < 32; ++j) mx = fmaxf(mx, v[j]);
-        const float mn = fmaxf(m, mx);
-        const float ml = mn * kLog2e;
-        float s = 0.0f;
-#pragma unroll
-        for (int j = 0; j < 32; ++j) s += tc::ex2(fmaf(v[j], kLog2e, -ml));
-        l = l * tc::ex2((m - mn) * kLog2e) + s;
-        m = mn;
+        for (int j = 0; j < 32; ++j) m = fmaxf(m, fmaxf(v[j], w[j]));
       }
-      tc::tc_fence_before();
-      tc::mbar_arrive(&sempty[sb]);
-    }
-    // pass 2: P = exp(S - m) / l -> bf16 smem tile for the P g MMA
-    const float ml = m * kLog2e, inv_l = 1.0f / l;
-    for (int c = 0; c < NC; ++c) {
-      const int u = NC + c, sb = u & 1, pb = c & 1;
-      tc::mbar_wait(&sfull[sb], (u >> 1) & 1);
-      tc::mbar_wait(&pempty[pb], ((c >> 1) & 1) ^ 1);
+      float* rb = red + (it & 1) * 2 * kT;
+      rb[h * kT + row] = m;
+      tc::named_bar(1, kSoftThreads);
+      m = fmaxf(rb[row], rb[kT + row]);
+      // pass 2: P~ = exp(S - m) (<= 1) -> bf16 smem tile for the P~ g MMA; l = sum of P~ in fp32
+      const float ml = m * kLog2e;
+      float l = 0.0f;
+      for (int c = 0; c < NC; ++c, ++su, ++pc) {
+        const int sb = su & 1, pb = pc & 1;
+        tc::mbar_wait(&sfull[sb], (su >> 1) & 1);
+        tc::tc_fence_after();
+        float v[32], w[32];
+        tc::tmem_ld32(lrow + sb * kT + h * 64, v);
+        tc::tmem_ld32(lrow + sb * kT + h * 64 + 32, w);
+        tc::tc_fence_before();
+        tc::mbar_arrive(&sempty[sb]);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          v[j] = tc::ex2(fmaf(v[j], kLog2e, -ml));
+          w[j] = tc::ex2(fmaf(w[j], kLog2e, -ml));
+          l += v[j] + w[j];
+        }
+        tc::mbar_wait(&pempty[pb], ((pc >> 1) & 1) ^ 1);
+        uint8_t* atom = sP + pb * 2 * kAtom + h * kAtom;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          st_sw128(atom, row, j, make_uint4(pack2(v[j * 8], v[j * 8 + 1]), pack2(v[j * 8 + 2], v[j * 8 + 3]),
+                                            pack2(v[j * 8 + 4], v[j * 8 + 5]), pack2(v[j * 8 + 6], v[j * 8 + 7])));
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          st_sw128(atom, row, 4 + j, make_uint4(pack2(w[j * 8], w[j * 8 + 1]), pack2(w[j * 8 + 2], w[j * 8 + 3]),
+                                                pack2(w[j * 8 + 4], w[j * 8 + 5]), pack2(w[j * 8 + 6], w[j * 8 + 7])));
+        tc::fence_async_smem();
+        tc::mbar_arrive(&pfull[pb]);
+      }
+      // combine the two halves' sums
+      float* lb = rb + 0;   // reuse: max already consumed by both halves after this barrier
+      tc::named_bar(1, kSoftThreads);
+      lb[h * kT + row] = l;
+      tc::named_bar(1, kSoftThreads);
+      l = lb[row] + lb[kT + row];
+      const float inv_l = 1.0f / l;
+      // epilogue: O = (P~ g) / l -> bf16 (+ fp32); lse = m + log l
+      tc::mbar_wait(ofull, it & 1);
       tc::tc_fence_after();
-      uint8_t* p = sP + pb * 2 * kAtom;
+      const long long grow = (long long)b * a.HW + q0 + row;
+      bf16* op = static_cast<bf16*>(a.o) + grow * C2;
+      float* op32 = a.o32 ? a.o32 + grow * C2 : nullptr;
 #pragma unroll 1
-      for (int g = 0; g < 4; ++g) {
+      for (int cb = h * 32; cb < C2; cb += 64) {
         float v[32];
-        tc::tmem_ld32(lrow + sb * kT + g * 32, v);
-        uint8_t* atom = p + (g >> 1) * kAtom;
+        tc::tmem_ld32(lrow + 256 + cb, v);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] *= inv_l;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          float e[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) e[i] = tc::ex2(fmaf(v[j * 8 + i], kLog2e, -ml)) * inv_l;
-          st_sw128(atom, row, (g & 1) * 4 + j,
-                   make_uint4(pack2(e[0], e[1]), pack2(e[2], e[3]), pack2(e[4], e[5]), pack2(e[6], e[7])));
-        }
-      }
-      tc::tc_fence_before();
-      tc::mbar_arrive(&sempty[sb]);
-      tc::fence_async_smem();
-      tc::mbar_arrive(&pfull[pb]);
-    }
-    // epilogue: O (TMEM cols 256..) -> bf16 (+ fp32), lse
-    tc::mbar_wait(ofull, 0);
-    tc::tc_fence_after();
-    const long long grow = (long long)b * a.HW + q0 + row;
-    bf16* op = static_cast<bf16*>(a.o) + grow * C2;
-    float* op32 = a.o32 ? a.o32 + grow * C2 : nullptr;
-#pragma unroll 1
-    for (int cb = 0; cb < C2; cb += 32) {
-      float v[32];
-      tc::tmem_ld32(lrow + 256 + cb, v);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        if (cb + j * 8 < C2) {
-          *reinterpret_cast<uint4*>(op + cb + j * 8) =
-              make_uint4(pack2(v[j * 8], v[j * 8 + 1]), pack2(v[j * 8 + 2], v[j * 8 + 3]),
-                         pack2(v[j * 8 + 4], v[j * 8 + 5]), pack2(v[j * 8 + 6], v[j * 8 + 7]));
-          if (op32) {
-            *reinterpret_cast<float4*>(op32 + cb + j * 8) =
-                make_float4(v[j * 8], v[j * 8 + 1], v[j * 8 + 2], v[j * 8 + 3]);
-            *reinterpret_cast<float4*>(op32 + cb + j * 8 + 4) =
-                make_float4(v[j * 8 + 4], v[j * 8 + 5], v[j * 8 + 6], v[j * 8 + 7]);
+          if (cb + j * 8 < C2) {
+            *reinterpret_cast<uint4*>(op + cb + j * 8) =
+                make_uint4(pack2(v[j * 8], v[j * 8 + 1]), pack2(v[j * 8 + 2], v[j * 8 + 3]),
+                           pack2(v[j * 8 + 4], v[j * 8 + 5]), pack2(v[j * 8 + 6], v[j * 8 + 7]));
+            if (op32) {
+              *reinterpret_cast<float4*>(op32 + cb + j * 8) =
+                  make_float4(v[j * 8], v[j * 8 + 1], v[j * 8 + 2], v[j * 8 + 3]);
+              *reinterpret_cast<float4*>(op32 + cb + j * 8 + 4) =
+                  make_float4(v[j * 8 + 4], v[j * 8 + 5], v[j * 8 + 6], v[j * 8 + 7]);
+            }
           }
         }
       }
+      tc::tc_fence_before();
+      tc::mbar_arrive(oempty);
+      if (h == 0) a.lse[grow] = m + logf(l);
     }
-    a.lse[grow] = m + logf(l);
   }
   tc::tc_fence_before();
   __syncthreads();
@@ -275,31 +310,35 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 // ===========================================================================
 // backward (key-block outer loop)
 // ===========================================================================
+// 10 warps: the fullest SM sub-partition holds 3, so <= 168 registers per thread
 __global__ void __launch_bounds__(kBwdThreads, 1)
     k_attn_bwd(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmO,
-               const TcAttnArgs a) {
+               const TcAttnArgs a, const int NS) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   const int C2 = a.C2, Cq = a.Cq;
   const int g_atoms = C2 > 64 ? 2 : 1;
-  uint8_t* sPhi = smem;                       // [128 keys][64]   1 atom
-  uint8_t* sG = sPhi + kAtom;                 // [128 keys][128]  2 atoms
-  uint8_t* sPT = sG + 2 * kAtom;              // P^T  [128 keys][128 q] 2 atoms
+  // one stage = {theta atom, dO g_atoms atoms, lse[128], D[128]}; NS stages (2..4, host-chosen)
+  const uint32_t stage_bytes = (1 + g_atoms) * kAtom + 1024;
+  const uint32_t ld_off = (1 + g_atoms) * kAtom;   // lse / D inside a stage
+  uint8_t* sPhi = smem;                       // [128 keys][64]        1 atom
+  uint8_t* sG = sPhi + kAtom;                 // [128 keys][64 x g]    g_atoms atoms
+  uint8_t* sPT = sG + g_atoms * kAtom;        // P^T  [128 keys][128 q] 2 atoms
   uint8_t* sDS = sPT + 2 * kAtom;             // dS^T [128 keys][128 q] 2 atoms
-  uint8_t* sStage = sDS + 2 * kAtom;          // 2 x {theta atom, dO 2 atoms, lse[128], D[128]}
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sStage + 2 * kBwdStageBytes);
+  uint8_t* sStage = sDS + 2 * kAtom;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sStage + NS * stage_bytes);
   uint64_t* kvfull = bars;
-  uint64_t* qfull = bars + 1;      // [2]
-  uint64_t* qempty = bars + 3;     // [2]
-  uint64_t* sfull = bars + 5;
-  uint64_t* sempty = bars + 6;
-  uint64_t* pfull = bars + 7;
-  uint64_t* pempty = bars + 8;
-  uint64_t* dtfull = bars + 9;     // [2]
-  uint64_t* dtempty = bars + 11;   // [2]
-  uint64_t* accfull = bars + 13;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+  uint64_t* qfull = bars + 1;      // [4]
+  uint64_t* qempty = bars + 5;     // [4]
+  uint64_t* sfull = bars + 9;
+  uint64_t* sempty = bars + 10;
+  uint64_t* pfull = bars + 11;
+  uint64_t* pempty = bars + 12;
+  uint64_t* dtfull = bars + 13;    // [2]
+  uint64_t* dtempty = bars + 15;   // [2]
+  uint64_t* accfull = bars + 17;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
@@ -308,9 +347,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     tc::tma_prefetch(&tmG);
     tc::tma_prefetch(&tmO);
     tc::mbar_init(kvfull, 1);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < NS; ++s) {
       tc::mbar_init(&qfull[s], 1);
       tc::mbar_init(&qempty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
       tc::mbar_init(&dtfull[s], 1);
       tc::mbar_init(&dtempty[s], 256);
     }
@@ -340,17 +381,25 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tc::tma_load_3d(sPhi, &tmK, kvfull, 0, kb * kT, b);
       tc::tma_load_3d(sG, &tmG, kvfull, 0, kb * kT, b);
       if (g_atoms == 2) tc::tma_load_3d(sG + kAtom, &tmG, kvfull, 64, kb * kT, b);
+      int st = 0;
+      uint32_t ph = 0;
       for (int t = 0; t < T; ++t) {
-        const int st = t & 1;
-        tc::mbar_wait(&qempty[st], ((t >> 1) & 1) ^ 1);
-        uint8_t* sb = sStage + st * kBwdStageBytes;
+        // warm L2 with the tile NS ahead (the stage ring hides L2, not DRAM, latency)
+        if (t + NS < T) {
+          tc::tma_prefetch_l2_3d(&tmQ, 0, (t + NS) * kT, b);
+          tc::tma_prefetch_l2_3d(&tmO, 0, (t + NS) * kT, b);
+          if (g_atoms == 2) tc::tma_prefetch_l2_3d(&tmO, 64, (t + NS) * kT, b);
+        }
+        tc::mbar_wait(&qempty[st], ph ^ 1);
+        uint8_t* sb = sStage + st * stage_bytes;
         tc::mbar_expect_tx(&qfull[st], (1 + g_atoms) * kAtom + 1024);
         tc::tma_load_3d(sb, &tmQ, &qfull[st], 0, t * kT, b);
         tc::tma_load_3d(sb + kAtom, &tmO, &qfull[st], 0, t * kT, b);
         if (g_atoms == 2) tc::tma_load_3d(sb + 2 * kAtom, &tmO, &qfull[st], 64, t * kT, b);
         const long long r0 = (long long)b * a.HW + t * kT;
-        tc::bulk_load_1d(sb + 3 * kAtom, a.lse + r0, 512, &qfull[st]);
-        tc::bulk_load_1d(sb + 3 * kAtom + 512, a.Dr + r0, 512, &qfull[st]);
+        tc::bulk_load_1d(sb + ld_off, a.lse + r0, 512, &qfull[st]);
+        tc::bulk_load_1d(sb + ld_off + 512, a.Dr + r0, 512, &qfull[st]);
+        if (++st == NS) { st = 0; ph ^= 1; }
       }
     }
   } else if (warp == 1) {
@@ -362,11 +411,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const int qsteps = Cq / 16, gsteps = C2 / 16;
       tc::mbar_wait(kvfull, 0);
       auto issue_s = [&](int t) {
-        const int st = t & 1;
-        tc::mbar_wait(&qfull[st], (t >> 1) & 1);
+        const int st = t % NS;
+        tc::mbar_wait(&qfull[st], (t / NS) & 1);
         tc::mbar_wait(sempty, (t & 1) ^ 1);
         tc::tc_fence_after();
-        const uint8_t* sb = sStage + st * kBwdStageBytes;
+        const uint8_t* sb = sStage + st * stage_bytes;
         for (int k = 0; k < qsteps; ++k)
           tc::mma_bf16(tmem + cS, kdesc(sPhi + k * 32), kdesc(sb + k * 32), idS, k > 0);
         for (int k = 0; k < gsteps; ++k) {
@@ -378,10 +427,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       issue_s(0);
       for (int t = 0; t < T; ++t) {
         if (t + 1 < T) issue_s(t + 1);
-        const int st = t & 1;
-        const uint8_t* sb = sStage + st * kBwdStageBytes;
+        const int st = t % NS, db = t & 1;
+        const uint8_t* sb = sStage + st * stage_bytes;
         tc::mbar_wait(pfull, t & 1);
-        tc::mbar_wait(&dtempty[st], ((t >> 1) & 1) ^ 1);
+        tc::mbar_wait(&dtempty[db], ((t >> 1) & 1) ^ 1);
         tc::tc_fence_after();
 #pragma unroll 1
         for (int k = 0; k < 8; ++k) {   // K = 128 queries in steps of 16
@@ -391,10 +440,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
 #pragma unroll 1
         for (int k = 0; k < 8; ++k)     // K = 128 keys in steps of 16
-          tc::mma_bf16(tmem + cDT + st * 32, mndesc(sDS + k * 2048), mndesc(sPhi + k * 2048), idDT, k > 0);
+          tc::mma_bf16(tmem + cDT + db * 32, mndesc(sDS + k * 2048), mndesc(sPhi + k * 2048), idDT, k > 0);
         tc::mma_commit(pempty);
         tc::mma_commit(&qempty[st]);
-        tc::mma_commit(&dtfull[st]);
+        tc::mma_commit(&dtfull[db]);
       }
       tc::mma_commit(accfull);
     }
@@ -419,38 +468,41 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tc::mbar_arrive(&dtempty[st]);
     };
     for (int t = 0; t < T; ++t) {
-      const int st = t & 1;
-      const uint8_t* sb = sStage + st * kBwdStageBytes;
-      const float* sl = reinterpret_cast<const float*>(sb + 3 * kAtom) + h * 64;
-      const float* sd = reinterpret_cast<const float*>(sb + 3 * kAtom + 512) + h * 64;
+      const int st = t % NS;
+      const uint8_t* sb = sStage + st * stage_bytes;
+      const float* sl = reinterpret_cast<const float*>(sb + ld_off) + h * 64;
+      const float* sd = reinterpret_cast<const float*>(sb + ld_off + 512) + h * 64;
       tc::mbar_wait(sfull, t & 1);
-      tc::mbar_wait(&qfull[st], (t >> 1) & 1);   // lse / D of this tile are in smem
+      tc::mbar_wait(&qfull[st], (t / NS) & 1);   // lse / D of this tile are in smem
       tc::tc_fence_after();
-      float s[64], dp[64];
-      tc::tmem_ld32(lrow + cS + h * 64, *reinterpret_cast<float(*)[32]>(s));
-      tc::tmem_ld32(lrow + cS + h * 64 + 32, *reinterpret_cast<float(*)[32]>(s + 32));
-      tc::tmem_ld32(lrow + cDP + h * 64, *reinterpret_cast<float(*)[32]>(dp));
-      tc::tmem_ld32(lrow + cDP + h * 64 + 32, *reinterpret_cast<float(*)[32]>(dp + 32));
-      tc::tc_fence_before();
-      tc::mbar_arrive(sempty);
-      // P recomputed in fp32 from the scores; dS = P (dP - D)
+      // P recomputed in fp32 from the scores; dS = P (dP - D); both packed to bf16 pairs at once.
+      // Two 32-column halves keep the register footprint under the 168-register cap.
+      uint32_t pk[32], dk[32];
 #pragma unroll
-      for (int j = 0; j < 64; ++j) {
-        const float p = tc::ex2(fmaf(s[j], kLog2e, -sl[j] * kLog2e));
-        dp[j] = p * (dp[j] - sd[j]);
-        s[j] = p;
+      for (int half = 0; half < 2; ++half) {
+        float s[32], dp[32];
+        tc::tmem_ld32(lrow + cS + h * 64 + half * 32, s);
+        tc::tmem_ld32(lrow + cDP + h * 64 + half * 32, dp);
+        if (half == 1) {
+          tc::tc_fence_before();
+          tc::mbar_arrive(sempty);
+        }
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) {
+          const int jj = half * 32 + j;
+          const float p0 = tc::ex2(fmaf(s[j], kLog2e, -sl[jj] * kLog2e));
+          const float p1 = tc::ex2(fmaf(s[j + 1], kLog2e, -sl[jj + 1] * kLog2e));
+          pk[jj >> 1] = pack2(p0, p1);
+          dk[jj >> 1] = pack2(p0 * (dp[j] - sd[jj]), p1 * (dp[j + 1] - sd[jj + 1]));
+        }
       }
       tc::mbar_wait(pempty, (t & 1) ^ 1);
       uint8_t* pa = sPT + h * kAtom;
       uint8_t* da = sDS + h * kAtom;
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
-        st_sw128(pa, row, c,
-                 make_uint4(pack2(s[c * 8], s[c * 8 + 1]), pack2(s[c * 8 + 2], s[c * 8 + 3]),
-                            pack2(s[c * 8 + 4], s[c * 8 + 5]), pack2(s[c * 8 + 6], s[c * 8 + 7])));
-        st_sw128(da, row, c,
-                 make_uint4(pack2(dp[c * 8], dp[c * 8 + 1]), pack2(dp[c * 8 + 2], dp[c * 8 + 3]),
-                            pack2(dp[c * 8 + 4], dp[c * 8 + 5]), pack2(dp[c * 8 + 6], dp[c * 8 + 7])));
+        st_sw128(pa, row, c, make_uint4(pk[c * 4], pk[c * 4 + 1], pk[c * 4 + 2], pk[c * 4 + 3]));
+        st_sw128(da, row, c, make_uint4(dk[c * 4], dk[c * 4 + 1], dk[c * 4 + 2], dk[c * 4 + 3]));
       }
       tc::fence_async_smem();
       tc::mbar_arrive(pfull);
@@ -508,8 +560,20 @@ cudaError_t map3(CUtensorMap* m, const void* base, long long d0, long long d1, l
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-size_t fwd_smem(int C2) { return 1024 + (1 + kFwdKStages + 4) * kAtom + kFwdVStages * 2u * C2 * 128 + 256; }
-size_t bwd_smem() { return 1024 + 7 * kAtom + 2 * kBwdStageBytes + 256; }
+size_t fwd_smem(int C2) {
+  return 1024 + (1 + kFwdKStages + 4) * kAtom + kFwdVStages * 2u * C2 * 128 + 4 * kT * sizeof(float) + 256;
+}
+constexpr size_t kSmemMax = 232448;   // 227 KB opt-in per CTA
+// fixed part (phi, g, P^T, dS^T) + NS stages; the largest NS <= 4 that fits
+int bwd_stages(int C2, size_t* smem) {
+  const size_t g = C2 > 64 ? 2 : 1;
+  const size_t fixed = 1024 + (1 + g + 4) * kAtom + 256;
+  const size_t stage = (1 + g) * kAtom + 1024;
+  int ns = (int)((kSmemMax - fixed) / stage);
+  if (ns > 4) ns = 4;
+  *smem = fixed + ns * stage;
+  return ns;
+}
 
 }  // namespace
 
@@ -525,7 +589,11 @@ cudaError_t tc_attn_fwd(const TcAttnArgs& a, cudaStream_t st) {
   PG_CUDA(map3(&mv, a.gT, a.Q, a.C2, a.n, 64, a.C2));
   const size_t smem = fwd_smem(a.C2);
   PG_CUDA(cudaFuncSetAttribute(k_attn_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_attn_fwd<<<a.n * (a.HW / kT), kFwdThreads, smem, st>>>(mq, mk, mv, a);
+  int dev = 0, sms = 148;
+  PG_CUDA(cudaGetDevice(&dev));
+  PG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int tiles = a.n * (a.HW / kT);
+  k_attn_fwd<<<tiles < sms ? tiles : sms, kFwdThreads, smem, st>>>(mq, mk, mv, a);
   return cudaGetLastError();
 }
 
@@ -536,9 +604,11 @@ cudaError_t tc_attn_bwd(const TcAttnArgs& a, cudaStream_t st) {
   PG_CUDA(map3(&mk, a.phi, a.Cq, a.Q, a.n, 64, kT));
   PG_CUDA(map3(&mg, a.gp, a.C2, a.Q, a.n, 64, kT));
   PG_CUDA(map3(&mo, a.dO, a.C2, a.HW, a.n, 64, kT));
-  const size_t smem = bwd_smem();
+  size_t smem = 0;
+  const int ns = bwd_stages(a.C2, &smem);
+  if (ns < 2) return cudaErrorInvalidValue;
   PG_CUDA(cudaFuncSetAttribute(k_attn_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_attn_bwd<<<a.n * (a.Q / kT), kBwdThreads, smem, st>>>(mq, mk, mg, mo, a);
+  k_attn_bwd<<<a.n * (a.Q / kT), kBwdThreads, smem, st>>>(mq, mk, mg, mo, a, ns);
   return cudaGetLastError();
 }
 

@@ -1,8 +1,10 @@
 """Fused tcgen05 attention core (reading R8) through the C-ABI
 (`paragan_op_attn_fwd` / `paragan_op_attn_bwd`), element by element against the plain
-definition in float64 with the bf16 storage points of R14 (beta and dS stored bf16):
+definition in float64 with the bf16 storage points of R14 / R21 (the unnormalised
+exp(S - m) and dS stored bf16):
 
-    S = theta phi^T,  beta = softmax_rows(S),  o = bf16(beta) g
+    S = theta phi^T,  m = rowmax(S),  l = rowsum(exp(S - m)),  beta = exp(S - m) / l
+    o = bf16(exp(S - m)) g / l
     dP = dO g^T,  dS = beta * (dP - rowsum(dP * beta))
     dtheta = bf16(dS) phi,  dphi = bf16(dS)^T theta,  dg = bf16(beta)^T dO
 """
@@ -39,7 +41,8 @@ def _reference(qkv, phi, gp, dO, cq):
     S = th @ ph.transpose(1, 2)
     P = torch.softmax(S, dim=-1)
     Pb = _bf(P)
-    o = Pb @ g
+    E = torch.exp(S - S.amax(-1, keepdim=True))
+    o = (_bf(E) @ g) / E.sum(-1, keepdim=True)
     lse = torch.logsumexp(S, dim=-1)
     dP = do @ g.transpose(1, 2)
     dS = P * (dP - (dP * P).sum(-1, keepdim=True))
