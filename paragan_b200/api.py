@@ -75,6 +75,8 @@ SYMBOLS = {
                                       C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
     "paragan_op_conv_wgrad": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                         C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
+    "paragan_op_conv_dgrad": (C.c_int, [C.c_int, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
+                                        C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
     "paragan_op_attn_fwd": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                       C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "paragan_op_attn_bwd": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
@@ -174,6 +176,12 @@ def op_conv_wgrad(dtype, x, dy, cout, ksz, dw, stream=None):
     n, h, w, cin = x.shape
     _check("paragan_op_conv_wgrad", lib().paragan_op_conv_wgrad(dtype, _ptr(x), _ptr(dy), n, h, w, cin, cout, ksz,
                                                                 _ptr(dw), _stream(stream)))
+
+
+def op_conv_dgrad(dtype, dy, wgt, cin, ksz, dx, stream=None):
+    n, h, w, cout = dy.shape
+    _check("paragan_op_conv_dgrad", lib().paragan_op_conv_dgrad(dtype, _ptr(dy), n, h, w, cout, _ptr(wgt), cin, ksz,
+                                                                _ptr(dx), _stream(stream)))
 
 
 def op_attn_fwd(qkv, phi, gp, cq, c2, o, o32, lse, stream=None):

@@ -181,6 +181,9 @@ paragan_status paragan_op_conv_fwd(paragan_dtype dt, const void* x, int32_t n, i
     e.out = y;
     return cuda_status(tc_conv_fprop(x, n, h, w, cin, wgt, cout, ksz, e, st));
   }
+  if (dt == PARAGAN_F32 && cout == 3 && ksz == 3 && cin % 4 == 0 && aligned16(x))   // G's output layer kernel
+    return cuda_status(thin_conv_fwd(static_cast<const float*>(x), n, h, w, cin, static_cast<const float*>(wgt), 3,
+                                     bias, static_cast<float*>(y), st));
   if (dt == PARAGAN_F32)
     return cuda_status(simt_conv_fwd<float, float, float>(static_cast<const float*>(x), n, h, w, cin,
                                                           static_cast<const float*>(wgt), cout, ksz, bias, nullptr,
@@ -204,10 +207,29 @@ paragan_status paragan_op_conv_wgrad(paragan_dtype dt, const void* x, const void
     cudaFreeAsync(scratch, st);
     return cuda_status(e);
   }
+  if (dt == PARAGAN_F32 && cout == 3 && ksz == 3 && cin % 4 == 0 && cin <= 128 && aligned16(x)) {
+    const size_t scratch_n = (size_t)4 * 148 * 27 * cin;
+    float* scratch = nullptr;
+    if (cudaMallocAsync(reinterpret_cast<void**>(&scratch), scratch_n * sizeof(float), st) != cudaSuccess)
+      return PARAGAN_ERR_CUDA;
+    cudaError_t e = thin_conv_wgrad(static_cast<const float*>(x), static_cast<const float*>(dy), n, h, w, cin, 3, dw,
+                                    scratch, scratch_n, st);
+    cudaFreeAsync(scratch, st);
+    return cuda_status(e);
+  }
   if (dt == PARAGAN_F32)
     return cuda_status(simt_conv_wgrad<float, float>(static_cast<const float*>(x), static_cast<const float*>(dy), n, h,
                                                      w, cin, cout, ksz, dw, 0, st));
   return PARAGAN_ERR_INVALID_ARG;
+}
+
+paragan_status paragan_op_conv_dgrad(paragan_dtype dt, const void* dy, int32_t n, int32_t h, int32_t w, int32_t cout,
+                                     const void* wgt, int32_t cin, int32_t ksz, void* dx, void* stream) {
+  if (dt != PARAGAN_F32 || !dy || !wgt || !dx || n < 1 || h < 1 || w < 1 || cout != 3 || ksz != 3 || cin % 4 ||
+      !aligned16(dx))
+    return PARAGAN_ERR_INVALID_ARG;
+  return cuda_status(thin_conv_dgrad(static_cast<const float*>(dy), n, h, w, cin, static_cast<const float*>(wgt), 3,
+                                     static_cast<float*>(dx), static_cast<cudaStream_t>(stream)));
 }
 
 paragan_status paragan_op_attn_fwd(const void* qkv, const void* phi, const void* gp, int32_t n, int32_t hw,

@@ -127,6 +127,7 @@ struct GBlock {
   // activations (batch B)
   void *x, *u1, *h1, *a2, *s, *out;
   float *gain1, *bias1, *gain2, *bias2, *cond, *dcond;
+  float *ab1 = nullptr, *ab2 = nullptr;   // CBN backward per-sample [dbias | dgain] rows [B][2C]
   float *mean1, *rstd1, *mean2, *rstd2;
   double *sums1, *sums2;
 };
@@ -706,6 +707,8 @@ class Engine final : public EngineBase {
       b.bias2 = A.get<float>((size_t)B * b.cout);
       b.cond = A.get<float>((size_t)B * cd_);
       b.dcond = A.get<float>((size_t)B * cd_);
+      b.ab1 = A.get<float>((size_t)B * 2 * b.cin);
+      b.ab2 = A.get<float>((size_t)B * 2 * b.cout);
       b.mean1 = A.get<float>(b.cin);
       b.rstd1 = A.get<float>(b.cin);
       b.mean2 = A.get<float>(b.cout);
@@ -785,6 +788,13 @@ class Engine final : public EngineBase {
     daout_ = A.get<float>((size_t)B * R_ * R_ * cl_);
     dh0f_ = A.get<float>((size_t)B * 16 * c0_);
     ab_ = A.get<float>((size_t)B * 2 * maxc_);
+    // grouped CBN-linear GEMM tables (A4): forward (4 per block + the G linear), dW (4 per block), dcond (1 per block)
+    {
+      const size_t nb = gb_.size();
+      cbn_fwd_d_ = A.get<GemmProblem>(4 * nb + 1);
+      cbn_dw_d_ = A.get<GemmProblem>(4 * nb);
+      cbn_dcond_d_ = A.get<GemmProblem>(nb);
+    }
     bn_part_ = A.get<float>((size_t)B * 64 * 2 * maxc_);
     dpart_ = A.get<double>((size_t)kMaxPartialBlocks * 2 * std::max(maxc_, 16 * c0_));
     tot_ = A.get<double>(4 * maxc_);   // fp64 channel sums + fp32 means (bn_bwd_apply)
@@ -845,7 +855,80 @@ class Engine final : public EngineBase {
   }
 
   // SN job tables and pack lists (host -> device once)
+  paragan_status upload_cbn_tables() {
+    const int B = B_;
+    auto seg = [](const float* A, long long sam, long long sak, const float* Bm, long long sbn, long long sbk, int K) {
+      GemmSeg g{};
+      g.A = A;
+      g.sam = sam;
+      g.sak = sak;
+      g.B = Bm;
+      g.sbn = sbn;
+      g.sbk = sbk;
+      g.K = K;
+      return g;
+    };
+    std::vector<GemmProblem> fw, dw, dc;
+    {
+      // G linear: h0f = z0 W^T + b
+      GemmProblem p{};
+      p.M = B;
+      p.N = 16 * c0_;
+      p.nseg = 1;
+      p.seg[0] = seg(zin_, dimz_, 1, glin_.what, zc_, 1, zc_);
+      p.C = h0f_;
+      p.ldc = 16 * c0_;
+      p.bias = G_.P(glin_.b);
+      fw.push_back(p);
+    }
+    for (GBlock& b : gb_) {
+      const LinL* L[4] = {&b.g1, &b.b1, &b.g2, &b.b2};
+      float* outs[4] = {b.gain1, b.bias1, b.gain2, b.bias2};
+      float* abs_[4] = {b.ab1 + b.cin, b.ab1, b.ab2 + b.cout, b.ab2};   // dgain = AB[:, C:2C], dbias = AB[:, 0:C]
+      const int Cs[4] = {b.cin, b.cin, b.cout, b.cout};
+      GemmProblem pc{};
+      pc.M = B;
+      pc.N = cd_;
+      pc.C = b.dcond;
+      pc.ldc = cd_;
+      for (int k = 0; k < 4; ++k) {
+        GemmProblem p{};
+        p.M = B;
+        p.N = Cs[k];
+        p.nseg = 1;
+        p.seg[0] = seg(b.cond, cd_, 1, L[k]->what, cd_, 1, cd_);
+        p.C = outs[k];
+        p.ldc = Cs[k];
+        fw.push_back(p);
+        // dW[c][k] = sum_n dX[n][c] cond[n][k]
+        GemmProblem q{};
+        q.M = Cs[k];
+        q.N = cd_;
+        q.nseg = 1;
+        q.seg[0] = seg(abs_[k], 1, 2 * Cs[k], b.cond, 1, cd_, B);
+        q.C = G_.G(L[k]->w);
+        q.ldc = cd_;
+        dw.push_back(q);
+        // dcond[n][k] = sum over the four linears of sum_c dX[n][c] What[c][k]
+        pc.seg[pc.nseg++] = seg(abs_[k], 2 * Cs[k], 1, L[k]->what, 1, cd_, Cs[k]);
+      }
+      dc.push_back(pc);
+    }
+    cbn_fwd_n_ = (int)fw.size();
+    cbn_fwd_tiles_ = gemm_grouped_plan(fw.data(), cbn_fwd_n_);
+    cbn_dw_n_ = (int)dw.size();
+    cbn_dw_tiles_ = gemm_grouped_plan(dw.data(), cbn_dw_n_);
+    cbn_dcond_n_ = (int)dc.size();
+    cbn_dcond_tiles_ = gemm_grouped_plan(dc.data(), cbn_dcond_n_);
+    CK(cudaMemcpyAsync(cbn_fwd_d_, fw.data(), sizeof(GemmProblem) * fw.size(), cudaMemcpyHostToDevice, st_));
+    CK(cudaMemcpyAsync(cbn_dw_d_, dw.data(), sizeof(GemmProblem) * dw.size(), cudaMemcpyHostToDevice, st_));
+    CK(cudaMemcpyAsync(cbn_dcond_d_, dc.data(), sizeof(GemmProblem) * dc.size(), cudaMemcpyHostToDevice, st_));
+    CK(cudaStreamSynchronize(st_));   // the host vectors die here
+    return PARAGAN_OK;
+  }
+
   paragan_status upload_tables() {
+    CKS(upload_cbn_tables());
     for (Net* N : {&G_, &D_}) {
       std::vector<SnJob> jobs;
       std::vector<int> b1j, b1k, b1r, b1bj, b1bk, b2j, b2r;
@@ -1156,19 +1239,18 @@ class Engine final : public EngineBase {
     CK(cudaMemcpyAsync(zin_, z, sizeof(float) * B * dimz_, cudaMemcpyDeviceToDevice, st_));
     CK(cudaMemcpyAsync(yg_, y, sizeof(int32_t) * B, cudaMemcpyDeviceToDevice, st_));
     CK(gather_rows(G_.P(shared_), yg_, B, cfg_.shared_dim, emb_, cfg_.shared_dim, st_));
-    // linear z0 -> [B, 4, 4, C0]  (R10: NHWC view of the 16*C0 vector)
-    CK(gemm_f32(B, 16 * c0_, zc_, zin_, dimz_, 1, glin_.what, zc_, 1, h0f_, 16 * c0_, 0.0f, G_.P(glin_.b), st_));
+    for (size_t i = 0; i < gb_.size(); ++i) {
+      // cond_i = [shared[y] | z_{i+1}]  (R11)
+      CK(copy_cols(emb_, cfg_.shared_dim, B, cfg_.shared_dim, gb_[i].cond, cd_, st_));
+      CK(copy_cols(zin_ + (i + 1) * zc_, dimz_, B, zc_, gb_[i].cond + cfg_.shared_dim, cd_, st_));
+    }
+    // the G linear z0 -> [B, 4, 4, C0] (R10: NHWC view of the 16*C0 vector) and every CBN gain / bias
+    // linear of every block, one grouped launch
+    CK(gemm_f32_grouped(cbn_fwd_d_, cbn_fwd_n_, cbn_fwd_tiles_, st_));
     CK(convert_f32<T>(h0f_, static_cast<T*>(gb_[0].x), (long long)B * 16 * c0_, st_));
     for (size_t i = 0; i < gb_.size(); ++i) {
       GBlock& b = gb_[i];
       const int H = b.hin, H2 = 2 * H;
-      // cond_i = [shared[y] | z_{i+1}]  (R11)
-      CK(copy_cols(emb_, cfg_.shared_dim, B, cfg_.shared_dim, b.cond, cd_, st_));
-      CK(copy_cols(zin_ + (i + 1) * zc_, dimz_, B, zc_, b.cond + cfg_.shared_dim, cd_, st_));
-      CK(gemm_f32(B, b.cin, cd_, b.cond, cd_, 1, b.g1.what, cd_, 1, b.gain1, b.cin, 0.0f, nullptr, st_));
-      CK(gemm_f32(B, b.cin, cd_, b.cond, cd_, 1, b.b1.what, cd_, 1, b.bias1, b.cin, 0.0f, nullptr, st_));
-      CK(gemm_f32(B, b.cout, cd_, b.cond, cd_, 1, b.g2.what, cd_, 1, b.gain2, b.cout, 0.0f, nullptr, st_));
-      CK(gemm_f32(B, b.cout, cd_, b.cond, cd_, 1, b.b2.what, cd_, 1, b.bias2, b.cout, 0.0f, nullptr, st_));
       // CBN1 -> ReLU -> up x2 (fused)
       CKS(bn_forward_stats(b.x, (long long)B * H * H, b.cin, b.sums1, b.mean1, b.rstd1));
       CK((bn_apply_relu<T, T>(static_cast<const T*>(b.x), B, H, H, b.cin, b.mean1, b.rstd1, b.gain1, b.bias1, nullptr,
@@ -1531,18 +1613,25 @@ class Engine final : public EngineBase {
       CKS(conv_dgrad(tmp(i_ds), B, H, b.sc, tmp(i_dxs), nullptr));
       // CBN2 backward: da2 -> dh1 (into cur's buffer)
       CKS(cbn_backward(b.h1, tmp(i_a2), B, H2, b.cout, b.mean2, b.rstd2, b.gain2, b.bias2, false, nullptr, cur,
-                       b.g2, b.b2, b.cond, b.dcond, true));
+                       b.ab2));
       // conv1 on the upsampled activation
       CKS(conv_wgrad(G_, b.u1, cur, B, H2, b.c1));
       CKS(bias_grad(G_, b.c1, cur, Mhi));
       CKS(conv_dgrad(cur, B, H2, b.c1, tmp(i_a2), nullptr));
       // CBN1 backward through the upsample (2x2 sum), plus the skip gradient
       CKS(cbn_backward(b.x, tmp(i_a2), B, H, b.cin, b.mean1, b.rstd1, b.gain1, b.bias1, true, tmp(i_dxs), tmp(i_ds),
-                       b.g1, b.b1, b.cond, b.dcond, false));
-      // cond -> shared embedding gradient (first shared_dim columns)
-      CK(scatter_add_rows(b.dcond, cd_, yg_, B, cfg_.shared_dim, G_.G(shared_), st_));
+                       b.ab1));
       ic = i_ds;
       cur = tmp(ic);
+    }
+    // CBN linears: every dW, then every block's dcond (sum over its four linears), one launch each
+    CK(gemm_f32_grouped(cbn_dw_d_, cbn_dw_n_, cbn_dw_tiles_, st_));
+    CK(gemm_f32_grouped(cbn_dcond_d_, cbn_dcond_n_, cbn_dcond_tiles_, st_));
+    // cond -> shared embedding gradient (first shared_dim columns), blocks in order
+    for (size_t i0 = 0; i0 < gb_.size(); i0 += 8) {
+      RowSrcs rs{};
+      for (size_t i = i0; i < gb_.size() && i < i0 + 8; ++i) rs.p[rs.n++] = gb_[i].dcond;
+      CK(scatter_add_rows_multi(rs, cd_, yg_, B, cfg_.shared_dim, cfg_.n_classes, G_.G(shared_), st_));
     }
     // G linear: h0 = z0 W^T + b
     CK(to_f32<T>(static_cast<const T*>(cur), dh0f_, (long long)B * 16 * c0_, st_));
@@ -1552,25 +1641,16 @@ class Engine final : public EngineBase {
   }
   // conditional BN backward; writes dx (+ add), per-sample gain/bias grads into the CBN linears and dcond
   paragan_status cbn_backward(const void* x, const void* dy, int n, int H, int C, const float* mean, const float* rstd,
-                              const float* gain, const float* bias, bool up2, const void* add, void* dx,
-                              const LinL& lg, const LinL& lb, const float* cond, float* dcond, bool first) {
+                              const float* gain, const float* bias, bool up2, const void* add, void* dx, float* ab) {
     CK((bn_bwd_reduce<T, T>(static_cast<const T*>(x), static_cast<const T*>(dy), n, H, H, C, mean, rstd, gain, bias,
-                            nullptr, nullptr, up2, bn_part_, bn_chunks(H * H), ab_, st_)));
-    CK(bn_bwd_totals(ab_, n, C, gain, nullptr, tot_, st_));
+                            nullptr, nullptr, up2, bn_part_, bn_chunks(H * H), ab, st_)));
+    CK(bn_bwd_totals(ab, n, C, gain, nullptr, tot_, st_));
     CKS(allreduce_small(tot_, 2 * C));
     CK((bn_bwd_apply<T, T, T>(static_cast<const T*>(x), static_cast<const T*>(dy), n, H, H, C, mean, rstd, gain, bias,
                               nullptr, nullptr, up2, tot_, (double)n * H * H * cfg_.world_size,
                               static_cast<const T*>(add), static_cast<T*>(dx), st_)));
-    // AB[n][0:C] = dbias (sum g0), AB[n][C:2C] = dgain (sum g0 * x_hat)
-    const float* dbias = ab_;
-    const float* dgain = ab_ + C;
-    const int ld = 2 * C;
-    // dW_gain[c][k] = sum_n dgain[n][c] cond[n][k]; same for bias
-    CK(gemm_f32(C, cd_, n, dgain, 1, ld, cond, 1, cd_, G_.G(lg.w), cd_, 0.0f, nullptr, st_));
-    CK(gemm_f32(C, cd_, n, dbias, 1, ld, cond, 1, cd_, G_.G(lb.w), cd_, 0.0f, nullptr, st_));
-    // dcond[n][k] (+)= sum_c dgain[n][c] What[c][k] + dbias[n][c] Bhat[c][k]
-    CK(gemm_f32(n, cd_, C, dgain, ld, 1, lg.what, 1, cd_, dcond, cd_, first ? 0.0f : 1.0f, nullptr, st_));
-    CK(gemm_f32(n, cd_, C, dbias, ld, 1, lb.what, 1, cd_, dcond, cd_, 1.0f, nullptr, st_));
+    // AB[n][0:C] = dbias (sum g0), AB[n][C:2C] = dgain (sum g0 * x_hat): consumed by the grouped
+    // CBN-linear GEMMs at the end of g_backward
     return PARAGAN_OK;
   }
   int bn_chunks(long long hw) const {
@@ -1633,6 +1713,8 @@ class Engine final : public EngineBase {
   float* demb_hat_ = nullptr;
   float *feat_ = nullptr, *logits_ = nullptr, *dlogits_ = nullptr;
   float *ab_ = nullptr, *bn_part_ = nullptr;
+  GemmProblem *cbn_fwd_d_ = nullptr, *cbn_dw_d_ = nullptr, *cbn_dcond_d_ = nullptr;
+  int cbn_fwd_n_ = 0, cbn_fwd_tiles_ = 0, cbn_dw_n_ = 0, cbn_dw_tiles_ = 0, cbn_dcond_n_ = 0, cbn_dcond_tiles_ = 0;
   double *dpart_ = nullptr, *tot_ = nullptr;
   float *scratch_f_ = nullptr, *wg_scratch_ = nullptr, *dpool_ = nullptr;
   size_t scratch_floats_ = 0;

@@ -143,6 +143,108 @@ __global__ void __launch_bounds__(256) k_gemm(int M, int N, int K, const float* 
   }
 }
 
+// ===================================================================== grouped fp32 GEMM
+// 64x64 tile, 256 threads (4x4 each), K chunks of 16 double-buffered through registers
+__global__ void __launch_bounds__(256) k_gemm_grouped(const GemmProblem* __restrict__ probs, int nprob) {
+  __shared__ float As[2][16][65];
+  __shared__ float Bs[2][16][65];
+  const int bid = blockIdx.x;
+  int pi = 0;
+  while (pi + 1 < nprob && probs[pi + 1].tile0 <= bid) ++pi;
+  const GemmProblem& P = probs[pi];
+  const int tiles_n = (P.N + 63) / 64;
+  const int lt = bid - P.tile0;
+  const int m0 = (lt / tiles_n) * 64, n0 = (lt % tiles_n) * 64;
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  float acc[4][4] = {};
+  // flatten (segment, k chunk) into one chunk sequence
+  int nch = 0;
+  for (int s = 0; s < P.nseg; ++s) nch += (P.seg[s].K + 15) / 16;
+  float ra[4], rb[4];
+  auto load = [&](int ch) {
+    int s = 0, c = ch;
+    while (c >= (P.seg[s].K + 15) / 16) { c -= (P.seg[s].K + 15) / 16; ++s; }
+    const GemmSeg& G = P.seg[s];
+    const int k0 = c * 16;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int i = tid + r * 256;
+      int mm, kk;
+      if (G.sak == 1) { mm = i >> 4; kk = i & 15; } else { kk = i >> 6; mm = i & 63; }
+      const int m = m0 + mm, k = k0 + kk;
+      ra[r] = (m < P.M && k < G.K) ? G.A[m * G.sam + k * G.sak] : 0.0f;
+      int nn, kb;
+      if (G.sbk == 1) { nn = i >> 4; kb = i & 15; } else { kb = i >> 6; nn = i & 63; }
+      const int n = n0 + nn, k2 = k0 + kb;
+      rb[r] = (n < P.N && k2 < G.K) ? G.B[n * G.sbn + k2 * G.sbk] : 0.0f;
+    }
+  };
+  auto store = [&](int ch, int buf) {
+    int s = 0, c = ch;
+    while (c >= (P.seg[s].K + 15) / 16) { c -= (P.seg[s].K + 15) / 16; ++s; }
+    const GemmSeg& G = P.seg[s];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int i = tid + r * 256;
+      int mm, kk;
+      if (G.sak == 1) { mm = i >> 4; kk = i & 15; } else { kk = i >> 6; mm = i & 63; }
+      As[buf][kk][mm] = ra[r];
+      int nn, kb;
+      if (G.sbk == 1) { nn = i >> 4; kb = i & 15; } else { kb = i >> 6; nn = i & 63; }
+      Bs[buf][kb][nn] = rb[r];
+    }
+  };
+  if (nch > 0) {
+    load(0);
+    store(0, 0);
+  }
+  __syncthreads();
+  for (int ch = 0; ch < nch; ++ch) {
+    const int buf = ch & 1;
+    if (ch + 1 < nch) load(ch + 1);
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      float a[4], bb[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[buf][kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bb[j] = Bs[buf][kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], bb[j], acc[i][j]);
+    }
+    if (ch + 1 < nch) store(ch + 1, buf ^ 1);
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int m = m0 + ty * 4 + i;
+    if (m >= P.M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int n = n0 + tx * 4 + j;
+      if (n >= P.N) continue;
+      float v = acc[i][j];
+      if (P.bias) v += P.bias[n];
+      float* cp = P.C + m * P.ldc + n;
+      if (P.beta != 0.0f) v += P.beta * *cp;
+      *cp = v;
+    }
+  }
+}
+
+// column sums of a short, wide matrix: one thread per column, fp64 over the rows
+template <typename T>
+__global__ void k_col_sum_tall(const T* __restrict__ x, long long M, int C, float* __restrict__ out, int accumulate) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  double s = 0.0;
+  for (long long p = 0; p < M; ++p) s += (double)to_f<T>(x[p * C + c]);
+  out[c] = accumulate ? out[c] + (float)s : (float)s;
+}
+
 // ===================================================================== gathers
 __global__ void k_gather_rows(const float* __restrict__ table, const int32_t* __restrict__ idx, int n, int dim,
                               float* __restrict__ out, int ldo) {
@@ -167,6 +269,20 @@ __global__ void k_scatter_add_rows(const float* __restrict__ src, int lds, const
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= dim) return;
   for (int i = 0; i < n; ++i) dtable[(long long)idx[i] * dim + j] += src[(long long)i * lds + j];
+}
+__global__ void k_scatter_add_rows_multi(const RowSrcs srcs, int lds, const int32_t* __restrict__ idx, int n, int dim,
+                                         float* __restrict__ dtable) {
+  const int r = blockIdx.y;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= dim) return;
+  float acc = 0.0f;
+  bool hit = false;
+  for (int i = 0; i < n; ++i) {
+    if (idx[i] != r) continue;
+    hit = true;
+    for (int s = 0; s < srcs.n; ++s) acc += srcs.p[s][(long long)i * lds + j];
+  }
+  if (hit) dtable[(long long)r * dim + j] += acc;
 }
 template <typename TD>
 __global__ void k_convert(const float* __restrict__ s, TD* __restrict__ d, long long n) {
@@ -1391,6 +1507,19 @@ cudaError_t gemm_f32(int M, int N, int K, const float* A, long long sam, long lo
   k_gemm<float><<<g, 256, 0, st>>>(M, N, K, A, 0, sam, sak, B, 0, sbn, sbk, C, 0, ldc, beta, bias);
   return cudaGetLastError();
 }
+int gemm_grouped_plan(GemmProblem* probs, int nprob) {
+  int t = 0;
+  for (int i = 0; i < nprob; ++i) {
+    probs[i].tile0 = t;
+    t += ceil_div(probs[i].M, 64) * ceil_div(probs[i].N, 64);
+  }
+  return t;
+}
+cudaError_t gemm_f32_grouped(const GemmProblem* probs_dev, int nprob, int total_tiles, cudaStream_t st) {
+  if (total_tiles <= 0) return cudaSuccess;
+  k_gemm_grouped<<<total_tiles, 256, 0, st>>>(probs_dev, nprob);
+  return cudaGetLastError();
+}
 cudaError_t gemm_f32_batched(int batch, int M, int N, int K, const float* A, long long sab, long long sam,
                              long long sak, const float* B, long long sbb, long long sbn, long long sbk, float* C,
                              long long scb, long long ldc, float beta, cudaStream_t st) {
@@ -1420,6 +1549,13 @@ cudaError_t gather_rows(const float* table, const int32_t* idx, int n, int dim, 
 }
 cudaError_t copy_cols(const float* src, int lds, int n, int cols, float* dst, int ldd, cudaStream_t st) {
   k_copy_cols<<<grid_for((long long)n * cols, 256), 256, 0, st>>>(src, lds, n, cols, dst, ldd);
+  return cudaGetLastError();
+}
+cudaError_t scatter_add_rows_multi(const RowSrcs& srcs, int lds, const int32_t* idx, int n, int dim, int table_rows,
+                                   float* dtable, cudaStream_t st) {
+  if (srcs.n < 1 || srcs.n > 8) return cudaErrorInvalidValue;
+  dim3 g(ceil_div(dim, 128), table_rows);
+  k_scatter_add_rows_multi<<<g, 128, 0, st>>>(srcs, lds, idx, n, dim, dtable);
   return cudaGetLastError();
 }
 cudaError_t scatter_add_rows(const float* src, int lds, const int32_t* idx, int n, int dim, float* dtable,
@@ -1594,6 +1730,10 @@ cudaError_t up2_bwd(const T* dy, int N, int H, int W, int C, T* dx, cudaStream_t
 template <typename T>
 cudaError_t col_sum(const T* dy, long long M, int C, double* partial, int max_blocks, float* db, int accumulate,
                     cudaStream_t st) {
+  if (M <= 1024 && C >= 1024) {   // short and wide (e.g. the G linear's bias): a thread per column
+    k_col_sum_tall<T><<<ceil_div(C, 256), 256, 0, st>>>(dy, M, C, db, accumulate);
+    return cudaGetLastError();
+  }
   int nblk = (int)((M + 1023) / 1024);
   if (nblk > max_blocks) nblk = max_blocks;
   const long long per = (M + nblk - 1) / nblk;
@@ -1819,179 +1959,261 @@ cudaError_t scale_f32(float* p, long long n, float s, cudaStream_t st) {
 // ============================================================================
 namespace pg {
 namespace {
-constexpr int kTH = 8, kTW = 32;                 // output tile: 8 rows x 32 cols
-constexpr int kHR = kTH + 2, kHC = kTW + 2;      // halo tile
-constexpr int kPlane = kHR * kHC + 13;           // 353 = 1 (mod 32)
-constexpr int kCC = 16;                          // channels per chunk
-
-template <typename TI>
-__device__ __forceinline__ void load_halo(const TI* __restrict__ x, int n, int H, int W, int C, int h0, int w0, int c0,
-                                          int cc, float* xs) {
-  // xs[c][r][s] <- x[n][h0 - 1 + r][w0 - 1 + s][c0 + c]  (zero outside the image / channel range)
-  for (int i = threadIdx.x; i < kHR * kHC * cc; i += blockDim.x) {
-    const int c = i % cc;
-    const int rs = i / cc;
-    const int s = rs % kHC, r = rs / kHC;
-    const int h = h0 - 1 + r, w = w0 - 1 + s;
-    float v = 0.0f;
-    if (h >= 0 && h < H && w >= 0 && w < W && c0 + c < C) v = to_f<TI>(x[(((long long)n * H + h) * W + w) * C + c0 + c]);
-    xs[c * kPlane + r * kHC + s] = v;
-  }
-}
-
-// y[m][o] = bias[o] + sum_{tap,c} x[m+tap][c] w[o][tap][c]; one thread per output pixel
+// ---------------------------------------------------------------------------
+// fprop: y[m][o] = bias[o] + sum_{tap,c} x[m+tap][c] w[o][tap][c]
+// tile 32 rows x 64 cols, thread = 8 consecutive pixels of one row (acc[8][CO] in registers);
+// 8-channel halo chunks staged in smem ([c][row][68] planes), weights as [c][28] so each
+// channel's 27 taps x outputs come in 7 broadcast float4 loads; rows slide through 3 float4s.
+constexpr int kFTH = 32, kFTW = 64, kFCC = 8, kFRS = 68;
+constexpr int kFPlane = (kFTH + 2) * kFRS;
 template <int CO>
-__global__ void __launch_bounds__(256) k_thin_fwd(const float* __restrict__ x, int N, int H, int W, int C,
+__global__ void __launch_bounds__(256, 2) k_thin_fwd(const float* __restrict__ x, int N, int H, int W, int C,
                                                   const float* __restrict__ w, const float* __restrict__ bias,
                                                   float* __restrict__ y) {
-  extern __shared__ float sm[];
-  float* ws = sm;                       // [CO][9][C]
-  float* xs = sm + CO * 9 * C;          // [kCC][kPlane]
-  const int tiles_w = (W + kTW - 1) / kTW, tiles_h = (H + kTH - 1) / kTH;
+  extern __shared__ float4 sm4[];
+  float* ws = reinterpret_cast<float*>(sm4);   // [C][28]
+  float* xs = ws + C * 28;                      // [kFCC][kFPlane]
+  const int tiles_w = (W + kFTW - 1) / kFTW, tiles_h = (H + kFTH - 1) / kFTH;
   int t = blockIdx.x;
   const int tw = t % tiles_w;
   t /= tiles_w;
   const int th = t % tiles_h;
   const int n = t / tiles_h;
-  const int h0 = th * kTH, w0 = tw * kTW;
-  for (int i = threadIdx.x; i < CO * 9 * C; i += blockDim.x) ws[i] = w[i];
-  const int py = threadIdx.x / kTW, px = threadIdx.x % kTW;
-  float acc[CO];
+  const int h0 = th * kFTH, w0 = tw * kFTW;
+  for (int i = threadIdx.x; i < C * 28; i += blockDim.x) {
+    const int c = i / 28, k = i - c * 28;
+    ws[i] = k < CO * 9 ? w[(long long)k * C + c] : 0.0f;
+  }
+  const int py = threadIdx.x >> 3, px0 = (threadIdx.x & 7) * 8;
+  float acc[8][CO];
 #pragma unroll
-  for (int o = 0; o < CO; ++o) acc[o] = 0.0f;
-  for (int c0 = 0; c0 < C; c0 += kCC) {
-    const int cc = min(kCC, C - c0);
+  for (int p = 0; p < 8; ++p)
+#pragma unroll
+    for (int o = 0; o < CO; ++o) acc[p][o] = 0.0f;
+  for (int c0 = 0; c0 < C; c0 += kFCC) {
     __syncthreads();
-    load_halo<float>(x, n, H, W, C, h0, w0, c0, cc, xs);
+    for (int i = threadIdx.x; i < (kFTH + 2) * (kFTW + 2) * 2; i += blockDim.x) {
+      const int half = i & 1, rs = i >> 1;
+      const int sx = rs % (kFTW + 2), r = rs / (kFTW + 2);
+      const int h = h0 - 1 + r, ww = w0 - 1 + sx;
+      const int c = c0 + half * 4;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (h >= 0 && h < H && ww >= 0 && ww < W && c < C)
+        v = *reinterpret_cast<const float4*>(x + (((long long)n * H + h) * W + ww) * C + c);
+      float* d = xs + half * 4 * kFPlane + r * kFRS + sx;
+      d[0] = v.x;
+      d[kFPlane] = v.y;
+      d[2 * kFPlane] = v.z;
+      d[3 * kFPlane] = v.w;
+    }
     __syncthreads();
+    const int cc = min(kFCC, C - c0);
     for (int c = 0; c < cc; ++c) {
-      const float* plane = xs + c * kPlane;
+      const float* plane = xs + c * kFPlane;
+      float wv[28];
 #pragma unroll
-      for (int r = 0; r < 3; ++r)
+      for (int k = 0; k < 7; ++k) {
+        const float4 q = *reinterpret_cast<const float4*>(ws + (c0 + c) * 28 + 4 * k);
+        wv[4 * k] = q.x;
+        wv[4 * k + 1] = q.y;
+        wv[4 * k + 2] = q.z;
+        wv[4 * k + 3] = q.w;
+      }
 #pragma unroll
-        for (int s = 0; s < 3; ++s) {
-          const float xv = plane[(py + r) * kHC + px + s];
+      for (int r = 0; r < 3; ++r) {
+        float xr[12];
 #pragma unroll
-          for (int o = 0; o < CO; ++o) acc[o] = fmaf(xv, ws[(o * 9 + r * 3 + s) * C + c0 + c], acc[o]);
+        for (int k = 0; k < 3; ++k) {
+          const float4 q = *reinterpret_cast<const float4*>(plane + (py + r) * kFRS + px0 + 4 * k);
+          xr[4 * k] = q.x;
+          xr[4 * k + 1] = q.y;
+          xr[4 * k + 2] = q.z;
+          xr[4 * k + 3] = q.w;
         }
+#pragma unroll
+        for (int sx = 0; sx < 3; ++sx)
+#pragma unroll
+          for (int p = 0; p < 8; ++p)
+#pragma unroll
+            for (int o = 0; o < CO; ++o) acc[p][o] = fmaf(xr[p + sx], wv[o * 9 + r * 3 + sx], acc[p][o]);
+      }
     }
   }
-  const int h = h0 + py, ww = w0 + px;
-  if (h < H && ww < W) {
+  const int h = h0 + py;
+  if (h >= H) return;
+#pragma unroll
+  for (int p = 0; p < 8; ++p) {
+    const int ww = w0 + px0 + p;
+    if (ww >= W) break;
     const long long m = ((long long)n * H + h) * W + ww;
 #pragma unroll
-    for (int o = 0; o < CO; ++o) y[m * CO + o] = acc[o] + (bias ? bias[o] : 0.0f);
+    for (int o = 0; o < CO; ++o) y[m * CO + o] = acc[p][o] + (bias ? bias[o] : 0.0f);
   }
 }
 
-// dx[m][c] = sum_{tap,o} dy[m - delta_tap][o] w[o][tap][c]  (transposed 3x3, pad 1)
-// block = 64 pixels (2 rows x 32) x 4 channel groups; each thread CPT channels of one pixel
-template <int CO, int CPT>
+// ---------------------------------------------------------------------------
+// dgrad: dx[m][c] = sum_{o,r,s} dy[h+1-r][w+1-s][o] w[o][r][s][c]  (transposed 3x3, pad 1)
+// tile 8 rows x 64 cols; thread = pixels (row, px) and (row, px+32) with their 2 x 27 dy taps in
+// registers; loops over channels in fours: 4 x 7 broadcast float4 weight loads per 216 FMAs.
+constexpr int kDTH = 8, kDTW = 64;
+template <int CO>
 __global__ void __launch_bounds__(256) k_thin_dgrad(const float* __restrict__ dy, int N, int H, int W, int C,
                                                     const float* __restrict__ w, float* __restrict__ dx) {
-  extern __shared__ float sm[];
-  float* ws = sm;                                 // [CO][9][C]
-  float* ds = sm + CO * 9 * C;                    // [CO][4][34] halo of dy for a 2 x 32 tile
-  const int tiles_w = (W + 31) / 32, tiles_h = (H + 1) / 2;
+  extern __shared__ float4 sm4[];
+  float* ws = reinterpret_cast<float*>(sm4);        // [C][28]
+  float* ds = ws + C * 28;                           // [CO][kDTH + 2][kDTW + 2]
+  const int tiles_w = (W + kDTW - 1) / kDTW, tiles_h = (H + kDTH - 1) / kDTH;
   int t = blockIdx.x;
   const int tw = t % tiles_w;
   t /= tiles_w;
   const int th = t % tiles_h;
   const int n = t / tiles_h;
-  const int h0 = th * 2, w0 = tw * 32;
-  for (int i = threadIdx.x; i < CO * 9 * C; i += blockDim.x) ws[i] = w[i];
-  for (int i = threadIdx.x; i < CO * 4 * 34; i += blockDim.x) {
-    const int s = i % 34, r = (i / 34) % 4, o = i / 136;
-    const int h = h0 - 1 + r, ww = w0 - 1 + s;
-    ds[i] = (h >= 0 && h < H && ww >= 0 && ww < W) ? dy[(((long long)n * H + h) * W + ww) * CO + o] : 0.0f;
+  const int h0 = th * kDTH, w0 = tw * kDTW;
+  for (int i = threadIdx.x; i < C * 28; i += blockDim.x) {
+    const int c = i / 28, k = i - c * 28;
+    ws[i] = k < CO * 9 ? w[(long long)k * C + c] : 0.0f;
+  }
+  constexpr int HR = kDTH + 2, HC = kDTW + 2;
+  for (int i = threadIdx.x; i < CO * HR * HC; i += blockDim.x) {
+    const int o = i % CO, rs = i / CO;
+    const int sx = rs % HC, r = rs / HC;
+    const int h = h0 - 1 + r, ww = w0 - 1 + sx;
+    ds[(o * HR + r) * HC + sx] =
+        (h >= 0 && h < H && ww >= 0 && ww < W) ? dy[(((long long)n * H + h) * W + ww) * CO + o] : 0.0f;
   }
   __syncthreads();
-  const int pix = threadIdx.x & 63, grp = threadIdx.x >> 6;
-  const int py = pix >> 5, px = pix & 31;
-  const int h = h0 + py, ww = w0 + px;
-  if (h >= H || ww >= W) return;
-  // dx at (h, w) gathers dy at (h + 1 - r, w + 1 - s) with tap (r, s)
-  float d[CO][9];
+  const int row = threadIdx.x >> 5, px = threadIdx.x & 31;
+  const int h = h0 + row;
+  // dx at (h, w) gathers dy at (h + 1 - r, w + 1 - s): halo row row + 2 - r, column px + 2 - s
+  float d0[CO * 9], d1[CO * 9];
 #pragma unroll
   for (int o = 0; o < CO; ++o)
 #pragma unroll
     for (int r = 0; r < 3; ++r)
 #pragma unroll
-      for (int s = 0; s < 3; ++s) d[o][r * 3 + s] = ds[(o * 4 + (py + 2 - r)) * 34 + (px + 2 - s)];
-  const long long m = ((long long)n * H + h) * W + ww;
-  for (int cb = grp * CPT; cb < C; cb += 4 * CPT) {
-    float acc[CPT];
-#pragma unroll
-    for (int j = 0; j < CPT; ++j) acc[j] = 0.0f;
-#pragma unroll
-    for (int o = 0; o < CO; ++o)
-#pragma unroll
-      for (int tp = 0; tp < 9; ++tp) {
-        const float dv = d[o][tp];
-        const float* wr = ws + (o * 9 + tp) * C + cb;
-#pragma unroll
-        for (int j = 0; j < CPT; ++j) acc[j] = fmaf(dv, wr[j], acc[j]);
+      for (int sx = 0; sx < 3; ++sx) {
+        d0[o * 9 + r * 3 + sx] = ds[(o * HR + row + 2 - r) * HC + px + 2 - sx];
+        d1[o * 9 + r * 3 + sx] = ds[(o * HR + row + 2 - r) * HC + px + 32 + 2 - sx];
       }
+  const int wa = w0 + px, wb = w0 + px + 32;
+  const bool va = h < H && wa < W, vb = h < H && wb < W;
+  float* xa = dx + (((long long)n * H + h) * W + wa) * C;
+  float* xb = dx + (((long long)n * H + h) * W + wb) * C;
+  for (int c = 0; c < C; c += 4) {
+    float a[4], bq[4];
 #pragma unroll
-    for (int j = 0; j < CPT; ++j)
-      if (cb + j < C) dx[m * C + cb + j] = acc[j];
+    for (int j = 0; j < 4; ++j) {
+      float wv[28];
+#pragma unroll
+      for (int k = 0; k < 7; ++k) {
+        const float4 q = *reinterpret_cast<const float4*>(ws + (c + j) * 28 + 4 * k);
+        wv[4 * k] = q.x;
+        wv[4 * k + 1] = q.y;
+        wv[4 * k + 2] = q.z;
+        wv[4 * k + 3] = q.w;
+      }
+      float sa = 0.0f, sb = 0.0f;
+#pragma unroll
+      for (int k = 0; k < CO * 9; ++k) {
+        sa = fmaf(d0[k], wv[k], sa);
+        sb = fmaf(d1[k], wv[k], sb);
+      }
+      a[j] = sa;
+      bq[j] = sb;
+    }
+    if (va) *reinterpret_cast<float4*>(xa + c) = make_float4(a[0], a[1], a[2], a[3]);
+    if (vb) *reinterpret_cast<float4*>(xb + c) = make_float4(bq[0], bq[1], bq[2], bq[3]);
   }
 }
 
-// dW[o][tap][c] partials: persistent blocks over 8x32 pixel tiles; thread = (c-lane, tap), 3 channel
-// chunks of 32 kept in registers; per-block partials [grid][CO*9*C] reduced in fixed order afterwards
+// ---------------------------------------------------------------------------
+// wgrad partials: dW[o][tap][c] over one block's pixel tiles.  Persistent blocks walk 8 x 16
+// pixel tiles; thread = (channel c, row half) keeps all 27 (o, tap) sums in registers; x is staged
+// channel-innermost ([10][18][C]) so a warp reads consecutive channels, dy as [128][4] (one
+// broadcast float4 per pixel), and the 3x3 neighbourhood slides along the row (3 new loads/pixel).
+constexpr int kWTH = 8, kWTW = 16;
 template <int CO>
-__global__ void __launch_bounds__(288) k_thin_wgrad(const float* __restrict__ x, const float* __restrict__ dy, int N,
+__global__ void __launch_bounds__(256) k_thin_wgrad(const float* __restrict__ x, const float* __restrict__ dy, int N,
                                                     int H, int W, int C, float* __restrict__ partial) {
-  extern __shared__ float sm[];
-  float* xs = sm;                          // [32][kPlane]
-  float* ds = sm + 32 * kPlane;            // [CO][256]
-  const int tiles_w = (W + kTW - 1) / kTW, tiles_h = (H + kTH - 1) / kTH;
+  extern __shared__ float4 sm4[];
+  float* xs = reinterpret_cast<float*>(sm4);                 // [kWTH+2][kWTW+2][C]
+  float* dys = xs + (kWTH + 2) * (kWTW + 2) * C;              // [kWTH*kWTW][4]
+  float* red = dys + kWTH * kWTW * 4;                         // [C][CO*9] second-half sums
+  const int tiles_w = (W + kWTW - 1) / kWTW, tiles_h = (H + kWTH - 1) / kWTH;
   const int tiles = N * tiles_h * tiles_w;
-  const int cl = threadIdx.x & 31, tap = threadIdx.x >> 5;   // tap 0..8
-  const int r = tap / 3, s = tap % 3;
-  constexpr int MAXCH = 4;                 // up to 128 channels = 4 chunks of 32
-  float acc[MAXCH][CO];
+  const int c = threadIdx.x % C, half = threadIdx.x / C;      // blockDim = 2 C
+  float acc[CO * 9];
 #pragma unroll
-  for (int k = 0; k < MAXCH; ++k)
-#pragma unroll
-    for (int o = 0; o < CO; ++o) acc[k][o] = 0.0f;
-  const int nch = (C + 31) / 32;
+  for (int k = 0; k < CO * 9; ++k) acc[k] = 0.0f;
+  constexpr int HC = kWTW + 2;
   for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
     int u = t;
     const int tw = u % tiles_w;
     u /= tiles_w;
     const int th = u % tiles_h;
     const int n = u / tiles_h;
-    const int h0 = th * kTH, w0 = tw * kTW;
+    const int h0 = th * kWTH, w0 = tw * kWTW;
     __syncthreads();
-    for (int i = threadIdx.x; i < CO * 256; i += blockDim.x) {
-      const int o = i / 256, p = i % 256;
-      const int h = h0 + p / kTW, ww = w0 + p % kTW;
-      ds[i] = (h < H && ww < W) ? dy[(((long long)n * H + h) * W + ww) * CO + o] : 0.0f;
+    const int nvec = (kWTH + 2) * HC * (C / 4);
+    for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
+      const int cv = i % (C / 4), rs = i / (C / 4);
+      const int sx = rs % HC, r = rs / HC;
+      const int h = h0 - 1 + r, ww = w0 - 1 + sx;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (h >= 0 && h < H && ww >= 0 && ww < W)
+        v = *reinterpret_cast<const float4*>(x + (((long long)n * H + h) * W + ww) * C + cv * 4);
+      *reinterpret_cast<float4*>(xs + rs * C + cv * 4) = v;
     }
+    for (int i = threadIdx.x; i < kWTH * kWTW; i += blockDim.x) {
+      const int h = h0 + i / kWTW, ww = w0 + i % kWTW;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (h < H && ww < W) {
+        const float* q = dy + (((long long)n * H + h) * W + ww) * CO;
+        v.x = q[0];
+        if (CO > 1) v.y = q[1];
+        if (CO > 2) v.z = q[2];
+      }
+      *reinterpret_cast<float4*>(dys + i * 4) = v;
+    }
+    __syncthreads();
+    for (int py = half; py < kWTH; py += 2) {
+      // window xw[r][s] = x[py + r][px + s][c] for the current px
+      float xw[3][3];
 #pragma unroll
-    for (int k = 0; k < MAXCH; ++k) {
-      if (k >= nch) break;
-      __syncthreads();
-      load_halo<float>(x, n, H, W, C, h0, w0, k * 32, min(32, C - k * 32), xs);
-      __syncthreads();
-      const float* plane = xs + cl * kPlane;
-      for (int p = 0; p < 256; ++p) {
-        const int py = p / kTW, px = p % kTW;
-        const float xv = plane[(py + r) * kHC + px + s];
+      for (int r = 0; r < 3; ++r) {
+        xw[r][0] = xs[((py + r) * HC + 0) * C + c];
+        xw[r][1] = xs[((py + r) * HC + 1) * C + c];
+      }
+#pragma unroll 4
+      for (int px = 0; px < kWTW; ++px) {
 #pragma unroll
-        for (int o = 0; o < CO; ++o) acc[k][o] = fmaf(xv, ds[o * 256 + p], acc[k][o]);
+        for (int r = 0; r < 3; ++r) xw[r][2] = xs[((py + r) * HC + px + 2) * C + c];
+        const float4 g = *reinterpret_cast<const float4*>(dys + (py * kWTW + px) * 4);
+        const float gv[3] = {g.x, g.y, g.z};
+#pragma unroll
+        for (int o = 0; o < CO; ++o)
+#pragma unroll
+          for (int r = 0; r < 3; ++r)
+#pragma unroll
+            for (int sx = 0; sx < 3; ++sx) acc[o * 9 + r * 3 + sx] = fmaf(gv[o], xw[r][sx], acc[o * 9 + r * 3 + sx]);
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          xw[r][0] = xw[r][1];
+          xw[r][1] = xw[r][2];
+        }
       }
     }
   }
-  float* pb = partial + (long long)blockIdx.x * CO * 9 * C;
+  // combine the two row halves, write this block's partial [CO*9][C]
+  __syncthreads();
+  if (half == 1)
 #pragma unroll
-  for (int k = 0; k < MAXCH; ++k) {
-    const int c = k * 32 + cl;
-    if (k < nch && c < C)
+    for (int k = 0; k < CO * 9; ++k) red[c * CO * 9 + k] = acc[k];
+  __syncthreads();
+  if (half == 0) {
+    float* pb = partial + (long long)blockIdx.x * CO * 9 * C;
 #pragma unroll
-      for (int o = 0; o < CO; ++o) pb[(o * 9 + tap) * C + c] = acc[k][o];
+    for (int k = 0; k < CO * 9; ++k) pb[k * C + c] = acc[k] + red[c * CO * 9 + k];
   }
 }
 __global__ void k_reduce_rows_f32(const float* __restrict__ partial, int rows, int n, float* __restrict__ out) {
@@ -2005,34 +2227,36 @@ __global__ void k_reduce_rows_f32(const float* __restrict__ partial, int rows, i
 
 cudaError_t thin_conv_fwd(const float* x, int N, int H, int W, int C, const float* w, int CO, const float* bias,
                           float* y, cudaStream_t st) {
-  if (CO != 3) return cudaErrorInvalidValue;
-  const int tiles = N * ((H + kTH - 1) / kTH) * ((W + kTW - 1) / kTW);
-  const size_t sm = (size_t)(CO * 9 * C + kCC * kPlane) * sizeof(float);
-  if (sm > 48 * 1024) PG_CUDA(cudaFuncSetAttribute(k_thin_fwd<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  if (CO != 3 || C % 4 || ((uintptr_t)x & 15)) return cudaErrorInvalidValue;
+  const int tiles = N * ((H + kFTH - 1) / kFTH) * ((W + kFTW - 1) / kFTW);
+  const size_t sm = (size_t)(C * 28 + kFCC * kFPlane) * sizeof(float);
+  PG_CUDA(cudaFuncSetAttribute(k_thin_fwd<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   k_thin_fwd<3><<<tiles, 256, sm, st>>>(x, N, H, W, C, w, bias, y);
   return cudaGetLastError();
 }
 cudaError_t thin_conv_dgrad(const float* dy, int N, int H, int W, int C, const float* w, int CO, float* dx,
                             cudaStream_t st) {
-  if (CO != 3 || C % 8) return cudaErrorInvalidValue;
-  const int tiles = N * ((H + 1) / 2) * ((W + 31) / 32);
-  const size_t sm = (size_t)(CO * 9 * C + CO * 4 * 34) * sizeof(float);
-  if (sm > 48 * 1024)
-    PG_CUDA(cudaFuncSetAttribute(k_thin_dgrad<3, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  k_thin_dgrad<3, 8><<<tiles, 256, sm, st>>>(dy, N, H, W, C, w, dx);
+  if (CO != 3 || C % 4 || ((uintptr_t)dx & 15)) return cudaErrorInvalidValue;
+  const int tiles = N * ((H + kDTH - 1) / kDTH) * ((W + kDTW - 1) / kDTW);
+  const size_t sm = (size_t)(C * 28 + CO * (kDTH + 2) * (kDTW + 2)) * sizeof(float);
+  PG_CUDA(cudaFuncSetAttribute(k_thin_dgrad<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  k_thin_dgrad<3><<<tiles, 256, sm, st>>>(dy, N, H, W, C, w, dx);
   return cudaGetLastError();
 }
 cudaError_t thin_conv_wgrad(const float* x, const float* dy, int N, int H, int W, int C, int CO, float* dw,
                             float* scratch, size_t scratch_floats, cudaStream_t st) {
-  if (CO != 3 || C > 128) return cudaErrorInvalidValue;
-  const int tiles = N * ((H + kTH - 1) / kTH) * ((W + kTW - 1) / kTW);
-  int grid = 4 * kNumSMs;
+  if (CO != 3 || C % 4 || C > 128 || ((uintptr_t)x & 15)) return cudaErrorInvalidValue;
+  const int tiles = N * ((H + kWTH - 1) / kWTH) * ((W + kWTW - 1) / kWTW);
+  const size_t sm = (size_t)((kWTH + 2) * (kWTW + 2) * C + kWTH * kWTW * 4 + C * CO * 9) * sizeof(float);
+  int per_sm = (int)(200 * 1024 / sm);
+  if (per_sm < 1) per_sm = 1;
+  if (per_sm > 4) per_sm = 4;
+  int grid = per_sm * kNumSMs;
   if (grid > tiles) grid = tiles;
   const int n = CO * 9 * C;
   while ((size_t)grid * n > scratch_floats && grid > 1) grid /= 2;
-  const size_t sm = (size_t)(32 * kPlane + CO * 256) * sizeof(float);
-  if (sm > 48 * 1024) PG_CUDA(cudaFuncSetAttribute(k_thin_wgrad<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  k_thin_wgrad<3><<<grid, 288, sm, st>>>(x, dy, N, H, W, C, scratch);
+  PG_CUDA(cudaFuncSetAttribute(k_thin_wgrad<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  k_thin_wgrad<3><<<grid, 2 * C, sm, st>>>(x, dy, N, H, W, C, scratch);
   PG_LAUNCH_CHECK();
   k_reduce_rows_f32<<<ceil_div(n, 256), 256, 0, st>>>(scratch, grid, n, dw);
   return cudaGetLastError();

@@ -19,6 +19,28 @@ cudaError_t layout_unpack(const TS* src, float* dst, int n, int c, int h, int w,
 
 // ---------------- small fp32 GEMM: C[m][n] = beta*C + sum_k A(m,k) B(n,k) (+ bias[n])
 // A(m,k) = A[m*sam + k*sak]; B(n,k) = B[n*sbn + k*sbk]; C[m*ldc + n]
+// Grouped fp32 GEMM: every problem p computes
+//   C_p[M][N] = beta * C_p + bias_p[n] + sum_{s < nseg} A_s[M][K_s] B_s[N][K_s]^T
+// (general strides), all problems in one launch; the table lives in device memory and
+// tile0 is the prefix sum of the problems' 64x64 tile counts (see gemm_grouped_plan).
+struct GemmSeg {
+  const float* A;
+  long long sam, sak;
+  const float* B;
+  long long sbn, sbk;
+  int K;
+};
+struct GemmProblem {
+  int M, N, nseg, tile0;
+  GemmSeg seg[4];
+  float* C;
+  long long ldc;
+  float beta;
+  const float* bias;
+};
+// fills tile0 and returns the total tile count
+int gemm_grouped_plan(GemmProblem* probs, int nprob);
+cudaError_t gemm_f32_grouped(const GemmProblem* probs_dev, int nprob, int total_tiles, cudaStream_t st);
 cudaError_t gemm_f32(int M, int N, int K, const float* A, long long sam, long long sak, const float* B,
                      long long sbn, long long sbk, float* C, long long ldc, float beta, const float* bias,
                      cudaStream_t st);
@@ -31,6 +53,14 @@ cudaError_t to_f32(const TS* src, float* dst, long long n, cudaStream_t st);
 cudaError_t gather_rows(const float* table, const int32_t* idx, int n, int dim, float* out, int ldo, cudaStream_t st);
 cudaError_t copy_cols(const float* src, int lds, int n, int cols, float* dst, int ldd, cudaStream_t st);
 // dtable[idx[i]][j] += src[i*lds + j]; deterministic (sequential over i per column)
+// dtable[r][j] += sum_{i: idx[i] == r} sum_s srcs.p[s][i][j]  for up to 8 sources; one thread per
+// (table row, j), rows i visited in order (deterministic, no atomics)
+struct RowSrcs {
+  const float* p[8];
+  int n;
+};
+cudaError_t scatter_add_rows_multi(const RowSrcs& srcs, int lds, const int32_t* idx, int n, int dim, int table_rows,
+                                   float* dtable, cudaStream_t st);
 cudaError_t scatter_add_rows(const float* src, int lds, const int32_t* idx, int n, int dim, float* dtable,
                              cudaStream_t st);
 

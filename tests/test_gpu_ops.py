@@ -162,3 +162,33 @@ def test_simt_conv_f32(shape):
     (gw,) = torch.autograd.grad((ops.conv2d(xt, wv, None) * torch.from_numpy(dy).double().permute(0, 3, 1, 2)).sum(), wv)
     wantw = gw.permute(0, 2, 3, 1).reshape(cout, k * k, cin).numpy()
     assert np.linalg.norm(dw.cpu().numpy() - wantw) <= 1e-5 * np.linalg.norm(wantw)
+
+
+@pytest.mark.parametrize("shape", [(2, 128, 128, 96), (3, 37, 70, 8), (1, 16, 16, 4), (2, 33, 65, 12), (1, 9, 130, 128)])
+def test_thin_conv_f32_fwd_dgrad_wgrad(shape):
+    """G's fp32 output layer (C_out = 3): the three thin kernels against fp64 autograd of
+    the plain cross-correlation, ragged tiles at the image edges included."""
+    n, h, w, cin = shape
+    cout, k = 3, 3
+    rng = np.random.default_rng(h * w + cin)
+    x = rng.standard_normal((n, h, w, cin)).astype(np.float32)
+    wt = rng.standard_normal((cout, k * k, cin)).astype(np.float32)
+    b = rng.standard_normal(cout).astype(np.float32)
+    dy = rng.standard_normal((n, h, w, cout)).astype(np.float32)
+    xd, wd, bd, dyd = (torch.from_numpy(a).to(DEV) for a in (x, wt, b, dy))
+    y = torch.empty((n, h, w, cout), dtype=torch.float32, device=DEV)
+    dx = torch.empty((n, h, w, cin), dtype=torch.float32, device=DEV)
+    dw = torch.empty((cout, k * k, cin), dtype=torch.float32, device=DEV)
+    api.op_conv_fwd(api.F32, xd, wd, bd, cout, k, y)
+    api.op_conv_dgrad(api.F32, dyd, wd, cin, k, dx)
+    api.op_conv_wgrad(api.F32, xd, dyd, cout, k, dw)
+    torch.cuda.synchronize()
+    xt = torch.from_numpy(x).double().permute(0, 3, 1, 2).requires_grad_(True)
+    wv = torch.from_numpy(wt).double().reshape(cout, k, k, cin).permute(0, 3, 1, 2).contiguous().requires_grad_(True)
+    yt = ops.conv2d(xt, wv, torch.from_numpy(b).double())
+    gx, gw = torch.autograd.grad((yt * torch.from_numpy(dy).double().permute(0, 3, 1, 2)).sum(), (xt, wv))
+    want_y = yt.detach().permute(0, 2, 3, 1).numpy()
+    want_dx = gx.permute(0, 2, 3, 1).numpy()
+    want_dw = gw.permute(0, 2, 3, 1).reshape(cout, k * k, cin).numpy()
+    for got, want in ((y, want_y), (dx, want_dx), (dw, want_dw)):
+        assert np.linalg.norm(got.cpu().numpy() - want) <= 1e-5 * np.linalg.norm(want)
