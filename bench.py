@@ -137,6 +137,18 @@ def run_reference(args):
     return 0
 
 
+def _traffic():
+    """Per-launch DRAM bytes of the conv kernels from the committed ncu launch list (profiles/)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "round*_traffic.json")))
+    if not files:
+        return {}
+    with open(files[-1]) as f:
+        d = json.load(f)
+    d["source"] = os.path.relpath(files[-1], os.path.dirname(os.path.abspath(__file__))) + " (ncu launch list, cold cache)"
+    return d
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -260,6 +272,7 @@ def main():
 
     if rank == 0:
         burst, sustained, hbm, src = _peaks()
+        traffic = _traffic()
         roof = None
         if prof:
             n0, t0, f0_ = prof[0]
@@ -268,7 +281,8 @@ def main():
             roof = {"bound": "tensor", "kernel": "k_conv_fprop (tcgen05 implicit-GEMM conv, fprop+dgrad launches)",
                     "achieved": ach, "peak": sustained, "unit": "TFLOP/s", "frac": ach / sustained,
                     "peak_source": f"bf16_tflops_sustained ({src}); kernel timed inside a long step",
-                    "traffic": None, "launches": n0, "kernel_ms_per_step": t0 / args.steps,
+                    "traffic": traffic.get("conv_fprop", {}).get("dram_bytes_per_launch"),
+                    "traffic_source": traffic.get("source"), "launches": n0, "kernel_ms_per_step": t0 / args.steps,
                     "share_of_step": (t0 / args.steps) / (ms_max / args.steps),
                     "wgrad": {"achieved": (f1_ / (t1 / 1000.0)) / 1e12 if t1 > 0 else 0.0, "launches": n1,
                               "ms_per_step": t1 / args.steps}}

@@ -196,10 +196,12 @@ paragan_status paragan_destroy(paragan_ctx* ctx);
 paragan_status paragan_op_conv_fwd(paragan_dtype dt, const void* x, int32_t n, int32_t h, int32_t w, int32_t cin,
                                    const void* wgt, const float* bias, int32_t cout, int32_t ksz, void* y,
                                    void* stream);
-/* dw[Cout][k*k][Cin] (fp32) = sum_p dy[p][o] * x[p + tap][c].
+/* dw[Cout][k*k][Cin] (fp32) = sum_p dy[p][o] * x[p + tap][c]; db[Cout] (fp32, optional, NULL to skip) =
+ * sum_p dy[p][o], the bias gradient (BF16: computed by the same tcgen05 launch).
  * F32 with Cout = 3, 3x3 (G's fp32 output layer) runs the thin kernels, also in op_conv_fwd. */
 paragan_status paragan_op_conv_wgrad(paragan_dtype dt, const void* x, const void* dy, int32_t n, int32_t h,
-                                     int32_t w, int32_t cin, int32_t cout, int32_t ksz, float* dw, void* stream);
+                                     int32_t w, int32_t cin, int32_t cout, int32_t ksz, float* dw, float* db,
+                                     void* stream);
 /* dx[N,H,W,Cin] = sum_{o,tap} dy[p - delta_tap][o] w[o][tap][c]: the input gradient of the 3x3 conv.
  * F32 only, Cout = 3 (G's fp32 output layer), Cin % 4 == 0; dx 16-byte aligned. */
 paragan_status paragan_op_conv_dgrad(paragan_dtype dt, const void* dy, int32_t n, int32_t h, int32_t w, int32_t cout,

@@ -74,7 +74,7 @@ SYMBOLS = {
     "paragan_op_conv_fwd": (C.c_int, [C.c_int, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
                                       C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
     "paragan_op_conv_wgrad": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
-                                        C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
+                                        C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
     "paragan_op_conv_dgrad": (C.c_int, [C.c_int, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
                                         C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
     "paragan_op_attn_fwd": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
@@ -172,10 +172,10 @@ def op_conv_fwd(dtype, x, wgt, bias, cout, ksz, y, stream=None):
                                                             ksz, _ptr(y), _stream(stream)))
 
 
-def op_conv_wgrad(dtype, x, dy, cout, ksz, dw, stream=None):
+def op_conv_wgrad(dtype, x, dy, cout, ksz, dw, stream=None, db=None):
     n, h, w, cin = x.shape
     _check("paragan_op_conv_wgrad", lib().paragan_op_conv_wgrad(dtype, _ptr(x), _ptr(dy), n, h, w, cin, cout, ksz,
-                                                                _ptr(dw), _stream(stream)))
+                                                                _ptr(dw), _ptr(db), _stream(stream)))
 
 
 def op_conv_dgrad(dtype, dy, wgt, cin, ksz, dx, stream=None):

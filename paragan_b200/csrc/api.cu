@@ -192,7 +192,7 @@ paragan_status paragan_op_conv_fwd(paragan_dtype dt, const void* x, int32_t n, i
 }
 
 paragan_status paragan_op_conv_wgrad(paragan_dtype dt, const void* x, const void* dy, int32_t n, int32_t h, int32_t w,
-                                     int32_t cin, int32_t cout, int32_t ksz, float* dw, void* stream) {
+                                     int32_t cin, int32_t cout, int32_t ksz, float* dw, float* db, void* stream) {
   if (!x || !dy || !dw || n < 1 || h < 1 || w < 1 || cin < 1 || cout < 1 || (ksz != 1 && ksz != 3))
     return PARAGAN_ERR_INVALID_ARG;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -203,24 +203,33 @@ paragan_status paragan_op_conv_wgrad(paragan_dtype dt, const void* x, const void
     float* scratch = nullptr;
     if (cudaMallocAsync(reinterpret_cast<void**>(&scratch), scratch_n * sizeof(float), st) != cudaSuccess)
       return PARAGAN_ERR_CUDA;
-    cudaError_t e = tc_conv_wgrad(x, dy, n, h, w, cin, cout, ksz, dw, 0, scratch, scratch_n, st);
+    cudaError_t e = tc_conv_wgrad(x, dy, n, h, w, cin, cout, ksz, dw, 0, scratch, scratch_n, st, db);
     cudaFreeAsync(scratch, st);
     return cuda_status(e);
   }
-  if (dt == PARAGAN_F32 && cout == 3 && ksz == 3 && cin % 4 == 0 && cin <= 128 && aligned16(x)) {
+  if (dt != PARAGAN_F32) return PARAGAN_ERR_INVALID_ARG;
+  cudaError_t e;
+  if (cout == 3 && ksz == 3 && cin % 4 == 0 && cin <= 128 && aligned16(x)) {
     const size_t scratch_n = (size_t)4 * 148 * 27 * cin;
     float* scratch = nullptr;
     if (cudaMallocAsync(reinterpret_cast<void**>(&scratch), scratch_n * sizeof(float), st) != cudaSuccess)
       return PARAGAN_ERR_CUDA;
-    cudaError_t e = thin_conv_wgrad(static_cast<const float*>(x), static_cast<const float*>(dy), n, h, w, cin, 3, dw,
-                                    scratch, scratch_n, st);
+    e = thin_conv_wgrad(static_cast<const float*>(x), static_cast<const float*>(dy), n, h, w, cin, 3, dw, scratch,
+                        scratch_n, st);
     cudaFreeAsync(scratch, st);
-    return cuda_status(e);
+  } else {
+    e = simt_conv_wgrad<float, float>(static_cast<const float*>(x), static_cast<const float*>(dy), n, h, w, cin, cout,
+                                      ksz, dw, 0, st);
   }
-  if (dt == PARAGAN_F32)
-    return cuda_status(simt_conv_wgrad<float, float>(static_cast<const float*>(x), static_cast<const float*>(dy), n, h,
-                                                     w, cin, cout, ksz, dw, 0, st));
-  return PARAGAN_ERR_INVALID_ARG;
+  if (e == cudaSuccess && db) {
+    double* part = nullptr;
+    constexpr int kBlocks = 1024;
+    if (cudaMallocAsync(reinterpret_cast<void**>(&part), (size_t)kBlocks * cout * sizeof(double), st) != cudaSuccess)
+      return PARAGAN_ERR_CUDA;
+    e = col_sum<float>(static_cast<const float*>(dy), (long long)n * h * w, cout, part, kBlocks, db, 0, st);
+    cudaFreeAsync(part, st);
+  }
+  return cuda_status(e);
 }
 
 paragan_status paragan_op_conv_dgrad(paragan_dtype dt, const void* dy, int32_t n, int32_t h, int32_t w, int32_t cout,

@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <type_traits>
@@ -450,6 +451,7 @@ class Engine final : public EngineBase {
     if (cudaStreamSynchronize(st_) != cudaSuccess) return fail_cuda(cudaGetLastError(), "profile sync");
     uint64_t c = 0;
     double t = 0, f = 0;
+    const bool verbose = std::getenv("PARAGAN_PROFILE_VERBOSE") != nullptr;
     for (auto& r : recs_) {
       if (r.kind != kind) continue;
       float e = 0;
@@ -457,6 +459,7 @@ class Engine final : public EngineBase {
       ++c;
       t += e;
       f += r.flops;
+      if (verbose) std::fprintf(stderr, "PROF kind=%d ms=%.4f tflops=%.1f %s\n", kind, e, r.flops / (e * 1e9), r.what);
     }
     if (n) *n = c;
     if (ms) *ms = t;
@@ -1096,6 +1099,7 @@ class Engine final : public EngineBase {
     int kind;
     double flops;
     cudaEvent_t a, b;
+    char what[48];
   };
   cudaEvent_t ev_get() {
     if (!ev_free_.empty()) {
@@ -1109,9 +1113,10 @@ class Engine final : public EngineBase {
   }
   // brackets one launch with events when profiling; kind 0 = tcgen05 fprop/dgrad, 1 = tcgen05 wgrad
   template <class F>
-  cudaError_t timed(int kind, double flops, F&& f) {
+  cudaError_t timed(int kind, double flops, F&& f, const char* what = "") {
     if (!prof_) return f();
-    ProfRec r{kind, flops, ev_get(), ev_get()};
+    ProfRec r{kind, flops, ev_get(), ev_get(), {0}};
+    std::snprintf(r.what, sizeof(r.what), "%s", what);
     cudaEventRecord(r.a, st_);
     cudaError_t e = f();
     cudaEventRecord(r.b, st_);
@@ -1131,7 +1136,9 @@ class Engine final : public EngineBase {
         e.res_mode = res ? res_mode : 0;
         e.out = y;
         const double fl = 2.0 * n * H * H * (double)c.cout * c.ksz * c.ksz * c.cin;
-        CK(timed(0, fl, [&] { return tc_conv_fprop(x, n, H, H, c.cin_x, c.wp, c.cout, c.ksz, e, st_); }));
+        char what[48];
+        std::snprintf(what, sizeof(what), "fprop n%d %dx%d %d->%d k%d", n, H, H, c.cin, c.cout, c.ksz);
+        CK(timed(0, fl, [&] { return tc_conv_fprop(x, n, H, H, c.cin_x, c.wp, c.cout, c.ksz, e, st_); }, what));
         return PARAGAN_OK;
       }
     }
@@ -1152,7 +1159,9 @@ class Engine final : public EngineBase {
         e.res_mode = add ? 1 : 0;
         e.out = dx;
         const double fl = 2.0 * n * H * H * (double)c.cout * c.ksz * c.ksz * c.cin;
-        CK(timed(0, fl, [&] { return tc_conv_fprop(dy, n, H, H, c.cout, c.wt, c.cin_x, c.ksz, e, st_); }));
+        char what[48];
+        std::snprintf(what, sizeof(what), "dgrad n%d %dx%d %d->%d k%d", n, H, H, c.cout, c.cin, c.ksz);
+        CK(timed(0, fl, [&] { return tc_conv_fprop(dy, n, H, H, c.cout, c.wt, c.cin_x, c.ksz, e, st_); }, what));
         return PARAGAN_OK;
       }
     }
@@ -1162,17 +1171,21 @@ class Engine final : public EngineBase {
                                            st_, static_cast<const float*>(relu_ref))));
     return PARAGAN_OK;
   }
-  // dW (into the net's grad slot, OHWI) = wgrad(x, dy)
-  paragan_status conv_wgrad(Net& N, const void* x, const void* dy, int n, int H, const ConvL& c) {
+  // dW (into the net's grad slot, OHWI) = wgrad(x, dy); db = column sums of dy when bias_entry >= 0
+  // (fused into the tcgen05 wgrad launch in BF16 mode)
+  paragan_status conv_wgrad(Net& N, const void* x, const void* dy, int n, int H, const ConvL& c, int bias_entry = -1) {
     float* dst = N.G(c.w);
     const bool pad = c.cin_x != c.cin;
     float* out = pad ? wg_scratch_ : dst;
     if constexpr (kBF) {
       if (!c.f32) {
         const double fl = 2.0 * n * H * H * (double)c.cout * c.ksz * c.ksz * c.cin;
+        char what[48];
+        std::snprintf(what, sizeof(what), "wgrad n%d %dx%d %d->%d k%d", n, H, H, c.cin, c.cout, c.ksz);
+        float* db = bias_entry >= 0 ? N.G(bias_entry) : nullptr;
         CK(timed(1, fl, [&] {
-          return tc_conv_wgrad(x, dy, n, H, H, c.cin_x, c.cout, c.ksz, out, 0, scratch_f_, scratch_floats_, st_);
-        }));
+          return tc_conv_wgrad(x, dy, n, H, H, c.cin_x, c.cout, c.ksz, out, 0, scratch_f_, scratch_floats_, st_, db);
+        }, what));
         if (pad) CK(copy_rows_cols(out, c.cin_x, (long long)c.cout * c.ksz * c.ksz, c.cin, dst, c.cin, 0, st_));
         return PARAGAN_OK;
       }
@@ -1180,11 +1193,9 @@ class Engine final : public EngineBase {
     CK((simt_conv_wgrad<float, float>(static_cast<const float*>(x), static_cast<const float*>(dy), n, H, H, c.cin_x,
                                       c.cout, c.ksz, out, 0, st_)));
     if (pad) CK(copy_rows_cols(out, c.cin_x, (long long)c.cout * c.ksz * c.ksz, c.cin, dst, c.cin, 0, st_));
-    return PARAGAN_OK;
-  }
-  paragan_status bias_grad(Net& N, const ConvL& c, const void* dy, long long M) {
-    if (c.b < 0) return PARAGAN_OK;
-    CK(col_sum<T>(static_cast<const T*>(dy), M, c.cout, dpart_, kMaxPartialBlocks, N.G(c.b), 0, st_));
+    if (bias_entry >= 0)
+      CK(col_sum<T>(static_cast<const T*>(dy), (long long)n * H * H, c.cout, dpart_, kMaxPartialBlocks,
+                    N.G(bias_entry), 0, st_));
     return PARAGAN_OK;
   }
   paragan_status bgemm(int batch, int M, int N, int K, const void* A, long long sab, long long sam, long long sak,
@@ -1478,7 +1489,6 @@ class Engine final : public EngineBase {
     for (int j = (int)db_.size() - 1; j >= 0; --j) {
       DBlock& b = db_[j];
       const int H = b.hin, Ho = b.hout;
-      const long long Mi = (long long)n * H * H;
       if (b.attn) {
         const int k = other(ic);
         CKS(attn_backward(D_, dattn_, b.out, n, cur, tmp(k), want_w));
@@ -1502,8 +1512,7 @@ class Engine final : public EngineBase {
       // gradient at the conv1 output: dgrad(conv2) masked by relu'(c1) in the epilogue
       CKS(conv_dgrad(dt, n, H, b.c2, dr1, nullptr, nullptr, b.r1));
       if (want_w) {
-        CKS(conv_wgrad(D_, b.r1, dt, n, H, b.c2));
-        CKS(bias_grad(D_, b.c2, dt, Mi));
+        CKS(conv_wgrad(D_, b.r1, dt, n, H, b.c2, b.c2.b));
       }
       // skip branch
       const bool need_dx = (j > 0) || want_dimg;
@@ -1512,8 +1521,7 @@ class Engine final : public EngineBase {
       if (j == 0 && b.down) {
         // s = sc(avgpool(x)) at half res; its gradient is cur (half res)
         if (want_w) {
-          CKS(conv_wgrad(D_, b.xp, cur, n, Ho, b.sc));
-          CKS(bias_grad(D_, b.sc, cur, (long long)n * Ho * Ho));
+          CKS(conv_wgrad(D_, b.xp, cur, n, Ho, b.sc, b.sc.b));
         }
         if (need_dx) {
           isk = other(ic, it, ir1);
@@ -1526,8 +1534,7 @@ class Engine final : public EngineBase {
         }
       } else if (b.learn_sc) {
         if (want_w) {
-          CKS(conv_wgrad(D_, b.x, dt, n, H, b.sc));
-          CKS(bias_grad(D_, b.sc, dt, Mi));
+          CKS(conv_wgrad(D_, b.x, dt, n, H, b.sc, b.sc.b));
         }
         if (need_dx) {
           isk = other(ic, it, ir1);
@@ -1540,9 +1547,8 @@ class Engine final : public EngineBase {
       }
       const void* cin = (j > 0) ? b.rx : b.x;
       if (want_w) {
-        if (b.im2col) CKS(conv_wgrad(D_, b.xi, dr1, n, H, b.c1x));
-        else CKS(conv_wgrad(D_, cin, dr1, n, H, b.c1));
-        CKS(bias_grad(D_, b.c1, dr1, Mi));
+        if (b.im2col) CKS(conv_wgrad(D_, b.xi, dr1, n, H, b.c1x, b.c1.b));
+        else CKS(conv_wgrad(D_, cin, dr1, n, H, b.c1, b.c1.b));
       }
       if (!need_dx) break;
       // dx = relu'(x) * dgrad(conv1) + dskip   (block 0: no pre-activation)
@@ -1594,7 +1600,6 @@ class Engine final : public EngineBase {
     for (int i = (int)gb_.size() - 1; i >= 0; --i) {
       GBlock& b = gb_[i];
       const int H = b.hin, H2 = 2 * H;
-      const long long Mlo = (long long)B * H * H, Mhi = (long long)B * H2 * H2;
       if (b.attn) {
         const int k = (ic + 1) % 4;
         CKS(attn_backward(G_, gattn_, b.out, B, cur, tmp(k), true));
@@ -1604,19 +1609,16 @@ class Engine final : public EngineBase {
       const int i_a2 = (ic + 1) % 4, i_ds = (ic + 2) % 4, i_dxs = (ic + 3) % 4;
       // conv2
       CKS(conv_dgrad(cur, B, H2, b.c2, tmp(i_a2), nullptr));
-      CKS(conv_wgrad(G_, b.a2, cur, B, H2, b.c2));
-      CKS(bias_grad(G_, b.c2, cur, Mhi));
+      CKS(conv_wgrad(G_, b.a2, cur, B, H2, b.c2, b.c2.b));
       // skip: out += up2(s) -> ds = 2x2 sum of dout
       CK(up2_bwd<T>(static_cast<const T*>(cur), B, H, H, b.cout, static_cast<T*>(tmp(i_ds)), st_));
-      CKS(conv_wgrad(G_, b.x, tmp(i_ds), B, H, b.sc));
-      CKS(bias_grad(G_, b.sc, tmp(i_ds), Mlo));
+      CKS(conv_wgrad(G_, b.x, tmp(i_ds), B, H, b.sc, b.sc.b));
       CKS(conv_dgrad(tmp(i_ds), B, H, b.sc, tmp(i_dxs), nullptr));
       // CBN2 backward: da2 -> dh1 (into cur's buffer)
       CKS(cbn_backward(b.h1, tmp(i_a2), B, H2, b.cout, b.mean2, b.rstd2, b.gain2, b.bias2, false, nullptr, cur,
                        b.ab2));
       // conv1 on the upsampled activation
-      CKS(conv_wgrad(G_, b.u1, cur, B, H2, b.c1));
-      CKS(bias_grad(G_, b.c1, cur, Mhi));
+      CKS(conv_wgrad(G_, b.u1, cur, B, H2, b.c1, b.c1.b));
       CKS(conv_dgrad(cur, B, H2, b.c1, tmp(i_a2), nullptr));
       // CBN1 backward through the upsample (2x2 sum), plus the skip gradient
       CKS(cbn_backward(b.x, tmp(i_a2), B, H, b.cin, b.mean1, b.rstd1, b.gain1, b.bias1, true, tmp(i_dxs), tmp(i_ds),

@@ -1166,19 +1166,23 @@ __global__ void __launch_bounds__(256) k_sn_pack(const SnPack* __restrict__ jobs
     if (blk_start[mid] <= b) lo = mid; else hi = mid - 1;
   }
   const SnPack J = jobs[lo];
-  const long long n = (long long)J.rows * J.taps * J.cin;
-  const long long i = (b - blk_start[lo]) * 256 + threadIdx.x;
+  const int n = J.rows * J.taps * J.cin;   // < 2^31 for every weight of the model
+  const int i = (int)(b - blk_start[lo]) * 256 + threadIdx.x;
   if (i >= n) return;
   const float v = J.w[i] * J.sigma[1];
-  const int c = (int)(i % J.cin);
-  const long long rt = i / J.cin;
-  const int t = (int)(rt % J.taps);
-  const int o = (int)(rt / J.taps);
   long long d;
-  if (J.mode == 1) {  // dgrad layout [cin][taps-1-t][rows]
-    d = ((long long)c * J.taps + (J.taps - 1 - t)) * J.dst_rows + (o + J.dst_row_offset);
+  if (J.mode == 0 && J.dst_cin == J.cin) {   // same layout: a scaled, converted copy
+    d = (long long)J.dst_row_offset * J.taps * J.cin + i;
   } else {
-    d = ((long long)(o + J.dst_row_offset) * J.taps + t) * J.dst_cin + c;
+    const int c = i % J.cin;
+    const int rt = i / J.cin;
+    const int t = rt % J.taps;
+    const int o = rt / J.taps;
+    if (J.mode == 1) {  // dgrad layout [cin][taps-1-t][rows]
+      d = ((long long)c * J.taps + (J.taps - 1 - t)) * J.dst_rows + (o + J.dst_row_offset);
+    } else {
+      d = ((long long)(o + J.dst_row_offset) * J.taps + t) * J.dst_cin + c;
+    }
   }
   if (J.dst_bf16) reinterpret_cast<bf16*>(J.dst)[d] = __float2bfloat16_rn(v);
   else reinterpret_cast<float*>(J.dst)[d] = v;

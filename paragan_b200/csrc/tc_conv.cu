@@ -56,10 +56,12 @@ struct WgradCfg {
   static constexpr int NB = (BN + 63) / 64;           // 64-wide MN atoms of B
   static constexpr uint32_t A_BYTES = 2 * kAtomBytes;  // M = 128 output channels
   static constexpr uint32_t B_BYTES = NB * kAtomBytes;
-  static constexpr int STAGES_RAW = (232448 - 2048) / (A_BYTES + B_BYTES);
+  static constexpr uint32_t ONES_BYTES = kAtomBytes;    // constant bf16 1.0 tile: bias-gradient B operand
+  static constexpr int STAGES_RAW = (232448 - 2048 - (int)ONES_BYTES) / (A_BYTES + B_BYTES);
   static constexpr int STAGES = STAGES_RAW > 6 ? 6 : STAGES_RAW;
-  static constexpr uint32_t TMEM_COLS = (BN <= 32) ? 32 : (BN <= 64) ? 64 : (BN <= 128) ? 128 : 256;
-  static constexpr size_t SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + 256;
+  // dW accumulator in columns [0, BN), bias sums in [BN, BN + 16) (read as one 32-column load)
+  static constexpr uint32_t TMEM_COLS = (BN + 32 <= 64) ? 64 : (BN + 32 <= 128) ? 128 : (BN + 32 <= 256) ? 256 : 512;
+  static constexpr size_t SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + ONES_BYTES + 256;
 };
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
@@ -140,8 +142,6 @@ __device__ __forceinline__ void epilogue_loop(const TcFpropArgs& a, const CUtens
     const int buf = it & 1;
     const int nt = tile % a.n_tiles;
     const int mt = CG == 2 ? (tile / a.n_tiles) * 2 + rank : tile / a.n_tiles;
-    tc::mbar_wait(&tfull[buf], (it >> 1) & 1);
-    tc::tc_fence_after();
     const long long m = (long long)mt * kTileM + row;
     const bool valid = m < a.M;
     long long rbase = 0;
@@ -156,6 +156,36 @@ __device__ __forceinline__ void epilogue_loop(const TcFpropArgs& a, const CUtens
         rbase = m * a.ldr;
       }
     }
+    // one bf16 side input per chunk (the ReLU mask reference, else the residual) is loaded one chunk
+    // ahead — the first before the accumulator wait — so its global latency overlaps the pipeline
+    const bf16* side = nullptr;
+    long long sbase = 0;
+    if (valid) {
+      if (a.relu_ref) {
+        side = reinterpret_cast<const bf16*>(a.relu_ref);
+        sbase = m * a.ldo;
+      } else if (a.residual) {
+        side = reinterpret_cast<const bf16*>(a.residual);
+        sbase = rbase;
+      }
+    }
+    auto load_side = [&](int cb, uint4 (&dst)[4]) {
+      const int col0 = nt * BN + cb;
+      if (side && cb >= 0 && col0 + 32 <= a.Cout) {
+        const uint4* p = reinterpret_cast<const uint4*>(side + sbase + col0);
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq) dst[qq] = p[qq];
+      }
+    };
+    auto next_cb = [&](int cb) {   // this thread's chunk after cb: within the 64-wide group, else the next group
+      const int g = cb & ~63;
+      if (cb + 32 < g + 64 && cb + 32 < BN) return cb + 32;
+      return g + 128 < BN ? g + 128 : -1;
+    };
+    uint4 scur[4] = {};
+    load_side(half * 64 < BN ? half * 64 : -1, scur);
+    tc::mbar_wait(&tfull[buf], (it >> 1) & 1);
+    tc::tc_fence_after();
 #pragma unroll 1
     for (int g = half * 64; g < BN; g += 128) {
       if (a.tma_store) {
@@ -166,6 +196,8 @@ __device__ __forceinline__ void epilogue_loop(const TcFpropArgs& a, const CUtens
       for (int cb = g; cb < g + 64 && cb < BN; cb += 32) {
         float v[32];
         tc::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + buf * BN + cb, v);
+        uint4 snext[4] = {};
+        load_side(next_cb(cb), snext);
         const int col0 = nt * BN + cb;
         if (valid && col0 + 32 <= a.Cout) {
           // ---- full 32-column chunk: straight-line, vectorised
@@ -174,11 +206,10 @@ __device__ __forceinline__ void epilogue_loop(const TcFpropArgs& a, const CUtens
             for (int j = 0; j < 32; ++j) v[j] *= alpha;
           }
           if (a.relu_ref) {
-            const uint4* rr = reinterpret_cast<const uint4*>(reinterpret_cast<const bf16*>(a.relu_ref) + m * a.ldo + col0);
 #pragma unroll
             for (int qq = 0; qq < 4; ++qq) {
               float r[8];
-              bf16x8_to_f32(rr[qq], r);
+              bf16x8_to_f32(scur[qq], r);
 #pragma unroll
               for (int j = 0; j < 8; ++j) v[qq * 8 + j] = r[j] > 0.0f ? v[qq * 8 + j] : 0.0f;
             }
@@ -204,7 +235,7 @@ __device__ __forceinline__ void epilogue_loop(const TcFpropArgs& a, const CUtens
 #pragma unroll
             for (int qq = 0; qq < 4; ++qq) {
               float r[8];
-              bf16x8_to_f32(rp[qq], r);
+              bf16x8_to_f32(a.relu_ref ? rp[qq] : scur[qq], r);
 #pragma unroll
               for (int j = 0; j < 8; ++j) v[qq * 8 + j] += r[j];
             }
@@ -253,6 +284,8 @@ __device__ __forceinline__ void epilogue_loop(const TcFpropArgs& a, const CUtens
             *reinterpret_cast<uint4*>(st + row * 128 + chunk * 16) = u;
           }
         }
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq) scur[qq] = snext[qq];
       }
       if (a.tma_store) {
         tc::fence_async_smem();
@@ -264,9 +297,14 @@ __device__ __forceinline__ void epilogue_loop(const TcFpropArgs& a, const CUtens
         }
       }
     }
+    // one arrival per warp (the barrier counts warps): every lane's tcgen05.ld has completed
+    // (wait::ld) and is ordered before lane 0's arrive by the fence + warp sync
     tc::tc_fence_before();
-    if (CG == 2) tc::mbar_arrive_cluster(tc::map_to_rank(&tempty[buf], 0));
-    else tc::mbar_arrive(&tempty[buf]);
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) {
+      if (CG == 2 && rank != 0) tc::mbar_arrive_cluster(tc::map_to_rank(&tempty[buf], 0));
+      else tc::mbar_arrive(&tempty[buf]);
+    }
   }
   if (a.tma_store && leader) tc::bulk_wait_all();
 }
@@ -302,7 +340,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&tfull[b], 1);
-      tc::mbar_init(&tempty[b], 32 * kEpiWarps);
+      tc::mbar_init(&tempty[b], kEpiWarps);
     }
     tc::fence_barrier_init();
   }
@@ -387,12 +425,22 @@ __global__ void __launch_bounds__(192, 1)
   uint8_t* smem = align1024(smem_raw);
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * C::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * C::B_BYTES);
+  uint8_t* sOnes = sB + STAGES * C::B_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sOnes + C::ONES_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // the CTAs of tap 0 / channel block 0 also sum dY over their pixels: db[o] = sum_p dY[p][o]
+  // (an extra N = 16 MMA per K step against a constant all-ones B tile)
+  const bool do_bias = a.bias_out != nullptr && (int)(blockIdx.x % (a.m_tiles * a.n_tiles)) % a.n_tiles == 0;
+  if (do_bias) {
+    uint4* o4 = reinterpret_cast<uint4*>(sOnes);
+    for (int i = threadIdx.x; i < (int)(C::ONES_BYTES / 16); i += blockDim.x)
+      o4[i] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
+    tc::fence_async_smem();
+  }
   if (warp == 0 && lane == 0) {
     tc::tma_prefetch(&tmDY);
     tc::tma_prefetch(&tmX);
@@ -459,6 +507,14 @@ __global__ void __launch_bounds__(192, 1)
           const uint64_t bd = tc::sdesc_sw128(b_base + k * 2048, kAtomBytes, 1024);
           tc::mma_bf16(tmem, ad, bd, idesc, (kb != kb0) || (k != 0));
         }
+        if (do_bias) {
+          constexpr uint32_t idb = tc::idesc_bf16(128, 16, true, true);
+          const uint32_t o_base = tc::smem_u32(sOnes);
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            tc::mma_bf16(tmem + BN, tc::sdesc_sw128(a_base + k * 2048, kAtomBytes, 1024),
+                         tc::sdesc_sw128(o_base + k * 2048, kAtomBytes, 1024), idb, (kb != kb0) || (k != 0));
+        }
         tc::mma_commit(&empty[stage]);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
@@ -470,6 +526,11 @@ __global__ void __launch_bounds__(192, 1)
     tc::mbar_wait(&tfull[0], 0);
     tc::tc_fence_after();
     const int o = o0 + row;
+    if (do_bias) {
+      float v[32];
+      tc::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + BN, v);
+      if (o < a.Cout) a.bias_out[(long long)split * a.Cout + o] = v[0];
+    }
 #pragma unroll 1
     for (int cbk = 0; cbk < BN; cbk += 32) {
       float v[32];
@@ -551,7 +612,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&tfull[b], 1);
-      tc::mbar_init(&tempty[b], 32 * kEpiWarps);
+      tc::mbar_init(&tempty[b], kEpiWarps);
     }
     tc::fence_barrier_init();
   }
@@ -691,7 +752,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&tfull[b], 1);
-      tc::mbar_init(&tempty[b], 2 * 32 * kEpiWarps);   // both CTAs' epilogue threads (leader's copy is used)
+      tc::mbar_init(&tempty[b], 2 * kEpiWarps);   // both CTAs' epilogue warps (leader's copy is used)
     }
     tc::fence_barrier_init();
   }
@@ -1082,7 +1143,8 @@ size_t tc_wgrad_workspace_floats(int N, int H, int W, int Cin, int Cout, int ksz
 }
 
 cudaError_t tc_conv_wgrad(const void* x, const void* dy, int N, int H, int W, int Cin, int Cout, int ksz,
-                          float* dw, int accumulate, float* scratch, size_t scratch_floats, cudaStream_t st) {
+                          float* dw, int accumulate, float* scratch, size_t scratch_floats, cudaStream_t st,
+                          float* dbias) {
   if (Cin % 8 || Cout % 8 || ((uintptr_t)x & 15) || ((uintptr_t)dy & 15) || !tileable(H, W))
     return cudaErrorInvalidValue;
   int bn;
@@ -1113,14 +1175,16 @@ cudaError_t tc_conv_wgrad(const void* x, const void* dy, int N, int H, int W, in
   if (splits > a.total_kb / 4) splits = a.total_kb / 4;
   if (splits < 1) splits = 1;
   const size_t out_floats = (size_t)Cout * a.taps * Cin;
+  const size_t bias_floats = dbias ? (size_t)Cout : 0;
   const bool direct = (splits == 1 && !accumulate);
   if (!direct) {
-    while (splits > 1 && (size_t)splits * out_floats > scratch_floats) --splits;
-    if ((size_t)splits * out_floats > scratch_floats) return cudaErrorMemoryAllocation;
+    while (splits > 1 && (size_t)splits * (out_floats + bias_floats) > scratch_floats) --splits;
+    if ((size_t)splits * (out_floats + bias_floats) > scratch_floats) return cudaErrorMemoryAllocation;
   }
   a.kb_per_split = ceil_div(a.total_kb, splits);
   a.splits = ceil_div(a.total_kb, a.kb_per_split);
   a.out = direct ? dw : scratch;
+  a.bias_out = dbias ? (direct ? dbias : scratch + (size_t)a.splits * out_floats) : nullptr;
   cudaError_t e;
   switch (bn) {
     case 32: e = launch_wgrad_bn<32>(mdy, mx, a, st); break;
@@ -1137,6 +1201,10 @@ cudaError_t tc_conv_wgrad(const void* x, const void* dy, int N, int H, int W, in
     if (blocks > 4 * kNumSMs) blocks = 4 * kNumSMs;
     k_split_reduce<<<blocks, 256, 0, st>>>(scratch, dw, n, a.splits, accumulate);
     PG_LAUNCH_CHECK();
+    if (dbias) {
+      k_split_reduce<<<ceil_div(Cout, 256), 256, 0, st>>>(a.bias_out, dbias, Cout, a.splits, 0);
+      PG_LAUNCH_CHECK();
+    }
   }
   return cudaSuccess;
 }

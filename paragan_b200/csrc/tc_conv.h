@@ -34,6 +34,7 @@ struct TcFpropArgs {
 struct TcWgradArgs {
   int H, W, ksz, taps, Cin, Cout, c_blocks, m_tiles, n_tiles, total_kb, kb_per_split, splits;
   float* out;   // [splits][Cout][taps][Cin] partials, or dW directly
+  float* bias_out;   // [splits][Cout] partial bias gradients (sum of dY over pixels), or db directly; may be null
 };
 
 // Y[N,H,W,Cout] = epilogue( conv(X[N,H,W,Cin] bf16, Wp[Cout][ksz*ksz][Cin] bf16) )
@@ -43,8 +44,10 @@ cudaError_t tc_conv_fprop(const void* x, int N, int H, int W, int Cin, const voi
 
 // dW[Cout][ksz*ksz][Cin] (+)= sum_p dY[p][o] X[p + tap][c]   (fp32; split-K with a
 // deterministic reduction through ``scratch``)
+// dbias (optional, fp32 [Cout]) = sum_p dY[p][o], computed by the same launch (written, not accumulated)
 cudaError_t tc_conv_wgrad(const void* x, const void* dy, int N, int H, int W, int Cin, int Cout, int ksz,
-                          float* dw, int accumulate, float* scratch, size_t scratch_floats, cudaStream_t st);
+                          float* dw, int accumulate, float* scratch, size_t scratch_floats, cudaStream_t st,
+                          float* dbias = nullptr);
 
 size_t tc_wgrad_workspace_floats(int N, int H, int W, int Cin, int Cout, int ksz);
 int tc_fprop_bn(int cout);

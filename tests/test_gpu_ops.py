@@ -119,10 +119,13 @@ def test_tc_conv_wgrad_integer_exact(shape):
     want = gw.permute(0, 2, 3, 1).reshape(cout, k * k, cin).numpy().astype(np.float32)
     assert np.abs(want).max() < 2 ** 24
     dw = torch.full((cout, k * k, cin), float("nan"), dtype=torch.float32, device=DEV)
-    api.op_conv_wgrad(api.BF16, _bf16_np(x).to(DEV), _bf16_np(dy).to(DEV), cout, k, dw)
+    db = torch.full((cout,), float("nan"), dtype=torch.float32, device=DEV)
+    api.op_conv_wgrad(api.BF16, _bf16_np(x).to(DEV), _bf16_np(dy).to(DEV), cout, k, dw, db=db)
     torch.cuda.synchronize()
     got = dw.cpu().numpy()
     assert np.array_equal(got, want), np.argwhere(got != want)[:5]
+    # the bias gradient from the same launch: sum of dy over every pixel (exact integers)
+    assert np.array_equal(db.cpu().numpy(), dy.reshape(-1, cout).sum(0).astype(np.float32))
 
 
 @pytest.mark.parametrize("shape", CONV_SHAPES[:4])
@@ -181,8 +184,10 @@ def test_thin_conv_f32_fwd_dgrad_wgrad(shape):
     dw = torch.empty((cout, k * k, cin), dtype=torch.float32, device=DEV)
     api.op_conv_fwd(api.F32, xd, wd, bd, cout, k, y)
     api.op_conv_dgrad(api.F32, dyd, wd, cin, k, dx)
-    api.op_conv_wgrad(api.F32, xd, dyd, cout, k, dw)
+    db = torch.empty((cout,), dtype=torch.float32, device=DEV)
+    api.op_conv_wgrad(api.F32, xd, dyd, cout, k, dw, db=db)
     torch.cuda.synchronize()
+    assert np.allclose(db.cpu().numpy(), dy.reshape(-1, cout).astype(np.float64).sum(0), rtol=1e-5, atol=1e-3)
     xt = torch.from_numpy(x).double().permute(0, 3, 1, 2).requires_grad_(True)
     wv = torch.from_numpy(wt).double().reshape(cout, k, k, cin).permute(0, 3, 1, 2).contiguous().requires_grad_(True)
     yt = ops.conv2d(xt, wv, torch.from_numpy(b).double())

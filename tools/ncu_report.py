@@ -15,6 +15,8 @@ METRICS = [
     ("sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed", "tensor pipe %"),
     ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "L2 %"),
     ("l1tex__throughput.avg.pct_of_peak_sustained_elapsed", "L1tex %"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", "smem LSU %"),
+    ("l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", "smem TC %"),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM %"),
     ("launch__registers_per_thread", "regs"),
 ]
@@ -34,6 +36,8 @@ def main():
         cells = []
         for m, _ in METRICS:
             i = idx.get(m)
+            if i is None:   # section-prefixed names (e.g. "TPC.TriageCompute.<metric>")
+                i = next((j for h, j in idx.items() if h.endswith("." + m)), None)
             cells.append(f"{r[i]} {units[i]}".strip() if i is not None else "-")
         print(f"| `{name}` | {r[idx.get('Grid Size', 0)]} | " + " | ".join(cells) + " |")
     stall = [h for h in hdr if h.startswith("smsp__pcsamp_warps_issue_stalled_") and not h.endswith("not_issued")]
