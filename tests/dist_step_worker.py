@@ -38,17 +38,52 @@ def main():
     same = all(torch.equal(hs[0], x) for x in hs)
     out = {"rank": rank, "replicas_identical": bool(same)}
     if rank == 0:
+        # the same global batch on ONE GPU: the data-parallel decomposition (R15) up to the
+        # reassociation of the cross-replica sums
+        scfg = api.make_config(resolution=32, ch=4, attn_res=16, n_classes=10, shared_dim=16, z_chunk=4,
+                               local_batch=B * world, compute=compute, device=local)
+        single = P.run_gpu(scfg, g0, d0, dbs, gb)
+        # gradients: reassociation only (1e-5 fp32); updated weights: Adam's first step is ~ -lr*sign(g), so
+        # elements whose gradient is ~0 (a bias feeding a BN) may flip sign: the oracle's state bar (1e-4)
+        dp_tol = {"d_grads": 1e-5, "g_grads": 1e-5, "d_state": 1e-4, "g_state": 1e-4}
+        if compute == api.BF16:
+            dp_tol = {k: 5e-3 for k in dp_tol}
+        out["vs_single"] = {k: P.rel(got[k], single[k]) for k in dp_tol}
+        out["vs_single_bad"] = [k for k, v in out["vs_single"].items() if not v < dp_tol[k]]
         want = P.run_oracle(ocfg, gs, ds, g0, d0, dbs, gb)
+        noise = {}
+        if compute == api.BF16:
+            # bf16 noise floor (as tests/test_gpu_step.py): the emulating oracle's own distance from fp64
+            import dataclasses
+            pcfg = dataclasses.replace(ocfg, bf16=False)
+            plain = P.run_oracle(pcfg, *P.make_inputs(pcfg, B * world, seed=31))
+            noise = {k: plain[k] for k in ("d_grads", "g_grads")}
         out["d_loss"] = abs(got["d_loss"] - want["d_loss"]) / max(abs(want["d_loss"]), 1e-3)
         out["g_loss"] = abs(got["g_loss"] - want["g_loss"]) / max(abs(want["g_loss"]), 1e-3)
-        # same bars as the single-GPU micro tests: fp32 per tensor 1e-4; bf16 global 2e-2, per tensor 6e-2
-        ttol = tol if compute == api.F32 else 6e-2
+        # fp32: per tensor and global 1e-4.  bf16: per tensor and global max(2e-2, 1.5 x the bf16 noise
+        # floor |emulating oracle - fp64 oracle|), tensors >= 16 elements that are not ~0
         for key, specs in (("d_grads", ds), ("g_grads", gs)):
-            bad, worst = P.compare_tensors(specs, got[key], want[key], ttol)
-            out[key + "_bad"] = [b[0] for b in bad]
-            out[key + "_worst"] = max(worst.values())
             out[key + "_global"] = P.rel(got[key], want[key])
-            if out[key + "_global"] > tol:
+            if compute == api.F32:
+                bad, worst = P.compare_tensors(specs, got[key], want[key], tol)
+                out[key + "_bad"] = [b[0] for b in bad]
+                out[key + "_worst"] = max(worst.values())
+                gbar = tol
+            else:
+                bad, o, worst = [], 0, 0.0
+                for sp in specs:
+                    n = int(np.prod(sp.shape))
+                    e = P.rel(got[key][o:o + n], want[key][o:o + n])
+                    e_bf = P.rel(want[key][o:o + n], noise[key][o:o + n])
+                    if n >= 16 and np.linalg.norm(want[key][o:o + n]) > 1e-6 * np.linalg.norm(want[key]):
+                        worst = max(worst, e / max(tol, 1.5 * e_bf))
+                        if e > max(tol, 1.5 * e_bf):
+                            bad.append(sp.name)
+                    o += n
+                out[key + "_bad"] = bad
+                out[key + "_worst"] = worst   # error / bar (<= 1 passes)
+                gbar = max(tol, 1.5 * P.rel(want[key], noise[key]))
+            if out[key + "_global"] > gbar:
                 out[key + "_bad"].append("GLOBAL")
         g_rel = 1e-4 if compute == api.F32 else 2e-2
         from oracle import biggan as bg

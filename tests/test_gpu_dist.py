@@ -1,6 +1,6 @@
 """Multi-GPU parity (needs >= 2 GPUs in one box): 2 ranks x B images with
 cross-replica BN and the NCCL gradient all-reduce equal the oracle on the 2B global
-batch; replicas stay bit-identical."""
+batch and the same 2B batch on one GPU; replicas stay bit-identical."""
 import json
 import os
 import socket
@@ -39,3 +39,5 @@ def test_two_gpu_step_parity(compute):
     assert r0["d_loss"] < r0["tol"] and r0["g_loss"] < r0["tol"]
     for k in ("d_grads", "g_grads", "d_state", "g_state"):
         assert not r0[k + "_bad"], (k, r0[k + "_bad"][:5])
+    # 2 ranks x B == 1 rank x 2B (the data-parallel decomposition on the GPU itself)
+    assert not r0["vs_single_bad"], r0["vs_single"]
