@@ -271,7 +271,7 @@ def main():
             for i in range(args.steps):
                 step(i)
             ctx.profile(False)
-            for kind in (0, 1):
+            for kind in (0, 1, 2):
                 prof[kind] = ctx.profile_read(kind)
             barrier()
 
@@ -291,6 +291,11 @@ def main():
                     "share_of_step": (t0 / args.steps) / (ms_max / args.steps),
                     "wgrad": {"achieved": (f1_ / (t1 / 1000.0)) / 1e12 if t1 > 0 else 0.0, "launches": n1,
                               "ms_per_step": t1 / args.steps}}
+            if world > 1:
+                n2, t2, b2 = prof[2]
+                roof["collectives"] = {"launches_per_step": n2 / args.steps, "ms_per_step": t2 / args.steps,
+                                       "bytes_per_step": b2 / args.steps,
+                                       "note": "NCCL all-reduces on the compute stream (rank 0), device time"}
         cpu = None
         if not args.no_cpu_baseline and world == 1:
             v, dt, cores = cpu_oracle_sample()

@@ -175,9 +175,10 @@ paragan_status paragan_kernel_launches(const paragan_ctx* ctx, uint64_t* n);
 /* Live kernel timing for the roofline report: while enabled, every tcgen05
  * convolution launch of the step is bracketed by CUDA events on the context's
  * stream.  profile_read (synchronises) returns, for kind 0 = implicit-GEMM
- * fprop/dgrad kernel, 1 = wgrad (incl. its split-K reduction), the number of
- * launches, their summed device time (ms) and their ALGORITHMIC flops
- * (2*M*N*K with unpadded channel counts).  enable=1 also clears the record. */
+ * fprop/dgrad kernel, 1 = wgrad (incl. its split-K reduction), 2 = NCCL collectives
+ * (gradient, cross-replica BN and loss all-reduces), the number of launches, their
+ * summed device time (ms) and their ALGORITHMIC flops (2*M*N*K with unpadded channel
+ * counts; for kind 2: bytes reduced).  enable=1 also clears the record. */
 paragan_status paragan_profile(paragan_ctx* ctx, int32_t enable);
 paragan_status paragan_profile_read(paragan_ctx* ctx, int32_t kind, uint64_t* launches, double* ms, double* flops);
 

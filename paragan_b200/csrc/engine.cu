@@ -386,8 +386,7 @@ class Engine final : public EngineBase {
     if (!ready_ || poisoned_) return PARAGAN_ERR_ORDER;
     Net& N = net == PARAGAN_NET_D ? D_ : G_;
     if (cfg_.world_size > 1) {
-      ncclResult_t r = ncclAllReduce(N.g, N.g, (size_t)N.n, ncclFloat32, ncclSum, comm_, st_);
-      if (r != ncclSuccess) return fail_msg(PARAGAN_ERR_NCCL, std::string("allreduce: ") + ncclGetErrorString(r));
+      CKS(nccl_sum(N.g, (size_t)N.n, ncclFloat32, "grad allreduce"));
       CK(scale_f32(N.g, N.n, 1.0f / cfg_.world_size, st_));   // mean over ranks (R15)
       ++launches_;
     }
@@ -1219,25 +1218,36 @@ class Engine final : public EngineBase {
     CK(bn_stats<T>(static_cast<const T*>(x), M, C, dpart_, kMaxPartialBlocks, sums, st_));
     ++launches_;
     if (cfg_.world_size > 1) {
-      ncclResult_t r = ncclAllReduce(sums, sums, 2 * C, ncclFloat64, ncclSum, comm_, st_);
-      if (r != ncclSuccess) return fail_msg(PARAGAN_ERR_NCCL, std::string("bn allreduce: ") + ncclGetErrorString(r));
+      CKS(nccl_sum(sums, (size_t)2 * C, ncclFloat64, "bn allreduce"));
     }
     CK(bn_finalize(sums, C, (double)M * cfg_.world_size, cfg_.bn_eps, mean, rstd, st_));
     return PARAGAN_OK;
   }
   // losses / logit means are local means: sum over ranks here, / world_size in sync_stats (R15);
   // the non-finite flag (loss[3]) becomes the number of ranks that saw one
+  // in-place sum over ranks on the compute stream; timed as profile kind 2 (collectives)
+  paragan_status nccl_sum(void* buf, size_t count, ncclDataType_t dt, const char* what) {
+    ncclResult_t r = ncclSuccess;
+    const size_t bytes = count * (dt == ncclFloat64 ? 8 : 4);
+    char label[48];
+    std::snprintf(label, sizeof(label), "%s %zu B", what, bytes);
+    cudaError_t e = timed(2, (double)bytes, [&] {
+      r = ncclAllReduce(buf, buf, count, dt, ncclSum, comm_, st_);
+      return r == ncclSuccess ? cudaSuccess : cudaErrorUnknown;
+    }, label);
+    if (r != ncclSuccess) return fail_msg(PARAGAN_ERR_NCCL, std::string(what) + ": " + ncclGetErrorString(r));
+    CK(e);
+    return PARAGAN_OK;
+  }
   paragan_status allreduce_loss(float* loss4) {
     if (cfg_.world_size > 1) {
-      ncclResult_t r = ncclAllReduce(loss4, loss4, 4, ncclFloat32, ncclSum, comm_, st_);
-      if (r != ncclSuccess) return fail_msg(PARAGAN_ERR_NCCL, std::string("loss allreduce: ") + ncclGetErrorString(r));
+      CKS(nccl_sum(loss4, 4, ncclFloat32, "loss allreduce"));
     }
     return PARAGAN_OK;
   }
   paragan_status allreduce_small(double* p, int n) {
     if (cfg_.world_size > 1) {
-      ncclResult_t r = ncclAllReduce(p, p, n, ncclFloat64, ncclSum, comm_, st_);
-      if (r != ncclSuccess) return fail_msg(PARAGAN_ERR_NCCL, std::string("allreduce: ") + ncclGetErrorString(r));
+      CKS(nccl_sum(p, (size_t)n, ncclFloat64, "allreduce"));
     }
     return PARAGAN_OK;
   }
