@@ -203,6 +203,23 @@ paragan_status paragan_op_conv_fwd(paragan_dtype dt, const void* x, int32_t n, i
 paragan_status paragan_op_conv_wgrad(paragan_dtype dt, const void* x, const void* dy, int32_t n, int32_t h,
                                      int32_t w, int32_t cin, int32_t cout, int32_t ksz, float* dw, float* db,
                                      void* stream);
+/* y[N,2H,2W,Cout] = conv3x3(up2_nearest(x[N,H,W,Cin])) + bias — G's conv1 (SURVEY §8(f) NEXT-1,
+ * sub-pixel phase decomposition): BF16 only; w fp32 [Cout][9][Cin] (OHWI), folded on the device into
+ * four 2x2 phase kernels (rounded to bf16 after the fold), x / y bf16 NHWC, Cin and Cout % 8 == 0. */
+paragan_status paragan_op_conv_up2_fwd(const void* x, int32_t n, int32_t h, int32_t w, int32_t cin, const float* wgt,
+                                       const float* bias, int32_t cout, void* y, void* stream);
+
+/* dx[N,H,W,Cin] = the input gradient of conv3x3(up2_nearest(x)) at LOW resolution from dy[N,2H,2W,Cout]
+ * (the up2 adjoint included), through the same phase decomposition; BF16; w fp32 [Cout][9][Cin]. */
+paragan_status paragan_op_conv_up2_dgrad(const void* dy, int32_t n, int32_t h, int32_t w, int32_t cout,
+                                         const float* wgt, int32_t cin, void* dx, void* stream);
+
+/* dw[Cout][9][Cin] (fp32) = weight gradient of conv3x3(up2_nearest(x)) from the LOW-resolution
+ * x[N,H,W,Cin] and dy[N,2H,2W,Cout] through the phase decomposition (16 folded taps, unfolded onto the
+ * 3x3 taps); db[Cout] (optional) = sum of dy.  BF16. */
+paragan_status paragan_op_conv_up2_wgrad(const void* x, const void* dy, int32_t n, int32_t h, int32_t w, int32_t cin,
+                                         int32_t cout, float* dw, float* db, void* stream);
+
 /* dx[N,H,W,Cin] = sum_{o,tap} dy[p - delta_tap][o] w[o][tap][c]: the input gradient of the 3x3 conv.
  * F32 only, Cout = 3 (G's fp32 output layer), Cin % 4 == 0; dx 16-byte aligned. */
 paragan_status paragan_op_conv_dgrad(paragan_dtype dt, const void* dy, int32_t n, int32_t h, int32_t w, int32_t cout,

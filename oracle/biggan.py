@@ -72,6 +72,7 @@ class Config:
     sn_eps: float = 1e-12
     d_steps_per_g: int = 1
     bf16: bool = False           # emulate the bf16 storage points of R14
+    subpixel: bool = True         # with bf16: G's conv1 through the phase decomposition (R24)
     adam_d: AdamHP = field(default_factory=lambda: AdamHP(2e-4, 0.0, 0.999, 1e-8))
     adam_g: AdamHP = field(default_factory=lambda: AdamHP(5e-5, 0.0, 0.999, 1e-8))
 
@@ -259,8 +260,13 @@ def g_forward(cfg: Config, sn: _SN, z: torch.Tensor, y: torch.Tensor) -> torch.T
         b1 = cond @ sn.w(pre + "cbn1.bias").t()
         x = h
         a = qv(torch.relu(ops.cbn(x, g1, b1, cfg.bn_eps)), bf)
-        a = qg(ops.up2(a), bf)                       # the conv input's gradient is stored at full resolution
-        a = q(ops.conv2d(a, _qw(sn, pre + "conv1.w"), p[pre + "conv1.b"]), bf)
+        if bf and cfg.subpixel:
+            # R24: conv3x3(up2(a)) as four phase 2x2 convs of the low-resolution a with the folded kernel
+            # stored bf16; the conv input's gradient is stored at low resolution (up2 adjoint included)
+            a = q(ops.up2_conv3x3_phases(qg(a, bf), sn.w(pre + "conv1.w"), p[pre + "conv1.b"], bf), bf)
+        else:
+            a = qg(ops.up2(a), bf)                   # the conv input's gradient is stored at full resolution
+            a = q(ops.conv2d(a, _qw(sn, pre + "conv1.w"), p[pre + "conv1.b"]), bf)
         g2 = cond @ sn.w(pre + "cbn2.gain").t()
         b2 = cond @ sn.w(pre + "cbn2.bias").t()
         a = q(torch.relu(ops.cbn(a, g2, b2, cfg.bn_eps)), bf)

@@ -142,6 +142,33 @@ def up2(x: torch.Tensor) -> torch.Tensor:
     return x.repeat_interleave(2, dim=2).repeat_interleave(2, dim=3)
 
 
+def up2_conv3x3_phases(x: torch.Tensor, w: torch.Tensor, b: torch.Tensor | None, bf16: bool) -> torch.Tensor:
+    """conv3x3(up2(x)) written as four 2x2 convs of the low-resolution x, one per output phase (a, b)
+    (reading R24).  Output row 2i+a reads input rows i-1+a+p, p in {0, 1}, with the
+    folded kernel Wf_ab[p][q] = sum_{r in R(a,p), s in R(b,q)} W[r][s], R(0,0)={0}, R(0,1)={1,2},
+    R(1,0)={0,1}, R(1,1)={2}.  Identical to conv2d(up2(x), w, b) in exact arithmetic (pinned in
+    tests/test_oracle_primitives.py).  With ``bf16`` the folded kernel is the stored bf16 operand
+    (straight-through: the gradient w.r.t. w is the exact unfold)."""
+    rows = {(0, 0): (0,), (0, 1): (1, 2), (1, 0): (0, 1), (1, 1): (2,)}
+    phases = []
+    for a in (0, 1):
+        row = []
+        for bb in (0, 1):
+            taps = []
+            for p in (0, 1):
+                for q_ in (0, 1):
+                    taps.append(sum(w[:, :, r, sc] for r in rows[(a, p)] for sc in rows[(bb, q_)]))
+            wf = torch.stack(taps, dim=-1).reshape(w.shape[0], w.shape[1], 2, 2)
+            if bf16:
+                wf = bf16_round(wf.detach()) + (wf - wf.detach())
+            xp = F.pad(x, (1 - bb, bb, 1 - a, a))      # (left, right, top, bottom)
+            row.append(F.conv2d(xp, wf, b))
+        phases.append(torch.stack(row, dim=-1))          # [N, C, H, W, 2(b)]
+    y = torch.stack(phases, dim=3)                       # [N, C, H, 2(a), W, 2(b)]
+    n, c, h, _, w_, _ = y.shape
+    return y.reshape(n, c, 2 * h, 2 * w_)
+
+
 def avgpool2(x: torch.Tensor) -> torch.Tensor:
     """2x2 average pool, stride 2."""
     n, c, h, w = x.shape

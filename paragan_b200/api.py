@@ -75,6 +75,12 @@ SYMBOLS = {
                                       C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
     "paragan_op_conv_wgrad": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                         C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "paragan_op_conv_up2_fwd": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
+                                          C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
+    "paragan_op_conv_up2_dgrad": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
+                                            C.c_int32, C.c_void_p, C.c_void_p]),
+    "paragan_op_conv_up2_wgrad": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                            C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
     "paragan_op_conv_dgrad": (C.c_int, [C.c_int, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
                                         C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
     "paragan_op_attn_fwd": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
@@ -176,6 +182,27 @@ def op_conv_wgrad(dtype, x, dy, cout, ksz, dw, stream=None, db=None):
     n, h, w, cin = x.shape
     _check("paragan_op_conv_wgrad", lib().paragan_op_conv_wgrad(dtype, _ptr(x), _ptr(dy), n, h, w, cin, cout, ksz,
                                                                 _ptr(dw), _ptr(db), _stream(stream)))
+
+
+def op_conv_up2_fwd(x, wgt, bias, cout, y, stream=None):
+    """y [n,2h,2w,cout] = conv3x3(up2(x)) + bias; x bf16 [n,h,w,cin], wgt fp32 [cout,9,cin]."""
+    n, h, w, cin = x.shape
+    _check("paragan_op_conv_up2_fwd", lib().paragan_op_conv_up2_fwd(_ptr(x), n, h, w, cin, _ptr(wgt), _ptr(bias), cout,
+                                                                    _ptr(y), _stream(stream)))
+
+
+def op_conv_up2_dgrad(dy, wgt, cin, dx, stream=None):
+    """dx [n,h,w,cin] (low resolution) = d/dx of conv3x3(up2(x)) given dy [n,2h,2w,cout]."""
+    n, h2, w2, cout = dy.shape
+    _check("paragan_op_conv_up2_dgrad", lib().paragan_op_conv_up2_dgrad(_ptr(dy), n, h2 // 2, w2 // 2, cout, _ptr(wgt),
+                                                                        cin, _ptr(dx), _stream(stream)))
+
+
+def op_conv_up2_wgrad(x, dy, cout, dw, db=None, stream=None):
+    """dw [cout,9,cin] (+ db) of conv3x3(up2(x)); x bf16 [n,h,w,cin] low resolution, dy [n,2h,2w,cout]."""
+    n, h, w, cin = x.shape
+    _check("paragan_op_conv_up2_wgrad", lib().paragan_op_conv_up2_wgrad(_ptr(x), _ptr(dy), n, h, w, cin, cout,
+                                                                        _ptr(dw), _ptr(db), _stream(stream)))
 
 
 def op_conv_dgrad(dtype, dy, wgt, cin, ksz, dx, stream=None):

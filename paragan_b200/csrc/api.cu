@@ -232,6 +232,60 @@ paragan_status paragan_op_conv_wgrad(paragan_dtype dt, const void* x, const void
   return cuda_status(e);
 }
 
+paragan_status paragan_op_conv_up2_fwd(const void* x, int32_t n, int32_t h, int32_t w, int32_t cin, const float* wgt,
+                                       const float* bias, int32_t cout, void* y, void* stream) {
+  if (!x || !wgt || !y || n < 1 || h < 1 || w < 1 || cin % 8 || cout % 8 || cin < 8 || cout < 8 || !aligned16(x) ||
+      !aligned16(y) || !tc_geometry_ok(h, w))
+    return PARAGAN_ERR_INVALID_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  char* buf = nullptr;
+  const size_t wbytes = (size_t)16 * cout * cin * 2;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&buf), wbytes + 256, st) != cudaSuccess) return PARAGAN_ERR_CUDA;
+  float* one = reinterpret_cast<float*>(buf + wbytes);
+  cudaError_t e = fill_const(one, 1, 1.0f, st);
+  if (e == cudaSuccess) e = fold_up2_weights(wgt, one, cout, cin, reinterpret_cast<bf16*>(buf), st);
+  TcEpilogue ep;
+  ep.bias = bias;
+  ep.out = y;
+  if (e == cudaSuccess) e = tc_conv_fprop_up2(x, n, h, w, cin, buf, cout, ep, st);
+  cudaFreeAsync(buf, st);
+  return cuda_status(e);
+}
+
+paragan_status paragan_op_conv_up2_dgrad(const void* dy, int32_t n, int32_t h, int32_t w, int32_t cout,
+                                         const float* wgt, int32_t cin, void* dx, void* stream) {
+  if (!dy || !wgt || !dx || n < 1 || h < 1 || w < 1 || cin % 8 || cout % 8 || cin < 8 || cout < 8 || !aligned16(dy) ||
+      !aligned16(dx) || !tc_geometry_ok(h, w))
+    return PARAGAN_ERR_INVALID_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  char* buf = nullptr;
+  const size_t wbytes = (size_t)16 * cout * cin * 2;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&buf), wbytes + 256, st) != cudaSuccess) return PARAGAN_ERR_CUDA;
+  float* one = reinterpret_cast<float*>(buf + wbytes);
+  cudaError_t e = fill_const(one, 1, 1.0f, st);
+  if (e == cudaSuccess) e = fold_up2_weights(wgt, one, cout, cin, reinterpret_cast<bf16*>(buf), st, 1);
+  TcEpilogue ep;
+  ep.out = dx;
+  if (e == cudaSuccess) e = tc_conv_dgrad_up2(dy, n, h, w, cout, buf, cin, ep, st);
+  cudaFreeAsync(buf, st);
+  return cuda_status(e);
+}
+
+paragan_status paragan_op_conv_up2_wgrad(const void* x, const void* dy, int32_t n, int32_t h, int32_t w, int32_t cin,
+                                         int32_t cout, float* dw, float* db, void* stream) {
+  if (!x || !dy || !dw || n < 1 || h < 1 || w < 1 || cin % 8 || cout % 8 || cin < 8 || cout < 8 || !aligned16(x) ||
+      !aligned16(dy) || !tc_geometry_ok(h, w))
+    return PARAGAN_ERR_INVALID_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t scratch_n = (size_t)64 * (16 * (size_t)cout * cin + 4 * (size_t)cout);
+  float* scratch = nullptr;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&scratch), scratch_n * sizeof(float), st) != cudaSuccess)
+    return PARAGAN_ERR_CUDA;
+  cudaError_t e = tc_conv_wgrad_up2(x, dy, n, h, w, cin, cout, dw, scratch, scratch_n, st, db);
+  cudaFreeAsync(scratch, st);
+  return cuda_status(e);
+}
+
 paragan_status paragan_op_conv_dgrad(paragan_dtype dt, const void* dy, int32_t n, int32_t h, int32_t w, int32_t cout,
                                      const void* wgt, int32_t cin, int32_t ksz, void* dx, void* stream) {
   if (dt != PARAGAN_F32 || !dy || !wgt || !dx || n < 1 || h < 1 || w < 1 || cout != 3 || ksz != 3 || cin % 4 ||

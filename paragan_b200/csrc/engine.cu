@@ -99,6 +99,8 @@ struct ConvL {
   int cin = 0, cin_x = 0, cout = 0, ksz = 3;
   void* wp = nullptr;              // fprop operand [cout][taps][cin_x]
   void* wt = nullptr;              // dgrad operand [cin_x][taps][cout]
+  void* wp4 = nullptr;             // sub-pixel fprop operand [4 phases][cout][4 taps][cin] (G conv1, BF16)
+  void* wt4 = nullptr;             // sub-pixel dgrad operand [cin][4 phases x 4 taps][cout]
   bool f32 = false;                // SIMT fp32 layer (G output conv)
 };
 struct LinL {
@@ -127,6 +129,7 @@ struct GBlock {
   bool attn = false;
   // activations (batch B)
   void *x, *u1, *h1, *a2, *s, *out;
+  void* u1lo = nullptr;            // CBN1-ReLU output before the upsample (sub-pixel conv1 input)
   float *gain1, *bias1, *gain2, *bias2, *cond, *dcond;
   float *ab1 = nullptr, *ab2 = nullptr;   // CBN backward per-sample [dbias | dgain] rows [B][2C]
   float *mean1, *rstd1, *mean2, *rstd2;
@@ -208,7 +211,10 @@ class Engine final : public EngineBase {
   static constexpr bool kBF = std::is_same<T, bf16>::value;
 
  public:
-  Engine(const paragan_config& c, cudaStream_t st) : cfg_(c), st_(st) {}
+  Engine(const paragan_config& c, cudaStream_t st) : cfg_(c), st_(st) {
+    const char* sp = std::getenv("PARAGAN_SUBPIXEL");
+    subpix_ = kBF && (sp == nullptr || std::atoi(sp) != 0);
+  }
   ~Engine() override {
     if (comm_) ncclCommDestroy(comm_);
     if (cublas_) cublasDestroy(cublas_);
@@ -336,6 +342,7 @@ class Engine final : public EngineBase {
     if (!real || !real_y || !z || !fake_y || ((uintptr_t)real & 15)) return fail_arg("d_step: bad pointer");
     // SN(G) + G forward (no grad) writes fakes into D-input rows [0, B)
     CKS(sn_forward(G_, false));
+    CKS(fold_subpixel());
     CKS(g_forward(z, fake_y, false));
     // reals into rows [B, 2B) (one D pass over the concatenated batch)
     const size_t img_bytes = (size_t)B_ * R_ * R_ * cpad_ * sizeof(T);
@@ -365,6 +372,7 @@ class Engine final : public EngineBase {
     }
     if (!z || !y) return fail_arg("g_step: bad pointer");
     CKS(sn_forward(G_, true));
+    CKS(fold_subpixel());
     CKS(g_forward(z, y, true));
     CK(cudaMemcpyAsync(ylab_, y, sizeof(int32_t) * B_, cudaMemcpyDeviceToDevice, st_));
     CKS(sn_forward(D_, true));
@@ -667,6 +675,10 @@ class Engine final : public EngineBase {
     for (auto& b : gb_) {
       alloc_lin(b.g1); alloc_lin(b.b1); alloc_lin(b.g2); alloc_lin(b.b2);
       alloc_conv(b.c1); alloc_conv(b.c2); alloc_conv(b.sc);
+      if (kBF && subpix_) {
+        b.c1.wp4 = A.get<char>((size_t)16 * b.c1.cout * b.c1.cin * 2);
+        b.c1.wt4 = A.get<char>((size_t)16 * b.c1.cout * b.c1.cin * 2);
+      }
     }
     alloc_conv(oconv_);
     for (auto& b : db_) {
@@ -698,7 +710,8 @@ class Engine final : public EngineBase {
     for (auto& b : gb_) {
       const int H = b.hin;
       b.x = (&b == &gb_[0]) ? act(B, H, H, b.cin) : nullptr;   // later blocks read the previous output in place
-      b.u1 = act(B, 2 * H, 2 * H, b.cin);
+      b.u1 = (kBF && subpix_) ? nullptr : act(B, 2 * H, 2 * H, b.cin);
+      b.u1lo = (kBF && subpix_) ? act(B, H, H, b.cin) : nullptr;
       b.h1 = act(B, 2 * H, 2 * H, b.cout);
       b.a2 = act(B, 2 * H, 2 * H, b.cout);
       b.s = act(B, H, H, b.cout);
@@ -1088,6 +1101,19 @@ class Engine final : public EngineBase {
     if (need_dgrad) CK(sn_pack_t(N.pb_d, N.pb_start, (int)N.pb_h.size(), N.pb_blocks, st_));
     return PARAGAN_OK;
   }
+  // W/sigma of every G conv1 folded into the four phase kernels of the sub-pixel conv
+  paragan_status fold_subpixel() {
+    if (!subpix_) return PARAGAN_OK;
+    for (GBlock& b : gb_) {
+      const PEntry& e = G_.E[b.c1.w];
+      CK(fold_up2_weights(G_.p + e.off, G_.sigma + 2 * e.job + 1, b.c1.cout, b.c1.cin,
+                          static_cast<bf16*>(b.c1.wp4), st_, 0));
+      CK(fold_up2_weights(G_.p + e.off, G_.sigma + 2 * e.job + 1, b.c1.cout, b.c1.cin,
+                          static_cast<bf16*>(b.c1.wt4), st_, 1));
+      launches_ += 2;
+    }
+    return PARAGAN_OK;
+  }
   paragan_status sn_backward_net(Net& N) {
     CK(sn_backward(N.jobs_d, (int)N.sn_entries.size(), N.snb_start, N.snb_blocks, N.sn_dotp, st_));
     launches_ += 2;
@@ -1145,6 +1171,48 @@ class Engine final : public EngineBase {
                                            static_cast<const float*>(c.wp), c.cout, c.ksz, bias, alpha,
                                            static_cast<const float*>(res), res_mode, static_cast<float*>(y), st_)));
     return PARAGAN_OK;
+  }
+  // y[n,2H,2H,cout] = conv3x3(up2(x[n,H,H,cin])) + bias via the phase decomposition (BF16 only)
+  paragan_status conv_fwd_up2(const void* x, int n, int H, const ConvL& c, void* y, const float* bias) {
+    if constexpr (kBF) {
+      TcEpilogue e;
+      e.bias = bias;
+      e.out = y;
+      // executed tensor work: 4 phases x 4 taps per low-resolution pixel (the 9-tap conv on the
+      // upsampled tensor would be 2.25x this)
+      const double fl = 2.0 * n * H * H * 16.0 * c.cout * c.cin;
+      char what[48];
+      std::snprintf(what, sizeof(what), "fprop-up2 n%d %dx%d %d->%d", n, H, H, c.cin, c.cout);
+      CK(timed(0, fl, [&] { return tc_conv_fprop_up2(x, n, H, H, c.cin, c.wp4, c.cout, e, st_); }, what));
+      return PARAGAN_OK;
+    }
+    return fail_msg(PARAGAN_ERR_CONFIG, "sub-pixel conv needs the BF16 engine");
+  }
+  // conv3x3(up2(x)) backward through the phase decomposition (BF16 only): dW + db into the grad slots
+  paragan_status conv_wgrad_up2(const void* x_lo, const void* dy, int n, int H, const ConvL& c) {
+    if constexpr (kBF) {
+      const double fl = 2.0 * n * H * H * 16.0 * c.cout * c.cin;
+      char what[48];
+      std::snprintf(what, sizeof(what), "wgrad-up2 n%d %dx%d %d->%d", n, H, H, c.cin, c.cout);
+      float* db = c.b >= 0 ? G_.G(c.b) : nullptr;
+      CK(timed(1, fl, [&] {
+        return tc_conv_wgrad_up2(x_lo, dy, n, H, H, c.cin, c.cout, G_.G(c.w), scratch_f_, scratch_floats_, st_, db);
+      }, what));
+      return PARAGAN_OK;
+    }
+    return fail_msg(PARAGAN_ERR_CONFIG, "sub-pixel conv needs the BF16 engine");
+  }
+  paragan_status conv_dgrad_up2(const void* dy, int n, int H, const ConvL& c, void* dx_lo) {
+    if constexpr (kBF) {
+      TcEpilogue e;
+      e.out = dx_lo;
+      const double fl = 2.0 * n * H * H * 16.0 * c.cout * c.cin;
+      char what[48];
+      std::snprintf(what, sizeof(what), "dgrad-up2 n%d %dx%d %d->%d", n, H, H, c.cout, c.cin);
+      CK(timed(0, fl, [&] { return tc_conv_dgrad_up2(dy, n, H, H, c.cout, c.wt4, c.cin, e, st_); }, what));
+      return PARAGAN_OK;
+    }
+    return fail_msg(PARAGAN_ERR_CONFIG, "sub-pixel conv needs the BF16 engine");
   }
   // dx[n,H,H,cin_x] = alpha * dgrad(dy) (+ add)
   paragan_status conv_dgrad(const void* dy, int n, int H, const ConvL& c, void* dx, const void* add,
@@ -1274,9 +1342,17 @@ class Engine final : public EngineBase {
       const int H = b.hin, H2 = 2 * H;
       // CBN1 -> ReLU -> up x2 (fused)
       CKS(bn_forward_stats(b.x, (long long)B * H * H, b.cin, b.sums1, b.mean1, b.rstd1));
-      CK((bn_apply_relu<T, T>(static_cast<const T*>(b.x), B, H, H, b.cin, b.mean1, b.rstd1, b.gain1, b.bias1, nullptr,
-                              nullptr, static_cast<T*>(b.u1), true, st_)));
-      CKS(conv_fwd(b.u1, B, H2, b.c1, b.h1, G_.P(b.c1.b), nullptr, 0));
+      if (subpix_) {
+        // conv3x3(up2(u)) as four 2x2 phase convs of the low-resolution u (2.25x fewer MACs); the
+        // upsampled tensor is materialised only when G's backward (conv1 wgrad) will read it
+        CK((bn_apply_relu<T, T>(static_cast<const T*>(b.x), B, H, H, b.cin, b.mean1, b.rstd1, b.gain1, b.bias1,
+                                nullptr, nullptr, static_cast<T*>(b.u1lo), false, st_)));
+        CKS(conv_fwd_up2(b.u1lo, B, H, b.c1, b.h1, G_.P(b.c1.b)));
+      } else {
+        CK((bn_apply_relu<T, T>(static_cast<const T*>(b.x), B, H, H, b.cin, b.mean1, b.rstd1, b.gain1, b.bias1,
+                                nullptr, nullptr, static_cast<T*>(b.u1), true, st_)));
+        CKS(conv_fwd(b.u1, B, H2, b.c1, b.h1, G_.P(b.c1.b), nullptr, 0));
+      }
       CKS(bn_forward_stats(b.h1, (long long)B * H2 * H2, b.cout, b.sums2, b.mean2, b.rstd2));
       CK((bn_apply_relu<T, T>(static_cast<const T*>(b.h1), B, H2, H2, b.cout, b.mean2, b.rstd2, b.gain2, b.bias2,
                               nullptr, nullptr, static_cast<T*>(b.a2), false, st_)));
@@ -1627,12 +1703,21 @@ class Engine final : public EngineBase {
       // CBN2 backward: da2 -> dh1 (into cur's buffer)
       CKS(cbn_backward(b.h1, tmp(i_a2), B, H2, b.cout, b.mean2, b.rstd2, b.gain2, b.bias2, false, nullptr, cur,
                        b.ab2));
-      // conv1 on the upsampled activation
-      CKS(conv_wgrad(G_, b.u1, cur, B, H2, b.c1, b.c1.b));
-      CKS(conv_dgrad(cur, B, H2, b.c1, tmp(i_a2), nullptr));
-      // CBN1 backward through the upsample (2x2 sum), plus the skip gradient
-      CKS(cbn_backward(b.x, tmp(i_a2), B, H, b.cin, b.mean1, b.rstd1, b.gain1, b.bias1, true, tmp(i_dxs), tmp(i_ds),
-                       b.ab1));
+      if (subpix_) {
+        // conv1 through the phase decomposition: dW from the low-resolution input, and the input
+        // gradient at low resolution with the upsample's adjoint included
+        CKS(conv_wgrad_up2(b.u1lo, cur, B, H, b.c1));
+        CKS(conv_dgrad_up2(cur, B, H, b.c1, tmp(i_a2)));
+        CKS(cbn_backward(b.x, tmp(i_a2), B, H, b.cin, b.mean1, b.rstd1, b.gain1, b.bias1, false, tmp(i_dxs),
+                         tmp(i_ds), b.ab1));
+      } else {
+        // conv1 on the upsampled activation
+        CKS(conv_wgrad(G_, b.u1, cur, B, H2, b.c1, b.c1.b));
+        CKS(conv_dgrad(cur, B, H2, b.c1, tmp(i_a2), nullptr));
+        // CBN1 backward through the upsample (2x2 sum), plus the skip gradient
+        CKS(cbn_backward(b.x, tmp(i_a2), B, H, b.cin, b.mean1, b.rstd1, b.gain1, b.bias1, true, tmp(i_dxs),
+                         tmp(i_ds), b.ab1));
+      }
       ic = i_ds;
       cur = tmp(ic);
     }
@@ -1687,6 +1772,7 @@ class Engine final : public EngineBase {
   ncclComm_t comm_ = nullptr;
   cublasHandle_t cublas_ = nullptr;
   bool ready_ = false, poisoned_ = false, planned_ = false, ones_ready_ = false;
+  bool subpix_ = false;   // G conv1 as four phase 2x2 convs of the low-resolution input (NEXT-1)
   int d_since_g_ = 0;
   uint64_t launches_ = 0;
   Net G_, D_;

@@ -2229,6 +2229,44 @@ __global__ void k_reduce_rows_f32(const float* __restrict__ partial, int rows, i
 }
 }  // namespace
 
+__global__ void k_fold_up2(const float* __restrict__ w, const float* __restrict__ inv_sigma, int Cout, int Cin,
+                           bf16* __restrict__ dst, int layout) {
+  const long long n = 16LL * Cout * Cin;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    int c, t, o, ph;
+    if (layout == 0) {   // [phase][Cout][tap][Cin]
+      c = (int)(i % Cin);
+      long long r = i / Cin;
+      t = (int)(r % 4);
+      r /= 4;
+      o = (int)(r % Cout);
+      ph = (int)(r / Cout);
+    } else {             // [Cin][phase * 4 + tap][Cout]
+      o = (int)(i % Cout);
+      const long long r = i / Cout;
+      t = (int)(r % 4);
+      ph = (int)((r / 4) % 4);
+      c = (int)(r / 16);
+    }
+    const int a = ph >> 1, b = ph & 1, p = t >> 1, q = t & 1;
+    // rows r0..r1 of the 3x3 kernel that land on input row offset p for phase a (same for columns)
+    const int r0 = (a == 0) ? (p == 0 ? 0 : 1) : (p == 0 ? 0 : 2);
+    const int r1 = (a == 0) ? (p == 0 ? 0 : 2) : (p == 0 ? 1 : 2);
+    const int s0 = (b == 0) ? (q == 0 ? 0 : 1) : (q == 0 ? 0 : 2);
+    const int s1 = (b == 0) ? (q == 0 ? 0 : 2) : (q == 0 ? 1 : 2);
+    float acc = 0.0f;
+    for (int rr = r0; rr <= r1; ++rr)
+      for (int ss = s0; ss <= s1; ++ss) acc += w[((long long)o * 9 + rr * 3 + ss) * Cin + c];
+    dst[i] = __float2bfloat16_rn(acc * inv_sigma[0]);
+  }
+}
+
+cudaError_t fold_up2_weights(const float* w, const float* inv_sigma, int Cout, int Cin, bf16* dst, cudaStream_t st,
+                             int layout) {
+  k_fold_up2<<<grid_for(16LL * Cout * Cin, 256), 256, 0, st>>>(w, inv_sigma, Cout, Cin, dst, layout);
+  return cudaGetLastError();
+}
+
 cudaError_t thin_conv_fwd(const float* x, int N, int H, int W, int C, const float* w, int CO, const float* bias,
                           float* y, cudaStream_t st) {
   if (CO != 3 || C % 4 || ((uintptr_t)x & 15)) return cudaErrorInvalidValue;

@@ -138,6 +138,13 @@ cudaError_t im2col3(const T* x, int N, int H, int W, int cx, T* out, cudaStream_
 template <typename T>
 cudaError_t col2im3(const T* dxi, int N, int H, int W, int cx, const T* add, T* dx, cudaStream_t st);
 
+// Sub-pixel weight fold for a 3x3 conv applied to a x2-nearest-upsampled input:
+// dst[a*2+b][o][p*2+q][c] = bf16( inv_sigma[0] * sum_{r in R(a,p), s in R(b,q)} w[o][r*3+s][c] ),
+// R(0,0) = {0}, R(0,1) = {1,2}, R(1,0) = {0,1}, R(1,1) = {2}  (output phase a reads input row i-1+a+p)
+// layout 0: fprop operand [phase][Cout][tap][Cin]; layout 1: dgrad operand [Cin][phase * 4 + tap][Cout]
+cudaError_t fold_up2_weights(const float* w, const float* inv_sigma, int Cout, int Cin, bf16* dst, cudaStream_t st,
+                             int layout = 0);
+
 // ---------------- thin fp32 conv (C_out = 3): G's fp32 output layer, 3x3 pad 1
 cudaError_t thin_conv_fwd(const float* x, int N, int H, int W, int C, const float* w, int CO, const float* bias,
                           float* y, cudaStream_t st);

@@ -35,10 +35,11 @@ constexpr int kTileM = 128;
 constexpr uint32_t kAtomBytes = 128 * 128;   // 128 rows x 128 B (64 bf16)
 // 227 KB per CTA minus alignment slack, barriers and the 2 x 16 KB epilogue staging tiles
 constexpr uint32_t kStageBytes = 128 * 128;   // one [128 rows][64 bf16] SW128 output tile
+constexpr int kStageBufs = 4;                 // two per epilogue half: a store drains one while the other fills
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = 64 + 32 * kEpiWarps;   // producer warp, MMA warp, 8 epilogue warps
 constexpr int kMaxBiasSmem = 2048;              // floats of bias staged in shared memory
-constexpr int kSmemBudget = 232448 - 1024 - 2 * (int)kStageBytes - 1024 - 4 * kMaxBiasSmem;
+constexpr int kSmemBudget = 232448 - 1024 - kStageBufs * (int)kStageBytes - 1024 - 4 * kMaxBiasSmem;
 
 template <int BN>
 struct FpropCfg {
@@ -48,7 +49,7 @@ struct FpropCfg {
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr uint32_t TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
                                         : (2 * BN <= 256) ? 256 : 512;
-  static constexpr size_t SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + 2 * kStageBytes + 512 + 4 * kMaxBiasSmem;
+  static constexpr size_t SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + kStageBufs * kStageBytes + 512 + 4 * kMaxBiasSmem;
 };
 
 template <int BN>
@@ -135,13 +136,19 @@ __device__ __forceinline__ void epilogue_loop(const TcFpropArgs& a, const CUtens
     tile0 = blockIdx.x;
     tile_step = gridDim.x;
   }
-  uint8_t* st = stage + half * kStageBytes;
+  int sb = 0;   // which of this half's two staging tiles the next 64-column group fills
   int it = 0;
   bool pending = false;
   for (int tile = tile0; tile < num_tiles; tile += tile_step, ++it) {
     const int buf = it & 1;
     const int nt = tile % a.n_tiles;
-    const int mt = CG == 2 ? (tile / a.n_tiles) * 2 + rank : tile / a.n_tiles;
+    int mt = CG == 2 ? (tile / a.n_tiles) * 2 + rank : tile / a.n_tiles;
+    int phase = 0;
+    if (CG == 2 && a.phases > 1) {   // tile = (phase * mpairs + pair) * n_tiles + nt
+      const int mpairs = (a.m_tiles + 1) / 2;
+      phase = (tile / a.n_tiles) / mpairs;
+      mt = ((tile / a.n_tiles) - phase * mpairs) * 2 + rank;
+    }
     const long long m = (long long)mt * kTileM + row;
     const bool valid = m < a.M;
     long long rbase = 0;
@@ -188,8 +195,11 @@ __device__ __forceinline__ void epilogue_loop(const TcFpropArgs& a, const CUtens
     tc::tc_fence_after();
 #pragma unroll 1
     for (int g = half * 64; g < BN; g += 128) {
+      uint8_t* st = stage + (half * 2 + sb) * kStageBytes;
       if (a.tma_store) {
-        if (leader && pending) tc::bulk_wait_read<0>();   // this half's previous store has read the tile
+        // the store that last used this staging tile (two groups ago) has read it; the previous
+        // group's store may still be draining the other tile
+        if (leader && pending) tc::bulk_wait_read<1>();
         tc::named_bar(1 + half, 128);
       }
 #pragma unroll 1
@@ -291,11 +301,18 @@ __device__ __forceinline__ void epilogue_loop(const TcFpropArgs& a, const CUtens
         tc::fence_async_smem();
         tc::named_bar(1 + half, 128);
         if (leader) {
-          tc::tma_store_2d(tmO, st, nt * BN + g, mt * kTileM);
+          if (CG == 2 && a.phases > 1) {
+            int n0, h0, w0;
+            pix_origin(mt * kTileM, a.H, a.W, n0, h0, w0);
+            tc::tma_store_5d(tmO, st, nt * BN + g, phase & 1, w0, phase >> 1, n0 * a.H + h0);
+          } else {
+            tc::tma_store_2d(tmO, st, nt * BN + g, mt * kTileM);
+          }
           tc::bulk_commit();
           pending = true;
         }
       }
+      sb ^= 1;
     }
     // one arrival per warp (the barrier counts warps): every lane's tcgen05.ld has completed
     // (wait::ld) and is ordered before lane 0's arrive by the fence + warp sync
@@ -323,7 +340,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * C::A_BYTES;
   uint8_t* sO = sB + STAGES * C::B_BYTES;            // 2 epilogue staging tiles
-  uint64_t* full = reinterpret_cast<uint64_t*>(sO + 2 * kStageBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sO + kStageBufs * kStageBytes);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -418,7 +435,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 template <int BN>
 __global__ void __launch_bounds__(192, 1)
     k_conv_wgrad(const __grid_constant__ CUtensorMap tmDY, const __grid_constant__ CUtensorMap tmX,
-                 const TcWgradArgs a) {
+                 const TcWgradArgs a, const __grid_constant__ TmaQuad tq) {
   using C = WgradCfg<BN>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -434,7 +451,9 @@ __global__ void __launch_bounds__(192, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // the CTAs of tap 0 / channel block 0 also sum dY over their pixels: db[o] = sum_p dY[p][o]
   // (an extra N = 16 MMA per K step against a constant all-ones B tile)
-  const bool do_bias = a.bias_out != nullptr && (int)(blockIdx.x % (a.m_tiles * a.n_tiles)) % a.n_tiles == 0;
+  const int nt_ = (int)(blockIdx.x % (a.m_tiles * a.n_tiles)) % a.n_tiles;
+  const bool do_bias = a.bias_out != nullptr &&
+                       (a.phases > 1 ? (nt_ % a.c_blocks == 0 && (nt_ / a.c_blocks) % 4 == 0) : nt_ == 0);
   if (do_bias) {
     uint4* o4 = reinterpret_cast<uint4*>(sOnes);
     for (int i = threadIdx.x; i < (int)(C::ONES_BYTES / 16); i += blockDim.x)
@@ -467,7 +486,13 @@ __global__ void __launch_bounds__(192, 1)
   const int mt = u / a.n_tiles;
   const int tap = nt / a.c_blocks, cb = nt - tap * a.c_blocks;
   const int pad = a.ksz >> 1;
-  const int dy = tap / a.ksz - pad, dx = tap % a.ksz - pad;
+  int dy = tap / a.ksz - pad, dx = tap % a.ksz - pad;
+  const int ph = a.phases > 1 ? tap >> 2 : 0;   // phase wgrad: tap = phase * 4 + p * 2 + q
+  if (a.phases > 1) {
+    dy = ((tap >> 1) & 1) - 1 + (ph >> 1);
+    dx = (tap & 1) - 1 + (ph & 1);
+  }
+  const CUtensorMap* mdy = a.phases > 1 ? &tq.m[ph] : &tmDY;
   const int kb0 = split * a.kb_per_split;
   const int kb1 = min(a.total_kb, kb0 + a.kb_per_split);
   const int o0 = mt * 128, c0 = cb * BN;
@@ -482,8 +507,8 @@ __global__ void __launch_bounds__(192, 1)
         tc::mbar_wait(&empty[stage], phase ^ 1);
         tc::mbar_expect_tx(&full[stage], C::A_BYTES + C::B_BYTES);
         uint8_t* da = sA + stage * C::A_BYTES;
-        tc::tma_load_4d(da, &tmDY, &full[stage], o0, w0, h0, n0);
-        tc::tma_load_4d(da + kAtomBytes, &tmDY, &full[stage], o0 + 64, w0, h0, n0);
+        tc::tma_load_4d(da, mdy, &full[stage], o0, w0, h0, n0);
+        tc::tma_load_4d(da + kAtomBytes, mdy, &full[stage], o0 + 64, w0, h0, n0);
         uint8_t* db = sB + stage * C::B_BYTES;
 #pragma unroll
         for (int j = 0; j < C::NB; ++j)
@@ -529,7 +554,7 @@ __global__ void __launch_bounds__(192, 1)
     if (do_bias) {
       float v[32];
       tc::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + BN, v);
-      if (o < a.Cout) a.bias_out[(long long)split * a.Cout + o] = v[0];
+      if (o < a.Cout) a.bias_out[((long long)split * (a.phases > 1 ? 4 : 1) + ph) * a.Cout + o] = v[0];
     }
 #pragma unroll 1
     for (int cbk = 0; cbk < BN; cbk += 32) {
@@ -574,7 +599,7 @@ struct HaloCfg {
   static constexpr int STAGES_RAW = (kSmemBudget - NA * (int)UNIT_BYTES) / (int)B_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr uint32_t TMEM_COLS = FpropCfg<BN>::TMEM_COLS;
-  static constexpr size_t SMEM = 1024 + NA * UNIT_BYTES + STAGES * B_BYTES + 2 * kStageBytes + 512 + 4 * kMaxBiasSmem;
+  static constexpr size_t SMEM = 1024 + NA * UNIT_BYTES + STAGES * B_BYTES + kStageBufs * kStageBytes + 512 + 4 * kMaxBiasSmem;
 };
 
 template <int BN, int MODE>
@@ -589,7 +614,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sH = smem;
   uint8_t* sB = smem + NA * C::UNIT_BYTES;
   uint8_t* sO = sB + STAGES * C::B_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sO + 2 * kStageBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sO + kStageBufs * kStageBytes);
   uint64_t* empty = full + STAGES;
   uint64_t* hfull = empty + STAGES;
   uint64_t* hempty = hfull + NA;
@@ -712,14 +737,16 @@ struct Cg2Cfg {
   static constexpr uint32_t B_BYTES = (BN / 2) * 128;
   static constexpr int STAGES_RAW = (kSmemBudget - NA * (int)UNIT_BYTES) / (int)B_BYTES;
   static constexpr int STAGES = STAGES_RAW > 12 ? 12 : STAGES_RAW;
+  static_assert(STAGES >= 2, "CTA-pair conv needs a >= 2 stage B ring");
   static constexpr uint32_t TMEM_COLS = FpropCfg<BN>::TMEM_COLS;
-  static constexpr size_t SMEM = 1024 + NA * UNIT_BYTES + STAGES * B_BYTES + 2 * kStageBytes + 512 + 4 * kMaxBiasSmem;
+  static constexpr size_t SMEM = 1024 + NA * UNIT_BYTES + STAGES * B_BYTES + kStageBufs * kStageBytes + 512 + 4 * kMaxBiasSmem;
 };
 
 template <int BN, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
     k_conv_fprop_cg2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     const __grid_constant__ CUtensorMap tmO, const TcFpropArgs a, const uint32_t unit_tx) {
+                     const __grid_constant__ CUtensorMap tmO, const TcFpropArgs a, const uint32_t unit_tx,
+                     const __grid_constant__ TmaQuad tq) {
   using C = Cg2Cfg<BN, MODE>;
   constexpr int STAGES = C::STAGES, NA = C::NA;
   extern __shared__ uint8_t smem_raw[];
@@ -727,7 +754,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sH = smem;
   uint8_t* sB = smem + NA * C::UNIT_BYTES;
   uint8_t* sO = sB + STAGES * C::B_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sO + 2 * kStageBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sO + kStageBufs * kStageBytes);
   uint64_t* empty = full + STAGES;
   uint64_t* hfull = empty + STAGES;
   uint64_t* hempty = hfull + NA;
@@ -762,7 +789,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int mpairs = (a.m_tiles + 1) / 2;
-  const int num_tiles = mpairs * a.n_tiles;
+  const int num_tiles = mpairs * a.n_tiles * (a.phases > 1 ? a.phases : 1);
   const int cid = (int)tc::cluster_id_x(), ncl = (int)tc::num_clusters_x();
   constexpr int UNITS_PER_CHUNK_FIXED = MODE == 0 ? 1 : (MODE == 1 ? 3 : 0);
   const int units_per_chunk = MODE == 2 ? a.taps : UNITS_PER_CHUNK_FIXED;
@@ -775,7 +802,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0, hphase = 0;
       for (int tile = cid; tile < num_tiles; tile += ncl) {
         const int nt = tile % a.n_tiles;
-        const int mt = (tile / a.n_tiles) * 2 + (int)rank;
+        const int mp = tile / a.n_tiles;
+        const int oph = a.phases > 1 ? mp / mpairs : 0;   // output phase (sub-pixel mode)
+        const int mt = (mp - oph * mpairs) * 2 + (int)rank;
+        const int pa = oph >> 1, pb = oph & 1;         // its row / column parity
+        const int wrow = oph * a.Cout;                 // its weight rows
         int n0, h0, w0;
         pix_origin(mt * kTileM, a.H, a.W, n0, h0, w0);
         for (int cc = 0; cc < a.c_chunks; ++cc) {
@@ -787,6 +818,13 @@ __global__ void __launch_bounds__(kThreads, 1)
               tc::tma_load_4d_cg2(sH + hs * C::UNIT_BYTES, &tmA, hbar, cc * 64, w0 - 1, h0 - 1, n0);
             } else if (MODE == 1) {
               tc::tma_load_4d_cg2(sH + hs * C::UNIT_BYTES, &tmA, hbar, cc * 64, w0 - 1 + u, h0 - 1, n0);
+            } else if (a.phase_dgrad) {   // tap u = phase * 4 + p * 2 + q: dY of phase (a, b) at (i+1-a-p, j+1-b-q)
+              const int ph = u >> 2, ta = ph >> 1, tb = ph & 1, p = (u >> 1) & 1, q = u & 1;
+              tc::tma_load_4d_cg2(sH + hs * C::UNIT_BYTES, &tq.m[ph], hbar, cc * 64, w0 + 1 - tb - q, h0 + 1 - ta - p,
+                                  n0);
+            } else if (a.phases > 1) {   // 2x2 taps (p, q) of phase (pa, pb): offsets p - 1 + pa, q - 1 + pb
+              const int dy = (u >> 1) - 1 + pa, dx = (u & 1) - 1 + pb;
+              tc::tma_load_4d_cg2(sH + hs * C::UNIT_BYTES, &tmA, hbar, cc * 64, w0 + dx, h0 + dy, n0);
             } else {
               const int dy = u / a.ksz - pad, dx = u % a.ksz - pad;
               tc::tma_load_4d_cg2(sH + hs * C::UNIT_BYTES, &tmA, hbar, cc * 64, w0 + dx, h0 + dy, n0);
@@ -796,7 +834,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               tc::mbar_wait(&empty[stage], phase ^ 1);
               const uint32_t fbar = tc::map_to_rank(&full[stage], 0);
               if (is_leader) tc::mbar_expect_tx(&full[stage], 2 * C::B_BYTES);
-              tc::tma_load_3d_cg2(sB + stage * C::B_BYTES, &tmB, fbar, cc * 64, tap, nt * BN + (int)rank * (BN / 2));
+              tc::tma_load_3d_cg2(sB + stage * C::B_BYTES, &tmB, fbar, cc * 64, tap,
+                                  wrow + nt * BN + (int)rank * (BN / 2));
               if (++stage == STAGES) { stage = 0; phase ^= 1; }
             }
             if (++hs == NA) { hs = 0; hphase ^= 1; }
@@ -862,6 +901,38 @@ __global__ void k_split_reduce(const float* __restrict__ part, float* __restrict
     float s = accumulate ? dst[i] : 0.0f;
     for (int k = 0; k < splits; ++k) s += part[(long long)k * n + i];
     dst[i] = s;
+  }
+}
+
+// phase wgrad reduction: dW[o][r*3+s][c] = sum_splits sum over the four (phase, tap) pairs whose folded
+// 2x2 tap covers (r, s) of part[split][o][phase*4 + p*2 + q][c]  (the adjoint of fold_up2_weights)
+__global__ void k_split_reduce_unfold(const float* __restrict__ part, float* __restrict__ dw, int Cout, int Cin,
+                                      int splits) {
+  const long long n = 9LL * Cout * Cin;
+  const long long pstride = 16LL * Cout * Cin;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(i % Cin);
+    const long long r9 = i / Cin;
+    const int rs = (int)(r9 % 9);
+    const int o = (int)(r9 / 9);
+    const int r = rs / 3, sc = rs % 3;
+    // (a, p) pairs whose row set R(a, p) contains r (R(0,0)={0}, R(0,1)={1,2}, R(1,0)={0,1}, R(1,1)={2})
+    const int ra[2] = {r == 0 ? 0 : 0, r == 0 ? 1 : 1};
+    const int rp[2] = {r == 0 ? 0 : 1, r == 2 ? 1 : 0};
+    const int sa[2] = {0, 1};
+    const int sp[2] = {sc == 0 ? 0 : 1, sc == 2 ? 1 : 0};
+    float acc = 0.0f;
+    for (int k = 0; k < splits; ++k) {
+      const float* pk = part + k * pstride + (long long)o * 16 * Cin + c;
+#pragma unroll
+      for (int i1 = 0; i1 < 2; ++i1)
+#pragma unroll
+        for (int i2 = 0; i2 < 2; ++i2) {
+          const int ph = ra[i1] * 2 + sa[i2], t = rp[i1] * 2 + sp[i2];
+          acc += pk[(long long)(ph * 4 + t) * Cin];
+        }
+    }
+    dw[i] = acc;
   }
 }
 
@@ -980,7 +1051,7 @@ cudaError_t launch_halo(int bn, const CUtensorMap& ma, const CUtensorMap& mb, co
 
 template <int BN, int MODE>
 cudaError_t launch_cg2_bn(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo, const TcFpropArgs& a,
-                          uint32_t unit_tx, cudaStream_t st) {
+                          uint32_t unit_tx, cudaStream_t st, const TmaQuad* quad) {
   using C = Cg2Cfg<BN, MODE>;
   static bool attr = false;
   if (!attr) {
@@ -988,7 +1059,7 @@ cudaError_t launch_cg2_bn(const CUtensorMap& ma, const CUtensorMap& mb, const CU
                                  (int)C::SMEM));
     attr = true;
   }
-  const int tiles = ((a.m_tiles + 1) / 2) * a.n_tiles;
+  const int tiles = ((a.m_tiles + 1) / 2) * a.n_tiles * (a.phases > 1 ? a.phases : 1);
   int clusters = tiles < kNumSMs / 2 ? tiles : kNumSMs / 2;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * clusters, 1, 1);
@@ -1002,19 +1073,21 @@ cudaError_t launch_cg2_bn(const CUtensorMap& ma, const CUtensorMap& mb, const CU
   attrs[0].val.clusterDim.z = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_conv_fprop_cg2<BN, MODE>, ma, mb, mo, a, unit_tx);
+  TmaQuad tq;
+  for (int i = 0; i < 4; ++i) tq.m[i] = quad ? quad->m[i] : ma;
+  return cudaLaunchKernelEx(&cfg, k_conv_fprop_cg2<BN, MODE>, ma, mb, mo, a, unit_tx, tq);
 }
 
 template <int MODE>
 cudaError_t launch_cg2(int bn, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo,
-                       const TcFpropArgs& a, uint32_t unit_tx, cudaStream_t st) {
+                       const TcFpropArgs& a, uint32_t unit_tx, cudaStream_t st, const TmaQuad* quad = nullptr) {
   switch (bn) {
-    case 32: return launch_cg2_bn<32, MODE>(ma, mb, mo, a, unit_tx, st);
-    case 64: return launch_cg2_bn<64, MODE>(ma, mb, mo, a, unit_tx, st);
-    case 96: return launch_cg2_bn<96, MODE>(ma, mb, mo, a, unit_tx, st);
-    case 128: return launch_cg2_bn<128, MODE>(ma, mb, mo, a, unit_tx, st);
-    case 192: return launch_cg2_bn<192, MODE>(ma, mb, mo, a, unit_tx, st);
-    default: return launch_cg2_bn<256, MODE>(ma, mb, mo, a, unit_tx, st);
+    case 32: return launch_cg2_bn<32, MODE>(ma, mb, mo, a, unit_tx, st, quad);
+    case 64: return launch_cg2_bn<64, MODE>(ma, mb, mo, a, unit_tx, st, quad);
+    case 96: return launch_cg2_bn<96, MODE>(ma, mb, mo, a, unit_tx, st, quad);
+    case 128: return launch_cg2_bn<128, MODE>(ma, mb, mo, a, unit_tx, st, quad);
+    case 192: return launch_cg2_bn<192, MODE>(ma, mb, mo, a, unit_tx, st, quad);
+    default: return launch_cg2_bn<256, MODE>(ma, mb, mo, a, unit_tx, st, quad);
   }
 }
 
@@ -1024,7 +1097,8 @@ int env_int(const char* name, int dflt) {
 }
 
 template <int BN>
-cudaError_t launch_wgrad_bn(const CUtensorMap& ma, const CUtensorMap& mb, const TcWgradArgs& a, cudaStream_t st) {
+cudaError_t launch_wgrad_bn(const CUtensorMap& ma, const CUtensorMap& mb, const TcWgradArgs& a, cudaStream_t st,
+                            const TmaQuad* quad = nullptr) {
   using C = WgradCfg<BN>;
   static bool attr = false;
   if (!attr) {
@@ -1032,7 +1106,9 @@ cudaError_t launch_wgrad_bn(const CUtensorMap& ma, const CUtensorMap& mb, const 
     attr = true;
   }
   const int units = a.m_tiles * a.n_tiles * a.splits;
-  k_conv_wgrad<BN><<<units, 192, C::SMEM, st>>>(ma, mb, a);
+  TmaQuad tq;
+  for (int i = 0; i < 4; ++i) tq.m[i] = quad ? quad->m[i] : ma;
+  k_conv_wgrad<BN><<<units, 192, C::SMEM, st>>>(ma, mb, a, tq);
   return cudaGetLastError();
 }
 
@@ -1134,6 +1210,185 @@ cudaError_t tc_conv_fprop(const void* x, int N, int H, int W, int Cin, const voi
     case 192: return launch_fprop_bn<192>(ma, mb, mo, a, sms, st);
     default: return launch_fprop_bn<256>(ma, mb, mo, a, sms, st);
   }
+}
+
+cudaError_t tc_conv_fprop_up2(const void* x, int N, int H, int W, int Cin, const void* wpack4, int Cout,
+                              const TcEpilogue& epi, cudaStream_t st) {
+  if (Cin % 8 || Cout % 8 || ((uintptr_t)x & 15) || ((uintptr_t)wpack4 & 15) || ((uintptr_t)epi.out & 15) ||
+      !tileable(H, W) || epi.residual || epi.relu_ref || epi.out_f32 || (epi.ldo && epi.ldo != Cout))
+    return cudaErrorInvalidValue;
+  const int bn = pick_bn(Cout);
+  TcFpropArgs a{};
+  a.M = (long long)N * H * W;
+  a.H = H;
+  a.W = W;
+  a.ksz = 2;
+  a.taps = 4;
+  a.c_chunks = ceil_div(Cin, 64);
+  a.last_ksteps = ceil_div(Cin - (a.c_chunks - 1) * 64, 16);
+  a.Cout = Cout;
+  a.m_tiles = ceil_div(a.M, kTileM);
+  a.n_tiles = ceil_div(Cout, bn);
+  a.bias = epi.bias;
+  a.alpha = epi.alpha;
+  a.out = epi.out;
+  a.ldo = Cout;
+  a.ldr = Cout;
+  a.tma_store = 1;
+  a.phases = 4;
+  if (!(bn % 64 == 0 || a.n_tiles == 1)) return cudaErrorInvalidValue;
+  CUtensorMap ma, mb2, mo;
+  PG_CUDA(act_map(&ma, x, N, H, W, Cin));
+  PG_CUDA(weight_map(&mb2, wpack4, 4 * Cout, 4, Cin, bn / 2));
+  {
+    // output [N][2H][2W][C] viewed as {C, 2 (column phase), W, 2 (row phase), N*H}
+    PG_CUDA(get_encoder());
+    int bw, bh, bnn;
+    tile_box(N, H, W, bw, bh, bnn);
+    cuuint64_t dims[5] = {(cuuint64_t)Cout, 2, (cuuint64_t)W, 2, (cuuint64_t)N * H};
+    cuuint64_t strides[4] = {(cuuint64_t)Cout * 2, (cuuint64_t)Cout * 4, (cuuint64_t)W * Cout * 4,
+                             (cuuint64_t)W * Cout * 8};
+    cuuint32_t box[5] = {64, 1, (cuuint32_t)bw, 1, (cuuint32_t)(bh * bnn)};
+    cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    CUresult r = g_encode(&mo, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, epi.out, dims, strides, box, es,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  }
+  return launch_cg2<2>(bn, ma, mb2, mo, a, kAtomBytes, st);
+}
+
+cudaError_t tc_conv_dgrad_up2(const void* dy, int N, int H, int W, int Cout, const void* wt4, int Cin,
+                              const TcEpilogue& epi, cudaStream_t st) {
+  if (Cin % 8 || Cout % 8 || ((uintptr_t)dy & 15) || ((uintptr_t)wt4 & 15) || ((uintptr_t)epi.out & 15) ||
+      !tileable(H, W) || epi.out_f32)
+    return cudaErrorInvalidValue;
+  const int bn = pick_bn(Cin);
+  TcFpropArgs a{};
+  a.M = (long long)N * H * W;
+  a.H = H;
+  a.W = W;
+  a.ksz = 2;
+  a.taps = 16;
+  a.c_chunks = ceil_div(Cout, 64);
+  a.last_ksteps = ceil_div(Cout - (a.c_chunks - 1) * 64, 16);
+  a.Cout = Cin;
+  a.m_tiles = ceil_div(a.M, kTileM);
+  a.n_tiles = ceil_div(Cin, bn);
+  a.bias = epi.bias;
+  a.alpha = epi.alpha;
+  a.residual = epi.residual;
+  a.res_mode = epi.res_mode;
+  a.ldr = epi.ldr ? epi.ldr : Cin;
+  a.relu_ref = epi.relu_ref;
+  a.out = epi.out;
+  a.ldo = epi.ldo ? epi.ldo : Cin;
+  a.tma_store = (bn % 64 == 0 || a.n_tiles == 1) && a.ldo % 8 == 0;
+  a.phases = 1;
+  a.phase_dgrad = 1;
+  if (!a.tma_store) return cudaErrorInvalidValue;
+  CUtensorMap mb2, mo;
+  PG_CUDA(weight_map(&mb2, wt4, Cin, 16, Cout, bn / 2));
+  PG_CUDA(out_map(&mo, epi.out, a.M, Cin, a.ldo));
+  TmaQuad tq;
+  {
+    PG_CUDA(get_encoder());
+    int bw, bh, bnn;
+    tile_box(N, H, W, bw, bh, bnn);
+    for (int ph = 0; ph < 4; ++ph) {
+      // dY of output phase (a, b) as a low-resolution [N][H][W][Cout] tensor
+      const int pa = ph >> 1, pb = ph & 1;
+      const char* base = static_cast<const char*>(dy) + ((size_t)pa * 2 * W + pb) * Cout * 2;
+      cuuint64_t dims[4] = {(cuuint64_t)Cout, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
+      cuuint64_t strides[3] = {(cuuint64_t)Cout * 4, (cuuint64_t)W * Cout * 8, (cuuint64_t)H * W * Cout * 8};
+      cuuint32_t box[4] = {64, (cuuint32_t)bw, (cuuint32_t)bh, (cuuint32_t)bnn};
+      cuuint32_t es[4] = {1, 1, 1, 1};
+      CUresult r = g_encode(&tq.m[ph], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<char*>(base), dims, strides,
+                            box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    }
+  }
+  return launch_cg2<2>(bn, tq.m[0], mb2, mo, a, kAtomBytes, st, &tq);
+}
+
+cudaError_t tc_conv_wgrad_up2(const void* x, const void* dy, int N, int H, int W, int Cin, int Cout, float* dw,
+                              float* scratch, size_t scratch_floats, cudaStream_t st, float* dbias) {
+  if (Cin % 8 || Cout % 8 || ((uintptr_t)x & 15) || ((uintptr_t)dy & 15) || !tileable(H, W))
+    return cudaErrorInvalidValue;
+  int bn;
+  if (Cin % 256 == 0) bn = 256;
+  else if (Cin % 192 == 0) bn = 192;
+  else if (Cin % 128 == 0) bn = 128;
+  else if (Cin <= 32) bn = 32;
+  else if (Cin <= 64) bn = 64;
+  else if (Cin <= 96) bn = 96;
+  else bn = 128;
+  CUtensorMap mx;
+  PG_CUDA(act_map(&mx, x, N, H, W, Cin));
+  TmaQuad tq;
+  {
+    PG_CUDA(get_encoder());
+    int bw, bh, bnn;
+    tile_box(N, H, W, bw, bh, bnn);
+    for (int ph = 0; ph < 4; ++ph) {   // dY of output phase (a, b) as a low-resolution tensor
+      const char* base = static_cast<const char*>(dy) + ((size_t)(ph >> 1) * 2 * W + (ph & 1)) * Cout * 2;
+      cuuint64_t dims[4] = {(cuuint64_t)Cout, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
+      cuuint64_t strides[3] = {(cuuint64_t)Cout * 4, (cuuint64_t)W * Cout * 8, (cuuint64_t)H * W * Cout * 8};
+      cuuint32_t box[4] = {64, (cuuint32_t)bw, (cuuint32_t)bh, (cuuint32_t)bnn};
+      cuuint32_t es[4] = {1, 1, 1, 1};
+      CUresult r = g_encode(&tq.m[ph], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<char*>(base), dims, strides,
+                            box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    }
+  }
+  TcWgradArgs a{};
+  a.H = H;
+  a.W = W;
+  a.ksz = 2;
+  a.taps = 16;
+  a.Cin = Cin;
+  a.Cout = Cout;
+  a.c_blocks = ceil_div(Cin, bn);
+  a.m_tiles = ceil_div(Cout, 128);
+  a.n_tiles = a.taps * a.c_blocks;
+  a.total_kb = ceil_div((long long)N * H * W, kTileM);
+  a.phases = 4;
+  const int tiles = a.m_tiles * a.n_tiles;
+  int splits = (2 * kNumSMs + tiles - 1) / tiles;
+  if (splits > a.total_kb / 4) splits = a.total_kb / 4;
+  if (splits < 1) splits = 1;
+  const size_t out_floats = (size_t)Cout * a.taps * Cin;
+  const size_t bias_floats = dbias ? (size_t)4 * Cout : 0;
+  while (splits > 1 && (size_t)splits * (out_floats + bias_floats) > scratch_floats) --splits;
+  if ((size_t)splits * (out_floats + bias_floats) > scratch_floats) return cudaErrorMemoryAllocation;
+  a.kb_per_split = ceil_div(a.total_kb, splits);
+  a.splits = ceil_div(a.total_kb, a.kb_per_split);
+  a.out = scratch;
+  a.bias_out = dbias ? scratch + (size_t)a.splits * out_floats : nullptr;
+  cudaError_t e;
+  switch (bn) {
+    case 32: e = launch_wgrad_bn<32>(tq.m[0], mx, a, st, &tq); break;
+    case 64: e = launch_wgrad_bn<64>(tq.m[0], mx, a, st, &tq); break;
+    case 96: e = launch_wgrad_bn<96>(tq.m[0], mx, a, st, &tq); break;
+    case 128: e = launch_wgrad_bn<128>(tq.m[0], mx, a, st, &tq); break;
+    case 192: e = launch_wgrad_bn<192>(tq.m[0], mx, a, st, &tq); break;
+    default: e = launch_wgrad_bn<256>(tq.m[0], mx, a, st, &tq); break;
+  }
+  PG_CUDA(e);
+  {
+    const long long n = 9LL * Cout * Cin;
+    int blocks = ceil_div(n, 256);
+    if (blocks > 8 * kNumSMs) blocks = 8 * kNumSMs;
+    k_split_reduce_unfold<<<blocks, 256, 0, st>>>(scratch, dw, Cout, Cin, a.splits);
+    PG_LAUNCH_CHECK();
+  }
+  if (dbias) {
+    k_split_reduce<<<ceil_div(Cout, 256), 256, 0, st>>>(a.bias_out, dbias, Cout, a.splits * 4, 0);
+    PG_LAUNCH_CHECK();
+  }
+  return cudaSuccess;
 }
 
 size_t tc_wgrad_workspace_floats(int N, int H, int W, int Cin, int Cout, int ksz) {

@@ -197,3 +197,100 @@ def test_thin_conv_f32_fwd_dgrad_wgrad(shape):
     want_dw = gw.permute(0, 2, 3, 1).reshape(cout, k * k, cin).numpy()
     for got, want in ((y, want_y), (dx, want_dx), (dw, want_dw)):
         assert np.linalg.norm(got.cpu().numpy() - want) <= 1e-5 * np.linalg.norm(want)
+
+
+UP2_SHAPES = [  # n, h, w, cin, cout  (low-resolution input; output 2h x 2w)
+    (2, 4, 4, 64, 128),          # G block 0 geometry: 16-pixel images, 8 images per tile
+    (1, 8, 8, 96, 96),
+    (2, 16, 16, 192, 96),        # 96-channel tail chunk, odd N tiles
+    (1, 64, 64, 192, 96),        # G's last conv1 at quarter batch
+    (3, 8, 8, 32, 256),          # several N tiles, odd number of M tiles
+]
+
+
+def _oracle_up2_conv(x_nhwc, w_otc, b):
+    x = torch.from_numpy(x_nhwc).double().permute(0, 3, 1, 2)
+    cout, _, cin = w_otc.shape
+    w = torch.from_numpy(w_otc).double().reshape(cout, 3, 3, cin).permute(0, 3, 1, 2)
+    y = ops.conv2d(ops.up2(x), w, torch.from_numpy(b).double())
+    return y.permute(0, 2, 3, 1).numpy()
+
+
+@pytest.mark.parametrize("shape", UP2_SHAPES)
+def test_conv_up2_phase_decomposition_integer_exact(shape):
+    """The sub-pixel (phase-decomposed) conv3x3(up2(x)) equals the plain conv on the upsampled
+    tensor bit for bit on integer data (folded weights are small exact integers)."""
+    n, h, w, cin, cout = shape
+    rng = np.random.default_rng(h * 31 + cin)
+    x = rng.integers(-2, 3, size=(n, h, w, cin)).astype(np.float32)
+    wt = rng.integers(-1, 2, size=(cout, 9, cin)).astype(np.float32)
+    b = rng.integers(-3, 4, size=(cout,)).astype(np.float32)
+    want = _oracle_up2_conv(x, wt, b).astype(np.float32)
+    y = torch.full((n, 2 * h, 2 * w, cout), float("nan"), dtype=torch.bfloat16, device=DEV)
+    api.op_conv_up2_fwd(_bf16_np(x).to(DEV), torch.from_numpy(wt).to(DEV), torch.from_numpy(b).to(DEV), cout, y)
+    torch.cuda.synchronize()
+    got = y.float().cpu().numpy()
+    assert np.abs(want).max() < 256   # exact in bf16
+    assert np.array_equal(got, want), np.argwhere(got != want)[:5]
+
+
+def test_conv_up2_random_within_bf16_error():
+    n, h, w, cin, cout = 2, 32, 32, 96, 192
+    rng = np.random.default_rng(7)
+    x = rng.standard_normal((n, h, w, cin)).astype(np.float32)
+    wt = (rng.standard_normal((cout, 9, cin)) * 0.05).astype(np.float32)
+    b = rng.standard_normal(cout).astype(np.float32)
+    xb = _bf16_np(x)
+    want = _oracle_up2_conv(xb.float().numpy(), wt, b)
+    y = torch.empty((n, 2 * h, 2 * w, cout), dtype=torch.bfloat16, device=DEV)
+    api.op_conv_up2_fwd(xb.to(DEV), torch.from_numpy(wt).to(DEV), torch.from_numpy(b).to(DEV), cout, y)
+    torch.cuda.synchronize()
+    err = np.linalg.norm(y.float().cpu().numpy() - want) / np.linalg.norm(want)
+    assert err < 4e-3   # folded weights and the output rounded once each to bf16
+
+
+@pytest.mark.parametrize("shape", UP2_SHAPES)
+def test_conv_up2_dgrad_integer_exact(shape):
+    """Input gradient of conv3x3(up2(x)) at low resolution through the phase decomposition (the 2x2
+    up2 adjoint included) equals fp64 autograd of the plain definition bit for bit on integers."""
+    n, h, w, cin, cout = shape
+    rng = np.random.default_rng(h * 37 + cout)
+    x = np.zeros((n, h, w, cin), np.float32)
+    wt = rng.integers(-1, 2, size=(cout, 9, cin)).astype(np.float32)
+    dy = rng.integers(-2, 3, size=(n, 2 * h, 2 * w, cout)).astype(np.float32)
+    xt = torch.from_numpy(x).double().permute(0, 3, 1, 2).requires_grad_(True)
+    wv = torch.from_numpy(wt).double().reshape(cout, 3, 3, cin).permute(0, 3, 1, 2)
+    (gx,) = torch.autograd.grad((ops.conv2d(ops.up2(xt), wv, None) *
+                                 torch.from_numpy(dy).double().permute(0, 3, 1, 2)).sum(), xt)
+    want = gx.permute(0, 2, 3, 1).numpy().astype(np.float32)
+    assert np.abs(want).max() < 2 ** 24
+    dx = torch.full((n, h, w, cin), float("nan"), dtype=torch.float32, device=DEV).to(torch.bfloat16)
+    api.op_conv_up2_dgrad(_bf16_np(dy).to(DEV), torch.from_numpy(wt).to(DEV), cin, dx)
+    torch.cuda.synchronize()
+    got = dx.float().cpu().numpy()
+    # bf16 output: compare against the bf16 rounding of the exact integer result
+    want_b = torch.from_numpy(want).to(torch.bfloat16).float().numpy()
+    assert np.array_equal(got, want_b), np.argwhere(got != want_b)[:5]
+
+
+@pytest.mark.parametrize("shape", UP2_SHAPES)
+def test_conv_up2_wgrad_integer_exact(shape):
+    """Weight (and bias) gradient of conv3x3(up2(x)) from the low-resolution x through the 16 folded
+    phase taps and the unfolding reduction equals fp64 autograd of the plain definition bit for bit."""
+    n, h, w, cin, cout = shape
+    rng = np.random.default_rng(h * 41 + cin + cout)
+    x = rng.integers(-2, 3, size=(n, h, w, cin)).astype(np.float32)
+    dy = rng.integers(-2, 3, size=(n, 2 * h, 2 * w, cout)).astype(np.float32)
+    xt = torch.from_numpy(x).double().permute(0, 3, 1, 2)
+    wv = torch.zeros(cout, cin, 3, 3, dtype=torch.float64, requires_grad=True)
+    (gw,) = torch.autograd.grad((ops.conv2d(ops.up2(xt), wv, None) *
+                                 torch.from_numpy(dy).double().permute(0, 3, 1, 2)).sum(), wv)
+    want = gw.permute(0, 2, 3, 1).reshape(cout, 9, cin).numpy().astype(np.float32)
+    assert np.abs(want).max() < 2 ** 24
+    dw = torch.full((cout, 9, cin), float("nan"), dtype=torch.float32, device=DEV)
+    db = torch.full((cout,), float("nan"), dtype=torch.float32, device=DEV)
+    api.op_conv_up2_wgrad(_bf16_np(x).to(DEV), _bf16_np(dy).to(DEV), cout, dw, db=db)
+    torch.cuda.synchronize()
+    got = dw.cpu().numpy()
+    assert np.array_equal(got, want), np.argwhere(got != want)[:5]
+    assert np.array_equal(db.cpu().numpy(), dy.reshape(-1, cout).sum(0).astype(np.float32))

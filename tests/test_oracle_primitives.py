@@ -326,3 +326,27 @@ def test_adam_scalar_reference_1000_steps():
         ws = ws - lr * (ms / (1 - b1 ** t)) / ((vs / (1 - b2 ** t)) ** 0.5 + eps)
     assert abs(float(w) - ws) < 1e-12
     assert abs(ws) < 0.05
+
+
+def test_up2_conv_phase_decomposition_is_conv_of_upsampled():
+    """R24: the four 2x2 phase convs of the low-resolution input equal conv3x3(up2(x)) — values and
+    both gradients, in fp64 (the bf16 variant only moves the rounding point of the weights)."""
+    rng = np.random.default_rng(11)
+    x = torch.from_numpy(rng.standard_normal((2, 3, 5, 4))).requires_grad_(True)
+    w = torch.from_numpy(rng.standard_normal((4, 3, 3, 3))).requires_grad_(True)
+    b = torch.from_numpy(rng.standard_normal(4))
+    dy = torch.from_numpy(rng.standard_normal((2, 4, 10, 8)))
+    y1 = ops.up2_conv3x3_phases(x, w, b, bf16=False)
+    y2 = ops.conv2d(ops.up2(x), w, b)
+    assert torch.allclose(y1, y2, rtol=1e-12, atol=1e-12)
+    g1 = torch.autograd.grad((y1 * dy).sum(), (x, w))
+    g2 = torch.autograd.grad((y2 * dy).sum(), (x, w))
+    for a, c in zip(g1, g2):
+        assert torch.allclose(a, c, rtol=1e-12, atol=1e-12)
+    # each output pixel of phase (a, b) reads exactly a 2x2 low-resolution window: a delta input
+    # lights the 4x4 high-resolution block the 3x3 kernel over the 2x2 replicated pixel covers
+    xd = torch.zeros(1, 1, 4, 4, dtype=torch.float64)
+    xd[0, 0, 1, 2] = 1.0
+    yd = ops.up2_conv3x3_phases(xd, torch.ones(1, 1, 3, 3, dtype=torch.float64), None, bf16=False)
+    nz = torch.nonzero(yd[0, 0]).tolist()
+    assert sorted({r for r, _ in nz}) == [1, 2, 3, 4] and sorted({c for _, c in nz}) == [3, 4, 5, 6]
