@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define PARAGAN_ABI_VERSION 1
+#define PARAGAN_ABI_VERSION 2
 
 typedef struct paragan_ctx paragan_ctx; /* opaque, library-owned */
 
@@ -54,6 +54,8 @@ typedef enum {
 } paragan_status;
 
 typedef enum { PARAGAN_F32 = 0, PARAGAN_BF16 = 1 } paragan_dtype;
+/* BigGAN (configs 2-5, R1) or the tiny SN-DCGAN 32x32 (config 1, R25; fp32 SIMT path only). */
+typedef enum { PARAGAN_ARCH_BIGGAN = 0, PARAGAN_ARCH_SNDCGAN = 1 } paragan_arch;
 typedef enum { PARAGAN_NET_D = 0, PARAGAN_NET_G = 1 } paragan_net;
 
 /* Adam hyper-parameters of one network (asymmetric policy, PAPER.md:285-307;
@@ -62,9 +64,11 @@ typedef struct {
   float lr, beta1, beta2, eps;
 } paragan_adam;
 
-/* BigGAN configuration.  The architecture is derived from (resolution, ch)
+/* Model configuration.  BigGAN: the architecture is derived from (resolution, ch)
  * exactly as DESIGN.md §3 R1 states (BigGAN channel tables; 128/256/512 and the
- * small 16/32 test resolutions). */
+ * small 16/32 test resolutions).  SN-DCGAN (arch = PARAGAN_ARCH_SNDCGAN): resolution 32,
+ * widths x ch/64, dim_z 128, unconditional (labels ignored; n_classes only sizes
+ * the label inputs), compute = F32 (R25). */
 typedef struct {
   int32_t abi_version;   /* PARAGAN_ABI_VERSION */
   int32_t resolution;    /* 16, 32, 64, 128, 256, 512 */
@@ -81,6 +85,7 @@ typedef struct {
   float sn_eps, bn_eps;
   int32_t rank, world_size, device;
   uint64_t seed;         /* on-device weight init (paragan_init_params) */
+  int32_t arch;          /* a paragan_arch value; field added in ABI 2 */
 } paragan_config;
 
 typedef struct {

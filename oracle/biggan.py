@@ -73,6 +73,7 @@ class Config:
     d_steps_per_g: int = 1
     bf16: bool = False           # emulate the bf16 storage points of R14
     subpixel: bool = True         # with bf16: G's conv1 through the phase decomposition (R24)
+    arch: str = "biggan"          # "biggan" (R1) or "sndcgan" (config 1, R25; oracle/sndcgan.py)
     adam_d: AdamHP = field(default_factory=lambda: AdamHP(2e-4, 0.0, 0.999, 1e-8))
     adam_g: AdamHP = field(default_factory=lambda: AdamHP(5e-5, 0.0, 0.999, 1e-8))
 
@@ -82,6 +83,8 @@ class Config:
 
     @property
     def dim_z(self) -> int:
+        if self.arch == "sndcgan":
+            return 128
         return (self.n_blocks_g + 1) * self.z_chunk
 
     @property
@@ -127,6 +130,9 @@ class PSpec:
 
 
 def g_param_specs(cfg: Config) -> list[PSpec]:
+    if cfg.arch == "sndcgan":
+        from . import sndcgan
+        return sndcgan.g_param_specs(cfg)
     c0 = g_blocks(cfg)[0][0]
     s = [PSpec("shared", (cfg.n_classes, cfg.shared_dim), "normal"),
          PSpec("linear.w", (16 * c0, cfg.z_chunk), "normal", True),
@@ -152,6 +158,9 @@ def g_param_specs(cfg: Config) -> list[PSpec]:
 
 
 def d_param_specs(cfg: Config) -> list[PSpec]:
+    if cfg.arch == "sndcgan":
+        from . import sndcgan
+        return sndcgan.d_param_specs(cfg)
     s = []
     for j, (ci, co, _, dn, att) in enumerate(d_blocks(cfg)):
         p = f"b{j}."
@@ -244,6 +253,9 @@ def _qw(sn: _SN, name: str) -> torch.Tensor:
 
 def g_forward(cfg: Config, sn: _SN, z: torch.Tensor, y: torch.Tensor) -> torch.Tensor:
     """Generator (Appendix A of SURVEY; R1, R10, R11).  Returns images NCHW in [-1, 1]."""
+    if cfg.arch == "sndcgan":
+        from . import sndcgan
+        return sndcgan.g_forward(cfg, sn, z, y)
     bf = cfg.bf16
     p = sn.params
     B = z.shape[0]
@@ -297,6 +309,9 @@ def _attention(cfg: Config, sn: _SN, pre: str, x: torch.Tensor) -> torch.Tensor:
 
 def d_forward(cfg: Config, sn: _SN, x: torch.Tensor, y: torch.Tensor) -> torch.Tensor:
     """Projection discriminator (Appendix A; R1, R7).  x NCHW; returns logits [N] (fp32 head)."""
+    if cfg.arch == "sndcgan":
+        from . import sndcgan
+        return sndcgan.d_forward(cfg, sn, x, y)
     bf = cfg.bf16
     p = sn.params
     h = x

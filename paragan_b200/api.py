@@ -13,8 +13,9 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libparagan.so")
 
-PARAGAN_ABI_VERSION = 1
+PARAGAN_ABI_VERSION = 2
 F32, BF16 = 0, 1
+ARCH_BIGGAN, ARCH_SNDCGAN = 0, 1
 NET_D, NET_G = 0, 1
 FLAG_NO_ALLREDUCE, FLAG_NO_UPDATE = 1, 2
 STATUS = {0: "OK", 1: "INVALID_ARG", 2: "CONFIG", 3: "NONFINITE", 4: "IO", 5: "CUDA", 6: "NCCL", 7: "ORDER", 8: "OOM"}
@@ -30,7 +31,7 @@ class Config(C.Structure):
                 ("attn_res", C.c_int32), ("local_batch", C.c_int32), ("d_steps_per_g", C.c_int32),
                 ("compute", C.c_int32), ("c_pad_image", C.c_int32), ("adam_d", Adam), ("adam_g", Adam),
                 ("sn_eps", C.c_float), ("bn_eps", C.c_float), ("rank", C.c_int32), ("world_size", C.c_int32),
-                ("device", C.c_int32), ("seed", C.c_uint64)]
+                ("device", C.c_int32), ("seed", C.c_uint64), ("arch", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -128,16 +129,24 @@ def _stream(stream):
 def make_config(resolution=128, ch=96, n_classes=1000, shared_dim=128, z_chunk=20, attn_res=64, local_batch=256,
                 d_steps_per_g=1, compute=BF16, c_pad_image=8, adam_d=(2e-4, 0.0, 0.999, None),
                 adam_g=(5e-5, 0.0, 0.999, None), sn_eps=1e-12, bn_eps=1e-5, rank=0, world_size=1, device=0,
-                seed=0) -> Config:
+                seed=0, arch=0) -> Config:
     """BigGAN config; Adam eps defaults to 1e-6 under bf16 and 1e-8 in fp32."""
     eps = 1e-6 if compute == BF16 else 1e-8
     ad = Adam(adam_d[0], adam_d[1], adam_d[2], adam_d[3] if adam_d[3] is not None else eps)
     ag = Adam(adam_g[0], adam_g[1], adam_g[2], adam_g[3] if adam_g[3] is not None else eps)
     return Config(PARAGAN_ABI_VERSION, resolution, ch, n_classes, shared_dim, z_chunk, attn_res, local_batch,
-                  d_steps_per_g, compute, c_pad_image, ad, ag, sn_eps, bn_eps, rank, world_size, device, seed)
+                  d_steps_per_g, compute, c_pad_image, ad, ag, sn_eps, bn_eps, rank, world_size, device, seed, arch)
+
+
+def make_sndcgan_config(ch=32, n_classes=10, local_batch=8, d_steps_per_g=1, **kw) -> Config:
+    """Config 1: SN-DCGAN 32x32 (R25), fp32."""
+    return make_config(resolution=32, ch=ch, n_classes=n_classes, shared_dim=1, z_chunk=1, attn_res=0,
+                       local_batch=local_batch, d_steps_per_g=d_steps_per_g, compute=F32, arch=ARCH_SNDCGAN, **kw)
 
 
 def dim_z(cfg: Config) -> int:
+    if cfg.arch == ARCH_SNDCGAN:
+        return 128
     nb = {16: 2, 32: 3, 64: 4, 128: 5, 256: 6, 512: 7}[cfg.resolution]
     return (nb + 1) * cfg.z_chunk
 

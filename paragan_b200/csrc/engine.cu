@@ -214,6 +214,7 @@ class Engine final : public EngineBase {
   Engine(const paragan_config& c, cudaStream_t st) : cfg_(c), st_(st) {
     const char* sp = std::getenv("PARAGAN_SUBPIXEL");
     subpix_ = kBF && (sp == nullptr || std::atoi(sp) != 0);
+    dcgan_ = c.arch == PARAGAN_ARCH_SNDCGAN;
   }
   ~Engine() override {
     if (comm_) ncclCommDestroy(comm_);
@@ -272,10 +273,14 @@ class Engine final : public EngineBase {
       for (auto& e : N->E) {
         float* p = N->P((int)(&e - N->E.data()));
         const std::string& nm = e.name;
-        const bool is_bias = nm.size() >= 2 && (nm.compare(nm.size() - 2, 2, ".b") == 0 || nm == "out_bn.beta");
+        auto ends = [&](const char* suf) {
+          const size_t l = std::strlen(suf);
+          return nm.size() >= l && nm.compare(nm.size() - l, l, suf) == 0;
+        };
+        const bool is_bias = ends(".b") || ends(".beta");
         if (nm.find("gamma") != std::string::npos && nm.find("attn") != std::string::npos) {
           CK(fill_const(p, e.n, attn_gamma, st_));
-        } else if (nm == "out_bn.gamma") {
+        } else if (ends(".gamma")) {   // BN gains
           CK(fill_const(p, e.n, 1.0f, st_));
         } else if (is_bias) {
           CK(fill_const(p, e.n, 0.0f, st_));
@@ -343,7 +348,8 @@ class Engine final : public EngineBase {
     // SN(G) + G forward (no grad) writes fakes into D-input rows [0, B)
     CKS(sn_forward(G_, false));
     CKS(fold_subpixel());
-    CKS(g_forward(z, fake_y, false));
+    if (dcgan_) CKS(g_forward_dc(z));
+    else CKS(g_forward(z, fake_y, false));
     // reals into rows [B, 2B) (one D pass over the concatenated batch)
     const size_t img_bytes = (size_t)B_ * R_ * R_ * cpad_ * sizeof(T);
     if (cudaMemcpyAsync(static_cast<char*>(dimg_) + img_bytes, real, img_bytes, cudaMemcpyDeviceToDevice, st_))
@@ -351,12 +357,14 @@ class Engine final : public EngineBase {
     CK(cudaMemcpyAsync(ylab_, fake_y, sizeof(int32_t) * B_, cudaMemcpyDeviceToDevice, st_));
     CK(cudaMemcpyAsync(ylab_ + B_, real_y, sizeof(int32_t) * B_, cudaMemcpyDeviceToDevice, st_));
     CKS(sn_forward(D_, true));
-    CKS(d_forward(2 * B_));
+    if (dcgan_) CKS(d_forward_dc(2 * B_));
+    else CKS(d_forward(2 * B_));
     CK(hinge_loss(logits_, B_, 0, dlogits_, D_.loss, st_));
     ++launches_;
     CKS(allreduce_loss(D_.loss));
     CK(cudaMemsetAsync(D_.g, 0, sizeof(float) * D_.n, st_));
-    CKS(d_backward(2 * B_, true, false));
+    if (dcgan_) CKS(d_backward_dc(2 * B_, true, false));
+    else CKS(d_backward(2 * B_, true, false));
     CKS(sn_backward_net(D_));
     if (!(flags & PARAGAN_FLAG_NO_ALLREDUCE)) CKS(allreduce(PARAGAN_NET_D));
     if (!(flags & PARAGAN_FLAG_NO_UPDATE)) CKS(update(PARAGAN_NET_D));
@@ -373,16 +381,23 @@ class Engine final : public EngineBase {
     if (!z || !y) return fail_arg("g_step: bad pointer");
     CKS(sn_forward(G_, true));
     CKS(fold_subpixel());
-    CKS(g_forward(z, y, true));
+    if (dcgan_) CKS(g_forward_dc(z));
+    else CKS(g_forward(z, y, true));
     CK(cudaMemcpyAsync(ylab_, y, sizeof(int32_t) * B_, cudaMemcpyDeviceToDevice, st_));
     CKS(sn_forward(D_, true));
-    CKS(d_forward(B_));
+    if (dcgan_) CKS(d_forward_dc(B_));
+    else CKS(d_forward(B_));
     CK(hinge_loss(logits_, B_, 1, dlogits_, G_.loss, st_));
     ++launches_;
     CKS(allreduce_loss(G_.loss));
     CK(cudaMemsetAsync(G_.g, 0, sizeof(float) * G_.n, st_));
-    CKS(d_backward(B_, false, true));   // dgrad only, down to the image
-    CKS(g_backward());
+    if (dcgan_) {
+      CKS(d_backward_dc(B_, false, true));   // dgrad only, down to the image
+      CKS(g_backward_dc());
+    } else {
+      CKS(d_backward(B_, false, true));   // dgrad only, down to the image
+      CKS(g_backward());
+    }
     CKS(sn_backward_net(G_));
     if (!(flags & PARAGAN_FLAG_NO_ALLREDUCE)) CKS(allreduce(PARAGAN_NET_G));
     if (!(flags & PARAGAN_FLAG_NO_UPDATE)) CKS(update(PARAGAN_NET_G));
@@ -557,11 +572,90 @@ class Engine final : public EngineBase {
     return a;
   }
 
+  // SN bookkeeping (u / v offsets, job ids) and the flat parameter / optimiser buffers of both nets
+  void finalize_nets(Arena& A) {
+    // u / v offsets
+    for (Net* N : {&G_, &D_}) {
+      N->nu = 0;
+      N->nv = 0;
+      N->sn_entries.clear();
+      for (auto& e : N->E)
+        if (e.sn) {
+          e.u_off = N->nu;
+          N->nu += e.shape[0];
+          e.v_off = N->nv;
+          N->nv += e.n / e.shape[0];
+          e.job = (int)N->sn_entries.size();
+          N->sn_entries.push_back((int)(&e - N->E.data()));
+        }
+    }
+    // ---------------- device memory
+    for (Net* N : {&G_, &D_}) {
+      N->p = A.get<float>(N->n);
+      N->g = A.get<float>(N->n);
+      N->m = A.get<float>(N->n);
+      N->v = A.get<float>(N->n);
+      N->u = A.get<float>(N->nu);
+      N->sn_s = A.get<float>(N->nu);
+      N->sn_v = A.get<float>(N->nv);
+      N->sn_t = A.get<float>(N->nv);
+      N->sigma = A.get<float>(2 * N->sn_entries.size());
+      N->t_dev = A.get<long long>(1);
+      N->flag = A.get<int>(1);
+      N->loss = A.get<float>(4);
+    }
+    nonfinite_sticky_ = A.get<int>(1);
+  }
+  // device tables of the grouped SN power iteration / backward and the SN pack lists
+  void alloc_sn_tables(Arena& A) {
+    // tables
+    for (Net* N : {&G_, &D_}) {
+      N->jobs_d = A.get<SnJob>(N->sn_entries.size());
+      long long nb1 = 0, nb1b = 0, nb2 = 0, npart = 0, nbw = 0;
+      for (int ei : N->sn_entries) {
+        const PEntry& e = N->E[ei];
+        const long long K = e.n / e.shape[0];
+        const int nrc = ceil_div(e.shape[0], 128);
+        nb1 += ceil_div(K, 256) * nrc;
+        nb1b += ceil_div(K, 256);
+        nb2 += ceil_div(e.shape[0], 8);
+        npart += nrc * K;
+        nbw += ceil_div(e.n, 4096);
+      }
+      N->nb1 = (int)nb1;
+      N->nb1b = (int)nb1b;
+      N->nb2 = (int)nb2;
+      N->npart = npart;
+      N->snb_blocks = nbw;
+      N->b1_job = A.get<int>(nb1);
+      N->b1_k0 = A.get<int>(nb1);
+      N->b1_rc = A.get<int>(nb1);
+      N->b1b_job = A.get<int>(nb1b);
+      N->b1b_k0 = A.get<int>(nb1b);
+      N->b2_job = A.get<int>(nb2);
+      N->b2_r0 = A.get<int>(nb2);
+      N->sn_part = A.get<float>(npart);
+      N->sn_coef = A.get<double>(N->sn_entries.size());
+      N->sn_dotp = A.get<double>(nbw);
+      N->snb_start = A.get<long long>(N->sn_entries.size());
+      N->snb_idx = A.get<int>(N->sn_entries.size());
+      N->snb_grad = A.get<float*>(N->sn_entries.size());
+      N->pf_d = A.get<SnPack>(64 + N->sn_entries.size() * 2);
+      N->pb_d = A.get<SnPack>(64 + N->sn_entries.size() * 2);
+      N->pf_start = A.get<long long>(64 + N->sn_entries.size() * 2);
+      N->pb_start = A.get<long long>(64 + N->sn_entries.size() * 2);
+    }
+  }
+
   void build(Arena& A) {
     G_ = Net();
     D_ = Net();
     gb_.clear();
     db_.clear();
+    if (dcgan_) {
+      build_dcgan(A);
+      return;
+    }
     const int ch = cfg_.ch;
     B_ = cfg_.local_batch;
     R_ = cfg_.resolution;
@@ -632,37 +726,7 @@ class Engine final : public EngineBase {
     hl_ = h;
     dlin_ = lin(D_, "linear", cdl_, 1, true, true);
     demb_ = D_.add("embed", {cfg_.n_classes, cdl_}, false, true);
-    // u / v offsets
-    for (Net* N : {&G_, &D_}) {
-      N->nu = 0;
-      N->nv = 0;
-      N->sn_entries.clear();
-      for (auto& e : N->E)
-        if (e.sn) {
-          e.u_off = N->nu;
-          N->nu += e.shape[0];
-          e.v_off = N->nv;
-          N->nv += e.n / e.shape[0];
-          e.job = (int)N->sn_entries.size();
-          N->sn_entries.push_back((int)(&e - N->E.data()));
-        }
-    }
-    // ---------------- device memory
-    for (Net* N : {&G_, &D_}) {
-      N->p = A.get<float>(N->n);
-      N->g = A.get<float>(N->n);
-      N->m = A.get<float>(N->n);
-      N->v = A.get<float>(N->n);
-      N->u = A.get<float>(N->nu);
-      N->sn_s = A.get<float>(N->nu);
-      N->sn_v = A.get<float>(N->nv);
-      N->sn_t = A.get<float>(N->nv);
-      N->sigma = A.get<float>(2 * N->sn_entries.size());
-      N->t_dev = A.get<long long>(1);
-      N->flag = A.get<int>(1);
-      N->loss = A.get<float>(4);
-    }
-    nonfinite_sticky_ = A.get<int>(1);
+    finalize_nets(A);
     const size_t wsz = kBF ? 2 : 4;
     auto alloc_conv = [&](ConvL& c) {
       const size_t nw = (size_t)c.cout * c.ksz * c.ksz * c.cin_x;
@@ -819,43 +883,7 @@ class Engine final : public EngineBase {
     scratch_f_ = A.get<float>(sf);
     wg_scratch_ = A.get<float>((size_t)16 << 20);   // padded / qkv weight-gradient staging
     dpool_ = A.get<float>(std::max<size_t>(dpool_floats_, 1));
-    // tables
-    for (Net* N : {&G_, &D_}) {
-      N->jobs_d = A.get<SnJob>(N->sn_entries.size());
-      long long nb1 = 0, nb1b = 0, nb2 = 0, npart = 0, nbw = 0;
-      for (int ei : N->sn_entries) {
-        const PEntry& e = N->E[ei];
-        const long long K = e.n / e.shape[0];
-        const int nrc = ceil_div(e.shape[0], 128);
-        nb1 += ceil_div(K, 256) * nrc;
-        nb1b += ceil_div(K, 256);
-        nb2 += ceil_div(e.shape[0], 8);
-        npart += nrc * K;
-        nbw += ceil_div(e.n, 4096);
-      }
-      N->nb1 = (int)nb1;
-      N->nb1b = (int)nb1b;
-      N->nb2 = (int)nb2;
-      N->npart = npart;
-      N->snb_blocks = nbw;
-      N->b1_job = A.get<int>(nb1);
-      N->b1_k0 = A.get<int>(nb1);
-      N->b1_rc = A.get<int>(nb1);
-      N->b1b_job = A.get<int>(nb1b);
-      N->b1b_k0 = A.get<int>(nb1b);
-      N->b2_job = A.get<int>(nb2);
-      N->b2_r0 = A.get<int>(nb2);
-      N->sn_part = A.get<float>(npart);
-      N->sn_coef = A.get<double>(N->sn_entries.size());
-      N->sn_dotp = A.get<double>(nbw);
-      N->snb_start = A.get<long long>(N->sn_entries.size());
-      N->snb_idx = A.get<int>(N->sn_entries.size());
-      N->snb_grad = A.get<float*>(N->sn_entries.size());
-      N->pf_d = A.get<SnPack>(64 + N->sn_entries.size() * 2);
-      N->pb_d = A.get<SnPack>(64 + N->sn_entries.size() * 2);
-      N->pf_start = A.get<long long>(64 + N->sn_entries.size() * 2);
-      N->pb_start = A.get<long long>(64 + N->sn_entries.size() * 2);
-    }
+    alloc_sn_tables(A);
     // chain G block inputs (block i+1 reads block i's output, or the attention output, in place)
     for (size_t i = 1; i < gb_.size(); ++i) gb_[i].x = gb_[i - 1].attn ? attn_out_[0] : gb_[i - 1].out;
     gout_in_ = gb_.back().attn ? attn_out_[0] : gb_.back().out;
@@ -943,7 +971,7 @@ class Engine final : public EngineBase {
   }
 
   paragan_status upload_tables() {
-    CKS(upload_cbn_tables());
+    if (!dcgan_) CKS(upload_cbn_tables());
     for (Net* N : {&G_, &D_}) {
       std::vector<SnJob> jobs;
       std::vector<int> b1j, b1k, b1r, b1bj, b1bk, b2j, b2r;
@@ -1050,6 +1078,10 @@ class Engine final : public EngineBase {
       add_conv(N, a.oc);
     };
     G_.pf_h.clear(); G_.pb_h.clear(); D_.pf_h.clear(); D_.pb_h.clear();
+    if (dcgan_) {
+      for (auto& L : dcd_) add_conv(D_, L.c);
+      add_lin(D_, dlin_);
+    } else {
     add_lin(G_, glin_);
     for (auto& b : gb_) {
       add_lin(G_, b.g1); add_lin(G_, b.b1); add_lin(G_, b.g2); add_lin(G_, b.b2);
@@ -1071,6 +1103,7 @@ class Engine final : public EngineBase {
       e.out = cfg_.n_classes;
       e.what = demb_hat_;
       add_lin(D_, e);
+    }
     }
     for (Net* N : {&G_, &D_}) {
       for (int pass = 0; pass < 2; ++pass) {
@@ -1094,6 +1127,7 @@ class Engine final : public EngineBase {
 
   // ------------------------------------------------------------------ SN forward (A2)
   paragan_status sn_forward(Net& N, bool need_dgrad) {
+    if (N.sn_entries.empty()) return PARAGAN_OK;
     CK(sn_power(N.jobs_d, (int)N.sn_entries.size(), N.b1_job, N.b1_k0, N.b1_rc, N.nb1, N.b1b_job, N.b1b_k0, N.nb1b,
                 N.b2_job, N.b2_r0, N.nb2, st_));
     launches_ += 3;
@@ -1115,6 +1149,7 @@ class Engine final : public EngineBase {
     return PARAGAN_OK;
   }
   paragan_status sn_backward_net(Net& N) {
+    if (N.sn_entries.empty()) return PARAGAN_OK;
     CK(sn_backward(N.jobs_d, (int)N.sn_entries.size(), N.snb_start, N.snb_blocks, N.sn_dotp, st_));
     launches_ += 2;
     return PARAGAN_OK;
@@ -1375,6 +1410,263 @@ class Engine final : public EngineBase {
     return PARAGAN_OK;
   }
 
+
+  // ================================================================== SN-DCGAN (config 1; R25; fp32 SIMT)
+  struct DcD {          // D conv: SN'd, bias, LeakyReLU 0.1
+    ConvL c;
+    int k = 3, s = 1, hin = 0, hout = 0;
+    float *pre = nullptr, *act = nullptr;
+  };
+  struct DcG {          // G deconv 4x4 s2 p1 (no SN) + BN (learned gamma/beta, cross-replica) + ReLU
+    int w = -1, b = -1, g = -1, be = -1;
+    int cin = 0, cout = 0, hin = 0, hout = 0;
+    float *pre = nullptr, *act = nullptr, *mean = nullptr, *rstd = nullptr;
+    double* sums = nullptr;
+  };
+  std::vector<DcD> dcd_;
+  std::vector<DcG> dcg_;
+  int dc_lin_w_ = -1, dc_lin_b_ = -1, dc_bn0_g_ = -1, dc_bn0_b_ = -1, dc_out_w_ = -1, dc_out_b_ = -1, dc_f0_ = 0;
+  float *dc_h0_ = nullptr, *dc_a0_ = nullptr, *dc_mean0_ = nullptr, *dc_rstd0_ = nullptr, *dc_tmpw_ = nullptr;
+  float* dc_g_[2] = {nullptr, nullptr};
+  double* dc_sums0_ = nullptr;
+  float* dc_z_ = nullptr;
+  static constexpr float kLrelu = 0.1f;
+
+  void build_dcgan(Arena& A) {
+    const int ch = cfg_.ch;
+    B_ = cfg_.local_batch;
+    R_ = 32;
+    cpad_ = cfg_.c_pad_image;
+    dimz_ = 128;
+    const int gw[4] = {8 * ch, 4 * ch, 2 * ch, ch};
+    const int dw[7] = {ch, ch, 2 * ch, 2 * ch, 4 * ch, 4 * ch, 8 * ch};
+    const int dk[7] = {3, 4, 3, 4, 3, 4, 3}, dst[7] = {1, 2, 1, 2, 1, 2, 1};
+    dc_f0_ = 16 * gw[0];
+    // G, canonical order (no SN); the deconv weight [C_in, C_out, 4, 4] is stored OHWI = [C_in][4][4][C_out],
+    // i.e. exactly the conv weight whose adjoint the deconv is
+    dc_lin_w_ = G_.add("linear.w", {dc_f0_, dimz_}, false, false);
+    dc_lin_b_ = G_.add("linear.b", {dc_f0_}, false, false);
+    dc_bn0_g_ = G_.add("bn0.gamma", {dc_f0_}, false, false);
+    dc_bn0_b_ = G_.add("bn0.beta", {dc_f0_}, false, false);
+    dcg_.clear();
+    int h = 4;
+    for (int i = 0; i < 3; ++i) {
+      DcG L;
+      L.cin = gw[i];
+      L.cout = gw[i + 1];
+      L.hin = h;
+      L.hout = 2 * h;
+      const std::string k = std::to_string(i + 1);
+      L.w = G_.add("deconv" + k + ".w", {L.cin, L.cout, 4, 4}, true, false);
+      L.b = G_.add("deconv" + k + ".b", {L.cout}, false, false);
+      L.g = G_.add("bn" + k + ".gamma", {L.cout}, false, false);
+      L.be = G_.add("bn" + k + ".beta", {L.cout}, false, false);
+      dcg_.push_back(L);
+      h *= 2;
+    }
+    dc_out_w_ = G_.add("out_conv.w", {3, gw[3], 3, 3}, true, false);
+    dc_out_b_ = G_.add("out_conv.b", {3}, false, false);
+    cl_ = gw[3];
+    // D, canonical order (SN on every layer)
+    dcd_.clear();
+    h = R_;
+    int cin = 3;
+    for (int i = 0; i < 7; ++i) {
+      DcD L;
+      L.k = dk[i];
+      L.s = dst[i];
+      L.hin = h;
+      L.hout = h / dst[i];
+      L.c = conv(D_, "conv" + std::to_string(i + 1), cin, i == 0 ? cpad_ : cin, dw[i], dk[i], true, true);
+      dcd_.push_back(L);
+      cin = dw[i];
+      h = L.hout;
+    }
+    cdl_ = 16 * dw[6];
+    dlin_ = lin(D_, "linear", cdl_, 1, true, true);
+    finalize_nets(A);
+    size_t maxw = 0;
+    for (auto& L : dcd_) {
+      const size_t nw = (size_t)L.c.cout * L.c.ksz * L.c.ksz * L.c.cin_x;
+      L.c.wp = A.get<float>(nw);
+      L.c.wt = A.get<float>(nw);
+      maxw = std::max(maxw, nw);
+    }
+    dlin_.what = A.get<float>((size_t)dlin_.in * dlin_.out);
+    dc_tmpw_ = A.get<float>(maxw);
+    // activations (fp32)
+    const int B = B_, B2 = 2 * B_;
+    dimg_ = A.get<float>((size_t)B2 * R_ * R_ * cpad_);
+    ylab_ = A.get<int32_t>(B2);
+    long long big = (long long)B2 * R_ * R_ * cpad_;
+    for (auto& L : dcd_) {
+      const long long e = (long long)B2 * L.hout * L.hout * L.c.cout;
+      L.pre = A.get<float>(e);
+      L.act = A.get<float>(e);
+      big = std::max(big, e);
+    }
+    dc_z_ = A.get<float>((size_t)B * dimz_);
+    dc_h0_ = A.get<float>((size_t)B * dc_f0_);
+    dc_a0_ = A.get<float>((size_t)B * dc_f0_);
+    dc_mean0_ = A.get<float>(dc_f0_);
+    dc_rstd0_ = A.get<float>(dc_f0_);
+    dc_sums0_ = A.get<double>(2 * dc_f0_);
+    for (auto& L : dcg_) {
+      const long long e = (long long)B * L.hout * L.hout * L.cout;
+      L.pre = A.get<float>(e);
+      L.act = A.get<float>(e);
+      L.mean = A.get<float>(L.cout);
+      L.rstd = A.get<float>(L.cout);
+      L.sums = A.get<double>(2 * L.cout);
+      big = std::max(big, e);
+    }
+    big = std::max(big, (long long)B * dc_f0_);
+    aout_ = dcg_.back().act;
+    pre_ = A.get<float>((size_t)B * R_ * R_ * 3);
+    img_ = A.get<float>((size_t)B * R_ * R_ * 3);
+    dpre_ = A.get<float>((size_t)B * R_ * R_ * 3);
+    for (int i = 0; i < 2; ++i) dc_g_[i] = A.get<float>((size_t)big);
+    feat_ = dcd_.back().act;
+    logits_ = A.get<float>(B2);
+    dlogits_ = A.get<float>(B2);
+    maxc_ = dc_f0_;
+    ones_buf_ = A.get<float>(maxc_);
+    tot_ = A.get<double>(4 * maxc_);
+    dpart_ = A.get<double>((size_t)kMaxPartialBlocks * 2 * maxc_);
+    scratch_floats_ = std::max<size_t>((size_t)std::max(G_.n, D_.n), (size_t)B * 3 * R_ * R_);
+    scratch_floats_ = std::max<size_t>(scratch_floats_, (size_t)4 * 148 * 27 * cl_);
+    scratch_f_ = A.get<float>(scratch_floats_);
+    alloc_sn_tables(A);
+  }
+
+  // cross-replica BN (learned gamma/beta) over [M][C] rows, then ReLU
+  paragan_status dc_bn_forward(const float* x, long long M, int C, double* sums, float* mean, float* rstd,
+                               const float* gamma, const float* beta, float* y) {
+    CK(bn_sums_generic(x, M, C, sums, st_));
+    CKS(allreduce_small(sums, 2 * C));
+    CK(bn_finalize(sums, C, (double)M * cfg_.world_size, cfg_.bn_eps, mean, rstd, st_));
+    CK(bn_apply_generic(x, M, C, mean, rstd, gamma, beta, 1, y, st_));
+    launches_ += 3;
+    return PARAGAN_OK;
+  }
+  // its backward: dy is the gradient of the ReLU output; writes dgamma / dbeta (local sums) and dx
+  paragan_status dc_bn_backward(const float* x, const float* dy, long long M, int C, const float* mean,
+                                const float* rstd, int g_entry, int b_entry, float* dx) {
+    CK(bn_bwd_sums_generic(x, dy, M, C, mean, rstd, G_.P(g_entry), G_.P(b_entry), 1, tot_, G_.G(g_entry),
+                           G_.G(b_entry), st_));
+    CKS(allreduce_small(tot_, 2 * C));
+    CK(bn_bwd_apply_generic(x, dy, M, C, mean, rstd, G_.P(g_entry), G_.P(b_entry), 1, tot_,
+                            (double)M * cfg_.world_size, dx, st_));
+    launches_ += 2;
+    return PARAGAN_OK;
+  }
+
+  paragan_status g_forward_dc(const float* z) {
+    const int B = B_;
+    CK(cudaMemcpyAsync(zin_dc(), z, sizeof(float) * B * dimz_, cudaMemcpyDeviceToDevice, st_));
+    // linear 128 -> 16*8ch, per-feature BN (the [B,1,1,F] view), ReLU; the F vector is NHWC [4,4,8ch] (R10)
+    CK(gemm_f32(B, dc_f0_, dimz_, zin_dc(), dimz_, 1, G_.P(dc_lin_w_), dimz_, 1, dc_h0_, dc_f0_, 0.0f,
+                G_.P(dc_lin_b_), st_));
+    CKS(dc_bn_forward(dc_h0_, B, dc_f0_, dc_sums0_, dc_mean0_, dc_rstd0_, G_.P(dc_bn0_g_), G_.P(dc_bn0_b_),
+                      dc_a0_));
+    const float* x = dc_a0_;
+    for (auto& L : dcg_) {
+      // deconv = adjoint of the stride-2 conv with the same weight (OHWI [cin][4][4][cout]), plus bias
+      CK(gconv_dgrad(x, B, L.hin, L.hin, L.cin, G_.P(L.w), L.cout, L.cout, 4, 2, 1, L.hout, L.hout, G_.P(L.b),
+                     L.pre, st_));
+      CKS(dc_bn_forward(L.pre, (long long)B * L.hout * L.hout, L.cout, L.sums, L.mean, L.rstd, G_.P(L.g),
+                        G_.P(L.be), L.act));
+      x = L.act;
+      launches_ += 1;
+    }
+    CK(thin_conv_fwd(x, B, R_, R_, cl_, G_.P(dc_out_w_), 3, G_.P(dc_out_b_), pre_, st_));
+    CK(tanh_to_image<T>(pre_, img_, static_cast<T*>(dimg_), (long long)B * R_ * R_, cpad_, st_));
+    launches_ += 3;
+    return PARAGAN_OK;
+  }
+  float* zin_dc() { return dc_z_; }
+
+  paragan_status d_forward_dc(int n) {
+    const float* x = static_cast<const float*>(dimg_);
+    for (auto& L : dcd_) {
+      CK(gconv_fwd(x, n, L.hin, L.hin, L.c.cin_x, static_cast<const float*>(L.c.wp), L.c.cin_x, L.c.cout, L.k, L.s,
+                   1, L.hout, L.hout, D_.P(L.c.b), L.pre, st_));
+      CK(lrelu_fwd(L.pre, L.act, (long long)n * L.hout * L.hout * L.c.cout, kLrelu, st_));
+      x = L.act;
+      launches_ += 2;
+    }
+    // logits = SN-linear(flatten NHWC) + b
+    CK(gemm_f32(n, 1, cdl_, feat_, cdl_, 1, dlin_.what, cdl_, 1, logits_, 1, 0.0f, D_.P(dlin_.b), st_));
+    ++launches_;
+    return PARAGAN_OK;
+  }
+
+  paragan_status d_backward_dc(int n, bool want_w, bool want_dimg) {
+    float* g = dc_g_[0];
+    float* other = dc_g_[1];
+    if (want_w) {   // head: dW = dlogit^T feat, db = sum dlogit
+      CK(gemm_f32(1, cdl_, n, dlogits_, 1, 1, feat_, 1, cdl_, D_.G(dlin_.w), cdl_, 0.0f, nullptr, st_));
+      CK(col_sum<float>(dlogits_, n, 1, dpart_, kMaxPartialBlocks, D_.G(dlin_.b), 0, st_));
+    }
+    // dfeat[n][k] = dlogit[n] * W_hat[0][k]
+    CK(gemm_f32(n, cdl_, 1, dlogits_, 1, 1, dlin_.what, 1, 1, g, cdl_, 0.0f, nullptr, st_));
+    for (int i = (int)dcd_.size() - 1; i >= 0; --i) {
+      DcD& L = dcd_[i];
+      const long long no = (long long)n * L.hout * L.hout * L.c.cout;
+      CK(lrelu_bwd(g, L.pre, other, no, kLrelu, st_));
+      std::swap(g, other);   // g = d pre
+      const float* xin = i == 0 ? static_cast<const float*>(dimg_) : dcd_[i - 1].act;
+      if (want_w) {
+        const bool pad = L.c.cin_x != L.c.cin;
+        float* dst = pad ? dc_tmpw_ : D_.G(L.c.w);
+        CK(gconv_wgrad(xin, n, L.hin, L.hin, L.c.cin_x, g, L.hout, L.hout, L.c.cout, L.k, L.s, 1, dst, st_));
+        if (pad)
+          CK(copy_rows_cols(dst, L.c.cin_x, (long long)L.c.cout * L.k * L.k, L.c.cin, D_.G(L.c.w), L.c.cin, 0, st_));
+        CK(col_sum<float>(g, (long long)n * L.hout * L.hout, L.c.cout, dpart_, kMaxPartialBlocks, D_.G(L.c.b), 0, st_));
+        launches_ += 3;
+      }
+      if (i > 0 || want_dimg) {
+        CK(gconv_dgrad(g, n, L.hout, L.hout, L.c.cout, static_cast<const float*>(L.c.wp), L.c.cin_x, L.c.cin_x, L.k,
+                       L.s, 1, L.hin, L.hin, nullptr, other, st_));
+        std::swap(g, other);
+        ++launches_;
+      }
+    }
+    dimg_grad_ = want_dimg ? g : nullptr;   // [n][32][32][c_pad] gradient of the D input
+    return PARAGAN_OK;
+  }
+
+  paragan_status g_backward_dc() {
+    const int B = B_;
+    const long long M = (long long)B * R_ * R_;
+    CK(tanh_bwd<T>(static_cast<const T*>(dimg_grad_), cpad_, img_, dpre_, M, st_));
+    CK(thin_conv_wgrad(aout_, dpre_, B, R_, R_, cl_, 3, G_.G(dc_out_w_), scratch_f_, scratch_floats_, st_));
+    CK(col_sum<float>(dpre_, M, 3, dpart_, kMaxPartialBlocks, G_.G(dc_out_b_), 0, st_));
+    float* g = (dimg_grad_ == dc_g_[0]) ? dc_g_[1] : dc_g_[0];
+    float* other = (g == dc_g_[0]) ? dc_g_[1] : dc_g_[0];
+    CK(thin_conv_dgrad(dpre_, B, R_, R_, cl_, G_.P(dc_out_w_), 3, g, st_));
+    launches_ += 4;
+    for (int i = (int)dcg_.size() - 1; i >= 0; --i) {
+      DcG& L = dcg_[i];
+      const long long Mo = (long long)B * L.hout * L.hout;
+      CKS(dc_bn_backward(L.pre, g, Mo, L.cout, L.mean, L.rstd, L.g, L.be, other));
+      std::swap(g, other);   // g = d(deconv output)
+      const float* xin = i == 0 ? dc_a0_ : dcg_[i - 1].act;
+      // deconv wgrad: the conv wgrad with the roles of input and output exchanged
+      CK(gconv_wgrad(g, B, L.hout, L.hout, L.cout, xin, L.hin, L.hin, L.cin, 4, 2, 1, G_.G(L.w), st_));
+      CK(col_sum<float>(g, Mo, L.cout, dpart_, kMaxPartialBlocks, G_.G(L.b), 0, st_));
+      // deconv input gradient = the strided conv of g with the same weight
+      CK(gconv_fwd(g, B, L.hout, L.hout, L.cout, G_.P(L.w), L.cout, L.cin, 4, 2, 1, L.hin, L.hin, nullptr, other, st_));
+      std::swap(g, other);
+      launches_ += 3;
+    }
+    CKS(dc_bn_backward(dc_h0_, g, B, dc_f0_, dc_mean0_, dc_rstd0_, dc_bn0_g_, dc_bn0_b_, other));
+    // linear: dW = dh0^T z, db = sum dh0
+    CK(gemm_f32(dc_f0_, dimz_, B, other, 1, dc_f0_, zin_dc(), 1, dimz_, G_.G(dc_lin_w_), dimz_, 0.0f, nullptr, st_));
+    CK(col_sum<float>(other, B, dc_f0_, dpart_, kMaxPartialBlocks, G_.G(dc_lin_b_), 0, st_));
+    launches_ += 2;
+    return PARAGAN_OK;
+  }
   // ------------------------------------------------------------------ attention (A6)
   TcAttnArgs attn_args(const AttnL& a, int n) {
     TcAttnArgs t{};
@@ -1773,6 +2065,7 @@ class Engine final : public EngineBase {
   cublasHandle_t cublas_ = nullptr;
   bool ready_ = false, poisoned_ = false, planned_ = false, ones_ready_ = false;
   bool subpix_ = false;   // G conv1 as four phase 2x2 convs of the low-resolution input (NEXT-1)
+  bool dcgan_ = false;    // SN-DCGAN (config 1) instead of BigGAN
   int d_since_g_ = 0;
   uint64_t launches_ = 0;
   Net G_, D_;
@@ -1836,6 +2129,14 @@ cudaError_t Engine<T>::d2f(const double* s, float* d, int n, cudaStream_t st) {
 paragan_status validate_config(const paragan_config* c) {
   if (!c) return PARAGAN_ERR_INVALID_ARG;
   if (c->abi_version != PARAGAN_ABI_VERSION) return PARAGAN_ERR_CONFIG;
+  if (c->arch == PARAGAN_ARCH_SNDCGAN) {   // config 1 (R25): 32x32, fp32 SIMT path
+    if (c->resolution != 32 || c->compute != PARAGAN_F32 || c->ch < 1 || c->ch % 4 || c->local_batch < 1 ||
+        c->d_steps_per_g < 1 || c->world_size < 1 || c->rank < 0 || c->rank >= c->world_size || c->n_classes < 1 ||
+        c->c_pad_image < 3 || !(c->sn_eps > 0) || !(c->bn_eps > 0))
+      return PARAGAN_ERR_CONFIG;
+    return PARAGAN_OK;
+  }
+  if (c->arch != PARAGAN_ARCH_BIGGAN) return PARAGAN_ERR_CONFIG;
   Arch a;
   if (!arch_for(c->resolution, a)) return PARAGAN_ERR_CONFIG;
   if (c->ch < 1 || c->n_classes < 1 || c->shared_dim < 1 || c->z_chunk < 1 || c->local_batch < 1 ||

@@ -2267,6 +2267,237 @@ cudaError_t fold_up2_weights(const float* w, const float* inv_sigma, int Cout, i
   return cudaGetLastError();
 }
 
+// ===================================================================== SN-DCGAN generic fp32 kernels
+namespace {
+__global__ void k_gconv_fwd(const float* __restrict__ x, int N, int H, int W, int Cin, const float* __restrict__ w,
+                            int ldw, int Cout, int k, int s, int p, int Ho, int Wo, const float* __restrict__ bias,
+                            float* __restrict__ y) {
+  const long long total = (long long)N * Ho * Wo * Cout;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const int co = (int)(i % Cout);
+    long long r = i / Cout;
+    const int ox = (int)(r % Wo);
+    r /= Wo;
+    const int oy = (int)(r % Ho);
+    const int n = (int)(r / Ho);
+    // fp64 accumulation: this config-1 path is the exact reference-grade SIMT path (R25)
+    double acc = bias ? bias[co] : 0.0;
+    for (int ky = 0; ky < k; ++ky) {
+      const int iy = oy * s - p + ky;
+      if (iy < 0 || iy >= H) continue;
+      for (int kx = 0; kx < k; ++kx) {
+        const int ix = ox * s - p + kx;
+        if (ix < 0 || ix >= W) continue;
+        const float* xp = x + (((long long)n * H + iy) * W + ix) * Cin;
+        const float* wp = w + ((long long)(co * k + ky) * k + kx) * ldw;
+        for (int ci = 0; ci < Cin; ++ci) acc += (double)xp[ci] * wp[ci];
+      }
+    }
+    y[i] = (float)acc;
+  }
+}
+__global__ void k_gconv_dgrad(const float* __restrict__ dy, int N, int Ho, int Wo, int Cout,
+                              const float* __restrict__ w, int ldw, int Cin, int k, int s, int p, int H, int W,
+                              const float* __restrict__ bias, float* __restrict__ dx) {
+  const long long total = (long long)N * H * W * Cin;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const int ci = (int)(i % Cin);
+    long long r = i / Cin;
+    const int ix = (int)(r % W);
+    r /= W;
+    const int iy = (int)(r % H);
+    const int n = (int)(r / H);
+    double acc = bias ? bias[ci] : 0.0;
+    for (int ky = 0; ky < k; ++ky) {
+      const int ty = iy + p - ky;
+      if (ty < 0 || ty % s) continue;
+      const int oy = ty / s;
+      if (oy >= Ho) continue;
+      for (int kx = 0; kx < k; ++kx) {
+        const int tx = ix + p - kx;
+        if (tx < 0 || tx % s) continue;
+        const int ox = tx / s;
+        if (ox >= Wo) continue;
+        const float* dp = dy + (((long long)n * Ho + oy) * Wo + ox) * Cout;
+        for (int co = 0; co < Cout; ++co) acc += (double)dp[co] * w[((long long)(co * k + ky) * k + kx) * ldw + ci];
+      }
+    }
+    dx[i] = (float)acc;
+  }
+}
+// one block per weight element group: thread-strided sum over pixels in fp64, block reduce
+__global__ void k_gconv_wgrad(const float* __restrict__ x, int N, int H, int W, int Cin, const float* __restrict__ dy,
+                              int Ho, int Wo, int Cout, int k, int s, int p, float* __restrict__ dw) {
+  __shared__ double red[256];
+  const long long widx = blockIdx.x;   // (co, ky, kx, ci)
+  const int ci = (int)(widx % Cin);
+  long long r = widx / Cin;
+  const int kx = (int)(r % k);
+  r /= k;
+  const int ky = (int)(r % k);
+  const int co = (int)(r / k);
+  const long long P = (long long)N * Ho * Wo;
+  double acc = 0.0;
+  for (long long q = threadIdx.x; q < P; q += blockDim.x) {
+    const int ox = (int)(q % Wo);
+    const long long t = q / Wo;
+    const int oy = (int)(t % Ho);
+    const int n = (int)(t / Ho);
+    const int iy = oy * s - p + ky, ix = ox * s - p + kx;
+    if (iy < 0 || iy >= H || ix < 0 || ix >= W) continue;
+    acc += (double)dy[q * Cout + co] * (double)x[(((long long)n * H + iy) * W + ix) * Cin + ci];
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) dw[widx] = (float)red[0];
+}
+__global__ void k_lrelu_fwd(const float* __restrict__ x, float* __restrict__ y, long long n, float slope) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const float v = x[i];
+    y[i] = v > 0.0f ? v : slope * v;
+  }
+}
+__global__ void k_lrelu_bwd(const float* __restrict__ dy, const float* __restrict__ pre, float* __restrict__ dx,
+                            long long n, float slope) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    dx[i] = pre[i] > 0.0f ? dy[i] : slope * dy[i];
+}
+// one block per channel, fp64 block reduction over the rows
+__global__ void k_bn_sums_generic(const float* __restrict__ x, long long M, int C, double* __restrict__ sums) {
+  __shared__ double r1[256], r2[256];
+  const int c = blockIdx.x;
+  double a = 0.0, b = 0.0;
+  for (long long m = threadIdx.x; m < M; m += blockDim.x) {
+    const double v = x[m * C + c];
+    a += v;
+    b += v * v;
+  }
+  r1[threadIdx.x] = a;
+  r2[threadIdx.x] = b;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) {
+      r1[threadIdx.x] += r1[threadIdx.x + o];
+      r2[threadIdx.x] += r2[threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    sums[c] = r1[0];
+    sums[C + c] = r2[0];
+  }
+}
+__global__ void k_bn_apply_generic(const float* __restrict__ x, long long M, int C, const float* __restrict__ mean,
+                                   const float* __restrict__ rstd, const float* __restrict__ gamma,
+                                   const float* __restrict__ beta, int relu, float* __restrict__ y) {
+  const long long n = M * C;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(i % C);
+    float v = (x[i] - mean[c]) * rstd[c] * gamma[c] + beta[c];
+    y[i] = relu ? fmaxf(v, 0.0f) : v;
+  }
+}
+__global__ void k_bn_bwd_sums_generic(const float* __restrict__ x, const float* __restrict__ dy, long long M, int C,
+                                      const float* __restrict__ mean, const float* __restrict__ rstd,
+                                      const float* __restrict__ gamma, const float* __restrict__ beta, int relu,
+                                      double* __restrict__ tot, float* __restrict__ dgamma,
+                                      float* __restrict__ dbeta) {
+  __shared__ double r1[256], r2[256];
+  const int c = blockIdx.x;
+  double a = 0.0, b = 0.0;
+  for (long long m = threadIdx.x; m < M; m += blockDim.x) {
+    const float xh = (x[m * C + c] - mean[c]) * rstd[c];
+    float g = dy[m * C + c];
+    if (relu && xh * gamma[c] + beta[c] <= 0.0f) g = 0.0f;
+    a += g;
+    b += (double)g * xh;
+  }
+  r1[threadIdx.x] = a;
+  r2[threadIdx.x] = b;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) {
+      r1[threadIdx.x] += r1[threadIdx.x + o];
+      r2[threadIdx.x] += r2[threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    tot[c] = r1[0];
+    tot[C + c] = r2[0];
+    if (dbeta) dbeta[c] = (float)r1[0];
+    if (dgamma) dgamma[c] = (float)r2[0];
+  }
+}
+__global__ void k_bn_bwd_apply_generic(const float* __restrict__ x, const float* __restrict__ dy, long long M, int C,
+                                       const float* __restrict__ mean, const float* __restrict__ rstd,
+                                       const float* __restrict__ gamma, const float* __restrict__ beta, int relu,
+                                       const double* __restrict__ tot, double count, float* __restrict__ dx) {
+  const long long n = M * C;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(i % C);
+    const float xh = (x[i] - mean[c]) * rstd[c];
+    float g = dy[i];
+    if (relu && xh * gamma[c] + beta[c] <= 0.0f) g = 0.0f;
+    const float mg = (float)(tot[c] / count), mgx = (float)(tot[C + c] / count);
+    dx[i] = gamma[c] * rstd[c] * (g - mg - xh * mgx);
+  }
+}
+}  // namespace
+
+cudaError_t gconv_fwd(const float* x, int N, int H, int W, int Cin, const float* w, int ldw, int Cout, int k, int s,
+                      int p, int Ho, int Wo, const float* bias, float* y, cudaStream_t st) {
+  k_gconv_fwd<<<grid_for((long long)N * Ho * Wo * Cout, 256), 256, 0, st>>>(x, N, H, W, Cin, w, ldw, Cout, k, s, p, Ho,
+                                                                           Wo, bias, y);
+  return cudaGetLastError();
+}
+cudaError_t gconv_dgrad(const float* dy, int N, int Ho, int Wo, int Cout, const float* w, int ldw, int Cin, int k,
+                        int s, int p, int H, int W, const float* bias, float* dx, cudaStream_t st) {
+  k_gconv_dgrad<<<grid_for((long long)N * H * W * Cin, 256), 256, 0, st>>>(dy, N, Ho, Wo, Cout, w, ldw, Cin, k, s, p,
+                                                                           H, W, bias, dx);
+  return cudaGetLastError();
+}
+cudaError_t gconv_wgrad(const float* x, int N, int H, int W, int Cin, const float* dy, int Ho, int Wo, int Cout,
+                        int k, int s, int p, float* dw, cudaStream_t st) {
+  const long long nw = (long long)Cout * k * k * Cin;
+  k_gconv_wgrad<<<(unsigned)nw, 256, 0, st>>>(x, N, H, W, Cin, dy, Ho, Wo, Cout, k, s, p, dw);
+  return cudaGetLastError();
+}
+cudaError_t lrelu_fwd(const float* x, float* y, long long n, float slope, cudaStream_t st) {
+  k_lrelu_fwd<<<grid_for(n, 256), 256, 0, st>>>(x, y, n, slope);
+  return cudaGetLastError();
+}
+cudaError_t lrelu_bwd(const float* dy, const float* pre, float* dx, long long n, float slope, cudaStream_t st) {
+  k_lrelu_bwd<<<grid_for(n, 256), 256, 0, st>>>(dy, pre, dx, n, slope);
+  return cudaGetLastError();
+}
+cudaError_t bn_sums_generic(const float* x, long long M, int C, double* sums, cudaStream_t st) {
+  k_bn_sums_generic<<<C, 256, 0, st>>>(x, M, C, sums);
+  return cudaGetLastError();
+}
+cudaError_t bn_apply_generic(const float* x, long long M, int C, const float* mean, const float* rstd,
+                             const float* gamma, const float* beta, int relu, float* y, cudaStream_t st) {
+  k_bn_apply_generic<<<grid_for(M * C, 256), 256, 0, st>>>(x, M, C, mean, rstd, gamma, beta, relu, y);
+  return cudaGetLastError();
+}
+cudaError_t bn_bwd_sums_generic(const float* x, const float* dy, long long M, int C, const float* mean,
+                                const float* rstd, const float* gamma, const float* beta, int relu, double* tot,
+                                float* dgamma, float* dbeta, cudaStream_t st) {
+  k_bn_bwd_sums_generic<<<C, 256, 0, st>>>(x, dy, M, C, mean, rstd, gamma, beta, relu, tot, dgamma, dbeta);
+  return cudaGetLastError();
+}
+cudaError_t bn_bwd_apply_generic(const float* x, const float* dy, long long M, int C, const float* mean,
+                                 const float* rstd, const float* gamma, const float* beta, int relu, const double* tot,
+                                 double count, float* dx, cudaStream_t st) {
+  k_bn_bwd_apply_generic<<<grid_for(M * C, 256), 256, 0, st>>>(x, dy, M, C, mean, rstd, gamma, beta, relu, tot,
+                                                               count, dx);
+  return cudaGetLastError();
+}
+
 cudaError_t thin_conv_fwd(const float* x, int N, int H, int W, int C, const float* w, int CO, const float* bias,
                           float* y, cudaStream_t st) {
   if (CO != 3 || C % 4 || ((uintptr_t)x & 15)) return cudaErrorInvalidValue;

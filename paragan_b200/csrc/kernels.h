@@ -145,6 +145,35 @@ cudaError_t col2im3(const T* dxi, int N, int H, int W, int cx, const T* add, T* 
 cudaError_t fold_up2_weights(const float* w, const float* inv_sigma, int Cout, int Cin, bf16* dst, cudaStream_t st,
                              int layout = 0);
 
+// ---------------- generic fp32 SIMT kernels of the SN-DCGAN path (config 1; SURVEY Appendix B "K7")
+// strided k x k conv, NHWC, zero padding p; w OHWI [Cout][k][k][ldw] (first Cin of ldw used)
+cudaError_t gconv_fwd(const float* x, int N, int H, int W, int Cin, const float* w, int ldw, int Cout, int k, int s,
+                      int p, int Ho, int Wo, const float* bias, float* y, cudaStream_t st);
+// dx[n,iy,ix,ci] = bias[ci] + sum_{co,ky,kx: iy = oy*s - p + ky} dy[n,oy,ox,co] w[co][ky][kx][ci]  (the conv's
+// adjoint; with bias it is the transposed conv / deconv forward)
+cudaError_t gconv_dgrad(const float* dy, int N, int Ho, int Wo, int Cout, const float* w, int ldw, int Cin, int k,
+                        int s, int p, int H, int W, const float* bias, float* dx, cudaStream_t st);
+// dw[co][ky][kx][ci] (ldw = Cin) = sum_{n,oy,ox} dy[n,oy,ox,co] x[n, oy*s-p+ky, ox*s-p+kx, ci]  (fp64 sums)
+cudaError_t gconv_wgrad(const float* x, int N, int H, int W, int Cin, const float* dy, int Ho, int Wo, int Cout,
+                        int k, int s, int p, float* dw, cudaStream_t st);
+// y = x > 0 ? x : slope * x ;  dx = dy * (pre > 0 ? 1 : slope)
+cudaError_t lrelu_fwd(const float* x, float* y, long long n, float slope, cudaStream_t st);
+cudaError_t lrelu_bwd(const float* dy, const float* pre, float* dx, long long n, float slope, cudaStream_t st);
+// per-channel BN over [M][C] fp32 (any C): local sums[2C] = (sum x, sum x^2) in fp64
+cudaError_t bn_sums_generic(const float* x, long long M, int C, double* sums, cudaStream_t st);
+// y = (relu?) ((x - mean) * rstd * gamma + beta)
+cudaError_t bn_apply_generic(const float* x, long long M, int C, const float* mean, const float* rstd,
+                             const float* gamma, const float* beta, int relu, float* y, cudaStream_t st);
+// tot[0:C] = sum g, tot[C:2C] = sum g * xhat over the local rows, g = dy masked by the output ReLU; also
+// written (fp32) to dbeta / dgamma (local parameter gradients)
+cudaError_t bn_bwd_sums_generic(const float* x, const float* dy, long long M, int C, const float* mean,
+                                const float* rstd, const float* gamma, const float* beta, int relu, double* tot,
+                                float* dgamma, float* dbeta, cudaStream_t st);
+// dx = gamma * rstd * (g - tot[c] / count - xhat * tot[C + c] / count)   (tot all-reduced over ranks)
+cudaError_t bn_bwd_apply_generic(const float* x, const float* dy, long long M, int C, const float* mean,
+                                 const float* rstd, const float* gamma, const float* beta, int relu, const double* tot,
+                                 double count, float* dx, cudaStream_t st);
+
 // ---------------- thin fp32 conv (C_out = 3): G's fp32 output layer, 3x3 pad 1
 cudaError_t thin_conv_fwd(const float* x, int N, int H, int W, int C, const float* w, int CO, const float* bias,
                           float* y, cudaStream_t st);

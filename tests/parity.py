@@ -16,6 +16,12 @@ def oracle_config(res, ch, attn, n_classes, shared_dim, z_chunk, n_d=1, bf16=Fal
                      adam_d=bg.AdamHP(2e-4, 0.0, 0.999, eps), adam_g=bg.AdamHP(5e-5, 0.0, 0.999, eps))
 
 
+def sndcgan_oracle_config(ch=32, n_classes=10, n_d=1):
+    """Config 1 (SN-DCGAN 32x32, fp32; R25) with the same Adam policy as the BigGAN configs."""
+    return bg.Config(arch="sndcgan", resolution=32, ch=ch, n_classes=n_classes, d_steps_per_g=n_d, attn_res=0,
+                     adam_d=bg.AdamHP(2e-4, 0.0, 0.999, 1e-8), adam_g=bg.AdamHP(5e-5, 0.0, 0.999, 1e-8))
+
+
 def make_inputs(ocfg, B, seed, n_d=1, gamma=0.1):
     """Global-batch inputs: initial states and n_d D batches + 1 G batch (R18)."""
     gs, ds = bg.g_param_specs(ocfg), bg.d_param_specs(ocfg)

@@ -38,6 +38,24 @@ def test_param_layout_matches_oracle(res, ch, attn):
         assert ns == bg.n_state(specs)
 
 
+@pytest.mark.parametrize("ch", [32, 4])
+def test_sndcgan_param_layout_matches_oracle(ch):
+    """Config 1 (R25): the library's SN-DCGAN state layout is the oracle's (written independently)."""
+    ocfg = bg.Config(arch="sndcgan", resolution=32, ch=ch)
+    cfg = api.make_sndcgan_config(ch=ch)
+    for net, specs in ((api.NET_G, bg.g_param_specs(ocfg)), (api.NET_D, bg.d_param_specs(ocfg))):
+        ns, nt = api.param_count(cfg, net)
+        assert nt == bg.n_trainable(specs)
+        assert ns == bg.n_state(specs)
+    # bf16 and other resolutions are rejected for this architecture
+    for kw in (dict(compute=api.BF16), dict(resolution=64)):
+        bad = api.make_sndcgan_config(ch=ch)
+        for k, v in kw.items():
+            setattr(bad, k, v)
+        with pytest.raises(api.ParaganError):
+            api.workspace_size(bad)
+
+
 def test_biggan128_total_is_paper_count():
     cfg = api.make_config()
     tot = api.param_count(cfg, api.NET_G)[1] + api.param_count(cfg, api.NET_D)[1]

@@ -15,6 +15,7 @@ from paragan_b200 import inputs
 
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 MICRO = dict(resolution=16, ch=2, n_classes=5, shared_dim=4, z_chunk=3, attn_res=8)
+MICRO_DCGAN = dict(arch="sndcgan", resolution=32, ch=4, n_classes=5)   # config 1's topology at ch=4
 
 
 def test_biggan128_parameter_count_matches_paper():
@@ -68,8 +69,9 @@ def _dir_check(loss_fn, params: dict, grads: dict, rng, h=1e-6):
     return worst
 
 
-def test_d_step_gradients_match_finite_differences():
-    cfg = bg.Config(**MICRO)
+@pytest.mark.parametrize("micro", [MICRO, MICRO_DCGAN], ids=["biggan", "sndcgan"])
+def test_d_step_gradients_match_finite_differences(micro):
+    cfg = bg.Config(**micro)
     G, D, real, ry, z, fy = _setup(cfg, B=3)
     Dp0 = {k: v.clone() for k, v in D.params.items()}
     us_d0 = {k: v.clone() for k, v in D.us.items()}
@@ -94,8 +96,9 @@ def test_d_step_gradients_match_finite_differences():
     _dir_check(loss, Dp0, grads, np.random.default_rng(0))
 
 
-def test_g_step_gradients_match_finite_differences():
-    cfg = bg.Config(**MICRO)
+@pytest.mark.parametrize("micro", [MICRO, MICRO_DCGAN], ids=["biggan", "sndcgan"])
+def test_g_step_gradients_match_finite_differences(micro):
+    cfg = bg.Config(**micro)
     G, D, real, ry, z, fy = _setup(cfg, B=3)
     Gp0 = {k: v.clone() for k, v in G.params.items()}
     us_g0 = {k: v.clone() for k, v in G.us.items()}
@@ -175,3 +178,19 @@ def test_data_parallel_decomposition_of_d_gradient():
                           for g, s in zip(gl, D.specs)]).numpy()
         acc = flat / W if acc is None else acc + flat / W
     assert np.allclose(acc, out["grads"], rtol=1e-9, atol=1e-12)
+
+
+def test_sndcgan_parameter_counts_and_deconv_adjoint():
+    """Config 1 (R25): SURVEY Appendix B's counts follow from the layer listing (a reading — the
+    paper prints none), and the deconv is the adjoint of the strided conv with the same weight."""
+    cfg = bg.Config(arch="sndcgan", resolution=32, ch=32)
+    assert bg.n_trainable(bg.g_param_specs(cfg)) == 1_226_243
+    assert bg.n_trainable(bg.d_param_specs(cfg)) == 736_801
+    assert sum(s.sn for s in bg.g_param_specs(cfg)) == 0 and sum(s.sn for s in bg.d_param_specs(cfg)) == 8
+    rng = np.random.default_rng(3)
+    x = torch.tensor(rng.standard_normal((2, 5, 4, 4)))
+    y = torch.tensor(rng.standard_normal((2, 3, 8, 8)))
+    w = torch.tensor(rng.standard_normal((5, 3, 4, 4)))
+    lhs = (torch.nn.functional.conv_transpose2d(x, w, stride=2, padding=1) * y).sum()
+    rhs = (x * torch.nn.functional.conv2d(y, w, stride=2, padding=1)).sum()
+    assert abs(float(lhs - rhs)) < 1e-10 * abs(float(lhs))
