@@ -347,7 +347,7 @@ class Engine final : public EngineBase {
     if (!real || !real_y || !z || !fake_y || ((uintptr_t)real & 15)) return fail_arg("d_step: bad pointer");
     // SN(G) + G forward (no grad) writes fakes into D-input rows [0, B)
     CKS(sn_forward(G_, false));
-    CKS(fold_subpixel());
+    CKS(fold_subpixel(false));
     if (dcgan_) CKS(g_forward_dc(z));
     else CKS(g_forward(z, fake_y, false));
     // reals into rows [B, 2B) (one D pass over the concatenated batch)
@@ -380,7 +380,7 @@ class Engine final : public EngineBase {
     }
     if (!z || !y) return fail_arg("g_step: bad pointer");
     CKS(sn_forward(G_, true));
-    CKS(fold_subpixel());
+    CKS(fold_subpixel(true));
     if (dcgan_) CKS(g_forward_dc(z));
     else CKS(g_forward(z, y, true));
     CK(cudaMemcpyAsync(ylab_, y, sizeof(int32_t) * B_, cudaMemcpyDeviceToDevice, st_));
@@ -1136,15 +1136,16 @@ class Engine final : public EngineBase {
     return PARAGAN_OK;
   }
   // W/sigma of every G conv1 folded into the four phase kernels of the sub-pixel conv
-  paragan_status fold_subpixel() {
+  paragan_status fold_subpixel(bool need_dgrad) {
     if (!subpix_) return PARAGAN_OK;
     for (GBlock& b : gb_) {
       const PEntry& e = G_.E[b.c1.w];
       CK(fold_up2_weights(G_.p + e.off, G_.sigma + 2 * e.job + 1, b.c1.cout, b.c1.cin,
                           static_cast<bf16*>(b.c1.wp4), st_, 0));
-      CK(fold_up2_weights(G_.p + e.off, G_.sigma + 2 * e.job + 1, b.c1.cout, b.c1.cin,
-                          static_cast<bf16*>(b.c1.wt4), st_, 1));
-      launches_ += 2;
+      if (need_dgrad)
+        CK(fold_up2_weights(G_.p + e.off, G_.sigma + 2 * e.job + 1, b.c1.cout, b.c1.cin,
+                            static_cast<bf16*>(b.c1.wt4), st_, 1));
+      launches_ += need_dgrad ? 2 : 1;
     }
     return PARAGAN_OK;
   }

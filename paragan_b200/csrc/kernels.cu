@@ -2229,41 +2229,52 @@ __global__ void k_reduce_rows_f32(const float* __restrict__ partial, int rows, i
 }
 }  // namespace
 
+// one thread per (o, c): the nine 3x3 taps read once, the sixteen folded (phase, tap) weights written.
+// layout 0: c fastest across threads (coalesced reads and writes); layout 1: o fastest (coalesced writes)
 __global__ void k_fold_up2(const float* __restrict__ w, const float* __restrict__ inv_sigma, int Cout, int Cin,
                            bf16* __restrict__ dst, int layout) {
-  const long long n = 16LL * Cout * Cin;
+  const long long n = (long long)Cout * Cin;
+  const float is = inv_sigma[0];
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    int c, t, o, ph;
-    if (layout == 0) {   // [phase][Cout][tap][Cin]
-      c = (int)(i % Cin);
-      long long r = i / Cin;
-      t = (int)(r % 4);
-      r /= 4;
-      o = (int)(r % Cout);
-      ph = (int)(r / Cout);
-    } else {             // [Cin][phase * 4 + tap][Cout]
-      o = (int)(i % Cout);
-      const long long r = i / Cout;
-      t = (int)(r % 4);
-      ph = (int)((r / 4) % 4);
-      c = (int)(r / 16);
+    int o, c;
+    if (layout == 0) {
+      o = (int)(i / Cin);
+      c = (int)(i - (long long)o * Cin);
+    } else {
+      c = (int)(i / Cout);
+      o = (int)(i - (long long)c * Cout);
     }
-    const int a = ph >> 1, b = ph & 1, p = t >> 1, q = t & 1;
-    // rows r0..r1 of the 3x3 kernel that land on input row offset p for phase a (same for columns)
-    const int r0 = (a == 0) ? (p == 0 ? 0 : 1) : (p == 0 ? 0 : 2);
-    const int r1 = (a == 0) ? (p == 0 ? 0 : 2) : (p == 0 ? 1 : 2);
-    const int s0 = (b == 0) ? (q == 0 ? 0 : 1) : (q == 0 ? 0 : 2);
-    const int s1 = (b == 0) ? (q == 0 ? 0 : 2) : (q == 0 ? 1 : 2);
-    float acc = 0.0f;
-    for (int rr = r0; rr <= r1; ++rr)
-      for (int ss = s0; ss <= s1; ++ss) acc += w[((long long)o * 9 + rr * 3 + ss) * Cin + c];
-    dst[i] = __float2bfloat16_rn(acc * inv_sigma[0]);
+    float t9[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) t9[k] = w[((long long)o * 9 + k) * Cin + c];
+#pragma unroll
+    for (int ph = 0; ph < 4; ++ph) {
+      const int a = ph >> 1, b = ph & 1;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int p = t >> 1, q = t & 1;
+        // rows of the 3x3 kernel landing on input row offset p for phase a (same for columns)
+        const int r0 = (a == 0) ? (p == 0 ? 0 : 1) : (p == 0 ? 0 : 2);
+        const int r1 = (a == 0) ? (p == 0 ? 0 : 2) : (p == 0 ? 1 : 2);
+        const int s0 = (b == 0) ? (q == 0 ? 0 : 1) : (q == 0 ? 0 : 2);
+        const int s1 = (b == 0) ? (q == 0 ? 0 : 2) : (q == 0 ? 1 : 2);
+        float acc = 0.0f;
+#pragma unroll
+        for (int rr = 0; rr < 3; ++rr)
+#pragma unroll
+          for (int ss = 0; ss < 3; ++ss)
+            if (rr >= r0 && rr <= r1 && ss >= s0 && ss <= s1) acc += t9[rr * 3 + ss];
+        const bf16 v = __float2bfloat16_rn(acc * is);
+        if (layout == 0) dst[(((long long)ph * Cout + o) * 4 + t) * Cin + c] = v;
+        else dst[((long long)c * 16 + ph * 4 + t) * Cout + o] = v;
+      }
+    }
   }
 }
 
 cudaError_t fold_up2_weights(const float* w, const float* inv_sigma, int Cout, int Cin, bf16* dst, cudaStream_t st,
                              int layout) {
-  k_fold_up2<<<grid_for(16LL * Cout * Cin, 256), 256, 0, st>>>(w, inv_sigma, Cout, Cin, dst, layout);
+  k_fold_up2<<<grid_for((long long)Cout * Cin, 256), 256, 0, st>>>(w, inv_sigma, Cout, Cin, dst, layout);
   return cudaGetLastError();
 }
 

@@ -24,9 +24,14 @@ def main():
     obj = [api.get_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     B = 4
-    ocfg = P.oracle_config(32, 4, 16, 10, 16, 4, bf16=(compute == api.BF16))
-    cfg = api.make_config(resolution=32, ch=4, attn_res=16, n_classes=10, shared_dim=16, z_chunk=4, local_batch=B,
-                          compute=compute, rank=rank, world_size=world, device=local)
+    dcgan = os.environ.get("PARAGAN_ARCH", "biggan") == "sndcgan"
+    if dcgan:   # config 1 (SN-DCGAN, fp32): cross-replica BN in G, SN in D
+        ocfg = P.sndcgan_oracle_config(ch=8)
+        cfg = api.make_sndcgan_config(ch=8, local_batch=B, rank=rank, world_size=world, device=local)
+    else:
+        ocfg = P.oracle_config(32, 4, 16, 10, 16, 4, bf16=(compute == api.BF16))
+        cfg = api.make_config(resolution=32, ch=4, attn_res=16, n_classes=10, shared_dim=16, z_chunk=4,
+                              local_batch=B, compute=compute, rank=rank, world_size=world, device=local)
     gs, ds, g0, d0, dbs, gb = P.make_inputs(ocfg, B * world, seed=31)
     got = P.run_gpu(cfg, g0, d0, dbs, gb, rank=rank, world=world, nccl_id=obj[0])
     # replicas bit-identical
@@ -40,8 +45,11 @@ def main():
     if rank == 0:
         # the same global batch on ONE GPU: the data-parallel decomposition (R15) up to the
         # reassociation of the cross-replica sums
-        scfg = api.make_config(resolution=32, ch=4, attn_res=16, n_classes=10, shared_dim=16, z_chunk=4,
-                               local_batch=B * world, compute=compute, device=local)
+        if dcgan:
+            scfg = api.make_sndcgan_config(ch=8, local_batch=B * world, device=local)
+        else:
+            scfg = api.make_config(resolution=32, ch=4, attn_res=16, n_classes=10, shared_dim=16, z_chunk=4,
+                                   local_batch=B * world, compute=compute, device=local)
         single = P.run_gpu(scfg, g0, d0, dbs, gb)
         # gradients: reassociation only (1e-5 fp32); updated weights: Adam's first step is ~ -lr*sign(g), so
         # elements whose gradient is ~0 (a bias feeding a BN) may flip sign: the oracle's state bar (1e-4)
