@@ -548,6 +548,108 @@ __global__ void k_bn_bwd_means(const double* __restrict__ tot, int C, double cou
   mgrad[c] = (float)(tot[c] / count);
 }
 
+// Channel-group-stationary variants (no upsample): thread (pixel lane, channel group g) keeps its 8 channels'
+// statistics in registers and walks pixels, two per iteration; per-sample CBN gains are reloaded only
+// when the image changes.  blockDim = G * P (G = C/8 groups, P pixel lanes).
+template <typename TI, typename TO>
+__global__ void __launch_bounds__(256) k_bn_apply_relu_cs(const TI* __restrict__ x, long long P_total, int HW, int C,
+                                                          const float* __restrict__ mean,
+                                                          const float* __restrict__ rstd, BnAffine af,
+                                                          TO* __restrict__ y) {
+  const int G = C >> 3;
+  const int lanes = blockDim.x / G;
+  const int g = threadIdx.x % G, lane = threadIdx.x / G;
+  if (lane >= lanes) return;
+  float mu[8], rs[8], ga[8], be[8];
+  BnAffine::ld8(mean + g * 8, mu);
+  BnAffine::ld8(rstd + g * 8, rs);
+  int ncur = -1;
+  if (!af.gain) af.get8(0, g * 8, C, ga, be);
+  // each block owns a contiguous pixel range, so an image's CBN gains are reloaded ~once per block
+  const long long chunk = (P_total + gridDim.x - 1) / gridDim.x;
+  const long long p_end = min(P_total, (blockIdx.x + 1) * chunk);
+  const long long step = lanes;
+  for (long long p = blockIdx.x * chunk + lane; p < p_end; p += 2 * step) {
+    const long long p2 = p + step;
+    float v[8], v2[8];
+    Vec8<TI>::load(x + p * C + g * 8, v);
+    const bool has2 = p2 < p_end;
+    if (has2) Vec8<TI>::load(x + p2 * C + g * 8, v2);
+    if (af.gain) {
+      const int n = (int)((unsigned)p / (unsigned)HW);   // pixel counts < 2^31
+      if (n != ncur) {
+        af.get8(n, g * 8, C, ga, be);
+        ncur = n;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float t = (v[j] - mu[j]) * rs[j] * ga[j] + be[j];
+      v[j] = t > 0.0f ? t : 0.0f;
+    }
+    Vec8<TO>::store(y + p * C + g * 8, v);
+    if (has2) {
+      if (af.gain) {
+        const int n = (int)((unsigned)p2 / (unsigned)HW);
+        if (n != ncur) {
+          af.get8(n, g * 8, C, ga, be);
+          ncur = n;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float t = (v2[j] - mu[j]) * rs[j] * ga[j] + be[j];
+        v2[j] = t > 0.0f ? t : 0.0f;
+      }
+      Vec8<TO>::store(y + p2 * C + g * 8, v2);
+    }
+  }
+}
+
+template <typename TI, typename TG, typename TO>
+__global__ void __launch_bounds__(256) k_bn_bwd_apply_cs(const TI* __restrict__ x, const TG* __restrict__ dy,
+                                                         long long P_total, int HW, int C,
+                                                         const float* __restrict__ mean,
+                                                         const float* __restrict__ rstd, BnAffine af,
+                                                         const float* __restrict__ mgrad, const TO* __restrict__ add,
+                                                         TO* __restrict__ dx) {
+  const int G = C >> 3;
+  const int lanes = blockDim.x / G;
+  const int g = threadIdx.x % G, lane = threadIdx.x / G;
+  if (lane >= lanes) return;
+  float mu[8], rs[8], ga[8], be[8], mg[8], mgx[8];
+  BnAffine::ld8(mean + g * 8, mu);
+  BnAffine::ld8(rstd + g * 8, rs);
+  BnAffine::ld8(mgrad + g * 8, mg);
+  BnAffine::ld8(mgrad + C + g * 8, mgx);
+  int ncur = -1;
+  if (!af.gain) af.get8(0, g * 8, C, ga, be);
+  const long long chunk = (P_total + gridDim.x - 1) / gridDim.x;
+  const long long p_end = min(P_total, (blockIdx.x + 1) * chunk);
+  for (long long p = blockIdx.x * chunk + lane; p < p_end; p += lanes) {
+    float v[8], d[8], ad[8], o[8];
+    Vec8<TI>::load(x + p * C + g * 8, v);
+    Vec8<TG>::load(dy + p * C + g * 8, d);
+    if (add) Vec8<TO>::load(add + p * C + g * 8, ad);
+    if (af.gain) {
+      const int n = (int)((unsigned)p / (unsigned)HW);   // pixel counts < 2^31
+      if (n != ncur) {
+        af.get8(n, g * 8, C, ga, be);
+        ncur = n;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float xh = (v[j] - mu[j]) * rs[j];
+      const float z = xh * ga[j] + be[j];
+      const float g0 = z > 0.0f ? d[j] : 0.0f;
+      o[j] = rs[j] * (ga[j] * g0 - mg[j] - xh * mgx[j]);
+      if (add) o[j] += ad[j];
+    }
+    Vec8<TO>::store(dx + p * C + g * 8, o);
+  }
+}
+
 // ===================================================================== elementwise
 template <typename T>
 __global__ void k_relu_copy(const T* __restrict__ x, T* __restrict__ y, long long n) {
@@ -1595,6 +1697,16 @@ cudaError_t bn_apply_relu(const TI* x, int N, int H, int W, int C, const float* 
                           const float* gain, const float* bias, const float* gamma, const float* beta, TO* y, bool up2,
                           cudaStream_t st) {
   const long long total = (long long)N * H * W * (C / 8);
+  const int G = C / 8;
+  if (!up2 && C % 8 == 0 && G <= 256) {
+    const int lanes = 256 / G;
+    const long long P = (long long)N * H * W;
+    long long blocks = (P + 2LL * lanes - 1) / (2LL * lanes);
+    if (blocks > 8LL * kNumSMs) blocks = 8LL * kNumSMs;
+    k_bn_apply_relu_cs<TI, TO><<<(unsigned)blocks, lanes * G, 0, st>>>(x, P, H * W, C, mean, rstd,
+                                                                       BnAffine{gain, bias, gamma, beta}, y);
+    return cudaGetLastError();
+  }
   k_bn_apply_relu<TI, TO><<<grid_for(total, 256), 256, 0, st>>>(x, N, H, W, C, mean, rstd,
                                                                 BnAffine{gain, bias, gamma, beta}, y, up2 ? 1 : 0);
   return cudaGetLastError();
@@ -1650,6 +1762,16 @@ cudaError_t bn_bwd_apply(const TI* x, const TG* dy, int N, int H, int W, int C, 
   k_bn_bwd_means<<<ceil_div(2 * C, 256), 256, 0, st>>>(tot, C, count, mgrad);
   PG_LAUNCH_CHECK();
   const long long total = (long long)N * H * W * (C / 8);
+  const int G = C / 8;
+  if (!up2 && C % 8 == 0 && G <= 256) {
+    const int lanes = 256 / G;
+    const long long P = (long long)N * H * W;
+    long long blocks = (P + lanes - 1) / lanes;
+    if (blocks > 8LL * kNumSMs) blocks = 8LL * kNumSMs;
+    k_bn_bwd_apply_cs<TI, TG, TO><<<(unsigned)blocks, lanes * G, 0, st>>>(
+        x, dy, P, H * W, C, mean, rstd, BnAffine{gain, bias, gamma, beta}, mgrad, add, dx);
+    return cudaGetLastError();
+  }
   k_bn_bwd_apply<TI, TG, TO><<<grid_for(total, 256), 256, 0, st>>>(
       x, dy, N, H, W, C, mean, rstd, BnAffine{gain, bias, gamma, beta}, up2 ? 1 : 0, mgrad, add, dx);
   return cudaGetLastError();
