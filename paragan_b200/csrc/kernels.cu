@@ -1673,10 +1673,13 @@ cudaError_t scatter_add_rows(const float* src, int lds, const int32_t* idx, int 
 template <typename T>
 cudaError_t bn_stats(const T* x, long long M, int C, double* partial, int max_blocks, double* sums, cudaStream_t st) {
   if (C % 8 || C / 8 > 256) return cudaErrorInvalidValue;
-  int nblk = (int)((M + 511) / 512);
-  if (nblk > max_blocks) nblk = max_blocks;
-  const long long per = (M + nblk - 1) / nblk;
   const int R = 256 / (C / 8);
+  // ~8 pixels per thread row: wide layers at low resolution (C = 1536, R = 1) get enough blocks
+  long long nb = M / (8LL * R);
+  if (nb < 1) nb = 1;
+  if (nb > max_blocks) nb = max_blocks;
+  const int nblk = (int)nb;
+  const long long per = (M + nblk - 1) / nblk;
   const size_t sm = (size_t)R * 2 * C * sizeof(double);
   if (sm > 48 * 1024) PG_CUDA(cudaFuncSetAttribute(k_bn_stats<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   k_bn_stats<T><<<nblk, 256, sm, st>>>(x, M, C, partial, per);
@@ -2118,19 +2121,37 @@ __global__ void __launch_bounds__(256, 2) k_thin_fwd(const float* __restrict__ x
     for (int o = 0; o < CO; ++o) acc[p][o] = 0.0f;
   for (int c0 = 0; c0 < C; c0 += kFCC) {
     __syncthreads();
-    for (int i = threadIdx.x; i < (kFTH + 2) * (kFTW + 2) * 2; i += blockDim.x) {
-      const int half = i & 1, rs = i >> 1;
-      const int sx = rs % (kFTW + 2), r = rs / (kFTW + 2);
-      const int h = h0 - 1 + r, ww = w0 - 1 + sx;
-      const int c = c0 + half * 4;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (h >= 0 && h < H && ww >= 0 && ww < W && c < C)
-        v = *reinterpret_cast<const float4*>(x + (((long long)n * H + h) * W + ww) * C + c);
-      float* d = xs + half * 4 * kFPlane + r * kFRS + sx;
-      d[0] = v.x;
-      d[kFPlane] = v.y;
-      d[2 * kFPlane] = v.z;
-      d[3 * kFPlane] = v.w;
+    // halo chunk: batches of 6 independent 16-byte loads per thread in flight, then the planar stores
+    constexpr int kItems = (kFTH + 2) * (kFTW + 2) * 2;
+    constexpr int kBatch = 6;
+    for (int i0 = threadIdx.x; i0 < kItems; i0 += kBatch * 256) {
+      float4 v[kBatch];
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) {
+        const int i = i0 + u * 256;
+        v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (i < kItems) {
+          const int half = i & 1, rs = i >> 1;
+          const int sx = rs % (kFTW + 2), r = rs / (kFTW + 2);
+          const int h = h0 - 1 + r, ww = w0 - 1 + sx;
+          const int c = c0 + half * 4;
+          if (h >= 0 && h < H && ww >= 0 && ww < W && c < C)
+            v[u] = __ldg(reinterpret_cast<const float4*>(x + (((long long)n * H + h) * W + ww) * C + c));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) {
+        const int i = i0 + u * 256;
+        if (i < kItems) {
+          const int half = i & 1, rs = i >> 1;
+          const int sx = rs % (kFTW + 2), r = rs / (kFTW + 2);
+          float* d = xs + half * 4 * kFPlane + r * kFRS + sx;
+          d[0] = v[u].x;
+          d[kFPlane] = v[u].y;
+          d[2 * kFPlane] = v[u].z;
+          d[3 * kFPlane] = v[u].w;
+        }
+      }
     }
     __syncthreads();
     const int cc = min(kFCC, C - c0);
@@ -2281,14 +2302,29 @@ __global__ void __launch_bounds__(256) k_thin_wgrad(const float* __restrict__ x,
     const int h0 = th * kWTH, w0 = tw * kWTW;
     __syncthreads();
     const int nvec = (kWTH + 2) * HC * (C / 4);
-    for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
-      const int cv = i % (C / 4), rs = i / (C / 4);
-      const int sx = rs % HC, r = rs / HC;
-      const int h = h0 - 1 + r, ww = w0 - 1 + sx;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (h >= 0 && h < H && ww >= 0 && ww < W)
-        v = *reinterpret_cast<const float4*>(x + (((long long)n * H + h) * W + ww) * C + cv * 4);
-      *reinterpret_cast<float4*>(xs + rs * C + cv * 4) = v;
+    constexpr int kBatch = 6;   // independent 16-byte loads in flight per thread
+    for (int i0 = threadIdx.x; i0 < nvec; i0 += kBatch * blockDim.x) {
+      float4 v[kBatch];
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) {
+        const int i = i0 + u * blockDim.x;
+        v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (i < nvec) {
+          const int cv = i % (C / 4), rs = i / (C / 4);
+          const int sx = rs % HC, r = rs / HC;
+          const int h = h0 - 1 + r, ww = w0 - 1 + sx;
+          if (h >= 0 && h < H && ww >= 0 && ww < W)
+            v[u] = __ldg(reinterpret_cast<const float4*>(x + (((long long)n * H + h) * W + ww) * C + cv * 4));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) {
+        const int i = i0 + u * blockDim.x;
+        if (i < nvec) {
+          const int cv = i % (C / 4), rs = i / (C / 4);
+          *reinterpret_cast<float4*>(xs + rs * C + cv * 4) = v[u];
+        }
+      }
     }
     for (int i = threadIdx.x; i < kWTH * kWTW; i += blockDim.x) {
       const int h = h0 + i / kWTW, ww = w0 + i % kWTW;
