@@ -314,9 +314,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 __global__ void __launch_bounds__(kBwdThreads, 1)
     k_attn_bwd(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmO,
-               const TcAttnArgs a, const int NS) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = align1024(smem_raw);
+               const TcAttnArgs a, const int NS, const int NP) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw;   // the layout needs 1024-byte alignment (checked on the host, see bwd_stages)
+  if (threadIdx.x == 0 && (tc::smem_u32(smem) & 1023u)) __trap();
   const int C2 = a.C2, Cq = a.Cq;
   const int g_atoms = C2 > 64 ? 2 : 1;
   // one stage = {theta atom, dO g_atoms atoms, lse[128], D[128]}; NS stages (2..4, host-chosen)
@@ -324,21 +325,22 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const uint32_t ld_off = (1 + g_atoms) * kAtom;   // lse / D inside a stage
   uint8_t* sPhi = smem;                       // [128 keys][64]        1 atom
   uint8_t* sG = sPhi + kAtom;                 // [128 keys][64 x g]    g_atoms atoms
-  uint8_t* sPT = sG + g_atoms * kAtom;        // P^T  [128 keys][128 q] 2 atoms
-  uint8_t* sDS = sPT + 2 * kAtom;             // dS^T [128 keys][128 q] 2 atoms
-  uint8_t* sStage = sDS + 2 * kAtom;
+  // NP buffers of {P^T [128 keys][128 q] 2 atoms, dS^T 2 atoms}: with two, the softmax warps fill tile t+1
+  // while the MMAs of tile t still read theirs
+  uint8_t* sPD = sG + g_atoms * kAtom;
+  uint8_t* sStage = sPD + NP * 4 * kAtom;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sStage + NS * stage_bytes);
   uint64_t* kvfull = bars;
   uint64_t* qfull = bars + 1;      // [4]
   uint64_t* qempty = bars + 5;     // [4]
   uint64_t* sfull = bars + 9;
   uint64_t* sempty = bars + 10;
-  uint64_t* pfull = bars + 11;
-  uint64_t* pempty = bars + 12;
-  uint64_t* dtfull = bars + 13;    // [2]
-  uint64_t* dtempty = bars + 15;   // [2]
-  uint64_t* accfull = bars + 17;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
+  uint64_t* pfull = bars + 11;     // [2]
+  uint64_t* pempty = bars + 13;    // [2]
+  uint64_t* dtfull = bars + 15;    // [2]
+  uint64_t* dtempty = bars + 17;   // [2]
+  uint64_t* accfull = bars + 19;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
@@ -357,8 +359,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
     tc::mbar_init(sfull, 1);
     tc::mbar_init(sempty, 256);
-    tc::mbar_init(pfull, 256);
-    tc::mbar_init(pempty, 1);
+    for (int s = 0; s < 2; ++s) {
+      tc::mbar_init(&pfull[s], 256);
+      tc::mbar_init(&pempty[s], 1);
+    }
     tc::mbar_init(accfull, 1);
     tc::fence_barrier_init();
   }
@@ -427,9 +431,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       issue_s(0);
       for (int t = 0; t < T; ++t) {
         if (t + 1 < T) issue_s(t + 1);
-        const int st = t % NS, db = t & 1;
+        const int st = t % NS, db = t & 1, pb = t % NP;
         const uint8_t* sb = sStage + st * stage_bytes;
-        tc::mbar_wait(pfull, t & 1);
+        const uint8_t* sPT = sPD + pb * 4 * kAtom;
+        const uint8_t* sDS = sPT + 2 * kAtom;
+        tc::mbar_wait(&pfull[pb], (t / NP) & 1);
         tc::mbar_wait(&dtempty[db], ((t >> 1) & 1) ^ 1);
         tc::tc_fence_after();
 #pragma unroll 1
@@ -441,7 +447,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll 1
         for (int k = 0; k < 8; ++k)     // K = 128 keys in steps of 16
           tc::mma_bf16(tmem + cDT + db * 32, mndesc(sDS + k * 2048), mndesc(sPhi + k * 2048), idDT, k > 0);
-        tc::mma_commit(pempty);
+        tc::mma_commit(&pempty[pb]);
         tc::mma_commit(&qempty[st]);
         tc::mma_commit(&dtfull[db]);
       }
@@ -496,16 +502,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           dk[jj >> 1] = pack2(p0 * (dp[j] - sd[jj]), p1 * (dp[j + 1] - sd[jj + 1]));
         }
       }
-      tc::mbar_wait(pempty, (t & 1) ^ 1);
-      uint8_t* pa = sPT + h * kAtom;
-      uint8_t* da = sDS + h * kAtom;
+      const int pb = t % NP;
+      tc::mbar_wait(&pempty[pb], ((t / NP) & 1) ^ 1);
+      uint8_t* pa = sPD + pb * 4 * kAtom + h * kAtom;
+      uint8_t* da = pa + 2 * kAtom;
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         st_sw128(pa, row, c, make_uint4(pk[c * 4], pk[c * 4 + 1], pk[c * 4 + 2], pk[c * 4 + 3]));
         st_sw128(da, row, c, make_uint4(dk[c * 4], dk[c * 4 + 1], dk[c * 4 + 2], dk[c * 4 + 3]));
       }
       tc::fence_async_smem();
-      tc::mbar_arrive(pfull);
+      tc::mbar_arrive(&pfull[pb]);
       if (t > 0) drain_dt(t - 1);
     }
     drain_dt(T - 1);
@@ -565,14 +572,22 @@ size_t fwd_smem(int C2) {
 }
 constexpr size_t kSmemMax = 232448;   // 227 KB opt-in per CTA
 // fixed part (phi, g, P^T, dS^T) + NS stages; the largest NS <= 4 that fits
-int bwd_stages(int C2, size_t* smem) {
+// NP (P/dS buffers) = 2 only when a 3-stage theta/dO ring still fits (measured: NP 2 with a 2-stage ring is
+// slower than NP 1 with 3 stages for D's block, 2.4 vs 2.2 ms), else 1; then the largest NS <= 4
+int bwd_stages(int C2, size_t* smem, int* np) {
   const size_t g = C2 > 64 ? 2 : 1;
-  const size_t fixed = 1024 + (1 + g + 4) * kAtom + 256;
   const size_t stage = (1 + g) * kAtom + 1024;
-  int ns = (int)((kSmemMax - fixed) / stage);
-  if (ns > 4) ns = 4;
-  *smem = fixed + ns * stage;
-  return ns;
+  for (int p = 2; p >= 1; --p) {
+    const size_t fixed = (1 + g + 4 * (size_t)p) * kAtom + 256;
+    int ns = (int)((kSmemMax - fixed) / stage);
+    if (ns > 4) ns = 4;
+    if (ns >= 3 || p == 1) {
+      *np = p;
+      *smem = fixed + ns * stage;
+      return ns;
+    }
+  }
+  return 0;
 }
 
 }  // namespace
@@ -605,10 +620,11 @@ cudaError_t tc_attn_bwd(const TcAttnArgs& a, cudaStream_t st) {
   PG_CUDA(map3(&mg, a.gp, a.C2, a.Q, a.n, 64, kT));
   PG_CUDA(map3(&mo, a.dO, a.C2, a.HW, a.n, 64, kT));
   size_t smem = 0;
-  const int ns = bwd_stages(a.C2, &smem);
+  int np = 1;
+  const int ns = bwd_stages(a.C2, &smem, &np);
   if (ns < 2) return cudaErrorInvalidValue;
   PG_CUDA(cudaFuncSetAttribute(k_attn_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_attn_bwd<<<a.n * (a.Q / kT), kBwdThreads, smem, st>>>(mq, mk, mg, mo, a, ns);
+  k_attn_bwd<<<a.n * (a.Q / kT), kBwdThreads, smem, st>>>(mq, mk, mg, mo, a, ns, np);
   return cudaGetLastError();
 }
 
