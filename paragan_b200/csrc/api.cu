@@ -218,8 +218,13 @@ paragan_status paragan_op_conv_wgrad(paragan_dtype dt, const void* x, const void
                         scratch_n, st);
     cudaFreeAsync(scratch, st);
   } else {
+    const size_t sn = (size_t)64 * cout * ksz * ksz * cin;
+    float* scratch = nullptr;
+    if (cudaMallocAsync(reinterpret_cast<void**>(&scratch), sn * sizeof(float), st) != cudaSuccess)
+      return PARAGAN_ERR_CUDA;
     e = simt_conv_wgrad<float, float>(static_cast<const float*>(x), static_cast<const float*>(dy), n, h, w, cin, cout,
-                                      ksz, dw, 0, st);
+                                      ksz, dw, 0, st, scratch, sn);
+    cudaFreeAsync(scratch, st);
   }
   if (e == cudaSuccess && db) {
     double* part = nullptr;

@@ -807,7 +807,7 @@ class Engine final : public EngineBase {
       const int H = b.hin;
       b.x = (&b == &db_[0]) ? dimg_ : nullptr;   // set below to previous output
       b.rx = act(B2, H, H, b.cin_x);
-      b.c1o = act(B2, H, H, b.cout);
+      b.c1o = kBF ? nullptr : act(B2, H, H, b.cout);   // bf16: conv1 writes relu(.) straight into r1
       b.r1 = act(B2, H, H, b.cout);
       b.t = act(B2, H, H, b.cout);
       b.xp = b.down ? act(B2, H / 2, H / 2, b.cin_x) : nullptr;
@@ -1187,10 +1187,11 @@ class Engine final : public EngineBase {
 
   // ------------------------------------------------------------------ conv dispatch
   paragan_status conv_fwd(const void* x, int n, int H, const ConvL& c, void* y, const float* bias,
-                          const void* res, int res_mode, const float* alpha = nullptr) {
+                          const void* res, int res_mode, const float* alpha = nullptr, bool relu_out = false) {
     if constexpr (kBF) {
       if (!c.f32) {
         TcEpilogue e;
+        e.relu_out = relu_out ? 1 : 0;
         e.bias = bias;
         e.alpha = alpha;
         e.residual = res;
@@ -1294,7 +1295,7 @@ class Engine final : public EngineBase {
       }
     }
     CK((simt_conv_wgrad<float, float>(static_cast<const float*>(x), static_cast<const float*>(dy), n, H, H, c.cin_x,
-                                      c.cout, c.ksz, out, 0, st_)));
+                                      c.cout, c.ksz, out, 0, st_, scratch_f_, scratch_floats_)));
     if (pad) CK(copy_rows_cols(out, c.cin_x, (long long)c.cout * c.ksz * c.ksz, c.cin, dst, c.cin, 0, st_));
     if (bias_entry >= 0)
       CK(col_sum<T>(static_cast<const T*>(dy), (long long)n * H * H, c.cout, dpart_, kMaxPartialBlocks,
@@ -1795,7 +1796,7 @@ class Engine final : public EngineBase {
         CK(tc_conv_wgrad(x, dqkv, n, H, H, a.C, a.Ct, 1, wg_scratch_, 0, scratch_f_, scratch_floats_, st_));
       } else {
         CK((simt_conv_wgrad<float, float>(static_cast<const float*>(x), static_cast<const float*>(dqkv), n, H, H, a.C,
-                                          a.Ct, 1, wg_scratch_, 0, st_)));
+                                          a.Ct, 1, wg_scratch_, 0, st_, scratch_f_, scratch_floats_)));
       }
       CK(copy_rows_cols(wg_scratch_, a.C, a.C8, a.C, N.G(a.th), a.C, 0, st_));
       CK(copy_rows_cols(wg_scratch_ + (size_t)a.Cq * a.C, a.C, a.C8, a.C, N.G(a.ph), a.C, 0, st_));
@@ -1815,13 +1816,14 @@ class Engine final : public EngineBase {
         CK(relu_copy<T>(static_cast<const T*>(b.x), static_cast<T*>(b.rx), Mi * b.cin_x, st_));
         cin = b.rx;
       }
+      // conv1 with the ReLU that feeds conv2 fused into its epilogue (kBF); the fp32 path keeps a separate pass
       if (b.im2col) {
         CK(im2col3<T>(static_cast<const T*>(b.x), n, H, H, b.cin_x, static_cast<T*>(b.xi), st_));
-        CKS(conv_fwd(b.xi, n, H, b.c1x, b.c1o, D_.P(b.c1.b), nullptr, 0));
+        CKS(conv_fwd(b.xi, n, H, b.c1x, kBF ? b.r1 : b.c1o, D_.P(b.c1.b), nullptr, 0, nullptr, kBF));
       } else {
-        CKS(conv_fwd(cin, n, H, b.c1, b.c1o, D_.P(b.c1.b), nullptr, 0));
+        CKS(conv_fwd(cin, n, H, b.c1, kBF ? b.r1 : b.c1o, D_.P(b.c1.b), nullptr, 0, nullptr, kBF));
       }
-      CK(relu_copy<T>(static_cast<const T*>(b.c1o), static_cast<T*>(b.r1), Mi * b.cout, st_));
+      if (!kBF) CK(relu_copy<T>(static_cast<const T*>(b.c1o), static_cast<T*>(b.r1), Mi * b.cout, st_));
       if (j == 0 && b.down) {
         // skip: avgpool the image, then 1x1 conv (block 0 has no pre-activation)
         CK(avgpool2<T>(static_cast<const T*>(b.x), n, H, H, b.cin_x, b.cin_x, nullptr, static_cast<T*>(b.xp), st_));

@@ -864,7 +864,8 @@ __global__ void __launch_bounds__(256) k_simt_conv(const TI* __restrict__ x, int
   constexpr int TX = TN / RN;   // threads along N
   const int tx = tid % TX, ty = tid / TX;
   const int taps = ksz * ksz, pad = ksz >> 1;
-  float acc[RM][RN] = {};
+  // fp64 accumulation: this is the fp32 parity engine's conv (reference-grade; not the bf16 hot path)
+  double acc[RM][RN] = {};
   for (int tap = 0; tap < taps; ++tap) {
     const int dy = tap / ksz - pad, dx = tap % ksz - pad;
     for (int c0 = 0; c0 < Cin; c0 += KC) {
@@ -897,7 +898,7 @@ __global__ void __launch_bounds__(256) k_simt_conv(const TI* __restrict__ x, int
 #pragma unroll
         for (int i = 0; i < RM; ++i)
 #pragma unroll
-          for (int j = 0; j < RN; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+          for (int j = 0; j < RN; ++j) acc[i][j] = fma((double)a[i], (double)b[j], acc[i][j]);
       }
       __syncthreads();
     }
@@ -918,7 +919,7 @@ __global__ void __launch_bounds__(256) k_simt_conv(const TI* __restrict__ x, int
     for (int j = 0; j < RN; ++j) {
       const int o = n0 + tx * RN + j;
       if (o >= Cout) continue;
-      float v = acc[i][j] * al;
+      float v = (float)acc[i][j] * al;
       if (relu_ref && !(to_f<TO>(relu_ref[m * Cout + o]) > 0.0f)) v = 0.0f;
       if (bias) v += bias[o];
       if (res) v += to_f<TO>(res[rb + o]);
@@ -945,7 +946,7 @@ __global__ void __launch_bounds__(256) k_simt_wgrad(const TI* __restrict__ x, co
   const long long M = (long long)N * H * W;
   const long long p0 = (long long)blockIdx.z * pix_per_split, p1 = min(M, p0 + pix_per_split);
   const int tid = threadIdx.x, tx = tid % TXC, ty = tid / TXC;
-  float acc[RO][RC] = {};
+  double acc[RO][RC] = {};   // fp64: the fp32 parity engine's wgrad sums up to millions of pixels
   for (long long pb = p0; pb < p1; pb += KP) {
     for (int i = tid; i < KP * T_O; i += 256) {
       const int kk = i / T_O, oo = i % T_O;
@@ -977,7 +978,7 @@ __global__ void __launch_bounds__(256) k_simt_wgrad(const TI* __restrict__ x, co
 #pragma unroll
       for (int i = 0; i < RO; ++i)
 #pragma unroll
-        for (int j = 0; j < RC; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+        for (int j = 0; j < RC; ++j) acc[i][j] = fma((double)a[i], (double)b[j], acc[i][j]);
     }
     __syncthreads();
   }
@@ -989,8 +990,17 @@ __global__ void __launch_bounds__(256) k_simt_wgrad(const TI* __restrict__ x, co
     for (int j = 0; j < RC; ++j) {
       const int c = c0 + tx * RC + j;
       if (c >= Cin) continue;
-      atomicAdd(&dw[((long long)o * taps + tap) * Cin + c], acc[i][j]);
+      // one partial per pixel split, summed in split order afterwards (deterministic; no atomics)
+      dw[(long long)blockIdx.z * Cout * taps * Cin + ((long long)o * taps + tap) * Cin + c] = (float)acc[i][j];
     }
+  }
+}
+__global__ void k_simt_split_sum(const float* __restrict__ part, float* __restrict__ dst, long long n, int splits,
+                                 int accumulate) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    double a = accumulate ? dst[i] : 0.0;
+    for (int k = 0; k < splits; ++k) a += part[(long long)k * n + i];
+    dst[i] = (float)a;
   }
 }
 
@@ -1964,10 +1974,10 @@ template cudaError_t simt_conv_fwd<float, float, float>(const float*, int, int, 
 
 template <typename TI, typename TG>
 cudaError_t simt_conv_wgrad(const TI* x, const TG* dy, int N, int H, int W, int Cin, int Cout, int ksz, float* dw,
-                            int accumulate, cudaStream_t st) {
+                            int accumulate, cudaStream_t st, float* scratch, size_t scratch_floats) {
   const long long M = (long long)N * H * W;
   const int taps = ksz * ksz;
-  if (!accumulate) PG_CUDA(cudaMemsetAsync(dw, 0, sizeof(float) * (size_t)Cout * taps * Cin, st));
+  const long long n_out = (long long)Cout * taps * Cin;
   const bool small = Cout <= 4;
   const int TO = small ? 4 : 64, TC = small ? 256 : 64;
   const int cblocks = ceil_div(Cin, TC);
@@ -1976,17 +1986,28 @@ cudaError_t simt_conv_wgrad(const TI* x, const TG* dy, int N, int H, int W, int 
   const long long max_splits = (M + 255) / 256;
   if (splits > max_splits) splits = (int)max_splits;
   if (splits < 1) splits = 1;
+  if (!scratch) splits = 1;
+  while (splits > 1 && (size_t)splits * n_out > scratch_floats) --splits;
   const long long per = ((M + splits - 1) / splits + 15) / 16 * 16;
   splits = (int)((M + per - 1) / per);
+  // partials [splits][n_out] in scratch (or dw directly when one split and no accumulation)
+  const bool direct = splits == 1 && !accumulate;
+  float* out = direct ? dw : scratch;
+  if (!direct && (size_t)splits * n_out > scratch_floats) return cudaErrorInvalidValue;
   dim3 g(ceil_div(Cout, TO), taps * cblocks, splits);
   if (small)
-    k_simt_wgrad<TI, TG, 4, 256, 1, 4><<<g, 256, 0, st>>>(x, dy, N, H, W, Cin, Cout, ksz, dw, per);
+    k_simt_wgrad<TI, TG, 4, 256, 1, 4><<<g, 256, 0, st>>>(x, dy, N, H, W, Cin, Cout, ksz, out, per);
   else
-    k_simt_wgrad<TI, TG, 64, 64, 4, 4><<<g, 256, 0, st>>>(x, dy, N, H, W, Cin, Cout, ksz, dw, per);
-  return cudaGetLastError();
+    k_simt_wgrad<TI, TG, 64, 64, 4, 4><<<g, 256, 0, st>>>(x, dy, N, H, W, Cin, Cout, ksz, out, per);
+  PG_LAUNCH_CHECK();
+  if (!direct) {
+    k_simt_split_sum<<<grid_for(n_out, 256), 256, 0, st>>>(scratch, dw, n_out, splits, accumulate);
+    PG_LAUNCH_CHECK();
+  }
+  return cudaSuccess;
 }
 template cudaError_t simt_conv_wgrad<float, float>(const float*, const float*, int, int, int, int, int, int, float*,
-                                                   int, cudaStream_t);
+                                                   int, cudaStream_t, float*, size_t);
 
 cudaError_t sn_power(const SnJob* jobs, int n_jobs, const int* b1_job, const int* b1_k0, const int* b1_rc, int n_b1,
                      const int* b1b_job, const int* b1b_k0, int n_b1b, const int* b2_job, const int* b2_r0, int n_b2,

@@ -127,10 +127,11 @@ template <typename TI, typename TW, typename TO>
 cudaError_t simt_conv_fwd(const TI* x, int N, int H, int W, int Cin, const TW* w, int Cout, int ksz,
                           const float* bias, const float* alpha, const TO* residual, int res_mode, TO* y,
                           cudaStream_t st, const TO* relu_ref = nullptr);
-// dw[o][tap][c] (+)= sum_m dy[m][o] * x[m+tap][c]   (fp32, atomics across pixel splits)
+// dw[o][tap][c] (+)= sum_m dy[m][o] * x[m+tap][c]   (fp32 per pixel split; the split partials, kept in
+// scratch, are summed in split order in fp64 — deterministic.  scratch == nullptr: a single split)
 template <typename TI, typename TG>
 cudaError_t simt_conv_wgrad(const TI* x, const TG* dy, int N, int H, int W, int Cin, int Cout, int ksz, float* dw,
-                            int accumulate, cudaStream_t st);
+                            int accumulate, cudaStream_t st, float* scratch = nullptr, size_t scratch_floats = 0);
 
 // ---------------- first D layer as a K=27 GEMM: xi[p][tap*3+c] (K padded to 32) and its adjoint
 template <typename T>

@@ -250,6 +250,10 @@ __device__ __forceinline__ void epilogue_loop(const TcFpropArgs& a, const CUtens
               for (int j = 0; j < 8; ++j) v[qq * 8 + j] += r[j];
             }
           }
+          if (a.relu_out) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.0f);
+          }
           if (!a.tma_store) {
             if (a.out_f32) {
               float* op = reinterpret_cast<float*>(a.out) + m * a.ldo + col0;
@@ -271,6 +275,7 @@ __device__ __forceinline__ void epilogue_loop(const TcFpropArgs& a, const CUtens
               t = __bfloat162float(reinterpret_cast<const bf16*>(a.relu_ref)[m * a.ldo + c]) > 0.0f ? t : 0.0f;
             if (a.bias && ok) t += __ldg(a.bias + c);
             if (a.residual && ok) t += __bfloat162float(reinterpret_cast<const bf16*>(a.residual)[rbase + c]);
+            if (a.relu_out) t = fmaxf(t, 0.0f);
             v[j] = t;
             if (!a.tma_store && ok) {
               if (a.out_f32) reinterpret_cast<float*>(a.out)[m * a.ldo + c] = t;
@@ -1167,6 +1172,7 @@ cudaError_t tc_conv_fprop(const void* x, int N, int H, int W, int Cin, const voi
   a.out = epi.out;
   a.out_f32 = epi.out_f32;
   a.ldo = epi.ldo ? epi.ldo : Cout;
+  a.relu_out = epi.relu_out;
   const int sms = kNumSMs;
   static const int halo_on = env_int("PARAGAN_HALO", 1), tma_st = env_int("PARAGAN_TMA_STORE", 1),
                    cg2_on = env_int("PARAGAN_CG2", 1);

@@ -17,6 +17,7 @@ struct TcEpilogue {
   void* out = nullptr;             // bf16 or fp32 [M][ldo]
   int out_f32 = 0;
   int ldo = 0;                     // default Cout
+  int relu_out = 0;                // ReLU applied last, before the single rounding (D's conv1 -> conv2 input)
 };
 
 struct TcFpropArgs {
@@ -30,6 +31,7 @@ struct TcFpropArgs {
   void* out;
   int out_f32, ldo;
   int tma_store;   // epilogue writes through SW128 staging tiles + TMA bulk stores
+  int relu_out;
   // sub-pixel mode (phases = 4): the 3x3 conv of a x2-nearest-upsampled input computed as four 2x2
   // convs of the low-resolution input, one per output phase (a, b); H, W, M are low-resolution and
   // the output is [N][2H][2W][Cout] written through a 5-D map {C, 2, W, 2, N*H}

@@ -182,10 +182,13 @@ def test_d_step_isolated_f32_biggan512():
 
 def test_step_parity_f32_biggan256_ratio2():
     """Config 4's asymmetric D:G step ratio 2:1 on BigGAN-256 shapes (one image): two D steps, each
-    updating D, then the G step against the twice-updated D — bars as the BigGAN-128 full step."""
+    updating D, then the G step against the twice-updated D.  D's arithmetic alone is at ~2e-7
+    (test_d_step_isolated_*); here the second D step starts from weights after Adam's first step,
+    ~ -lr * sign(g), whose sign is indeterminate for gradients at the fp32 noise level — those elements
+    move by 2 lr between the two computations, so the bars are 2e-3 (D) / 5e-3 (G), measured 6.4e-4."""
     ocfg = P.oracle_config(256, 96, 64, 1000, 128, 20, n_d=2, bf16=False)
     cfg = api.make_config(resolution=256, local_batch=1, d_steps_per_g=2, compute=api.F32)
-    got = _check(ocfg, cfg, 1, seed=27, tol=5e-4, n_d=2, tensor_tol=1e-2, g_global_tol=5e-3, per_tensor_state=False)
+    got = _check(ocfg, cfg, 1, seed=27, tol=2e-3, n_d=2, tensor_tol=1e-2, g_global_tol=5e-3, per_tensor_state=False)
     assert got["stats"].t_d == 2 and got["stats"].t_g == 1
 
 
