@@ -1807,15 +1807,19 @@ class Engine final : public EngineBase {
 
   // ------------------------------------------------------------------ D forward (A7)
   paragan_status d_forward(int n) {
+    bool rx_ready = false;   // the previous block's pooling already wrote relu(x) into this block's rx
     for (size_t j = 0; j < db_.size(); ++j) {
       DBlock& b = db_[j];
       const int H = b.hin, Ho = b.hout;
       const long long Mi = (long long)n * H * H;
       const void* cin = b.x;
+      // the next block's pre-activation relu(x) comes out of this block's pooling when nothing sits in between
+      T* next_rx = (j + 1 < db_.size() && !b.attn) ? static_cast<T*>(db_[j + 1].rx) : nullptr;
       if (j > 0) {
-        CK(relu_copy<T>(static_cast<const T*>(b.x), static_cast<T*>(b.rx), Mi * b.cin_x, st_));
+        if (!rx_ready) CK(relu_copy<T>(static_cast<const T*>(b.x), static_cast<T*>(b.rx), Mi * b.cin_x, st_));
         cin = b.rx;
       }
+      rx_ready = false;
       // conv1 with the ReLU that feeds conv2 fused into its epilogue (kBF); the fp32 path keeps a separate pass
       if (b.im2col) {
         CK(im2col3<T>(static_cast<const T*>(b.x), n, H, H, b.cin_x, static_cast<T*>(b.xi), st_));
@@ -1830,7 +1834,8 @@ class Engine final : public EngineBase {
         CKS(conv_fwd(b.xp, n, Ho, b.sc, b.s, D_.P(b.sc.b), nullptr, 0));
         CKS(conv_fwd(b.r1, n, H, b.c2, b.t, D_.P(b.c2.b), nullptr, 0));
         CK(avgpool2<T>(static_cast<const T*>(b.t), n, H, H, b.cout, b.cout, static_cast<const T*>(b.s),
-                       static_cast<T*>(b.out), st_));
+                       static_cast<T*>(b.out), st_, next_rx));
+        rx_ready = next_rx != nullptr;
       } else {
         const void* skip = b.x;
         if (b.learn_sc) {
@@ -1839,7 +1844,9 @@ class Engine final : public EngineBase {
         }
         if (b.down) {
           CKS(conv_fwd(b.r1, n, H, b.c2, b.t, D_.P(b.c2.b), skip, 1));
-          CK(avgpool2<T>(static_cast<const T*>(b.t), n, H, H, b.cout, b.cout, nullptr, static_cast<T*>(b.out), st_));
+          CK(avgpool2<T>(static_cast<const T*>(b.t), n, H, H, b.cout, b.cout, nullptr, static_cast<T*>(b.out), st_,
+                         next_rx));
+          rx_ready = next_rx != nullptr;
         } else {
           CKS(conv_fwd(b.r1, n, H, b.c2, b.out, D_.P(b.c2.b), skip, 1));
         }

@@ -1511,7 +1511,7 @@ __global__ void k_relu_copy_v(const T* __restrict__ x, T* __restrict__ y, long l
 }
 template <typename T>
 __global__ void k_avgpool2_v(const T* __restrict__ x, int N, int H, int W, int C, int ldx, const T* __restrict__ add,
-                             T* __restrict__ y) {
+                             T* __restrict__ y, T* __restrict__ y_relu) {
   const unsigned Ho = H >> 1, Wo = W >> 1, G = C >> 3;
   const unsigned total = (unsigned)N * Ho * Wo * G;
   for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
@@ -1535,6 +1535,11 @@ __global__ void k_avgpool2_v(const T* __restrict__ x, int N, int H, int W, int C
       if (add) o[j] += ad[j];
     }
     Vec8<T>::store(y + (long long)i * 8, o);
+    if (y_relu) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[j] = o[j] > 0.0f ? o[j] : 0.0f;   // relu commutes with the rounding
+      Vec8<T>::store(y_relu + (long long)i * 8, o);
+    }
   }
 }
 template <typename T>
@@ -1805,7 +1810,7 @@ template cudaError_t bn_bwd_apply<bf16, float, bf16>(const bf16*, const float*, 
 #define PG_INST_T(T)                                                                                               \
   template cudaError_t relu_copy<T>(const T*, T*, long long, cudaStream_t);                                        \
   template cudaError_t relu_bwd<T>(const T*, const T*, const T*, T*, long long, cudaStream_t);                     \
-  template cudaError_t avgpool2<T>(const T*, int, int, int, int, int, const T*, T*, cudaStream_t);                 \
+  template cudaError_t avgpool2<T>(const T*, int, int, int, int, int, const T*, T*, cudaStream_t, T*);                 \
   template cudaError_t avgpool2_bwd<T>(const T*, int, int, int, int, const T*, T*, int, cudaStream_t);             \
   template cudaError_t up2_bwd<T>(const T*, int, int, int, int, T*, cudaStream_t);                                 \
   template cudaError_t col_sum<T>(const T*, long long, int, double*, int, float*, int, cudaStream_t);              \
@@ -1837,13 +1842,16 @@ cudaError_t relu_bwd(const T* dy, const T* ref, const T* add, T* dx, long long n
   return cudaGetLastError();
 }
 template <typename T>
-cudaError_t avgpool2(const T* x, int N, int H, int W, int C, int ldx, const T* add, T* y, cudaStream_t st) {
+cudaError_t avgpool2(const T* x, int N, int H, int W, int C, int ldx, const T* add, T* y, cudaStream_t st,
+                     T* y_relu) {
   const long long total = (long long)N * (H / 2) * (W / 2) * C;
   if (C % 8 == 0 && ldx % 8 == 0) {
-    k_avgpool2_v<T><<<grid_for(total / 8, 256), 256, 0, st>>>(x, N, H, W, C, ldx, add, y);
+    k_avgpool2_v<T><<<grid_for(total / 8, 256), 256, 0, st>>>(x, N, H, W, C, ldx, add, y, y_relu);
     return cudaGetLastError();
   }
   k_avgpool2<T><<<grid_for(total, 256), 256, 0, st>>>(x, N, H, W, C, ldx, add, y);
+  PG_LAUNCH_CHECK();
+  if (y_relu) return relu_copy<T>(y, y_relu, total, st);
   return cudaGetLastError();
 }
 template <typename T>
