@@ -73,7 +73,8 @@ def main():
         for key, specs in (("d_grads", ds), ("g_grads", gs)):
             out[key + "_global"] = P.rel(got[key], want[key])
             if compute == api.F32:
-                bad, worst = P.compare_tensors(specs, got[key], want[key], tol)
+                # SN-DCGAN's deconv biases feed BNs: exact gradient 0, fp32 residual ~1e-5 of the RMS gradient
+                bad, worst = P.compare_tensors(specs, got[key], want[key], tol, floor_frac=1e-1 if dcgan else 1e-2)
                 out[key + "_bad"] = [b[0] for b in bad]
                 out[key + "_worst"] = max(worst.values())
                 gbar = tol
