@@ -271,7 +271,7 @@ def main():
             for i in range(args.steps):
                 step(i)
             ctx.profile(False)
-            for kind in (0, 1, 2):
+            for kind in (0, 1, 2, 3, 4):
                 prof[kind] = ctx.profile_read(kind)
             barrier()
 
@@ -289,8 +289,13 @@ def main():
                     "traffic": traffic.get("conv_fprop", {}).get("dram_bytes_per_launch"),
                     "traffic_source": traffic.get("source"), "launches": n0, "kernel_ms_per_step": t0 / args.steps,
                     "share_of_step": (t0 / args.steps) / (ms_max / args.steps),
-                    "wgrad": {"achieved": (f1_ / (t1 / 1000.0)) / 1e12 if t1 > 0 else 0.0, "launches": n1,
-                              "ms_per_step": t1 / args.steps}}
+                    "achieved_executed": (prof[3][2] / (t0 / 1000.0)) / 1e12 if t0 > 0 else 0.0,
+                    "note": "achieved = algorithmic flops (G's conv1 over the upsampled tensor, SURVEY 8(d)) / time; "
+                            "achieved_executed = flops issued to the tensor cores (sub-pixel conv1: 1/2.25 of its "
+                            "algorithmic work) / time",
+                    "wgrad": {"achieved": (f1_ / (t1 / 1000.0)) / 1e12 if t1 > 0 else 0.0,
+                              "achieved_executed": (prof[4][2] / (t1 / 1000.0)) / 1e12 if t1 > 0 else 0.0,
+                              "launches": n1, "ms_per_step": t1 / args.steps}}
             if world > 1:
                 n2, t2, b2 = prof[2]
                 roof["collectives"] = {"launches_per_step": n2 / args.steps, "ms_per_step": t2 / args.steps,

@@ -183,7 +183,10 @@ paragan_status paragan_kernel_launches(const paragan_ctx* ctx, uint64_t* n);
  * fprop/dgrad kernel, 1 = wgrad (incl. its split-K reduction), 2 = NCCL collectives
  * (gradient, cross-replica BN and loss all-reduces), the number of launches, their
  * summed device time (ms) and their ALGORITHMIC flops (2*M*N*K with unpadded channel
- * counts; for kind 2: bytes reduced).  enable=1 also clears the record. */
+ * counts, G's conv1 counted over the upsampled tensor as BigGAN defines it; for kind 2:
+ * bytes reduced).  Kinds 3 / 4: the launches of kinds 0 / 1 with the flops actually
+ * issued to the tensor cores (the sub-pixel conv1 issues 1/2.25 of its algorithmic
+ * work).  enable=1 also clears the record. */
 paragan_status paragan_profile(paragan_ctx* ctx, int32_t enable);
 paragan_status paragan_profile_read(paragan_ctx* ctx, int32_t kind, uint64_t* launches, double* ms, double* flops);
 

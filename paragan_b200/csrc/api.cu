@@ -153,7 +153,7 @@ paragan_status paragan_profile(paragan_ctx* ctx, int32_t enable) {
   return ctx->eng->profile(enable);
 }
 paragan_status paragan_profile_read(paragan_ctx* ctx, int32_t kind, uint64_t* launches, double* ms, double* flops) {
-  if (!ctx || !ctx->eng || kind < 0 || kind > 2) return PARAGAN_ERR_INVALID_ARG;
+  if (!ctx || !ctx->eng || kind < 0 || kind > 4) return PARAGAN_ERR_INVALID_ARG;
   return ctx->eng->profile_read(kind, launches, ms, flops);
 }
 const char* paragan_last_error(const paragan_ctx* ctx) {

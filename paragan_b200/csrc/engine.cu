@@ -474,14 +474,18 @@ class Engine final : public EngineBase {
     uint64_t c = 0;
     double t = 0, f = 0;
     const bool verbose = std::getenv("PARAGAN_PROFILE_VERBOSE") != nullptr;
+    // kinds 3 / 4: the launches of kinds 0 / 1 with their executed instead of algorithmic flops
+    const int k = kind >= 3 ? kind - 3 : kind;
     for (auto& r : recs_) {
-      if (r.kind != kind) continue;
+      if (r.kind != k) continue;
       float e = 0;
       if (cudaEventElapsedTime(&e, r.a, r.b) != cudaSuccess) return fail_cuda(cudaGetLastError(), "event time");
       ++c;
       t += e;
-      f += r.flops;
-      if (verbose) std::fprintf(stderr, "PROF kind=%d ms=%.4f tflops=%.1f %s\n", kind, e, r.flops / (e * 1e9), r.what);
+      f += kind >= 3 ? r.exec_flops : r.flops;
+      if (verbose)
+        std::fprintf(stderr, "PROF kind=%d ms=%.4f tflops=%.1f exec_tflops=%.1f %s\n", k, e, r.flops / (e * 1e9),
+                     r.exec_flops / (e * 1e9), r.what);
     }
     if (n) *n = c;
     if (ms) *ms = t;
@@ -1158,9 +1162,10 @@ class Engine final : public EngineBase {
 
   struct ProfRec {
     int kind;
-    double flops;
+    double flops;        // algorithmic (the BigGAN-defined work of the launch)
     cudaEvent_t a, b;
     char what[48];
+    double exec_flops;   // what the tensor cores were issued (differs for the sub-pixel G conv1)
   };
   cudaEvent_t ev_get() {
     if (!ev_free_.empty()) {
@@ -1174,9 +1179,9 @@ class Engine final : public EngineBase {
   }
   // brackets one launch with events when profiling; kind 0 = tcgen05 fprop/dgrad, 1 = tcgen05 wgrad
   template <class F>
-  cudaError_t timed(int kind, double flops, F&& f, const char* what = "") {
+  cudaError_t timed(int kind, double flops, F&& f, const char* what = "", double exec_flops = -1.0) {
     if (!prof_) return f();
-    ProfRec r{kind, flops, ev_get(), ev_get(), {0}};
+    ProfRec r{kind, flops, ev_get(), ev_get(), {0}, exec_flops < 0 ? flops : exec_flops};
     std::snprintf(r.what, sizeof(r.what), "%s", what);
     cudaEventRecord(r.a, st_);
     cudaError_t e = f();
@@ -1215,12 +1220,13 @@ class Engine final : public EngineBase {
       TcEpilogue e;
       e.bias = bias;
       e.out = y;
-      // executed tensor work: 4 phases x 4 taps per low-resolution pixel (the 9-tap conv on the
-      // upsampled tensor would be 2.25x this)
-      const double fl = 2.0 * n * H * H * 16.0 * c.cout * c.cin;
+      // algorithmic work: the 3x3 conv over the upsampled tensor; executed: 4 phases x 4 taps
+      // per low-resolution pixel, 1/2.25 of it
+      const double fl = 2.0 * n * (4.0 * H * H) * 9.0 * c.cout * c.cin;
+      const double fx = 2.0 * n * H * H * 16.0 * c.cout * c.cin;
       char what[48];
       std::snprintf(what, sizeof(what), "fprop-up2 n%d %dx%d %d->%d", n, H, H, c.cin, c.cout);
-      CK(timed(0, fl, [&] { return tc_conv_fprop_up2(x, n, H, H, c.cin, c.wp4, c.cout, e, st_); }, what));
+      CK(timed(0, fl, [&] { return tc_conv_fprop_up2(x, n, H, H, c.cin, c.wp4, c.cout, e, st_); }, what, fx));
       return PARAGAN_OK;
     }
     return fail_msg(PARAGAN_ERR_CONFIG, "sub-pixel conv needs the BF16 engine");
@@ -1228,13 +1234,14 @@ class Engine final : public EngineBase {
   // conv3x3(up2(x)) backward through the phase decomposition (BF16 only): dW + db into the grad slots
   paragan_status conv_wgrad_up2(const void* x_lo, const void* dy, int n, int H, const ConvL& c) {
     if constexpr (kBF) {
-      const double fl = 2.0 * n * H * H * 16.0 * c.cout * c.cin;
+      const double fl = 2.0 * n * (4.0 * H * H) * 9.0 * c.cout * c.cin;
+      const double fx = 2.0 * n * H * H * 16.0 * c.cout * c.cin;
       char what[48];
       std::snprintf(what, sizeof(what), "wgrad-up2 n%d %dx%d %d->%d", n, H, H, c.cin, c.cout);
       float* db = c.b >= 0 ? G_.G(c.b) : nullptr;
       CK(timed(1, fl, [&] {
         return tc_conv_wgrad_up2(x_lo, dy, n, H, H, c.cin, c.cout, G_.G(c.w), scratch_f_, scratch_floats_, st_, db);
-      }, what));
+      }, what, fx));
       return PARAGAN_OK;
     }
     return fail_msg(PARAGAN_ERR_CONFIG, "sub-pixel conv needs the BF16 engine");
@@ -1243,10 +1250,11 @@ class Engine final : public EngineBase {
     if constexpr (kBF) {
       TcEpilogue e;
       e.out = dx_lo;
-      const double fl = 2.0 * n * H * H * 16.0 * c.cout * c.cin;
+      const double fl = 2.0 * n * (4.0 * H * H) * 9.0 * c.cout * c.cin;
+      const double fx = 2.0 * n * H * H * 16.0 * c.cout * c.cin;
       char what[48];
       std::snprintf(what, sizeof(what), "dgrad-up2 n%d %dx%d %d->%d", n, H, H, c.cout, c.cin);
-      CK(timed(0, fl, [&] { return tc_conv_dgrad_up2(dy, n, H, H, c.cout, c.wt4, c.cin, e, st_); }, what));
+      CK(timed(0, fl, [&] { return tc_conv_dgrad_up2(dy, n, H, H, c.cout, c.wt4, c.cin, e, st_); }, what, fx));
       return PARAGAN_OK;
     }
     return fail_msg(PARAGAN_ERR_CONFIG, "sub-pixel conv needs the BF16 engine");

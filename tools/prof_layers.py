@@ -5,7 +5,7 @@ import sys
 
 rows = []
 for l in open(sys.argv[1]):
-    m = re.match(r"PROF kind=(\d) ms=([\d.]+) tflops=([\d.]+) (.*)", l.strip())
+    m = re.match(r"PROF kind=(\d) ms=([\d.]+) tflops=([\d.]+)(?: exec_tflops=[\d.]+)? (.*)", l.strip())
     if m:
         rows.append((int(m[1]), float(m[2]), float(m[3]), m[4]))
 agg = collections.defaultdict(lambda: [0, 0.0, 0.0])
