@@ -1116,8 +1116,7 @@ class Engine final : public EngineBase {
         long long acc = 0;
         for (auto& j : lst) {
           st.push_back(acc);
-          acc += pass == 0 ? ceil_div((long long)j.rows * j.taps * j.cin, 256)
-                           : (long long)j.taps * ceil_div(j.rows, 32) * ceil_div(j.cin, 32);
+          acc += pass == 0 ? sn_pack_prepare(j) : (long long)j.taps * ceil_div(j.rows, 32) * ceil_div(j.cin, 32);
         }
         (pass == 0 ? N->pf_blocks : N->pb_blocks) = acc;
         CK(cudaMemcpyAsync(pass == 0 ? N->pf_d : N->pb_d, lst.data(), lst.size() * sizeof(SnPack),

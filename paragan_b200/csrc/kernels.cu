@@ -1279,6 +1279,25 @@ __global__ void __launch_bounds__(256) k_sn_pack(const SnPack* __restrict__ jobs
   }
   const SnPack J = jobs[lo];
   const int n = J.rows * J.taps * J.cin;   // < 2^31 for every weight of the model
+  if (J.vec8) {   // 8 consecutive input channels per thread: two float4 loads, one 16-byte bf16 store
+    const int i = ((int)(b - blk_start[lo]) * 256 + threadIdx.x) * 8;
+    if (i >= n) return;
+    const float inv = J.sigma[1];
+    const float4 a0 = *reinterpret_cast<const float4*>(J.w + i);
+    const float4 a1 = *reinterpret_cast<const float4*>(J.w + i + 4);
+    const int c = i % J.cin, rt = i / J.cin;
+    const int t = rt % J.taps, o = rt / J.taps;
+    const long long d = ((long long)(o + J.dst_row_offset) * J.taps + t) * J.dst_cin + c;
+    uint4 u;
+    __nv_bfloat162 h0 = __floats2bfloat162_rn(a0.x * inv, a0.y * inv), h1 = __floats2bfloat162_rn(a0.z * inv, a0.w * inv);
+    __nv_bfloat162 h2 = __floats2bfloat162_rn(a1.x * inv, a1.y * inv), h3 = __floats2bfloat162_rn(a1.z * inv, a1.w * inv);
+    u.x = *reinterpret_cast<uint32_t*>(&h0);
+    u.y = *reinterpret_cast<uint32_t*>(&h1);
+    u.z = *reinterpret_cast<uint32_t*>(&h2);
+    u.w = *reinterpret_cast<uint32_t*>(&h3);
+    *reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(J.dst) + d) = u;
+    return;
+  }
   const int i = (int)(b - blk_start[lo]) * 256 + threadIdx.x;
   if (i >= n) return;
   const float v = J.w[i] * J.sigma[1];
@@ -1362,26 +1381,46 @@ __global__ void __launch_bounds__(256) k_snb_dot(const SnJob* __restrict__ jobs,
     dotp[blockIdx.x] = t;
   }
 }
-// pass b: coef = <g, W> / sigma^2 (sum of the job's partials in block order)
+// pass b: coef = <g, W> / sigma^2; one warp per job: lane l sums partials l, l + 32, ... in order,
+// then a fixed shuffle tree (deterministic)
 __global__ void k_snb_coef(const SnJob* __restrict__ jobs, int n_jobs, const double* __restrict__ dotp) {
-  const int ji = blockIdx.x * blockDim.x + threadIdx.x;
+  const int ji = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
   if (ji >= n_jobs) return;
   const SnJob j = jobs[ji];
   double t = 0.0;
-  for (long long b = 0; b < j.bwd_nblk; ++b) t += dotp[j.bwd_blk0 + b];
-  const double is = (double)j.sigma[1];
-  j.coef[0] = t * is * is;
+  for (long long b = lane; b < j.bwd_nblk; b += 32) t += dotp[j.bwd_blk0 + b];
+  t = warp_sum_d(t);
+  if (lane == 0) {
+    const double is = (double)j.sigma[1];
+    j.coef[0] = t * is * is;
+  }
 }
-// pass c: g = g / sigma - coef * u[r] * v[k]
+// pass c: g = g / sigma - coef * u[r] * v[k]   (float4 when K % 4 == 0: the 4 elements share a row)
 __global__ void __launch_bounds__(256) k_snb_apply(const SnJob* __restrict__ jobs, const long long* __restrict__ start,
                                                    int n_jobs) {
   const int ji = find_job(start, n_jobs, blockIdx.x);
   const SnJob j = jobs[ji];
-  const long long n = (long long)j.rows * j.K;
-  const long long e0 = (blockIdx.x - start[ji]) * 4096;
+  const int n = j.rows * j.K;   // < 2^31 for every weight of the model
+  const int e0 = (int)(blockIdx.x - start[ji]) * 4096;
+  const int e1 = min(n, e0 + 4096);
   const float c = (float)j.coef[0], inv = j.sigma[1];
-  for (long long i = e0 + threadIdx.x; i < min(n, e0 + 4096); i += 256) {
-    const int r = (int)(i / j.K), k = (int)(i - (long long)r * j.K);
+  if ((j.K & 3) == 0 && ((reinterpret_cast<uintptr_t>(j.grad) | reinterpret_cast<uintptr_t>(j.v)) & 15) == 0) {
+    for (int i = e0 + 4 * threadIdx.x; i < e1; i += 1024) {
+      const int r = i / j.K, k = i - r * j.K;
+      float4 g = *reinterpret_cast<float4*>(j.grad + i);
+      const float4 vv = *reinterpret_cast<const float4*>(j.v + k);
+      const float cu = c * j.u[r];
+      g.x = g.x * inv - cu * vv.x;
+      g.y = g.y * inv - cu * vv.y;
+      g.z = g.z * inv - cu * vv.z;
+      g.w = g.w * inv - cu * vv.w;
+      *reinterpret_cast<float4*>(j.grad + i) = g;
+    }
+    return;
+  }
+  for (int i = e0 + threadIdx.x; i < e1; i += 256) {
+    const int r = i / j.K, k = i - r * j.K;
     j.grad[i] = j.grad[i] * inv - c * j.u[r] * j.v[k];
   }
 }
@@ -1397,20 +1436,42 @@ __global__ void k_check_finite(const float* __restrict__ g, long long n, int* fl
 __global__ void k_check_finite_scalar(const float* loss, int* flag) {
   if (!isfinite(loss[0]) || loss[3] != 0.0f) atomicOr(flag, 1);
 }
+__device__ __forceinline__ float adam_one(float& w, float g, float& m, float& v, float lr, float b1, float b2,
+                                          float eps, float gscale, float bc1, float bc2) {
+  const float gi = g * gscale;
+  const float mi = b1 * m + (1.0f - b1) * gi;
+  const float vi = b2 * v + (1.0f - b2) * gi * gi;
+  m = mi;
+  v = vi;
+  w -= lr * (mi / bc1) / (sqrtf(vi / bc2) + eps);
+  return w;
+}
 __global__ void k_adam(float* __restrict__ w, const float* __restrict__ g, float* __restrict__ m, float* __restrict__ v,
                        long long n, float lr, float b1, float b2, float eps, const long long* __restrict__ t_dev,
                        float gscale, const int* __restrict__ flag) {
   if (*flag) return;
   const double t = (double)(*t_dev + 1);
   const float bc1 = (float)(1.0 - pow((double)b1, t)), bc2 = (float)(1.0 - pow((double)b2, t));
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const float gi = g[i] * gscale;
-    const float mi = b1 * m[i] + (1.0f - b1) * gi;
-    const float vi = b2 * v[i] + (1.0f - b2) * gi * gi;
-    m[i] = mi;
-    v[i] = vi;
-    w[i] -= lr * (mi / bc1) / (sqrtf(vi / bc2) + eps);
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x, nth = (long long)gridDim.x * blockDim.x;
+  const bool vec = ((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(m) |
+                     reinterpret_cast<uintptr_t>(v)) & 15) == 0;
+  long long done = 0;
+  if (vec) {   // float4 body, scalar tail (same arithmetic per element)
+    const long long n4 = n >> 2;
+    for (long long i = tid; i < n4; i += nth) {
+      float4 W = reinterpret_cast<float4*>(w)[i], M = reinterpret_cast<float4*>(m)[i], V = reinterpret_cast<float4*>(v)[i];
+      const float4 Gv = reinterpret_cast<const float4*>(g)[i];
+      adam_one(W.x, Gv.x, M.x, V.x, lr, b1, b2, eps, gscale, bc1, bc2);
+      adam_one(W.y, Gv.y, M.y, V.y, lr, b1, b2, eps, gscale, bc1, bc2);
+      adam_one(W.z, Gv.z, M.z, V.z, lr, b1, b2, eps, gscale, bc1, bc2);
+      adam_one(W.w, Gv.w, M.w, V.w, lr, b1, b2, eps, gscale, bc1, bc2);
+      reinterpret_cast<float4*>(w)[i] = W;
+      reinterpret_cast<float4*>(m)[i] = M;
+      reinterpret_cast<float4*>(v)[i] = V;
+    }
+    done = n4 << 2;
   }
+  for (long long i = done + tid; i < n; i += nth) adam_one(w[i], g[i], m[i], v[i], lr, b1, b2, eps, gscale, bc1, bc2);
 }
 __global__ void k_adam_bookkeep(long long* t_dev, const int* flag, int* sticky) {
   if (*flag) *sticky = 1;
@@ -2029,6 +2090,12 @@ cudaError_t sn_power(const SnJob* jobs, int n_jobs, const int* b1_job, const int
   k_sn_finish<<<n_jobs, 256, 0, st>>>(jobs);
   return cudaGetLastError();
 }
+long long sn_pack_prepare(SnPack& j) {
+  const long long n = (long long)j.rows * j.taps * j.cin;
+  j.vec8 = j.mode == 0 && j.dst_bf16 && j.cin % 8 == 0 && j.dst_cin % 8 == 0 &&
+           ((reinterpret_cast<uintptr_t>(j.w) | reinterpret_cast<uintptr_t>(j.dst)) & 15) == 0;
+  return ceil_div(n, j.vec8 ? 2048 : 256);
+}
 cudaError_t sn_pack(const SnPack* jobs, const long long* blk_start, int n_jobs, long long total_blocks,
                     cudaStream_t st) {
   k_sn_pack<<<(unsigned)total_blocks, 256, 0, st>>>(jobs, blk_start, n_jobs);
@@ -2043,7 +2110,7 @@ cudaError_t sn_backward(const SnJob* jobs, int n_jobs, const long long* blk_star
                         double* dotp, cudaStream_t st) {
   k_snb_dot<<<(unsigned)total_blocks, 256, 0, st>>>(jobs, blk_start, n_jobs, dotp);
   PG_LAUNCH_CHECK();
-  k_snb_coef<<<ceil_div(n_jobs, 128), 128, 0, st>>>(jobs, n_jobs, dotp);
+  k_snb_coef<<<ceil_div(n_jobs, 4), 128, 0, st>>>(jobs, n_jobs, dotp);
   PG_LAUNCH_CHECK();
   k_snb_apply<<<(unsigned)total_blocks, 256, 0, st>>>(jobs, blk_start, n_jobs);
   return cudaGetLastError();
@@ -2120,12 +2187,13 @@ namespace {
 // ---------------------------------------------------------------------------
 // fprop: y[m][o] = bias[o] + sum_{tap,c} x[m+tap][c] w[o][tap][c]
 // tile 32 rows x 64 cols, thread = 8 consecutive pixels of one row (acc[8][CO] in registers);
-// 8-channel halo chunks staged in smem ([c][row][68] planes), weights as [c][28] so each
-// channel's 27 taps x outputs come in 7 broadcast float4 loads; rows slide through 3 float4s.
-constexpr int kFTH = 32, kFTW = 64, kFCC = 8, kFRS = 68;
+// 4-channel halo chunks staged in smem ([c][row][68] planes; 3 blocks per SM, so one stages while
+// the others compute), weights as [c][28] so each channel's 27 taps x outputs come in 7 broadcast
+// float4 loads; rows slide through 3 float4s.
+constexpr int kFTH = 32, kFTW = 64, kFCC = 4, kFRS = 68, kFV = kFCC / 4;
 constexpr int kFPlane = (kFTH + 2) * kFRS;
 template <int CO>
-__global__ void __launch_bounds__(256, 2) k_thin_fwd(const float* __restrict__ x, int N, int H, int W, int C,
+__global__ void __launch_bounds__(256, 3) k_thin_fwd(const float* __restrict__ x, int N, int H, int W, int C,
                                                   const float* __restrict__ w, const float* __restrict__ bias,
                                                   float* __restrict__ y) {
   extern __shared__ float4 sm4[];
@@ -2151,8 +2219,8 @@ __global__ void __launch_bounds__(256, 2) k_thin_fwd(const float* __restrict__ x
   for (int c0 = 0; c0 < C; c0 += kFCC) {
     __syncthreads();
     // halo chunk: batches of 6 independent 16-byte loads per thread in flight, then the planar stores
-    constexpr int kItems = (kFTH + 2) * (kFTW + 2) * 2;
-    constexpr int kBatch = 6;
+    constexpr int kItems = (kFTH + 2) * (kFTW + 2) * kFV;
+    constexpr int kBatch = 9;
     for (int i0 = threadIdx.x; i0 < kItems; i0 += kBatch * 256) {
       float4 v[kBatch];
 #pragma unroll
@@ -2160,7 +2228,7 @@ __global__ void __launch_bounds__(256, 2) k_thin_fwd(const float* __restrict__ x
         const int i = i0 + u * 256;
         v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
         if (i < kItems) {
-          const int half = i & 1, rs = i >> 1;
+          const int half = i % kFV, rs = i / kFV;
           const int sx = rs % (kFTW + 2), r = rs / (kFTW + 2);
           const int h = h0 - 1 + r, ww = w0 - 1 + sx;
           const int c = c0 + half * 4;
@@ -2172,7 +2240,7 @@ __global__ void __launch_bounds__(256, 2) k_thin_fwd(const float* __restrict__ x
       for (int u = 0; u < kBatch; ++u) {
         const int i = i0 + u * 256;
         if (i < kItems) {
-          const int half = i & 1, rs = i >> 1;
+          const int half = i % kFV, rs = i / kFV;
           const int sx = rs % (kFTW + 2), r = rs / (kFTW + 2);
           float* d = xs + half * 4 * kFPlane + r * kFRS + sx;
           d[0] = v[u].x;
@@ -2229,8 +2297,10 @@ __global__ void __launch_bounds__(256, 2) k_thin_fwd(const float* __restrict__ x
 
 // ---------------------------------------------------------------------------
 // dgrad: dx[m][c] = sum_{o,r,s} dy[h+1-r][w+1-s][o] w[o][r][s][c]  (transposed 3x3, pad 1)
-// tile 8 rows x 64 cols; thread = pixels (row, px) and (row, px+32) with their 2 x 27 dy taps in
-// registers; loops over channels in fours: 4 x 7 broadcast float4 weight loads per 216 FMAs.
+// Persistent blocks (weights staged once) walk 8 rows x 64 cols tiles; thread = pixels (row, px)
+// and (row, px+32) with their 2 x 27 dy taps in registers; loops over channels in fours:
+// 4 x 7 broadcast float4 weight loads per 216 FMAs.  The dy halo's loads are all issued before
+// any is stored (one memory round trip per tile).
 constexpr int kDTH = 8, kDTW = 64;
 template <int CO>
 __global__ void __launch_bounds__(256) k_thin_dgrad(const float* __restrict__ dy, int N, int H, int W, int C,
@@ -2239,172 +2309,191 @@ __global__ void __launch_bounds__(256) k_thin_dgrad(const float* __restrict__ dy
   float* ws = reinterpret_cast<float*>(sm4);        // [C][28]
   float* ds = ws + C * 28;                           // [CO][kDTH + 2][kDTW + 2]
   const int tiles_w = (W + kDTW - 1) / kDTW, tiles_h = (H + kDTH - 1) / kDTH;
-  int t = blockIdx.x;
-  const int tw = t % tiles_w;
-  t /= tiles_w;
-  const int th = t % tiles_h;
-  const int n = t / tiles_h;
-  const int h0 = th * kDTH, w0 = tw * kDTW;
+  const int tiles = N * tiles_h * tiles_w;
   for (int i = threadIdx.x; i < C * 28; i += blockDim.x) {
     const int c = i / 28, k = i - c * 28;
     ws[i] = k < CO * 9 ? w[(long long)k * C + c] : 0.0f;
   }
   constexpr int HR = kDTH + 2, HC = kDTW + 2;
-  for (int i = threadIdx.x; i < CO * HR * HC; i += blockDim.x) {
-    const int o = i % CO, rs = i / CO;
-    const int sx = rs % HC, r = rs / HC;
-    const int h = h0 - 1 + r, ww = w0 - 1 + sx;
-    ds[(o * HR + r) * HC + sx] =
-        (h >= 0 && h < H && ww >= 0 && ww < W) ? dy[(((long long)n * H + h) * W + ww) * CO + o] : 0.0f;
-  }
-  __syncthreads();
+  constexpr int kItems = CO * HR * HC, kPer = (kItems + 255) / 256;
   const int row = threadIdx.x >> 5, px = threadIdx.x & 31;
-  const int h = h0 + row;
-  // dx at (h, w) gathers dy at (h + 1 - r, w + 1 - s): halo row row + 2 - r, column px + 2 - s
-  float d0[CO * 9], d1[CO * 9];
-#pragma unroll
-  for (int o = 0; o < CO; ++o)
-#pragma unroll
-    for (int r = 0; r < 3; ++r)
-#pragma unroll
-      for (int sx = 0; sx < 3; ++sx) {
-        d0[o * 9 + r * 3 + sx] = ds[(o * HR + row + 2 - r) * HC + px + 2 - sx];
-        d1[o * 9 + r * 3 + sx] = ds[(o * HR + row + 2 - r) * HC + px + 32 + 2 - sx];
-      }
-  const int wa = w0 + px, wb = w0 + px + 32;
-  const bool va = h < H && wa < W, vb = h < H && wb < W;
-  float* xa = dx + (((long long)n * H + h) * W + wa) * C;
-  float* xb = dx + (((long long)n * H + h) * W + wb) * C;
-  for (int c = 0; c < C; c += 4) {
-    float a[4], bq[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      float wv[28];
-#pragma unroll
-      for (int k = 0; k < 7; ++k) {
-        const float4 q = *reinterpret_cast<const float4*>(ws + (c + j) * 28 + 4 * k);
-        wv[4 * k] = q.x;
-        wv[4 * k + 1] = q.y;
-        wv[4 * k + 2] = q.z;
-        wv[4 * k + 3] = q.w;
-      }
-      float sa = 0.0f, sb = 0.0f;
-#pragma unroll
-      for (int k = 0; k < CO * 9; ++k) {
-        sa = fmaf(d0[k], wv[k], sa);
-        sb = fmaf(d1[k], wv[k], sb);
-      }
-      a[j] = sa;
-      bq[j] = sb;
-    }
-    if (va) *reinterpret_cast<float4*>(xa + c) = make_float4(a[0], a[1], a[2], a[3]);
-    if (vb) *reinterpret_cast<float4*>(xb + c) = make_float4(bq[0], bq[1], bq[2], bq[3]);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// wgrad partials: dW[o][tap][c] over one block's pixel tiles.  Persistent blocks walk 8 x 16
-// pixel tiles; thread = (channel c, row half) keeps all 27 (o, tap) sums in registers; x is staged
-// channel-innermost ([10][18][C]) so a warp reads consecutive channels, dy as [128][4] (one
-// broadcast float4 per pixel), and the 3x3 neighbourhood slides along the row (3 new loads/pixel).
-constexpr int kWTH = 8, kWTW = 16;
-template <int CO>
-__global__ void __launch_bounds__(256) k_thin_wgrad(const float* __restrict__ x, const float* __restrict__ dy, int N,
-                                                    int H, int W, int C, float* __restrict__ partial) {
-  extern __shared__ float4 sm4[];
-  float* xs = reinterpret_cast<float*>(sm4);                 // [kWTH+2][kWTW+2][C]
-  float* dys = xs + (kWTH + 2) * (kWTW + 2) * C;              // [kWTH*kWTW][4]
-  float* red = dys + kWTH * kWTW * 4;                         // [C][CO*9] second-half sums
-  const int tiles_w = (W + kWTW - 1) / kWTW, tiles_h = (H + kWTH - 1) / kWTH;
-  const int tiles = N * tiles_h * tiles_w;
-  const int c = threadIdx.x % C, half = threadIdx.x / C;      // blockDim = 2 C
-  float acc[CO * 9];
-#pragma unroll
-  for (int k = 0; k < CO * 9; ++k) acc[k] = 0.0f;
-  constexpr int HC = kWTW + 2;
   for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
     int u = t;
     const int tw = u % tiles_w;
     u /= tiles_w;
     const int th = u % tiles_h;
     const int n = u / tiles_h;
+    const int h0 = th * kDTH, w0 = tw * kDTW;
+    float v[kPer];
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int i = threadIdx.x + j * 256;
+      v[j] = 0.0f;
+      if (i < kItems) {
+        const int o = i % CO, rs = i / CO;
+        const int sx = rs % HC, r = rs / HC;
+        const int h = h0 - 1 + r, ww = w0 - 1 + sx;
+        if (h >= 0 && h < H && ww >= 0 && ww < W) v[j] = __ldg(dy + (((long long)n * H + h) * W + ww) * CO + o);
+      }
+    }
+    __syncthreads();   // previous tile's ds reads (and, first time, the weight stores) are done
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int i = threadIdx.x + j * 256;
+      if (i < kItems) {
+        const int o = i % CO, rs = i / CO;
+        ds[o * HR * HC + rs] = v[j];
+      }
+    }
+    __syncthreads();
+    const int h = h0 + row;
+    // dx at (h, w) gathers dy at (h + 1 - r, w + 1 - s): halo row row + 2 - r, column px + 2 - s
+    float d0[CO * 9], d1[CO * 9];
+#pragma unroll
+    for (int o = 0; o < CO; ++o)
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int sx = 0; sx < 3; ++sx) {
+          d0[o * 9 + r * 3 + sx] = ds[(o * HR + row + 2 - r) * HC + px + 2 - sx];
+          d1[o * 9 + r * 3 + sx] = ds[(o * HR + row + 2 - r) * HC + px + 32 + 2 - sx];
+        }
+    const int wa = w0 + px, wb = w0 + px + 32;
+    const bool va = h < H && wa < W, vb = h < H && wb < W;
+    float* xa = dx + (((long long)n * H + h) * W + wa) * C;
+    float* xb = dx + (((long long)n * H + h) * W + wb) * C;
+    for (int c = 0; c < C; c += 4) {
+      float a[4], bq[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float wv[28];
+#pragma unroll
+        for (int k = 0; k < 7; ++k) {
+          const float4 q = *reinterpret_cast<const float4*>(ws + (c + j) * 28 + 4 * k);
+          wv[4 * k] = q.x;
+          wv[4 * k + 1] = q.y;
+          wv[4 * k + 2] = q.z;
+          wv[4 * k + 3] = q.w;
+        }
+        float sa = 0.0f, sb = 0.0f;
+#pragma unroll
+        for (int k = 0; k < CO * 9; ++k) {
+          sa = fmaf(d0[k], wv[k], sa);
+          sb = fmaf(d1[k], wv[k], sb);
+        }
+        a[j] = sa;
+        bq[j] = sb;
+      }
+      if (va) *reinterpret_cast<float4*>(xa + c) = make_float4(a[0], a[1], a[2], a[3]);
+      if (vb) *reinterpret_cast<float4*>(xb + c) = make_float4(bq[0], bq[1], bq[2], bq[3]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// wgrad partials: dW[o][tap][c] over one block's pixel tiles.  Persistent blocks walk 4 x 16
+// pixel tiles; thread = (channel c, tile row) keeps all 27 (o, tap) sums in registers; x is staged
+// channel-innermost ([6][18][C], the global NHWC order, so 16-byte cp.async copies with zero fill
+// for the padding), dy as [64][4] (one broadcast float4 per pixel), double-buffered so the next
+// tile's copies fly during this tile's FMAs; the 3x3 neighbourhood slides along the row.
+constexpr int kWTH = 4, kWTW = 16;
+__device__ __forceinline__ void cp_async_zfill(void* dst, const void* src, int bytes_valid, int size) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  if (size == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(bytes_valid) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(src), "r"(bytes_valid) : "memory");
+}
+template <int CO>
+__global__ void __launch_bounds__(512) k_thin_wgrad(const float* __restrict__ x, const float* __restrict__ dy, int N,
+                                                    int H, int W, int C, float* __restrict__ partial) {
+  extern __shared__ float4 sm4[];
+  constexpr int HC = kWTW + 2;
+  const int xs_floats = (kWTH + 2) * HC * C;
+  float* xs0 = reinterpret_cast<float*>(sm4);                 // 2 x [kWTH+2][kWTW+2][C]
+  float* dys0 = xs0 + 2 * xs_floats;                          // 2 x [kWTH*kWTW][4]
+  float* red = xs0;                                           // [kWTH-1][C][CO*9] after the loop
+  const int tiles_w = (W + kWTW - 1) / kWTW, tiles_h = (H + kWTH - 1) / kWTH;
+  const int tiles = N * tiles_h * tiles_w;
+  const int c = threadIdx.x % C, py = threadIdx.x / C;        // blockDim = kWTH * C
+  const int nvec = (kWTH + 2) * HC * (C / 4);
+  auto stage = [&](int t, int buf) {
+    int u = t;
+    const int tw = u % tiles_w;
+    u /= tiles_w;
+    const int th = u % tiles_h;
+    const int n = u / tiles_h;
     const int h0 = th * kWTH, w0 = tw * kWTW;
-    __syncthreads();
-    const int nvec = (kWTH + 2) * HC * (C / 4);
-    constexpr int kBatch = 6;   // independent 16-byte loads in flight per thread
-    for (int i0 = threadIdx.x; i0 < nvec; i0 += kBatch * blockDim.x) {
-      float4 v[kBatch];
-#pragma unroll
-      for (int u = 0; u < kBatch; ++u) {
-        const int i = i0 + u * blockDim.x;
-        v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (i < nvec) {
-          const int cv = i % (C / 4), rs = i / (C / 4);
-          const int sx = rs % HC, r = rs / HC;
-          const int h = h0 - 1 + r, ww = w0 - 1 + sx;
-          if (h >= 0 && h < H && ww >= 0 && ww < W)
-            v[u] = __ldg(reinterpret_cast<const float4*>(x + (((long long)n * H + h) * W + ww) * C + cv * 4));
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < kBatch; ++u) {
-        const int i = i0 + u * blockDim.x;
-        if (i < nvec) {
-          const int cv = i % (C / 4), rs = i / (C / 4);
-          *reinterpret_cast<float4*>(xs + rs * C + cv * 4) = v[u];
-        }
-      }
+    float* xs = xs0 + buf * xs_floats;
+    for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
+      const int cv = i % (C / 4), rs = i / (C / 4);
+      const int sx = rs % HC, r = rs / HC;
+      const int h = h0 - 1 + r, ww = w0 - 1 + sx;
+      const bool ok = h >= 0 && h < H && ww >= 0 && ww < W;
+      const float* src = ok ? x + (((long long)n * H + h) * W + ww) * C + cv * 4 : x;
+      cp_async_zfill(xs + rs * C + cv * 4, src, ok ? 16 : 0, 16);
     }
-    for (int i = threadIdx.x; i < kWTH * kWTW; i += blockDim.x) {
-      const int h = h0 + i / kWTW, ww = w0 + i % kWTW;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (h < H && ww < W) {
-        const float* q = dy + (((long long)n * H + h) * W + ww) * CO;
-        v.x = q[0];
-        if (CO > 1) v.y = q[1];
-        if (CO > 2) v.z = q[2];
-      }
-      *reinterpret_cast<float4*>(dys + i * 4) = v;
+    float* dys = dys0 + buf * kWTH * kWTW * 4;
+    for (int i = threadIdx.x; i < kWTH * kWTW * CO; i += blockDim.x) {
+      const int o = i % CO, p = i / CO;
+      const int h = h0 + p / kWTW, ww = w0 + p % kWTW;
+      const bool ok = h < H && ww < W;
+      cp_async_zfill(dys + p * 4 + o, ok ? dy + (((long long)n * H + h) * W + ww) * CO + o : dy, ok ? 4 : 0, 4);
     }
-    __syncthreads();
-    for (int py = half; py < kWTH; py += 2) {
-      // window xw[r][s] = x[py + r][px + s][c] for the current px
-      float xw[3][3];
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  float acc[CO * 9];
+#pragma unroll
+  for (int k = 0; k < CO * 9; ++k) acc[k] = 0.0f;
+  int buf = 0;
+  if (blockIdx.x < tiles) stage(blockIdx.x, 0);
+  for (int t = blockIdx.x; t < tiles; t += gridDim.x, buf ^= 1) {
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();   // this tile landed for every thread; the other buffer's readers are done
+    if (t + (int)gridDim.x < tiles) stage(t + gridDim.x, buf ^ 1);
+    const float* xs = xs0 + buf * xs_floats;
+    const float* dys = dys0 + buf * kWTH * kWTW * 4;
+    // window xw[r][s] = x[py + r][px + s][c] for the current px
+    float xw[3][3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      xw[r][0] = xs[((py + r) * HC + 0) * C + c];
+      xw[r][1] = xs[((py + r) * HC + 1) * C + c];
+    }
+#pragma unroll 4
+    for (int px = 0; px < kWTW; ++px) {
+#pragma unroll
+      for (int r = 0; r < 3; ++r) xw[r][2] = xs[((py + r) * HC + px + 2) * C + c];
+      const float4 g = *reinterpret_cast<const float4*>(dys + (py * kWTW + px) * 4);
+      const float gv[3] = {g.x, g.y, g.z};
+#pragma unroll
+      for (int o = 0; o < CO; ++o)
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+          for (int sx = 0; sx < 3; ++sx) acc[o * 9 + r * 3 + sx] = fmaf(gv[o], xw[r][sx], acc[o * 9 + r * 3 + sx]);
 #pragma unroll
       for (int r = 0; r < 3; ++r) {
-        xw[r][0] = xs[((py + r) * HC + 0) * C + c];
-        xw[r][1] = xs[((py + r) * HC + 1) * C + c];
-      }
-#pragma unroll 4
-      for (int px = 0; px < kWTW; ++px) {
-#pragma unroll
-        for (int r = 0; r < 3; ++r) xw[r][2] = xs[((py + r) * HC + px + 2) * C + c];
-        const float4 g = *reinterpret_cast<const float4*>(dys + (py * kWTW + px) * 4);
-        const float gv[3] = {g.x, g.y, g.z};
-#pragma unroll
-        for (int o = 0; o < CO; ++o)
-#pragma unroll
-          for (int r = 0; r < 3; ++r)
-#pragma unroll
-            for (int sx = 0; sx < 3; ++sx) acc[o * 9 + r * 3 + sx] = fmaf(gv[o], xw[r][sx], acc[o * 9 + r * 3 + sx]);
-#pragma unroll
-        for (int r = 0; r < 3; ++r) {
-          xw[r][0] = xw[r][1];
-          xw[r][1] = xw[r][2];
-        }
+        xw[r][0] = xw[r][1];
+        xw[r][1] = xw[r][2];
       }
     }
   }
-  // combine the two row halves, write this block's partial [CO*9][C]
+  // combine the row groups in order 0, 1, .., kWTH-1; write this block's partial [CO*9][C]
+  asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
-  if (half == 1)
+  if (py > 0)
 #pragma unroll
-    for (int k = 0; k < CO * 9; ++k) red[c * CO * 9 + k] = acc[k];
+    for (int k = 0; k < CO * 9; ++k) red[((py - 1) * C + c) * CO * 9 + k] = acc[k];
   __syncthreads();
-  if (half == 0) {
+  if (py == 0) {
     float* pb = partial + (long long)blockIdx.x * CO * 9 * C;
 #pragma unroll
-    for (int k = 0; k < CO * 9; ++k) pb[k * C + c] = acc[k] + red[c * CO * 9 + k];
+    for (int k = 0; k < CO * 9; ++k) {
+      float s = acc[k];
+      for (int g = 1; g < kWTH; ++g) s += red[((g - 1) * C + c) * CO * 9 + k];
+      pb[k * C + c] = s;
+    }
   }
 }
 __global__ void k_reduce_rows_f32(const float* __restrict__ partial, int rows, int n, float* __restrict__ out) {
@@ -2711,14 +2800,18 @@ cudaError_t thin_conv_dgrad(const float* dy, int N, int H, int W, int C, const f
   const int tiles = N * ((H + kDTH - 1) / kDTH) * ((W + kDTW - 1) / kDTW);
   const size_t sm = (size_t)(C * 28 + CO * (kDTH + 2) * (kDTW + 2)) * sizeof(float);
   PG_CUDA(cudaFuncSetAttribute(k_thin_dgrad<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  k_thin_dgrad<3><<<tiles, 256, sm, st>>>(dy, N, H, W, C, w, dx);
+  int per_sm = 1;
+  PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_thin_dgrad<3>, 256, sm));
+  if (per_sm < 1) per_sm = 1;
+  const int grid = tiles < per_sm * kNumSMs ? tiles : per_sm * kNumSMs;
+  k_thin_dgrad<3><<<grid, 256, sm, st>>>(dy, N, H, W, C, w, dx);
   return cudaGetLastError();
 }
 cudaError_t thin_conv_wgrad(const float* x, const float* dy, int N, int H, int W, int C, int CO, float* dw,
                             float* scratch, size_t scratch_floats, cudaStream_t st) {
   if (CO != 3 || C % 4 || C > 128 || ((uintptr_t)x & 15)) return cudaErrorInvalidValue;
   const int tiles = N * ((H + kWTH - 1) / kWTH) * ((W + kWTW - 1) / kWTW);
-  const size_t sm = (size_t)((kWTH + 2) * (kWTW + 2) * C + kWTH * kWTW * 4 + C * CO * 9) * sizeof(float);
+  const size_t sm = (size_t)(2 * (kWTH + 2) * (kWTW + 2) * C + 2 * kWTH * kWTW * 4) * sizeof(float);
   int per_sm = (int)(200 * 1024 / sm);
   if (per_sm < 1) per_sm = 1;
   if (per_sm > 4) per_sm = 4;
@@ -2727,7 +2820,7 @@ cudaError_t thin_conv_wgrad(const float* x, const float* dy, int N, int H, int W
   const int n = CO * 9 * C;
   while ((size_t)grid * n > scratch_floats && grid > 1) grid /= 2;
   PG_CUDA(cudaFuncSetAttribute(k_thin_wgrad<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  k_thin_wgrad<3><<<grid, 2 * C, sm, st>>>(x, dy, N, H, W, C, scratch);
+  k_thin_wgrad<3><<<grid, kWTH * C, sm, st>>>(x, dy, N, H, W, C, scratch);
   PG_LAUNCH_CHECK();
   k_reduce_rows_f32<<<ceil_div(n, 256), 256, 0, st>>>(scratch, grid, n, dw);
   return cudaGetLastError();

@@ -243,7 +243,10 @@ struct SnPack {     // one packed copy of W/sigma
   int dst_row_offset;  // sub-block placement (qkv packing)
   int dst_rows;        // mode 1: total rows (row stride of the transposed layout)
   int dst_cin;         // mode 0: padded input channels (>= cin; pads left untouched = 0)
+  int vec8;            // set by sn_pack_prepare: 8 channels per thread (mode 0, bf16, aligned)
 };
+// decides SnPack::vec8 and returns the number of 256-thread blocks the job needs in sn_pack
+long long sn_pack_prepare(SnPack& j);
 // power step over all SN weights of a net: pass 1a blocks = (job, 256 columns, 128-row chunk),
 // pass 1b blocks = (job, 256 columns), pass 2 blocks = (job, 8 rows), pass 3 = one block per job
 cudaError_t sn_power(const SnJob* jobs_dev, int n_jobs, const int* b1_job, const int* b1_k0, const int* b1_rc, int n_b1,

@@ -646,16 +646,26 @@ __global__ void k_attn_transpose(const bf16* __restrict__ in, int Q, int C, bf16
   }
 }
 
+// four lanes per row, 8 channels (one 16-byte bf16 load, two float4 loads) per lane per step
 __global__ void k_attn_rowdot(const bf16* __restrict__ dO, const float* __restrict__ o32, long long rows, int C,
                               float* __restrict__ D) {
-  const long long r = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (r >= rows) return;
+  const long long r = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 2;
+  const int l = threadIdx.x & 3;
   float s = 0.0f;
-  for (int c = lane; c < C; c += 32) s += __bfloat162float(dO[r * C + c]) * o32[r * C + c];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane == 0) D[r] = s;
+  if (r < rows) {
+    for (int c = 8 * l; c < C; c += 32) {
+      const uint4 u = *reinterpret_cast<const uint4*>(dO + r * C + c);
+      const float4 a = *reinterpret_cast<const float4*>(o32 + r * C + c);
+      const float4 b = *reinterpret_cast<const float4*>(o32 + r * C + c + 4);
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+      const float2 f0 = __bfloat1622float2(h[0]), f1 = __bfloat1622float2(h[1]);
+      const float2 f2 = __bfloat1622float2(h[2]), f3 = __bfloat1622float2(h[3]);
+      s += f0.x * a.x + f0.y * a.y + f1.x * a.z + f1.y * a.w + f2.x * b.x + f2.y * b.y + f3.x * b.z + f3.y * b.w;
+    }
+  }
+  s += __shfl_xor_sync(0xffffffffu, s, 1);
+  s += __shfl_xor_sync(0xffffffffu, s, 2);
+  if (r < rows && l == 0) D[r] = s;
 }
 
 __global__ void k_attn_dtheta_reduce(const float* __restrict__ part, int nkb, long long rows, int Cq,
@@ -689,7 +699,8 @@ cudaError_t attn_transpose(const void* gp, int n, int Q, int C, void* gT, cudaSt
 }
 
 cudaError_t attn_rowdot(const void* dO, const float* o32, long long rows, int C, float* D, cudaStream_t st) {
-  const long long blocks = (rows + 7) / 8;
+  if (C % 8 || ((uintptr_t)dO & 15) || ((uintptr_t)o32 & 15)) return cudaErrorInvalidValue;
+  const long long blocks = (rows + 63) / 64;
   k_attn_rowdot<<<(unsigned)blocks, 256, 0, st>>>(static_cast<const bf16*>(dO), o32, rows, C, D);
   return cudaGetLastError();
 }

@@ -65,6 +65,22 @@ struct WgradCfg {
   static constexpr size_t SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + ONES_BYTES + 256;
 };
 
+template <int BN>
+struct Wgrad3Cfg {
+  static constexpr int NB = (BN + 63) / 64;            // 64-channel chunks of the X halo
+  static constexpr uint32_t XCH = 18432;               // one chunk: up to 144 halo pixel rows x 128 B
+  static constexpr uint32_t A_BYTES = 2 * kAtomBytes;
+  static constexpr uint32_t B_BYTES = NB * XCH;
+  static constexpr uint32_t ONES_BYTES = kAtomBytes;
+  static constexpr int STAGES_RAW = (232448 - 2048 - (int)ONES_BYTES) / (A_BYTES + B_BYTES);
+  static constexpr int STAGES = STAGES_RAW > 6 ? 6 : STAGES_RAW;
+  // three taps' accumulators in [0, 3 BN), bias sums at 3 BN
+  static constexpr uint32_t TMEM_COLS = (3 * BN + 32 <= 256) ? 256 : 512;
+  static constexpr size_t SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + ONES_BYTES + 256;
+  static_assert(3 * BN + 32 <= 512, "three taps must fit TMEM");
+  static_assert(STAGES >= 2, "pipeline needs two stages");
+};
+
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
   uintptr_t a = reinterpret_cast<uintptr_t>(p);
   return reinterpret_cast<uint8_t*>((a + 1023) & ~uintptr_t(1023));
@@ -575,6 +591,158 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
         for (int j = 0; j < 32; ++j)
           if (col0 + j < a.Cin) op[j] = v[j];
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tmem, C::TMEM_COLS);
+}
+
+// ===========================================================================
+// wgrad, 3x3, one filter row per CTA: the three taps (r, 0..2) of a row share the dY tile (A,
+// loaded once instead of three times) and one X halo box {64 ch, Wt + 2, 128 / Wt rows, 1}
+// (Wt = min(W, 128)) per 64-channel chunk, which each tap reads through a descriptor shifted by
+// s pixel rows (the SW128 swizzle is a function of the absolute address; the MN-major K=16
+// step of 16 pixels stays inside one image row because W >= 16).  L2 -> SM traffic per K-block
+// drops from 3 x (dY + X) to dY + X(1 + 2 / Wt), which is what bounded the 96/192-channel layers.
+// ===========================================================================
+template <int BN>
+__global__ void __launch_bounds__(192, 1)
+    k_conv_wgrad3(const __grid_constant__ CUtensorMap tmDY, const __grid_constant__ CUtensorMap tmXh,
+                  const TcWgradArgs a) {
+  using C = Wgrad3Cfg<BN>;
+  constexpr int STAGES = C::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * C::A_BYTES;
+  uint8_t* sOnes = sB + STAGES * C::B_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sOnes + C::ONES_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tiles = a.m_tiles * a.n_tiles;   // n_tiles = 3 rows x c_blocks
+  const int split = blockIdx.x / tiles;
+  const int u = blockIdx.x - split * tiles;
+  const int nt = u % a.n_tiles;
+  const int mt = u / a.n_tiles;
+  const int r = nt / a.c_blocks, cb = nt - r * a.c_blocks;
+  const bool do_bias = a.bias_out != nullptr && nt == 0;
+  if (do_bias) {
+    uint4* o4 = reinterpret_cast<uint4*>(sOnes);
+    for (int i = threadIdx.x; i < (int)(C::ONES_BYTES / 16); i += blockDim.x)
+      o4[i] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
+    tc::fence_async_smem();
+  }
+  if (warp == 0 && lane == 0) {
+    tc::tma_prefetch(&tmDY);
+    tc::tma_prefetch(&tmXh);
+    for (int s = 0; s < STAGES; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    tc::mbar_init(&tfull[0], 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tmem_slot, C::TMEM_COLS);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const int Wt = a.W < 128 ? a.W : 128;          // pixels of one tile row
+  const int rowsT = 128 / Wt;                    // image rows per tile
+  const uint32_t x_tx = (uint32_t)(C::NB * (Wt + 2) * rowsT * 128);
+  const int kb0 = split * a.kb_per_split;
+  const int kb1 = min(a.total_kb, kb0 + a.kb_per_split);
+  const int o0 = mt * 128, c0 = cb * BN;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        int n0, h0, w0;
+        pix_origin(kb * kTileM, a.H, a.W, n0, h0, w0);
+        tc::mbar_wait(&empty[stage], phase ^ 1);
+        tc::mbar_expect_tx(&full[stage], C::A_BYTES + x_tx);
+        uint8_t* da = sA + stage * C::A_BYTES;
+        tc::tma_load_4d(da, &tmDY, &full[stage], o0, w0, h0, n0);
+        tc::tma_load_4d(da + kAtomBytes, &tmDY, &full[stage], o0 + 64, w0, h0, n0);
+        uint8_t* db = sB + stage * C::B_BYTES;
+#pragma unroll
+        for (int j = 0; j < C::NB; ++j)
+          tc::tma_load_4d(db + j * C::XCH, &tmXh, &full[stage], c0 + 64 * j, w0 - 1, h0 + r - 1, n0);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = tc::idesc_bf16(128, BN, true, true);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        tc::mbar_wait(&full[stage], phase);
+        tc::tc_fence_after();
+        const uint32_t a_base = tc::smem_u32(sA + stage * C::A_BYTES);
+        const uint32_t b_base = tc::smem_u32(sB + stage * C::B_BYTES);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {   // 8 x K=16 pixels
+          const uint64_t ad = tc::sdesc_sw128(a_base + k * 2048, kAtomBytes, 1024);
+          const int p0 = 16 * k, ir = p0 / Wt, jc = p0 - ir * Wt;
+          const uint32_t hrow = (uint32_t)(ir * (Wt + 2) + jc);   // halo row of tap s = 0
+#pragma unroll
+          for (int sx = 0; sx < 3; ++sx) {
+            const uint64_t bd = tc::sdesc_sw128(b_base + (hrow + sx) * 128, C::XCH, 1024);
+            tc::mma_bf16(tmem + sx * BN, ad, bd, idesc, (kb != kb0) || (k != 0));
+          }
+        }
+        if (do_bias) {
+          constexpr uint32_t idb = tc::idesc_bf16(128, 16, true, true);
+          const uint32_t o_base = tc::smem_u32(sOnes);
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            tc::mma_bf16(tmem + 3 * BN, tc::sdesc_sw128(a_base + k * 2048, kAtomBytes, 1024),
+                         tc::sdesc_sw128(o_base + k * 2048, kAtomBytes, 1024), idb, (kb != kb0) || (k != 0));
+        }
+        tc::mma_commit(&empty[stage]);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+      tc::mma_commit(&tfull[0]);
+    }
+  } else {
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    tc::mbar_wait(&tfull[0], 0);
+    tc::tc_fence_after();
+    const int o = o0 + row;
+    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+    if (do_bias) {
+      float v[32];
+      tc::tmem_ld32(lane_base + 3 * BN, v);
+      if (o < a.Cout) a.bias_out[(long long)split * a.Cout + o] = v[0];
+    }
+#pragma unroll 1
+    for (int sx = 0; sx < 3; ++sx) {
+      const int tap = r * 3 + sx;
+#pragma unroll 1
+      for (int cbk = 0; cbk < BN; cbk += 32) {
+        float v[32];
+        tc::tmem_ld32(lane_base + sx * BN + cbk, v);
+        const int col0 = c0 + cbk;
+        if (o >= a.Cout || col0 >= a.Cin) continue;
+        float* op = a.out + (((long long)split * a.Cout + o) * a.taps + tap) * a.Cin + col0;
+        if (col0 + 32 <= a.Cin && ((reinterpret_cast<uintptr_t>(op) & 15) == 0)) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(op + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (col0 + j < a.Cin) op[j] = v[j];
+        }
       }
     }
   }
@@ -1117,6 +1285,18 @@ cudaError_t launch_wgrad_bn(const CUtensorMap& ma, const CUtensorMap& mb, const 
   return cudaGetLastError();
 }
 
+template <int BN>
+cudaError_t launch_wgrad3_bn(const CUtensorMap& ma, const CUtensorMap& mb, const TcWgradArgs& a, cudaStream_t st) {
+  using C = Wgrad3Cfg<BN>;
+  static bool attr = false;
+  if (!attr) {
+    PG_CUDA(cudaFuncSetAttribute(k_conv_wgrad3<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    attr = true;
+  }
+  k_conv_wgrad3<BN><<<a.m_tiles * a.n_tiles * a.splits, 192, C::SMEM, st>>>(ma, mb, a);
+  return cudaGetLastError();
+}
+
 int pick_bn(int cout) {
   if (cout % 256 == 0) return 256;
   if (cout % 192 == 0) return 192;
@@ -1318,6 +1498,33 @@ cudaError_t tc_conv_dgrad_up2(const void* dy, int N, int H, int W, int Cout, con
   return launch_cg2<2>(bn, tq.m[0], mb2, mo, a, kAtomBytes, st, &tq);
 }
 
+// Split-K factor for the wgrad grid (one CTA per SM, one work unit per CTA): minimise
+//   waves(s) * (K-blocks per split + prologue/epilogue) * t_kb + the split reduction's traffic,
+// waves(s) = ceil(tiles * s / #SMs).  (Taking the smallest s that fills the SMs twice can leave a
+// third wave with a handful of CTAs — e.g. 9 taps x 33 splits = 297 CTAs on 148 SMs.)
+int choose_wgrad_splits(int tiles, long long total_kb, int bn, size_t part_floats, size_t scratch_floats,
+                        bool reduce_always) {
+  const double t_kb = 2.0 * 128 * bn * 128 / 7.0e6;   // us per K-block per SM (~7 TFLOP/s per SM)
+  long long smax = total_kb / 4;
+  if (smax < 1) smax = 1;
+  if (smax > 4096) smax = 4096;
+  int best = 1;
+  double best_cost = 1e300;
+  for (long long s = 1; s <= smax; ++s) {
+    if (s > 1 && (size_t)s * part_floats > scratch_floats) break;
+    const long long units = (long long)tiles * s;
+    const long long waves = (units + kNumSMs - 1) / kNumSMs;
+    const long long kb = (total_kb + s - 1) / s;
+    double cost = (double)waves * (double)(kb + 3) * t_kb;
+    if (s > 1 || reduce_always) cost += (double)s * part_floats * 8.0 / 6.0e6;   // write + read partials
+    if (cost < best_cost * 0.999) {
+      best_cost = cost;
+      best = (int)s;
+    }
+  }
+  return best;
+}
+
 cudaError_t tc_conv_wgrad_up2(const void* x, const void* dy, int N, int H, int W, int Cin, int Cout, float* dw,
                               float* scratch, size_t scratch_floats, cudaStream_t st, float* dbias) {
   if (Cin % 8 || Cout % 8 || ((uintptr_t)x & 15) || ((uintptr_t)dy & 15) || !tileable(H, W))
@@ -1362,12 +1569,9 @@ cudaError_t tc_conv_wgrad_up2(const void* x, const void* dy, int N, int H, int W
   a.total_kb = ceil_div((long long)N * H * W, kTileM);
   a.phases = 4;
   const int tiles = a.m_tiles * a.n_tiles;
-  int splits = (2 * kNumSMs + tiles - 1) / tiles;
-  if (splits > a.total_kb / 4) splits = a.total_kb / 4;
-  if (splits < 1) splits = 1;
   const size_t out_floats = (size_t)Cout * a.taps * Cin;
   const size_t bias_floats = dbias ? (size_t)4 * Cout : 0;
-  while (splits > 1 && (size_t)splits * (out_floats + bias_floats) > scratch_floats) --splits;
+  const int splits = choose_wgrad_splits(tiles, a.total_kb, bn, out_floats + bias_floats, scratch_floats, true);
   if ((size_t)splits * (out_floats + bias_floats) > scratch_floats) return cudaErrorMemoryAllocation;
   a.kb_per_split = ceil_div(a.total_kb, splits);
   a.splits = ceil_div(a.total_kb, a.kb_per_split);
@@ -1416,9 +1620,25 @@ cudaError_t tc_conv_wgrad(const void* x, const void* dy, int N, int H, int W, in
   else if (Cin <= 64) bn = 64;
   else if (Cin <= 96) bn = 96;
   else bn = 128;
+  // one filter row per CTA (k_conv_wgrad3) for 3x3 convs whose tile rows are >= 16 pixels
+  static const int row3_on = env_int("PARAGAN_WGRAD3", 1);
+  int bn3 = 0;
+  // (measured, B200: 96 -> 96 at 128x128 490 -> 673 TFLOP/s, 384 -> 384 953 -> 1011; C_in = 192 is faster
+  // as one N = 192 tap per CTA, 818 vs 700)
+  if (row3_on && ksz == 3 && W >= 16) {
+    if (Cin <= 64) bn3 = 64;
+    else if (Cin <= 96) bn3 = 96;
+    else if (Cin % 128 == 0) bn3 = 128;
+  }
   CUtensorMap mdy, mx;
   PG_CUDA(act_map(&mdy, dy, N, H, W, Cout));
-  PG_CUDA(act_map(&mx, x, N, H, W, Cin));
+  if (bn3) {
+    const int Wt = W < 128 ? W : 128;
+    PG_CUDA(halo_map(&mx, x, N, H, W, Cin, Wt + 2, 128 / Wt));
+    bn = bn3;
+  } else {
+    PG_CUDA(act_map(&mx, x, N, H, W, Cin));
+  }
   TcWgradArgs a{};
   a.H = H;
   a.W = W;
@@ -1428,26 +1648,28 @@ cudaError_t tc_conv_wgrad(const void* x, const void* dy, int N, int H, int W, in
   a.Cout = Cout;
   a.c_blocks = ceil_div(Cin, bn);
   a.m_tiles = ceil_div(Cout, 128);
-  a.n_tiles = a.taps * a.c_blocks;
+  a.n_tiles = (bn3 ? 3 : a.taps) * a.c_blocks;
   a.total_kb = ceil_div((long long)N * H * W, kTileM);
   const int tiles = a.m_tiles * a.n_tiles;
-  // split K so that tiles * splits covers the SMs ~2x, with >= 4 K-blocks per split
-  int splits = (2 * kNumSMs + tiles - 1) / tiles;
-  if (splits > a.total_kb / 4) splits = a.total_kb / 4;
-  if (splits < 1) splits = 1;
   const size_t out_floats = (size_t)Cout * a.taps * Cin;
   const size_t bias_floats = dbias ? (size_t)Cout : 0;
+  const int splits = choose_wgrad_splits(tiles, a.total_kb, bn3 ? 3 * bn3 : bn, out_floats + bias_floats,
+                                         scratch_floats, accumulate != 0);
   const bool direct = (splits == 1 && !accumulate);
-  if (!direct) {
-    while (splits > 1 && (size_t)splits * (out_floats + bias_floats) > scratch_floats) --splits;
-    if ((size_t)splits * (out_floats + bias_floats) > scratch_floats) return cudaErrorMemoryAllocation;
-  }
+  if (!direct && (size_t)splits * (out_floats + bias_floats) > scratch_floats) return cudaErrorMemoryAllocation;
   a.kb_per_split = ceil_div(a.total_kb, splits);
   a.splits = ceil_div(a.total_kb, a.kb_per_split);
   a.out = direct ? dw : scratch;
   a.bias_out = dbias ? (direct ? dbias : scratch + (size_t)a.splits * out_floats) : nullptr;
   cudaError_t e;
-  switch (bn) {
+  if (bn3) {
+    // the cost model's per-K-block time covers the three taps
+    switch (bn3) {
+      case 64: e = launch_wgrad3_bn<64>(mdy, mx, a, st); break;
+      case 96: e = launch_wgrad3_bn<96>(mdy, mx, a, st); break;
+      default: e = launch_wgrad3_bn<128>(mdy, mx, a, st); break;
+    }
+  } else switch (bn) {
     case 32: e = launch_wgrad_bn<32>(mdy, mx, a, st); break;
     case 64: e = launch_wgrad_bn<64>(mdy, mx, a, st); break;
     case 96: e = launch_wgrad_bn<96>(mdy, mx, a, st); break;

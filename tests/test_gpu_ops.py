@@ -71,6 +71,7 @@ CONV_SHAPES = [  # n, h, w, cin, cout, k
     (1, 16, 16, 8, 32, 3),       # column-shifted halo units, W = 16, one K step
     (5, 8, 8, 64, 128, 3),       # odd number of M tiles (CTA-pair kernel: last pair half empty)
     (4, 8, 8, 1536, 1536, 3),    # CTA pairs with several N tiles
+    (2, 16, 32, 384, 136, 3),    # wgrad, one filter row per CTA: 3 x 128-channel blocks, C_out tail
 ]
 
 
