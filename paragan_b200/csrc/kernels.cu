@@ -497,18 +497,35 @@ __global__ void k_bn_bwd_fold(const float* __restrict__ partial, int N, int chun
     AB[i] = (float)a;
   }
 }
-__global__ void k_bn_bwd_totals(const float* __restrict__ AB, int N, int C, const float* __restrict__ gain,
-                                const float* __restrict__ gamma, double* __restrict__ tot) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= C) return;
+// tot[c] = sum_n g(n, c) AB[n][c], tot[C + c] = sum_n g(n, c) AB[n][C + c]: block = 32 channels x 8
+// sample groups (group j sums n = j, j + 8, .. in order), groups combined in order (deterministic)
+__global__ void __launch_bounds__(256) k_bn_bwd_totals(const float* __restrict__ AB, int N, int C,
+                                                       const float* __restrict__ gain, const float* __restrict__ gamma,
+                                                       double* __restrict__ tot) {
+  __shared__ double red[2][8][32];
+  const int cx = threadIdx.x & 31, j = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + cx;
   double t0 = 0.0, t1 = 0.0;
-  for (int n = 0; n < N; ++n) {
-    const double g = gain ? 1.0 + (double)gain[(long long)n * C + c] : (double)gamma[c];
-    t0 += g * AB[(long long)n * 2 * C + c];
-    t1 += g * AB[(long long)n * 2 * C + C + c];
+  if (c < C) {
+    const double g0 = gain ? 0.0 : (double)gamma[c];
+    for (int n = j; n < N; n += 8) {
+      const double g = gain ? 1.0 + (double)gain[(long long)n * C + c] : g0;
+      t0 += g * AB[(long long)n * 2 * C + c];
+      t1 += g * AB[(long long)n * 2 * C + C + c];
+    }
   }
-  tot[c] = t0;
-  tot[C + c] = t1;
+  red[0][j][cx] = t0;
+  red[1][j][cx] = t1;
+  __syncthreads();
+  if (j == 0 && c < C) {
+    double a0 = 0.0, a1 = 0.0;
+    for (int k = 0; k < 8; ++k) {
+      a0 += red[0][k][cx];
+      a1 += red[1][k][cx];
+    }
+    tot[c] = a0;
+    tot[C + c] = a1;
+  }
 }
 template <typename TI, typename TG, typename TO>
 __global__ void k_bn_bwd_apply(const TI* __restrict__ x, const TG* __restrict__ dy, int N, int H, int W, int C,
@@ -1083,23 +1100,56 @@ __global__ void k_d_head_bwd_dh(const T* __restrict__ h, int N, int HW, int C, c
     dh[i] = from_f<T>(to_f<T>(h[i]) > 0.0f ? df : 0.0f);
   }
 }
-__global__ void k_d_head_bwd_w(int N, int C, const float* __restrict__ feat, const float* __restrict__ dl,
-                               const int32_t* __restrict__ y, float* __restrict__ dw_lin, float* __restrict__ db_lin,
-                               float* __restrict__ dembed) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c < C) {
-    double a = 0.0;
-    for (int n = 0; n < N; ++n) {
-      const float g = dl[n] * feat[(long long)n * C + c];
-      a += g;
-      dembed[(long long)y[n] * C + c] += g;  // sequential over n: deterministic
+// dw_lin[c] = sum_n dl[n] feat[n][c];  dembed[y][c] += sum_{n : y[n] = y} dl[n] feat[n][c]  (each class's
+// samples summed in n order by one thread: the samples are ranked by (class, n) in shared memory, the
+// thread at the first rank of a class walks its run);  db_lin = sum_n dl[n].  Block = 32 channels.
+constexpr int kHeadMaxN = 2048;
+__global__ void __launch_bounds__(256) k_d_head_bwd_w(int N, int C, const float* __restrict__ feat,
+                                                      const float* __restrict__ dl, const int32_t* __restrict__ y,
+                                                      float* __restrict__ dw_lin, float* __restrict__ db_lin,
+                                                      float* __restrict__ dembed) {
+  __shared__ int ys[kHeadMaxN];
+  __shared__ short perm[kHeadMaxN];
+  __shared__ double red[8][32];
+  for (int n = threadIdx.x; n < N; n += blockDim.x) ys[n] = y[n];
+  __syncthreads();
+  for (int n = threadIdx.x; n < N; n += blockDim.x) {   // stable rank by (class, n)
+    const int yn = ys[n];
+    int r = 0;
+    for (int m = 0; m < N; ++m) {
+      const int ym = ys[m];
+      r += (ym < yn) || (ym == yn && m < n);
     }
-    dw_lin[c] = (float)a;
+    perm[r] = (short)n;
   }
-  if (c == 0) {
-    double s = 0.0;
-    for (int n = 0; n < N; ++n) s += dl[n];
-    db_lin[0] = (float)s;
+  __syncthreads();
+  const int cx = threadIdx.x & 31, j = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + cx;
+  double a = 0.0;
+  if (c < C) {
+    for (int n = j; n < N; n += 8) a += (double)(dl[n] * feat[(long long)n * C + c]);
+    for (int p = j; p < N; p += 8) {
+      const int n0 = perm[p], k = ys[n0];
+      if (p > 0 && ys[perm[p - 1]] == k) continue;   // not the first sample of its class
+      float s = 0.0f;
+      for (int q = p; q < N && ys[perm[q]] == k; ++q) {
+        const int n = perm[q];
+        s += dl[n] * feat[(long long)n * C + c];
+      }
+      dembed[(long long)k * C + c] += s;
+    }
+  }
+  red[j][cx] = a;
+  __syncthreads();
+  if (j == 0 && c < C) {
+    double t = 0.0;
+    for (int k = 0; k < 8; ++k) t += red[k][cx];
+    dw_lin[c] = (float)t;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    double t = 0.0;
+    for (int n = 0; n < N; ++n) t += dl[n];
+    db_lin[0] = (float)t;
   }
 }
 
@@ -1147,6 +1197,63 @@ __global__ void k_maxpool2_split_bwd(const T* __restrict__ x, int N, int H, int 
     }
     const float g = dp[i];
     for (int k = 0; k < 4; ++k) dx[idx[k] * ldx + c_off + c] = from_f<T>(k == arg ? g : 0.0f);
+  }
+}
+// 8 channels per thread (C, ldx, c_off multiples of 8, 16-byte aligned): the same per-element
+// arithmetic as k_maxpool2_split / k_maxpool2_split_bwd with 16-byte accesses and 32-bit indexing
+template <typename T>
+__global__ void k_maxpool2_split_v(const T* __restrict__ x, int N, int H, int W, int ldx, int c_off, int C,
+                                   T* __restrict__ pooled) {
+  const int Ho = H >> 1, Wo = W >> 1, Q = Ho * Wo, G = C >> 3;
+  const unsigned total = (unsigned)N * Q * G;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int g = (int)(i % G);
+    const unsigned pq = i / G;
+    const int q = (int)(pq % Q), n = (int)(pq / Q);
+    const int ho = q / Wo, wo = q - ho * Wo;
+    const long long b = ((long long)n * H + 2 * ho) * W + 2 * wo;
+    float a0[8], a1[8], a2[8], a3[8], m[8];
+    Vec8<T>::load(x + b * ldx + c_off + 8 * g, a0);
+    Vec8<T>::load(x + (b + 1) * ldx + c_off + 8 * g, a1);
+    Vec8<T>::load(x + (b + W) * ldx + c_off + 8 * g, a2);
+    Vec8<T>::load(x + (b + W + 1) * ldx + c_off + 8 * g, a3);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) m[k] = fmaxf(fmaxf(a0[k], a1[k]), fmaxf(a2[k], a3[k]));
+    Vec8<T>::store(pooled + (long long)pq * C + 8 * g, m);
+  }
+}
+template <typename T>
+__global__ void k_maxpool2_split_bwd_v(const T* __restrict__ x, int N, int H, int W, int ldx, int c_off, int C,
+                                       const float* __restrict__ dp, T* __restrict__ dx) {
+  const int Ho = H >> 1, Wo = W >> 1, Q = Ho * Wo, G = C >> 3;
+  const unsigned total = (unsigned)N * Q * G;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int g = (int)(i % G);
+    const unsigned pq = i / G;
+    const int q = (int)(pq % Q), n = (int)(pq / Q);
+    const int ho = q / Wo, wo = q - ho * Wo;
+    const long long b = ((long long)n * H + 2 * ho) * W + 2 * wo;
+    const long long idx[4] = {b, b + 1, b + W, b + W + 1};
+    float a[4][8], gv[8];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) Vec8<T>::load(x + idx[k] * ldx + c_off + 8 * g, a[k]);
+    Vec8<float>::load(dp + (long long)pq * C + 8 * g, gv);
+    int arg[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {   // first maximum in row-major scan wins (R7)
+      float best = a[0][e];
+      arg[e] = 0;
+#pragma unroll
+      for (int k = 1; k < 4; ++k)
+        if (a[k][e] > best) { best = a[k][e]; arg[e] = k; }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      float o[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) o[e] = arg[e] == k ? gv[e] : 0.0f;
+      Vec8<T>::store(dx + idx[k] * ldx + c_off + 8 * g, o);
+    }
   }
 }
 // one warp per row
@@ -1828,7 +1935,7 @@ template cudaError_t bn_bwd_reduce<bf16, float>(const bf16*, const float*, int, 
 
 cudaError_t bn_bwd_totals(const float* AB, int N, int C, const float* gain, const float* gamma, double* tot,
                           cudaStream_t st) {
-  k_bn_bwd_totals<<<ceil_div(C, 128), 128, 0, st>>>(AB, N, C, gain, gamma, tot);
+  k_bn_bwd_totals<<<ceil_div(C, 32), 256, 0, st>>>(AB, N, C, gain, gamma, tot);
   return cudaGetLastError();
 }
 
@@ -1989,7 +2096,8 @@ cudaError_t d_head_bwd(const T* h, int N, int HW, int C, const float* w_lin, con
   k_d_head_bwd_dh<T><<<grid_for(total, 256), 256, 0, st>>>(h, N, HW, C, w_lin, embed, y, dlogits, dh);
   PG_LAUNCH_CHECK();
   if (want_wgrad) {
-    k_d_head_bwd_w<<<ceil_div(C, 128), 128, 0, st>>>(N, C, feat, dlogits, y, dw_lin, db_lin, dembed);
+    if (N > kHeadMaxN) return cudaErrorInvalidValue;
+    k_d_head_bwd_w<<<ceil_div(C, 32), 256, 0, st>>>(N, C, feat, dlogits, y, dw_lin, db_lin, dembed);
     PG_LAUNCH_CHECK();
   }
   return cudaSuccess;
@@ -1998,6 +2106,12 @@ template <typename T>
 cudaError_t maxpool2_split(const T* x, int N, int H, int W, int ldx, int c_off, int C, T* pooled, T* pooledT,
                            cudaStream_t st) {
   const long long total = (long long)N * (H / 2) * (W / 2) * C;
+  const bool vec = !pooledT && C % 8 == 0 && ldx % 8 == 0 && c_off % 8 == 0 &&
+                   ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(pooled)) & 15) == 0 && total < (1LL << 32);
+  if (vec) {
+    k_maxpool2_split_v<T><<<grid_for(total / 8, 256), 256, 0, st>>>(x, N, H, W, ldx, c_off, C, pooled);
+    return cudaGetLastError();
+  }
   k_maxpool2_split<T><<<grid_for(total, 256), 256, 0, st>>>(x, N, H, W, ldx, c_off, C, pooled, pooledT);
   return cudaGetLastError();
 }
@@ -2005,6 +2119,13 @@ template <typename T>
 cudaError_t maxpool2_split_bwd(const T* x, int N, int H, int W, int ldx, int c_off, int C, const float* dpooled, T* dx,
                                cudaStream_t st) {
   const long long total = (long long)N * (H / 2) * (W / 2) * C;
+  const bool vec = C % 8 == 0 && ldx % 8 == 0 && c_off % 8 == 0 &&
+                   ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(dx) |
+                     reinterpret_cast<uintptr_t>(dpooled)) & 15) == 0 && total < (1LL << 32);
+  if (vec) {
+    k_maxpool2_split_bwd_v<T><<<grid_for(total / 8, 256), 256, 0, st>>>(x, N, H, W, ldx, c_off, C, dpooled, dx);
+    return cudaGetLastError();
+  }
   k_maxpool2_split_bwd<T><<<grid_for(total, 256), 256, 0, st>>>(x, N, H, W, ldx, c_off, C, dpooled, dx);
   return cudaGetLastError();
 }
@@ -2187,13 +2308,13 @@ namespace {
 // ---------------------------------------------------------------------------
 // fprop: y[m][o] = bias[o] + sum_{tap,c} x[m+tap][c] w[o][tap][c]
 // tile 32 rows x 64 cols, thread = 8 consecutive pixels of one row (acc[8][CO] in registers);
-// 4-channel halo chunks staged in smem ([c][row][68] planes; 3 blocks per SM, so one stages while
-// the others compute), weights as [c][28] so each channel's 27 taps x outputs come in 7 broadcast
-// float4 loads; rows slide through 3 float4s.
-constexpr int kFTH = 32, kFTW = 64, kFCC = 4, kFRS = 68, kFV = kFCC / 4;
+// 8-channel halo chunks staged in smem ([c][row][68] planes; a whole 32-byte sector per pixel —
+// 4-channel chunks re-read every sector from DRAM), weights as [c][28] so each channel's 27 taps x
+// outputs come in 7 broadcast float4 loads; rows slide through 3 float4s.
+constexpr int kFTH = 32, kFTW = 64, kFCC = 8, kFRS = 68, kFV = kFCC / 4;
 constexpr int kFPlane = (kFTH + 2) * kFRS;
 template <int CO>
-__global__ void __launch_bounds__(256, 3) k_thin_fwd(const float* __restrict__ x, int N, int H, int W, int C,
+__global__ void __launch_bounds__(256, 2) k_thin_fwd(const float* __restrict__ x, int N, int H, int W, int C,
                                                   const float* __restrict__ w, const float* __restrict__ bias,
                                                   float* __restrict__ y) {
   extern __shared__ float4 sm4[];
@@ -2220,7 +2341,7 @@ __global__ void __launch_bounds__(256, 3) k_thin_fwd(const float* __restrict__ x
     __syncthreads();
     // halo chunk: batches of 6 independent 16-byte loads per thread in flight, then the planar stores
     constexpr int kItems = (kFTH + 2) * (kFTW + 2) * kFV;
-    constexpr int kBatch = 9;
+    constexpr int kBatch = 6;
     for (int i0 = threadIdx.x; i0 < kItems; i0 += kBatch * 256) {
       float4 v[kBatch];
 #pragma unroll
