@@ -116,8 +116,12 @@ __device__ __forceinline__ uint32_t map_to_rank(const void* p, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
   return r;
 }
+// arrive on a barrier of another CTA of the cluster with the default (.release.cta) semantics: the
+// accumulator hand-back only has to order this thread's tcgen05.ld (fenced by
+// tcgen05.fence::before_thread_sync) before the arrive; .release.cluster compiles to a GPU-scope
+// MEMBAR that waits for the epilogue's outstanding global writes on every tile
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 // TMA load for a CTA pair: data lands in this CTA's smem, completion is counted on the
 // (leader's) barrier at `bar_cluster`
