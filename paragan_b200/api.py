@@ -100,7 +100,8 @@ def lib():
             from . import build
             build.build()
         import torch  # noqa: F401  (loads the CUDA runtime / NCCL torch ships, which the .so shares)
-        L = C.CDLL(LIB_PATH)
+        # PARAGAN_LIB: load another build of the library (A/B measurements in one process tree)
+        L = C.CDLL(os.environ.get("PARAGAN_LIB", LIB_PATH))
         for name, (res, args) in SYMBOLS.items():
             f = getattr(L, name)
             f.restype, f.argtypes = res, args

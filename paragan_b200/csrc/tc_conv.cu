@@ -538,33 +538,38 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {   // the whole (converged) warp runs the loop; one elected lane issues (uniform descriptors)
       constexpr uint32_t idesc = tc::idesc_bf16(128, BN, true, true);
+      const bool issuer = tc::elect_one();
+      const uint32_t sA0 = tc::smem_u32(sA), sB0 = tc::smem_u32(sB), o_base = tc::smem_u32(sOnes);
       int stage = 0;
       uint32_t phase = 0;
       for (int kb = kb0; kb < kb1; ++kb) {
         tc::mbar_wait(&full[stage], phase);
         tc::tc_fence_after();
-        const uint32_t a_base = tc::smem_u32(sA + stage * C::A_BYTES);
-        const uint32_t b_base = tc::smem_u32(sB + stage * C::B_BYTES);
+        const uint32_t a_base = sA0 + stage * C::A_BYTES;
+        const uint32_t b_base = sB0 + stage * C::B_BYTES;
+        if (issuer) {
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {   // 8 x K=16 pixels; each K=16 step = two 8-row groups = 2048 B
-          const uint64_t ad = tc::sdesc_sw128(a_base + k * 2048, kAtomBytes, 1024);
-          const uint64_t bd = tc::sdesc_sw128(b_base + k * 2048, kAtomBytes, 1024);
-          tc::mma_bf16(tmem, ad, bd, idesc, (kb != kb0) || (k != 0));
-        }
-        if (do_bias) {
-          constexpr uint32_t idb = tc::idesc_bf16(128, 16, true, true);
-          const uint32_t o_base = tc::smem_u32(sOnes);
+          for (int k = 0; k < 8; ++k) {   // 8 x K=16 pixels; each K=16 step = two 8-row groups = 2048 B
+            const uint64_t ad = tc::sdesc_sw128(a_base + k * 2048, kAtomBytes, 1024);
+            const uint64_t bd = tc::sdesc_sw128(b_base + k * 2048, kAtomBytes, 1024);
+            tc::mma_bf16(tmem, ad, bd, idesc, (kb != kb0) || (k != 0));
+          }
+          if (do_bias) {
+            constexpr uint32_t idb = tc::idesc_bf16(128, 16, true, true);
 #pragma unroll
-          for (int k = 0; k < 8; ++k)
-            tc::mma_bf16(tmem + BN, tc::sdesc_sw128(a_base + k * 2048, kAtomBytes, 1024),
-                         tc::sdesc_sw128(o_base + k * 2048, kAtomBytes, 1024), idb, (kb != kb0) || (k != 0));
+            for (int k = 0; k < 8; ++k)
+              tc::mma_bf16(tmem + BN, tc::sdesc_sw128(a_base + k * 2048, kAtomBytes, 1024),
+                           tc::sdesc_sw128(o_base + k * 2048, kAtomBytes, 1024), idb, (kb != kb0) || (k != 0));
+          }
+          tc::mma_commit(&empty[stage]);
         }
-        tc::mma_commit(&empty[stage]);
+        __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
-      tc::mma_commit(&tfull[0]);
+      if (issuer) tc::mma_commit(&tfull[0]);
+      __syncwarp();
     }
   } else {
     const int q = warp & 3;
@@ -680,38 +685,43 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {   // the whole (converged) warp runs the loop; one elected lane issues (uniform descriptors)
       constexpr uint32_t idesc = tc::idesc_bf16(128, BN, true, true);
+      const bool issuer = tc::elect_one();
+      const uint32_t sA0 = tc::smem_u32(sA), sB0 = tc::smem_u32(sB), o_base = tc::smem_u32(sOnes);
       int stage = 0;
       uint32_t phase = 0;
       for (int kb = kb0; kb < kb1; ++kb) {
         tc::mbar_wait(&full[stage], phase);
         tc::tc_fence_after();
-        const uint32_t a_base = tc::smem_u32(sA + stage * C::A_BYTES);
-        const uint32_t b_base = tc::smem_u32(sB + stage * C::B_BYTES);
+        const uint32_t a_base = sA0 + stage * C::A_BYTES;
+        const uint32_t b_base = sB0 + stage * C::B_BYTES;
+        if (issuer) {
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {   // 8 x K=16 pixels
-          const uint64_t ad = tc::sdesc_sw128(a_base + k * 2048, kAtomBytes, 1024);
-          const int p0 = 16 * k, ir = p0 / Wt, jc = p0 - ir * Wt;
-          const uint32_t hrow = (uint32_t)(ir * (Wt + 2) + jc);   // halo row of tap s = 0
+          for (int k = 0; k < 8; ++k) {   // 8 x K=16 pixels
+            const uint64_t ad = tc::sdesc_sw128(a_base + k * 2048, kAtomBytes, 1024);
+            const int p0 = 16 * k, ir = p0 / Wt, jc = p0 - ir * Wt;
+            const uint32_t hrow = (uint32_t)(ir * (Wt + 2) + jc);   // halo row of tap s = 0
 #pragma unroll
-          for (int sx = 0; sx < 3; ++sx) {
-            const uint64_t bd = tc::sdesc_sw128(b_base + (hrow + sx) * 128, C::XCH, 1024);
-            tc::mma_bf16(tmem + sx * BN, ad, bd, idesc, (kb != kb0) || (k != 0));
+            for (int sx = 0; sx < 3; ++sx) {
+              const uint64_t bd = tc::sdesc_sw128(b_base + (hrow + sx) * 128, C::XCH, 1024);
+              tc::mma_bf16(tmem + sx * BN, ad, bd, idesc, (kb != kb0) || (k != 0));
+            }
           }
-        }
-        if (do_bias) {
-          constexpr uint32_t idb = tc::idesc_bf16(128, 16, true, true);
-          const uint32_t o_base = tc::smem_u32(sOnes);
+          if (do_bias) {
+            constexpr uint32_t idb = tc::idesc_bf16(128, 16, true, true);
 #pragma unroll
-          for (int k = 0; k < 8; ++k)
-            tc::mma_bf16(tmem + 3 * BN, tc::sdesc_sw128(a_base + k * 2048, kAtomBytes, 1024),
-                         tc::sdesc_sw128(o_base + k * 2048, kAtomBytes, 1024), idb, (kb != kb0) || (k != 0));
+            for (int k = 0; k < 8; ++k)
+              tc::mma_bf16(tmem + 3 * BN, tc::sdesc_sw128(a_base + k * 2048, kAtomBytes, 1024),
+                           tc::sdesc_sw128(o_base + k * 2048, kAtomBytes, 1024), idb, (kb != kb0) || (k != 0));
+          }
+          tc::mma_commit(&empty[stage]);
         }
-        tc::mma_commit(&empty[stage]);
+        __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
-      tc::mma_commit(&tfull[0]);
+      if (issuer) tc::mma_commit(&tfull[0]);
+      __syncwarp();
     }
   } else {
     const int q = warp & 3;
@@ -1017,8 +1027,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && is_leader) {
+    if (is_leader) {   // the whole (converged) warp runs the loop; one elected lane issues
       constexpr uint32_t idesc = tc::idesc_bf16(256, BN, false, false);
+      const bool issuer = tc::elect_one();
+      const uint32_t sH0 = tc::smem_u32(sH), sB0 = tc::smem_u32(sB);
       int stage = 0, hs = 0;
       uint32_t phase = 0, hphase = 0;
       int it = 0;
@@ -1027,13 +1039,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::mbar_wait(&tempty[buf], ((it >> 1) & 1) ^ 1);
         tc::tc_fence_after();
         const uint32_t d_tmem = tmem + buf * BN;
-        bool first = true;
+        uint32_t acc = 0u;
         for (int cc = 0; cc < a.c_chunks; ++cc) {
           const int ksteps = (cc == a.c_chunks - 1) ? a.last_ksteps : 4;
           for (int u = 0; u < units_per_chunk; ++u) {
             tc::mbar_wait(&hfull[hs], hphase);
             tc::tc_fence_after();
-            const uint32_t h_base = tc::smem_u32(sH + hs * C::UNIT_BYTES);
+            const uint32_t h_base = sH0 + hs * C::UNIT_BYTES;
             for (int j = 0; j < taps_per_unit; ++j) {
               tc::mbar_wait(&full[stage], phase);
               tc::tc_fence_after();
@@ -1041,20 +1053,25 @@ __global__ void __launch_bounds__(kThreads, 1)
                   MODE == 0 ? (uint32_t)((j / 3) * 130 + (j % 3)) : (MODE == 1 ? (uint32_t)(j * a.W) : 0u);
               // descriptors advance by 32 bytes (= 2 in the >>4 address field) per K=16 step
               const uint64_t ad0 = tc::sdesc_sw128(h_base + row * 128, 16, 1024);
-              const uint64_t bd0 = tc::sdesc_sw128(tc::smem_u32(sB + stage * C::B_BYTES), 16, 1024);
-              tc::mma_bf16_cg2(d_tmem, ad0, bd0, idesc, first ? 0u : 1u);
-              first = false;
-              if (ksteps > 1) tc::mma_bf16_cg2(d_tmem, ad0 + 2, bd0 + 2, idesc, 1u);
-              if (ksteps > 2) tc::mma_bf16_cg2(d_tmem, ad0 + 4, bd0 + 4, idesc, 1u);
-              if (ksteps > 3) tc::mma_bf16_cg2(d_tmem, ad0 + 6, bd0 + 6, idesc, 1u);
-              tc::mma_commit_cg2(&empty[stage], 3);
+              const uint64_t bd0 = tc::sdesc_sw128(sB0 + stage * C::B_BYTES, 16, 1024);
+              if (issuer) {
+                tc::mma_bf16_cg2(d_tmem, ad0, bd0, idesc, acc);
+                if (ksteps > 1) tc::mma_bf16_cg2(d_tmem, ad0 + 2, bd0 + 2, idesc, 1u);
+                if (ksteps > 2) tc::mma_bf16_cg2(d_tmem, ad0 + 4, bd0 + 4, idesc, 1u);
+                if (ksteps > 3) tc::mma_bf16_cg2(d_tmem, ad0 + 6, bd0 + 6, idesc, 1u);
+                tc::mma_commit_cg2(&empty[stage], 3);
+              }
+              __syncwarp();
+              acc = 1u;
               if (++stage == STAGES) { stage = 0; phase ^= 1; }
             }
-            tc::mma_commit_cg2(&hempty[hs], 3);
+            if (issuer) tc::mma_commit_cg2(&hempty[hs], 3);
+            __syncwarp();
             if (++hs == NA) { hs = 0; hphase ^= 1; }
           }
         }
-        tc::mma_commit_cg2(&tfull[buf], 3);
+        if (issuer) tc::mma_commit_cg2(&tfull[buf], 3);
+        __syncwarp();
       }
     }
   } else {

@@ -180,6 +180,14 @@ __device__ __forceinline__ void mma_commit_cg2(uint64_t* bar, uint16_t mask) {
       : "memory");
 }
 
+// one lane of a converged warp (the same lane on every call with the full mask): the MMA issuer.
+// Running the issue loop on the whole warp keeps its state warp-uniform, so the descriptors live in
+// uniform registers instead of going through a per-MMA R2UR / ELECT waterfall.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p;
+  asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\tselp.u32 %0, 1, 0, e;\n\t}" : "=r"(p));
+  return p != 0;
+}
 // D[tmem] (+)= A[smem] * B[smem]^T, bf16 x bf16 -> fp32, one CTA.
 __device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                          uint32_t accumulate) {
