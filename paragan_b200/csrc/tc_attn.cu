@@ -157,7 +157,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {   // whole (converged) warp runs the loop, one elected lane issues: uniform descriptors
+      const bool issuer = tc::elect_one();
       const uint32_t idS = tc::idesc_bf16(kT, kT, false, false);
       const uint32_t idO = tc::idesc_bf16(kT, C2, false, false);
       const int ksteps = a.Cq / 16;
@@ -169,11 +170,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         tc::mbar_wait(&sempty[sb], ((su >> 1) & 1) ^ 1);
         tc::mbar_wait(&kfull[ks], kph);
         tc::tc_fence_after();
-        for (int k = 0; k < ksteps; ++k)
-          tc::mma_bf16(tmem + sb * kT, kdesc(sQ + k * 32), kdesc(sK + ks * kAtom + k * 32), idS, k > 0);
-        tc::mma_commit(&kempty[ks]);
-        tc::mma_commit(&sfull[sb]);
-        if (last) tc::mma_commit(qempty);
+        if (issuer) {
+          for (int k = 0; k < ksteps; ++k)
+            tc::mma_bf16(tmem + sb * kT, kdesc(sQ + k * 32), kdesc(sK + ks * kAtom + k * 32), idS, k > 0);
+          tc::mma_commit(&kempty[ks]);
+          tc::mma_commit(&sfull[sb]);
+          if (last) tc::mma_commit(qempty);
+        }
+        __syncwarp();
         if (++ks == kFwdKStages) { ks = 0; kph ^= 1; }
         ++su;
       };
@@ -191,16 +195,20 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           tc::tc_fence_after();
           const uint8_t* p = sP + pb * 2 * kAtom;
           const uint8_t* v = sV + vs * v_bytes;
+          if (issuer) {
 #pragma unroll
-          for (int k = 0; k < 8; ++k)
-            tc::mma_bf16(tmem + 256, kdesc(p + (k >> 2) * kAtom + (k & 3) * 32),
-                         kdesc(v + (k >> 2) * C2 * 128 + (k & 3) * 32), idO, (c | k) != 0);
-          tc::mma_commit(&pempty[pb]);
-          tc::mma_commit(&vempty[vs]);
+            for (int k = 0; k < 8; ++k)
+              tc::mma_bf16(tmem + 256, kdesc(p + (k >> 2) * kAtom + (k & 3) * 32),
+                           kdesc(v + (k >> 2) * C2 * 128 + (k & 3) * 32), idO, (c | k) != 0);
+            tc::mma_commit(&pempty[pb]);
+            tc::mma_commit(&vempty[vs]);
+          }
+          __syncwarp();
           if (++vs == kFwdVStages) { vs = 0; vph ^= 1; }
           ++pc;
         }
-        tc::mma_commit(ofull);
+        if (issuer) tc::mma_commit(ofull);
+        __syncwarp();
       }
     }
   } else {
@@ -407,7 +415,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {   // whole (converged) warp runs the loop, one elected lane issues: uniform descriptors
+      const bool issuer = tc::elect_one();
       const uint32_t idS = tc::idesc_bf16(kT, kT, false, false);
       const uint32_t idDG = tc::idesc_bf16(kT, C2, false, true);
       const uint32_t idDPH = tc::idesc_bf16(kT, Cq, false, true);
@@ -420,13 +429,16 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tc::mbar_wait(sempty, (t & 1) ^ 1);
         tc::tc_fence_after();
         const uint8_t* sb = sStage + st * stage_bytes;
-        for (int k = 0; k < qsteps; ++k)
-          tc::mma_bf16(tmem + cS, kdesc(sPhi + k * 32), kdesc(sb + k * 32), idS, k > 0);
-        for (int k = 0; k < gsteps; ++k) {
-          const uint32_t off = (k >> 2) * kAtom + (k & 3) * 32;
-          tc::mma_bf16(tmem + cDP, kdesc(sG + off), kdesc(sb + kAtom + off), idS, k > 0);
+        if (issuer) {
+          for (int k = 0; k < qsteps; ++k)
+            tc::mma_bf16(tmem + cS, kdesc(sPhi + k * 32), kdesc(sb + k * 32), idS, k > 0);
+          for (int k = 0; k < gsteps; ++k) {
+            const uint32_t off = (k >> 2) * kAtom + (k & 3) * 32;
+            tc::mma_bf16(tmem + cDP, kdesc(sG + off), kdesc(sb + kAtom + off), idS, k > 0);
+          }
+          tc::mma_commit(sfull);
         }
-        tc::mma_commit(sfull);
+        __syncwarp();
       };
       issue_s(0);
       for (int t = 0; t < T; ++t) {
@@ -438,20 +450,24 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tc::mbar_wait(&pfull[pb], (t / NP) & 1);
         tc::mbar_wait(&dtempty[db], ((t >> 1) & 1) ^ 1);
         tc::tc_fence_after();
-#pragma unroll 1
-        for (int k = 0; k < 8; ++k) {   // K = 128 queries in steps of 16
-          const uint32_t koff = (k >> 2) * kAtom + (k & 3) * 32;
-          tc::mma_bf16(tmem + cDG, kdesc(sPT + koff), mndesc(sb + kAtom + k * 2048), idDG, (t | k) != 0);
-          tc::mma_bf16(tmem + cDPH, kdesc(sDS + koff), mndesc(sb + k * 2048), idDPH, (t | k) != 0);
+        if (issuer) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {   // K = 128 queries in steps of 16
+            const uint32_t koff = (k >> 2) * kAtom + (k & 3) * 32;
+            tc::mma_bf16(tmem + cDG, kdesc(sPT + koff), mndesc(sb + kAtom + k * 2048), idDG, (t | k) != 0);
+            tc::mma_bf16(tmem + cDPH, kdesc(sDS + koff), mndesc(sb + k * 2048), idDPH, (t | k) != 0);
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k)     // K = 128 keys in steps of 16
+            tc::mma_bf16(tmem + cDT + db * 32, mndesc(sDS + k * 2048), mndesc(sPhi + k * 2048), idDT, k > 0);
+          tc::mma_commit(&pempty[pb]);
+          tc::mma_commit(&qempty[st]);
+          tc::mma_commit(&dtfull[db]);
         }
-#pragma unroll 1
-        for (int k = 0; k < 8; ++k)     // K = 128 keys in steps of 16
-          tc::mma_bf16(tmem + cDT + db * 32, mndesc(sDS + k * 2048), mndesc(sPhi + k * 2048), idDT, k > 0);
-        tc::mma_commit(&pempty[pb]);
-        tc::mma_commit(&qempty[st]);
-        tc::mma_commit(&dtfull[db]);
+        __syncwarp();
       }
-      tc::mma_commit(accfull);
+      if (issuer) tc::mma_commit(accfull);
+      __syncwarp();
     }
   } else {
     const int qd = warp & 3;

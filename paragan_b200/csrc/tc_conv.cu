@@ -1640,12 +1640,13 @@ cudaError_t tc_conv_wgrad(const void* x, const void* dy, int N, int H, int W, in
   // one filter row per CTA (k_conv_wgrad3) for 3x3 convs whose tile rows are >= 16 pixels
   static const int row3_on = env_int("PARAGAN_WGRAD3", 1);
   int bn3 = 0;
-  // (measured, B200: 96 -> 96 at 128x128 490 -> 673 TFLOP/s, 384 -> 384 953 -> 1011; C_in = 192 is faster
-  // as one N = 192 tap per CTA, 818 vs 700)
+  // (measured in the bench step, B200: 96 -> 96 at 128x128 665 -> 816 TFLOP/s, 192 -> 192 at 64x64 828 -> 872
+  // as two 96-channel blocks, 384 -> 384 at 32x32 1185 -> 1342)
   if (row3_on && ksz == 3 && W >= 16) {
     if (Cin <= 64) bn3 = 64;
     else if (Cin <= 96) bn3 = 96;
     else if (Cin % 128 == 0) bn3 = 128;
+    else if (Cin % 96 == 0) bn3 = 96;
   }
   CUtensorMap mdy, mx;
   PG_CUDA(act_map(&mdy, dy, N, H, W, Cout));
