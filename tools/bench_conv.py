@@ -15,6 +15,10 @@ SHAPES = [  # n, h, w, cin, cout, k
     (256, 64, 64, 96, 192, 1),
     (512, 64, 64, 96, 192, 1),
     (512, 64, 64, 96, 48, 1),
+    (512, 64, 64, 96, 64, 1),
+    (512, 64, 64, 96, 96, 1),
+    (512, 64, 64, 128, 48, 1),
+    (512, 64, 64, 64, 48, 1),
     (512, 128, 128, 96, 96, 3),
     (512, 64, 64, 192, 192, 3),
 ]
