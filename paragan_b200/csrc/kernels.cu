@@ -2418,97 +2418,88 @@ __global__ void __launch_bounds__(256, 2) k_thin_fwd(const float* __restrict__ x
 
 // ---------------------------------------------------------------------------
 // dgrad: dx[m][c] = sum_{o,r,s} dy[h+1-r][w+1-s][o] w[o][r][s][c]  (transposed 3x3, pad 1)
-// Persistent blocks (weights staged once) walk 8 rows x 64 cols tiles; thread = pixels (row, px)
-// and (row, px+32) with their 2 x 27 dy taps in registers; loops over channels in fours:
-// 4 x 7 broadcast float4 weight loads per 216 FMAs.  The dy halo's loads are all issued before
-// any is stored (one memory round trip per tile).
-constexpr int kDTH = 8, kDTW = 64;
+// Thread = (input channel c, pixel group): its 27 weights w[.][.][.][c] live in registers and it
+// walks 4-pixel row chunks of the tile; the dy halo ([10][34] pixels x 4, the 3 channels padded) is
+// staged per tile with cp.async (double-buffered) and read as broadcast float4s (18 per chunk for
+// 108 FMAs).  A warp's stores cover 32 consecutive channels of one pixel: fully coalesced.
+constexpr int kDTH = 8, kDTW = 32;
+__device__ __forceinline__ void cp_async4_zfill(float* dst, const float* src, bool ok) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(src), "r"(ok ? 4 : 0) : "memory");
+}
 template <int CO>
-__global__ void __launch_bounds__(256) k_thin_dgrad(const float* __restrict__ dy, int N, int H, int W, int C,
-                                                    const float* __restrict__ w, float* __restrict__ dx) {
-  extern __shared__ float4 sm4[];
-  float* ws = reinterpret_cast<float*>(sm4);        // [C][28]
-  float* ds = ws + C * 28;                           // [CO][kDTH + 2][kDTW + 2]
+__global__ void __launch_bounds__(384, 2) k_thin_dgrad(const float* __restrict__ dy, int N, int H, int W, int C,
+                                                       const float* __restrict__ w, float* __restrict__ dx) {
+  constexpr int HR = kDTH + 2, HC = kDTW + 2, kHalo = HR * HC;
+  __shared__ float4 ds[2][kHalo];
   const int tiles_w = (W + kDTW - 1) / kDTW, tiles_h = (H + kDTH - 1) / kDTH;
   const int tiles = N * tiles_h * tiles_w;
-  for (int i = threadIdx.x; i < C * 28; i += blockDim.x) {
-    const int c = i / 28, k = i - c * 28;
-    ws[i] = k < CO * 9 ? w[(long long)k * C + c] : 0.0f;
-  }
-  constexpr int HR = kDTH + 2, HC = kDTW + 2;
-  constexpr int kItems = CO * HR * HC, kPer = (kItems + 255) / 256;
-  const int row = threadIdx.x >> 5, px = threadIdx.x & 31;
-  for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+  const int c = threadIdx.x % C, pg = threadIdx.x / C, npg = blockDim.x / C;
+  float wv[CO * 9];   // wv[o*9 + r*3 + s] = w[o][r][s][c]
+#pragma unroll
+  for (int k = 0; k < CO * 9; ++k) wv[k] = w[(long long)k * C + c];
+  auto stage = [&](int t, int buf) {
     int u = t;
     const int tw = u % tiles_w;
     u /= tiles_w;
     const int th = u % tiles_h;
     const int n = u / tiles_h;
     const int h0 = th * kDTH, w0 = tw * kDTW;
-    float v[kPer];
-#pragma unroll
-    for (int j = 0; j < kPer; ++j) {
-      const int i = threadIdx.x + j * 256;
-      v[j] = 0.0f;
-      if (i < kItems) {
-        const int o = i % CO, rs = i / CO;
-        const int sx = rs % HC, r = rs / HC;
-        const int h = h0 - 1 + r, ww = w0 - 1 + sx;
-        if (h >= 0 && h < H && ww >= 0 && ww < W) v[j] = __ldg(dy + (((long long)n * H + h) * W + ww) * CO + o);
-      }
+    float* d = reinterpret_cast<float*>(ds[buf]);
+    for (int i = threadIdx.x; i < kHalo * CO; i += blockDim.x) {
+      const int o = i % CO, rs = i / CO;
+      const int sx = rs % HC, r = rs / HC;
+      const int h = h0 - 1 + r, ww = w0 - 1 + sx;
+      const bool ok = h >= 0 && h < H && ww >= 0 && ww < W;
+      cp_async4_zfill(d + rs * 4 + o, ok ? dy + (((long long)n * H + h) * W + ww) * CO + o : dy, ok);
     }
-    __syncthreads();   // previous tile's ds reads (and, first time, the weight stores) are done
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  int buf = 0;
+  if (blockIdx.x < tiles) stage(blockIdx.x, 0);
+  for (int t = blockIdx.x; t < tiles; t += gridDim.x, buf ^= 1) {
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();   // tile t landed for every thread; the other buffer's readers are done
+    if (t + (int)gridDim.x < tiles) stage(t + gridDim.x, buf ^ 1);
+    int u = t;
+    const int tw = u % tiles_w;
+    u /= tiles_w;
+    const int th = u % tiles_h;
+    const int n = u / tiles_h;
+    const int h0 = th * kDTH, w0 = tw * kDTW;
+    const float4* hal = ds[buf];
+    for (int q = pg; q < kDTH * (kDTW / 4); q += npg) {
+      const int row = q / (kDTW / 4), x0 = (q % (kDTW / 4)) * 4;
+      float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+      // output (row, x0 + i) reads halo (row + 2 - r, x0 + i + 2 - s)
 #pragma unroll
-    for (int j = 0; j < kPer; ++j) {
-      const int i = threadIdx.x + j * 256;
-      if (i < kItems) {
-        const int o = i % CO, rs = i / CO;
-        ds[o * HR * HC + rs] = v[j];
+      for (int hr = 0; hr < 3; ++hr) {        // halo row row + hr  <->  r = 2 - hr
+        const int r = 2 - hr;
+#pragma unroll
+        for (int cc = 0; cc < 6; ++cc) {      // halo column x0 + cc  <->  s = i + 2 - cc
+          const float4 g = hal[(row + hr) * HC + x0 + cc];
+          const float gv[3] = {g.x, g.y, g.z};
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int sx = i + 2 - cc;
+            if (sx >= 0 && sx <= 2) {
+#pragma unroll
+              for (int o = 0; o < CO; ++o) acc[i] = fmaf(gv[o], wv[o * 9 + r * 3 + sx], acc[i]);
+            }
+          }
+        }
       }
-    }
-    __syncthreads();
-    const int h = h0 + row;
-    // dx at (h, w) gathers dy at (h + 1 - r, w + 1 - s): halo row row + 2 - r, column px + 2 - s
-    float d0[CO * 9], d1[CO * 9];
+      const int h = h0 + row;
+      if (h < H) {
 #pragma unroll
-    for (int o = 0; o < CO; ++o)
-#pragma unroll
-      for (int r = 0; r < 3; ++r)
-#pragma unroll
-        for (int sx = 0; sx < 3; ++sx) {
-          d0[o * 9 + r * 3 + sx] = ds[(o * HR + row + 2 - r) * HC + px + 2 - sx];
-          d1[o * 9 + r * 3 + sx] = ds[(o * HR + row + 2 - r) * HC + px + 32 + 2 - sx];
+        for (int i = 0; i < 4; ++i) {
+          const int ww = w0 + x0 + i;
+          if (ww < W) dx[(((long long)n * H + h) * W + ww) * C + c] = acc[i];
         }
-    const int wa = w0 + px, wb = w0 + px + 32;
-    const bool va = h < H && wa < W, vb = h < H && wb < W;
-    float* xa = dx + (((long long)n * H + h) * W + wa) * C;
-    float* xb = dx + (((long long)n * H + h) * W + wb) * C;
-    for (int c = 0; c < C; c += 4) {
-      float a[4], bq[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        float wv[28];
-#pragma unroll
-        for (int k = 0; k < 7; ++k) {
-          const float4 q = *reinterpret_cast<const float4*>(ws + (c + j) * 28 + 4 * k);
-          wv[4 * k] = q.x;
-          wv[4 * k + 1] = q.y;
-          wv[4 * k + 2] = q.z;
-          wv[4 * k + 3] = q.w;
-        }
-        float sa = 0.0f, sb = 0.0f;
-#pragma unroll
-        for (int k = 0; k < CO * 9; ++k) {
-          sa = fmaf(d0[k], wv[k], sa);
-          sb = fmaf(d1[k], wv[k], sb);
-        }
-        a[j] = sa;
-        bq[j] = sb;
       }
-      if (va) *reinterpret_cast<float4*>(xa + c) = make_float4(a[0], a[1], a[2], a[3]);
-      if (vb) *reinterpret_cast<float4*>(xb + c) = make_float4(bq[0], bq[1], bq[2], bq[3]);
     }
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -2537,7 +2528,6 @@ __global__ void __launch_bounds__(512) k_thin_wgrad(const float* __restrict__ x,
   const int tiles_w = (W + kWTW - 1) / kWTW, tiles_h = (H + kWTH - 1) / kWTH;
   const int tiles = N * tiles_h * tiles_w;
   const int c = threadIdx.x % C, py = threadIdx.x / C;        // blockDim = kWTH * C
-  const int nvec = (kWTH + 2) * HC * (C / 4);
   auto stage = [&](int t, int buf) {
     int u = t;
     const int tw = u % tiles_w;
@@ -2546,8 +2536,9 @@ __global__ void __launch_bounds__(512) k_thin_wgrad(const float* __restrict__ x,
     const int n = u / tiles_h;
     const int h0 = th * kWTH, w0 = tw * kWTW;
     float* xs = xs0 + buf * xs_floats;
-    for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
-      const int cv = i % (C / 4), rs = i / (C / 4);
+    // blockDim = kWTH * C = 16 * (C / 4): the vector index cv is fixed per thread, rs advances by 16
+    const int cv = threadIdx.x % (C / 4);
+    for (int rs = threadIdx.x / (C / 4); rs < (kWTH + 2) * HC; rs += 4 * kWTH) {
       const int sx = rs % HC, r = rs / HC;
       const int h = h0 - 1 + r, ww = w0 - 1 + sx;
       const bool ok = h >= 0 && h < H && ww >= 0 && ww < W;
@@ -2917,15 +2908,14 @@ cudaError_t thin_conv_fwd(const float* x, int N, int H, int W, int C, const floa
 }
 cudaError_t thin_conv_dgrad(const float* dy, int N, int H, int W, int C, const float* w, int CO, float* dx,
                             cudaStream_t st) {
-  if (CO != 3 || C % 4 || ((uintptr_t)dx & 15)) return cudaErrorInvalidValue;
+  if (CO != 3 || C > 384) return cudaErrorInvalidValue;
   const int tiles = N * ((H + kDTH - 1) / kDTH) * ((W + kDTW - 1) / kDTW);
-  const size_t sm = (size_t)(C * 28 + CO * (kDTH + 2) * (kDTW + 2)) * sizeof(float);
-  PG_CUDA(cudaFuncSetAttribute(k_thin_dgrad<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  const int npg = 384 / C;
   int per_sm = 1;
-  PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_thin_dgrad<3>, 256, sm));
+  PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_thin_dgrad<3>, npg * C, 0));
   if (per_sm < 1) per_sm = 1;
   const int grid = tiles < per_sm * kNumSMs ? tiles : per_sm * kNumSMs;
-  k_thin_dgrad<3><<<grid, 256, sm, st>>>(dy, N, H, W, C, w, dx);
+  k_thin_dgrad<3><<<grid, npg * C, 0, st>>>(dy, N, H, W, C, w, dx);
   return cudaGetLastError();
 }
 cudaError_t thin_conv_wgrad(const float* x, const float* dy, int N, int H, int W, int C, int CO, float* dw,
