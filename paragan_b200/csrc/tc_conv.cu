@@ -66,6 +66,19 @@ struct WgradCfg {
 };
 
 template <int BN>
+struct WgradCg2Cfg {   // per CTA: 128 dY channels x 128 pixels (A), BN / 2 input channels (B half)
+  static constexpr int NB = BN / 128;                  // 64-wide MN atoms of this CTA's B half
+  static constexpr uint32_t A_BYTES = 2 * kAtomBytes;
+  static constexpr uint32_t B_BYTES = NB * kAtomBytes;
+  static constexpr uint32_t ONES_BYTES = kAtomBytes;
+  static constexpr int STAGES_RAW = (232448 - 2048 - (int)ONES_BYTES) / (A_BYTES + B_BYTES);
+  static constexpr int STAGES = STAGES_RAW > 6 ? 6 : STAGES_RAW;
+  static constexpr uint32_t TMEM_COLS = (BN + 32 <= 128) ? 128 : (BN + 32 <= 256) ? 256 : 512;
+  static constexpr size_t SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + ONES_BYTES + 256;
+  static_assert(BN % 128 == 0, "each CTA's B half must be whole 64-channel atoms");
+};
+
+template <int BN>
 struct Wgrad3Cfg {
   static constexpr int NB = (BN + 63) / 64;            // 64-channel chunks of the X halo
   static constexpr uint32_t XCH = 18432;               // one chunk: up to 144 halo pixel rows x 128 B
@@ -602,6 +615,166 @@ __global__ void __launch_bounds__(192, 1)
   tc::tc_fence_before();
   __syncthreads();
   if (warp == 1) tc::tmem_dealloc(tmem, C::TMEM_COLS);
+}
+
+// ===========================================================================
+// wgrad, CTA pair (cta_group::2): M = 256 output channels per pair tile — each CTA stages its own
+// 128 dY channels (A) and HALF of the B tile (BN / 2 input channels of X), the leader issues
+// tcgen05.mma.cta_group::2 over both CTAs' shared memory and each CTA's TMEM holds its 128 rows.
+// Per SM this halves the B traffic (TMA writes and tensor-core reads), the shared-memory
+// bandwidth the one-CTA kernel saturates at C_in, C_out >= 256.  Same work units / split-K
+// partials / phase (sub-pixel) taps as k_conv_wgrad, with unit = (split, pair tile, n tile).
+// ===========================================================================
+template <int BN>
+__global__ void __launch_bounds__(192, 1)
+    k_conv_wgrad_cg2(const __grid_constant__ CUtensorMap tmDY, const __grid_constant__ CUtensorMap tmX,
+                     const TcWgradArgs a, const __grid_constant__ TmaQuad tq) {
+  using C = WgradCg2Cfg<BN>;
+  constexpr int STAGES = C::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * C::A_BYTES;
+  uint8_t* sOnes = sB + STAGES * C::B_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sOnes + C::ONES_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = tc::cluster_rank();
+  const bool is_leader = rank == 0;
+  const int unit = (int)tc::cluster_id_x();
+  const int mpairs = (a.m_tiles + 1) / 2;
+  const int tiles = mpairs * a.n_tiles;
+  const int split = unit / tiles;
+  const int uu = unit - split * tiles;
+  const int nt = uu % a.n_tiles;
+  const int mp = uu / a.n_tiles;
+  const bool do_bias = a.bias_out != nullptr &&
+                       (a.phases > 1 ? (nt % a.c_blocks == 0 && (nt / a.c_blocks) % 4 == 0) : nt == 0);
+  if (do_bias) {
+    uint4* o4 = reinterpret_cast<uint4*>(sOnes);
+    for (int i = threadIdx.x; i < (int)(C::ONES_BYTES / 16); i += blockDim.x)
+      o4[i] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
+    tc::fence_async_smem();
+  }
+  if (warp == 0 && lane == 0) {
+    tc::tma_prefetch(&tmDY);
+    tc::tma_prefetch(&tmX);
+    for (int s = 0; s < STAGES; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    tc::mbar_init(&tfull[0], 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc_cg2(tmem_slot, C::TMEM_COLS);
+  tc::tc_fence_before();
+  tc::cluster_sync();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const int tap = nt / a.c_blocks, cb = nt - tap * a.c_blocks;
+  const int pad = a.ksz >> 1;
+  int dy = tap / a.ksz - pad, dx = tap % a.ksz - pad;
+  const int ph = a.phases > 1 ? tap >> 2 : 0;
+  if (a.phases > 1) {
+    dy = ((tap >> 1) & 1) - 1 + (ph >> 1);
+    dx = (tap & 1) - 1 + (ph & 1);
+  }
+  const CUtensorMap* mdy = a.phases > 1 ? &tq.m[ph] : &tmDY;
+  const int kb0 = split * a.kb_per_split;
+  const int kb1 = min(a.total_kb, kb0 + a.kb_per_split);
+  const int o0 = mp * 256 + (int)rank * 128;          // this CTA's 128 output channels
+  const int c0 = cb * BN + (int)rank * (BN / 2);      // this CTA's half of the input channels
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        int n0, h0, w0;
+        pix_origin(kb * kTileM, a.H, a.W, n0, h0, w0);
+        tc::mbar_wait(&empty[stage], phase ^ 1);
+        const uint32_t fbar = tc::map_to_rank(&full[stage], 0);
+        if (is_leader) tc::mbar_expect_tx(&full[stage], 2 * (C::A_BYTES + C::B_BYTES));
+        uint8_t* da = sA + stage * C::A_BYTES;
+        tc::tma_load_4d_cg2(da, mdy, fbar, o0, w0, h0, n0);
+        tc::tma_load_4d_cg2(da + kAtomBytes, mdy, fbar, o0 + 64, w0, h0, n0);
+        uint8_t* db = sB + stage * C::B_BYTES;
+#pragma unroll
+        for (int j = 0; j < C::NB; ++j)
+          tc::tma_load_4d_cg2(db + j * kAtomBytes, &tmX, fbar, c0 + 64 * j, w0 + dx, h0 + dy, n0);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    if (is_leader) {   // whole (converged) warp runs the loop; one elected lane issues
+      constexpr uint32_t idesc = tc::idesc_bf16(256, BN, true, true);
+      constexpr uint32_t idb = tc::idesc_bf16(256, 16, true, true);
+      const bool issuer = tc::elect_one();
+      const uint32_t sA0 = tc::smem_u32(sA), sB0 = tc::smem_u32(sB), o_base = tc::smem_u32(sOnes);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        tc::mbar_wait(&full[stage], phase);
+        tc::tc_fence_after();
+        const uint32_t a_base = sA0 + stage * C::A_BYTES;
+        const uint32_t b_base = sB0 + stage * C::B_BYTES;
+        if (issuer) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {   // 8 x K=16 pixels
+            const uint64_t ad = tc::sdesc_sw128(a_base + k * 2048, kAtomBytes, 1024);
+            const uint64_t bd = tc::sdesc_sw128(b_base + k * 2048, kAtomBytes, 1024);
+            tc::mma_bf16_cg2(tmem, ad, bd, idesc, (kb != kb0) || (k != 0));
+          }
+          if (do_bias) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              tc::mma_bf16_cg2(tmem + BN, tc::sdesc_sw128(a_base + k * 2048, kAtomBytes, 1024),
+                               tc::sdesc_sw128(o_base + k * 2048, kAtomBytes, 1024), idb, (kb != kb0) || (k != 0));
+          }
+          tc::mma_commit_cg2(&empty[stage], 3);
+        }
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+      if (issuer) tc::mma_commit_cg2(&tfull[0], 3);
+      __syncwarp();
+    }
+  } else {
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    tc::mbar_wait(&tfull[0], 0);
+    tc::tc_fence_after();
+    const int o = o0 + row;
+    if (do_bias) {
+      float v[32];
+      tc::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + BN, v);
+      if (o < a.Cout) a.bias_out[((long long)split * (a.phases > 1 ? 4 : 1) + ph) * a.Cout + o] = v[0];
+    }
+    const int cbase = cb * BN;
+#pragma unroll 1
+    for (int cbk = 0; cbk < BN; cbk += 32) {
+      float v[32];
+      tc::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + cbk, v);
+      const int col0 = cbase + cbk;
+      if (o >= a.Cout || col0 >= a.Cin) continue;
+      float* op = a.out + (((long long)split * a.Cout + o) * a.taps + tap) * a.Cin + col0;
+      if (col0 + 32 <= a.Cin && ((reinterpret_cast<uintptr_t>(op) & 15) == 0)) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(op + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (col0 + j < a.Cin) op[j] = v[j];
+      }
+    }
+  }
+  tc::tc_fence_before();
+  tc::cluster_sync();
+  if (warp == 1) tc::tmem_dealloc_cg2(tmem, C::TMEM_COLS);
 }
 
 // ===========================================================================
@@ -1303,6 +1476,33 @@ cudaError_t launch_wgrad_bn(const CUtensorMap& ma, const CUtensorMap& mb, const 
 }
 
 template <int BN>
+cudaError_t launch_wgrad_cg2_bn(const CUtensorMap& ma, const CUtensorMap& mb, const TcWgradArgs& a, cudaStream_t st,
+                                const TmaQuad* quad = nullptr) {
+  using C = WgradCg2Cfg<BN>;
+  static bool attr = false;
+  if (!attr) {
+    PG_CUDA(cudaFuncSetAttribute(k_conv_wgrad_cg2<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    attr = true;
+  }
+  const int units = ((a.m_tiles + 1) / 2) * a.n_tiles * a.splits;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * units, 1, 1);
+  cfg.blockDim = dim3(192, 1, 1);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeClusterDimension;
+  attrs[0].val.clusterDim.x = 2;
+  attrs[0].val.clusterDim.y = 1;
+  attrs[0].val.clusterDim.z = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  TmaQuad tq;
+  for (int i = 0; i < 4; ++i) tq.m[i] = quad ? quad->m[i] : ma;
+  return cudaLaunchKernelEx(&cfg, k_conv_wgrad_cg2<BN>, ma, mb, a, tq);
+}
+
+template <int BN>
 cudaError_t launch_wgrad3_bn(const CUtensorMap& ma, const CUtensorMap& mb, const TcWgradArgs& a, cudaStream_t st) {
   using C = Wgrad3Cfg<BN>;
   static bool attr = false;
@@ -1594,8 +1794,10 @@ cudaError_t tc_conv_wgrad_up2(const void* x, const void* dy, int N, int H, int W
   a.splits = ceil_div(a.total_kb, a.kb_per_split);
   a.out = scratch;
   a.bias_out = dbias ? scratch + (size_t)a.splits * out_floats : nullptr;
+  static const int wg_cg2 = env_int("PARAGAN_WGRAD_CG2", 2);
   cudaError_t e;
-  switch (bn) {
+  if (wg_cg2 && bn == 256 && Cout % 256 == 0) e = launch_wgrad_cg2_bn<256>(tq.m[0], mx, a, st, &tq);
+  else switch (bn) {
     case 32: e = launch_wgrad_bn<32>(tq.m[0], mx, a, st, &tq); break;
     case 64: e = launch_wgrad_bn<64>(tq.m[0], mx, a, st, &tq); break;
     case 96: e = launch_wgrad_bn<96>(tq.m[0], mx, a, st, &tq); break;
@@ -1638,11 +1840,15 @@ cudaError_t tc_conv_wgrad(const void* x, const void* dy, int N, int H, int W, in
   else if (Cin <= 96) bn = 96;
   else bn = 128;
   // one filter row per CTA (k_conv_wgrad3) for 3x3 convs whose tile rows are >= 16 pixels
-  static const int row3_on = env_int("PARAGAN_WGRAD3", 1);
+  static const int row3_on = env_int("PARAGAN_WGRAD3", 1), wg_cg2 = env_int("PARAGAN_WGRAD_CG2", 2);
+  // CTA-pair kernel for C_in, C_out multiples of 256 (measured in the bench step: 1536 -> 1536 at 8x8
+  // 1093 -> 1394 TFLOP/s, 768 -> 768 at 16x16 1421 (one-row kernel) -> 1520); PARAGAN_WGRAD_CG2=1 keeps
+  // the one-row kernel for 3x3 layers with W >= 16, 0 disables the pair kernel
+  const bool pair = wg_cg2 && Cin % 256 == 0 && Cout % 256 == 0 && (wg_cg2 == 2 || ksz != 3 || W < 16);
   int bn3 = 0;
   // (measured in the bench step, B200: 96 -> 96 at 128x128 665 -> 816 TFLOP/s, 192 -> 192 at 64x64 828 -> 872
   // as two 96-channel blocks, 384 -> 384 at 32x32 1185 -> 1342)
-  if (row3_on && ksz == 3 && W >= 16) {
+  if (row3_on && ksz == 3 && W >= 16 && !pair) {
     if (Cin <= 64) bn3 = 64;
     else if (Cin <= 96) bn3 = 96;
     else if (Cin % 128 == 0) bn3 = 128;
@@ -1680,7 +1886,9 @@ cudaError_t tc_conv_wgrad(const void* x, const void* dy, int N, int H, int W, in
   a.out = direct ? dw : scratch;
   a.bias_out = dbias ? (direct ? dbias : scratch + (size_t)a.splits * out_floats) : nullptr;
   cudaError_t e;
-  if (bn3) {
+  if (pair) {
+    e = launch_wgrad_cg2_bn<256>(mdy, mx, a, st);
+  } else if (bn3) {
     // the cost model's per-K-block time covers the three taps
     switch (bn3) {
       case 64: e = launch_wgrad3_bn<64>(mdy, mx, a, st); break;

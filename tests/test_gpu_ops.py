@@ -72,6 +72,8 @@ CONV_SHAPES = [  # n, h, w, cin, cout, k
     (5, 8, 8, 64, 128, 3),       # odd number of M tiles (CTA-pair kernel: last pair half empty)
     (4, 8, 8, 1536, 1536, 3),    # CTA pairs with several N tiles
     (2, 16, 32, 384, 136, 3),    # wgrad, one filter row per CTA: 3 x 128-channel blocks, C_out tail
+    (3, 4, 8, 512, 256, 1),      # wgrad on the CTA-pair kernel, 1x1, odd M tile count
+    (2, 8, 8, 256, 768, 3),      # wgrad on the CTA-pair kernel, three pair tiles
 ]
 
 
@@ -206,6 +208,7 @@ UP2_SHAPES = [  # n, h, w, cin, cout  (low-resolution input; output 2h x 2w)
     (2, 16, 16, 192, 96),        # 96-channel tail chunk, odd N tiles
     (1, 64, 64, 192, 96),        # G's last conv1 at quarter batch
     (3, 8, 8, 32, 256),          # several N tiles, odd number of M tiles
+    (2, 4, 4, 256, 512),         # wgrad on the CTA-pair kernel (C_in, C_out multiples of 256)
 ]
 
 
