@@ -30,6 +30,7 @@ namespace pg {
 namespace {
 
 constexpr int kMaxPartialBlocks = 1184;  // 8 waves of 148 SMs
+constexpr int kDcondK = 256;              // K slice of the split-K CBN dcond GEMMs
 
 struct Arena {
   char* base = nullptr;
@@ -131,6 +132,8 @@ struct GBlock {
   void *x, *u1, *h1, *a2, *s, *out;
   void* u1lo = nullptr;            // CBN1-ReLU output before the upsample (sub-pixel conv1 input)
   float *gain1, *bias1, *gain2, *bias2, *cond, *dcond;
+  float* dcond_part;   // [slices][B][cond_dim] split-K partials of dcond
+  int dcond_nslot;
   float *ab1 = nullptr, *ab2 = nullptr;   // CBN backward per-sample [dbias | dgain] rows [B][2C]
   float *mean1, *rstd1, *mean2, *rstd2;
   double *sums1, *sums2;
@@ -790,6 +793,7 @@ class Engine final : public EngineBase {
       b.bias2 = A.get<float>((size_t)B * b.cout);
       b.cond = A.get<float>((size_t)B * cd_);
       b.dcond = A.get<float>((size_t)B * cd_);
+      b.dcond_part = A.get<float>((size_t)B * cd_ * (2 * ceil_div(b.cin, kDcondK) + 2 * ceil_div(b.cout, kDcondK)));
       b.ab1 = A.get<float>((size_t)B * 2 * b.cin);
       b.ab2 = A.get<float>((size_t)B * 2 * b.cout);
       b.mean1 = A.get<float>(b.cin);
@@ -876,7 +880,9 @@ class Engine final : public EngineBase {
       const size_t nb = gb_.size();
       cbn_fwd_d_ = A.get<GemmProblem>(4 * nb + 1);
       cbn_dw_d_ = A.get<GemmProblem>(4 * nb);
-      cbn_dcond_d_ = A.get<GemmProblem>(nb);
+      size_t nslots = 0;
+      for (auto& b : gb_) nslots += 2 * ceil_div(b.cin, kDcondK) + 2 * ceil_div(b.cout, kDcondK);
+      cbn_dcond_d_ = A.get<GemmProblem>(std::max<size_t>(nslots, 1));
     }
     bn_part_ = A.get<float>((size_t)B * 64 * 2 * maxc_);
     dpart_ = A.get<double>((size_t)kMaxPartialBlocks * 2 * std::max(maxc_, 16 * c0_));
@@ -933,11 +939,7 @@ class Engine final : public EngineBase {
       float* outs[4] = {b.gain1, b.bias1, b.gain2, b.bias2};
       float* abs_[4] = {b.ab1 + b.cin, b.ab1, b.ab2 + b.cout, b.ab2};   // dgain = AB[:, C:2C], dbias = AB[:, 0:C]
       const int Cs[4] = {b.cin, b.cin, b.cout, b.cout};
-      GemmProblem pc{};
-      pc.M = B;
-      pc.N = cd_;
-      pc.C = b.dcond;
-      pc.ldc = cd_;
+      b.dcond_nslot = 0;
       for (int k = 0; k < 4; ++k) {
         GemmProblem p{};
         p.M = B;
@@ -956,10 +958,21 @@ class Engine final : public EngineBase {
         q.C = G_.G(L[k]->w);
         q.ldc = cd_;
         dw.push_back(q);
-        // dcond[n][k] = sum over the four linears of sum_c dX[n][c] What[c][k]
-        pc.seg[pc.nseg++] = seg(abs_[k], 2 * Cs[k], 1, L[k]->what, 1, cd_, Cs[k]);
+        // dcond[n][k] = sum over the four linears of sum_c dX[n][c] What[c][k]: M x N = B x cond_dim
+        // is small and K = C long, so split K into kDcondK-channel slices (one partial each, summed
+        // in slice order afterwards) — as one tile row per block it ran on 60 SMs for 0.7 ms
+        for (int c0 = 0; c0 < Cs[k]; c0 += kDcondK) {
+          GemmProblem pc{};
+          pc.M = B;
+          pc.N = cd_;
+          pc.nseg = 1;
+          pc.seg[0] = seg(abs_[k] + c0, 2 * Cs[k], 1, L[k]->what + (size_t)c0 * cd_, 1, cd_,
+                          std::min(kDcondK, Cs[k] - c0));
+          pc.C = b.dcond_part + (size_t)b.dcond_nslot++ * B * cd_;
+          pc.ldc = cd_;
+          dc.push_back(pc);
+        }
       }
-      dc.push_back(pc);
     }
     cbn_fwd_n_ = (int)fw.size();
     cbn_fwd_tiles_ = gemm_grouped_plan(fw.data(), cbn_fwd_n_);
@@ -2033,6 +2046,7 @@ class Engine final : public EngineBase {
     // CBN linears: every dW, then every block's dcond (sum over its four linears), one launch each
     CK(gemm_f32_grouped(cbn_dw_d_, cbn_dw_n_, cbn_dw_tiles_, st_));
     CK(gemm_f32_grouped(cbn_dcond_d_, cbn_dcond_n_, cbn_dcond_tiles_, st_));
+    for (GBlock& b : gb_) CK(sum_slices(b.dcond_part, b.dcond_nslot, B * cd_, b.dcond, st_));
     // cond -> shared embedding gradient (first shared_dim columns), blocks in order
     for (size_t i0 = 0; i0 < gb_.size(); i0 += 8) {
       RowSrcs rs{};

@@ -90,8 +90,8 @@ __global__ void __launch_bounds__(256) k_gemm(int M, int N, int K, const float* 
                                               long long sam, long long sak, const float* __restrict__ B, long long sbb,
                                               long long sbn, long long sbk, TC* __restrict__ C, long long scb,
                                               long long ldc, float beta, const float* __restrict__ bias) {
-  __shared__ float As[16][65];
-  __shared__ float Bs[16][65];
+  __shared__ __align__(16) float As[16][68];
+  __shared__ __align__(16) float Bs[16][68];
   const int b = blockIdx.z;
   A += b * sab;
   B += b * sbb;
@@ -114,11 +114,9 @@ __global__ void __launch_bounds__(256) k_gemm(int M, int N, int K, const float* 
     __syncthreads();
 #pragma unroll
     for (int kk = 0; kk < 16; ++kk) {
-      float a[4], bb[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) bb[j] = Bs[kk][tx * 4 + j];
+      const float4 a4 = *reinterpret_cast<const float4*>(&As[kk][ty * 4]);
+      const float4 b4 = *reinterpret_cast<const float4*>(&Bs[kk][tx * 4]);
+      const float a[4] = {a4.x, a4.y, a4.z, a4.w}, bb[4] = {b4.x, b4.y, b4.z, b4.w};
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -146,8 +144,10 @@ __global__ void __launch_bounds__(256) k_gemm(int M, int N, int K, const float* 
 // ===================================================================== grouped fp32 GEMM
 // 64x64 tile, 256 threads (4x4 each), K chunks of 16 double-buffered through registers
 __global__ void __launch_bounds__(256) k_gemm_grouped(const GemmProblem* __restrict__ probs, int nprob) {
-  __shared__ float As[2][16][65];
-  __shared__ float Bs[2][16][65];
+  // rows padded to 68 floats: 16-byte aligned, so the inner loop reads each thread's 4 A and 4 B
+  // values as one float4 each (2 shared loads per 16 FMAs instead of 8)
+  __shared__ __align__(16) float As[2][16][68];
+  __shared__ __align__(16) float Bs[2][16][68];
   const int bid = blockIdx.x;
   int pi = 0;
   while (pi + 1 < nprob && probs[pi + 1].tile0 <= bid) ++pi;
@@ -205,11 +205,9 @@ __global__ void __launch_bounds__(256) k_gemm_grouped(const GemmProblem* __restr
     if (ch + 1 < nch) load(ch + 1);
 #pragma unroll
     for (int kk = 0; kk < 16; ++kk) {
-      float a[4], bb[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[buf][kk][ty * 4 + i];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) bb[j] = Bs[buf][kk][tx * 4 + j];
+      const float4 a4 = *reinterpret_cast<const float4*>(&As[buf][kk][ty * 4]);
+      const float4 b4 = *reinterpret_cast<const float4*>(&Bs[buf][kk][tx * 4]);
+      const float a[4] = {a4.x, a4.y, a4.z, a4.w}, bb[4] = {b4.x, b4.y, b4.z, b4.w};
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -2616,6 +2614,11 @@ __global__ void k_reduce_rows_f32(const float* __restrict__ partial, int rows, i
   }
 }
 }  // namespace
+
+cudaError_t sum_slices(const float* part, int nslices, int n, float* dst, cudaStream_t st) {
+  k_reduce_rows_f32<<<ceil_div(n, 256), 256, 0, st>>>(part, nslices, n, dst);
+  return cudaGetLastError();
+}
 
 // one thread per (o, c): the nine 3x3 taps read once, the sixteen folded (phase, tap) weights written.
 // layout 0: c fastest across threads (coalesced reads and writes); layout 1: o fastest (coalesced writes)

@@ -38,6 +38,8 @@ struct GemmProblem {
   float beta;
   const float* bias;
 };
+// dst[i] = sum_{j < nslices} part[j * n + i]   (fp64 sum in slice order: deterministic)
+cudaError_t sum_slices(const float* part, int nslices, int n, float* dst, cudaStream_t st);
 // fills tile0 and returns the total tile count
 int gemm_grouped_plan(GemmProblem* probs, int nprob);
 cudaError_t gemm_f32_grouped(const GemmProblem* probs_dev, int nprob, int total_tiles, cudaStream_t st);
