@@ -7,6 +7,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "tc_ptx.cuh"
 
 namespace pg {
 
@@ -662,6 +663,81 @@ __global__ void __launch_bounds__(256) k_bn_bwd_apply_cs(const TI* __restrict__ 
       if (add) o[j] += ad[j];
     }
     Vec8<TO>::store(dx + p * C + g * 8, o);
+  }
+}
+
+// Bulk-staged variants (memory-level parallelism without registers): each block walks chunks
+// of kBnChunkBytes of consecutive pixels; one thread issues cp.async.bulk copies of the chunk's
+// input(s) into a double-buffered smem ring (mbarrier complete_tx), the threads compute from
+// shared memory with their channel group's constants in registers and store with 16-byte
+// stores.  (The register-staged kernels held 2 x 16 B per thread in flight at 68-90 registers,
+// ~24 KB per SM: 4.1-4.5 TB/s.)
+constexpr int kBnChunkBytes = 16384;
+__device__ __forceinline__ int bn_chunk_pix(int C, int esize) { return kBnChunkBytes / (C * esize); }
+
+template <typename TI, typename TO>
+__global__ void __launch_bounds__(256) k_bn_apply_relu_bulk(const TI* __restrict__ x, long long P_total, int HW, int C,
+                                                            const float* __restrict__ mean,
+                                                            const float* __restrict__ rstd, BnAffine af,
+                                                            TO* __restrict__ y) {
+  __shared__ __align__(128) uint8_t buf[2][kBnChunkBytes];
+  __shared__ __align__(8) uint64_t full[2];
+  const int G = C >> 3;
+  const int lanes = blockDim.x / G;
+  const int g = threadIdx.x % G, lane = threadIdx.x / G;
+  const int cpix = bn_chunk_pix(C, (int)sizeof(TI));
+  const long long nchunks = (P_total + cpix - 1) / cpix;
+  if (threadIdx.x == 0) {
+    tc::mbar_init(&full[0], 1);
+    tc::mbar_init(&full[1], 1);
+    tc::fence_barrier_init();
+  }
+  __syncthreads();
+  auto issue = [&](long long t, int b) {
+    const long long p0 = t * cpix;
+    const int np = (int)min((long long)cpix, P_total - p0);
+    const uint32_t bytes = (uint32_t)np * C * sizeof(TI);
+    tc::mbar_expect_tx(&full[b], bytes);
+    tc::bulk_load_1d(buf[b], x + p0 * C, bytes, &full[b]);
+  };
+  if (threadIdx.x == 0) {
+    if (blockIdx.x < nchunks) issue(blockIdx.x, 0);
+    if (blockIdx.x + gridDim.x < nchunks) issue(blockIdx.x + gridDim.x, 1);
+  }
+  float mu[8], rs[8], ga[8], be[8];
+  BnAffine::ld8(mean + g * 8, mu);
+  BnAffine::ld8(rstd + g * 8, rs);
+  int ncur = -1;
+  if (!af.gain) af.get8(0, g * 8, C, ga, be);
+  int it = 0;
+  for (long long t = blockIdx.x; t < nchunks; t += gridDim.x, ++it) {
+    const int b = it & 1;
+    tc::mbar_wait(&full[b], (it >> 1) & 1);
+    const long long p0 = t * cpix;
+    const int np = (int)min((long long)cpix, P_total - p0);
+    const TI* xs = reinterpret_cast<const TI*>(buf[b]);
+    if (lane < lanes) {
+      for (int q = lane; q < np; q += lanes) {
+        const long long p = p0 + q;
+        float v[8];
+        Vec8<TI>::load(xs + q * C + g * 8, v);
+        if (af.gain) {
+          const int n = (int)((unsigned)p / (unsigned)HW);   // pixel counts < 2^31
+          if (n != ncur) {
+            af.get8(n, g * 8, C, ga, be);
+            ncur = n;
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float tt = (v[j] - mu[j]) * rs[j] * ga[j] + be[j];
+          v[j] = tt > 0.0f ? tt : 0.0f;
+        }
+        Vec8<TO>::store(y + p * C + g * 8, v);
+      }
+    }
+    __syncthreads();   // every thread is done with buf[b]
+    if (threadIdx.x == 0 && t + 2LL * gridDim.x < nchunks) issue(t + 2LL * gridDim.x, b);
   }
 }
 
@@ -1882,6 +1958,18 @@ cudaError_t bn_apply_relu(const TI* x, int N, int H, int W, int C, const float* 
                           cudaStream_t st) {
   const long long total = (long long)N * H * W * (C / 8);
   const int G = C / 8;
+  static const int bulk_on = getenv("PARAGAN_BN_BULK") ? atoi(getenv("PARAGAN_BN_BULK")) : 1;
+  if (bulk_on && !up2 && C % 8 == 0 && G <= 256 && (long long)C * sizeof(TI) <= kBnChunkBytes &&
+      ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) == 0) {
+    const int lanes = 256 / G;
+    const long long P = (long long)N * H * W;
+    const long long cpix = kBnChunkBytes / ((long long)C * sizeof(TI));
+    long long blocks = (P + cpix - 1) / cpix;
+    if (blocks > 4LL * kNumSMs) blocks = 4LL * kNumSMs;
+    k_bn_apply_relu_bulk<TI, TO><<<(unsigned)blocks, lanes * G, 0, st>>>(x, P, H * W, C, mean, rstd,
+                                                                         BnAffine{gain, bias, gamma, beta}, y);
+    return cudaGetLastError();
+  }
   if (!up2 && C % 8 == 0 && G <= 256) {
     const int lanes = 256 / G;
     const long long P = (long long)N * H * W;
