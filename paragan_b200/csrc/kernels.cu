@@ -486,6 +486,92 @@ __global__ void __launch_bounds__(256) k_bn_bwd_reduce(const TI* __restrict__ x,
     partial[((long long)n * chunks + blockIdx.x) * 2 * C + c] = a;
   }
 }
+// bulk-staged streaming (cp.async.bulk into a double-buffered smem ring) for the BN kernels below
+constexpr int kBnChunkBytes = 16384;
+__device__ __forceinline__ int bn_chunk_pix(int C, int esize) { return kBnChunkBytes / (C * esize); }
+
+// bulk-staged version (no up2): this block's pixel range of image n streams through a double-
+// buffered 2 x 16 KB ring (x and dy side by side), the per-thread sums are the register kernel's
+template <typename TI, typename TG>
+__global__ void __launch_bounds__(256) k_bn_bwd_reduce_bulk(const TI* __restrict__ x, const TG* __restrict__ dy,
+                                                            int N, int H, int W, int C, int cpix,
+                                                            const float* __restrict__ mean,
+                                                            const float* __restrict__ rstd, BnAffine af,
+                                                            float* __restrict__ partial, int chunks) {
+  extern __shared__ float shf[];  // [R][2C]
+  __shared__ __align__(128) uint8_t buf[2][kBnChunkBytes];
+  __shared__ __align__(8) uint64_t full[2];
+  const int G = C >> 3;
+  const int R = 256 / G;
+  const int tid = threadIdx.x;
+  const int g = tid % G, r = tid / G;
+  const int n = blockIdx.y;
+  const long long HW = (long long)H * W;
+  const long long per = (HW + chunks - 1) / chunks;
+  const long long q0 = blockIdx.x * per, q1 = min(HW, q0 + per);
+  const int nsub = q1 > q0 ? (int)((q1 - q0 + cpix - 1) / cpix) : 0;
+  const uint32_t off_dy = (uint32_t)cpix * C * sizeof(TI);
+  if (tid == 0) {
+    tc::mbar_init(&full[0], 1);
+    tc::mbar_init(&full[1], 1);
+    tc::fence_barrier_init();
+  }
+  __syncthreads();
+  auto issue = [&](int sub, int b) {
+    const long long p0 = (long long)n * HW + q0 + (long long)sub * cpix;
+    const uint32_t np = (uint32_t)min((long long)cpix, q1 - q0 - (long long)sub * cpix);
+    const uint32_t bx = np * C * sizeof(TI), bd = np * C * sizeof(TG);
+    tc::mbar_expect_tx(&full[b], bx + bd);
+    tc::bulk_load_1d(buf[b], x + p0 * C, bx, &full[b]);
+    tc::bulk_load_1d(buf[b] + off_dy, dy + p0 * C, bd, &full[b]);
+  };
+  if (tid == 0) {
+    if (nsub > 0) issue(0, 0);
+    if (nsub > 1) issue(1, 1);
+  }
+  float sa[8] = {}, sb[8] = {};
+  float ga[8], be[8], mu[8], rs[8];
+  af.get8(n, g * 8, C, ga, be);
+  BnAffine::ld8(mean + g * 8, mu);
+  BnAffine::ld8(rstd + g * 8, rs);
+  for (int sub = 0; sub < nsub; ++sub) {
+    const int b = sub & 1;
+    tc::mbar_wait(&full[b], (sub >> 1) & 1);
+    const int np = (int)min((long long)cpix, q1 - q0 - (long long)sub * cpix);
+    const TI* xs = reinterpret_cast<const TI*>(buf[b]);
+    const TG* ds = reinterpret_cast<const TG*>(buf[b] + off_dy);
+    if (r < R) {
+      for (int q = r; q < np; q += R) {
+        float v[8], d[8];
+        Vec8<TI>::load(xs + q * C + g * 8, v);
+        Vec8<TG>::load(ds + q * C + g * 8, d);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float xh = (v[j] - mu[j]) * rs[j];
+          const float z = xh * ga[j] + be[j];
+          const float g0 = z > 0.0f ? d[j] : 0.0f;
+          sa[j] += g0;
+          sb[j] = fmaf(g0, xh, sb[j]);
+        }
+      }
+    }
+    __syncthreads();
+    if (tid == 0 && sub + 2 < nsub) issue(sub + 2, b);
+  }
+  if (r < R) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      shf[r * 2 * C + g * 8 + j] = sa[j];
+      shf[r * 2 * C + C + g * 8 + j] = sb[j];
+    }
+  }
+  __syncthreads();
+  for (int c = tid; c < 2 * C; c += 256) {
+    float a = 0.0f;
+    for (int rr = 0; rr < R; ++rr) a += shf[rr * 2 * C + c];
+    partial[((long long)n * chunks + blockIdx.x) * 2 * C + c] = a;
+  }
+}
 __global__ void k_bn_bwd_fold(const float* __restrict__ partial, int N, int chunks, int C, float* __restrict__ AB) {
   const long long total = (long long)N * 2 * C;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
@@ -672,8 +758,6 @@ __global__ void __launch_bounds__(256) k_bn_bwd_apply_cs(const TI* __restrict__ 
 // shared memory with their channel group's constants in registers and store with 16-byte
 // stores.  (The register-staged kernels held 2 x 16 B per thread in flight at 68-90 registers,
 // ~24 KB per SM: 4.1-4.5 TB/s.)
-constexpr int kBnChunkBytes = 16384;
-__device__ __forceinline__ int bn_chunk_pix(int C, int esize) { return kBnChunkBytes / (C * esize); }
 
 template <typename TI, typename TO>
 __global__ void __launch_bounds__(256) k_bn_apply_relu_bulk(const TI* __restrict__ x, long long P_total, int HW, int C,
@@ -735,6 +819,86 @@ __global__ void __launch_bounds__(256) k_bn_apply_relu_bulk(const TI* __restrict
         }
         Vec8<TO>::store(y + p * C + g * 8, v);
       }
+    }
+    __syncthreads();   // every thread is done with buf[b]
+    if (threadIdx.x == 0 && t + 2LL * gridDim.x < nchunks) issue(t + 2LL * gridDim.x, b);
+  }
+}
+
+// backward apply, bulk-staged: x, dy (and the optional residual gradient `add`) of a chunk of
+// pixels land side by side in one 16 KB stage of the ring
+template <typename TI, typename TG, typename TO>
+__global__ void __launch_bounds__(256) k_bn_bwd_apply_bulk(const TI* __restrict__ x, const TG* __restrict__ dy,
+                                                           long long P_total, int HW, int C, int cpix,
+                                                           const float* __restrict__ mean,
+                                                           const float* __restrict__ rstd, BnAffine af,
+                                                           const float* __restrict__ mgrad, const TO* __restrict__ add,
+                                                           TO* __restrict__ dx) {
+  __shared__ __align__(128) uint8_t buf[2][kBnChunkBytes];
+  __shared__ __align__(8) uint64_t full[2];
+  const int G = C >> 3;
+  const int lanes = blockDim.x / G;
+  const int g = threadIdx.x % G, lane = threadIdx.x / G;
+  const long long nchunks = (P_total + cpix - 1) / cpix;
+  const uint32_t off_dy = (uint32_t)cpix * C * sizeof(TI);
+  const uint32_t off_add = off_dy + (uint32_t)cpix * C * sizeof(TG);
+  if (threadIdx.x == 0) {
+    tc::mbar_init(&full[0], 1);
+    tc::mbar_init(&full[1], 1);
+    tc::fence_barrier_init();
+  }
+  __syncthreads();
+  auto issue = [&](long long t, int b) {
+    const long long p0 = t * cpix;
+    const uint32_t np = (uint32_t)min((long long)cpix, P_total - p0);
+    const uint32_t bx = np * C * sizeof(TI), bd = np * C * sizeof(TG), ba = add ? np * C * sizeof(TO) : 0u;
+    tc::mbar_expect_tx(&full[b], bx + bd + ba);
+    tc::bulk_load_1d(buf[b], x + p0 * C, bx, &full[b]);
+    tc::bulk_load_1d(buf[b] + off_dy, dy + p0 * C, bd, &full[b]);
+    if (add) tc::bulk_load_1d(buf[b] + off_add, add + p0 * C, ba, &full[b]);
+  };
+  if (threadIdx.x == 0) {
+    if (blockIdx.x < nchunks) issue(blockIdx.x, 0);
+    if (blockIdx.x + gridDim.x < nchunks) issue(blockIdx.x + gridDim.x, 1);
+  }
+  float mu[8], rs[8], ga[8], be[8], mg[8], mgx[8];
+  BnAffine::ld8(mean + g * 8, mu);
+  BnAffine::ld8(rstd + g * 8, rs);
+  BnAffine::ld8(mgrad + g * 8, mg);
+  BnAffine::ld8(mgrad + C + g * 8, mgx);
+  int ncur = -1;
+  if (!af.gain) af.get8(0, g * 8, C, ga, be);
+  int it = 0;
+  for (long long t = blockIdx.x; t < nchunks; t += gridDim.x, ++it) {
+    const int b = it & 1;
+    tc::mbar_wait(&full[b], (it >> 1) & 1);
+    const long long p0 = t * cpix;
+    const int np = (int)min((long long)cpix, P_total - p0);
+    const TI* xs = reinterpret_cast<const TI*>(buf[b]);
+    const TG* ds = reinterpret_cast<const TG*>(buf[b] + off_dy);
+    const TO* as = reinterpret_cast<const TO*>(buf[b] + off_add);
+    for (int q = lane; q < np; q += lanes) {
+      const long long p = p0 + q;
+      float v[8], d[8], ad[8], o[8];
+      Vec8<TI>::load(xs + q * C + g * 8, v);
+      Vec8<TG>::load(ds + q * C + g * 8, d);
+      if (add) Vec8<TO>::load(as + q * C + g * 8, ad);
+      if (af.gain) {
+        const int n = (int)((unsigned)p / (unsigned)HW);   // pixel counts < 2^31
+        if (n != ncur) {
+          af.get8(n, g * 8, C, ga, be);
+          ncur = n;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float xh = (v[j] - mu[j]) * rs[j];
+        const float z = xh * ga[j] + be[j];
+        const float g0 = z > 0.0f ? d[j] : 0.0f;
+        o[j] = rs[j] * (ga[j] * g0 - mg[j] - xh * mgx[j]);
+        if (add) o[j] += ad[j];
+      }
+      Vec8<TO>::store(dx + p * C + g * 8, o);
     }
     __syncthreads();   // every thread is done with buf[b]
     if (threadIdx.x == 0 && t + 2LL * gridDim.x < nchunks) issue(t + 2LL * gridDim.x, b);
@@ -2003,8 +2167,18 @@ cudaError_t bn_bwd_reduce(const TI* x, const TG* dy, int N, int H, int W, int C,
   if (sm > 48 * 1024)
     PG_CUDA(cudaFuncSetAttribute(k_bn_bwd_reduce<TI, TG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   dim3 g(chunks, N);
-  k_bn_bwd_reduce<TI, TG><<<g, 256, sm, st>>>(x, dy, N, H, W, C, mean, rstd, BnAffine{gain, bias, gamma, beta},
-                                              up2 ? 1 : 0, partial, chunks);
+  static const int bulk_on = getenv("PARAGAN_BN_BULK") ? atoi(getenv("PARAGAN_BN_BULK")) : 1;
+  const long long per_pix = (long long)C * (sizeof(TI) + sizeof(TG));
+  if (bulk_on && !up2 && per_pix <= kBnChunkBytes && sm <= 32 * 1024 &&
+      ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(dy)) & 15) == 0) {
+    // (each thread's pixel order restarts per 16 KB sub-chunk: a different, still fixed, summation order)
+    PG_CUDA(cudaFuncSetAttribute(k_bn_bwd_reduce_bulk<TI, TG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    k_bn_bwd_reduce_bulk<TI, TG><<<g, 256, sm, st>>>(x, dy, N, H, W, C, (int)(kBnChunkBytes / per_pix), mean, rstd,
+                                                     BnAffine{gain, bias, gamma, beta}, partial, chunks);
+  } else {
+    k_bn_bwd_reduce<TI, TG><<<g, 256, sm, st>>>(x, dy, N, H, W, C, mean, rstd, BnAffine{gain, bias, gamma, beta},
+                                                up2 ? 1 : 0, partial, chunks);
+  }
   PG_LAUNCH_CHECK();
   k_bn_bwd_fold<<<grid_for((long long)N * 2 * C, 256), 256, 0, st>>>(partial, N, chunks, C, AB);
   return cudaGetLastError();
@@ -2035,6 +2209,20 @@ cudaError_t bn_bwd_apply(const TI* x, const TG* dy, int N, int H, int W, int C, 
   PG_LAUNCH_CHECK();
   const long long total = (long long)N * H * W * (C / 8);
   const int G = C / 8;
+  static const int bulk_on = getenv("PARAGAN_BN_BULK") ? atoi(getenv("PARAGAN_BN_BULK")) : 1;
+  const long long per_pix = (long long)C * (sizeof(TI) + sizeof(TG) + (add ? sizeof(TO) : 0));
+  if (bulk_on && !up2 && C % 8 == 0 && G <= 256 && per_pix <= kBnChunkBytes &&
+      ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(dy) | reinterpret_cast<uintptr_t>(add) |
+        reinterpret_cast<uintptr_t>(dx)) & 15) == 0) {
+    const int lanes = 256 / G;
+    const long long P = (long long)N * H * W;
+    const int cpix = (int)(kBnChunkBytes / per_pix);
+    long long blocks = (P + cpix - 1) / cpix;
+    if (blocks > 4LL * kNumSMs) blocks = 4LL * kNumSMs;
+    k_bn_bwd_apply_bulk<TI, TG, TO><<<(unsigned)blocks, lanes * G, 0, st>>>(
+        x, dy, P, H * W, C, cpix, mean, rstd, BnAffine{gain, bias, gamma, beta}, mgrad, add, dx);
+    return cudaGetLastError();
+  }
   if (!up2 && C % 8 == 0 && G <= 256) {
     const int lanes = 256 / G;
     const long long P = (long long)N * H * W;
