@@ -769,7 +769,9 @@ __global__ void __launch_bounds__(256) k_bn_apply_relu_bulk(const TI* __restrict
   const int G = C >> 3;
   const int lanes = blockDim.x / G;
   const int g = threadIdx.x % G, lane = threadIdx.x / G;
-  const int cpix = bn_chunk_pix(C, (int)sizeof(TI));
+  // whole rounds of the block's pixel lanes per chunk
+  const int cmax = bn_chunk_pix(C, (int)sizeof(TI));
+  const int cpix = cmax >= lanes ? cmax / lanes * lanes : cmax;
   const long long nchunks = (P_total + cpix - 1) / cpix;
   if (threadIdx.x == 0) {
     tc::mbar_init(&full[0], 1);
@@ -2127,7 +2129,8 @@ cudaError_t bn_apply_relu(const TI* x, int N, int H, int W, int C, const float* 
       ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) == 0) {
     const int lanes = 256 / G;
     const long long P = (long long)N * H * W;
-    const long long cpix = kBnChunkBytes / ((long long)C * sizeof(TI));
+    const long long cmax = kBnChunkBytes / ((long long)C * sizeof(TI));
+    const long long cpix = cmax >= lanes ? cmax / lanes * lanes : cmax;
     long long blocks = (P + cpix - 1) / cpix;
     if (blocks > 4LL * kNumSMs) blocks = 4LL * kNumSMs;
     k_bn_apply_relu_bulk<TI, TO><<<(unsigned)blocks, lanes * G, 0, st>>>(x, P, H * W, C, mean, rstd,
@@ -2173,7 +2176,9 @@ cudaError_t bn_bwd_reduce(const TI* x, const TG* dy, int N, int H, int W, int C,
       ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(dy)) & 15) == 0) {
     // (each thread's pixel order restarts per 16 KB sub-chunk: a different, still fixed, summation order)
     PG_CUDA(cudaFuncSetAttribute(k_bn_bwd_reduce_bulk<TI, TG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    k_bn_bwd_reduce_bulk<TI, TG><<<g, 256, sm, st>>>(x, dy, N, H, W, C, (int)(kBnChunkBytes / per_pix), mean, rstd,
+    const int cmax = (int)(kBnChunkBytes / per_pix);
+    const int cpix = cmax >= R ? cmax / R * R : cmax;   // whole rounds of the R pixel lanes
+    k_bn_bwd_reduce_bulk<TI, TG><<<g, 256, sm, st>>>(x, dy, N, H, W, C, cpix, mean, rstd,
                                                      BnAffine{gain, bias, gamma, beta}, partial, chunks);
   } else {
     k_bn_bwd_reduce<TI, TG><<<g, 256, sm, st>>>(x, dy, N, H, W, C, mean, rstd, BnAffine{gain, bias, gamma, beta},
@@ -2216,7 +2221,8 @@ cudaError_t bn_bwd_apply(const TI* x, const TG* dy, int N, int H, int W, int C, 
         reinterpret_cast<uintptr_t>(dx)) & 15) == 0) {
     const int lanes = 256 / G;
     const long long P = (long long)N * H * W;
-    const int cpix = (int)(kBnChunkBytes / per_pix);
+    const int cmax = (int)(kBnChunkBytes / per_pix);
+    const int cpix = cmax >= lanes ? cmax / lanes * lanes : cmax;   // whole rounds of the pixel lanes
     long long blocks = (P + cpix - 1) / cpix;
     if (blocks > 4LL * kNumSMs) blocks = 4LL * kNumSMs;
     k_bn_bwd_apply_bulk<TI, TG, TO><<<(unsigned)blocks, lanes * G, 0, st>>>(
