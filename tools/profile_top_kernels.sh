@@ -20,7 +20,12 @@ thin_fwd|k_thin_fwd|1
 thin_wgrad|k_thin_wgrad|0
 thin_dgrad|k_thin_dgrad|0
 attn_fwd|k_attn_fwd|1
-attn_bwd|k_attn_bwd|0""".splitlines()
+attn_bwd|k_attn_bwd|0
+wgrad3_96|k_conv_wgrad3<.int.96>|2
+wgrad_cg2_256|k_conv_wgrad_cg2<.int.256>|2
+bn_apply_bulk|k_bn_apply_relu_bulk|4
+bn_bwd_apply_bulk|k_bn_bwd_apply_bulk|2
+bn_bwd_reduce_bulk|k_bn_bwd_reduce_bulk|2""".splitlines()
 want = sys.argv[1].split()
 for s in specs:
     if not want or s.split("|")[0] in want:
