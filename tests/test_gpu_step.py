@@ -260,3 +260,19 @@ def test_init_params_replicas_identical_and_finite():
     assert abs(pa[:n].std() - 0.02) < 0.005
     a.close()
     b.close()
+
+
+def test_step_bitwise_reproducible_bf16():
+    """Every reduction of the step has a fixed order (split-K partials, BN and SN sums, attention dtheta
+    partials, CBN dcond slices, the D-head embedding gradient): two runs of the same iteration from the
+    same state give bit-identical gradients, weights and fakes.  ch = 32 at 128x128 keeps the layers on
+    the tcgen05 / fused-attention / bulk-copy BN paths (every channel count a multiple of 32)."""
+    ocfg = P.oracle_config(128, 32, 64, 1000, 128, 20, bf16=True)
+    cfg = api.make_config(resolution=128, ch=32, attn_res=64, n_classes=1000, shared_dim=128, z_chunk=20,
+                          local_batch=8, compute=api.BF16)
+    gs, ds, g0, d0, dbs, gb = P.make_inputs(ocfg, 8, seed=31)
+    runs = [P.run_gpu(cfg, g0, d0, dbs, gb) for _ in range(2)]
+    for key in ("d_grads", "g_grads", "d_state", "g_state", "fake"):
+        a, b = (np.asarray(r[key]) for r in runs)
+        assert a.shape == b.shape and np.array_equal(a, b), key
+    assert runs[0]["d_loss"] == runs[1]["d_loss"] and runs[0]["g_loss"] == runs[1]["g_loss"]
