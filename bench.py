@@ -168,7 +168,7 @@ def main():
 
     import numpy as np
     import torch
-    from paragan_b200 import api, inputs
+    from paper_2411_03999_b200 import api, inputs
 
     world, rank, local = _dist()
     torch.cuda.set_device(local)

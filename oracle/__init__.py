@@ -2,10 +2,10 @@
 
 TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and the
 ``cpu_baseline`` / ``--impl reference`` legs of ``bench.py`` may import or run
-anything in this package.  The product path (``paragan_b200`` + ``libparagan.so``)
+anything in this package.  The product path (``paper_2411_03999_b200`` + ``libparagan.so``)
 never imports it, and the oracle never imports the product: the two share no
 code, tables or constants.  Only the seeded input generators
-(``paragan_b200/inputs.py``, which hold none of the method's arithmetic) feed
+(``paper_2411_03999_b200/inputs.py``, which hold none of the method's arithmetic) feed
 both sides.
 
 Everything here is plain PyTorch CPU arithmetic in float64 (autograd supplies

@@ -1,6 +1,6 @@
 """Builds libparagan.so in-tree with nvcc for sm_100a (no JIT cache, no pip install).
 
-    python -m paragan_b200.build [--force]
+    python -m paper_2411_03999_b200.build [--force]
 """
 from __future__ import annotations
 

@@ -13,7 +13,7 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paragan_b200 import api
+    from paper_2411_03999_b200 import api
     from tests import parity as P
 
     rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])

@@ -6,7 +6,7 @@ from __future__ import annotations
 import numpy as np
 
 from oracle import biggan as bg
-from paragan_b200 import inputs
+from paper_2411_03999_b200 import inputs
 
 
 def oracle_config(res, ch, attn, n_classes, shared_dim, z_chunk, n_d=1, bf16=False):
@@ -48,7 +48,7 @@ def run_oracle(ocfg, gs, ds, g0, d0, dbs, gb):
 def run_gpu(cfg, g0, d0, dbs, gb, rank=0, world=1, nccl_id=None, ctx=None):
     """One iteration through the C-ABI on this rank's shard of the global batch."""
     import torch
-    from paragan_b200 import api
+    from paper_2411_03999_b200 import api
     dev = f"cuda:{cfg.device}"
     own = ctx is None
     if own:

@@ -7,7 +7,7 @@ import re
 import pytest
 
 from oracle import biggan as bg
-from paragan_b200 import api
+from paper_2411_03999_b200 import api
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 

@@ -29,7 +29,7 @@ def _worker(rank, port, q):
     try:
         from oracle import biggan as bg
         from oracle import ops
-        from paragan_b200 import api, inputs
+        from paper_2411_03999_b200 import api, inputs
         from tests import parity as P
         res = {}
         # 1. NCCL unique-id bootstrap exactly as bench.py does it

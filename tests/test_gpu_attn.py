@@ -11,7 +11,7 @@ exp(S - m) and dS stored bf16):
 import pytest
 import torch
 
-from paragan_b200 import api
+from paper_2411_03999_b200 import api
 
 pytestmark = pytest.mark.gpu
 DEV = "cuda:0"

@@ -6,7 +6,7 @@ import pytest
 import torch
 
 from oracle import ops
-from paragan_b200 import api
+from paper_2411_03999_b200 import api
 
 pytestmark = pytest.mark.gpu
 DEV = "cuda:0"

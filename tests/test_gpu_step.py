@@ -7,7 +7,7 @@ import pytest
 import torch
 
 from oracle import biggan as bg
-from paragan_b200 import api
+from paper_2411_03999_b200 import api
 from tests import parity as P
 
 pytestmark = pytest.mark.gpu

@@ -11,7 +11,7 @@ import torch
 
 from oracle import biggan as bg
 from oracle import ops
-from paragan_b200 import inputs
+from paper_2411_03999_b200 import inputs
 
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 MICRO = dict(resolution=16, ch=2, n_classes=5, shared_dim=4, z_chunk=3, attn_res=8)

@@ -8,7 +8,7 @@ import sys
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paragan_b200 import api  # noqa: E402
+from paper_2411_03999_b200 import api  # noqa: E402
 
 SHAPES = [  # n, h, w, cin, cout, k
     (512, 128, 128, 32, 96, 1),

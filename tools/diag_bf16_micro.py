@@ -1,7 +1,7 @@
 import sys, os
 sys.path.insert(0, os.getcwd())
 import numpy as np
-from paragan_b200 import api
+from paper_2411_03999_b200 import api
 from tests import parity as P
 B = 8
 ocfg = P.oracle_config(32, 4, 16, 10, 16, 4, bf16=True)

@@ -5,7 +5,7 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 
-from paragan_b200 import api  # noqa: E402
+from paper_2411_03999_b200 import api  # noqa: E402
 from tests import parity as P  # noqa: E402
 
 ch = int(sys.argv[1]) if len(sys.argv) > 1 else 32

@@ -26,7 +26,7 @@ def main():
     ap.add_argument("--d-only", action="store_true", help="D step alone, oracle fed the GPU's fake images")
     a = ap.parse_args()
     import numpy as np
-    from paragan_b200 import api
+    from paper_2411_03999_b200 import api
     from tests import parity as P
     compute = api.BF16 if a.bf16 else api.F32
     cfg = api.make_config(resolution=a.res, ch=a.ch, attn_res=a.attn, n_classes=a.classes, shared_dim=a.shared,
