@@ -410,7 +410,7 @@ def d_step(cfg: Config, G: NetState, D: NetState, real, real_y, z, fake_y, updat
     return dict(loss=float(loss.detach()), logits=logits.detach().numpy(), fake=fake.detach().numpy(),
                 grads=D.grad_flat(grads), applied=ok,
                 sigma_g=dict(sng.sigma), sigma_d=dict(snd.sigma),
-                d_real_mean=float(l_real.mean()), d_fake_mean=float(l_fake.mean()))
+                d_real_mean=float(l_real.detach().mean()), d_fake_mean=float(l_fake.detach().mean()))
 
 
 def g_step(cfg: Config, G: NetState, D: NetState, z, y, update: bool = True) -> dict:
