@@ -161,6 +161,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
+    ap.add_argument("--compute", default="bf16", choices=["bf16", "f32"],
+                    help="Table 3 precision toggle (P:420-434): bf16 tcgen05 path (default, the bench line) or the "
+                         "fp32 SIMT parity engine (an ablation line, never the headline)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -181,7 +184,10 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
     B, R = args.batch, args.res
-    cfg = api.make_config(resolution=R, local_batch=B, d_steps_per_g=args.d_steps, compute=api.BF16, rank=rank,
+    compute = api.BF16 if args.compute == "bf16" else api.F32
+    if compute == api.F32:
+        args.no_profile = True          # no tcgen05 launches to bracket: roofline is the bf16 path's
+    cfg = api.make_config(resolution=R, local_batch=B, d_steps_per_g=args.d_steps, compute=compute, rank=rank,
                           world_size=world, device=local, seed=1234)
     stream = torch.cuda.Stream(device=dev)
     with torch.cuda.stream(stream):
@@ -200,12 +206,13 @@ def main():
                              host=dict(real=torch.from_numpy(real).pin_memory(), ry=torch.from_numpy(ry).pin_memory(),
                                        z=torch.from_numpy(z).pin_memory(), fy=torch.from_numpy(fy).pin_memory(),
                                        zg=torch.from_numpy(zg).pin_memory(), yg=torch.from_numpy(yg).pin_memory())))
-        packed = torch.empty((B, R, R, cfg.c_pad_image), dtype=torch.bfloat16, device=dev)
+        packed = torch.empty((B, R, R, cfg.c_pad_image),
+                             dtype=torch.bfloat16 if compute == api.BF16 else torch.float32, device=dev)
 
         def step(i, src=None):
             p = src if src is not None else pool[i % 4]
             for _ in range(args.d_steps):
-                api.layout_pack(p["real"], packed, api.BF16, cfg.c_pad_image, stream)
+                api.layout_pack(p["real"], packed, compute, cfg.c_pad_image, stream)
                 ctx.d_step(packed, p["ry"], p["z"], p["fy"])
             ctx.g_step(p["zg"], p["yg"])
 
@@ -308,11 +315,13 @@ def main():
                    "sample": f"one BigGAN-128 D+G iteration on 1 image ({dt:.1f} s, fp64 torch CPU oracle)"}
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+                "scaling": "weak", "vs_baseline": None, "dtype": args.compute, "data": "synthetic",
                 "config": {"workload": f"BigGAN-{R} ch=96 training iteration (n_d={args.d_steps} D steps + 1 G step)",
                            "model": f"BigGAN-{R} ch=96 (158.42M params)" if R == 128 else f"BigGAN-{R} ch=96",
                            "global_batch": world * B, "per_gpu_batch": B, "seq_len": None,
-                           "parallelism": f"dp{world}", "l2": "inputs+activations >> 126 MB L2 (no flush needed)"},
+                           "parallelism": f"dp{world}", "l2": "inputs+activations >> 126 MB L2 (no flush needed)",
+                           **({"ablation": "Table 3 precision toggle: fp32 SIMT engine (P:420-434)"}
+                              if compute == api.F32 else {})},
                 "img_per_s_per_gpu": value / world, "real_img_per_s": value * args.d_steps,
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                 "clocks": clk.summary(), "losses": {"d": st.d_loss, "g": st.g_loss}}
