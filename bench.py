@@ -128,8 +128,10 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": "BigGAN-128 ch=96 1:1 iteration, CPU oracle sample of 1 image",
-                                            "global_batch": 1, "resolution": 128},
+            "data": "synthetic",
+            "config": {"workload": "BigGAN-128 ch=96 training iteration (n_d=1 D steps + 1 G step)",
+                       "model": "BigGAN-128 ch=96 (158.42M params)", "global_batch": 1, "per_gpu_batch": 1,
+                       "seq_len": None, "parallelism": "dp1", "sample": "1 image per step (bounded CPU sample)"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": torch.get_num_threads(), "kind": "oracle",
                              "sample": "one BigGAN-128 D+G iteration on 1 image per step (fp64 torch CPU oracle)"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
