@@ -79,3 +79,24 @@ def test_config_validation():
 def test_workspace_fits_b200_at_paper_config():
     n = api.workspace_size(api.make_config(local_batch=256))
     assert 1e9 < n < 170e9
+
+
+def test_product_path_has_no_fallback():
+    """The product package never reaches the oracle, and a missing library is an error, not a fallback."""
+    import ast
+    import subprocess
+    import sys
+    pkg = os.path.join(ROOT, "paper_2411_03999_b200")
+    for fn in os.listdir(pkg):
+        if fn.endswith(".py"):
+            tree = ast.parse(open(os.path.join(pkg, fn)).read())
+            for node in ast.walk(tree):
+                if isinstance(node, ast.Import):
+                    assert not any(a.name.split(".")[0] == "oracle" for a in node.names), fn
+                if isinstance(node, ast.ImportFrom):
+                    assert (node.module or "").split(".")[0] != "oracle", fn
+    code = ("import os, paper_2411_03999_b200.api as a\n"
+            "try:\n    a.lib()\nexcept OSError as e:\n    print('LOUD', e)\nelse:\n    print('LOADED')\n")
+    env = dict(os.environ, PARAGAN_LIB="/nonexistent/libparagan.so")
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True, timeout=300)
+    assert "LOUD" in r.stdout, r.stdout + r.stderr
