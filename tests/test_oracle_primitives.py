@@ -198,7 +198,7 @@ def test_conv_delta_kernel_shifts_and_adjoint_identity():
     dy = torch.tensor(rng.standard_normal((2, 4, 5, 5)))
     y = ops.conv2d(x, w, None)
     gx, gw = torch.autograd.grad((y * dy).sum(), [x, w])
-    lhs = float((y * dy).sum())
+    lhs = float((y * dy).sum().detach())
     assert abs(lhs - float((x * gx).sum())) < 1e-10 * abs(lhs)
     assert abs(lhs - float((w * gw).sum())) < 1e-10 * abs(lhs)
 
