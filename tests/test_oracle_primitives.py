@@ -199,7 +199,7 @@ def test_conv_delta_kernel_shifts_and_adjoint_identity():
     y = ops.conv2d(x, w, None)
     gx, gw = torch.autograd.grad((y * dy).sum(), [x, w])
     lhs = float((y * dy).sum().detach())
-    assert abs(lhs - float((x * gx).sum())) < 1e-10 * abs(lhs)
+    assert abs(lhs - float((x * gx).sum().detach())) < 1e-10 * abs(lhs)
     assert abs(lhs - float((w * gw).sum())) < 1e-10 * abs(lhs)
 
 
