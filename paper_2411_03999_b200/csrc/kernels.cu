@@ -1615,6 +1615,7 @@ __global__ void k_sn_finish(const SnJob* __restrict__ jobs) {
   const float inv = 1.0f / fmaxf(s_n, 1e-12f);
   for (int r = threadIdx.x; r < j.rows; r += 256) j.u[r] = j.s[r] * inv;
 }
+constexpr int kSnPackItems = 4;
 __global__ void __launch_bounds__(256) k_sn_pack(const SnPack* __restrict__ jobs, const long long* __restrict__ blk_start,
                                                  int n_jobs) {
   // find job by binary search over block starts
@@ -1626,23 +1627,37 @@ __global__ void __launch_bounds__(256) k_sn_pack(const SnPack* __restrict__ jobs
   }
   const SnPack J = jobs[lo];
   const int n = J.rows * J.taps * J.cin;   // < 2^31 for every weight of the model
-  if (J.vec8) {   // 8 consecutive input channels per thread: two float4 loads, one 16-byte bf16 store
-    const int i = ((int)(b - blk_start[lo]) * 256 + threadIdx.x) * 8;
-    if (i >= n) return;
+  if (J.vec8) {   // 8 consecutive input channels per item: two float4 loads, one 16-byte bf16 store;
+                  // kSnPackItems items per thread so the job search above is paid once per 8192 elements
     const float inv = J.sigma[1];
-    const float4 a0 = *reinterpret_cast<const float4*>(J.w + i);
-    const float4 a1 = *reinterpret_cast<const float4*>(J.w + i + 4);
-    const int c = i % J.cin, rt = i / J.cin;
-    const int t = rt % J.taps, o = rt / J.taps;
-    const long long d = ((long long)(o + J.dst_row_offset) * J.taps + t) * J.dst_cin + c;
-    uint4 u;
-    __nv_bfloat162 h0 = __floats2bfloat162_rn(a0.x * inv, a0.y * inv), h1 = __floats2bfloat162_rn(a0.z * inv, a0.w * inv);
-    __nv_bfloat162 h2 = __floats2bfloat162_rn(a1.x * inv, a1.y * inv), h3 = __floats2bfloat162_rn(a1.z * inv, a1.w * inv);
-    u.x = *reinterpret_cast<uint32_t*>(&h0);
-    u.y = *reinterpret_cast<uint32_t*>(&h1);
-    u.z = *reinterpret_cast<uint32_t*>(&h2);
-    u.w = *reinterpret_cast<uint32_t*>(&h3);
-    *reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(J.dst) + d) = u;
+    const int base = (int)(b - blk_start[lo]) * (kSnPackItems * 256) + threadIdx.x;
+    float4 a0[kSnPackItems], a1[kSnPackItems];
+#pragma unroll
+    for (int u = 0; u < kSnPackItems; ++u) {
+      const int i = (base + u * 256) * 8;
+      if (i < n) {
+        a0[u] = *reinterpret_cast<const float4*>(J.w + i);
+        a1[u] = *reinterpret_cast<const float4*>(J.w + i + 4);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kSnPackItems; ++u) {
+      const int i = (base + u * 256) * 8;
+      if (i >= n) break;
+      const int c = i % J.cin, rt = i / J.cin;
+      const int t = rt % J.taps, o = rt / J.taps;
+      const long long d = ((long long)(o + J.dst_row_offset) * J.taps + t) * J.dst_cin + c;
+      uint4 q;
+      __nv_bfloat162 h0 = __floats2bfloat162_rn(a0[u].x * inv, a0[u].y * inv);
+      __nv_bfloat162 h1 = __floats2bfloat162_rn(a0[u].z * inv, a0[u].w * inv);
+      __nv_bfloat162 h2 = __floats2bfloat162_rn(a1[u].x * inv, a1[u].y * inv);
+      __nv_bfloat162 h3 = __floats2bfloat162_rn(a1[u].z * inv, a1[u].w * inv);
+      q.x = *reinterpret_cast<uint32_t*>(&h0);
+      q.y = *reinterpret_cast<uint32_t*>(&h1);
+      q.z = *reinterpret_cast<uint32_t*>(&h2);
+      q.w = *reinterpret_cast<uint32_t*>(&h3);
+      *reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(J.dst) + d) = q;
+    }
     return;
   }
   const int i = (int)(b - blk_start[lo]) * 256 + threadIdx.x;
@@ -2495,7 +2510,7 @@ long long sn_pack_prepare(SnPack& j) {
   const long long n = (long long)j.rows * j.taps * j.cin;
   j.vec8 = j.mode == 0 && j.dst_bf16 && j.cin % 8 == 0 && j.dst_cin % 8 == 0 &&
            ((reinterpret_cast<uintptr_t>(j.w) | reinterpret_cast<uintptr_t>(j.dst)) & 15) == 0;
-  return ceil_div(n, j.vec8 ? 2048 : 256);
+  return ceil_div(n, j.vec8 ? 2048 * kSnPackItems : 256);
 }
 cudaError_t sn_pack(const SnPack* jobs, const long long* blk_start, int n_jobs, long long total_blocks,
                     cudaStream_t st) {
