@@ -10,10 +10,13 @@ one G step — on BigGAN-128 (ch=96, 158.42M parameters) at 256 images per GPU,
 bf16 storage with fp32 last layers, synthetic ImageNet-shaped data and
 seeded random-init weights.  Weak scaling: per-GPU batch fixed as N grows.
 
-Inputs: a pool of 4 real batches (fp32 NCHW, resident in HBM) and 4 latent
-batches, cycled; every step's activations (~70 GB) exceed the 126 MB L2, so no
-explicit flush is needed.  Timing: W untimed iterations, barrier + device sync,
-CUDA events on the compute stream around exactly K iterations, max over ranks.
+Inputs: a pool of 4 real batches per D step (fp32 NCHW, resident in HBM; drawn
+from the run's random-init generator G0 plus pixel noise, so D is not saturated)
+and 4 latent batches, cycled; every step's activations (~70 GB) exceed the
+126 MB L2, so no explicit flush is needed.  Timing: W untimed iterations, then
+`--repeats` (default 3) timed runs of exactly K iterations, each bracketed by a
+barrier + device sync with CUDA events on the compute stream, max over ranks;
+the median repeat is reported.
 
 `--impl reference` runs the CPU oracle (oracle/, the only reference this
 paper-only task has) on the same metric: each step is a bounded sample of the
@@ -160,6 +163,7 @@ def main():
     ap.add_argument("--batch", type=int, default=256, help="images per GPU")
     ap.add_argument("--res", type=int, default=128)
     ap.add_argument("--d-steps", type=int, default=1)
+    ap.add_argument("--repeats", type=int, default=3, help="timed repeats of K steps; the median is reported")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
@@ -192,31 +196,56 @@ def main():
     cfg = api.make_config(resolution=R, local_batch=B, d_steps_per_g=args.d_steps, compute=compute, rank=rank,
                           world_size=world, device=local, seed=1234)
     stream = torch.cuda.Stream(device=dev)
+    nd = args.d_steps
     with torch.cuda.stream(stream):
         ctx = api.Context(cfg, nccl_id, stream=stream)
         ctx.init_params(attn_gamma=0.1)
         dz = api.dim_z(cfg)
-        # input pool: 4 batches per rank, resident in HBM (this rank's shard of the global batch)
+        tdt = torch.bfloat16 if compute == api.BF16 else torch.float32
+        packed = torch.empty((B, R, R, cfg.c_pad_image), dtype=tdt, device=dev)
+        # ---- input pool: 4 (real, labels, z) batches per D step and 4 (z, labels) per G step, resident in
+        # HBM (this rank's shard).  "Real" images are drawn from the random-init generator G0 the run
+        # starts from (independent latents) plus N(0, 0.05^2) pixel noise, clipped to [-1, 1]: D cannot
+        # separate them from the fakes trivially, so the hinge stays out of saturation and the timed D
+        # backward multiplies real (non-zero) gradients — unlike uniform-noise reals, which D separates
+        # within a few steps (d_loss = 0, dlogits = 0).
+        lat = [[inputs.latent_batch(1000 + i, inputs.ROLE_Z_D, rank * nd + k, B, dz, 1000) for k in range(nd)]
+               for i in range(4)]
+        glat = [inputs.latent_batch(1000 + i, inputs.ROLE_Z_G, rank, B, dz, 1000) for i in range(4)]
+        state = {net: ctx.get_params(net) for net in (api.NET_D, api.NET_G)}
+        noise_rng = np.random.default_rng(77 + rank)
         pool = []
         for i in range(4):
-            real, ry = inputs.real_batch(1000 + i, rank, B, R, 1000)
-            z, fy = inputs.latent_batch(1000 + i, inputs.ROLE_Z_D, rank, B, dz, 1000)
-            zg, yg = inputs.latent_batch(1000 + i, inputs.ROLE_Z_G, rank, B, dz, 1000)
-            pool.append(dict(real=torch.from_numpy(real).to(dev), ry=torch.from_numpy(ry).to(dev),
-                             z=torch.from_numpy(z).to(dev), fy=torch.from_numpy(fy).to(dev),
-                             zg=torch.from_numpy(zg).to(dev), yg=torch.from_numpy(yg).to(dev),
-                             host=dict(real=torch.from_numpy(real).pin_memory(), ry=torch.from_numpy(ry).pin_memory(),
-                                       z=torch.from_numpy(z).pin_memory(), fy=torch.from_numpy(fy).pin_memory(),
-                                       zg=torch.from_numpy(zg).pin_memory(), yg=torch.from_numpy(yg).pin_memory())))
-        packed = torch.empty((B, R, R, cfg.c_pad_image),
-                             dtype=torch.bfloat16 if compute == api.BF16 else torch.float32, device=dev)
+            reals = []
+            for k in range(nd):
+                zr, yr = inputs.latent_batch(5000 + i, inputs.ROLE_REAL, rank * nd + k, B, dz, 1000)
+                seed_img = torch.zeros((B, R, R, cfg.c_pad_image), dtype=tdt, device=dev)
+                ctx.d_step(seed_img, torch.from_numpy(yr).to(dev), torch.from_numpy(zr).to(dev),
+                           torch.from_numpy(yr).to(dev), flags=api.FLAG_NO_ALLREDUCE | api.FLAG_NO_UPDATE)
+                img = ctx.get_fakes() + noise_rng.normal(0.0, 0.05, size=(B, 3, R, R)).astype(np.float32)
+                reals.append((np.clip(img, -1.0, 1.0).astype(np.float32), yr))
+            ent = dict(d=[], g=None, host=dict(d=[], g=None))
+            for k in range(nd):
+                real, ry = reals[k]
+                z, fy = lat[i][k]
+                hb = dict(real=torch.from_numpy(real).pin_memory(), ry=torch.from_numpy(ry).pin_memory(),
+                          z=torch.from_numpy(z).pin_memory(), fy=torch.from_numpy(fy).pin_memory())
+                ent["host"]["d"].append(hb)
+                ent["d"].append({kk: v.to(dev) for kk, v in hb.items()})
+            zg, yg = glat[i]
+            hg = dict(zg=torch.from_numpy(zg).pin_memory(), yg=torch.from_numpy(yg).pin_memory())
+            ent["host"]["g"] = hg
+            ent["g"] = {kk: v.to(dev) for kk, v in hg.items()}
+            pool.append(ent)
+        for net, flat in state.items():      # back to the initial state (u vectors and Adam state too)
+            ctx.set_params(net, flat)
 
         def step(i, src=None):
             p = src if src is not None else pool[i % 4]
-            for _ in range(args.d_steps):
-                api.layout_pack(p["real"], packed, compute, cfg.c_pad_image, stream)
-                ctx.d_step(packed, p["ry"], p["z"], p["fy"])
-            ctx.g_step(p["zg"], p["yg"])
+            for d in p["d"]:
+                api.layout_pack(d["real"], packed, compute, cfg.c_pad_image, stream)
+                ctx.d_step(packed, d["ry"], d["z"], d["fy"])
+            ctx.g_step(p["g"]["zg"], p["g"]["yg"])
 
         def barrier():
             torch.cuda.synchronize(dev)
@@ -224,53 +253,66 @@ def main():
                 torch.distributed.barrier()
             torch.cuda.synchronize(dev)
 
+        def max_over_ranks(x):
+            t = torch.tensor([x], device=dev)
+            if world > 1:
+                torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            return float(t.item())
+
         for i in range(args.warmup):
             step(i)
         st = ctx.sync_stats(raise_nonfinite=False)
         barrier()
-        # ---------------- timed region (device-resident inputs)
-        l0 = ctx.kernel_launches()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        # ---------------- timed region (device-resident inputs): `repeats` x exactly K iterations, each
+        # bracketed by barrier + device sync, CUDA events on the compute stream, max over ranks; the
+        # reported value is the median repeat
+        rep_ms, launches = [], 0
         with ClockSampler(local) as clk:
-            e0.record(stream)
-            for i in range(args.steps):
-                step(i)
-            e1.record(stream)
-            barrier()
-        ms = e0.elapsed_time(e1)
-        launches = ctx.kernel_launches() - l0
+            for r in range(args.repeats):
+                l0 = ctx.kernel_launches()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for i in range(args.steps):
+                    step(i)
+                e1.record(stream)
+                barrier()
+                rep_ms.append(max_over_ranks(e0.elapsed_time(e1)))
+                launches = ctx.kernel_launches() - l0
         st = ctx.sync_stats(raise_nonfinite=False)
-        t = torch.tensor([ms], device=dev)
-        if world > 1:
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms_max = float(t.item())
+        ms_max = statistics.median(rep_ms)
         value = world * B * args.steps / (ms_max / 1000.0)
 
-        # ---------------- end-to-end through the public API with host buffers
+        # ---------------- end-to-end through the public API with host buffers: every step copies its
+        # inputs from pinned host memory and reads its losses back (paragan_sync_stats)
         e2e = None
+        d_losses, g_losses = [], []
         if not args.no_e2e:
-            dev_bufs = {k: torch.empty_like(v, device=dev) for k, v in pool[0]["host"].items()}
-            h2d = sum(v.numel() * v.element_size() for v in pool[0]["host"].values())
-            h2d = h2d + (args.d_steps - 1) * (pool[0]["host"]["real"].numel() * 4)
+            dev_d = [{k: torch.empty_like(v, device=dev) for k, v in pool[0]["host"]["d"][0].items()} for _ in range(nd)]
+            dev_g = {k: torch.empty_like(v, device=dev) for k, v in pool[0]["host"]["g"].items()}
+            h2d = sum(v.numel() * v.element_size() for hb in pool[0]["host"]["d"] for v in hb.values()) + \
+                sum(v.numel() * v.element_size() for v in pool[0]["host"]["g"].values())
             stats_bytes = 4 * 4 + 4 + 16
             barrier()
             f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             f0.record(stream)
             n_e2e = args.steps
             for i in range(n_e2e):
-                hb = pool[i % 4]["host"]
-                for k, v in hb.items():
-                    dev_bufs[k].copy_(v, non_blocking=True)
-                step(i, src=dict(real=dev_bufs["real"], ry=dev_bufs["ry"], z=dev_bufs["z"], fy=dev_bufs["fy"],
-                                 zg=dev_bufs["zg"], yg=dev_bufs["yg"]))
-                ctx.sync_stats(raise_nonfinite=False)      # device -> host read of the step's losses
+                hp = pool[i % 4]["host"]
+                for k in range(nd):
+                    for kk, v in hp["d"][k].items():
+                        dev_d[k][kk].copy_(v, non_blocking=True)
+                for kk, v in hp["g"].items():
+                    dev_g[kk].copy_(v, non_blocking=True)
+                step(i, src=dict(d=dev_d, g=dev_g))
+                s2 = ctx.sync_stats(raise_nonfinite=False)      # device -> host read of the step's losses
+                d_losses.append(round(float(s2.d_loss), 5))
+                g_losses.append(round(float(s2.g_loss), 5))
             f1.record(stream)
             barrier()
-            ms2 = torch.tensor([f0.elapsed_time(f1)], device=dev)
-            if world > 1:
-                torch.distributed.all_reduce(ms2, op=torch.distributed.ReduceOp.MAX)
-            e2e = {"value": world * B * n_e2e / (float(ms2.item()) / 1000.0), "unit": UNIT,
+            ms2 = max_over_ranks(f0.elapsed_time(f1))
+            e2e = {"value": world * B * n_e2e / (ms2 / 1000.0), "unit": UNIT,
                    "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(stats_bytes), "steps": n_e2e}
+        d_grad_norm = float(np.linalg.norm(ctx.get_grads(api.NET_D).astype(np.float64)))
 
         # ---------------- roofline pass: the same steps again with every tcgen05 conv launch bracketed
         # by CUDA events (kept out of the timed region above: the events cost ~2% of the step)
@@ -319,6 +361,7 @@ def main():
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": args.compute, "data": "synthetic",
                 "config": {"workload": f"BigGAN-{R} ch=96 training iteration (n_d={args.d_steps} D steps + 1 G step)",
+                           "repeats": args.repeats,
                            "model": f"BigGAN-{R} ch=96 (158.42M params)" if R == 128 else f"BigGAN-{R} ch=96",
                            "global_batch": world * B, "per_gpu_batch": B, "seq_len": None,
                            "parallelism": f"dp{world}", "l2": "inputs+activations >> 126 MB L2 (no flush needed)",
@@ -326,7 +369,11 @@ def main():
                               if compute == api.F32 else {})},
                 "img_per_s_per_gpu": value / world, "real_img_per_s": value * args.d_steps,
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-                "clocks": clk.summary(), "losses": {"d": st.d_loss, "g": st.g_loss}}
+                "clocks": clk.summary(),
+                "repeats_ms_per_step": [round(m / args.steps, 3) for m in rep_ms],
+                "losses": {"d": st.d_loss, "g": st.g_loss, "d_per_step_e2e": d_losses,
+                           "g_per_step_e2e": g_losses, "d_grad_norm_last": d_grad_norm,
+                           "reals": "G0(z') + N(0, 0.05^2) noise, clipped (G0 = the run's random-init generator)"}}
         print(json.dumps(line), flush=True)
     ctx.close()
     if world > 1:

@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define PARAGAN_ABI_VERSION 2
+#define PARAGAN_ABI_VERSION 3
 
 typedef struct paragan_ctx paragan_ctx; /* opaque, library-owned */
 
@@ -64,6 +64,32 @@ typedef struct {
   float lr, beta1, beta2, eps;
 } paragan_adam;
 
+/* Per-network optimisation policy (asymmetric policy, PAPER.md:285-307 [Sec. 5.2]: "users can set the
+ * optimization policy for the generator and discriminator respectively, which currently includes
+ * optimizers, learning rate schedulers, warmup epochs, and gradient norms"; the optimizers of P:293:
+ * AdaBelief, RAdam, Lookahead, LARS).  Hyper-parameters lr, beta1, beta2, eps come from the net's
+ * paragan_adam.  The update of step t (1-based count of applied updates):
+ *   g <- g * min(1, clip_norm / ||g||)           (global norm over the net; clip_norm 0 = off)
+ *   u  = rule(g; m, v, t)                        (ADAM / ADABELIEF / RADAM / SGD with momentum beta1)
+ *   u <- u * lars_trust * ||w_l|| / ||u_l||      (per parameter tensor l, when lars)
+ *   w <- w - lr(t) u,  lr(t) = lr * min(1, t / warmup_steps) * schedule(t)
+ *   every lookahead_k steps: phi <- phi + lookahead_alpha (w - phi); w <- phi
+ * schedule(t): CONSTANT 1, COSINE 0.5 (1 + cos(pi min(t,T)/T)), LINEAR max(0, 1 - t/T), T = total_steps.
+ * All-zero fields = plain Adam (the round-1 behaviour).  Exact rules: DESIGN.md R26-R30. */
+typedef enum { PARAGAN_OPT_ADAM = 0, PARAGAN_OPT_ADABELIEF = 1, PARAGAN_OPT_RADAM = 2, PARAGAN_OPT_SGD = 3 } paragan_opt_rule;
+typedef enum { PARAGAN_SCHED_CONSTANT = 0, PARAGAN_SCHED_COSINE = 1, PARAGAN_SCHED_LINEAR = 2 } paragan_schedule;
+typedef struct {
+  int32_t rule;          /* paragan_opt_rule */
+  int32_t lars;          /* 1 = LARS trust-ratio scaling per parameter tensor */
+  float lars_trust;      /* > 0 when lars */
+  int32_t lookahead_k;   /* 0 = off, else the slow-weight sync period */
+  float lookahead_alpha; /* (0, 1] */
+  int32_t warmup_steps;  /* 0 = off; linear ramp from 0 */
+  int32_t schedule;      /* paragan_schedule */
+  int32_t total_steps;   /* T of the COSINE / LINEAR schedules */
+  float clip_norm;       /* 0 = off */
+} paragan_policy;
+
 /* Model configuration.  BigGAN: the architecture is derived from (resolution, ch)
  * exactly as DESIGN.md §3 R1 states (BigGAN channel tables; 128/256/512 and the
  * small 16/32 test resolutions).  SN-DCGAN (arch = PARAGAN_ARCH_SNDCGAN): resolution 32,
@@ -86,6 +112,7 @@ typedef struct {
   int32_t rank, world_size, device;
   uint64_t seed;         /* on-device weight init (paragan_init_params) */
   int32_t arch;          /* a paragan_arch value; field added in ABI 2 */
+  paragan_policy policy_d, policy_g;   /* ABI 3 */
 } paragan_config;
 
 typedef struct {
@@ -157,14 +184,15 @@ paragan_status paragan_d_step(paragan_ctx* ctx, const void* real_nhwc, const int
  * Returns PARAGAN_ERR_ORDER unless d_steps_per_g D steps preceded it. */
 paragan_status paragan_g_step(paragan_ctx* ctx, const float* z, const int32_t* y, uint32_t flags);
 
-/* In-place mean of the net's gradient over all ranks (NCCL all-reduce over
- * NVLink).  d_step/g_step call it themselves unless
- * PARAGAN_FLAG_NO_ALLREDUCE is set. */
+/* In-place SUM of the net's gradient over all ranks (NCCL all-reduce over
+ * NVLink); the mean's 1/world_size is folded into the update
+ * (paragan_apply_update) and into paragan_get_grads, so no separate scaling pass
+ * runs.  d_step/g_step call it themselves unless PARAGAN_FLAG_NO_ALLREDUCE is set. */
 paragan_status paragan_allreduce_grads(paragan_ctx* ctx, paragan_net net);
 
-/* Adam on the net with its own hyper-parameters; skipped
- * (state unchanged) when the gradient is non-finite.  Pairs with
- * PARAGAN_FLAG_NO_UPDATE. */
+/* The net's optimiser update with its own policy and hyper-parameters
+ * (paragan_policy); skipped (state unchanged) when the gradient
+ * is non-finite.  Pairs with PARAGAN_FLAG_NO_UPDATE. */
 paragan_status paragan_apply_update(paragan_ctx* ctx, paragan_net net);
 
 /* Losses of the last D and G steps; synchronises the stream.  Returns
@@ -173,6 +201,13 @@ paragan_status paragan_sync_stats(paragan_ctx* ctx, paragan_stats* out);
 
 /* Copy the last generated images (bf16/fp32 NHWC as D saw them) to host NCHW fp32 [B,3,R,R]. */
 paragan_status paragan_get_fakes(paragan_ctx* ctx, float* host_nchw, size_t n);
+
+/* Test hook: the gradient of the last G step's loss with respect to the generated images, as D's
+ * backward produced it (the dgrad of D's first conv, in the compute dtype), unpacked to host NCHW fp32
+ * [B,3,R,R].  Available only after a paragan_g_step called with PARAGAN_FLAG_KEEP_DFAKE (otherwise
+ * PARAGAN_ERR_ORDER).  Lets tests compare G's backward and D's input gradient with the oracle
+ * separately (each fed the other side's tensor).  Synchronises the stream. */
+paragan_status paragan_get_dfake(paragan_ctx* ctx, float* host_nchw, size_t n);
 
 /* Number of kernels this context launched since creation (bench accounting). */
 paragan_status paragan_kernel_launches(const paragan_ctx* ctx, uint64_t* n);
@@ -195,6 +230,7 @@ paragan_status paragan_destroy(paragan_ctx* ctx);
 
 #define PARAGAN_FLAG_NO_ALLREDUCE 1u /* keep the local gradient (test hook) */
 #define PARAGAN_FLAG_NO_UPDATE 2u    /* skip Adam (test hook) */
+#define PARAGAN_FLAG_KEEP_DFAKE 4u   /* g_step keeps dL_G/d(fake images) for paragan_get_dfake (test hook) */
 
 /* ------------------------------------------------------- op-level test hooks
  * Single kernels of the path, exposed so tests can compare each with the
@@ -205,6 +241,16 @@ paragan_status paragan_destroy(paragan_ctx* ctx);
 paragan_status paragan_op_conv_fwd(paragan_dtype dt, const void* x, int32_t n, int32_t h, int32_t w, int32_t cin,
                                    const void* wgt, const float* bias, int32_t cout, int32_t ksz, void* y,
                                    void* stream);
+/* The same BF16 tcgen05 convolution with the fused epilogues the training step uses (tc_conv.cu):
+ *   y = bf16( relu_out ? max(0, acc + bias + r) : acc + bias + r ),  acc zeroed where relu_ref <= 0,
+ * r = residual[pixel] (res_mode 1, bf16 [N,H,W,Cout]) or residual at the half-resolution pixel
+ * (res_mode 2, bf16 [N,H/2,W/2,Cout]: the x2-nearest-upsampled skip of G's blocks), or 0 (residual
+ * NULL).  relu_ref: bf16 [N,H,W,Cout] or NULL (the dgrad's fused ReLU-backward mask).  All device
+ * pointers 16-byte aligned; shapes as op_conv_fwd. */
+paragan_status paragan_op_conv_fwd_ex(const void* x, int32_t n, int32_t h, int32_t w, int32_t cin, const void* wgt,
+                                      const float* bias, int32_t cout, int32_t ksz, const void* residual,
+                                      int32_t res_mode, const void* relu_ref, int32_t relu_out, void* y,
+                                      void* stream);
 /* dw[Cout][k*k][Cin] (fp32) = sum_p dy[p][o] * x[p + tap][c]; db[Cout] (fp32, optional, NULL to skip) =
  * sum_p dy[p][o], the bias gradient (BF16: computed by the same tcgen05 launch).
  * F32 with Cout = 3, 3x3 (G's fp32 output layer) runs the thin kernels, also in op_conv_fwd. */

@@ -11,7 +11,8 @@ What is computed, in the paper's order:
   * BigGAN backbone (topology reading R1, pinned by the parameter count
     158.42M of Table 1, P:56);
   * bf16 storage with fp32 last layers of G and D (R14) when
-    ``cfg.bf16`` is set — storage points are explicit ``q()`` calls;
+    ``cfg.bf16`` is set — one layer-by-layer rule (oracle/ops.py), written as
+    explicit ``q()`` / ``qv()`` / ``qg()`` calls;
   * the D input is the concatenation [fake; real] ("concatenate the two
     input matrices before the matrix multiplication");
   * hinge loss (R3), spectral norm with one power step per forward (R4),
@@ -71,11 +72,13 @@ class Config:
     bn_eps: float = 1e-5
     sn_eps: float = 1e-12
     d_steps_per_g: int = 1
-    bf16: bool = False           # emulate the bf16 storage points of R14
-    subpixel: bool = True         # with bf16: G's conv1 through the phase decomposition (R24)
+    bf16: bool = False           # emulate the bf16 storage rule of R14 (oracle/ops.py q/qv/qg)
     arch: str = "biggan"          # "biggan" (R1) or "sndcgan" (config 1, R25; oracle/sndcgan.py)
     adam_d: AdamHP = field(default_factory=lambda: AdamHP(2e-4, 0.0, 0.999, 1e-8))
     adam_g: AdamHP = field(default_factory=lambda: AdamHP(5e-5, 0.0, 0.999, 1e-8))
+    # asymmetric optimisation policy per network (NEXT-3; oracle/optim.py); None = Adam (R12)
+    policy_d: object = None
+    policy_g: object = None
 
     @property
     def n_blocks_g(self) -> int:
@@ -252,7 +255,10 @@ def _qw(sn: _SN, name: str) -> torch.Tensor:
 
 
 def g_forward(cfg: Config, sn: _SN, z: torch.Tensor, y: torch.Tensor) -> torch.Tensor:
-    """Generator (Appendix A of SURVEY; R1, R10, R11).  Returns images NCHW in [-1, 1]."""
+    """Generator (Appendix A of SURVEY; R1, R10, R11).  Returns images NCHW in [-1, 1].
+
+    bf16 mode: the layer-by-layer storage rule of R14 (oracle/ops.py): q() on every layer output,
+    qg() on every layer input, bf16(W/sigma) for every tensor-core weight."""
     if cfg.arch == "sndcgan":
         from . import sndcgan
         return sndcgan.g_forward(cfg, sn, z, y)
@@ -271,18 +277,13 @@ def g_forward(cfg: Config, sn: _SN, z: torch.Tensor, y: torch.Tensor) -> torch.T
         g1 = cond @ sn.w(pre + "cbn1.gain").t()
         b1 = cond @ sn.w(pre + "cbn1.bias").t()
         x = h
-        a = qv(torch.relu(ops.cbn(x, g1, b1, cfg.bn_eps)), bf)
-        if bf and cfg.subpixel:
-            # R24: conv3x3(up2(a)) as four phase 2x2 convs of the low-resolution a with the folded kernel
-            # stored bf16; the conv input's gradient is stored at low resolution (up2 adjoint included)
-            a = q(ops.up2_conv3x3_phases(qg(a, bf), sn.w(pre + "conv1.w"), p[pre + "conv1.b"], bf), bf)
-        else:
-            a = qg(ops.up2(a), bf)                   # the conv input's gradient is stored at full resolution
-            a = q(ops.conv2d(a, _qw(sn, pre + "conv1.w"), p[pre + "conv1.b"]), bf)
+        a = q(torch.relu(ops.cbn(qg(x, bf), g1, b1, cfg.bn_eps)), bf)       # CBN+ReLU layer
+        a = q(ops.up2(a), bf)                                                # nearest x2 (resampling layer)
+        a = q(ops.conv2d(a, _qw(sn, pre + "conv1.w"), p[pre + "conv1.b"]), bf)
         g2 = cond @ sn.w(pre + "cbn2.gain").t()
         b2 = cond @ sn.w(pre + "cbn2.bias").t()
         a = q(torch.relu(ops.cbn(a, g2, b2, cfg.bn_eps)), bf)
-        # skip 1x1 before the upsample (commutes); its input gradient is a separately stored partial
+        # skip 1x1 conv before the upsample (it commutes with nearest x2), added in conv2's fp32 epilogue
         s = q(ops.conv2d(qg(x, bf), _qw(sn, pre + "sc.w"), p[pre + "sc.b"]), bf)
         h = q(ops.conv2d(a, _qw(sn, pre + "conv2.w"), p[pre + "conv2.b"]) + ops.up2(s), bf)
         if att:
@@ -293,14 +294,14 @@ def g_forward(cfg: Config, sn: _SN, z: torch.Tensor, y: torch.Tensor) -> torch.T
 
 
 def _attention(cfg: Config, sn: _SN, pre: str, x: torch.Tensor) -> torch.Tensor:
-    """Non-local block with the bf16 storage points of R14: theta/phi/g conv outputs, the
-    softmax output and beta*g stored bf16; scores, their softmax and dP in fp32; dS and the
-    theta/phi/g/o gradients stored bf16."""
+    """Non-local block under the R14 rule: the theta/phi/g 1x1 convs and the o conv (with the
+    gamma-scaled residual add fused) are layers; the attention core's tensor-core operands beta
+    (forward) and the score gradient dS (backward) are bf16, the scores, softmax and dP fp32."""
     bf = cfg.bf16
     n, c, h, w = x.shape
-    theta = q(ops.conv2d(x, _qw(sn, pre + "theta"), None), bf).reshape(n, -1, h * w)
-    phi = ops.maxpool2(q(ops.conv2d(x, _qw(sn, pre + "phi"), None), bf)).reshape(n, -1, h * w // 4)
-    g = ops.maxpool2(q(ops.conv2d(x, _qw(sn, pre + "g"), None), bf)).reshape(n, -1, h * w // 4)
+    theta = q(ops.conv2d(qg(x, bf), _qw(sn, pre + "theta"), None), bf).reshape(n, -1, h * w)
+    phi = q(ops.maxpool2(q(ops.conv2d(qg(x, bf), _qw(sn, pre + "phi"), None), bf)), bf).reshape(n, -1, h * w // 4)
+    g = q(ops.maxpool2(q(ops.conv2d(qg(x, bf), _qw(sn, pre + "g"), None), bf)), bf).reshape(n, -1, h * w // 4)
     scores = qg(torch.bmm(theta.transpose(1, 2), phi), bf)
     beta = qv(torch.softmax(scores, dim=-1), bf)
     o = q(torch.bmm(g, beta.transpose(1, 2)).reshape(n, -1, h, w), bf)
@@ -308,7 +309,9 @@ def _attention(cfg: Config, sn: _SN, pre: str, x: torch.Tensor) -> torch.Tensor:
 
 
 def d_forward(cfg: Config, sn: _SN, x: torch.Tensor, y: torch.Tensor) -> torch.Tensor:
-    """Projection discriminator (Appendix A; R1, R7).  x NCHW; returns logits [N] (fp32 head)."""
+    """Projection discriminator (Appendix A; R1, R7).  x NCHW; returns logits [N] (fp32 head).
+
+    bf16 mode: the R14 rule as in g_forward (ReLU is exact on bf16 values and gradients)."""
     if cfg.arch == "sndcgan":
         from . import sndcgan
         return sndcgan.d_forward(cfg, sn, x, y)
@@ -318,17 +321,18 @@ def d_forward(cfg: Config, sn: _SN, x: torch.Tensor, y: torch.Tensor) -> torch.T
     blocks = d_blocks(cfg)
     for j, (ci, co, _, dn, att) in enumerate(blocks):
         pre = f"b{j}."
-        a = h if j == 0 else qv(torch.relu(h), bf)
-        a = q(ops.conv2d(a, _qw(sn, pre + "conv1.w"), p[pre + "conv1.b"]), bf)
-        c2 = ops.conv2d(q(torch.relu(a), bf), _qw(sn, pre + "conv2.w"), p[pre + "conv2.b"])
+        a = h if j == 0 else torch.relu(h)
+        a = q(ops.conv2d(qg(a, bf), _qw(sn, pre + "conv1.w"), p[pre + "conv1.b"]), bf)
+        c2 = ops.conv2d(qg(torch.relu(a), bf), _qw(sn, pre + "conv2.w"), p[pre + "conv2.b"])
         learn = ci != co or dn
         if dn and j == 0:
-            # block 0 (no pre-activation): pool the image, then the 1x1 skip conv (R7)
-            s = q(ops.conv2d(q(ops.avgpool2(h), bf), _qw(sn, pre + "sc.w"), p[pre + "sc.b"]), bf)
+            # block 0 (no pre-activation): pool the image, then the 1x1 skip conv (R7); the main branch's
+            # conv2 output is a layer output, pooled and added to the skip in one layer
+            s = q(ops.conv2d(qg(q(ops.avgpool2(h), bf), bf), _qw(sn, pre + "sc.w"), p[pre + "sc.b"]), bf)
             h = q(ops.avgpool2(q(c2, bf)) + s, bf)
         else:
-            # later blocks: 1x1 skip conv, residual add, then pool (= pool of each branch, R7);
-            # the skip conv's input gradient is a separately stored partial
+            # later blocks: 1x1 skip conv, conv2 with the residual add fused, then pool (= pool of each
+            # branch, R7)
             s = q(ops.conv2d(qg(h, bf), _qw(sn, pre + "sc.w"), p[pre + "sc.b"]), bf) if learn else h
             t = q(c2 + s, bf)
             h = q(ops.avgpool2(t), bf) if dn else t
@@ -364,11 +368,19 @@ class NetState:
         return torch.cat([grads[s.name].reshape(-1) for s in self.specs]).numpy()
 
 
-def _adam(st: NetState, grads: dict, hp: AdamHP) -> bool:
-    """One Adam update (R12); skipped entirely when any gradient is non-finite (R16)."""
+def _adam(st: NetState, grads: dict, hp: AdamHP, policy=None) -> bool:
+    """One Adam update (R12), or the net's optimisation policy (oracle/optim.py) when given; skipped
+    entirely when any gradient is non-finite (R16)."""
     if not all(torch.isfinite(g).all() for g in grads.values()):
         return False
     st.t += 1
+    if policy is not None:
+        from . import optim
+        p = dataclasses.replace(policy, lr=hp.lr, beta1=hp.beta1, beta2=hp.beta2, eps=hp.eps)
+        if not hasattr(st, "opt_states"):
+            st.opt_states = {k: optim.State(v) for k, v in st.params.items()}
+        optim.step(p, st.params, grads, st.opt_states, st.t)
+        return True
     for name, g in grads.items():
         st.params[name], st.m[name], st.v[name] = ops.adam_update(
             st.params[name], g, st.m[name], st.v[name], st.t, hp.lr, hp.beta1, hp.beta2, hp.eps)
@@ -406,7 +418,7 @@ def d_step(cfg: Config, G: NetState, D: NetState, real, real_y, z, fake_y, updat
     gl = torch.autograd.grad(loss, [dparams[n] for n in names], allow_unused=True)
     grads = {n: (g if g is not None else torch.zeros_like(dparams[n])).detach() for n, g in zip(names, gl)}
     D.params = {k: v.detach() for k, v in dparams.items()}
-    ok = _adam(D, grads, cfg.adam_d) if update else True
+    ok = _adam(D, grads, cfg.adam_d, cfg.policy_d) if update else True
     return dict(loss=float(loss.detach()), logits=logits.detach().numpy(), fake=fake.detach().numpy(),
                 grads=D.grad_flat(grads), applied=ok,
                 sigma_g=dict(sng.sigma), sigma_d=dict(snd.sigma),
@@ -428,7 +440,7 @@ def g_step(cfg: Config, G: NetState, D: NetState, z, y, update: bool = True) -> 
     gl = torch.autograd.grad(loss, [gparams[n] for n in names], allow_unused=True)
     grads = {n: (g if g is not None else torch.zeros_like(gparams[n])).detach() for n, g in zip(names, gl)}
     G.params = {k: v.detach() for k, v in gparams.items()}
-    ok = _adam(G, grads, cfg.adam_g) if update else True
+    ok = _adam(G, grads, cfg.adam_g, cfg.policy_g) if update else True
     return dict(loss=float(loss.detach()), logits=logits.detach().numpy(), fake=fake.detach().numpy(),
                 grads=G.grad_flat(grads), applied=ok, sigma_g=dict(sng.sigma), sigma_d=dict(snd.sigma))
 

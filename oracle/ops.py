@@ -27,7 +27,7 @@ def bf16_round(x: torch.Tensor) -> torch.Tensor:
 
 class _Q(torch.autograd.Function):
     """Identity in exact arithmetic; rounds the forward value and the incoming
-    gradient to bf16 — the storage points of the precision policy R14."""
+    gradient to bf16 (see :func:`q`)."""
 
     @staticmethod
     def forward(ctx, x):
@@ -39,7 +39,7 @@ class _Q(torch.autograd.Function):
 
 
 class _QV(torch.autograd.Function):
-    """Rounds the stored value to bf16; the gradient flowing back is not a stored tensor."""
+    """Rounds the value to bf16; the gradient passes unrounded (see :func:`qv`)."""
 
     @staticmethod
     def forward(ctx, x):
@@ -51,7 +51,7 @@ class _QV(torch.autograd.Function):
 
 
 class _QG(torch.autograd.Function):
-    """Identity value; the gradient w.r.t. this tensor is stored in bf16."""
+    """Identity value; rounds the gradient to bf16 (see :func:`qg`)."""
 
     @staticmethod
     def forward(ctx, x):
@@ -62,18 +62,28 @@ class _QG(torch.autograd.Function):
         return bf16_round(g)
 
 
+# The bf16 storage rule (precision policy R14, "mixed-precision training with bf16"),
+# stated once as layer-by-layer semantics: every layer (linear, conv with its bias and fused residual add,
+# CBN+ReLU, resampling, pool, the attention core) reads bf16 tensors and writes ONE bf16 output; its
+# backward reads the bf16 output gradient and writes a bf16 gradient for each input (a tensor read by
+# several layers receives one rounded contribution per layer, summed); inside a layer the arithmetic is
+# fp32 or better; tensor-core operands are bf16 in the forward and the backward.  G's output layer and
+# D's head are fp32 throughout.  Three primitives express it:
+
 def q(x: torch.Tensor, on: bool) -> torch.Tensor:
-    """Storage point: bf16 round-trip of value and gradient when ``on``."""
+    """A layer's output: value stored bf16, and its gradient (the next layers' backward output) bf16."""
     return _Q.apply(x) if on else x
 
 
 def qv(x: torch.Tensor, on: bool) -> torch.Tensor:
-    """Value-only storage point (the gradient of this tensor is kept in fp32)."""
+    """A tensor-core operand internal to one layer (the attention probabilities): bf16 value; its
+    gradient stays inside the layer in fp32."""
     return _QV.apply(x) if on else x
 
 
 def qg(x: torch.Tensor, on: bool) -> torch.Tensor:
-    """Gradient-only storage point (e.g. a branch's partial gradient written in bf16)."""
+    """A layer's input as seen by that layer's backward: the input-gradient contribution it writes is
+    bf16 (also a backward tensor-core operand internal to a layer, the attention score gradient)."""
     return _QG.apply(x) if on else x
 
 
@@ -142,13 +152,14 @@ def up2(x: torch.Tensor) -> torch.Tensor:
     return x.repeat_interleave(2, dim=2).repeat_interleave(2, dim=3)
 
 
-def up2_conv3x3_phases(x: torch.Tensor, w: torch.Tensor, b: torch.Tensor | None, bf16: bool) -> torch.Tensor:
+def up2_conv3x3_phases(x: torch.Tensor, w: torch.Tensor, b: torch.Tensor | None) -> torch.Tensor:
     """conv3x3(up2(x)) written as four 2x2 convs of the low-resolution x, one per output phase (a, b)
     (reading R24).  Output row 2i+a reads input rows i-1+a+p, p in {0, 1}, with the
     folded kernel Wf_ab[p][q] = sum_{r in R(a,p), s in R(b,q)} W[r][s], R(0,0)={0}, R(0,1)={1,2},
     R(1,0)={0,1}, R(1,1)={2}.  Identical to conv2d(up2(x), w, b) in exact arithmetic (pinned in
-    tests/test_oracle_primitives.py).  With ``bf16`` the folded kernel is the stored bf16 operand
-    (straight-through: the gradient w.r.t. w is the exact unfold)."""
+    tests/test_oracle_primitives.py).  Not used by the training-step oracle (which convolves the
+    upsampled tensor as BigGAN defines it); kept as the written-out statement of the identity the
+    CUDA path's G conv1 relies on."""
     rows = {(0, 0): (0,), (0, 1): (1, 2), (1, 0): (0, 1), (1, 1): (2,)}
     phases = []
     for a in (0, 1):
@@ -159,8 +170,6 @@ def up2_conv3x3_phases(x: torch.Tensor, w: torch.Tensor, b: torch.Tensor | None,
                 for q_ in (0, 1):
                     taps.append(sum(w[:, :, r, sc] for r in rows[(a, p)] for sc in rows[(bb, q_)]))
             wf = torch.stack(taps, dim=-1).reshape(w.shape[0], w.shape[1], 2, 2)
-            if bf16:
-                wf = bf16_round(wf.detach()) + (wf - wf.detach())
             xp = F.pad(x, (1 - bb, bb, 1 - a, a))      # (left, right, top, bottom)
             row.append(F.conv2d(xp, wf, b))
         phases.append(torch.stack(row, dim=-1))          # [N, C, H, W, 2(b)]

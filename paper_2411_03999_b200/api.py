@@ -13,16 +13,33 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libparagan.so")
 
-PARAGAN_ABI_VERSION = 2
+PARAGAN_ABI_VERSION = 3
 F32, BF16 = 0, 1
 ARCH_BIGGAN, ARCH_SNDCGAN = 0, 1
 NET_D, NET_G = 0, 1
-FLAG_NO_ALLREDUCE, FLAG_NO_UPDATE = 1, 2
+FLAG_NO_ALLREDUCE, FLAG_NO_UPDATE, FLAG_KEEP_DFAKE = 1, 2, 4
 STATUS = {0: "OK", 1: "INVALID_ARG", 2: "CONFIG", 3: "NONFINITE", 4: "IO", 5: "CUDA", 6: "NCCL", 7: "ORDER", 8: "OOM"}
 
 
 class Adam(C.Structure):
     _fields_ = [("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float)]
+
+
+OPT_ADAM, OPT_ADABELIEF, OPT_RADAM, OPT_SGD = 0, 1, 2, 3
+SCHED_CONSTANT, SCHED_COSINE, SCHED_LINEAR = 0, 1, 2
+
+
+class Policy(C.Structure):
+    """paragan_policy: per-network optimisation policy."""
+    _fields_ = [("rule", C.c_int32), ("lars", C.c_int32), ("lars_trust", C.c_float), ("lookahead_k", C.c_int32),
+                ("lookahead_alpha", C.c_float), ("warmup_steps", C.c_int32), ("schedule", C.c_int32),
+                ("total_steps", C.c_int32), ("clip_norm", C.c_float)]
+
+
+def make_policy(rule=OPT_ADAM, lars=False, lars_trust=1.0, lookahead_k=0, lookahead_alpha=0.5, warmup_steps=0,
+                schedule=SCHED_CONSTANT, total_steps=0, clip_norm=0.0) -> Policy:
+    return Policy(rule, 1 if lars else 0, lars_trust, lookahead_k, lookahead_alpha, warmup_steps, schedule,
+                  total_steps, clip_norm)
 
 
 class Config(C.Structure):
@@ -31,7 +48,8 @@ class Config(C.Structure):
                 ("attn_res", C.c_int32), ("local_batch", C.c_int32), ("d_steps_per_g", C.c_int32),
                 ("compute", C.c_int32), ("c_pad_image", C.c_int32), ("adam_d", Adam), ("adam_g", Adam),
                 ("sn_eps", C.c_float), ("bn_eps", C.c_float), ("rank", C.c_int32), ("world_size", C.c_int32),
-                ("device", C.c_int32), ("seed", C.c_uint64), ("arch", C.c_int32)]
+                ("device", C.c_int32), ("seed", C.c_uint64), ("arch", C.c_int32), ("policy_d", Policy),
+                ("policy_g", Policy)]
 
 
 class Stats(C.Structure):
@@ -66,6 +84,7 @@ SYMBOLS = {
     "paragan_apply_update": (C.c_int, [C.c_void_p, C.c_int]),
     "paragan_sync_stats": (C.c_int, [C.c_void_p, C.POINTER(Stats)]),
     "paragan_get_fakes": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t]),
+    "paragan_get_dfake": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t]),
     "paragan_kernel_launches": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64)]),
     "paragan_profile": (C.c_int, [C.c_void_p, C.c_int32]),
     "paragan_profile_read": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_uint64), C.POINTER(C.c_double),
@@ -74,6 +93,9 @@ SYMBOLS = {
     "paragan_destroy": (C.c_int, [C.c_void_p]),
     "paragan_op_conv_fwd": (C.c_int, [C.c_int, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
                                       C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
+    "paragan_op_conv_fwd_ex": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
+                                         C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p,
+                                         C.c_int32, C.c_void_p, C.c_void_p]),
     "paragan_op_conv_wgrad": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                         C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
     "paragan_op_conv_up2_fwd": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
@@ -130,13 +152,15 @@ def _stream(stream):
 def make_config(resolution=128, ch=96, n_classes=1000, shared_dim=128, z_chunk=20, attn_res=64, local_batch=256,
                 d_steps_per_g=1, compute=BF16, c_pad_image=8, adam_d=(2e-4, 0.0, 0.999, None),
                 adam_g=(5e-5, 0.0, 0.999, None), sn_eps=1e-12, bn_eps=1e-5, rank=0, world_size=1, device=0,
-                seed=0, arch=0) -> Config:
-    """BigGAN config; Adam eps defaults to 1e-6 under bf16 and 1e-8 in fp32."""
+                seed=0, arch=0, policy_d=None, policy_g=None) -> Config:
+    """BigGAN config; Adam eps defaults to 1e-6 under bf16 and 1e-8 in fp32.
+    policy_d / policy_g: paragan_policy (make_policy); None = plain Adam."""
     eps = 1e-6 if compute == BF16 else 1e-8
     ad = Adam(adam_d[0], adam_d[1], adam_d[2], adam_d[3] if adam_d[3] is not None else eps)
     ag = Adam(adam_g[0], adam_g[1], adam_g[2], adam_g[3] if adam_g[3] is not None else eps)
     return Config(PARAGAN_ABI_VERSION, resolution, ch, n_classes, shared_dim, z_chunk, attn_res, local_batch,
-                  d_steps_per_g, compute, c_pad_image, ad, ag, sn_eps, bn_eps, rank, world_size, device, seed, arch)
+                  d_steps_per_g, compute, c_pad_image, ad, ag, sn_eps, bn_eps, rank, world_size, device, seed, arch,
+                  policy_d or make_policy(), policy_g or make_policy())
 
 
 def make_sndcgan_config(ch=32, n_classes=10, local_batch=8, d_steps_per_g=1, **kw) -> Config:
@@ -186,6 +210,15 @@ def op_conv_fwd(dtype, x, wgt, bias, cout, ksz, y, stream=None):
     n, h, w, cin = x.shape
     _check("paragan_op_conv_fwd", lib().paragan_op_conv_fwd(dtype, _ptr(x), n, h, w, cin, _ptr(wgt), _ptr(bias), cout,
                                                             ksz, _ptr(y), _stream(stream)))
+
+
+def op_conv_fwd_ex(x, wgt, bias, cout, ksz, y, residual=None, res_mode=0, relu_ref=None, relu_out=False,
+                   stream=None):
+    """BF16 tcgen05 conv with the step's fused epilogues (residual add, ReLU-backward mask, ReLU)."""
+    n, h, w, cin = x.shape
+    _check("paragan_op_conv_fwd_ex", lib().paragan_op_conv_fwd_ex(
+        _ptr(x), n, h, w, cin, _ptr(wgt), _ptr(bias), cout, ksz, _ptr(residual), res_mode if residual is not None
+        else 0, _ptr(relu_ref), 1 if relu_out else 0, _ptr(y), _stream(stream)))
 
 
 def op_conv_wgrad(dtype, x, dy, cout, ksz, dw, stream=None, db=None):
@@ -289,6 +322,14 @@ class Context:
         r = self.cfg.resolution
         a = np.empty((self.cfg.local_batch, 3, r, r), dtype=np.float32)
         _check("paragan_get_fakes", lib().paragan_get_fakes(self.ctx, a.ctypes.data, a.size), self.ctx)
+        return a
+
+    def get_dfake(self):
+        """dL_G/d(fake images) of the last g_step run with FLAG_KEEP_DFAKE (test hook), NCHW fp32."""
+        import numpy as np
+        r = self.cfg.resolution
+        a = np.empty((self.cfg.local_batch, 3, r, r), dtype=np.float32)
+        _check("paragan_get_dfake", lib().paragan_get_dfake(self.ctx, a.ctypes.data, a.size), self.ctx)
         return a
 
     def d_step(self, real_nhwc, real_y, z, fake_y, flags=0):

@@ -143,6 +143,10 @@ paragan_status paragan_get_fakes(paragan_ctx* ctx, float* host, size_t n) {
   if (!ctx || !ctx->eng) return PARAGAN_ERR_INVALID_ARG;
   return ctx->eng->get_fakes(host, n);
 }
+paragan_status paragan_get_dfake(paragan_ctx* ctx, float* host, size_t n) {
+  if (!ctx || !ctx->eng) return PARAGAN_ERR_INVALID_ARG;
+  return ctx->eng->get_dfake(host, n);
+}
 paragan_status paragan_kernel_launches(const paragan_ctx* ctx, uint64_t* n) {
   if (!ctx || !ctx->eng || !n) return PARAGAN_ERR_INVALID_ARG;
   *n = ctx->eng->launches();
@@ -189,6 +193,25 @@ paragan_status paragan_op_conv_fwd(paragan_dtype dt, const void* x, int32_t n, i
                                                           static_cast<const float*>(wgt), cout, ksz, bias, nullptr,
                                                           nullptr, 0, static_cast<float*>(y), st));
   return PARAGAN_ERR_INVALID_ARG;
+}
+
+paragan_status paragan_op_conv_fwd_ex(const void* x, int32_t n, int32_t h, int32_t w, int32_t cin, const void* wgt,
+                                      const float* bias, int32_t cout, int32_t ksz, const void* residual,
+                                      int32_t res_mode, const void* relu_ref, int32_t relu_out, void* y,
+                                      void* stream) {
+  if (!x || !wgt || !y || n < 1 || h < 1 || w < 1 || cin < 8 || cout < 1 || (ksz != 1 && ksz != 3) || cin % 8 ||
+      !aligned16(x) || !aligned16(wgt) || !aligned16(y) || !tc_geometry_ok(h, w) ||
+      (residual && (res_mode != 1 && res_mode != 2)) || (residual && !aligned16(residual)) ||
+      (res_mode == 2 && (h % 2 || w % 2)) || (relu_ref && !aligned16(relu_ref)))
+    return PARAGAN_ERR_INVALID_ARG;
+  TcEpilogue e;
+  e.bias = bias;
+  e.residual = residual;
+  e.res_mode = residual ? res_mode : 0;
+  e.relu_ref = relu_ref;
+  e.relu_out = relu_out ? 1 : 0;
+  e.out = y;
+  return cuda_status(tc_conv_fprop(x, n, h, w, cin, wgt, cout, ksz, e, static_cast<cudaStream_t>(stream)));
 }
 
 paragan_status paragan_op_conv_wgrad(paragan_dtype dt, const void* x, const void* dy, int32_t n, int32_t h, int32_t w,

@@ -23,6 +23,7 @@
 #include "engine.h"
 #include "tc_attn.h"
 #include "kernels.h"
+#include "optim.h"
 #include "tc_conv.h"
 
 namespace pg {
@@ -78,6 +79,13 @@ struct Net {
   long long* t_dev = nullptr;
   int* flag = nullptr;
   float* loss = nullptr;   // [4]
+  // optimiser policy (NEXT-3): chunk table over the parameter tensors, reduction partials, slow weights
+  std::vector<OptChunk> chunks_h;
+  OptChunk* chunks_d = nullptr;
+  double *opt_wpart = nullptr, *opt_upart = nullptr;
+  float* clip_scale = nullptr;
+  float* slow = nullptr;   // Lookahead phi (only when enabled)
+  float gsum = 1.0f;       // ranks summed into g by the last all-reduce (1/gsum = the mean's factor)
   int add(const std::string& name, std::vector<int> shape, bool conv4d, bool sn) {
     PEntry e;
     e.name = name;
@@ -220,6 +228,7 @@ class Engine final : public EngineBase {
     dcgan_ = c.arch == PARAGAN_ARCH_SNDCGAN;
   }
   ~Engine() override {
+    if (dfake_keep_) cudaFree(dfake_keep_);
     if (comm_) ncclCommDestroy(comm_);
     if (cublas_) cublasDestroy(cublas_);
   }
@@ -331,7 +340,7 @@ class Engine final : public EngineBase {
     if (!ready_) return PARAGAN_ERR_ORDER;
     Net& N = net == PARAGAN_NET_D ? D_ : G_;
     if (!host || n != (size_t)N.n) return fail_arg("get_grads: size mismatch");
-    return export_flat(N, N.g, host, false);
+    return export_flat(N, N.g, host, false, 1.0f / N.gsum);
   }
   paragan_status get_fakes(float* host, size_t n) override {
     if (!ready_) return PARAGAN_ERR_ORDER;
@@ -341,6 +350,24 @@ class Engine final : public EngineBase {
     if (cudaMemcpyAsync(host, scratch_f_, need * sizeof(float), cudaMemcpyDeviceToHost, st_))
       return fail_cuda(cudaGetLastError(), "get_fakes");
     return sync_ok();
+  }
+
+  paragan_status get_dfake(float* host, size_t n) override {
+    if (!ready_ || !dfake_valid_) return PARAGAN_ERR_ORDER;
+    const size_t need = (size_t)B_ * 3 * R_ * R_;
+    if (!host || n != need) return fail_arg("get_dfake: size mismatch");
+    if (cudaMemcpyAsync(host, dfake_keep_, need * sizeof(float), cudaMemcpyDeviceToHost, st_))
+      return fail_cuda(cudaGetLastError(), "get_dfake");
+    return sync_ok();
+  }
+  // test hook (PARAGAN_FLAG_KEEP_DFAKE): keep dL_G/d(fake) before G's backward reuses the buffers
+  paragan_status keep_dfake() {
+    const size_t need = (size_t)B_ * 3 * R_ * R_;
+    if (!dfake_keep_ && cudaMalloc(&dfake_keep_, need * sizeof(float)) != cudaSuccess)
+      return fail_cuda(cudaGetLastError(), "keep_dfake alloc");
+    CK(layout_unpack<T>(static_cast<const T*>(dimg_grad_), dfake_keep_, B_, 3, R_, R_, cpad_, st_));
+    dfake_valid_ = true;
+    return PARAGAN_OK;
   }
 
   // ------------------------------------------------------------------ steps
@@ -366,6 +393,7 @@ class Engine final : public EngineBase {
     ++launches_;
     CKS(allreduce_loss(D_.loss));
     CK(cudaMemsetAsync(D_.g, 0, sizeof(float) * D_.n, st_));
+    D_.gsum = 1.0f;
     if (dcgan_) CKS(d_backward_dc(2 * B_, true, false));
     else CKS(d_backward(2 * B_, true, false));
     CKS(sn_backward_net(D_));
@@ -382,6 +410,7 @@ class Engine final : public EngineBase {
       return PARAGAN_ERR_ORDER;
     }
     if (!z || !y) return fail_arg("g_step: bad pointer");
+    dfake_valid_ = false;
     CKS(sn_forward(G_, true));
     CKS(fold_subpixel(true));
     if (dcgan_) CKS(g_forward_dc(z));
@@ -394,11 +423,14 @@ class Engine final : public EngineBase {
     ++launches_;
     CKS(allreduce_loss(G_.loss));
     CK(cudaMemsetAsync(G_.g, 0, sizeof(float) * G_.n, st_));
+    G_.gsum = 1.0f;
     if (dcgan_) {
       CKS(d_backward_dc(B_, false, true));   // dgrad only, down to the image
+      if (flags & PARAGAN_FLAG_KEEP_DFAKE) CKS(keep_dfake());
       CKS(g_backward_dc());
     } else {
       CKS(d_backward(B_, false, true));   // dgrad only, down to the image
+      if (flags & PARAGAN_FLAG_KEEP_DFAKE) CKS(keep_dfake());
       CKS(g_backward());
     }
     CKS(sn_backward_net(G_));
@@ -411,10 +443,10 @@ class Engine final : public EngineBase {
   paragan_status allreduce(paragan_net net) override {
     if (!ready_ || poisoned_) return PARAGAN_ERR_ORDER;
     Net& N = net == PARAGAN_NET_D ? D_ : G_;
-    if (cfg_.world_size > 1) {
+    if (cfg_.world_size > 1 && N.gsum == 1.0f) {
+      // sum over ranks; the mean's 1/W (R15) is folded into the update and into get_grads
       CKS(nccl_sum(N.g, (size_t)N.n, ncclFloat32, "grad allreduce"));
-      CK(scale_f32(N.g, N.n, 1.0f / cfg_.world_size, st_));   // mean over ranks (R15)
-      ++launches_;
+      N.gsum = (float)cfg_.world_size;
     }
     return PARAGAN_OK;
   }
@@ -423,12 +455,37 @@ class Engine final : public EngineBase {
     if (!ready_ || poisoned_) return PARAGAN_ERR_ORDER;
     Net& N = net == PARAGAN_NET_D ? D_ : G_;
     const paragan_adam& h = net == PARAGAN_NET_D ? cfg_.adam_d : cfg_.adam_g;
+    const float gscale = 1.0f / N.gsum;
     CK(cudaMemsetAsync(N.flag, 0, sizeof(int), st_));
-    CK(check_finite(N.g, N.n, N.flag, st_));
     CK(check_finite_scalar(N.loss, N.flag, st_));
-    CK(adam_flat(N.p, N.g, N.m, N.v, N.n, h.lr, h.beta1, h.beta2, h.eps, N.t_dev, 1.0f, N.flag, st_));
+    if (plain_adam(N)) {
+      CK(check_finite(N.g, N.n, N.flag, st_));
+      CK(adam_flat(N.p, N.g, N.m, N.v, N.n, h.lr, h.beta1, h.beta2, h.eps, N.t_dev, gscale, N.flag, st_));
+    } else {
+      // asymmetric optimisation policy (NEXT-3)
+      const paragan_policy& p = policy(N);
+      const int nc = (int)N.chunks_h.size();
+      OptRule r{p.rule, p.lars, p.lookahead_k, p.warmup_steps, p.schedule, p.total_steps,
+                h.lr, h.beta1, h.beta2, h.eps, p.lars_trust, p.lookahead_alpha, p.clip_norm, gscale};
+      const float* cs = nullptr;
+      if (p.clip_norm > 0.0f) {   // one pass gives the global norm and the finiteness of g
+        CK(opt_sumsq(N.g, N.chunks_d, nc, gscale, N.opt_wpart, st_));
+        CK(opt_clip_finalize(N.opt_wpart, nc, p.clip_norm, N.clip_scale, N.flag, st_));
+        cs = N.clip_scale;
+      } else {
+        CK(check_finite(N.g, N.n, N.flag, st_));
+      }
+      CK(opt_update(N.p, N.g, N.m, N.v, scratch_f_, N.chunks_d, nc, r, N.t_dev, cs, N.flag, N.opt_wpart, N.opt_upart,
+                    st_));
+      if (p.lars) {
+        CK(opt_lars_apply(N.p, scratch_f_, N.chunks_d, nc, r, N.t_dev, N.opt_wpart, N.opt_upart, N.flag, st_));
+      }
+    }
     CK(adam_bookkeep(N.t_dev, N.flag, nonfinite_sticky_, st_));
-    launches_ += 4;
+    if (N.slow) {
+      const paragan_policy& p = policy(N);
+      CK(opt_lookahead(N.p, N.slow, N.n, p.lookahead_k, p.lookahead_alpha, N.t_dev, N.flag, st_));
+    }
     return PARAGAN_OK;
   }
 
@@ -521,8 +578,9 @@ class Engine final : public EngineBase {
     cudaMemsetAsync(N.m, 0, sizeof(float) * N.n, st_);
     cudaMemsetAsync(N.v, 0, sizeof(float) * N.n, st_);
     cudaMemsetAsync(N.t_dev, 0, sizeof(long long), st_);
+    if (N.slow) cudaMemcpyAsync(N.slow, N.p, sizeof(float) * N.n, cudaMemcpyDeviceToDevice, st_);   // phi_0 = w_0
   }
-  paragan_status export_flat(Net& N, const float* src, float* host, bool with_u) {
+  paragan_status export_flat(Net& N, const float* src, float* host, bool with_u, float scale = 1.0f) {
     float* stage = scratch_f_;
     for (const PEntry& e : N.E) {
       if (e.conv4d) {
@@ -531,6 +589,7 @@ class Engine final : public EngineBase {
         CK(cudaMemcpyAsync(stage + e.off, src + e.off, sizeof(float) * e.n, cudaMemcpyDeviceToDevice, st_));
       }
     }
+    if (scale != 1.0f) CK(scale_f32(stage, N.n, scale, st_));   // sum over ranks -> mean (R15)
     if (cudaMemcpyAsync(host, stage, sizeof(float) * N.n, cudaMemcpyDeviceToHost, st_))
       return fail_cuda(cudaGetLastError(), "export copy");
     if (with_u && cudaMemcpyAsync(host + N.n, N.u, sizeof(float) * N.nu, cudaMemcpyDeviceToHost, st_))
@@ -612,6 +671,37 @@ class Engine final : public EngineBase {
       N->loss = A.get<float>(4);
     }
     nonfinite_sticky_ = A.get<int>(1);
+  }
+  const paragan_policy& policy(const Net& N) const { return &N == &D_ ? cfg_.policy_d : cfg_.policy_g; }
+  bool plain_adam(const Net& N) const {
+    const paragan_policy& p = policy(N);
+    return p.rule == PARAGAN_OPT_ADAM && !p.lars && p.lookahead_k == 0 && p.warmup_steps == 0 &&
+           (p.schedule == PARAGAN_SCHED_CONSTANT || p.total_steps == 0) && p.clip_norm == 0.0f;
+  }
+  // chunk table of the optimiser kernels: every parameter tensor split into kOptChunk pieces
+  void alloc_opt_tables(Arena& A) {
+    for (Net* N : {&G_, &D_}) {
+      N->chunks_h.clear();
+      for (const PEntry& e : N->E) {
+        const int first = (int)N->chunks_h.size(), cnt = ceil_div(e.n, kOptChunk);
+        for (int c = 0; c < cnt; ++c) {
+          const long long a = (long long)c * kOptChunk;
+          N->chunks_h.push_back(OptChunk{e.off + a, (int)std::min<long long>(kOptChunk, e.n - a), first, cnt});
+        }
+      }
+      const size_t nc = N->chunks_h.size();
+      N->chunks_d = A.get<OptChunk>(nc);
+      N->opt_wpart = A.get<double>(nc);
+      N->opt_upart = A.get<double>(nc);
+      N->clip_scale = A.get<float>(1);
+      N->slow = policy(*N).lookahead_k > 0 ? A.get<float>(N->n) : nullptr;
+    }
+  }
+  paragan_status upload_opt_tables() {
+    for (Net* N : {&G_, &D_})
+      CK(cudaMemcpyAsync(N->chunks_d, N->chunks_h.data(), N->chunks_h.size() * sizeof(OptChunk),
+                         cudaMemcpyHostToDevice, st_));
+    return PARAGAN_OK;
   }
   // device tables of the grouped SN power iteration / backward and the SN pack lists
   void alloc_sn_tables(Arena& A) {
@@ -894,6 +984,7 @@ class Engine final : public EngineBase {
     wg_scratch_ = A.get<float>((size_t)16 << 20);   // padded / qkv weight-gradient staging
     dpool_ = A.get<float>(std::max<size_t>(dpool_floats_, 1));
     alloc_sn_tables(A);
+    alloc_opt_tables(A);
     // chain G block inputs (block i+1 reads block i's output, or the attention output, in place)
     for (size_t i = 1; i < gb_.size(); ++i) gb_[i].x = gb_[i - 1].attn ? attn_out_[0] : gb_[i - 1].out;
     gout_in_ = gb_.back().attn ? attn_out_[0] : gb_.back().out;
@@ -988,6 +1079,7 @@ class Engine final : public EngineBase {
   }
 
   paragan_status upload_tables() {
+    CKS(upload_opt_tables());
     if (!dcgan_) CKS(upload_cbn_tables());
     for (Net* N : {&G_, &D_}) {
       std::vector<SnJob> jobs;
@@ -1559,6 +1651,7 @@ class Engine final : public EngineBase {
     scratch_floats_ = std::max<size_t>(scratch_floats_, (size_t)4 * 148 * 27 * cl_);
     scratch_f_ = A.get<float>(scratch_floats_);
     alloc_sn_tables(A);
+    alloc_opt_tables(A);
   }
 
   // cross-replica BN (learned gamma/beta) over [M][C] rows, then ReLU
@@ -2131,6 +2224,8 @@ class Engine final : public EngineBase {
   double* osums_ = nullptr;
   void* dimg_ = nullptr;
   void* dimg_grad_ = nullptr;
+  float* dfake_keep_ = nullptr;   // test hook buffer (PARAGAN_FLAG_KEEP_DFAKE), allocated on first use
+  bool dfake_valid_ = false;
   int dimg_idx_ = 0;
   float* demb_hat_ = nullptr;
   float *feat_ = nullptr, *logits_ = nullptr, *dlogits_ = nullptr;
@@ -2157,9 +2252,24 @@ cudaError_t Engine<T>::d2f(const double* s, float* d, int n, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+static bool policy_ok(const paragan_policy& p) {
+  if (p.rule < PARAGAN_OPT_ADAM || p.rule > PARAGAN_OPT_SGD) return false;
+  if (p.lars && !(p.lars_trust > 0.0f)) return false;
+  if (p.lookahead_k < 0 || (p.lookahead_k > 0 && !(p.lookahead_alpha > 0.0f && p.lookahead_alpha <= 1.0f))) return false;
+  if (p.warmup_steps < 0 || p.total_steps < 0 || !(p.clip_norm >= 0.0f)) return false;
+  if (p.schedule < PARAGAN_SCHED_CONSTANT || p.schedule > PARAGAN_SCHED_LINEAR) return false;
+  if (p.schedule != PARAGAN_SCHED_CONSTANT && p.total_steps == 0) return false;
+  return true;
+}
+
 paragan_status validate_config(const paragan_config* c) {
   if (!c) return PARAGAN_ERR_INVALID_ARG;
   if (c->abi_version != PARAGAN_ABI_VERSION) return PARAGAN_ERR_CONFIG;
+  if (!policy_ok(c->policy_d) || !policy_ok(c->policy_g)) return PARAGAN_ERR_CONFIG;
+  for (const paragan_adam* a : {&c->adam_d, &c->adam_g})
+    if (!(a->lr >= 0.0f) || !(a->beta1 >= 0.0f && a->beta1 < 1.0f) || !(a->beta2 >= 0.0f && a->beta2 < 1.0f) ||
+        !(a->eps > 0.0f))
+      return PARAGAN_ERR_CONFIG;
   if (c->arch == PARAGAN_ARCH_SNDCGAN) {   // config 1 (R25): 32x32, fp32 SIMT path
     if (c->resolution != 32 || c->compute != PARAGAN_F32 || c->ch < 1 || c->ch % 4 || c->local_batch < 1 ||
         c->d_steps_per_g < 1 || c->world_size < 1 || c->rank < 0 || c->rank >= c->world_size || c->n_classes < 1 ||

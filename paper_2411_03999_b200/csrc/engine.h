@@ -27,6 +27,7 @@ class EngineBase {
   virtual paragan_status update(paragan_net net) = 0;
   virtual paragan_status sync_stats(paragan_stats* out) = 0;
   virtual paragan_status get_fakes(float* host, size_t n) = 0;
+  virtual paragan_status get_dfake(float* host, size_t n) = 0;
   virtual uint64_t launches() const = 0;
   virtual paragan_status profile(int enable) = 0;
   virtual paragan_status profile_read(int kind, uint64_t* n, double* ms, double* flops) = 0;

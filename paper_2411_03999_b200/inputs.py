@@ -62,3 +62,36 @@ def init_params(specs, seed: int, role: int, attn_gamma: float = 0.1, std: float
             u = r.standard_normal(s.shape[0])
             parts.append(u / np.linalg.norm(u))
     return np.concatenate(parts).astype(np.float32)
+
+
+# ---------------------------------------------------------------------------
+# Counter-based integer generator: the value of element i is a pure function of
+# (seed, i), so a test can fill a full-size tensor on the device and recompute
+# any sampled element on the host without moving the tensor.  Written with torch
+# integer ops so the SAME code runs on either device.
+# ---------------------------------------------------------------------------
+def counter_ints(idx, seed: int, lo: int, hi: int):
+    """Integers in [lo, hi] for the int64 flat indices ``idx`` (< 2**31): a 32-bit multiply-xorshift
+    hash of (seed, i).  Every product stays below 2**63."""
+    import torch
+    h = (idx * 0x9E3779B1 + (int(seed) * 0x7FEB352D + 0x165667B1)) & 0xFFFFFFFF
+    h = h ^ (h >> 15)
+    h = (h * 0x2C1B3C6D) & 0xFFFFFFFF
+    h = h ^ (h >> 12)
+    h = (h * 0x297A2D39) & 0xFFFFFFFF
+    h = h ^ (h >> 15)
+    return lo + torch.remainder(h, hi - lo + 1)
+
+
+def counter_tensor(shape, seed: int, lo: int, hi: int, device, dtype, chunk: int = 1 << 26):
+    """A tensor of ``shape`` whose flat element i is counter_ints(i, seed, lo, hi), filled in chunks."""
+    import torch
+    n = 1
+    for s in shape:
+        n *= int(s)
+    assert n < 2 ** 31
+    out = torch.empty(n, dtype=dtype, device=device)
+    for a in range(0, n, chunk):
+        b = min(n, a + chunk)
+        out[a:b] = counter_ints(torch.arange(a, b, dtype=torch.int64, device=device), seed, lo, hi).to(dtype)
+    return out.reshape(shape)

@@ -76,10 +76,38 @@ def run_gpu(cfg, g0, d0, dbs, gb, rank=0, world=1, nccl_id=None, ctx=None):
     return res
 
 
+def tensor_norm(specs, flat, name):
+    o = 0
+    for s in specs:
+        n = int(np.prod(s.shape))
+        if s.name == name:
+            return float(np.linalg.norm(np.asarray(flat[o:o + n], np.float64)))
+        o += n
+    raise KeyError(name)
+
+
 def rel(a, b):
     a = np.asarray(a, np.float64)
     b = np.asarray(b, np.float64)
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def live_mask(specs, g_plain, dead_rel=1e-9):
+    """Elements of tensors whose EXACT (fp64 oracle) gradient is non-zero.  A tensor whose exact gradient
+    vanishes identically — a conv bias feeding a batch norm (the BN removes any per-channel shift), so
+    its gradient is a sum of BN-backward outputs that cancel exactly — has no relative error: any finite
+    precision returns rounding noise there.  Such tensors are dead if their fp64 norm is below dead_rel
+    of the network's gradient norm (fp64 cancellation leaves ~1e-16 relative)."""
+    g = np.asarray(g_plain, np.float64)
+    tot = np.linalg.norm(g)
+    m = np.ones(g.size, bool)
+    o = 0
+    for s in specs:
+        n = int(np.prod(s.shape))
+        if np.linalg.norm(g[o:o + n]) <= dead_rel * tot:
+            m[o:o + n] = False
+        o += n
+    return m
 
 
 def compare_tensors(specs, got, want, tol, floor_frac=1e-2, with_u=False):

@@ -1,0 +1,109 @@
+"""The asymmetric optimisation policy on the GPU (include/paragan.h
+paragan_policy) against oracle/optim.py: AdaBelief, RAdam, SGD-momentum, Adam with LARS, Lookahead,
+global-norm clipping and the warmup / cosine / linear learning-rate ramps, applied through
+paragan_apply_update to the gradient of a real D step; and the paper's pair (AdaBelief for G, Adam
+for D, Fig. 6) through a whole iteration vs the oracle iteration."""
+import dataclasses
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import biggan as bg
+from oracle import optim as O
+from paper_2411_03999_b200 import api
+from tests import parity as P
+
+pytestmark = pytest.mark.gpu
+MICRO = dict(resolution=32, ch=4, attn_res=16, n_classes=10, shared_dim=16, z_chunk=4)
+
+CASES = {
+    "adabelief": (api.make_policy(rule=api.OPT_ADABELIEF), O.Policy(rule="adabelief")),
+    "radam": (api.make_policy(rule=api.OPT_RADAM), O.Policy(rule="radam")),
+    "sgd_momentum": (api.make_policy(rule=api.OPT_SGD), O.Policy(rule="sgd")),
+    "adam_lars": (api.make_policy(lars=True, lars_trust=0.01), O.Policy(lars=True, lars_trust=0.01)),
+    "adabelief_lookahead": (api.make_policy(rule=api.OPT_ADABELIEF, lookahead_k=3, lookahead_alpha=0.5),
+                            O.Policy(rule="adabelief", lookahead_k=3, lookahead_alpha=0.5)),
+    "adam_clip_warmup_cosine": (api.make_policy(clip_norm=0.05, warmup_steps=3, schedule=api.SCHED_COSINE,
+                                                total_steps=8),
+                                O.Policy(clip_norm=0.05, warmup_steps=3, schedule="cosine", total_steps=8)),
+    "sgd_lars_linear": (api.make_policy(rule=api.OPT_SGD, lars=True, lars_trust=0.02, schedule=api.SCHED_LINEAR,
+                                        total_steps=10),
+                        O.Policy(rule="sgd", lars=True, lars_trust=0.02, schedule="linear", total_steps=10)),
+}
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_policy_update_matches_oracle(name):
+    """Six updates of D with the same (GPU-computed) gradient: GPU weights vs oracle/optim.py in fp64.
+    The bar is on the accumulated change w_T - w_0 (relative, 2e-5: fp32 vs fp64 arithmetic of the
+    update rule only — both sides start from the same gradient)."""
+    pol, opol = CASES[name]
+    hp = (1e-3, 0.5, 0.99, 1e-8) if pol.rule != api.OPT_SGD else (1e-2, 0.9, 0.99, 1e-8)
+    cfg = api.make_config(**MICRO, local_batch=4, compute=api.F32, adam_d=hp, policy_d=pol)
+    ocfg = P.oracle_config(32, 4, 16, 10, 16, 4)
+    gs, ds, g0, d0, dbs, gb = P.make_inputs(ocfg, 4, seed=51)
+    ctx = api.Context(cfg)
+    ctx.set_params(api.NET_G, g0)
+    ctx.set_params(api.NET_D, d0)
+    real, ry, z, fy = dbs[0]
+    rp = torch.empty((4, 32, 32, 8), dtype=torch.float32, device="cuda:0")
+    api.layout_pack(torch.from_numpy(real).cuda(), rp, api.F32, 8)
+    ctx.d_step(rp, torch.from_numpy(ry).cuda(), torch.from_numpy(z).cuda(), torch.from_numpy(fy).cuda(),
+               flags=api.FLAG_NO_UPDATE)
+    g = ctx.get_grads(api.NET_D)
+    w0 = ctx.get_params(api.NET_D)
+    T = 6
+    for _ in range(T):
+        ctx.apply_update(api.NET_D)
+    st = ctx.sync_stats()
+    w1 = ctx.get_params(api.NET_D)
+    assert st.t_d == T
+    ctx.close()
+    nt = bg.n_trainable(ds)
+    params, _ = bg.unflatten(ds, w0)
+    grads, _ = bg.unflatten(ds, np.concatenate([g, np.zeros(len(w0) - nt, np.float32)]))
+    states = {k: O.State(v) for k, v in params.items()}
+    op = dataclasses.replace(opol, lr=hp[0], beta1=hp[1], beta2=hp[2], eps=hp[3])
+    for t in range(1, T + 1):
+        O.step(op, params, grads, states, t)
+    want = bg.flatten(ds, params, None)
+    dw_got, dw_want = w1[:nt].astype(np.float64) - w0[:nt], want - w0[:nt]
+    err = np.linalg.norm(dw_got - dw_want) / np.linalg.norm(dw_want)
+    print(name, f"|dw| {np.linalg.norm(dw_want):.3e} rel err {err:.2e}")
+    assert err < 2e-5
+    assert np.array_equal(w1[nt:], w0[nt:])       # u vectors are not optimiser state
+
+
+def test_invalid_policy_is_config_error():
+    for bad in (api.make_policy(rule=7), api.make_policy(lars=True, lars_trust=0.0),
+                api.make_policy(lookahead_k=2, lookahead_alpha=1.5), api.make_policy(schedule=api.SCHED_COSINE),
+                api.make_policy(clip_norm=-1.0)):
+        cfg = api.make_config(**MICRO, local_batch=2, compute=api.F32, policy_g=bad)
+        with pytest.raises(api.ParaganError) as e:
+            api.workspace_size(cfg)
+        assert e.value.status == 2
+
+
+@pytest.mark.parametrize("compute", [api.F32, api.BF16])
+def test_asymmetric_pair_adabelief_g_adam_d_iteration(compute):
+    """The paper's best pair (Fig. 6: AdaBelief for G, Adam for D) through a full iteration vs the oracle
+    iteration with the same policies (fp32: 1e-4; bf16: 2e-2 vs the R14-emulating oracle).  With beta1 = 0
+    AdaBelief's first step is proportional to g (Adam's is ~ lr sign g), so in fp32 G's update itself is
+    also held to 1e-3."""
+    bf = compute == api.BF16
+    tol = 2e-2 if bf else 1e-4
+    ocfg = dataclasses.replace(P.oracle_config(32, 4, 16, 10, 16, 4, bf16=bf),
+                               policy_g=O.Policy(rule="adabelief"), policy_d=O.Policy(rule="adam"))
+    cfg = api.make_config(**MICRO, local_batch=4, compute=compute, policy_g=api.make_policy(rule=api.OPT_ADABELIEF))
+    gs, ds, g0, d0, dbs, gb = P.make_inputs(ocfg, 4, seed=52)
+    want = P.run_oracle(ocfg, gs, ds, g0, d0, dbs, gb)
+    got = P.run_gpu(cfg, g0, d0, dbs, gb)
+    for key, specs in (("g_state", gs), ("d_state", ds)):
+        nt = bg.n_trainable(specs)
+        p0 = (g0 if key == "g_state" else d0)[:nt].astype(np.float64)
+        e = P.rel(got[key][:nt] - p0, want[key][:nt] - p0)
+        print(key, f"update rel err {e:.2e}")
+        assert P.rel(got[key][:nt], want[key][:nt]) < tol
+        if not bf and key == "g_state":
+            assert e < 1e-3

@@ -194,3 +194,71 @@ def test_sndcgan_parameter_counts_and_deconv_adjoint():
     lhs = (torch.nn.functional.conv_transpose2d(x, w, stride=2, padding=1) * y).sum()
     rhs = (x * torch.nn.functional.conv2d(y, w, stride=2, padding=1)).sum()
     assert abs(float(lhs - rhs)) < 1e-10 * abs(float(lhs))
+
+
+def _bf16_exact(t: torch.Tensor) -> bool:
+    t = t.detach()
+    return bool(torch.equal(ops.bf16_round(t), t))
+
+
+@pytest.mark.parametrize("bf16", [True, False])
+def test_bf16_emulation_obeys_the_storage_rule(monkeypatch, bf16):
+    """Pin of the oracle's bf16 mode (R14) by the rule itself, independent of any
+    kernel: every tensor-core product of the step (each conv and each attention bmm) reads bf16
+    operands in the forward, and the output gradient its backward reads (the dgrad/wgrad operand) is
+    bf16 — except G's output conv, which is fp32 by P:202.  A dropped or misplaced q()/qv()/qg()
+    breaks one of these.  The fp64 mode (bf16=False) must violate it (the check is not vacuous), and
+    the emulation moves the losses by a bf16-sized amount, not zero and not more."""
+    cfg = bg.Config(**MICRO, bf16=bf16)
+    G, D, real, ry, z, fy = _setup(cfg, 3, seed=5)
+    seen = {"fwd": 0, "bad_fwd": [], "bwd": 0, "bad_bwd": []}
+    real_conv, real_bmm = ops.conv2d, torch.bmm
+
+    def watch(name, out):
+        def hook(g):
+            seen["bwd"] += 1
+            if not _bf16_exact(g):
+                seen["bad_bwd"].append(name)
+        if out.requires_grad:
+            out.register_hook(hook)
+        return out
+
+    def conv(x, w, b):
+        out = real_conv(x, w, b)
+        if w.shape[0] == 3 and w.shape[-1] == 3 and x.shape[1] == cfg.ch * 1 * 1 * \
+                bg._G_ARCH[cfg.resolution][1][-1]:
+            return out                                  # G's output conv: fp32 (P:202)
+        seen["fwd"] += 1
+        if not (_bf16_exact(x) and _bf16_exact(w)):
+            seen["bad_fwd"].append(("conv", tuple(w.shape)))
+        if w.shape[-1] == 1 and 2 * w.shape[1] == w.shape[0] and x.shape[1] == w.shape[1] \
+                and cfg.attn_res == x.shape[-1]:
+            return out      # attention o conv: its epilogue scales by gamma, so its input gradient is gamma x bf16
+        return watch(("conv", tuple(w.shape)), out)
+
+    def bmm(a, b):
+        out = real_bmm(a, b)
+        seen["fwd"] += 1
+        if not (_bf16_exact(a) and _bf16_exact(b)):
+            seen["bad_fwd"].append(("bmm", tuple(a.shape)))
+        return watch(("bmm", tuple(a.shape)), out)
+
+    monkeypatch.setattr(ops, "conv2d", conv)
+    monkeypatch.setattr(bg.torch, "bmm", bmm)
+    out_d = bg.d_step(cfg, G, D, real, ry, z, fy)
+    out_g = bg.g_step(cfg, G, D, z, fy)
+    monkeypatch.undo()
+    n_conv_d = sum(1 for s in bg.d_param_specs(cfg) if len(s.shape) == 4)
+    assert seen["fwd"] >= n_conv_d + 2 and seen["bwd"] >= n_conv_d
+    if bf16:
+        assert not seen["bad_fwd"], seen["bad_fwd"][:5]
+        assert not seen["bad_bwd"], seen["bad_bwd"][:5]
+        # against the fp64 step from the same state: a bf16-sized, non-zero change of the losses
+        cfg64 = bg.Config(**MICRO, bf16=False)
+        G2, D2, real, ry, z, fy = _setup(cfg64, 3, seed=5)
+        ref_d = bg.d_step(cfg64, G2, D2, real, ry, z, fy)
+        ref_g = bg.g_step(cfg64, G2, D2, z, fy)
+        for a, b in ((out_d["loss"], ref_d["loss"]), (out_g["loss"], ref_g["loss"])):
+            assert 0 < abs(a - b) / abs(b) < 2e-2
+    else:
+        assert seen["bad_fwd"] and seen["bad_bwd"]

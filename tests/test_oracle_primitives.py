@@ -336,7 +336,7 @@ def test_up2_conv_phase_decomposition_is_conv_of_upsampled():
     w = torch.from_numpy(rng.standard_normal((4, 3, 3, 3))).requires_grad_(True)
     b = torch.from_numpy(rng.standard_normal(4))
     dy = torch.from_numpy(rng.standard_normal((2, 4, 10, 8)))
-    y1 = ops.up2_conv3x3_phases(x, w, b, bf16=False)
+    y1 = ops.up2_conv3x3_phases(x, w, b)
     y2 = ops.conv2d(ops.up2(x), w, b)
     assert torch.allclose(y1, y2, rtol=1e-12, atol=1e-12)
     g1 = torch.autograd.grad((y1 * dy).sum(), (x, w))
@@ -347,6 +347,66 @@ def test_up2_conv_phase_decomposition_is_conv_of_upsampled():
     # lights the 4x4 high-resolution block the 3x3 kernel over the 2x2 replicated pixel covers
     xd = torch.zeros(1, 1, 4, 4, dtype=torch.float64)
     xd[0, 0, 1, 2] = 1.0
-    yd = ops.up2_conv3x3_phases(xd, torch.ones(1, 1, 3, 3, dtype=torch.float64), None, bf16=False)
+    yd = ops.up2_conv3x3_phases(xd, torch.ones(1, 1, 3, 3, dtype=torch.float64), None)
     nz = torch.nonzero(yd[0, 0]).tolist()
     assert sorted({r for r, _ in nz}) == [1, 2, 3, 4] and sorted({c for _, c in nz}) == [3, 4, 5, 6]
+
+
+# ------------------------------------------------- sampled conv definitions (oracle/sampled.py)
+def test_sampled_conv_definitions_match_full_oracle():
+    """oracle/sampled.py (used by the full-size GPU tests) against the full fp64 conv of ops.conv2d and
+    its autograd at every output element of small ragged shapes, epilogue terms included."""
+    from oracle import sampled as S
+    rng = np.random.default_rng(0)
+    for (n, H, W, cin, cout, k) in [(2, 5, 7, 3, 4, 3), (1, 4, 4, 6, 5, 1), (3, 6, 3, 2, 3, 3)]:
+        x = rng.integers(-2, 3, size=(n, H, W, cin)).astype(np.float64)
+        w = rng.integers(-1, 2, size=(cout, k * k, cin)).astype(np.float64)
+        b = rng.integers(-3, 4, size=cout).astype(np.float64)
+        ref = rng.integers(-1, 2, size=(n, H, W, cout)).astype(np.float64)
+        res = rng.integers(-2, 3, size=(n, H, W, cout)).astype(np.float64)
+        wt = torch.from_numpy(w).reshape(cout, k, k, cin).permute(0, 3, 1, 2)
+        xt = torch.from_numpy(x).permute(0, 3, 1, 2)
+        conv = ops.conv2d(xt, wt, None).permute(0, 2, 3, 1).numpy()
+        want = np.maximum(np.where(ref > 0, conv, 0.0) + b + res, 0.0)
+        nn, ii, jj = (a.ravel() for a in np.meshgrid(np.arange(n), np.arange(H), np.arange(W), indexing="ij"))
+        got = S.conv_fprop_at(lambda a, i, j: x[a, i, j], H, W, cin, w, k, nn, ii, jj, bias=b,
+                              relu_ref_at=lambda a, i, j: ref[a, i, j], residual_at=lambda a, i, j: res[a, i, j],
+                              relu_out=True)
+        assert np.array_equal(got.reshape(n, H, W, cout), want)
+        dy = rng.integers(-2, 3, size=(n, H, W, cout)).astype(np.float64)
+        wv = torch.zeros(cout, cin, k, k, dtype=torch.float64, requires_grad=True)
+        (gw,) = torch.autograd.grad((ops.conv2d(xt, wv, None) * torch.from_numpy(dy).permute(0, 3, 1, 2)).sum(), wv)
+        gw = gw.permute(0, 2, 3, 1).reshape(cout, k * k, cin).numpy()
+        cs, os_ = [0, cin - 1], [cout - 1, 0]
+        assert np.array_equal(S.conv_wgrad_at(x[..., cs], dy[..., os_], H, W, k), gw[os_][:, :, cs])
+    # G's conv1 on the upsampled input: forward, low-resolution input gradient, weight gradient
+    n, h, w_, cin, cout = 2, 3, 4, 3, 5
+    x = rng.integers(-2, 3, size=(n, h, w_, cin)).astype(np.float64)
+    w = rng.integers(-1, 2, size=(cout, 9, cin)).astype(np.float64)
+    b = rng.integers(-3, 4, size=cout).astype(np.float64)
+    xt = torch.from_numpy(x).permute(0, 3, 1, 2).requires_grad_(True)
+    wt = torch.from_numpy(w).reshape(cout, 3, 3, cin).permute(0, 3, 1, 2).contiguous().requires_grad_(True)
+    y = ops.conv2d(ops.up2(xt), wt, torch.from_numpy(b))
+    dy = rng.integers(-2, 3, size=tuple(y.shape)).astype(np.float64)
+    gx, gw = torch.autograd.grad((y * torch.from_numpy(dy)).sum(), (xt, wt))
+    nn, ii, jj = (a.ravel() for a in np.meshgrid(np.arange(n), np.arange(2 * h), np.arange(2 * w_), indexing="ij"))
+    got = S.up2_conv3x3_fprop_at(lambda a, i, j: x[a, i, j], h, w_, cin, w, nn, ii, jj, bias=b)
+    assert np.array_equal(got.reshape(n, 2 * h, 2 * w_, cout), y.detach().permute(0, 2, 3, 1).numpy())
+    dyn = dy.transpose(0, 2, 3, 1)
+    nn, ii, jj = (a.ravel() for a in np.meshgrid(np.arange(n), np.arange(h), np.arange(w_), indexing="ij"))
+    got = S.up2_conv3x3_dgrad_at(lambda a, i, j: dyn[a, i, j], h, w_, cout, w, nn, ii, jj)
+    assert np.array_equal(got.reshape(n, h, w_, cin), gx.permute(0, 2, 3, 1).numpy())
+    gwn = gw.permute(0, 2, 3, 1).reshape(cout, 9, cin).numpy()
+    assert np.array_equal(S.up2_conv3x3_wgrad_at(x, dyn, h, w_), gwn)
+
+
+def test_counter_generator_same_on_any_slice():
+    """The counter-based generator the full-size tests share: element i depends only on (seed, i)
+    (chunked fill == direct evaluation), values cover [lo, hi] roughly uniformly."""
+    from paper_2411_03999_b200.inputs import counter_ints, counter_tensor
+    t = counter_tensor((3, 5, 7, 11), 9, -1, 1, "cpu", torch.float32, chunk=97)
+    direct = counter_ints(torch.arange(t.numel(), dtype=torch.int64), 9, -1, 1).reshape(t.shape).float()
+    assert torch.equal(t, direct)
+    v = counter_ints(torch.arange(30000, dtype=torch.int64), 3, 0, 2)
+    counts = torch.bincount(v, minlength=3).numpy()
+    assert counts.min() > 9000 and v.min() == 0 and v.max() == 2

@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--bf16", action="store_true")
     ap.add_argument("--summary", action="store_true")
     ap.add_argument("--d-only", action="store_true", help="D step alone, oracle fed the GPU's fake images")
+    ap.add_argument("--g-isolated", action="store_true", help="G step alone, oracle fed the GPU's dL/dfake")
     a = ap.parse_args()
     import numpy as np
     from paper_2411_03999_b200 import api
@@ -31,6 +32,11 @@ def main():
     compute = api.BF16 if a.bf16 else api.F32
     cfg = api.make_config(resolution=a.res, ch=a.ch, attn_res=a.attn, n_classes=a.classes, shared_dim=a.shared,
                           z_chunk=a.zc, local_batch=a.batch, compute=compute)
+    if a.g_isolated:
+        import numpy as np
+        from tests import test_gpu_step as T
+        T._g_isolated(a.res, a.ch, a.attn, a.classes, a.shared, a.zc, a.batch, a.seed, compute, verbose=True)
+        return
     if a.d_only:
         import torch
         from oracle import biggan as bg
@@ -70,6 +76,12 @@ def main():
     print("fake rel err vs " + " ".join(f"emu={k}: {P.rel(got['fake'], v['fake']):.2e}" for k, v in res.items()))
     print("d_grads global " + " ".join(f"emu={k}: {P.rel(got['d_grads'], v['d_grads']):.2e}" for k, v in res.items()))
     print("g_grads global " + " ".join(f"emu={k}: {P.rel(got['g_grads'], v['g_grads']):.2e}" for k, v in res.items()))
+    ref = res[False]
+    for key, specs in (("d_grads", ds), ("g_grads", gs)):
+        live = P.live_mask(specs, ref[key])
+        print(f"{key} global over live tensors (exact gradient non-zero, {live.mean():.4f} of elements): " +
+              " ".join(f"emu={k}: {P.rel(got[key][live], v[key][live]):.2e}" for k, v in res.items()) +
+              f"; dead-tensor noise |gpu| / |g| = {np.linalg.norm(got[key][~live]) / np.linalg.norm(ref[key]):.2e}")
     if a.summary:
         return
     for key, specs in (("d_grads", ds), ("g_grads", gs)):
@@ -83,7 +95,8 @@ def main():
             extra = ""
             if len(res) == 2:
                 extra = f" | {P.rel(res[True][key][o:o + n], res[False][key][o:o + n]):.2e}"
-            print(f"  {s.name:22s} " + " ".join(f"{r:.2e}" for r in row) + extra)
+            nrm = np.linalg.norm(res[False][key][o:o + n]) / np.linalg.norm(res[False][key])
+            print(f"  {s.name:22s} " + " ".join(f"{r:.2e}" for r in row) + extra + f" | norm share {nrm:.2e}")
             o += n
 
 
