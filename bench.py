@@ -154,6 +154,85 @@ def _traffic():
     return d
 
 
+def run_async(args):
+    """The asynchronous update scheme on N = 2k GPUs: G steps on ranks [0, k),
+    D steps on ranks [k, 2k) (paper_2411_03999_b200/async_gan.DistributedAsync), staleness 1, G batch
+    --g-batch per G rank, D batch --batch per D rank (n_d = g_batch / d_batch D steps per tick).  Images/s
+    counts the images G trains on (k * g_batch per tick); the D side's real images/s is reported next to it."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2411_03999_b200 import api, inputs
+    from paper_2411_03999_b200.async_gan import DistributedAsync
+
+    world, rank, local = _dist()
+    assert world >= 2 and world % 2 == 0, "--async needs an even number of GPUs"
+    torch.cuda.set_device(local)
+    dev = f"cuda:{local}"
+    dist.init_process_group("nccl", device_id=torch.device(dev))
+    R, gb_, db_ = args.res, args.g_batch or args.batch, args.batch
+    n_d = gb_ // db_
+
+    def make_cfg(b, r, w):
+        return api.make_config(resolution=R, local_batch=b, d_steps_per_g=n_d, compute=api.BF16, rank=r,
+                               world_size=w, device=local, seed=1234)
+
+    da = DistributedAsync(make_cfg, gb_, db_, n_d)
+    da.init_params(0.1)
+    dz = api.dim_z(da.cfg)
+    if da.is_g:
+        pool = [inputs.latent_batch(3000 + i, inputs.ROLE_Z_G, da.grank, gb_, dz, 1000) for i in range(4)]
+        pool = [(torch.from_numpy(z).to(dev), torch.from_numpy(y).to(dev)) for z, y in pool]
+    else:
+        pool = []
+        for i in range(4):
+            ent = []
+            for k in range(n_d):
+                real, ry = inputs.real_batch(3000 + i, da.grank * n_d + k, db_, R, 1000)
+                rp = torch.empty((db_, R, R, 8), dtype=torch.bfloat16, device=dev)
+                api.layout_pack(torch.from_numpy(real).to(dev), rp, api.BF16, 8)
+                ent.append((rp, torch.from_numpy(ry).to(dev)))
+            pool.append(ent)
+
+    def tick(i):
+        if da.is_g:
+            da.tick(g_batch=pool[i % 4], boot=pool[0])
+        else:
+            da.tick(d_batches=pool[i % 4])
+
+    for i in range(args.warmup):
+        tick(i)
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(args.steps):
+        tick(args.warmup + i)
+    e1.record()
+    torch.cuda.synchronize()
+    dist.barrier()
+    t = torch.tensor([e0.elapsed_time(e1)], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    k = world // 2
+    value = k * gb_ * args.steps / (ms / 1000.0)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                          "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+                          "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+                          "config": {"workload": f"BigGAN-{R} asynchronous update scheme (P:266-282): G on {k} "
+                                                 f"GPUs x {gb_}, D on {k} GPUs x {db_} x n_d={n_d}, staleness 1",
+                                     "model": f"BigGAN-{R} ch=96", "g_batch_per_gpu": gb_, "d_batch_per_gpu": db_,
+                                     "parallelism": f"G dp{k} + D dp{k}"},
+                          "d_real_img_per_s": k * db_ * n_d * args.steps / (ms / 1000.0),
+                          "note": "a tick = one G step (G group) concurrent with n_d D steps (D group)"}),
+              flush=True)
+    da.close()
+    dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -164,6 +243,9 @@ def main():
     ap.add_argument("--res", type=int, default=128)
     ap.add_argument("--d-steps", type=int, default=1)
     ap.add_argument("--repeats", type=int, default=3, help="timed repeats of K steps; the median is reported")
+    ap.add_argument("--async", dest="async_", action="store_true",
+                    help="asynchronous update scheme (P:266-282): G and D on disjoint halves of the GPUs")
+    ap.add_argument("--g-batch", type=int, default=0, help="--async: G batch per G rank (default --batch)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
@@ -173,6 +255,8 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.async_:
+        return run_async(args)
     assert args.warmup >= 3 or os.environ.get("PARAGAN_ALLOW_SHORT_WARMUP"), "timing rules need >= 3 warm-up steps"
 
     import numpy as np

@@ -113,6 +113,9 @@ typedef struct {
   uint64_t seed;         /* on-device weight init (paragan_init_params) */
   int32_t arch;          /* a paragan_arch value; field added in ABI 2 */
   paragan_policy policy_d, policy_g;   /* ABI 3 */
+  int32_t grad_comm_bf16; /* 1 = gradient all-reduce in bf16 (half the NVLink bytes, "faster to ...
+                           * communicate"); 0 = fp32 (default; exact integer sums, bit-identical replicas
+                           * either way) */
 } paragan_config;
 
 typedef struct {
@@ -155,6 +158,9 @@ paragan_status paragan_init_params(paragan_ctx* ctx, float attn_gamma);
 paragan_status paragan_set_params(paragan_ctx* ctx, paragan_net net, const float* host, size_t n);
 paragan_status paragan_get_params(paragan_ctx* ctx, paragan_net net, float* host, size_t n);
 paragan_status paragan_get_grads(paragan_ctx* ctx, paragan_net net, float* host, size_t n);
+/* Test hook: overwrite the net's local gradient buffer with a canonical-layout host array (n_trainable
+ * floats), as if this rank's backward had produced it (the next paragan_allreduce_grads sums it). */
+paragan_status paragan_set_grads(paragan_ctx* ctx, paragan_net net, const float* host, size_t n);
 
 /* --------------------------------------------------------------- hot path */
 
@@ -183,6 +189,29 @@ paragan_status paragan_d_step(paragan_ctx* ctx, const void* real_nhwc, const int
  * backward through D (inputs only) and G -> all-reduce -> Adam(G).
  * Returns PARAGAN_ERR_ORDER unless d_steps_per_g D steps preceded it. */
 paragan_status paragan_g_step(paragan_ctx* ctx, const float* z, const int32_t* y, uint32_t flags);
+
+/* ---------------------------------------------- asynchronous update scheme (Sec. 5.1)
+ * "instead of waiting on the other component, the generator/discriminator can write their intermediate
+ * output to the buffer and proceed to update using the current state of the network.  For iteration t,
+ * discriminators D_t receive a batch of real and generated samples from the image buffer (img_buff).
+ * Similarly, the generators can use the snapshot of the current discriminator state ... breaking the data
+ * dependency."  The library provides the per-side steps; the buffers and the placement of G and D on
+ * disjoint GPU groups live in paper_2411_03999_b200/async_gan.py (R31-R33). */
+
+/* D step on GIVEN fakes (an img_buff entry): no SN(G) / G forward.  fakes_nhwc: device, [B,R,R,c_pad] in
+ * the compute dtype (as paragan_generate / paragan_export_fakes write them).  Otherwise as paragan_d_step. */
+paragan_status paragan_d_step_fakes(paragan_ctx* ctx, const void* real_nhwc, const int32_t* real_y,
+                                    const void* fakes_nhwc, const int32_t* fake_y, uint32_t flags);
+/* G forward only (SN(G) power step + cross-replica BN, as in the D step): fakes for img_buff, written to
+ * dst_nhwc (device, [B,R,R,c_pad], compute dtype). */
+paragan_status paragan_generate(paragan_ctx* ctx, const float* z, const int32_t* y, void* dst_nhwc);
+/* Copy the last generated images (the last G step's or D step's fakes) to dst_nhwc (device, as above). */
+paragan_status paragan_export_fakes(paragan_ctx* ctx, void* dst_nhwc);
+/* Device-to-device snapshot of a network's state (the D snapshot G uses): dst/src device fp32 buffers of
+ * paragan_param_count n_state floats in the library's INTERNAL layout (weights then u vectors; only
+ * meaningful between contexts of the same config).  import resets nothing else (Adam state stays). */
+paragan_status paragan_export_state(paragan_ctx* ctx, paragan_net net, float* dst_device);
+paragan_status paragan_import_state(paragan_ctx* ctx, paragan_net net, const float* src_device);
 
 /* In-place SUM of the net's gradient over all ranks (NCCL all-reduce over
  * NVLink); the mean's 1/world_size is folded into the update
@@ -231,6 +260,8 @@ paragan_status paragan_destroy(paragan_ctx* ctx);
 #define PARAGAN_FLAG_NO_ALLREDUCE 1u /* keep the local gradient (test hook) */
 #define PARAGAN_FLAG_NO_UPDATE 2u    /* skip Adam (test hook) */
 #define PARAGAN_FLAG_KEEP_DFAKE 4u   /* g_step keeps dL_G/d(fake images) for paragan_get_dfake (test hook) */
+#define PARAGAN_FLAG_ASYNC 8u        /* g_step in the asynchronous scheme: no D steps precede it in this
+                                      * context (it trains through an imported D snapshot) */
 
 /* ------------------------------------------------------- op-level test hooks
  * Single kernels of the path, exposed so tests can compare each with the

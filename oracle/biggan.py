@@ -394,24 +394,30 @@ def pack_real(cfg: Config, real_nchw: np.ndarray) -> torch.Tensor:
 
 
 def d_step(cfg: Config, G: NetState, D: NetState, real, real_y, z, fake_y, update: bool = True,
-           fake_override=None) -> dict:
+           fake_override=None, fakes=None) -> dict:
     """One D step: SN(G), G forward (no grad), SN(D), D([fake; real]),
     hinge L_D, backward through D, Adam on D.  ``fake_override`` (test hook) replaces the
-    generated images so D's own arithmetic can be compared in isolation."""
+    generated images so D's own arithmetic can be compared in isolation.  ``fakes`` (the
+    asynchronous scheme: D reads its generated batch from img_buff) skips SN(G) and
+    the G forward entirely (G may be None)."""
     real = pack_real(cfg, real)
     real_y = torch.as_tensor(np.asarray(real_y), dtype=torch.long)
     fake_y = torch.as_tensor(np.asarray(fake_y), dtype=torch.long)
-    z = torch.as_tensor(np.asarray(z, dtype=np.float32)).to(F64)
-    sng = _SN(G.specs, G.params, G.us, cfg.sn_eps, cfg.bf16)
-    with torch.no_grad():
-        fake = g_forward(cfg, sng, z, fake_y)
+    if fakes is not None:
+        fake = torch.as_tensor(np.asarray(fakes, dtype=np.float64))
+        sng = None
+    else:
+        z = torch.as_tensor(np.asarray(z, dtype=np.float32)).to(F64)
+        sng = _SN(G.specs, G.params, G.us, cfg.sn_eps, cfg.bf16)
+        with torch.no_grad():
+            fake = g_forward(cfg, sng, z, fake_y)
     if fake_override is not None:
         fake = torch.as_tensor(np.asarray(fake_override, dtype=np.float64))
     fake = q(fake, cfg.bf16)
     dparams = {k: v.detach().requires_grad_(True) for k, v in D.params.items()}
     snd = _SN(D.specs, dparams, D.us, cfg.sn_eps, cfg.bf16)
     logits = d_forward(cfg, snd, torch.cat([fake, real], 0), torch.cat([fake_y, real_y], 0))
-    B = z.shape[0]
+    B = fake.shape[0]
     l_fake, l_real = logits[:B], logits[B:]
     loss = ops.hinge_d(l_real, l_fake)
     names = [s.name for s in D.specs]
@@ -421,7 +427,7 @@ def d_step(cfg: Config, G: NetState, D: NetState, real, real_y, z, fake_y, updat
     ok = _adam(D, grads, cfg.adam_d, cfg.policy_d) if update else True
     return dict(loss=float(loss.detach()), logits=logits.detach().numpy(), fake=fake.detach().numpy(),
                 grads=D.grad_flat(grads), applied=ok,
-                sigma_g=dict(sng.sigma), sigma_d=dict(snd.sigma),
+                sigma_g=dict(sng.sigma) if sng is not None else {}, sigma_d=dict(snd.sigma),
                 d_real_mean=float(l_real.detach().mean()), d_fake_mean=float(l_fake.detach().mean()))
 
 

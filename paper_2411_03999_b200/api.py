@@ -17,7 +17,7 @@ PARAGAN_ABI_VERSION = 3
 F32, BF16 = 0, 1
 ARCH_BIGGAN, ARCH_SNDCGAN = 0, 1
 NET_D, NET_G = 0, 1
-FLAG_NO_ALLREDUCE, FLAG_NO_UPDATE, FLAG_KEEP_DFAKE = 1, 2, 4
+FLAG_NO_ALLREDUCE, FLAG_NO_UPDATE, FLAG_KEEP_DFAKE, FLAG_ASYNC = 1, 2, 4, 8
 STATUS = {0: "OK", 1: "INVALID_ARG", 2: "CONFIG", 3: "NONFINITE", 4: "IO", 5: "CUDA", 6: "NCCL", 7: "ORDER", 8: "OOM"}
 
 
@@ -49,7 +49,7 @@ class Config(C.Structure):
                 ("compute", C.c_int32), ("c_pad_image", C.c_int32), ("adam_d", Adam), ("adam_g", Adam),
                 ("sn_eps", C.c_float), ("bn_eps", C.c_float), ("rank", C.c_int32), ("world_size", C.c_int32),
                 ("device", C.c_int32), ("seed", C.c_uint64), ("arch", C.c_int32), ("policy_d", Policy),
-                ("policy_g", Policy)]
+                ("policy_g", Policy), ("grad_comm_bf16", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -74,12 +74,18 @@ SYMBOLS = {
     "paragan_set_params": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_size_t]),
     "paragan_get_params": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_size_t]),
     "paragan_get_grads": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_size_t]),
+    "paragan_set_grads": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_size_t]),
     "paragan_layout_pack": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                       C.c_int32, C.c_void_p]),
     "paragan_layout_unpack": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
                                         C.c_int32, C.c_int32, C.c_void_p]),
     "paragan_d_step": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32]),
     "paragan_g_step": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32]),
+    "paragan_d_step_fakes": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32]),
+    "paragan_generate": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "paragan_export_fakes": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "paragan_export_state": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
+    "paragan_import_state": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
     "paragan_allreduce_grads": (C.c_int, [C.c_void_p, C.c_int]),
     "paragan_apply_update": (C.c_int, [C.c_void_p, C.c_int]),
     "paragan_sync_stats": (C.c_int, [C.c_void_p, C.POINTER(Stats)]),
@@ -152,7 +158,7 @@ def _stream(stream):
 def make_config(resolution=128, ch=96, n_classes=1000, shared_dim=128, z_chunk=20, attn_res=64, local_batch=256,
                 d_steps_per_g=1, compute=BF16, c_pad_image=8, adam_d=(2e-4, 0.0, 0.999, None),
                 adam_g=(5e-5, 0.0, 0.999, None), sn_eps=1e-12, bn_eps=1e-5, rank=0, world_size=1, device=0,
-                seed=0, arch=0, policy_d=None, policy_g=None) -> Config:
+                seed=0, arch=0, policy_d=None, policy_g=None, grad_comm_bf16=False) -> Config:
     """BigGAN config; Adam eps defaults to 1e-6 under bf16 and 1e-8 in fp32.
     policy_d / policy_g: paragan_policy (make_policy); None = plain Adam."""
     eps = 1e-6 if compute == BF16 else 1e-8
@@ -160,7 +166,7 @@ def make_config(resolution=128, ch=96, n_classes=1000, shared_dim=128, z_chunk=2
     ag = Adam(adam_g[0], adam_g[1], adam_g[2], adam_g[3] if adam_g[3] is not None else eps)
     return Config(PARAGAN_ABI_VERSION, resolution, ch, n_classes, shared_dim, z_chunk, attn_res, local_batch,
                   d_steps_per_g, compute, c_pad_image, ad, ag, sn_eps, bn_eps, rank, world_size, device, seed, arch,
-                  policy_d or make_policy(), policy_g or make_policy())
+                  policy_d or make_policy(), policy_g or make_policy(), 1 if grad_comm_bf16 else 0)
 
 
 def make_sndcgan_config(ch=32, n_classes=10, local_batch=8, d_steps_per_g=1, **kw) -> Config:
@@ -317,6 +323,12 @@ class Context:
         _check("paragan_get_grads", lib().paragan_get_grads(self.ctx, net, a.ctypes.data, a.size), self.ctx)
         return a
 
+    def set_grads(self, net, flat):
+        """Test hook: this rank's local gradient (canonical layout, n_trainable floats)."""
+        import numpy as np
+        a = np.ascontiguousarray(flat, dtype=np.float32)
+        _check("paragan_set_grads", lib().paragan_set_grads(self.ctx, net, a.ctypes.data, a.size), self.ctx)
+
     def get_fakes(self):
         import numpy as np
         r = self.cfg.resolution
@@ -338,6 +350,22 @@ class Context:
 
     def g_step(self, z, y, flags=0):
         _check("paragan_g_step", lib().paragan_g_step(self.ctx, _ptr(z), _ptr(y), flags), self.ctx)
+
+    def d_step_fakes(self, real_nhwc, real_y, fakes_nhwc, fake_y, flags=0):
+        _check("paragan_d_step_fakes", lib().paragan_d_step_fakes(self.ctx, _ptr(real_nhwc), _ptr(real_y),
+                                                                  _ptr(fakes_nhwc), _ptr(fake_y), flags), self.ctx)
+
+    def generate(self, z, y, dst_nhwc):
+        _check("paragan_generate", lib().paragan_generate(self.ctx, _ptr(z), _ptr(y), _ptr(dst_nhwc)), self.ctx)
+
+    def export_fakes(self, dst_nhwc):
+        _check("paragan_export_fakes", lib().paragan_export_fakes(self.ctx, _ptr(dst_nhwc)), self.ctx)
+
+    def export_state(self, net, dst):
+        _check("paragan_export_state", lib().paragan_export_state(self.ctx, net, _ptr(dst)), self.ctx)
+
+    def import_state(self, net, src):
+        _check("paragan_import_state", lib().paragan_import_state(self.ctx, net, _ptr(src)), self.ctx)
 
     def allreduce_grads(self, net):
         _check("paragan_allreduce_grads", lib().paragan_allreduce_grads(self.ctx, net), self.ctx)

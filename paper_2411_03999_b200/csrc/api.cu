@@ -96,6 +96,11 @@ paragan_status paragan_get_grads(paragan_ctx* ctx, paragan_net net, float* host,
   return ctx->eng->get_grads(net, host, n);
 }
 
+paragan_status paragan_set_grads(paragan_ctx* ctx, paragan_net net, const float* host, size_t n) {
+  if (!ctx || !ctx->eng) return PARAGAN_ERR_INVALID_ARG;
+  return ctx->eng->set_grads(net, host, n);
+}
+
 paragan_status paragan_layout_pack(const float* src, void* dst, paragan_dtype dt, int32_t n, int32_t c, int32_t h,
                                    int32_t w, int32_t c_pad, void* stream) {
   if (!src || !dst || n < 0 || c < 1 || h < 1 || w < 1 || c_pad < c) return PARAGAN_ERR_INVALID_ARG;
@@ -126,6 +131,27 @@ paragan_status paragan_d_step(paragan_ctx* ctx, const void* real, const int32_t*
 paragan_status paragan_g_step(paragan_ctx* ctx, const float* z, const int32_t* y, uint32_t flags) {
   if (!ctx || !ctx->eng) return PARAGAN_ERR_INVALID_ARG;
   return ctx->eng->g_step(z, y, flags);
+}
+paragan_status paragan_d_step_fakes(paragan_ctx* ctx, const void* real, const int32_t* real_y, const void* fakes,
+                                    const int32_t* fake_y, uint32_t flags) {
+  if (!ctx || !ctx->eng) return PARAGAN_ERR_INVALID_ARG;
+  return ctx->eng->d_step_fakes(real, real_y, fakes, fake_y, flags);
+}
+paragan_status paragan_generate(paragan_ctx* ctx, const float* z, const int32_t* y, void* dst) {
+  if (!ctx || !ctx->eng || !dst || !aligned16(dst)) return PARAGAN_ERR_INVALID_ARG;
+  return ctx->eng->generate(z, y, dst);
+}
+paragan_status paragan_export_fakes(paragan_ctx* ctx, void* dst) {
+  if (!ctx || !ctx->eng || !dst) return PARAGAN_ERR_INVALID_ARG;
+  return ctx->eng->export_fakes(dst);
+}
+paragan_status paragan_export_state(paragan_ctx* ctx, paragan_net net, float* dst) {
+  if (!ctx || !ctx->eng || !dst || (net != PARAGAN_NET_D && net != PARAGAN_NET_G)) return PARAGAN_ERR_INVALID_ARG;
+  return ctx->eng->export_state(net, dst);
+}
+paragan_status paragan_import_state(paragan_ctx* ctx, paragan_net net, const float* src) {
+  if (!ctx || !ctx->eng || !src || (net != PARAGAN_NET_D && net != PARAGAN_NET_G)) return PARAGAN_ERR_INVALID_ARG;
+  return ctx->eng->import_state(net, src);
 }
 paragan_status paragan_allreduce_grads(paragan_ctx* ctx, paragan_net net) {
   if (!ctx || !ctx->eng || (net != PARAGAN_NET_D && net != PARAGAN_NET_G)) return PARAGAN_ERR_INVALID_ARG;

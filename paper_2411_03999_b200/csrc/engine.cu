@@ -86,6 +86,7 @@ struct Net {
   float* clip_scale = nullptr;
   float* slow = nullptr;   // Lookahead phi (only when enabled)
   float gsum = 1.0f;       // ranks summed into g by the last all-reduce (1/gsum = the mean's factor)
+  bf16* g16 = nullptr;     // bf16 wire copy of g (grad_comm_bf16 with world_size > 1)
   int add(const std::string& name, std::vector<int> shape, bool conv4d, bool sn) {
     PEntry e;
     e.name = name;
@@ -342,6 +343,20 @@ class Engine final : public EngineBase {
     if (!host || n != (size_t)N.n) return fail_arg("get_grads: size mismatch");
     return export_flat(N, N.g, host, false, 1.0f / N.gsum);
   }
+  paragan_status set_grads(paragan_net net, const float* host, size_t n) override {
+    if (!ready_ || poisoned_) return PARAGAN_ERR_ORDER;
+    Net& N = net == PARAGAN_NET_D ? D_ : G_;
+    if (!host || n != (size_t)N.n) return fail_arg("set_grads: size mismatch");
+    // canonical -> staging -> internal layout (conv OIHW -> OHWI), as set_params
+    if (cudaMemcpyAsync(scratch_f_, host, sizeof(float) * N.n, cudaMemcpyHostToDevice, st_) != cudaSuccess)
+      return fail_cuda(cudaGetLastError(), "set_grads copy");
+    for (const PEntry& e : N.E) {
+      if (e.conv4d) CK(oihw_to_ohwi(scratch_f_ + e.off, N.g + e.off, e.shape[0], e.shape[1], e.shape[2] * e.shape[3], st_));
+      else CK(cudaMemcpyAsync(N.g + e.off, scratch_f_ + e.off, sizeof(float) * e.n, cudaMemcpyDeviceToDevice, st_));
+    }
+    N.gsum = 1.0f;
+    return sync_ok();
+  }
   paragan_status get_fakes(float* host, size_t n) override {
     if (!ready_) return PARAGAN_ERR_ORDER;
     const size_t need = (size_t)B_ * 3 * R_ * R_;
@@ -380,6 +395,52 @@ class Engine final : public EngineBase {
     CKS(fold_subpixel(false));
     if (dcgan_) CKS(g_forward_dc(z));
     else CKS(g_forward(z, fake_y, false));
+    return d_step_body(real, real_y, fake_y, flags);
+  }
+  // asynchronous scheme: D on an img_buff entry instead of a fresh G forward
+  paragan_status d_step_fakes(const void* real, const int32_t* real_y, const void* fakes, const int32_t* fake_y,
+                              uint32_t flags) override {
+    if (!ready_ || poisoned_) return PARAGAN_ERR_ORDER;
+    if (!real || !real_y || !fakes || !fake_y || ((uintptr_t)real & 15) || ((uintptr_t)fakes & 15))
+      return fail_arg("d_step_fakes: bad pointer");
+    const size_t img_bytes = (size_t)B_ * R_ * R_ * cpad_ * sizeof(T);
+    if (cudaMemcpyAsync(dimg_, fakes, img_bytes, cudaMemcpyDeviceToDevice, st_))
+      return fail_cuda(cudaGetLastError(), "copy fakes");
+    return d_step_body(real, real_y, fake_y, flags);
+  }
+  paragan_status generate(const float* z, const int32_t* y, void* dst) override {
+    if (!ready_ || poisoned_) return PARAGAN_ERR_ORDER;
+    if (!z || !y) return fail_arg("generate: bad pointer");
+    CKS(sn_forward(G_, false));
+    CKS(fold_subpixel(false));
+    if (dcgan_) CKS(g_forward_dc(z));
+    else CKS(g_forward(z, y, false));
+    return export_fakes(dst);
+  }
+  paragan_status export_fakes(void* dst) override {
+    if (!ready_ || poisoned_) return PARAGAN_ERR_ORDER;
+    const size_t img_bytes = (size_t)B_ * R_ * R_ * cpad_ * sizeof(T);
+    if (cudaMemcpyAsync(dst, dimg_, img_bytes, cudaMemcpyDeviceToDevice, st_))
+      return fail_cuda(cudaGetLastError(), "export fakes");
+    return PARAGAN_OK;
+  }
+  paragan_status export_state(paragan_net net, float* dst) override {
+    if (!ready_ || poisoned_) return PARAGAN_ERR_ORDER;
+    Net& N = net == PARAGAN_NET_D ? D_ : G_;
+    if (cudaMemcpyAsync(dst, N.p, sizeof(float) * N.n, cudaMemcpyDeviceToDevice, st_) ||
+        cudaMemcpyAsync(dst + N.n, N.u, sizeof(float) * N.nu, cudaMemcpyDeviceToDevice, st_))
+      return fail_cuda(cudaGetLastError(), "export_state");
+    return PARAGAN_OK;
+  }
+  paragan_status import_state(paragan_net net, const float* src) override {
+    if (!ready_ || poisoned_) return PARAGAN_ERR_ORDER;
+    Net& N = net == PARAGAN_NET_D ? D_ : G_;
+    if (cudaMemcpyAsync(N.p, src, sizeof(float) * N.n, cudaMemcpyDeviceToDevice, st_) ||
+        cudaMemcpyAsync(N.u, src + N.n, sizeof(float) * N.nu, cudaMemcpyDeviceToDevice, st_))
+      return fail_cuda(cudaGetLastError(), "import_state");
+    return PARAGAN_OK;
+  }
+  paragan_status d_step_body(const void* real, const int32_t* real_y, const int32_t* fake_y, uint32_t flags) {
     // reals into rows [B, 2B) (one D pass over the concatenated batch)
     const size_t img_bytes = (size_t)B_ * R_ * R_ * cpad_ * sizeof(T);
     if (cudaMemcpyAsync(static_cast<char*>(dimg_) + img_bytes, real, img_bytes, cudaMemcpyDeviceToDevice, st_))
@@ -390,7 +451,6 @@ class Engine final : public EngineBase {
     if (dcgan_) CKS(d_forward_dc(2 * B_));
     else CKS(d_forward(2 * B_));
     CK(hinge_loss(logits_, B_, 0, dlogits_, D_.loss, st_));
-    ++launches_;
     CKS(allreduce_loss(D_.loss));
     CK(cudaMemsetAsync(D_.g, 0, sizeof(float) * D_.n, st_));
     D_.gsum = 1.0f;
@@ -405,7 +465,7 @@ class Engine final : public EngineBase {
 
   paragan_status g_step(const float* z, const int32_t* y, uint32_t flags) override {
     if (!ready_ || poisoned_) return PARAGAN_ERR_ORDER;
-    if (d_since_g_ < cfg_.d_steps_per_g) {
+    if (d_since_g_ < cfg_.d_steps_per_g && !(flags & PARAGAN_FLAG_ASYNC)) {
       err_ = "g_step before d_steps_per_g D steps";
       return PARAGAN_ERR_ORDER;
     }
@@ -420,7 +480,6 @@ class Engine final : public EngineBase {
     if (dcgan_) CKS(d_forward_dc(B_));
     else CKS(d_forward(B_));
     CK(hinge_loss(logits_, B_, 1, dlogits_, G_.loss, st_));
-    ++launches_;
     CKS(allreduce_loss(G_.loss));
     CK(cudaMemsetAsync(G_.g, 0, sizeof(float) * G_.n, st_));
     G_.gsum = 1.0f;
@@ -445,7 +504,13 @@ class Engine final : public EngineBase {
     Net& N = net == PARAGAN_NET_D ? D_ : G_;
     if (cfg_.world_size > 1 && N.gsum == 1.0f) {
       // sum over ranks; the mean's 1/W (R15) is folded into the update and into get_grads
-      CKS(nccl_sum(N.g, (size_t)N.n, ncclFloat32, "grad allreduce"));
+      if (N.g16) {   // bf16 on the wire: round, sum in bf16, widen back
+        CK(convert_f32<bf16>(N.g, N.g16, N.n, st_));
+        CKS(nccl_sum(N.g16, (size_t)N.n, ncclBfloat16, "grad allreduce (bf16)"));
+        CK(to_f32<bf16>(N.g16, N.g, N.n, st_));
+      } else {
+        CKS(nccl_sum(N.g, (size_t)N.n, ncclFloat32, "grad allreduce"));
+      }
       N.gsum = (float)cfg_.world_size;
     }
     return PARAGAN_OK;
@@ -695,6 +760,7 @@ class Engine final : public EngineBase {
       N->opt_upart = A.get<double>(nc);
       N->clip_scale = A.get<float>(1);
       N->slow = policy(*N).lookahead_k > 0 ? A.get<float>(N->n) : nullptr;
+      N->g16 = (cfg_.grad_comm_bf16 && cfg_.world_size > 1) ? A.get<bf16>(N->n) : nullptr;
     }
   }
   paragan_status upload_opt_tables() {
@@ -1445,7 +1511,7 @@ class Engine final : public EngineBase {
   // in-place sum over ranks on the compute stream; timed as profile kind 2 (collectives)
   paragan_status nccl_sum(void* buf, size_t count, ncclDataType_t dt, const char* what) {
     ncclResult_t r = ncclSuccess;
-    const size_t bytes = count * (dt == ncclFloat64 ? 8 : 4);
+    const size_t bytes = count * (dt == ncclFloat64 ? 8 : dt == ncclBfloat16 ? 2 : 4);
     char label[48];
     std::snprintf(label, sizeof(label), "%s %zu B", what, bytes);
     cudaError_t e = timed(2, (double)bytes, [&] {

@@ -20,6 +20,7 @@ class EngineBase {
   virtual paragan_status set_params(paragan_net net, const float* host, size_t n) = 0;
   virtual paragan_status get_params(paragan_net net, float* host, size_t n) = 0;
   virtual paragan_status get_grads(paragan_net net, float* host, size_t n) = 0;
+  virtual paragan_status set_grads(paragan_net net, const float* host, size_t n) = 0;
   virtual paragan_status d_step(const void* real, const int32_t* real_y, const float* z, const int32_t* fake_y,
                                 uint32_t flags) = 0;
   virtual paragan_status g_step(const float* z, const int32_t* y, uint32_t flags) = 0;
@@ -28,6 +29,12 @@ class EngineBase {
   virtual paragan_status sync_stats(paragan_stats* out) = 0;
   virtual paragan_status get_fakes(float* host, size_t n) = 0;
   virtual paragan_status get_dfake(float* host, size_t n) = 0;
+  virtual paragan_status d_step_fakes(const void* real, const int32_t* real_y, const void* fakes, const int32_t* fake_y,
+                                      uint32_t flags) = 0;
+  virtual paragan_status generate(const float* z, const int32_t* y, void* dst) = 0;
+  virtual paragan_status export_fakes(void* dst) = 0;
+  virtual paragan_status export_state(paragan_net net, float* dst) = 0;
+  virtual paragan_status import_state(paragan_net net, const float* src) = 0;
   virtual uint64_t launches() const = 0;
   virtual paragan_status profile(int enable) = 0;
   virtual paragan_status profile_read(int kind, uint64_t* n, double* ms, double* flops) = 0;

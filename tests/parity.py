@@ -45,6 +45,49 @@ def run_oracle(ocfg, gs, ds, g0, d0, dbs, gb):
                 d_logits=out["d"][-1]["logits"], g_logits=out["g"]["logits"])
 
 
+class perturbed_convs:
+    """Context manager (test infrastructure): every oracle conv output is multiplied by (1 + eps * xi), xi a
+    fixed standard-normal draw — fp32-sized rounding noise injected into the exact computation."""
+
+    def __init__(self, eps, seed=12345):
+        self.eps, self.seed = eps, seed
+
+    def __enter__(self):
+        import torch
+        from oracle import ops
+        self.ops, self.orig = ops, ops.conv2d
+        rng = np.random.default_rng(self.seed)
+
+        def conv(x, w, b):
+            y = self.orig(x, w, b)
+            return y * (1.0 + self.eps * torch.from_numpy(rng.standard_normal(tuple(y.shape))))
+        ops.conv2d = conv
+        return self
+
+    def __exit__(self, *a):
+        self.ops.conv2d = self.orig
+
+
+def well_posed_seed(ocfg, B, seed0, eps=1e-7, limit=5e-5, tries=4, n_d=1):
+    """R19 extended to ReLU kinks (R19): the first seed >= seed0 whose iteration is well posed at
+    fp32 precision — the oracle's own gradients move by < limit (relative) when fp32-sized noise (eps) is
+    injected into every conv output.  An activation within ~eps of a ReLU kink in a low-resolution layer
+    otherwise takes the other subgradient under ANY fp32 computation and moves the whole gradient by up to
+    ~2e-3 (BigGAN-128, B = 2, seeds 24-29 measured 7.9e-5, 1.8e-4, 2.4e-5, 1.8e-4, 2.1e-3, 6.1e-5 on a
+    B200 box; none is below 1e-5, so limit = 5e-5, half the 1e-4 bar).  Decided by the oracle alone;
+    returns (seed, clean oracle run)."""
+    for seed in range(seed0, seed0 + tries):
+        args = make_inputs(ocfg, B, seed, n_d)
+        clean = run_oracle(ocfg, *args)
+        with perturbed_convs(eps):
+            noisy = run_oracle(ocfg, *make_inputs(ocfg, B, seed, n_d))
+        moved = max(rel(noisy[k], clean[k]) for k in ("d_grads", "g_grads"))
+        print(f"well-posed check seed {seed}: gradient moves {moved:.2e} under {eps:.0e} conv noise")
+        if moved < limit:
+            return seed, clean
+    raise AssertionError(f"no well-posed seed in [{seed0}, {seed0 + tries})")
+
+
 def run_gpu(cfg, g0, d0, dbs, gb, rank=0, world=1, nccl_id=None, ctx=None):
     """One iteration through the C-ABI on this rank's shard of the global batch."""
     import torch

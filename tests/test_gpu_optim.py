@@ -36,8 +36,8 @@ CASES = {
 @pytest.mark.parametrize("name", list(CASES))
 def test_policy_update_matches_oracle(name):
     """Six updates of D with the same (GPU-computed) gradient: GPU weights vs oracle/optim.py in fp64.
-    The bar is on the accumulated change w_T - w_0 (relative, 2e-5: fp32 vs fp64 arithmetic of the
-    update rule only — both sides start from the same gradient)."""
+    The bar is the north_star's fp32 bar 1e-4 on the accumulated change w_T - w_0 (fp32 vs fp64
+    arithmetic of the update rule only — both sides start from the same gradient)."""
     pol, opol = CASES[name]
     hp = (1e-3, 0.5, 0.99, 1e-8) if pol.rule != api.OPT_SGD else (1e-2, 0.9, 0.99, 1e-8)
     cfg = api.make_config(**MICRO, local_batch=4, compute=api.F32, adam_d=hp, policy_d=pol)
@@ -71,7 +71,7 @@ def test_policy_update_matches_oracle(name):
     dw_got, dw_want = w1[:nt].astype(np.float64) - w0[:nt], want - w0[:nt]
     err = np.linalg.norm(dw_got - dw_want) / np.linalg.norm(dw_want)
     print(name, f"|dw| {np.linalg.norm(dw_want):.3e} rel err {err:.2e}")
-    assert err < 2e-5
+    assert err < 1e-4
     assert np.array_equal(w1[nt:], w0[nt:])       # u vectors are not optimiser state
 
 

@@ -262,3 +262,48 @@ def test_bf16_emulation_obeys_the_storage_rule(monkeypatch, bf16):
             assert 0 < abs(a - b) / abs(b) < 2e-2
     else:
         assert seen["bad_fwd"] and seen["bad_bwd"]
+
+
+def test_async_schedule_staleness0_reduces_to_sync_iteration():
+    """oracle/async_scheme.py with max_staleness = 0 is the synchronous iteration: same
+    losses, G state and D weights after a tick; D's u vectors differ only by the G step's power step,
+    which runs on the snapshot copy (R31) — and the snapshot copy equals the sync D exactly."""
+    import copy
+    from oracle import async_scheme as OA
+    cfg = bg.Config(**MICRO)
+    G, D, real, ry, z, fy = _setup(cfg, 2, seed=9)
+    zg, yg = inputs.latent_batch(9, inputs.ROLE_Z_G, 0, 2, cfg.dim_z, cfg.n_classes)
+    G2, D2 = copy.deepcopy(G), copy.deepcopy(D)
+    sync = bg.iteration(cfg, G, D, [(real, ry, z, fy)], (zg, yg))
+    rec = OA.run(cfg, G2, D2, [{"d": [(real, ry, z, fy)], "g": (zg, yg)}], max_staleness=0, d_batch=2)
+    assert rec[0]["d_loss"][0] == sync["d"][0]["loss"] and rec[0]["g_loss"] == sync["g"]["loss"]
+    assert rec[0]["d_staleness"] == [0] and rec[0]["g_snapshot_staleness"] == 0
+    assert np.array_equal(G2.flat(), G.flat())
+    nt = bg.n_trainable(D.specs)
+    assert np.array_equal(D2.flat()[:nt], D.flat()[:nt])
+
+
+def test_async_schedule_staleness1_uses_previous_tick():
+    """With max_staleness = 1 the D step of tick t trains on the fakes G produced at tick t-1 (P:275
+    "generator of the previous iteration") and the G step of tick t through D after tick t-1: the second
+    tick's D loss equals a D step on tick 1's G-step fakes, computed directly."""
+    import copy
+    from oracle import async_scheme as OA
+    cfg = bg.Config(**MICRO)
+    G, D, real, ry, z, fy = _setup(cfg, 2, seed=10)
+    ticks = []
+    for t in range(2):
+        r_, ry_ = inputs.real_batch(10, t, 2, cfg.resolution, cfg.n_classes)
+        zb, yb = inputs.latent_batch(10, inputs.ROLE_Z_D, t, 2, cfg.dim_z, cfg.n_classes)
+        zg, yg = inputs.latent_batch(10, inputs.ROLE_Z_G, t, 2, cfg.dim_z, cfg.n_classes)
+        ticks.append({"d": [(r_, ry_, zb, yb)], "g": (zg, yg)})
+    G0, D0 = copy.deepcopy(G), copy.deepcopy(D)
+    rec = OA.run(cfg, G, D, ticks, max_staleness=1, d_batch=2)
+    assert [r["d_staleness"] for r in rec] == [[0], [1]] and [r["g_snapshot_staleness"] for r in rec] == [1, 1]
+    # by hand: tick 0 = D on G0's fresh fakes; G through the initial D; tick 1 = D on those G-step fakes
+    r0 = bg.d_step(cfg, None, D0, *ticks[0]["d"][0][:2], None, ticks[0]["d"][0][3],
+                   fakes=OA.generate(cfg, G0, ticks[0]["d"][0][2], ticks[0]["d"][0][3]))
+    Dinit = bg.NetState.from_flat(D.specs, _setup(cfg, 2, seed=10)[1].flat())
+    rg = bg.g_step(cfg, G0, Dinit, *ticks[0]["g"])
+    r1 = bg.d_step(cfg, None, D0, *ticks[1]["d"][0][:2], None, ticks[0]["g"][1], fakes=rg["fake"])
+    assert rec[0]["d_loss"][0] == r0["loss"] and rec[1]["d_loss"][0] == r1["loss"]
