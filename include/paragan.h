@@ -208,8 +208,9 @@ paragan_status paragan_generate(paragan_ctx* ctx, const float* z, const int32_t*
 /* Copy the last generated images (the last G step's or D step's fakes) to dst_nhwc (device, as above). */
 paragan_status paragan_export_fakes(paragan_ctx* ctx, void* dst_nhwc);
 /* Device-to-device snapshot of a network's state (the D snapshot G uses): dst/src device fp32 buffers of
- * paragan_param_count n_state floats in the library's INTERNAL layout (weights then u vectors; only
- * meaningful between contexts of the same config).  import resets nothing else (Adam state stays). */
+ * paragan_state_size floats in the library's INTERNAL layout (16-byte aligned tensors, then the u vectors;
+ * only meaningful between contexts of the same config).  import resets nothing else (Adam state stays). */
+paragan_status paragan_state_size(paragan_ctx* ctx, paragan_net net, size_t* n_floats);
 paragan_status paragan_export_state(paragan_ctx* ctx, paragan_net net, float* dst_device);
 paragan_status paragan_import_state(paragan_ctx* ctx, paragan_net net, const float* src_device);
 
@@ -253,6 +254,56 @@ paragan_status paragan_kernel_launches(const paragan_ctx* ctx, uint64_t* n);
  * work).  enable=1 also clears the record. */
 paragan_status paragan_profile(paragan_ctx* ctx, int32_t enable);
 paragan_status paragan_profile_read(paragan_ctx* ctx, int32_t kind, uint64_t* launches, double* ms, double* flops);
+
+/* ------------------------------------------ host-side system features (PAPER.md:221-233 [Sec. 4.1]) */
+
+/* Asynchronous checkpoint writer ("We use an asynchronous checkpoint writer to save model
+ * checkpoints. The checkpoint will be streamed into the output buffer instead of having a blocking call to
+ * pass it to the CPU host"): the full training state (both networks' weights and SN u vectors, optimiser
+ * moments and step counts, Lookahead slow weights) is snapshotted stream-ordered into a device staging
+ * buffer on the caller's stream (a device-to-device copy), streamed to pinned host memory on a separate
+ * copy stream, and written to `path` (via `path`.tmp + rename) by a host thread while training continues.
+ * At most one checkpoint is in flight per context: a second save first waits for the first.  The file
+ * holds a header (magic, ABI version, the config fields that fix the layout, array sizes) and a 64-bit
+ * FNV-1a hash of the payload. */
+paragan_status paragan_checkpoint_save_async(paragan_ctx* ctx, const char* path);
+/* Blocks until the checkpoint in flight (if any) is on disk; PARAGAN_ERR_IO if writing it failed. */
+paragan_status paragan_checkpoint_wait(paragan_ctx* ctx);
+/* Synchronous restore into a context of the same configuration (PARAGAN_ERR_CONFIG on a layout mismatch,
+ * PARAGAN_ERR_IO on a short or corrupt file); resumes training exactly where the checkpoint was taken. */
+paragan_status paragan_checkpoint_load(paragan_ctx* ctx, const char* path);
+
+/* Congestion-aware prefetcher: reader threads fill a bounded queue of batches read from
+ * sample shards (paragan_shard_write format); a sliding window of per-batch read latencies (ms) adds a
+ * reader and doubles the queue depth when the window mean exceeds latency_threshold_ms, and releases a
+ * reader and halves the depth when it falls below half the threshold ("once the latency falls below the
+ * threshold, it releases the resources").  Batches come out in order (batch i = samples [iB, (i+1)B),
+ * cyclic over the shards).  Host only: no CUDA calls. */
+typedef struct {
+  int32_t batch, channels, height, width;  /* a sample: channels*height*width fp32 + one int32 label */
+  int32_t min_workers, max_workers;        /* reader threads (resources the tuner scales) */
+  int32_t min_depth, max_depth;            /* prefetched batches */
+  int32_t window;                          /* latency samples per decision */
+  float latency_threshold_ms;
+  float inject_latency_ms;                 /* test hook: simulated storage/network delay per batch read */
+} paragan_prefetch_config;
+typedef struct {
+  int32_t active_workers, depth, queued;
+  float window_mean_ms;
+  int64_t batches_read, scale_ups, scale_downs;
+} paragan_prefetch_stats;
+typedef struct paragan_prefetcher paragan_prefetcher;
+/* Writes n samples (images fp32 NCHW [n,c,h,w], labels int32 [n]) as one shard file. */
+paragan_status paragan_shard_write(const char* path, const float* images, const int32_t* labels, int32_t n,
+                                   int32_t c, int32_t h, int32_t w);
+paragan_status paragan_prefetch_create(const paragan_prefetch_config* cfg, const char* const* shard_paths,
+                                       int32_t n_shards, paragan_prefetcher** out);
+/* Copies the next batch (in order) into caller-owned host buffers ([batch,c,h,w] fp32, [batch] int32;
+ * pinned memory makes the following host-to-device copy asynchronous); blocks until it is read. */
+paragan_status paragan_prefetch_next(paragan_prefetcher* p, float* host_images, int32_t* host_labels);
+paragan_status paragan_prefetch_get_stats(paragan_prefetcher* p, paragan_prefetch_stats* out);
+paragan_status paragan_prefetch_set_latency(paragan_prefetcher* p, float inject_latency_ms);
+paragan_status paragan_prefetch_destroy(paragan_prefetcher* p);
 
 const char* paragan_last_error(const paragan_ctx* ctx);
 paragan_status paragan_destroy(paragan_ctx* ctx);

@@ -42,6 +42,19 @@ def make_policy(rule=OPT_ADAM, lars=False, lars_trust=1.0, lookahead_k=0, lookah
                   total_steps, clip_norm)
 
 
+class PrefetchConfig(C.Structure):
+    _fields_ = [("batch", C.c_int32), ("channels", C.c_int32), ("height", C.c_int32), ("width", C.c_int32),
+                ("min_workers", C.c_int32), ("max_workers", C.c_int32), ("min_depth", C.c_int32),
+                ("max_depth", C.c_int32), ("window", C.c_int32), ("latency_threshold_ms", C.c_float),
+                ("inject_latency_ms", C.c_float)]
+
+
+class PrefetchStats(C.Structure):
+    _fields_ = [("active_workers", C.c_int32), ("depth", C.c_int32), ("queued", C.c_int32),
+                ("window_mean_ms", C.c_float), ("batches_read", C.c_int64), ("scale_ups", C.c_int64),
+                ("scale_downs", C.c_int64)]
+
+
 class Config(C.Structure):
     _fields_ = [("abi_version", C.c_int32), ("resolution", C.c_int32), ("ch", C.c_int32),
                 ("n_classes", C.c_int32), ("shared_dim", C.c_int32), ("z_chunk", C.c_int32),
@@ -85,6 +98,7 @@ SYMBOLS = {
     "paragan_generate": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "paragan_export_fakes": (C.c_int, [C.c_void_p, C.c_void_p]),
     "paragan_export_state": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
+    "paragan_state_size": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_size_t)]),
     "paragan_import_state": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
     "paragan_allreduce_grads": (C.c_int, [C.c_void_p, C.c_int]),
     "paragan_apply_update": (C.c_int, [C.c_void_p, C.c_int]),
@@ -95,6 +109,16 @@ SYMBOLS = {
     "paragan_profile": (C.c_int, [C.c_void_p, C.c_int32]),
     "paragan_profile_read": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_uint64), C.POINTER(C.c_double),
                                        C.POINTER(C.c_double)]),
+    "paragan_checkpoint_save_async": (C.c_int, [C.c_void_p, C.c_char_p]),
+    "paragan_checkpoint_wait": (C.c_int, [C.c_void_p]),
+    "paragan_checkpoint_load": (C.c_int, [C.c_void_p, C.c_char_p]),
+    "paragan_shard_write": (C.c_int, [C.c_char_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32]),
+    "paragan_prefetch_create": (C.c_int, [C.POINTER(PrefetchConfig), C.POINTER(C.c_char_p), C.c_int32,
+                                          C.POINTER(C.c_void_p)]),
+    "paragan_prefetch_next": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "paragan_prefetch_get_stats": (C.c_int, [C.c_void_p, C.POINTER(PrefetchStats)]),
+    "paragan_prefetch_set_latency": (C.c_int, [C.c_void_p, C.c_float]),
+    "paragan_prefetch_destroy": (C.c_int, [C.c_void_p]),
     "paragan_last_error": (C.c_char_p, [C.c_void_p]),
     "paragan_destroy": (C.c_int, [C.c_void_p]),
     "paragan_op_conv_fwd": (C.c_int, [C.c_int, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
@@ -274,6 +298,59 @@ def op_attn_bwd(qkv, phi, gp, dO, o32, lse, cq, c2, dqkv, dphi, dgp, stream=None
                                                             _ptr(dgp), _stream(stream)))
 
 
+def shard_write(path: str, images, labels):
+    """images: float32 numpy [n, c, h, w]; labels: int32 [n]."""
+    import numpy as np
+    im = np.ascontiguousarray(images, dtype=np.float32)
+    lb = np.ascontiguousarray(labels, dtype=np.int32)
+    n, c, h, w = im.shape
+    _check("paragan_shard_write", lib().paragan_shard_write(path.encode(), im.ctypes.data, lb.ctypes.data, n, c, h, w))
+
+
+class Prefetcher:
+    """Congestion-aware prefetcher (paragan_prefetch_*)."""
+
+    def __init__(self, shards, batch, c, h, w, min_workers=1, max_workers=4, min_depth=2, max_depth=16, window=4,
+                 latency_threshold_ms=20.0, inject_latency_ms=0.0):
+        self.cfg = PrefetchConfig(batch, c, h, w, min_workers, max_workers, min_depth, max_depth, window,
+                                  latency_threshold_ms, inject_latency_ms)
+        arr = (C.c_char_p * len(shards))(*[s.encode() for s in shards])
+        self.p = C.c_void_p()
+        _check("paragan_prefetch_create", lib().paragan_prefetch_create(C.byref(self.cfg), arr, len(shards),
+                                                                        C.byref(self.p)))
+        self.shape = (batch, c, h, w)
+
+    def next(self, images=None, labels=None):
+        """Fills (or allocates) numpy / pinned-torch host buffers with the next batch."""
+        import numpy as np
+        if images is None:
+            images = np.empty(self.shape, np.float32)
+            labels = np.empty(self.shape[0], np.int32)
+        ip = images.data_ptr() if hasattr(images, "data_ptr") else images.ctypes.data
+        lp = labels.data_ptr() if hasattr(labels, "data_ptr") else labels.ctypes.data
+        _check("paragan_prefetch_next", lib().paragan_prefetch_next(self.p, C.c_void_p(ip), C.c_void_p(lp)))
+        return images, labels
+
+    def set_latency(self, ms):
+        _check("paragan_prefetch_set_latency", lib().paragan_prefetch_set_latency(self.p, ms))
+
+    def stats(self) -> PrefetchStats:
+        s = PrefetchStats()
+        _check("paragan_prefetch_get_stats", lib().paragan_prefetch_get_stats(self.p, C.byref(s)))
+        return s
+
+    def close(self):
+        if self.p:
+            lib().paragan_prefetch_destroy(self.p)
+            self.p = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class Context:
     """One rank's ParaGAN training context (paragan_init .. paragan_destroy)."""
 
@@ -360,6 +437,20 @@ class Context:
 
     def export_fakes(self, dst_nhwc):
         _check("paragan_export_fakes", lib().paragan_export_fakes(self.ctx, _ptr(dst_nhwc)), self.ctx)
+
+    def checkpoint_save_async(self, path: str):
+        _check("paragan_checkpoint_save_async", lib().paragan_checkpoint_save_async(self.ctx, path.encode()), self.ctx)
+
+    def checkpoint_wait(self):
+        _check("paragan_checkpoint_wait", lib().paragan_checkpoint_wait(self.ctx), self.ctx)
+
+    def checkpoint_load(self, path: str):
+        _check("paragan_checkpoint_load", lib().paragan_checkpoint_load(self.ctx, path.encode()), self.ctx)
+
+    def state_size(self, net) -> int:
+        n = C.c_size_t()
+        _check("paragan_state_size", lib().paragan_state_size(self.ctx, net, C.byref(n)), self.ctx)
+        return n.value
 
     def export_state(self, net, dst):
         _check("paragan_export_state", lib().paragan_export_state(self.ctx, net, _ptr(dst)), self.ctx)

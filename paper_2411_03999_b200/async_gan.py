@@ -105,8 +105,7 @@ class LocalAsync:
 
     def _state(self, ctx):
         import torch
-        ns, _ = api.param_count(ctx.cfg, api.NET_D)
-        buf = torch.empty(ns, dtype=torch.float32, device=self.dev)
+        buf = torch.empty(ctx.state_size(api.NET_D), dtype=torch.float32, device=self.dev)
         ctx.export_state(api.NET_D, buf)
         return buf
 
@@ -150,8 +149,7 @@ class LocalAsync:
             self.ctx_g.generate(z, y, dst)
         else:   # the D context keeps a copy of G (refreshed here) sized for d_batch
             import torch
-            ns, _ = api.param_count(self.cfg_g, api.NET_G)
-            buf = torch.empty(ns, dtype=torch.float32, device=self.dev)
+            buf = torch.empty(self.ctx_g.state_size(api.NET_G), dtype=torch.float32, device=self.dev)
             self.ctx_g.export_state(api.NET_G, buf)
             self.ctx_d.import_state(api.NET_G, buf)
             self.ctx_d.generate(z, y, dst)
@@ -192,8 +190,7 @@ class DistributedAsync:
         r = self.cfg.resolution
         self.fakes = torch.empty((g_batch, r, r, self.cfg.c_pad_image), dtype=tdt, device=self.dev)
         self.labels = torch.zeros(g_batch, dtype=torch.int32, device=self.dev)
-        ns, _ = api.param_count(self.cfg, api.NET_D)
-        self.snap = torch.empty(ns, dtype=torch.float32, device=self.dev)
+        self.snap = torch.empty(self.ctx.state_size(api.NET_D), dtype=torch.float32, device=self.dev)
         self.t = 0
 
     def init_params(self, attn_gamma=0.1):

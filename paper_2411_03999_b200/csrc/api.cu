@@ -145,6 +145,11 @@ paragan_status paragan_export_fakes(paragan_ctx* ctx, void* dst) {
   if (!ctx || !ctx->eng || !dst) return PARAGAN_ERR_INVALID_ARG;
   return ctx->eng->export_fakes(dst);
 }
+paragan_status paragan_state_size(paragan_ctx* ctx, paragan_net net, size_t* n_floats) {
+  if (!ctx || !ctx->eng || !n_floats || (net != PARAGAN_NET_D && net != PARAGAN_NET_G)) return PARAGAN_ERR_INVALID_ARG;
+  *n_floats = ctx->eng->state_floats(net);
+  return PARAGAN_OK;
+}
 paragan_status paragan_export_state(paragan_ctx* ctx, paragan_net net, float* dst) {
   if (!ctx || !ctx->eng || !dst || (net != PARAGAN_NET_D && net != PARAGAN_NET_G)) return PARAGAN_ERR_INVALID_ARG;
   return ctx->eng->export_state(net, dst);
@@ -185,6 +190,18 @@ paragan_status paragan_profile(paragan_ctx* ctx, int32_t enable) {
 paragan_status paragan_profile_read(paragan_ctx* ctx, int32_t kind, uint64_t* launches, double* ms, double* flops) {
   if (!ctx || !ctx->eng || kind < 0 || kind > 4) return PARAGAN_ERR_INVALID_ARG;
   return ctx->eng->profile_read(kind, launches, ms, flops);
+}
+paragan_status paragan_checkpoint_save_async(paragan_ctx* ctx, const char* path) {
+  if (!ctx || !ctx->eng) return PARAGAN_ERR_INVALID_ARG;
+  return ctx->eng->checkpoint_save_async(path);
+}
+paragan_status paragan_checkpoint_wait(paragan_ctx* ctx) {
+  if (!ctx || !ctx->eng) return PARAGAN_ERR_INVALID_ARG;
+  return ctx->eng->checkpoint_wait();
+}
+paragan_status paragan_checkpoint_load(paragan_ctx* ctx, const char* path) {
+  if (!ctx || !ctx->eng) return PARAGAN_ERR_INVALID_ARG;
+  return ctx->eng->checkpoint_load(path);
 }
 const char* paragan_last_error(const paragan_ctx* ctx) {
   if (!ctx || !ctx->eng) return "null context";

@@ -13,14 +13,17 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <type_traits>
 #include <vector>
 
 #include "common.cuh"
 #include "engine.h"
+#include "host_io.h"
 #include "tc_attn.h"
 #include "kernels.h"
 #include "optim.h"
@@ -50,14 +53,16 @@ struct PEntry {
   std::vector<int> shape;
   bool conv4d = false;
   bool sn = false;
-  long long off = 0, n = 0;
+  long long off = 0, n = 0;   // internal offset (16-byte aligned) and size
+  long long coff = 0;         // offset in the canonical (unpadded) flat layout of the C-ABI
   long long u_off = -1, v_off = -1;
   int job = -1;
 };
 
 struct Net {
   std::vector<PEntry> E;
-  long long n = 0, nu = 0, nv = 0;
+  long long n = 0, nu = 0, nv = 0;   // n: internal flat size (every tensor starts 16-byte aligned)
+  long long nc = 0;                  // canonical flat size (paragan_param_count n_trainable)
   float *p = nullptr, *g = nullptr, *m = nullptr, *v = nullptr, *u = nullptr;
   float *sn_v = nullptr, *sn_t = nullptr, *sn_s = nullptr, *sigma = nullptr;
   std::vector<int> sn_entries;                // entry index per SN job
@@ -95,8 +100,10 @@ struct Net {
     e.sn = sn;
     e.n = 1;
     for (int s : shape) e.n *= s;
-    e.off = n;
-    n += e.n;
+    e.coff = nc;
+    nc += e.n;
+    e.off = (n + 3) & ~3LL;   // 16-byte aligned tensors: float4 / 8 x bf16 vector paths everywhere
+    n = (e.off + e.n + 3) & ~3LL;
     E.push_back(e);
     return (int)E.size() - 1;
   }
@@ -229,6 +236,12 @@ class Engine final : public EngineBase {
     dcgan_ = c.arch == PARAGAN_ARCH_SNDCGAN;
   }
   ~Engine() override {
+    if (ck_thread_.joinable()) ck_thread_.join();
+    if (ck_dev_) cudaFree(ck_dev_);
+    if (ck_host_) cudaFreeHost(ck_host_);
+    if (ck_stream_) cudaStreamDestroy(ck_stream_);
+    if (ck_ev_snap_) cudaEventDestroy(ck_ev_snap_);
+    if (ck_ev_done_) cudaEventDestroy(ck_ev_done_);
     if (dfake_keep_) cudaFree(dfake_keep_);
     if (comm_) ncclCommDestroy(comm_);
     if (cublas_) cublasDestroy(cublas_);
@@ -246,8 +259,8 @@ class Engine final : public EngineBase {
       build(a);
     }
     const Net& N = net == PARAGAN_NET_D ? D_ : G_;
-    if (ns) *ns = (size_t)(N.n + N.nu);
-    if (nt) *nt = (size_t)N.n;
+    if (ns) *ns = (size_t)(N.nc + N.nu);
+    if (nt) *nt = (size_t)N.nc;
   }
 
   paragan_status init(const uint8_t* id, void* ws, size_t ws_bytes) override {
@@ -298,7 +311,7 @@ class Engine final : public EngineBase {
         } else if (is_bias) {
           CK(fill_const(p, e.n, 0.0f, st_));
         } else {
-          CK(fill_normal(p, e.n, 0.02f, cfg_.seed * 1000003ull + salt, (uint64_t)e.off, st_));
+          CK(fill_normal(p, e.n, 0.02f, cfg_.seed * 1000003ull + salt, (uint64_t)e.coff, st_));
         }
         if (e.sn) {
           float* u = N->u + e.u_off;
@@ -314,45 +327,47 @@ class Engine final : public EngineBase {
   paragan_status set_params(paragan_net net, const float* host, size_t n) override {
     if (!ready_) return PARAGAN_ERR_ORDER;
     Net& N = net == PARAGAN_NET_D ? D_ : G_;
-    if (!host || n != (size_t)(N.n + N.nu)) return fail_arg("set_params: size mismatch");
-    // canonical -> staging (g buffer) -> internal (conv OIHW -> OHWI)
-    if (cudaMemcpyAsync(N.g, host, sizeof(float) * N.n, cudaMemcpyHostToDevice, st_) != cudaSuccess ||
-        cudaMemcpyAsync(N.u, host + N.n, sizeof(float) * N.nu, cudaMemcpyHostToDevice, st_) != cudaSuccess)
+    if (!host || n != (size_t)(N.nc + N.nu)) return fail_arg("set_params: size mismatch");
+    // canonical -> staging (g buffer, canonical offsets) -> internal (conv OIHW -> OHWI, aligned offsets)
+    if (cudaMemcpyAsync(N.g, host, sizeof(float) * N.nc, cudaMemcpyHostToDevice, st_) != cudaSuccess ||
+        cudaMemcpyAsync(N.u, host + N.nc, sizeof(float) * N.nu, cudaMemcpyHostToDevice, st_) != cudaSuccess)
       return fail_cuda(cudaGetLastError(), "set_params copy");
     for (size_t i = 0; i < N.E.size(); ++i) {
       const PEntry& e = N.E[i];
       if (e.conv4d) {
-        CK(oihw_to_ohwi(N.g + e.off, N.p + e.off, e.shape[0], e.shape[1], e.shape[2] * e.shape[3], st_));
+        CK(oihw_to_ohwi(N.g + e.coff, N.p + e.off, e.shape[0], e.shape[1], e.shape[2] * e.shape[3], st_));
       } else {
-        if (cudaMemcpyAsync(N.p + e.off, N.g + e.off, sizeof(float) * e.n, cudaMemcpyDeviceToDevice, st_))
+        if (cudaMemcpyAsync(N.p + e.off, N.g + e.coff, sizeof(float) * e.n, cudaMemcpyDeviceToDevice, st_))
           return fail_cuda(cudaGetLastError(), "set_params d2d");
       }
     }
+    CK(cudaMemsetAsync(N.g, 0, sizeof(float) * N.n, st_));
     reset_opt(N);
     return sync_ok();
   }
   paragan_status get_params(paragan_net net, float* host, size_t n) override {
     if (!ready_) return PARAGAN_ERR_ORDER;
     Net& N = net == PARAGAN_NET_D ? D_ : G_;
-    if (!host || n != (size_t)(N.n + N.nu)) return fail_arg("get_params: size mismatch");
+    if (!host || n != (size_t)(N.nc + N.nu)) return fail_arg("get_params: size mismatch");
     return export_flat(N, N.p, host, true);
   }
   paragan_status get_grads(paragan_net net, float* host, size_t n) override {
     if (!ready_) return PARAGAN_ERR_ORDER;
     Net& N = net == PARAGAN_NET_D ? D_ : G_;
-    if (!host || n != (size_t)N.n) return fail_arg("get_grads: size mismatch");
+    if (!host || n != (size_t)N.nc) return fail_arg("get_grads: size mismatch");
     return export_flat(N, N.g, host, false, 1.0f / N.gsum);
   }
   paragan_status set_grads(paragan_net net, const float* host, size_t n) override {
     if (!ready_ || poisoned_) return PARAGAN_ERR_ORDER;
     Net& N = net == PARAGAN_NET_D ? D_ : G_;
-    if (!host || n != (size_t)N.n) return fail_arg("set_grads: size mismatch");
+    if (!host || n != (size_t)N.nc) return fail_arg("set_grads: size mismatch");
     // canonical -> staging -> internal layout (conv OIHW -> OHWI), as set_params
-    if (cudaMemcpyAsync(scratch_f_, host, sizeof(float) * N.n, cudaMemcpyHostToDevice, st_) != cudaSuccess)
+    if (cudaMemcpyAsync(scratch_f_, host, sizeof(float) * N.nc, cudaMemcpyHostToDevice, st_) != cudaSuccess)
       return fail_cuda(cudaGetLastError(), "set_grads copy");
+    CK(cudaMemsetAsync(N.g, 0, sizeof(float) * N.n, st_));
     for (const PEntry& e : N.E) {
-      if (e.conv4d) CK(oihw_to_ohwi(scratch_f_ + e.off, N.g + e.off, e.shape[0], e.shape[1], e.shape[2] * e.shape[3], st_));
-      else CK(cudaMemcpyAsync(N.g + e.off, scratch_f_ + e.off, sizeof(float) * e.n, cudaMemcpyDeviceToDevice, st_));
+      if (e.conv4d) CK(oihw_to_ohwi(scratch_f_ + e.coff, N.g + e.off, e.shape[0], e.shape[1], e.shape[2] * e.shape[3], st_));
+      else CK(cudaMemcpyAsync(N.g + e.off, scratch_f_ + e.coff, sizeof(float) * e.n, cudaMemcpyDeviceToDevice, st_));
     }
     N.gsum = 1.0f;
     return sync_ok();
@@ -383,6 +398,146 @@ class Engine final : public EngineBase {
     CK(layout_unpack<T>(static_cast<const T*>(dimg_grad_), dfake_keep_, B_, 3, R_, R_, cpad_, st_));
     dfake_valid_ = true;
     return PARAGAN_OK;
+  }
+
+  // ------------------------------------------------------------------ asynchronous checkpoint writer
+  // (P:233).  Payload: per net (D then G) p[n], u[nu], m[n], v[n], slow[n] (Lookahead only), then the two
+  // int64 step counters; internal (16-byte aligned) layout, so only a context of the same config reads it.
+  struct CkHeader {
+    char magic[8];
+    int32_t abi, arch, resolution, ch, n_classes, shared_dim, z_chunk, attn_res, compute, la_d, la_g, pad;
+    int64_t nD, nuD, nG, nuG, payload_bytes;
+    uint64_t hash;
+  };
+  CkHeader ck_header() const {
+    CkHeader h{};
+    std::memcpy(h.magic, "PGCKPT01", 8);
+    h.abi = PARAGAN_ABI_VERSION;
+    h.arch = cfg_.arch;
+    h.resolution = cfg_.resolution;
+    h.ch = cfg_.ch;
+    h.n_classes = cfg_.n_classes;
+    h.shared_dim = cfg_.shared_dim;
+    h.z_chunk = cfg_.z_chunk;
+    h.attn_res = cfg_.attn_res;
+    h.compute = cfg_.compute;
+    h.la_d = D_.slow != nullptr;
+    h.la_g = G_.slow != nullptr;
+    h.nD = D_.n;
+    h.nuD = D_.nu;
+    h.nG = G_.n;
+    h.nuG = G_.nu;
+    h.payload_bytes = (int64_t)ck_bytes();
+    return h;
+  }
+  size_t ck_bytes() const {
+    size_t f = 0;
+    for (const Net* N : {&D_, &G_}) f += (size_t)(3 * N->n + N->nu + (N->slow ? N->n : 0));
+    return f * sizeof(float) + 2 * sizeof(long long);
+  }
+  // visits the payload sections in order: fn(device pointer, bytes)
+  template <class F>
+  void ck_sections(F&& fn) {
+    for (Net* N : {&D_, &G_}) {
+      fn((void*)N->p, sizeof(float) * N->n);
+      fn((void*)N->u, sizeof(float) * N->nu);
+      fn((void*)N->m, sizeof(float) * N->n);
+      fn((void*)N->v, sizeof(float) * N->n);
+      if (N->slow) fn((void*)N->slow, sizeof(float) * N->n);
+    }
+    fn((void*)D_.t_dev, sizeof(long long));
+    fn((void*)G_.t_dev, sizeof(long long));
+  }
+  paragan_status checkpoint_save_async(const char* path) override {
+    if (!ready_ || poisoned_) return PARAGAN_ERR_ORDER;
+    if (!path) return fail_arg("checkpoint: null path");
+    paragan_status ws = checkpoint_wait();
+    if (ws != PARAGAN_OK) return ws;
+    const size_t bytes = ck_bytes();
+    if (!ck_dev_) {
+      if (cudaMalloc(&ck_dev_, bytes) != cudaSuccess || cudaMallocHost(&ck_host_, bytes) != cudaSuccess ||
+          cudaStreamCreateWithFlags(&ck_stream_, cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&ck_ev_snap_, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&ck_ev_done_, cudaEventDisableTiming) != cudaSuccess)
+        return fail_cuda(cudaGetLastError(), "checkpoint buffers");
+    }
+    // 1) stream-ordered snapshot on the compute stream (the next update cannot race it)
+    size_t off = 0;
+    cudaError_t e = cudaSuccess;
+    ck_sections([&](void* src, size_t b) {
+      if (e == cudaSuccess) e = cudaMemcpyAsync(static_cast<char*>(ck_dev_) + off, src, b, cudaMemcpyDeviceToDevice, st_);
+      off += b;
+    });
+    if (e != cudaSuccess) return fail_cuda(e, "checkpoint snapshot");
+    // 2) device -> pinned host on the copy stream, overlapping the following steps
+    if (cudaEventRecord(ck_ev_snap_, st_) || cudaStreamWaitEvent(ck_stream_, ck_ev_snap_, 0) ||
+        cudaMemcpyAsync(ck_host_, ck_dev_, bytes, cudaMemcpyDeviceToHost, ck_stream_) ||
+        cudaEventRecord(ck_ev_done_, ck_stream_))
+      return fail_cuda(cudaGetLastError(), "checkpoint stream");
+    // 3) a host thread writes the file once the copy has landed
+    CkHeader h = ck_header();
+    const std::string p(path);
+    const int dev = cfg_.device;
+    ck_status_ = PARAGAN_OK;
+    ck_thread_ = std::thread([this, h, p, bytes, dev]() mutable {
+      cudaSetDevice(dev);
+      if (cudaEventSynchronize(ck_ev_done_) != cudaSuccess) {
+        ck_status_ = PARAGAN_ERR_CUDA;
+        return;
+      }
+      h.hash = fnv1a64(ck_host_, bytes);
+      const std::string tmp = p + ".tmp";
+      FILE* f = std::fopen(tmp.c_str(), "wb");
+      bool ok = f && std::fwrite(&h, sizeof(h), 1, f) == 1 && std::fwrite(ck_host_, 1, bytes, f) == bytes;
+      if (f) ok = (std::fclose(f) == 0) && ok;
+      ok = ok && std::rename(tmp.c_str(), p.c_str()) == 0;
+      ck_status_ = ok ? PARAGAN_OK : PARAGAN_ERR_IO;
+    });
+    return PARAGAN_OK;
+  }
+  paragan_status checkpoint_wait() override {
+    if (ck_thread_.joinable()) ck_thread_.join();
+    const paragan_status s = ck_status_;
+    if (s == PARAGAN_ERR_IO) err_ = "checkpoint: writing the file failed";
+    ck_status_ = PARAGAN_OK;
+    return s;
+  }
+  paragan_status checkpoint_load(const char* path) override {
+    if (!ready_ || poisoned_) return PARAGAN_ERR_ORDER;
+    if (!path) return fail_arg("checkpoint: null path");
+    paragan_status ws = checkpoint_wait();
+    if (ws != PARAGAN_OK) return ws;
+    FILE* f = std::fopen(path, "rb");
+    if (!f) {
+      err_ = std::string("checkpoint: cannot open ") + path;
+      return PARAGAN_ERR_IO;
+    }
+    CkHeader h{}, want = ck_header();
+    std::vector<char> buf;
+    bool ok = std::fread(&h, sizeof(h), 1, f) == 1;
+    if (ok) {
+      want.hash = h.hash;
+      if (std::memcmp(&h, &want, sizeof(h)) != 0) {
+        std::fclose(f);
+        err_ = "checkpoint: configuration / layout mismatch";
+        return PARAGAN_ERR_CONFIG;
+      }
+      buf.resize((size_t)h.payload_bytes);
+      ok = std::fread(buf.data(), 1, buf.size(), f) == buf.size();
+    }
+    std::fclose(f);
+    if (!ok || fnv1a64(buf.data(), buf.size()) != h.hash) {
+      err_ = "checkpoint: short or corrupt file";
+      return PARAGAN_ERR_IO;
+    }
+    size_t off = 0;
+    cudaError_t e = cudaSuccess;
+    ck_sections([&](void* dst, size_t b) {
+      if (e == cudaSuccess) e = cudaMemcpyAsync(dst, buf.data() + off, b, cudaMemcpyHostToDevice, st_);
+      off += b;
+    });
+    if (e != cudaSuccess) return fail_cuda(e, "checkpoint restore");
+    return sync_ok();   // buf is released after the copies completed
   }
 
   // ------------------------------------------------------------------ steps
@@ -423,6 +578,10 @@ class Engine final : public EngineBase {
     if (cudaMemcpyAsync(dst, dimg_, img_bytes, cudaMemcpyDeviceToDevice, st_))
       return fail_cuda(cudaGetLastError(), "export fakes");
     return PARAGAN_OK;
+  }
+  size_t state_floats(paragan_net net) override {
+    const Net& N = net == PARAGAN_NET_D ? D_ : G_;
+    return (size_t)(N.n + N.nu);
   }
   paragan_status export_state(paragan_net net, float* dst) override {
     if (!ready_ || poisoned_) return PARAGAN_ERR_ORDER;
@@ -649,15 +808,15 @@ class Engine final : public EngineBase {
     float* stage = scratch_f_;
     for (const PEntry& e : N.E) {
       if (e.conv4d) {
-        CK(ohwi_to_oihw(src + e.off, stage + e.off, e.shape[0], e.shape[1], e.shape[2] * e.shape[3], st_));
+        CK(ohwi_to_oihw(src + e.off, stage + e.coff, e.shape[0], e.shape[1], e.shape[2] * e.shape[3], st_));
       } else {
-        CK(cudaMemcpyAsync(stage + e.off, src + e.off, sizeof(float) * e.n, cudaMemcpyDeviceToDevice, st_));
+        CK(cudaMemcpyAsync(stage + e.coff, src + e.off, sizeof(float) * e.n, cudaMemcpyDeviceToDevice, st_));
       }
     }
-    if (scale != 1.0f) CK(scale_f32(stage, N.n, scale, st_));   // sum over ranks -> mean (R15)
-    if (cudaMemcpyAsync(host, stage, sizeof(float) * N.n, cudaMemcpyDeviceToHost, st_))
+    if (scale != 1.0f) CK(scale_f32(stage, N.nc, scale, st_));   // sum over ranks -> mean (R15)
+    if (cudaMemcpyAsync(host, stage, sizeof(float) * N.nc, cudaMemcpyDeviceToHost, st_))
       return fail_cuda(cudaGetLastError(), "export copy");
-    if (with_u && cudaMemcpyAsync(host + N.n, N.u, sizeof(float) * N.nu, cudaMemcpyDeviceToHost, st_))
+    if (with_u && cudaMemcpyAsync(host + N.nc, N.u, sizeof(float) * N.nu, cudaMemcpyDeviceToHost, st_))
       return fail_cuda(cudaGetLastError(), "export u");
     return sync_ok();
   }
@@ -715,7 +874,7 @@ class Engine final : public EngineBase {
           e.u_off = N->nu;
           N->nu += e.shape[0];
           e.v_off = N->nv;
-          N->nv += e.n / e.shape[0];
+          N->nv += ((e.n / e.shape[0]) + 3) & ~3LL;   // 16-byte aligned v / t slices (float4 passes)
           e.job = (int)N->sn_entries.size();
           N->sn_entries.push_back((int)(&e - N->E.data()));
         }
@@ -779,10 +938,10 @@ class Engine final : public EngineBase {
         const PEntry& e = N->E[ei];
         const long long K = e.n / e.shape[0];
         const int nrc = ceil_div(e.shape[0], 128);
-        nb1 += ceil_div(K, 256) * nrc;
-        nb1b += ceil_div(K, 256);
+        nb1 += ceil_div(K, sn_cols_per_block(K)) * nrc;
+        nb1b += ceil_div(K, sn_cols_per_block(K));
         nb2 += ceil_div(e.shape[0], 8);
-        npart += nrc * K;
+        npart += ((long long)nrc * K + 3) & ~3LL;
         nbw += ceil_div(e.n, 4096);
       }
       N->nb1 = (int)nb1;
@@ -1164,8 +1323,9 @@ class Engine final : public EngineBase {
         j.rows = e.shape[0];
         j.K = (int)(e.n / e.shape[0]);
         j.nrc = ceil_div(j.rows, 128);
+        j.eps = cfg_.sn_eps;
         j.part = N->sn_part + part_off;
-        part_off += (long long)j.nrc * j.K;
+        part_off += ((long long)j.nrc * j.K + 3) & ~3LL;
         j.grad = N->g + e.off;
         const int ji = (int)jobs.size();
         j.coef = N->sn_coef + ji;
@@ -1173,9 +1333,10 @@ class Engine final : public EngineBase {
         j.bwd_nblk = ceil_div(e.n, 4096);
         bstart.push_back(bw);
         bw += j.bwd_nblk;
+        const int cpb = sn_cols_per_block(j.K);
         for (int rc = 0; rc < j.nrc; ++rc)
-          for (int k = 0; k < j.K; k += 256) { b1j.push_back(ji); b1k.push_back(k); b1r.push_back(rc); }
-        for (int k = 0; k < j.K; k += 256) { b1bj.push_back(ji); b1bk.push_back(k); }
+          for (int k = 0; k < j.K; k += cpb) { b1j.push_back(ji); b1k.push_back(k); b1r.push_back(rc); }
+        for (int k = 0; k < j.K; k += cpb) { b1bj.push_back(ji); b1bk.push_back(k); }
         for (int r = 0; r < j.rows; r += 8) { b2j.push_back(ji); b2r.push_back(r); }
         jobs.push_back(j);
       }
@@ -1287,7 +1448,7 @@ class Engine final : public EngineBase {
         long long acc = 0;
         for (auto& j : lst) {
           st.push_back(acc);
-          acc += pass == 0 ? sn_pack_prepare(j) : (long long)j.taps * ceil_div(j.rows, 32) * ceil_div(j.cin, 32);
+          acc += pass == 0 ? sn_pack_prepare(j) : sn_pack_t_prepare(j);
         }
         (pass == 0 ? N->pf_blocks : N->pb_blocks) = acc;
         CK(cudaMemcpyAsync(pass == 0 ? N->pf_d : N->pb_d, lst.data(), lst.size() * sizeof(SnPack),
@@ -2291,6 +2452,13 @@ class Engine final : public EngineBase {
   void* dimg_ = nullptr;
   void* dimg_grad_ = nullptr;
   float* dfake_keep_ = nullptr;   // test hook buffer (PARAGAN_FLAG_KEEP_DFAKE), allocated on first use
+  // asynchronous checkpoint writer (allocated on the first save)
+  void* ck_dev_ = nullptr;
+  void* ck_host_ = nullptr;
+  cudaStream_t ck_stream_ = nullptr;
+  cudaEvent_t ck_ev_snap_ = nullptr, ck_ev_done_ = nullptr;
+  std::thread ck_thread_;
+  volatile paragan_status ck_status_ = PARAGAN_OK;
   bool dfake_valid_ = false;
   int dimg_idx_ = 0;
   float* demb_hat_ = nullptr;

@@ -34,6 +34,10 @@ class EngineBase {
   virtual paragan_status generate(const float* z, const int32_t* y, void* dst) = 0;
   virtual paragan_status export_fakes(void* dst) = 0;
   virtual paragan_status export_state(paragan_net net, float* dst) = 0;
+  virtual size_t state_floats(paragan_net net) = 0;
+  virtual paragan_status checkpoint_save_async(const char* path) = 0;
+  virtual paragan_status checkpoint_wait() = 0;
+  virtual paragan_status checkpoint_load(const char* path) = 0;
   virtual paragan_status import_state(paragan_net net, const float* src) = 0;
   virtual uint64_t launches() const = 0;
   virtual paragan_status profile(int enable) = 0;

@@ -1542,44 +1542,101 @@ __global__ void k_softmax_bwd_rows(const float* __restrict__ S, const float* __r
 }
 
 // ===================================================================== SN
-// pass 1a: part[rc][k] = sum_{r in chunk rc} W[r][k] u[r]   (block = 256 columns x 128 rows of one job)
+// pass 1a: part[rc][k] = sum_{r in chunk rc} W[r][k] u[r]   (block = 128 rows x sn_cols_per_block(K)
+// columns of one job; with K % 4 == 0 each thread owns 4 consecutive columns: 16-byte row loads)
 __global__ void __launch_bounds__(256) k_sn_wtu(const SnJob* __restrict__ jobs, const int* __restrict__ blk_job,
                                                 const int* __restrict__ blk_k0, const int* __restrict__ blk_rc) {
   const SnJob j = jobs[blk_job[blockIdx.x]];
-  const int k = blk_k0[blockIdx.x] + threadIdx.x;
   const int rc = blk_rc[blockIdx.x];
-  if (k >= j.K) return;
   const int r0 = rc * 128, r1 = min(j.rows, r0 + 128);
+  __shared__ float us[128];
+  if (threadIdx.x < r1 - r0) us[threadIdx.x] = j.u[r0 + threadIdx.x];
+  __syncthreads();
+  if ((j.K & 3) == 0) {
+    const int k = blk_k0[blockIdx.x] + 4 * threadIdx.x;
+    if (k >= j.K) return;
+    const float* w = j.w + (long long)r0 * j.K + k;
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+    int r = r0;
+#pragma unroll 1
+    for (; r + 4 <= r1; r += 4) {   // four rows in flight per thread
+      const float4 w0 = __ldg(reinterpret_cast<const float4*>(w));
+      const float4 w1 = __ldg(reinterpret_cast<const float4*>(w + j.K));
+      const float4 w2 = __ldg(reinterpret_cast<const float4*>(w + 2 * (long long)j.K));
+      const float4 w3 = __ldg(reinterpret_cast<const float4*>(w + 3 * (long long)j.K));
+      const float u0 = us[r - r0], u1 = us[r - r0 + 1], u2 = us[r - r0 + 2], u3 = us[r - r0 + 3];
+      a.x = fmaf(w3.x, u3, fmaf(w2.x, u2, fmaf(w1.x, u1, fmaf(w0.x, u0, a.x))));
+      a.y = fmaf(w3.y, u3, fmaf(w2.y, u2, fmaf(w1.y, u1, fmaf(w0.y, u0, a.y))));
+      a.z = fmaf(w3.z, u3, fmaf(w2.z, u2, fmaf(w1.z, u1, fmaf(w0.z, u0, a.z))));
+      a.w = fmaf(w3.w, u3, fmaf(w2.w, u2, fmaf(w1.w, u1, fmaf(w0.w, u0, a.w))));
+      w += 4 * (long long)j.K;
+    }
+    for (; r < r1; ++r) {
+      const float4 w0 = __ldg(reinterpret_cast<const float4*>(w));
+      const float u0 = us[r - r0];
+      a.x = fmaf(w0.x, u0, a.x);
+      a.y = fmaf(w0.y, u0, a.y);
+      a.z = fmaf(w0.z, u0, a.z);
+      a.w = fmaf(w0.w, u0, a.w);
+      w += j.K;
+    }
+    *reinterpret_cast<float4*>(j.part + (long long)rc * j.K + k) = a;
+    return;
+  }
+  const int k = blk_k0[blockIdx.x] + threadIdx.x;
+  if (k >= j.K) return;
   float a = 0.0f;
-  for (int r = r0; r < r1; ++r) a = fmaf(j.w[(long long)r * j.K + k], j.u[r], a);
+  for (int r = r0; r < r1; ++r) a = fmaf(j.w[(long long)r * j.K + k], us[r - r0], a);
   j.part[(long long)rc * j.K + k] = a;
 }
 // pass 1b: t[k] = sum_rc part[rc][k] (fixed order)
 __global__ void __launch_bounds__(256) k_sn_wtu_reduce(const SnJob* __restrict__ jobs, const int* __restrict__ blk_job,
                                                        const int* __restrict__ blk_k0) {
   const SnJob j = jobs[blk_job[blockIdx.x]];
+  if ((j.K & 3) == 0) {
+    const int k = blk_k0[blockIdx.x] + 4 * threadIdx.x;
+    if (k >= j.K) return;
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int rc = 0; rc < j.nrc; ++rc) {
+      const float4 p = *reinterpret_cast<const float4*>(j.part + (long long)rc * j.K + k);
+      a.x += p.x;
+      a.y += p.y;
+      a.z += p.z;
+      a.w += p.w;
+    }
+    *reinterpret_cast<float4*>(j.t + k) = a;
+    return;
+  }
   const int k = blk_k0[blockIdx.x] + threadIdx.x;
   if (k >= j.K) return;
   float a = 0.0f;
   for (int rc = 0; rc < j.nrc; ++rc) a += j.part[(long long)rc * j.K + k];
   j.t[k] = a;
 }
-// pass 2: s[r] = sum_k W[r][k] t[k] / ||t||   (block = 8 rows, one warp per row)
+// pass 2: s[r] = sum_k W[r][k] t[k] / ||t||   (block = 8 rows, one warp per row, 16-byte loads)
 __global__ void __launch_bounds__(256) k_sn_wv(const SnJob* __restrict__ jobs, const int* __restrict__ blk_job,
                                                const int* __restrict__ blk_r0) {
   const SnJob j = jobs[blk_job[blockIdx.x]];
   __shared__ float red[8];
   __shared__ float s_inv;
+  const bool v4 = (j.K & 3) == 0;
   // ||t|| (every block recomputes it: K <= 14k floats from L2)
   float q = 0.0f;
-  for (int k = threadIdx.x; k < j.K; k += 256) q = fmaf(j.t[k], j.t[k], q);
+  if (v4) {
+    for (int k = threadIdx.x; k < (j.K >> 2); k += 256) {
+      const float4 t = reinterpret_cast<const float4*>(j.t)[k];
+      q = fmaf(t.x, t.x, fmaf(t.y, t.y, fmaf(t.z, t.z, fmaf(t.w, t.w, q))));
+    }
+  } else {
+    for (int k = threadIdx.x; k < j.K; k += 256) q = fmaf(j.t[k], j.t[k], q);
+  }
   q = warp_sum(q);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = q;
   __syncthreads();
   if (threadIdx.x == 0) {
     float a = 0.0f;
     for (int i = 0; i < 8; ++i) a += red[i];
-    s_inv = 1.0f / fmaxf(sqrtf(a), 1e-12f);
+    s_inv = 1.0f / fmaxf(sqrtf(a), j.eps);
   }
   __syncthreads();
   const float inv = s_inv;
@@ -1590,7 +1647,16 @@ __global__ void __launch_bounds__(256) k_sn_wv(const SnJob* __restrict__ jobs, c
   }
   if (r >= j.rows) return;
   float a = 0.0f;
-  for (int k = lane; k < j.K; k += 32) a = fmaf(j.w[(long long)r * j.K + k], j.t[k], a);
+  if (v4) {
+    const float4* w = reinterpret_cast<const float4*>(j.w + (long long)r * j.K);
+    const float4* t = reinterpret_cast<const float4*>(j.t);
+    for (int k = lane; k < (j.K >> 2); k += 32) {
+      const float4 x = __ldg(w + k), y = t[k];
+      a = fmaf(x.x, y.x, fmaf(x.y, y.y, fmaf(x.z, y.z, fmaf(x.w, y.w, a))));
+    }
+  } else {
+    for (int k = lane; k < j.K; k += 32) a = fmaf(j.w[(long long)r * j.K + k], j.t[k], a);
+  }
   a = warp_sum(a);
   if (lane == 0) j.s[r] = a * inv;
 }
@@ -1609,10 +1675,10 @@ __global__ void k_sn_finish(const SnJob* __restrict__ jobs) {
     for (int i = 0; i < 8; ++i) a += red[i];
     s_n = sqrtf(a);
     j.sigma[0] = s_n;   // sigma = u'^T W v = ||W v||
-    j.sigma[1] = 1.0f / s_n;
+    j.sigma[1] = 1.0f / fmaxf(s_n, j.eps);
   }
   __syncthreads();
-  const float inv = 1.0f / fmaxf(s_n, 1e-12f);
+  const float inv = 1.0f / fmaxf(s_n, j.eps);
   for (int r = threadIdx.x; r < j.rows; r += 256) j.u[r] = j.s[r] * inv;
 }
 constexpr int kSnPackItems = 4;
@@ -1680,11 +1746,13 @@ __global__ void __launch_bounds__(256) k_sn_pack(const SnPack* __restrict__ jobs
   if (J.dst_bf16) reinterpret_cast<bf16*>(J.dst)[d] = __float2bfloat16_rn(v);
   else reinterpret_cast<float*>(J.dst)[d] = v;
 }
-// dgrad-layout pack through a 32x32 shared-memory tile: reads W[o][t][c] along c,
-// writes Wt[c][T-1-t][o] along o (both coalesced).  One block = (job, t, o-tile, c-tile).
+// dgrad-layout pack: reads W[o][t][c] along c, writes Wt[c][T-1-t][o] along o (both coalesced).
+// vec8 jobs (rows, dst_rows, row offset % 8 == 0, cin % 4 == 0, bf16): one block = (job, t, 64-o tile,
+// 64-c tile) staged through shared memory, 16-byte float4 loads and 16-byte (8 x bf16) stores; other
+// jobs: 32x32 tiles, scalar.
 __global__ void __launch_bounds__(256) k_sn_pack_t(const SnPack* __restrict__ jobs, const long long* __restrict__ blk_start,
                                                    int n_jobs) {
-  __shared__ float tile[32][33];
+  __shared__ float tile[64][65];
   int lo = 0, hi = n_jobs - 1;
   const long long b = blockIdx.x;
   while (lo < hi) {
@@ -1692,14 +1760,51 @@ __global__ void __launch_bounds__(256) k_sn_pack_t(const SnPack* __restrict__ jo
     if (blk_start[mid] <= b) lo = mid; else hi = mid - 1;
   }
   const SnPack J = jobs[lo];
-  const int ot = (J.rows + 31) / 32, ct = (J.cin + 31) / 32;
+  const float inv = J.sigma[1];
   long long r = b - blk_start[lo];
+  if (J.vec8) {
+    const int ot = (J.rows + 63) / 64, ct = (J.cin + 63) / 64;
+    const int cti = (int)(r % ct);
+    r /= ct;
+    const int oti = (int)(r % ot);
+    const int t = (int)(r / ot);
+    const int o0 = oti * 64, c0 = cti * 64;
+    for (int i = threadIdx.x; i < 64 * 16; i += 256) {
+      const int ol = i >> 4, c4 = (i & 15) * 4;
+      const int o = o0 + ol, c = c0 + c4;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (o < J.rows && c < J.cin) v = __ldg(reinterpret_cast<const float4*>(J.w + ((long long)o * J.taps + t) * J.cin + c));
+      tile[ol][c4] = v.x * inv;
+      tile[ol][c4 + 1] = v.y * inv;
+      tile[ol][c4 + 2] = v.z * inv;
+      tile[ol][c4 + 3] = v.w * inv;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 64 * 8; i += 256) {
+      const int cl = i >> 3, og = (i & 7) * 8;
+      const int c = c0 + cl, o = o0 + og;
+      if (c < J.cin && o < J.rows) {
+        uint4 q;
+        __nv_bfloat162 h0 = __floats2bfloat162_rn(tile[og][cl], tile[og + 1][cl]);
+        __nv_bfloat162 h1 = __floats2bfloat162_rn(tile[og + 2][cl], tile[og + 3][cl]);
+        __nv_bfloat162 h2 = __floats2bfloat162_rn(tile[og + 4][cl], tile[og + 5][cl]);
+        __nv_bfloat162 h3 = __floats2bfloat162_rn(tile[og + 6][cl], tile[og + 7][cl]);
+        q.x = *reinterpret_cast<uint32_t*>(&h0);
+        q.y = *reinterpret_cast<uint32_t*>(&h1);
+        q.z = *reinterpret_cast<uint32_t*>(&h2);
+        q.w = *reinterpret_cast<uint32_t*>(&h3);
+        const long long d = ((long long)c * J.taps + (J.taps - 1 - t)) * J.dst_rows + (o + J.dst_row_offset);
+        *reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(J.dst) + d) = q;
+      }
+    }
+    return;
+  }
+  const int ot = (J.rows + 31) / 32, ct = (J.cin + 31) / 32;
   const int cti = (int)(r % ct);
   r /= ct;
   const int oti = (int)(r % ot);
   const int t = (int)(r / ot);
   const int o0 = oti * 32, c0 = cti * 32;
-  const float inv = J.sigma[1];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8
   for (int k = ty; k < 32; k += 8) {
     const int o = o0 + k, c = c0 + tx;
@@ -2511,6 +2616,12 @@ long long sn_pack_prepare(SnPack& j) {
   j.vec8 = j.mode == 0 && j.dst_bf16 && j.cin % 8 == 0 && j.dst_cin % 8 == 0 &&
            ((reinterpret_cast<uintptr_t>(j.w) | reinterpret_cast<uintptr_t>(j.dst)) & 15) == 0;
   return ceil_div(n, j.vec8 ? 2048 * kSnPackItems : 256);
+}
+long long sn_pack_t_prepare(SnPack& j) {
+  j.vec8 = j.mode == 1 && j.dst_bf16 && j.rows % 8 == 0 && j.dst_rows % 8 == 0 && j.dst_row_offset % 8 == 0 &&
+           j.cin % 4 == 0 && ((reinterpret_cast<uintptr_t>(j.w) | reinterpret_cast<uintptr_t>(j.dst)) & 15) == 0;
+  if (j.vec8) return (long long)j.taps * ceil_div(j.rows, 64) * ceil_div(j.cin, 64);
+  return (long long)j.taps * ceil_div(j.rows, 32) * ceil_div(j.cin, 32);
 }
 cudaError_t sn_pack(const SnPack* jobs, const long long* blk_start, int n_jobs, long long total_blocks,
                     cudaStream_t st) {

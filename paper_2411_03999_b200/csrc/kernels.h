@@ -233,6 +233,7 @@ struct SnJob {
   float* grad;      // [rows][K] gradient w.r.t. W/sigma (SN backward, in place)
   double* coef;     // [1] SN backward coefficient
   int rows, K, nrc;
+  float eps;        // n(x) = x / max(||x||, eps)  (paragan_config.sn_eps, R4)
   long long bwd_blk0, bwd_nblk;   // SN-backward block range of this job
 };
 struct SnPack {     // one packed copy of W/sigma
@@ -245,10 +246,15 @@ struct SnPack {     // one packed copy of W/sigma
   int dst_row_offset;  // sub-block placement (qkv packing)
   int dst_rows;        // mode 1: total rows (row stride of the transposed layout)
   int dst_cin;         // mode 0: padded input channels (>= cin; pads left untouched = 0)
-  int vec8;            // set by sn_pack_prepare: 8 channels per thread (mode 0, bf16, aligned)
+  int vec8;            // set by sn_pack_prepare: 8 channels per thread (mode 0, bf16, aligned);
+                       // set by sn_pack_t_prepare: 64x64 tiles with 16-byte stores (mode 1)
 };
 // decides SnPack::vec8 and returns the number of 256-thread blocks the job needs in sn_pack
 long long sn_pack_prepare(SnPack& j);
+// the same for the dgrad-layout pack (sn_pack_t)
+long long sn_pack_t_prepare(SnPack& j);
+// columns of W one pass-1 block of the power iteration covers (1024 with float4 rows, else 256)
+inline int sn_cols_per_block(long long K) { return (K % 4 == 0) ? 1024 : 256; }
 // power step over all SN weights of a net: pass 1a blocks = (job, 256 columns, 128-row chunk),
 // pass 1b blocks = (job, 256 columns), pass 2 blocks = (job, 8 rows), pass 3 = one block per job
 cudaError_t sn_power(const SnJob* jobs_dev, int n_jobs, const int* b1_job, const int* b1_k0, const int* b1_rc, int n_b1,

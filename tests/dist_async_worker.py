@@ -26,14 +26,18 @@ def main():
     dist.init_process_group("nccl", device_id=torch.device(dev))
     g_batch, d_batch, n_d = int(os.environ.get("ASYNC_G", 4)), int(os.environ.get("ASYNC_D", 4)), 1
     n_d = g_batch // d_batch
-    ocfg = P.oracle_config(32, 4, 16, 10, 16, 4)
+    from tests.test_gpu_async import SGD_D, SGD_G, sgd_configs
+    ocfg, _, _ = sgd_configs(g_batch, d_batch, n_d)
     gs, ds = bg.g_param_specs(ocfg), bg.d_param_specs(ocfg)
     g0 = inputs.init_params(gs, 81, inputs.ROLE_PARAMS_G)
     d0 = inputs.init_params(ds, 81, inputs.ROLE_PARAMS_D)
 
+    sgd = api.make_policy(rule=api.OPT_SGD)
+
     def make_cfg(b, r, w):
         return api.make_config(resolution=32, ch=4, attn_res=16, n_classes=10, shared_dim=16, z_chunk=4,
-                               local_batch=b, d_steps_per_g=n_d, compute=api.F32, rank=r, world_size=w, device=local)
+                               local_batch=b, d_steps_per_g=n_d, compute=api.F32, rank=r, world_size=w, device=local,
+                               adam_d=SGD_D, adam_g=SGD_G, policy_d=sgd, policy_g=sgd)
 
     da = DistributedAsync(make_cfg, g_batch, d_batch, n_d)
     da.ctx.set_params(api.NET_G, g0)
@@ -73,11 +77,11 @@ def main():
     if da.is_g:
         got = da.ctx.get_params(api.NET_G)
         nt = bg.n_trainable(gs)
-        out["err"] = P.rel(got[:nt], G.flat()[:nt])
+        out["err"] = P.rel(got[:nt] - g0[:nt], G.flat()[:nt] - g0[:nt])
     else:
         got = da.ctx.get_params(api.NET_D)
         nt = bg.n_trainable(ds)
-        out["err"] = P.rel(got[:nt], D.flat()[:nt])
+        out["err"] = P.rel(got[:nt] - d0[:nt], D.flat()[:nt] - d0[:nt])
         out["t_d"] = da.ctx.sync_stats(raise_nonfinite=False).t_d
     da.close()
     print("DISTRESULT " + json.dumps(out), flush=True)

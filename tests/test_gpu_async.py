@@ -10,6 +10,7 @@ import torch
 
 from oracle import async_scheme as OA
 from oracle import biggan as bg
+from oracle import optim as O
 from paper_2411_03999_b200 import api, inputs
 from paper_2411_03999_b200.async_gan import LocalAsync
 from tests import parity as P
@@ -68,13 +69,31 @@ def test_staleness0_equals_sync_iteration_bitwise():
     la.close()
 
 
+SGD_D, SGD_G = (0.1, 0.0, 0.999, None), (0.05, 0.0, 0.999, None)
+
+
+def sgd_configs(g_batch, d_batch, n_d, **kw):
+    """The schedule tests train with plain SGD at a large step (lr 0.1 / 0.05): every update is linear in its
+    gradient, so the comparison measures the schedule (which fakes / which D snapshot each step used) with
+    fp32 noise ~1e-6 — Adam's first steps ~ -lr sign(g) would turn rounding noise on near-zero gradients
+    into full-size sign flips."""
+    ocfg = dataclasses.replace(P.oracle_config(32, 4, 16, 10, 16, 4), adam_d=bg.AdamHP(0.1, 0.0, 0.999, 1e-8),
+                               adam_g=bg.AdamHP(0.05, 0.0, 0.999, 1e-8), policy_d=O.Policy(rule="sgd"),
+                               policy_g=O.Policy(rule="sgd"))
+    sgd = api.make_policy(rule=api.OPT_SGD)
+    cfg_g = api.make_config(**MICRO, local_batch=g_batch, compute=api.F32, adam_d=SGD_D, adam_g=SGD_G, policy_d=sgd,
+                            policy_g=sgd, **kw)
+    cfg_d = api.make_config(**MICRO, local_batch=d_batch, d_steps_per_g=n_d, compute=api.F32, adam_d=SGD_D,
+                            adam_g=SGD_G, policy_d=sgd, policy_g=sgd, **kw)
+    return ocfg, cfg_g, cfg_d
+
+
 @pytest.mark.parametrize("d_batch,g_batch,n_d", [(4, 4, 1), (2, 4, 2)])
 def test_staleness1_matches_oracle_schedule(d_batch, g_batch, n_d):
-    """Three ticks with max_staleness = 1: D on the previous tick's fakes, G through the previous tick's D."""
+    """Three ticks with max_staleness = 1: D on the previous tick's fakes, G through the previous tick's D;
+    the accumulated updates w_3 - w_0 of G and D vs the oracle's schedule at the fp32 bar 1e-4."""
     compute = api.F32
-    ocfg = P.oracle_config(32, 4, 16, 10, 16, 4)
-    cfg_g = api.make_config(**MICRO, local_batch=g_batch, compute=compute)
-    cfg_d = api.make_config(**MICRO, local_batch=d_batch, d_steps_per_g=n_d, compute=compute)
+    ocfg, cfg_g, cfg_d = sgd_configs(g_batch, d_batch, n_d)
     gs, ds = bg.g_param_specs(ocfg), bg.d_param_specs(ocfg)
     g0 = inputs.init_params(gs, 72, inputs.ROLE_PARAMS_G)
     d0 = inputs.init_params(ds, 72, inputs.ROLE_PARAMS_D)
@@ -93,9 +112,9 @@ def test_staleness1_matches_oracle_schedule(d_batch, g_batch, n_d):
     got_g, got_d = la.ctx_g.get_params(api.NET_G), la.ctx_d.get_params(api.NET_D)
     st = la.ctx_d.sync_stats(raise_nonfinite=False)
     la.close()
-    for got, st_, specs in ((got_g, G, gs), (got_d, D, ds)):
+    for got, st_, w0, specs in ((got_g, G, g0, gs), (got_d, D, d0, ds)):
         nt = bg.n_trainable(specs)
-        e = P.rel(got[:nt], st_.flat()[:nt])
-        print("async state rel err", f"{e:.2e}")
+        e = P.rel(got[:nt] - w0[:nt], st_.flat()[:nt] - w0[:nt])
+        print("async update rel err", f"{e:.2e}")
         assert e < 1e-4
     assert st.t_d == 3 * n_d
