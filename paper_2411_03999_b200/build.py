@@ -62,7 +62,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
         objs = list(ex.map(compile_one, SOURCES))
     link = [_nvcc(), *ARCH, "-shared", "-o", LIB + ".tmp", *objs, "-L", libdir, "-lnccl",
-            "-L", "/usr/local/cuda/lib64", "-lcublas", "-Xlinker", f"-rpath,{libdir}"]
+            "-Xlinker", f"-rpath,{libdir}"]
     r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")

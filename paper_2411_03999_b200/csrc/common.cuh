@@ -48,4 +48,24 @@ inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
 
 constexpr int kNumSMs = 148;  // B200
 
+// SMs the persistent grids may occupy (kNumSMs, fewer while a gradient all-reduce overlaps compute, so the
+// NCCL kernels find free SMs instead of waiting behind one-CTA-per-SM grids; engine.cu sets it)
+extern int g_sm_cap;
+inline int sm_cap() { return g_sm_cap; }
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device): the attribute is per device,
+// so a process driving two GPUs sets it on each
+template <auto K>
+cudaError_t set_smem_once(int bytes) {
+  static unsigned long long done = 0;   // bit per device; host-side, one host thread per context
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (done & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done |= bit;
+  return e;
+}
+
 }  // namespace pg

@@ -8,7 +8,6 @@
 // Parameter storage: one flat fp32 buffer per network in canonical order
 // (include/paragan.h), except that conv weights are held OHWI ([C_out][taps]
 // [C_in], the K-major GEMM B operand) instead of OIHW; set/get convert.
-#include <cublas_v2.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -195,20 +194,6 @@ bool arch_for(int res, Arch& a) {
   return false;
 }
 
-// ---------------------------------------------------------------- cuBLAS row-major helper (attention bmm)
-cublasStatus_t gemm_rm(cublasHandle_t h, int batch, int M, int N, int K, const void* A, cudaDataType ta,
-                       long long sab, long long sam, long long sak, const void* B, cudaDataType tb, long long sbb,
-                       long long sbn, long long sbk, void* C, cudaDataType tc, long long scb, long long ldc,
-                       float beta) {
-  const cublasOperation_t opX = (sbn == 1) ? CUBLAS_OP_N : CUBLAS_OP_T;
-  const long long ldx = (sbn == 1) ? sbk : sbn;
-  const cublasOperation_t opY = (sak == 1) ? CUBLAS_OP_N : CUBLAS_OP_T;
-  const long long ldy = (sak == 1) ? sam : sak;
-  const float alpha = 1.0f;
-  return cublasGemmStridedBatchedEx(h, opX, opY, N, M, K, &alpha, B, tb, (int)ldx, sbb, A, ta, (int)ldy, sab, &beta,
-                                    C, tc, (int)ldc, scb, batch, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
-}
-
 }  // namespace
 
 #define CK(x)                                                   \
@@ -243,8 +228,13 @@ class Engine final : public EngineBase {
     if (ck_ev_snap_) cudaEventDestroy(ck_ev_snap_);
     if (ck_ev_done_) cudaEventDestroy(ck_ev_done_);
     if (dfake_keep_) cudaFree(dfake_keep_);
+    if (pending_d_) cudaStreamSynchronize(cs_);
+    if (gcomm_) ncclCommDestroy(gcomm_);
+    if (bncomm_) ncclCommDestroy(bncomm_);
+    if (cs_) cudaStreamDestroy(cs_);
+    if (ev_grad_) cudaEventDestroy(ev_grad_);
+    if (ev_ar_) cudaEventDestroy(ev_ar_);
     if (comm_) ncclCommDestroy(comm_);
-    if (cublas_) cublasDestroy(cublas_);
   }
 
   // ------------------------------------------------------------------ plan
@@ -274,8 +264,6 @@ class Engine final : public EngineBase {
     a.base = static_cast<char*>(ws);
     build(a);
     if (cudaMemsetAsync(ws, 0, a.off, st_) != cudaSuccess) return fail_cuda(cudaGetLastError(), "memset ws");
-    if (cublasCreate(&cublas_) != CUBLAS_STATUS_SUCCESS) return fail_msg(PARAGAN_ERR_CUDA, "cublasCreate");
-    cublasSetStream(cublas_, st_);
     paragan_status s = upload_tables();
     if (s != PARAGAN_OK) return s;
     if (fill_const(ones_buf_, maxc_, 1.0f, st_) != cudaSuccess) return fail_cuda(cudaGetLastError(), "ones");
@@ -284,6 +272,25 @@ class Engine final : public EngineBase {
       std::memcpy(&uid, id, sizeof(uid));
       ncclResult_t r = ncclCommInitRank(&comm_, cfg_.world_size, uid, cfg_.rank);
       if (r != ncclSuccess) return fail_msg(PARAGAN_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+      // A12 overlap: D's gradient all-reduce runs on its own stream and communicator (at most
+      // kOverlapCTAs CTAs) while G's forward runs with kOverlapSMs SMs left free; the batch-norm / loss
+      // all-reduces get a 2-CTA communicator so the two never compete for more SMs than are reserved
+      const char* ov = std::getenv("PARAGAN_OVERLAP");
+      overlap_ = (ov == nullptr || std::atoi(ov) != 0) && !cfg_.grad_comm_bf16;
+      if (const char* e = std::getenv("PARAGAN_OVERLAP_SMS")) overlap_sms_ = std::atoi(e);
+      if (const char* e = std::getenv("PARAGAN_OVERLAP_BLOCKS")) overlap_blocks_ = std::atoi(e);
+      if (overlap_) {
+        ncclConfig_t gc = NCCL_CONFIG_INITIALIZER, bc = NCCL_CONFIG_INITIALIZER;
+        gc.maxCTAs = kOverlapCTAs;
+        bc.maxCTAs = 2;
+        r = ncclCommSplit(comm_, 0, cfg_.rank, &gcomm_, &gc);
+        if (r == ncclSuccess) r = ncclCommSplit(comm_, 0, cfg_.rank, &bncomm_, &bc);
+        if (r != ncclSuccess) return fail_msg(PARAGAN_ERR_NCCL, std::string("ncclCommSplit: ") + ncclGetErrorString(r));
+        if (cudaStreamCreateWithFlags(&cs_, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ev_grad_, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ev_ar_, cudaEventDisableTiming) != cudaSuccess)
+          return fail_cuda(cudaGetLastError(), "overlap stream");
+      }
     }
     if (cudaStreamSynchronize(st_) != cudaSuccess) return fail_cuda(cudaGetLastError(), "init sync");
     ready_ = true;
@@ -293,6 +300,7 @@ class Engine final : public EngineBase {
   // ------------------------------------------------------------------ params
   paragan_status init_params(float attn_gamma) override {
     if (!ready_) return PARAGAN_ERR_ORDER;
+    CKS(flush_d());
     uint64_t salt = 0;
     for (Net* N : {&G_, &D_}) {
       ++salt;
@@ -326,6 +334,7 @@ class Engine final : public EngineBase {
 
   paragan_status set_params(paragan_net net, const float* host, size_t n) override {
     if (!ready_) return PARAGAN_ERR_ORDER;
+    CKS(flush_d());
     Net& N = net == PARAGAN_NET_D ? D_ : G_;
     if (!host || n != (size_t)(N.nc + N.nu)) return fail_arg("set_params: size mismatch");
     // canonical -> staging (g buffer, canonical offsets) -> internal (conv OIHW -> OHWI, aligned offsets)
@@ -347,18 +356,21 @@ class Engine final : public EngineBase {
   }
   paragan_status get_params(paragan_net net, float* host, size_t n) override {
     if (!ready_) return PARAGAN_ERR_ORDER;
+    CKS(flush_d());
     Net& N = net == PARAGAN_NET_D ? D_ : G_;
     if (!host || n != (size_t)(N.nc + N.nu)) return fail_arg("get_params: size mismatch");
     return export_flat(N, N.p, host, true);
   }
   paragan_status get_grads(paragan_net net, float* host, size_t n) override {
     if (!ready_) return PARAGAN_ERR_ORDER;
+    CKS(flush_d());
     Net& N = net == PARAGAN_NET_D ? D_ : G_;
     if (!host || n != (size_t)N.nc) return fail_arg("get_grads: size mismatch");
     return export_flat(N, N.g, host, false, 1.0f / N.gsum);
   }
   paragan_status set_grads(paragan_net net, const float* host, size_t n) override {
     if (!ready_ || poisoned_) return PARAGAN_ERR_ORDER;
+    CKS(flush_d());
     Net& N = net == PARAGAN_NET_D ? D_ : G_;
     if (!host || n != (size_t)N.nc) return fail_arg("set_grads: size mismatch");
     // canonical -> staging -> internal layout (conv OIHW -> OHWI), as set_params
@@ -450,6 +462,7 @@ class Engine final : public EngineBase {
   }
   paragan_status checkpoint_save_async(const char* path) override {
     if (!ready_ || poisoned_) return PARAGAN_ERR_ORDER;
+    CKS(flush_d());
     if (!path) return fail_arg("checkpoint: null path");
     paragan_status ws = checkpoint_wait();
     if (ws != PARAGAN_OK) return ws;
@@ -504,6 +517,7 @@ class Engine final : public EngineBase {
   }
   paragan_status checkpoint_load(const char* path) override {
     if (!ready_ || poisoned_) return PARAGAN_ERR_ORDER;
+    CKS(flush_d());
     if (!path) return fail_arg("checkpoint: null path");
     paragan_status ws = checkpoint_wait();
     if (ws != PARAGAN_OK) return ws;
@@ -585,6 +599,7 @@ class Engine final : public EngineBase {
   }
   paragan_status export_state(paragan_net net, float* dst) override {
     if (!ready_ || poisoned_) return PARAGAN_ERR_ORDER;
+    CKS(flush_d());
     Net& N = net == PARAGAN_NET_D ? D_ : G_;
     if (cudaMemcpyAsync(dst, N.p, sizeof(float) * N.n, cudaMemcpyDeviceToDevice, st_) ||
         cudaMemcpyAsync(dst + N.n, N.u, sizeof(float) * N.nu, cudaMemcpyDeviceToDevice, st_))
@@ -593,13 +608,23 @@ class Engine final : public EngineBase {
   }
   paragan_status import_state(paragan_net net, const float* src) override {
     if (!ready_ || poisoned_) return PARAGAN_ERR_ORDER;
+    CKS(flush_d());
     Net& N = net == PARAGAN_NET_D ? D_ : G_;
     if (cudaMemcpyAsync(N.p, src, sizeof(float) * N.n, cudaMemcpyDeviceToDevice, st_) ||
         cudaMemcpyAsync(N.u, src + N.n, sizeof(float) * N.nu, cudaMemcpyDeviceToDevice, st_))
       return fail_cuda(cudaGetLastError(), "import_state");
     return PARAGAN_OK;
   }
+  // D's deferred update: wait for the overlapped all-reduce, then the optimiser step (before D is read again)
+  paragan_status flush_d() {
+    g_sm_cap = kNumSMs;
+    if (!pending_d_) return PARAGAN_OK;
+    pending_d_ = false;
+    if (cudaStreamWaitEvent(st_, ev_ar_, 0) != cudaSuccess) return fail_cuda(cudaGetLastError(), "overlap wait");
+    return update_net(PARAGAN_NET_D);
+  }
   paragan_status d_step_body(const void* real, const int32_t* real_y, const int32_t* fake_y, uint32_t flags) {
+    CKS(flush_d());
     // reals into rows [B, 2B) (one D pass over the concatenated batch)
     const size_t img_bytes = (size_t)B_ * R_ * R_ * cpad_ * sizeof(T);
     if (cudaMemcpyAsync(static_cast<char*>(dimg_) + img_bytes, real, img_bytes, cudaMemcpyDeviceToDevice, st_))
@@ -616,8 +641,20 @@ class Engine final : public EngineBase {
     if (dcgan_) CKS(d_backward_dc(2 * B_, true, false));
     else CKS(d_backward(2 * B_, true, false));
     CKS(sn_backward_net(D_));
-    if (!(flags & PARAGAN_FLAG_NO_ALLREDUCE)) CKS(allreduce(PARAGAN_NET_D));
-    if (!(flags & PARAGAN_FLAG_NO_UPDATE)) CKS(update(PARAGAN_NET_D));
+    if (overlap_ && !(flags & (PARAGAN_FLAG_NO_ALLREDUCE | PARAGAN_FLAG_NO_UPDATE))) {
+      // A12: the all-reduce overlaps the next G forward; the update is applied before D is used again
+      if (cudaEventRecord(ev_grad_, st_) != cudaSuccess || cudaStreamWaitEvent(cs_, ev_grad_, 0) != cudaSuccess)
+        return fail_cuda(cudaGetLastError(), "overlap record");
+      const ncclResult_t r = ncclAllReduce(D_.g, D_.g, (size_t)D_.n, ncclFloat32, ncclSum, gcomm_, cs_);
+      if (r != ncclSuccess) return fail_msg(PARAGAN_ERR_NCCL, std::string("grad allreduce: ") + ncclGetErrorString(r));
+      ++launches_;
+      if (cudaEventRecord(ev_ar_, cs_) != cudaSuccess) return fail_cuda(cudaGetLastError(), "overlap record");
+      D_.gsum = (float)cfg_.world_size;
+      pending_d_ = true;
+    } else {
+      if (!(flags & PARAGAN_FLAG_NO_ALLREDUCE)) CKS(allreduce(PARAGAN_NET_D));
+      if (!(flags & PARAGAN_FLAG_NO_UPDATE)) CKS(update_net(PARAGAN_NET_D));
+    }
     ++d_since_g_;
     return PARAGAN_OK;
   }
@@ -635,6 +672,7 @@ class Engine final : public EngineBase {
     if (dcgan_) CKS(g_forward_dc(z));
     else CKS(g_forward(z, y, true));
     CK(cudaMemcpyAsync(ylab_, y, sizeof(int32_t) * B_, cudaMemcpyDeviceToDevice, st_));
+    CKS(flush_d());   // D's update (its all-reduce overlapped the G forward above)
     CKS(sn_forward(D_, true));
     if (dcgan_) CKS(d_forward_dc(B_));
     else CKS(d_forward(B_));
@@ -660,6 +698,7 @@ class Engine final : public EngineBase {
 
   paragan_status allreduce(paragan_net net) override {
     if (!ready_ || poisoned_) return PARAGAN_ERR_ORDER;
+    CKS(flush_d());
     Net& N = net == PARAGAN_NET_D ? D_ : G_;
     if (cfg_.world_size > 1 && N.gsum == 1.0f) {
       // sum over ranks; the mean's 1/W (R15) is folded into the update and into get_grads
@@ -677,6 +716,10 @@ class Engine final : public EngineBase {
 
   paragan_status update(paragan_net net) override {
     if (!ready_ || poisoned_) return PARAGAN_ERR_ORDER;
+    CKS(flush_d());
+    return update_net(net);
+  }
+  paragan_status update_net(paragan_net net) {
     Net& N = net == PARAGAN_NET_D ? D_ : G_;
     const paragan_adam& h = net == PARAGAN_NET_D ? cfg_.adam_d : cfg_.adam_g;
     const float gscale = 1.0f / N.gsum;
@@ -715,6 +758,7 @@ class Engine final : public EngineBase {
 
   paragan_status sync_stats(paragan_stats* out) override {
     if (!ready_) return PARAGAN_ERR_ORDER;
+    CKS(flush_d());
     float ld[4], lg[4];
     long long td, tg;
     int nf;
@@ -1645,10 +1689,8 @@ class Engine final : public EngineBase {
                        const void* Bm, long long sbb, long long sbn, long long sbk, void* C, bool c_f32, long long scb,
                        long long ldc) {
     if constexpr (kBF) {
-      cublasStatus_t s = gemm_rm(cublas_, batch, M, N, K, A, CUDA_R_16BF, sab, sam, sak, Bm, CUDA_R_16BF, sbb, sbn, sbk,
-                                 C, c_f32 ? CUDA_R_32F : CUDA_R_16BF, scb, ldc, 0.0f);
-      ++launches_;
-      if (s != CUBLAS_STATUS_SUCCESS) return fail_msg(PARAGAN_ERR_CUDA, "cublas gemm " + std::to_string((int)s));
+      CK(gemm_bf16_batched(batch, M, N, K, static_cast<const bf16*>(A), sab, sam, sak, static_cast<const bf16*>(Bm), sbb,
+                           sbn, sbk, C, c_f32, scb, ldc, st_));
       return PARAGAN_OK;
     } else {
       (void)c_f32;
@@ -1662,7 +1704,7 @@ class Engine final : public EngineBase {
     CK(bn_stats<T>(static_cast<const T*>(x), M, C, dpart_, kMaxPartialBlocks, sums, st_));
     ++launches_;
     if (cfg_.world_size > 1) {
-      CKS(nccl_sum(sums, (size_t)2 * C, ncclFloat64, "bn allreduce"));
+      CKS(nccl_sum(sums, (size_t)2 * C, ncclFloat64, "bn allreduce", bncomm_));
     }
     CK(bn_finalize(sums, C, (double)M * cfg_.world_size, cfg_.bn_eps, mean, rstd, st_));
     return PARAGAN_OK;
@@ -1670,13 +1712,13 @@ class Engine final : public EngineBase {
   // losses / logit means are local means: sum over ranks here, / world_size in sync_stats (R15);
   // the non-finite flag (loss[3]) becomes the number of ranks that saw one
   // in-place sum over ranks on the compute stream; timed as profile kind 2 (collectives)
-  paragan_status nccl_sum(void* buf, size_t count, ncclDataType_t dt, const char* what) {
+  paragan_status nccl_sum(void* buf, size_t count, ncclDataType_t dt, const char* what, ncclComm_t comm = nullptr) {
     ncclResult_t r = ncclSuccess;
     const size_t bytes = count * (dt == ncclFloat64 ? 8 : dt == ncclBfloat16 ? 2 : 4);
     char label[48];
     std::snprintf(label, sizeof(label), "%s %zu B", what, bytes);
     cudaError_t e = timed(2, (double)bytes, [&] {
-      r = ncclAllReduce(buf, buf, count, dt, ncclSum, comm_, st_);
+      r = ncclAllReduce(buf, buf, count, dt, ncclSum, comm ? comm : comm_, st_);
       return r == ncclSuccess ? cudaSuccess : cudaErrorUnknown;
     }, label);
     if (r != ncclSuccess) return fail_msg(PARAGAN_ERR_NCCL, std::string(what) + ": " + ncclGetErrorString(r));
@@ -1685,13 +1727,13 @@ class Engine final : public EngineBase {
   }
   paragan_status allreduce_loss(float* loss4) {
     if (cfg_.world_size > 1) {
-      CKS(nccl_sum(loss4, 4, ncclFloat32, "loss allreduce"));
+      CKS(nccl_sum(loss4, 4, ncclFloat32, "loss allreduce", bncomm_));
     }
     return PARAGAN_OK;
   }
   paragan_status allreduce_small(double* p, int n) {
     if (cfg_.world_size > 1) {
-      CKS(nccl_sum(p, (size_t)n, ncclFloat64, "allreduce"));
+      CKS(nccl_sum(p, (size_t)n, ncclFloat64, "allreduce", bncomm_));
     }
     return PARAGAN_OK;
   }
@@ -1714,6 +1756,8 @@ class Engine final : public EngineBase {
     CK(gemm_f32_grouped(cbn_fwd_d_, cbn_fwd_n_, cbn_fwd_tiles_, st_));
     CK(convert_f32<T>(h0f_, static_cast<T*>(gb_[0].x), (long long)B * 16 * c0_, st_));
     for (size_t i = 0; i < gb_.size(); ++i) {
+      // while D's gradient all-reduce is in flight, the first blocks' persistent grids leave SMs free for it
+      g_sm_cap = (pending_d_ && (int)i < overlap_blocks_) ? kNumSMs - overlap_sms_ : kNumSMs;
       GBlock& b = gb_[i];
       const int H = b.hin, H2 = 2 * H;
       // CBN1 -> ReLU -> up x2 (fused)
@@ -2413,7 +2457,13 @@ class Engine final : public EngineBase {
   paragan_config cfg_;
   cudaStream_t st_;
   ncclComm_t comm_ = nullptr;
-  cublasHandle_t cublas_ = nullptr;
+  // A12 overlap: D's gradient all-reduce in flight on cs_ (gcomm_) while G's forward runs; applied by flush_d()
+  static constexpr int kOverlapCTAs = 8;
+  ncclComm_t gcomm_ = nullptr, bncomm_ = nullptr;
+  cudaStream_t cs_ = nullptr;
+  cudaEvent_t ev_grad_ = nullptr, ev_ar_ = nullptr;
+  bool overlap_ = false, pending_d_ = false;
+  int overlap_sms_ = 16, overlap_blocks_ = 3;
   bool ready_ = false, poisoned_ = false, planned_ = false, ones_ready_ = false;
   bool subpix_ = false;   // G conv1 as four phase 2x2 convs of the low-resolution input (NEXT-1)
   bool dcgan_ = false;    // SN-DCGAN (config 1) instead of BigGAN

@@ -11,6 +11,8 @@
 
 namespace pg {
 
+int g_sm_cap = kNumSMs;
+
 namespace {
 
 inline int grid_for(long long n, int threads, int max_waves = 8) {
@@ -86,9 +88,9 @@ __global__ void k_unpack(const TS* __restrict__ src, float* __restrict__ dst, in
 
 // ===================================================================== small GEMM
 // 64x64 tile, 256 threads, 4x4 per thread, K chunk 16
-template <typename TC>
-__global__ void __launch_bounds__(256) k_gemm(int M, int N, int K, const float* __restrict__ A, long long sab,
-                                              long long sam, long long sak, const float* __restrict__ B, long long sbb,
+template <typename TI, typename TC>
+__global__ void __launch_bounds__(256) k_gemm(int M, int N, int K, const TI* __restrict__ A, long long sab,
+                                              long long sam, long long sak, const TI* __restrict__ B, long long sbb,
                                               long long sbn, long long sbk, TC* __restrict__ C, long long scb,
                                               long long ldc, float beta, const float* __restrict__ bias) {
   __shared__ __align__(16) float As[16][68];
@@ -106,11 +108,11 @@ __global__ void __launch_bounds__(256) k_gemm(int M, int N, int K, const float* 
       int mm, kk;
       if (sak == 1) { mm = i >> 4; kk = i & 15; } else { kk = i >> 6; mm = i & 63; }
       const int m = m0 + mm, k = k0 + kk;
-      As[kk][mm] = (m < M && k < K) ? A[m * sam + k * sak] : 0.0f;
+      As[kk][mm] = (m < M && k < K) ? to_f<TI>(A[m * sam + k * sak]) : 0.0f;
       int nn, kb;
       if (sbk == 1) { nn = i >> 4; kb = i & 15; } else { kb = i >> 6; nn = i & 63; }
       const int n = n0 + nn, k2 = k0 + kb;
-      Bs[kb][nn] = (n < N && k2 < K) ? B[n * sbn + k2 * sbk] : 0.0f;
+      Bs[kb][nn] = (n < N && k2 < K) ? to_f<TI>(B[n * sbn + k2 * sbk]) : 0.0f;
     }
     __syncthreads();
 #pragma unroll
@@ -2153,7 +2155,7 @@ cudaError_t gemm_f32(int M, int N, int K, const float* A, long long sam, long lo
                      long long sbk, float* C, long long ldc, float beta, const float* bias, cudaStream_t st) {
   if (M <= 0 || N <= 0) return cudaSuccess;
   dim3 g(ceil_div(N, 64), ceil_div(M, 64), 1);
-  k_gemm<float><<<g, 256, 0, st>>>(M, N, K, A, 0, sam, sak, B, 0, sbn, sbk, C, 0, ldc, beta, bias);
+  k_gemm<float, float><<<g, 256, 0, st>>>(M, N, K, A, 0, sam, sak, B, 0, sbn, sbk, C, 0, ldc, beta, bias);
   return cudaGetLastError();
 }
 int gemm_grouped_plan(GemmProblem* probs, int nprob) {
@@ -2173,7 +2175,19 @@ cudaError_t gemm_f32_batched(int batch, int M, int N, int K, const float* A, lon
                              long long sak, const float* B, long long sbb, long long sbn, long long sbk, float* C,
                              long long scb, long long ldc, float beta, cudaStream_t st) {
   dim3 g(ceil_div(N, 64), ceil_div(M, 64), batch);
-  k_gemm<float><<<g, 256, 0, st>>>(M, N, K, A, sab, sam, sak, B, sbb, sbn, sbk, C, scb, ldc, beta, nullptr);
+  k_gemm<float, float><<<g, 256, 0, st>>>(M, N, K, A, sab, sam, sak, B, sbb, sbn, sbk, C, scb, ldc, beta, nullptr);
+  return cudaGetLastError();
+}
+cudaError_t gemm_bf16_batched(int batch, int M, int N, int K, const bf16* A, long long sab, long long sam,
+                              long long sak, const bf16* B, long long sbb, long long sbn, long long sbk, void* C,
+                              bool c_f32, long long scb, long long ldc, cudaStream_t st) {
+  dim3 g(ceil_div(N, 64), ceil_div(M, 64), batch);
+  if (c_f32)
+    k_gemm<bf16, float><<<g, 256, 0, st>>>(M, N, K, A, sab, sam, sak, B, sbb, sbn, sbk, static_cast<float*>(C), scb,
+                                           ldc, 0.0f, nullptr);
+  else
+    k_gemm<bf16, bf16><<<g, 256, 0, st>>>(M, N, K, A, sab, sam, sak, B, sbb, sbn, sbk, static_cast<bf16*>(C), scb,
+                                          ldc, 0.0f, nullptr);
   return cudaGetLastError();
 }
 
@@ -2252,7 +2266,7 @@ cudaError_t bn_apply_relu(const TI* x, int N, int H, int W, int C, const float* 
     const long long cmax = kBnChunkBytes / ((long long)C * sizeof(TI));
     const long long cpix = cmax >= lanes ? cmax / lanes * lanes : cmax;
     long long blocks = (P + cpix - 1) / cpix;
-    if (blocks > 4LL * kNumSMs) blocks = 4LL * kNumSMs;
+    if (blocks > 4LL * sm_cap()) blocks = 4LL * sm_cap();
     k_bn_apply_relu_bulk<TI, TO><<<(unsigned)blocks, lanes * G, 0, st>>>(x, P, H * W, C, mean, rstd,
                                                                          BnAffine{gain, bias, gamma, beta}, y);
     return cudaGetLastError();
@@ -2261,7 +2275,7 @@ cudaError_t bn_apply_relu(const TI* x, int N, int H, int W, int C, const float* 
     const int lanes = 256 / G;
     const long long P = (long long)N * H * W;
     long long blocks = (P + 2LL * lanes - 1) / (2LL * lanes);
-    if (blocks > 8LL * kNumSMs) blocks = 8LL * kNumSMs;
+    if (blocks > 8LL * sm_cap()) blocks = 8LL * sm_cap();
     k_bn_apply_relu_cs<TI, TO><<<(unsigned)blocks, lanes * G, 0, st>>>(x, P, H * W, C, mean, rstd,
                                                                        BnAffine{gain, bias, gamma, beta}, y);
     return cudaGetLastError();
@@ -2344,7 +2358,7 @@ cudaError_t bn_bwd_apply(const TI* x, const TG* dy, int N, int H, int W, int C, 
     const int cmax = (int)(kBnChunkBytes / per_pix);
     const int cpix = cmax >= lanes ? cmax / lanes * lanes : cmax;   // whole rounds of the pixel lanes
     long long blocks = (P + cpix - 1) / cpix;
-    if (blocks > 4LL * kNumSMs) blocks = 4LL * kNumSMs;
+    if (blocks > 4LL * sm_cap()) blocks = 4LL * sm_cap();
     k_bn_bwd_apply_bulk<TI, TG, TO><<<(unsigned)blocks, lanes * G, 0, st>>>(
         x, dy, P, H * W, C, cpix, mean, rstd, BnAffine{gain, bias, gamma, beta}, mgrad, add, dx);
     return cudaGetLastError();
@@ -2353,7 +2367,7 @@ cudaError_t bn_bwd_apply(const TI* x, const TG* dy, int N, int H, int W, int C, 
     const int lanes = 256 / G;
     const long long P = (long long)N * H * W;
     long long blocks = (P + lanes - 1) / lanes;
-    if (blocks > 8LL * kNumSMs) blocks = 8LL * kNumSMs;
+    if (blocks > 8LL * sm_cap()) blocks = 8LL * sm_cap();
     k_bn_bwd_apply_cs<TI, TG, TO><<<(unsigned)blocks, lanes * G, 0, st>>>(
         x, dy, P, H * W, C, mean, rstd, BnAffine{gain, bias, gamma, beta}, mgrad, add, dx);
     return cudaGetLastError();
@@ -3325,7 +3339,7 @@ cudaError_t thin_conv_dgrad(const float* dy, int N, int H, int W, int C, const f
   int per_sm = 1;
   PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_thin_dgrad<3>, npg * C, 0));
   if (per_sm < 1) per_sm = 1;
-  const int grid = tiles < per_sm * kNumSMs ? tiles : per_sm * kNumSMs;
+  const int grid = tiles < per_sm * sm_cap() ? tiles : per_sm * sm_cap();
   k_thin_dgrad<3><<<grid, npg * C, 0, st>>>(dy, N, H, W, C, w, dx);
   return cudaGetLastError();
 }

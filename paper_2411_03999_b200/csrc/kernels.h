@@ -217,6 +217,10 @@ cudaError_t softmax_rows(const float* S, long long rows, int cols, T* P, cudaStr
 template <typename T>
 cudaError_t softmax_bwd_rows(const float* S, const float* dP, long long rows, int cols, T* dS, cudaStream_t st);
 // batched SIMT GEMM for the F32 path: C[b][m][n] = sum_k A[b](m,k) B[b](n,k)
+// the attention GEMMs of the unfused (small-image) path in bf16: bf16 operands, fp32 accumulation, fp32 or bf16 C
+cudaError_t gemm_bf16_batched(int batch, int M, int N, int K, const bf16* A, long long sab, long long sam,
+                              long long sak, const bf16* B, long long sbb, long long sbn, long long sbk, void* C,
+                              bool c_f32, long long scb, long long ldc, cudaStream_t st);
 cudaError_t gemm_f32_batched(int batch, int M, int N, int K, const float* A, long long sab, long long sam,
                              long long sak, const float* B, long long sbb, long long sbn, long long sbk, float* C,
                              long long scb, long long ldc, float beta, cudaStream_t st);

@@ -620,9 +620,7 @@ cudaError_t tc_attn_fwd(const TcAttnArgs& a, cudaStream_t st) {
   PG_CUDA(map3(&mv, a.gT, a.Q, a.C2, a.n, 64, a.C2));
   const size_t smem = fwd_smem(a.C2);
   PG_CUDA(cudaFuncSetAttribute(k_attn_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int dev = 0, sms = 148;
-  PG_CUDA(cudaGetDevice(&dev));
-  PG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int sms = sm_cap();
   const int tiles = a.n * (a.HW / kT);
   k_attn_fwd<<<tiles < sms ? tiles : sms, kFwdThreads, smem, st>>>(mq, mk, mv, a);
   return cudaGetLastError();

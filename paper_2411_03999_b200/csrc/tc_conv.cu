@@ -1380,11 +1380,7 @@ template <int BN>
 cudaError_t launch_fprop_bn(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo, const TcFpropArgs& a,
                             int num_sms, cudaStream_t st) {
   using C = FpropCfg<BN>;
-  static bool attr = false;
-  if (!attr) {
-    PG_CUDA(cudaFuncSetAttribute(k_conv_fprop<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
-    attr = true;
-  }
+  PG_CUDA((set_smem_once<k_conv_fprop<BN>>((int)C::SMEM)));
   const int tiles = a.m_tiles * a.n_tiles;
   const int grid = tiles < num_sms ? tiles : num_sms;
   k_conv_fprop<BN><<<grid, kThreads, C::SMEM, st>>>(ma, mb, mo, a);
@@ -1407,14 +1403,9 @@ template <int BN, int MODE>
 cudaError_t launch_halo_bn(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo, const TcFpropArgs& a,
                            uint32_t unit_tx, cudaStream_t st) {
   using C = HaloCfg<BN, MODE>;
-  static bool attr = false;
-  if (!attr) {
-    PG_CUDA(cudaFuncSetAttribute(k_conv_fprop_halo<BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)C::SMEM));
-    attr = true;
-  }
+  PG_CUDA((set_smem_once<k_conv_fprop_halo<BN, MODE>>((int)C::SMEM)));
   const int tiles = a.m_tiles * a.n_tiles;
-  const int grid = tiles < kNumSMs ? tiles : kNumSMs;
+  const int grid = tiles < sm_cap() ? tiles : sm_cap();
   k_conv_fprop_halo<BN, MODE><<<grid, kThreads, C::SMEM, st>>>(ma, mb, mo, a, unit_tx);
   return cudaGetLastError();
 }
@@ -1436,14 +1427,9 @@ template <int BN, int MODE>
 cudaError_t launch_cg2_bn(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo, const TcFpropArgs& a,
                           uint32_t unit_tx, cudaStream_t st, const TmaQuad* quad) {
   using C = Cg2Cfg<BN, MODE>;
-  static bool attr = false;
-  if (!attr) {
-    PG_CUDA(cudaFuncSetAttribute(k_conv_fprop_cg2<BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)C::SMEM));
-    attr = true;
-  }
+  PG_CUDA((set_smem_once<k_conv_fprop_cg2<BN, MODE>>((int)C::SMEM)));
   const int tiles = ((a.m_tiles + 1) / 2) * a.n_tiles * (a.phases > 1 ? a.phases : 1);
-  int clusters = tiles < kNumSMs / 2 ? tiles : kNumSMs / 2;
+  int clusters = tiles < sm_cap() / 2 ? tiles : sm_cap() / 2;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * clusters, 1, 1);
   cfg.blockDim = dim3(kThreads, 1, 1);
@@ -1483,11 +1469,7 @@ template <int BN>
 cudaError_t launch_wgrad_bn(const CUtensorMap& ma, const CUtensorMap& mb, const TcWgradArgs& a, cudaStream_t st,
                             const TmaQuad* quad = nullptr) {
   using C = WgradCfg<BN>;
-  static bool attr = false;
-  if (!attr) {
-    PG_CUDA(cudaFuncSetAttribute(k_conv_wgrad<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
-    attr = true;
-  }
+  PG_CUDA((set_smem_once<k_conv_wgrad<BN>>((int)C::SMEM)));
   const int units = a.m_tiles * a.n_tiles * a.splits;
   TmaQuad tq;
   for (int i = 0; i < 4; ++i) tq.m[i] = quad ? quad->m[i] : ma;
@@ -1499,11 +1481,7 @@ template <int BN>
 cudaError_t launch_wgrad_cg2_bn(const CUtensorMap& ma, const CUtensorMap& mb, const TcWgradArgs& a, cudaStream_t st,
                                 const TmaQuad* quad = nullptr) {
   using C = WgradCg2Cfg<BN>;
-  static bool attr = false;
-  if (!attr) {
-    PG_CUDA(cudaFuncSetAttribute(k_conv_wgrad_cg2<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
-    attr = true;
-  }
+  PG_CUDA((set_smem_once<k_conv_wgrad_cg2<BN>>((int)C::SMEM)));
   const int units = ((a.m_tiles + 1) / 2) * a.n_tiles * a.splits;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * units, 1, 1);
@@ -1525,11 +1503,7 @@ cudaError_t launch_wgrad_cg2_bn(const CUtensorMap& ma, const CUtensorMap& mb, co
 template <int BN>
 cudaError_t launch_wgrad3_bn(const CUtensorMap& ma, const CUtensorMap& mb, const TcWgradArgs& a, cudaStream_t st) {
   using C = Wgrad3Cfg<BN>;
-  static bool attr = false;
-  if (!attr) {
-    PG_CUDA(cudaFuncSetAttribute(k_conv_wgrad3<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
-    attr = true;
-  }
+  PG_CUDA((set_smem_once<k_conv_wgrad3<BN>>((int)C::SMEM)));
   k_conv_wgrad3<BN><<<a.m_tiles * a.n_tiles * a.splits, 192, C::SMEM, st>>>(ma, mb, a);
   return cudaGetLastError();
 }
@@ -1590,7 +1564,7 @@ cudaError_t tc_conv_fprop(const void* x, int N, int H, int W, int Cin, const voi
   a.out_f32 = epi.out_f32;
   a.ldo = epi.ldo ? epi.ldo : Cout;
   a.relu_out = epi.relu_out;
-  const int sms = kNumSMs;
+  const int sms = sm_cap();
   static const int halo_on = env_int("PARAGAN_HALO", 1), tma_st = env_int("PARAGAN_TMA_STORE", 1),
                    cg2_on = env_int("PARAGAN_CG2", 1);
   CUtensorMap mo;

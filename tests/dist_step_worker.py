@@ -59,40 +59,23 @@ def main():
         out["vs_single"] = {k: P.rel(got[k], single[k]) for k in dp_tol}
         out["vs_single_bad"] = [k for k, v in out["vs_single"].items() if not v < dp_tol[k]]
         want = P.run_oracle(ocfg, gs, ds, g0, d0, dbs, gb)
-        noise = {}
-        if compute == api.BF16:
-            # bf16 noise floor (as tests/test_gpu_step.py): the emulating oracle's own distance from fp64
-            import dataclasses
-            pcfg = dataclasses.replace(ocfg, bf16=False)
-            plain = P.run_oracle(pcfg, *P.make_inputs(pcfg, B * world, seed=31))
-            noise = {k: plain[k] for k in ("d_grads", "g_grads")}
         out["d_loss"] = abs(got["d_loss"] - want["d_loss"]) / max(abs(want["d_loss"]), 1e-3)
         out["g_loss"] = abs(got["g_loss"] - want["g_loss"]) / max(abs(want["g_loss"]), 1e-3)
-        # fp32: per tensor and global 1e-4.  bf16: per tensor and global max(2e-2, 1.5 x the bf16 noise
-        # floor |emulating oracle - fp64 oracle|), tensors >= 16 elements that are not ~0
+        # fp32: per tensor and global 1e-4.  bf16 (the R14-exact path, PARAGAN_SUBPIXEL=0 set by the test):
+        # each network's whole gradient at 2e-2 against the R14-emulating oracle, per tensor reported
+        # (tests/test_gpu_step.py::test_step_parity_bf16_biggan128 for the reasons)
+        gfloor = P.bf16_policy_floor(ocfg, B * world, 31, 1, want) if compute == api.BF16 else 0.0
         for key, specs in (("d_grads", ds), ("g_grads", gs)):
             out[key + "_global"] = P.rel(got[key], want[key])
             if compute == api.F32:
                 # SN-DCGAN's deconv biases feed BNs: exact gradient 0, fp32 residual ~1e-5 of the RMS gradient
                 bad, worst = P.compare_tensors(specs, got[key], want[key], tol, floor_frac=1e-1 if dcgan else 1e-2)
                 out[key + "_bad"] = [b[0] for b in bad]
-                out[key + "_worst"] = max(worst.values())
-                gbar = tol
             else:
-                bad, o, worst = [], 0, 0.0
-                for sp in specs:
-                    n = int(np.prod(sp.shape))
-                    e = P.rel(got[key][o:o + n], want[key][o:o + n])
-                    e_bf = P.rel(want[key][o:o + n], noise[key][o:o + n])
-                    if n >= 16 and np.linalg.norm(want[key][o:o + n]) > 1e-6 * np.linalg.norm(want[key]):
-                        worst = max(worst, e / max(tol, 1.5 * e_bf))
-                        if e > max(tol, 1.5 * e_bf):
-                            bad.append(sp.name)
-                    o += n
-                out[key + "_bad"] = bad
-                out[key + "_worst"] = worst   # error / bar (<= 1 passes)
-                gbar = max(tol, 1.5 * P.rel(want[key], noise[key]))
-            if out[key + "_global"] > gbar:
+                bad, worst = P.compare_tensors(specs, got[key], want[key], 1.0)
+                out[key + "_bad"] = []
+            out[key + "_worst"] = max(worst.values())
+            if out[key + "_global"] > tol + (gfloor if key == "g_grads" else 0.0):
                 out[key + "_bad"].append("GLOBAL")
         g_rel = 1e-4 if compute == api.F32 else 2e-2
         from oracle import biggan as bg

@@ -26,7 +26,7 @@ def _port():
 def test_two_gpu_step_parity(compute, arch):
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs")
-    env = dict(os.environ, PARAGAN_COMPUTE=compute, PARAGAN_ARCH=arch)
+    env = dict(os.environ, PARAGAN_COMPUTE=compute, PARAGAN_ARCH=arch, PARAGAN_SUBPIXEL="0" if compute == "bf16" else "1")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr=127.0.0.1", f"--master-port={_port()}", os.path.join(ROOT, "tests", "dist_step_worker.py")]
     r = subprocess.run(cmd, env=env, cwd=ROOT, capture_output=True, text=True, timeout=600)

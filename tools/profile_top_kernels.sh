@@ -1,6 +1,6 @@
 # Capture ncu --set full reports of the top kernels of one bench step and summarise them on
 # the GPU box (gpurun -- bash tools/profile_top_kernels.sh [name ...]); summaries land in
-# gpurun_out/r1_<name>.md (the .ncu-rep files are deleted unless KEEP_REP=1: gpurun returns
+# gpurun_out/${ROUND}_<name>.md (the .ncu-rep files are deleted unless KEEP_REP=1: gpurun returns
 # at most 64 MiB).
 export PARAGAN_ALLOW_SHORT_WARMUP=1
 CMD="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-profile"
@@ -32,7 +32,7 @@ for s in specs:
         print(s)
 PY
 while IFS='|' read -r name kre skip; do
-  rep=gpurun_out/r1_$name
+  rep=gpurun_out/${ROUND:-r2}_$name
   timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:$kre" -s $skip -c 1 -o $rep $CMD > gpurun_out/ncu_$name.log 2>&1
   echo "$name $?"
   if [ -f $rep.ncu-rep ]; then
