@@ -2562,6 +2562,8 @@ paragan_status validate_config(const paragan_config* c) {
     return PARAGAN_OK;
   }
   if (c->arch != PARAGAN_ARCH_BIGGAN) return PARAGAN_ERR_CONFIG;
+  // D runs on [fake; real] = 2B rows; its projection-head gradient kernel handles at most 2048 rows per launch
+  if (c->local_batch > 1024) return PARAGAN_ERR_CONFIG;
   Arch a;
   if (!arch_for(c->resolution, a)) return PARAGAN_ERR_CONFIG;
   if (c->ch < 1 || c->n_classes < 1 || c->shared_dim < 1 || c->z_chunk < 1 || c->local_batch < 1 ||

@@ -1267,6 +1267,20 @@ __global__ void k_split_reduce(const float* __restrict__ part, float* __restrict
   }
 }
 
+// bias-gradient reduction: dst[c] (+)= sum_k part[k][c] for the few output channels of a wgrad launch with
+// many splits — one warp per channel, lane l sums splits l, l + 32, ... in order, then a fixed shuffle tree
+// (deterministic; replaces a serial per-thread loop that was latency-bound)
+__global__ void k_bias_reduce(const float* __restrict__ part, float* __restrict__ dst, int n, int splits,
+                              int accumulate) {
+  const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (c >= n) return;
+  float s = 0.0f;
+  for (int k = lane; k < splits; k += 32) s += __ldg(part + (long long)k * n + c);
+  s = warp_sum(s);
+  if (lane == 0) dst[c] = accumulate ? dst[c] + s : s;
+}
+
 // the same sum, four consecutive outputs per thread (16-byte loads); per element the order is unchanged
 // (dst or 0, then split 0, 1, ...), so the result is bit-identical to k_split_reduce
 __global__ void k_split_reduce4(const float4* __restrict__ part, float4* __restrict__ dst, long long n4, int splits,
@@ -1808,7 +1822,7 @@ cudaError_t tc_conv_wgrad_up2(const void* x, const void* dy, int N, int H, int W
     PG_LAUNCH_CHECK();
   }
   if (dbias) {
-    k_split_reduce<<<ceil_div(Cout, 256), 256, 0, st>>>(a.bias_out, dbias, Cout, a.splits * 4, 0);
+    k_bias_reduce<<<ceil_div(Cout, 8), 256, 0, st>>>(a.bias_out, dbias, Cout, a.splits * 4, 0);
     PG_LAUNCH_CHECK();
   }
   return cudaSuccess;
@@ -1912,7 +1926,7 @@ cudaError_t tc_conv_wgrad(const void* x, const void* dy, int N, int H, int W, in
     }
     PG_LAUNCH_CHECK();
     if (dbias) {
-      k_split_reduce<<<ceil_div(Cout, 256), 256, 0, st>>>(a.bias_out, dbias, Cout, a.splits, 0);
+      k_bias_reduce<<<ceil_div(Cout, 8), 256, 0, st>>>(a.bias_out, dbias, Cout, a.splits, accumulate);
       PG_LAUNCH_CHECK();
     }
   }
