@@ -246,6 +246,9 @@ def main():
     ap.add_argument("--async", dest="async_", action="store_true",
                     help="asynchronous update scheme (P:266-282): G and D on disjoint halves of the GPUs")
     ap.add_argument("--g-batch", type=int, default=0, help="--async: G batch per G rank (default --batch)")
+    ap.add_argument("--reals", default="g0", choices=["g0", "uniform"],
+                    help="g0: reals from the initial G plus noise (default, D unsaturated); uniform: U(-1,1) noise "
+                         "images without the generation pass (profiling runs: fewer launches before the step)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
@@ -302,6 +305,9 @@ def main():
         for i in range(4):
             reals = []
             for k in range(nd):
+                if args.reals == "uniform":
+                    reals.append(inputs.real_batch(1000 + i, rank * nd + k, B, R, 1000))
+                    continue
                 zr, yr = inputs.latent_batch(5000 + i, inputs.ROLE_REAL, rank * nd + k, B, dz, 1000)
                 seed_img = torch.zeros((B, R, R, cfg.c_pad_image), dtype=tdt, device=dev)
                 ctx.d_step(seed_img, torch.from_numpy(yr).to(dev), torch.from_numpy(zr).to(dev),
@@ -406,7 +412,7 @@ def main():
             for i in range(args.steps):
                 step(i)
             ctx.profile(False)
-            for kind in (0, 1, 2, 3, 4):
+            for kind in (0, 1, 2, 3, 4, 5, 6):
                 prof[kind] = ctx.profile_read(kind)
             barrier()
 
@@ -431,6 +437,9 @@ def main():
                     "wgrad": {"achieved": (f1_ / (t1 / 1000.0)) / 1e12 if t1 > 0 else 0.0,
                               "achieved_executed": (prof[4][2] / (t1 / 1000.0)) / 1e12 if t1 > 0 else 0.0,
                               "launches": n1, "ms_per_step": t1 / args.steps}}
+            roof["other_kernels_ms_per_step"] = {
+                "fused_attention_fwd_bwd": prof[5][1] / args.steps,
+                "g_output_layer_fp32_thin": prof[6][1] / args.steps}
             if world > 1:
                 n2, t2, b2 = prof[2]
                 roof["collectives"] = {"launches_per_step": n2 / args.steps, "ms_per_step": t2 / args.steps,
@@ -457,7 +466,8 @@ def main():
                 "repeats_ms_per_step": [round(m / args.steps, 3) for m in rep_ms],
                 "losses": {"d": st.d_loss, "g": st.g_loss, "d_per_step_e2e": d_losses,
                            "g_per_step_e2e": g_losses, "d_grad_norm_last": d_grad_norm,
-                           "reals": "G0(z') + N(0, 0.05^2) noise, clipped (G0 = the run's random-init generator)"}}
+                           "reals": ("G0(z') + N(0, 0.05^2) noise, clipped (G0 = the run's random-init generator)"
+                                     if args.reals == "g0" else "U(-1, 1) noise images")}}
         print(json.dumps(line), flush=True)
     ctx.close()
     if world > 1:

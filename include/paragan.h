@@ -251,7 +251,8 @@ paragan_status paragan_kernel_launches(const paragan_ctx* ctx, uint64_t* n);
  * counts, G's conv1 counted over the upsampled tensor as BigGAN defines it; for kind 2:
  * bytes reduced).  Kinds 3 / 4: the launches of kinds 0 / 1 with the flops actually
  * issued to the tensor cores (the sub-pixel conv1 issues 1/2.25 of its algorithmic
- * work).  enable=1 also clears the record. */
+ * work).  Kind 5: the fused attention kernels (forward + backward; flops = their MMA work); kind 6: G's fp32
+ * output layer (thin fprop / dgrad / wgrad; 2*27*C flops per pixel each).  enable=1 also clears the record. */
 paragan_status paragan_profile(paragan_ctx* ctx, int32_t enable);
 paragan_status paragan_profile_read(paragan_ctx* ctx, int32_t kind, uint64_t* launches, double* ms, double* flops);
 

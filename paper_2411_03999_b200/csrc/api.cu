@@ -188,7 +188,7 @@ paragan_status paragan_profile(paragan_ctx* ctx, int32_t enable) {
   return ctx->eng->profile(enable);
 }
 paragan_status paragan_profile_read(paragan_ctx* ctx, int32_t kind, uint64_t* launches, double* ms, double* flops) {
-  if (!ctx || !ctx->eng || kind < 0 || kind > 4) return PARAGAN_ERR_INVALID_ARG;
+  if (!ctx || !ctx->eng || kind < 0 || kind > 6) return PARAGAN_ERR_INVALID_ARG;
   return ctx->eng->profile_read(kind, launches, ms, flops);
 }
 paragan_status paragan_checkpoint_save_async(paragan_ctx* ctx, const char* path) {
@@ -375,7 +375,9 @@ paragan_status paragan_op_attn_fwd(const void* qkv, const void* phi, const void*
     return PARAGAN_ERR_INVALID_ARG;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   void* gT = nullptr;
-  if (cudaMallocAsync(&gT, (size_t)n * (hw / 4) * c2 * 2, st) != cudaSuccess) return PARAGAN_ERR_CUDA;
+  if (cudaMallocAsync(&gT, (size_t)n * (hw / 4) * c2 * 2 + (size_t)n * sizeof(float) + 256, st) != cudaSuccess)
+    return PARAGAN_ERR_CUDA;
+  float* phimax = reinterpret_cast<float*>(static_cast<char*>(gT) + (((size_t)n * (hw / 4) * c2 * 2 + 255) & ~size_t(255)));
   TcAttnArgs a{};
   a.n = n;
   a.HW = hw;
@@ -390,7 +392,9 @@ paragan_status paragan_op_attn_fwd(const void* qkv, const void* phi, const void*
   a.o = o;
   a.o32 = o32;
   a.lse = lse;
+  a.phimax = phimax;
   cudaError_t e = attn_transpose(gp, n, a.Q, c2, gT, st);
+  if (e == cudaSuccess) e = attn_phimax(phi, n, a.Q, cq, phimax, st);
   if (e == cudaSuccess) e = tc_attn_fwd(a, st);
   cudaFreeAsync(gT, st);
   return cuda_status(e);

@@ -137,6 +137,7 @@ struct AttnL {
   bool fused = false;
   void* gT = nullptr;              // pooled g transposed [n][C2][Q]
   float *o32 = nullptr, *lse = nullptr, *Dr = nullptr;
+  float* phimax = nullptr;         // [n] max_j |phi_j| (enables the single-pass fused forward)
 };
 struct GBlock {
   int cin, cout, hin;
@@ -216,6 +217,8 @@ class Engine final : public EngineBase {
 
  public:
   Engine(const paragan_config& c, cudaStream_t st) : cfg_(c), st_(st) {
+    const char* as = std::getenv("PARAGAN_ATTN_SINGLE");
+    attn_single_ = as == nullptr || std::atoi(as) != 0;
     const char* sp = std::getenv("PARAGAN_SUBPIXEL");
     subpix_ = kBF && (sp == nullptr || std::atoi(sp) != 0);
     dcgan_ = c.arch == PARAGAN_ARCH_SNDCGAN;
@@ -803,14 +806,14 @@ class Engine final : public EngineBase {
     double t = 0, f = 0;
     const bool verbose = std::getenv("PARAGAN_PROFILE_VERBOSE") != nullptr;
     // kinds 3 / 4: the launches of kinds 0 / 1 with their executed instead of algorithmic flops
-    const int k = kind >= 3 ? kind - 3 : kind;
+    const int k = (kind == 3 || kind == 4) ? kind - 3 : kind;
     for (auto& r : recs_) {
       if (r.kind != k) continue;
       float e = 0;
       if (cudaEventElapsedTime(&e, r.a, r.b) != cudaSuccess) return fail_cuda(cudaGetLastError(), "event time");
       ++c;
       t += e;
-      f += kind >= 3 ? r.exec_flops : r.flops;
+      f += (kind == 3 || kind == 4) ? r.exec_flops : r.flops;
       if (verbose)
         std::fprintf(stderr, "PROF kind=%d ms=%.4f tflops=%.1f exec_tflops=%.1f %s\n", k, e, r.flops / (e * 1e9),
                      r.exec_flops / (e * 1e9), r.what);
@@ -1197,6 +1200,7 @@ class Engine final : public EngineBase {
         at->gT = A.get<char>((size_t)n * Q * at->C2 * sizeof(T));
         at->o32 = A.get<float>((size_t)n * HW * at->C2);
         at->lse = A.get<float>((size_t)n * HW);
+        at->phimax = A.get<float>((size_t)n);
         at->Dr = A.get<float>((size_t)n * HW);
         dth_part_floats_ = std::max(dth_part_floats_, (size_t)((Q / 128) * n * HW * at->Cq));
       } else {
@@ -1790,7 +1794,9 @@ class Engine final : public EngineBase {
     CKS(bn_forward_stats(gout_in_, M, cl_, osums_, omean_, orstd_));
     CK((bn_apply_relu<T, float>(static_cast<const T*>(gout_in_), B, R_, R_, cl_, omean_, orstd_, nullptr, nullptr,
                                 G_.P(obn_g_), G_.P(obn_b_), aout_, false, st_)));
-    CK(thin_conv_fwd(aout_, B, R_, R_, cl_, static_cast<const float*>(oconv_.wp), 3, G_.P(oconv_.b), pre_, st_));
+    CK(timed(6, 2.0 * B * R_ * R_ * 27.0 * cl_, [&] {
+      return thin_conv_fwd(aout_, B, R_, R_, cl_, static_cast<const float*>(oconv_.wp), 3, G_.P(oconv_.b), pre_, st_);
+    }, "thin fwd"));
     CK(tanh_to_image<T>(pre_, img_, static_cast<T*>(dimg_), M, cpad_, st_));
     return PARAGAN_OK;
   }
@@ -2070,6 +2076,7 @@ class Engine final : public EngineBase {
     t.o32 = a.o32;
     t.lse = a.lse;
     t.Dr = a.Dr;
+    t.phimax = attn_single_ ? a.phimax : nullptr;
     return t;
   }
   paragan_status attn_forward(Net& N, AttnL& a, const void* x, int n, void* out) {
@@ -2092,8 +2099,9 @@ class Engine final : public EngineBase {
     CK(maxpool2_split<T>(qkv, n, H, H, a.Ct, 2 * a.Cq, a.C2, static_cast<T*>(a.g_p), nullptr, st_));
     if (a.fused) {
       CK(attn_transpose(a.g_p, n, (int)Q, a.C2, a.gT, st_));
+      CK(attn_phimax(a.phi_p, n, (int)Q, a.Cq, a.phimax, st_));
       TcAttnArgs t = attn_args(a, n);
-      CK(tc_attn_fwd(t, st_));
+      CK(timed(5, 2.0 * n * HW * Q * (double)(a.Cq + a.C2), [&] { return tc_attn_fwd(t, st_); }, "attn fwd"));
     } else {
       // S = theta phi^T  [n][HW][Q] fp32
       CKS(bgemm(n, (int)HW, (int)Q, a.Cq, qkv, HW * a.Ct, a.Ct, 1, a.phi_p, Q * a.Cq, a.Cq, 1, a.S, true, HW * Q, Q));
@@ -2134,7 +2142,7 @@ class Engine final : public EngineBase {
       t.dgp = dgp;
       t.dphi = dph;
       t.dth_part = dth_part_;
-      CK(tc_attn_bwd(t, st_));
+      CK(timed(5, 2.0 * n * HW * Q * (double)(3 * a.Cq + 2 * a.C2), [&] { return tc_attn_bwd(t, st_); }, "attn bwd"));
       // every channel of dqkv is written below: theta [0,Cq), phi [Cq,2Cq), g [2Cq,2Cq+C2)
       CK(attn_dtheta_reduce(dth_part_, (int)(Q / 128), M, a.Cq, dqkv, a.Ct, st_));
       CK(maxpool2_split_bwd<T>(static_cast<const T*>(a.qkv), n, H, H, a.Ct, a.Cq, a.Cq, dph, static_cast<T*>(dqkv),
@@ -2352,9 +2360,13 @@ class Engine final : public EngineBase {
     const long long M = (long long)B * R_ * R_;
     // tanh' and the fp32 output conv
     CK(tanh_bwd<T>(static_cast<const T*>(dimg_grad_), cpad_, img_, dpre_, M, st_));
-    CK(thin_conv_wgrad(aout_, dpre_, B, R_, R_, cl_, 3, G_.G(oconv_.w), scratch_f_, scratch_floats_, st_));
+    CK(timed(6, 2.0 * B * R_ * R_ * 27.0 * cl_, [&] {
+      return thin_conv_wgrad(aout_, dpre_, B, R_, R_, cl_, 3, G_.G(oconv_.w), scratch_f_, scratch_floats_, st_);
+    }, "thin wgrad"));
     CK(col_sum<float>(dpre_, M, 3, dpart_, kMaxPartialBlocks, G_.G(oconv_.b), 0, st_));
-    CK(thin_conv_dgrad(dpre_, B, R_, R_, cl_, static_cast<const float*>(oconv_.wp), 3, daout_, st_));
+    CK(timed(6, 2.0 * B * R_ * R_ * 27.0 * cl_, [&] {
+      return thin_conv_dgrad(dpre_, B, R_, R_, cl_, static_cast<const float*>(oconv_.wp), 3, daout_, st_);
+    }, "thin dgrad"));
     // output BN backward (plain BN, learned gamma/beta)
     int ic = (dimg_idx_ + 1) % 4;
     void* cur = tmp(ic);
@@ -2466,6 +2478,7 @@ class Engine final : public EngineBase {
   int overlap_sms_ = 16, overlap_blocks_ = 3;
   bool ready_ = false, poisoned_ = false, planned_ = false, ones_ready_ = false;
   bool subpix_ = false;   // G conv1 as four phase 2x2 convs of the low-resolution input (NEXT-1)
+  bool attn_single_ = true;   // single-pass fused attention forward when the score bound allows (R21)
   bool dcgan_ = false;    // SN-DCGAN (config 1) instead of BigGAN
   int d_since_g_ = 0;
   uint64_t launches_ = 0;

@@ -2728,11 +2728,14 @@ namespace {
 // ---------------------------------------------------------------------------
 // fprop: y[m][o] = bias[o] + sum_{tap,c} x[m+tap][c] w[o][tap][c]
 // tile 32 rows x 64 cols, thread = 8 consecutive pixels of one row (acc[8][CO] in registers);
-// 8-channel halo chunks staged in smem ([c][row][68] planes; a whole 32-byte sector per pixel —
-// 4-channel chunks re-read every sector from DRAM), weights as [c][28] so each channel's 27 taps x
-// outputs come in 7 broadcast float4 loads; rows slide through 3 float4s.
-constexpr int kFTH = 32, kFTW = 64, kFCC = 8, kFRS = 68, kFV = kFCC / 4;
+// 4-channel halo chunks staged in smem ([c][row][68] planes), software-pipelined: the global loads of
+// chunk c+1 (9 x 16 bytes per thread, held in registers) are in flight while chunk c is computed, so
+// the DRAM latency hides behind the FMA loop; weights as [c][28] so each channel's 27 taps x outputs
+// come in 7 broadcast float4 loads; rows slide through 3 float4s.
+constexpr int kFTH = 32, kFTW = 64, kFCC = 4, kFRS = 68;
 constexpr int kFPlane = (kFTH + 2) * kFRS;
+constexpr int kFItems = (kFTH + 2) * (kFTW + 2);          // 16-byte items per chunk (one per halo pixel)
+constexpr int kFPre = (kFItems + 255) / 256;              // per thread
 template <int CO>
 __global__ void __launch_bounds__(256, 2) k_thin_fwd(const float* __restrict__ x, int N, int H, int W, int C,
                                                   const float* __restrict__ w, const float* __restrict__ bias,
@@ -2757,41 +2760,37 @@ __global__ void __launch_bounds__(256, 2) k_thin_fwd(const float* __restrict__ x
   for (int p = 0; p < 8; ++p)
 #pragma unroll
     for (int o = 0; o < CO; ++o) acc[p][o] = 0.0f;
-  for (int c0 = 0; c0 < C; c0 += kFCC) {
-    __syncthreads();
-    // halo chunk: batches of 6 independent 16-byte loads per thread in flight, then the planar stores
-    constexpr int kItems = (kFTH + 2) * (kFTW + 2) * kFV;
-    constexpr int kBatch = 6;
-    for (int i0 = threadIdx.x; i0 < kItems; i0 += kBatch * 256) {
-      float4 v[kBatch];
+  float4 pre[kFPre];
+  auto fetch = [&](int c0) {
 #pragma unroll
-      for (int u = 0; u < kBatch; ++u) {
-        const int i = i0 + u * 256;
-        v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (i < kItems) {
-          const int half = i % kFV, rs = i / kFV;
-          const int sx = rs % (kFTW + 2), r = rs / (kFTW + 2);
-          const int h = h0 - 1 + r, ww = w0 - 1 + sx;
-          const int c = c0 + half * 4;
-          if (h >= 0 && h < H && ww >= 0 && ww < W && c < C)
-            v[u] = __ldg(reinterpret_cast<const float4*>(x + (((long long)n * H + h) * W + ww) * C + c));
-        }
+    for (int u = 0; u < kFPre; ++u) {
+      const int i = threadIdx.x + u * 256;
+      pre[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (i < kFItems) {
+        const int sx = i % (kFTW + 2), r = i / (kFTW + 2);
+        const int h = h0 - 1 + r, ww = w0 - 1 + sx;
+        if (h >= 0 && h < H && ww >= 0 && ww < W && c0 < C)
+          pre[u] = __ldg(reinterpret_cast<const float4*>(x + (((long long)n * H + h) * W + ww) * C + c0));
       }
+    }
+  };
+  fetch(0);
+  for (int c0 = 0; c0 < C; c0 += kFCC) {
+    __syncthreads();   // the previous chunk's planes are no longer read
 #pragma unroll
-      for (int u = 0; u < kBatch; ++u) {
-        const int i = i0 + u * 256;
-        if (i < kItems) {
-          const int half = i % kFV, rs = i / kFV;
-          const int sx = rs % (kFTW + 2), r = rs / (kFTW + 2);
-          float* d = xs + half * 4 * kFPlane + r * kFRS + sx;
-          d[0] = v[u].x;
-          d[kFPlane] = v[u].y;
-          d[2 * kFPlane] = v[u].z;
-          d[3 * kFPlane] = v[u].w;
-        }
+    for (int u = 0; u < kFPre; ++u) {
+      const int i = threadIdx.x + u * 256;
+      if (i < kFItems) {
+        const int sx = i % (kFTW + 2), r = i / (kFTW + 2);
+        float* d = xs + r * kFRS + sx;
+        d[0] = pre[u].x;
+        d[kFPlane] = pre[u].y;
+        d[2 * kFPlane] = pre[u].z;
+        d[3 * kFPlane] = pre[u].w;
       }
     }
     __syncthreads();
+    if (c0 + kFCC < C) fetch(c0 + kFCC);   // in flight during the FMA loop below
     const int cc = min(kFCC, C - c0);
     for (int c = 0; c < cc; ++c) {
       const float* plane = xs + c * kFPlane;

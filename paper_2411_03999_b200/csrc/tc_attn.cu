@@ -37,6 +37,7 @@ namespace {
 constexpr int kT = 128;                 // query rows per tile = keys per chunk
 constexpr uint32_t kAtom = 16384;       // 128 rows x 128 B, one SW128 operand atom
 constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kSpan = 16.0f;          // single-pass forward when every row's score bound is within e^16 of chunk 0's max
 constexpr int kFwdKStages = 3, kFwdVStages = 2;
 constexpr int kFwdThreads = 320;        // w0 TMA, w1 MMA, w2-9 softmax / epilogue
 constexpr int kSoftThreads = 256;
@@ -92,7 +93,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   uint64_t* pempty = pfull + 2;
   uint64_t* ofull = pempty + 2;
   uint64_t* oempty = ofull + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(oempty + 1);
+  uint64_t* decbar = oempty + 1;                                    // per tile: single- or two-pass decided
+  uint32_t* dec = reinterpret_cast<uint32_t*>(decbar + 1);
+  uint32_t* tmem_slot = dec + 1;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
@@ -117,6 +120,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     }
     tc::mbar_init(ofull, 1);
     tc::mbar_init(oempty, kSoftThreads);
+    tc::mbar_init(decbar, 1);
     tc::fence_barrier_init();
   }
   if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
@@ -139,19 +143,34 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         tc::mbar_wait(qempty, (it & 1) ^ 1);
         tc::mbar_expect_tx(qfull, kAtom);
         tc::tma_load_3d(sQ, &tmQ, qfull, 0, q0, b);
-        for (int u = 0; u < 2 * NC; ++u) {
-          const int c = u < NC ? u : u - NC;
+        auto load_k = [&](int c) {
           tc::mbar_wait(&kempty[ks], kph ^ 1);
           tc::mbar_expect_tx(&kfull[ks], kAtom);
           tc::tma_load_3d(sK + ks * kAtom, &tmK, &kfull[ks], 0, c * kT, b);
           if (++ks == kFwdKStages) { ks = 0; kph ^= 1; }
-          if (u >= NC) {
-            tc::mbar_wait(&vempty[vs], vph ^ 1);
-            tc::mbar_expect_tx(&vfull[vs], v_bytes);
-            uint8_t* dv = sV + vs * v_bytes;
-            tc::tma_load_3d(dv, &tmV, &vfull[vs], c * kT, 0, b);
-            tc::tma_load_3d(dv + C2 * 128, &tmV, &vfull[vs], c * kT + 64, 0, b);
-            if (++vs == kFwdVStages) { vs = 0; vph ^= 1; }
+        };
+        auto load_v = [&](int c) {
+          tc::mbar_wait(&vempty[vs], vph ^ 1);
+          tc::mbar_expect_tx(&vfull[vs], v_bytes);
+          uint8_t* dv = sV + vs * v_bytes;
+          tc::tma_load_3d(dv, &tmV, &vfull[vs], c * kT, 0, b);
+          tc::tma_load_3d(dv + C2 * 128, &tmV, &vfull[vs], c * kT + 64, 0, b);
+          if (++vs == kFwdVStages) { vs = 0; vph ^= 1; }
+        };
+        // chunks 0 and 1 come first in both schedules; the rest depends on the tile's decision
+        load_k(0);
+        if (NC > 1) load_k(1);
+        tc::mbar_wait(decbar, it & 1);
+        if (*reinterpret_cast<volatile uint32_t*>(dec)) {   // single pass: V(c), then K(c + 2)
+          for (int c = 0; c < NC; ++c) {
+            load_v(c);
+            if (c + 2 < NC) load_k(c + 2);
+          }
+        } else {                                            // two passes: the rest of pass 1, then pass 2
+          for (int c = 2; c < NC; ++c) load_k(c);
+          for (int c = 0; c < NC; ++c) {
+            load_k(c);
+            load_v(c);
           }
         }
       }
@@ -184,8 +203,13 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
         tc::mbar_wait(qfull, it & 1);
         tc::tc_fence_after();
-        for (int u = 0; u < NC; ++u) issue_s(false);
-        issue_s(NC == 1);
+        issue_s(false);                                     // chunk 0 (its max decides the schedule)
+        tc::mbar_wait(decbar, it & 1);
+        const bool single = *reinterpret_cast<volatile uint32_t*>(dec) != 0;
+        if (!single) {
+          for (int u = 1; u < NC; ++u) issue_s(false);      // rest of pass 1
+          issue_s(NC == 1);                                 // pass 2 starts again at chunk 0
+        }
         tc::mbar_wait(oempty, (it & 1) ^ 1);   // the previous tile's O has been read out
         for (int c = 0; c < NC; ++c) {
           if (c + 1 < NC) issue_s(c + 2 == NC);
@@ -222,36 +246,88 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
       const int b = tile / tiles_per_img;
       const int q0 = (tile - b * tiles_per_img) * kT;
-      // pass 1: row max (no exponentials)
-      float m = -INFINITY;
-      for (int u = 0; u < NC; ++u, ++su) {
+      // chunk 0: its row max m0 and the Cauchy-Schwarz bound U = |theta_i| max_j |phi_j| >= every score of
+      // the row.  When U - m0 <= kSpan for every row of the tile, m0 serves as the softmax offset for all
+      // chunks (P~ = exp(S - m0) <= e^kSpan: no overflow, and bf16 / fp32 keep their relative precision at
+      // any magnitude), so the scores are computed and exponentiated once (single pass); otherwise pass 1
+      // finds the exact row max first (two passes).  Either way O = (P~ g) / l and lse = m + log l exactly.
+      float v[32], w[32];
+      {
         const int sb = su & 1;
         tc::mbar_wait(&sfull[sb], (su >> 1) & 1);
         tc::tc_fence_after();
-        float v[32], w[32];
         tc::tmem_ld32(lrow + sb * kT + h * 64, v);
         tc::tmem_ld32(lrow + sb * kT + h * 64 + 32, w);
         tc::tc_fence_before();
         tc::mbar_arrive(&sempty[sb]);
-#pragma unroll
-        for (int j = 0; j < 32; ++j) m = fmaxf(m, fmaxf(v[j], w[j]));
+        ++su;
       }
+      float m = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) m = fmaxf(m, fmaxf(v[j], w[j]));
       float* rb = red + (it & 1) * 2 * kT;
       rb[h * kT + row] = m;
       tc::named_bar(1, kSoftThreads);
       m = fmaxf(rb[row], rb[kT + row]);
-      // pass 2: P~ = exp(S - m) (<= 1) -> bf16 smem tile for the P~ g MMA; l = sum of P~ in fp32
+      uint32_t ok = 0;
+      if (a.phimax && NC > 1) {
+        tc::mbar_wait(qfull, it & 1);   // theta's tile (already landed: the chunk-0 MMA read it)
+        const uint8_t* qrow = sQ + row * 128;
+        float t2 = 0.0f;
+        for (int c = 0; c < a.Cq / 8; ++c) {
+          const uint4 u4 = *reinterpret_cast<const uint4*>(qrow + ((c ^ (row & 7)) << 4));
+          const __nv_bfloat162* hp = reinterpret_cast<const __nv_bfloat162*>(&u4);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float2 f = __bfloat1622float2(hp[k]);
+            t2 = fmaf(f.x, f.x, fmaf(f.y, f.y, t2));
+          }
+        }
+        const float U = sqrtf(t2) * a.phimax[b] * 1.001f + 1e-3f;
+        ok = (U - m <= kSpan) ? 1u : 0u;   // false for NaN / inf
+      }
+      uint32_t single;
+      asm volatile("{\n\t.reg .pred p, q;\n\tsetp.ne.u32 p, %1, 0;\n\tbar.red.and.pred q, 2, %2, p;\n\t"
+                   "selp.u32 %0, 1, 0, q;\n\t}"
+                   : "=r"(single) : "r"(ok), "r"(kSoftThreads) : "memory");
+      if (threadIdx.x == 64) {   // warp 2 lane 0 publishes the decision to the TMA and MMA warps
+        *dec = single;
+        tc::mbar_arrive(decbar);
+      }
+      if (!single) {
+        // pass 1 (rest): exact row max (no exponentials)
+        for (int u = 1; u < NC; ++u, ++su) {
+          const int sb = su & 1;
+          tc::mbar_wait(&sfull[sb], (su >> 1) & 1);
+          tc::tc_fence_after();
+          float x[32], y[32];
+          tc::tmem_ld32(lrow + sb * kT + h * 64, x);
+          tc::tmem_ld32(lrow + sb * kT + h * 64 + 32, y);
+          tc::tc_fence_before();
+          tc::mbar_arrive(&sempty[sb]);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) m = fmaxf(m, fmaxf(x[j], y[j]));
+        }
+        tc::named_bar(1, kSoftThreads);   // every thread has read m0 from rb
+        rb[h * kT + row] = m;
+        tc::named_bar(1, kSoftThreads);
+        m = fmaxf(rb[row], rb[kT + row]);
+      }
+      // P~ = exp(S - m) -> bf16 smem tile for the P~ g MMA; l = sum of P~ in fp32
       const float ml = m * kLog2e;
       float l = 0.0f;
-      for (int c = 0; c < NC; ++c, ++su, ++pc) {
-        const int sb = su & 1, pb = pc & 1;
-        tc::mbar_wait(&sfull[sb], (su >> 1) & 1);
-        tc::tc_fence_after();
-        float v[32], w[32];
-        tc::tmem_ld32(lrow + sb * kT + h * 64, v);
-        tc::tmem_ld32(lrow + sb * kT + h * 64 + 32, w);
-        tc::tc_fence_before();
-        tc::mbar_arrive(&sempty[sb]);
+      for (int c = 0; c < NC; ++c, ++pc) {
+        const int pb = pc & 1;
+        if (c > 0 || !single) {   // single pass: chunk 0's scores are still in registers
+          const int sb = su & 1;
+          tc::mbar_wait(&sfull[sb], (su >> 1) & 1);
+          tc::tc_fence_after();
+          tc::tmem_ld32(lrow + sb * kT + h * 64, v);
+          tc::tmem_ld32(lrow + sb * kT + h * 64 + 32, w);
+          tc::tc_fence_before();
+          tc::mbar_arrive(&sempty[sb]);
+          ++su;
+        }
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           v[j] = tc::ex2(fmaf(v[j], kLog2e, -ml));
@@ -705,6 +781,34 @@ __global__ void k_attn_dtheta_reduce(const float* __restrict__ part, int nkb, lo
   }
 }
 }  // namespace
+
+__global__ void k_attn_phimax(const bf16* __restrict__ phi, int Q, int Cq, float* __restrict__ out) {
+  __shared__ float red[8];
+  const bf16* p = phi + (long long)blockIdx.x * Q * Cq;
+  float mx = 0.0f;
+  for (int j = threadIdx.x; j < Q; j += blockDim.x) {
+    float t = 0.0f;
+    for (int c = 0; c < Cq; ++c) {
+      const float x = __bfloat162float(p[(long long)j * Cq + c]);
+      t = fmaf(x, x, t);
+    }
+    mx = fmaxf(mx, t);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float m = 0.0f;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) m = fmaxf(m, red[i]);
+    out[blockIdx.x] = sqrtf(m);
+  }
+}
+
+cudaError_t attn_phimax(const void* phi, int n, int Q, int Cq, float* phimax, cudaStream_t st) {
+  k_attn_phimax<<<n, 256, 0, st>>>(static_cast<const bf16*>(phi), Q, Cq, phimax);
+  return cudaGetLastError();
+}
 
 cudaError_t attn_transpose(const void* gp, int n, int Q, int C, void* gT, cudaStream_t st) {
   dim3 grid((Q + 31) / 32, (C + 31) / 32, n);

@@ -1,7 +1,8 @@
 """Fused tcgen05 attention core (reading R8) through the C-ABI
 (`paragan_op_attn_fwd` / `paragan_op_attn_bwd`), element by element against the plain
 definition in float64 with the bf16 storage points of R14 / R21 (the unnormalised
-exp(S - m) and dS stored bf16):
+exp(S - m) and dS stored bf16; the kernel's offset m is the exact row max or, in the single-pass
+forward, chunk 0's max — a rounding-level difference):
 
     S = theta phi^T,  m = rowmax(S),  l = rowsum(exp(S - m)),  beta = exp(S - m) / l
     o = bf16(exp(S - m)) g / l
@@ -57,8 +58,11 @@ CASES = [(2, 4096, 16, 48, 80), (1, 4096, 32, 96, 160), (3, 512, 16, 16, 48), (2
 
 
 @pytest.mark.parametrize("n,hw,cq,c2,ct", CASES)
-@pytest.mark.parametrize("scale", [0.5, 1.5])
+@pytest.mark.parametrize("scale", [0.5, 1.5, 6.0])
 def test_attn_fwd_bwd_vs_definition(n, hw, cq, c2, ct, scale):
+    """scale 0.5 / 1.5: every tile takes the single-pass forward (the score bound is within e^16 of chunk 0's
+    max, R21); scale 6: the scores spread over hundreds, the bound check fails and the tiles take the exact
+    two-pass forward."""
     qkv, phi, gp, dO = _inputs(n, hw, cq, c2, ct, scale, seed=hw + cq + c2)
     want = _reference(qkv, phi, gp, dO, cq)
     q = hw // 4
@@ -73,9 +77,10 @@ def test_attn_fwd_bwd_vs_definition(n, hw, cq, c2, ct, scale):
     dgp = torch.empty(n, q, c2, dtype=torch.float32, device=DEV)
     api.op_attn_bwd(qkv_d, phi_d, gp_d, dO_d, o32, lse, cq, c2, dqkv, dphi, dgp)
     torch.cuda.synchronize()
-    # forward: o32 is the fp32 accumulation of the same bf16 products (a rounding flip of
-    # one beta entry is the only other difference); o adds one bf16 rounding
-    assert _rel(o32.double().cpu(), want["o"]) < 2e-3
+    # forward: o32 and the reference each carry one bf16 rounding of every P~ = exp(S - m) (<= 2^-9
+    # relative each), taken at different offsets m in the single-pass schedule: bar 2 * 2^-9; o adds one
+    # bf16 rounding of the output
+    assert _rel(o32.double().cpu(), want["o"]) < 2 * 2 ** -9
     assert _rel(o.double().cpu(), want["o"]) < 6e-3
     assert float((lse.double().cpu() - want["lse"]).abs().max()) < 1e-4 * max(1.0, float(want["lse"].abs().max()))
     # backward

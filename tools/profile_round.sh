@@ -4,13 +4,13 @@
 #   gpurun_out/layers.md             per-layer tcgen05 conv table from CUDA events inside a bench step
 #   gpurun_out/r1_<name>.md          ncu --set full summaries of the top kernels
 export PARAGAN_ALLOW_SHORT_WARMUP=1
-CMD="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-profile"
+CMD="python bench.py --steps 1 --warmup 1 --repeats 1 --reals uniform --no-cpu-baseline --no-e2e --no-profile"
 $CMD > gpurun_out/plain_round.log 2>&1 || exit 1
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 3000 --csv \
     --log-file gpurun_out/launches_raw.csv $CMD > gpurun_out/ncu_launches.log 2>&1
 python tools/ncu_compact.py gpurun_out/launches_raw.csv > gpurun_out/launches_compact.csv
 python tools/ncu_summary.py gpurun_out/launches_raw.csv --iters 2 > gpurun_out/launches_summary.md 2>&1
 rm -f gpurun_out/launches_raw.csv
-PARAGAN_PROFILE_VERBOSE=1 python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2> gpurun_out/layers.err
+PARAGAN_PROFILE_VERBOSE=1 python bench.py --steps 1 --warmup 3 --repeats 1 --reals uniform --no-cpu-baseline --no-e2e > /dev/null 2> gpurun_out/layers.err
 python tools/prof_layers.py gpurun_out/layers.err 60 > gpurun_out/layers.md
 bash tools/profile_top_kernels.sh "$@"
