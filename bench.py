@@ -233,6 +233,18 @@ def run_async(args):
     return 0
 
 
+def _tensor_pipe():
+    """ncu tensor-pipe utilisation of the profiled conv kernels (profiles/round*_tensor_pipe.json)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "round*_tensor_pipe.json")))
+    if not files:
+        return None, None
+    with open(files[-1]) as f:
+        d = json.load(f)
+    conv = {k: v["tensor_pipe_pct"] for k, v in d.items() if isinstance(v, dict) and k.startswith("k_conv")}
+    return conv, os.path.relpath(files[-1], ROOT)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -437,6 +449,13 @@ def main():
                     "wgrad": {"achieved": (f1_ / (t1 / 1000.0)) / 1e12 if t1 > 0 else 0.0,
                               "achieved_executed": (prof[4][2] / (t1 / 1000.0)) / 1e12 if t1 > 0 else 0.0,
                               "launches": n1, "ms_per_step": t1 / args.steps}}
+            pipe, pipe_src = _tensor_pipe()
+            ex = (prof[3][2] + prof[4][2]) / ((t0 + t1) / 1000.0) / 1e12 if (t0 + t1) > 0 else 0.0
+            conv_util = {"executed_tflops": ex, "frac_of_sustained_peak": ex / sustained,
+                         "algorithmic_tflops": (f0_ + f1_) / ((t0 + t1) / 1000.0) / 1e12 if (t0 + t1) > 0 else 0.0,
+                         "note": "all tcgen05 conv launches (fprop, dgrad, wgrad) of the step, CUDA events: flops "
+                                 "issued to the tensor cores / time, vs the measured sustained bf16 peak",
+                         "ncu_tensor_pipe_pct": pipe, "ncu_source": pipe_src}
             roof["other_kernels_ms_per_step"] = {
                 "fused_attention_fwd_bwd": prof[5][1] / args.steps,
                 "g_output_layer_fp32_thin": prof[6][1] / args.steps}
@@ -461,7 +480,8 @@ def main():
                            **({"ablation": "Table 3 precision toggle: fp32 SIMT engine (P:420-434)"}
                               if compute == api.F32 else {})},
                 "img_per_s_per_gpu": value / world, "real_img_per_s": value * args.d_steps,
-                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+                "roofline": roof, "conv_tensor_pipe_util": conv_util if prof else None,
+                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                 "clocks": clk.summary(),
                 "repeats_ms_per_step": [round(m / args.steps, 3) for m in rep_ms],
                 "losses": {"d": st.d_loss, "g": st.g_loss, "d_per_step_e2e": d_losses,

@@ -2991,8 +2991,8 @@ __global__ void __launch_bounds__(512) k_thin_wgrad(const float* __restrict__ x,
       xw[r][0] = xs[((py + r) * HC + 0) * C + c];
       xw[r][1] = xs[((py + r) * HC + 1) * C + c];
     }
-#pragma unroll 4
-    for (int px = 0; px < kWTW; ++px) {
+#pragma unroll
+    for (int px = 0; px < kWTW; ++px) {   // fully unrolled: the window slide is register renaming, not moves
 #pragma unroll
       for (int r = 0; r < 3; ++r) xw[r][2] = xs[((py + r) * HC + px + 2) * C + c];
       const float4 g = *reinterpret_cast<const float4*>(dys + (py * kWTW + px) * 4);
