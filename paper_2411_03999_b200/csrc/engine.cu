@@ -1076,7 +1076,11 @@ class Engine final : public EngineBase {
       b.learn_sc = (b.cin != b.cout) || b.down;
       const std::string p = "b" + std::to_string(j) + ".";
       b.c1 = conv(D_, p + "conv1", b.cin, b.cin_x, b.cout, 3, true);
-      if (kBF && ar.din[j] < 0) {
+      static const bool im2col_on = [] {
+        const char* e = std::getenv("PARAGAN_IM2COL");
+        return e == nullptr || std::atoi(e) != 0;
+      }();
+      if (kBF && ar.din[j] < 0 && im2col_on) {
         b.im2col = true;
         b.c1x = b.c1;
         b.c1x.cin = 27;
