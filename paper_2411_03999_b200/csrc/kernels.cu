@@ -2846,17 +2846,21 @@ __device__ __forceinline__ void cp_async4_zfill(float* dst, const float* src, bo
   const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(src), "r"(ok ? 4 : 0) : "memory");
 }
-template <int CO>
-__global__ void __launch_bounds__(384, 2) k_thin_dgrad(const float* __restrict__ dy, int N, int H, int W, int C,
+// CPT channels per thread (c and c + C/CPT): each broadcast dy load then feeds CPT x 27 FMAs
+template <int CO, int CPT>
+__global__ void __launch_bounds__(CPT == 1 ? 384 : 192, CPT == 1 ? 2 : 3) k_thin_dgrad(const float* __restrict__ dy, int N, int H, int W, int C,
                                                        const float* __restrict__ w, float* __restrict__ dx) {
   constexpr int HR = kDTH + 2, HC = kDTW + 2, kHalo = HR * HC;
   __shared__ float4 ds[2][kHalo];
   const int tiles_w = (W + kDTW - 1) / kDTW, tiles_h = (H + kDTH - 1) / kDTH;
   const int tiles = N * tiles_h * tiles_w;
-  const int c = threadIdx.x % C, pg = threadIdx.x / C, npg = blockDim.x / C;
-  float wv[CO * 9];   // wv[o*9 + r*3 + s] = w[o][r][s][c]
+  const int Ct = C / CPT;   // threads per pixel group
+  const int c = threadIdx.x % Ct, pg = threadIdx.x / Ct, npg = blockDim.x / Ct;
+  float wv[CPT][CO * 9];   // wv[j][o*9 + r*3 + s] = w[o][r][s][c + j*Ct]
 #pragma unroll
-  for (int k = 0; k < CO * 9; ++k) wv[k] = w[(long long)k * C + c];
+  for (int j = 0; j < CPT; ++j)
+#pragma unroll
+    for (int k = 0; k < CO * 9; ++k) wv[j][k] = w[(long long)k * C + c + j * Ct];
   auto stage = [&](int t, int buf) {
     int u = t;
     const int tw = u % tiles_w;
@@ -2889,7 +2893,11 @@ __global__ void __launch_bounds__(384, 2) k_thin_dgrad(const float* __restrict__
     const float4* hal = ds[buf];
     for (int q = pg; q < kDTH * (kDTW / 4); q += npg) {
       const int row = q / (kDTW / 4), x0 = (q % (kDTW / 4)) * 4;
-      float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+      float acc[CPT][4];
+#pragma unroll
+      for (int j = 0; j < CPT; ++j)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[j][i] = 0.0f;
       // output (row, x0 + i) reads halo (row + 2 - r, x0 + i + 2 - s)
 #pragma unroll
       for (int hr = 0; hr < 3; ++hr) {        // halo row row + hr  <->  r = 2 - hr
@@ -2903,7 +2911,9 @@ __global__ void __launch_bounds__(384, 2) k_thin_dgrad(const float* __restrict__
             const int sx = i + 2 - cc;
             if (sx >= 0 && sx <= 2) {
 #pragma unroll
-              for (int o = 0; o < CO; ++o) acc[i] = fmaf(gv[o], wv[o * 9 + r * 3 + sx], acc[i]);
+              for (int j = 0; j < CPT; ++j)
+#pragma unroll
+                for (int o = 0; o < CO; ++o) acc[j][i] = fmaf(gv[o], wv[j][o * 9 + r * 3 + sx], acc[j][i]);
             }
           }
         }
@@ -2913,7 +2923,10 @@ __global__ void __launch_bounds__(384, 2) k_thin_dgrad(const float* __restrict__
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int ww = w0 + x0 + i;
-          if (ww < W) dx[(((long long)n * H + h) * W + ww) * C + c] = acc[i];
+          if (ww < W) {
+#pragma unroll
+            for (int j = 0; j < CPT; ++j) dx[(((long long)n * H + h) * W + ww) * C + c + j * Ct] = acc[j][i];
+          }
         }
       }
     }
@@ -3334,12 +3347,16 @@ cudaError_t thin_conv_dgrad(const float* dy, int N, int H, int W, int C, const f
                             cudaStream_t st) {
   if (CO != 3 || C > 384) return cudaErrorInvalidValue;
   const int tiles = N * ((H + kDTH - 1) / kDTH) * ((W + kDTW - 1) / kDTW);
-  const int npg = 384 / C;
+  static const int cpt_env = getenv("PARAGAN_THIN_DG_CPT") ? atoi(getenv("PARAGAN_THIN_DG_CPT")) : 2;
+  const int cpt = (cpt_env == 2 && C % 2 == 0 && 192 % (C / 2) == 0) ? 2 : 1;
+  const int Ct = C / cpt, npg = (cpt == 2 ? 192 : 384) / Ct;
   int per_sm = 1;
-  PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_thin_dgrad<3>, npg * C, 0));
+  if (cpt == 2) PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_thin_dgrad<3, 2>, npg * Ct, 0));
+  else PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_thin_dgrad<3, 1>, npg * Ct, 0));
   if (per_sm < 1) per_sm = 1;
   const int grid = tiles < per_sm * sm_cap() ? tiles : per_sm * sm_cap();
-  k_thin_dgrad<3><<<grid, npg * C, 0, st>>>(dy, N, H, W, C, w, dx);
+  if (cpt == 2) k_thin_dgrad<3, 2><<<grid, npg * Ct, 0, st>>>(dy, N, H, W, C, w, dx);
+  else k_thin_dgrad<3, 1><<<grid, npg * Ct, 0, st>>>(dy, N, H, W, C, w, dx);
   return cudaGetLastError();
 }
 cudaError_t thin_conv_wgrad(const float* x, const float* dy, int N, int H, int W, int C, int CO, float* dw,
