@@ -12,5 +12,5 @@ python tools/ncu_compact.py gpurun_out/launches_raw.csv > gpurun_out/launches_co
 python tools/ncu_summary.py gpurun_out/launches_raw.csv --iters 2 > gpurun_out/launches_summary.md 2>&1
 rm -f gpurun_out/launches_raw.csv
 PARAGAN_PROFILE_VERBOSE=1 python bench.py --steps 1 --warmup 3 --repeats 1 --reals uniform --no-cpu-baseline --no-e2e > /dev/null 2> gpurun_out/layers.err
-python tools/prof_layers.py gpurun_out/layers.err 60 > gpurun_out/layers.md
+python tools/prof_layers.py gpurun_out/layers.err 70 2 > gpurun_out/layers.md
 bash tools/profile_top_kernels.sh "$@"
