@@ -261,6 +261,8 @@ def main():
     ap.add_argument("--reals", default="g0", choices=["g0", "uniform"],
                     help="g0: reals from the initial G plus noise (default, D unsaturated); uniform: U(-1,1) noise "
                          "images without the generation pass (profiling runs: fewer launches before the step)")
+    ap.add_argument("--trace", type=int, default=0,
+                    help="diagnostic: run this many steps from the initial state, print each step's losses, exit")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
@@ -361,6 +363,14 @@ def main():
                 torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             return float(t.item())
 
+        if args.trace:
+            for i in range(args.trace):
+                step(i)
+                s2 = ctx.sync_stats(raise_nonfinite=False)
+                print(json.dumps({"trace_step": i, "d_loss": float(s2.d_loss), "g_loss": float(s2.g_loss)}),
+                      flush=True)
+            ctx.close()
+            return 0
         for i in range(args.warmup):
             step(i)
         st = ctx.sync_stats(raise_nonfinite=False)

@@ -362,6 +362,19 @@ paragan_status paragan_op_conv_up2_wgrad(const void* x, const void* dy, int32_t 
 paragan_status paragan_op_conv_dgrad(paragan_dtype dt, const void* dy, int32_t n, int32_t h, int32_t w, int32_t cout,
                                      const void* wgt, int32_t cin, int32_t ksz, void* dx, void* stream);
 
+/* G's fp32 output layer as the BF16 engine runs it on the tensor cores (reading R36 in DESIGN.md):
+ * x fp32 [N,H,W,Cin] is split into two bf16 planes x1 = bf16(x), x2 = bf16(x - x1), w fp32 [3][9][Cin]
+ * (OHWI) into three bf16 terms w1 = bf16(w), w2 = bf16(w - w1), w3 = bf16(w - w1 - w2), and
+ *   y[p][o] = bias[o] + sum_{tap,c} (x1 + x2)[p + tap][c] (w1 + w2)[o][tap][c] + x1[p + tap][c] w3[o][tap][c]
+ * with fp32 tensor-core accumulation (y fp32 [N,H,W,3]; bias may be NULL).  When dy (fp32 [N,H,W,3]) and
+ * dw (fp32 [3][9][Cin]) are both non-NULL, also dw[o][tap][c] = sum_p dy[p][o] (x1 + x2)[p + tap][c] — the
+ * engine's weight gradient, read from the same split planes.  3x3 pad 1; Cin % 8 == 0, Cin <= 128, W a power
+ * of two with the 128-pixel tiling of op_conv_fwd; device pointers, 16-byte aligned; the split planes are a
+ * stream-ordered temporary.  PARAGAN_ERR_INVALID_ARG on a shape or alignment violation. */
+paragan_status paragan_op_out_conv_split(const float* x, int32_t n, int32_t h, int32_t w, int32_t cin,
+                                         const float* wgt, const float* bias, float* y, const float* dy, float* dw,
+                                         void* stream);
+
 /* Fused attention core of the non-local block (BigGAN's self-attention,
  * reading R8 — beta = softmax_rows(theta^T phi) without a 1/sqrt(d) scale, o = beta g).
  * BF16 only (tcgen05).  Per image of hw pixels and q = hw/4 pooled keys:

@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libparagan.so")
-SOURCES = ["tc_conv.cu", "tc_attn.cu", "kernels.cu", "optim.cu", "host_io.cu", "engine.cu", "api.cu"]
+SOURCES = ["tc_conv.cu", "tc_attn.cu", "tc_outconv.cu", "kernels.cu", "optim.cu", "host_io.cu", "engine.cu", "api.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -11,6 +11,7 @@
 #include "kernels.h"
 #include "tc_attn.h"
 #include "tc_conv.h"
+#include "tc_outconv.h"
 
 struct paragan_ctx {
   pg::EngineBase* eng = nullptr;
@@ -255,6 +256,30 @@ paragan_status paragan_op_conv_fwd_ex(const void* x, int32_t n, int32_t h, int32
   e.relu_out = relu_out ? 1 : 0;
   e.out = y;
   return cuda_status(tc_conv_fprop(x, n, h, w, cin, wgt, cout, ksz, e, static_cast<cudaStream_t>(stream)));
+}
+
+paragan_status paragan_op_out_conv_split(const float* x, int32_t n, int32_t h, int32_t w, int32_t cin,
+                                         const float* wgt, const float* bias, float* y, const float* dy, float* dw,
+                                         void* stream) {
+  if (!x || !wgt || !y || n < 1 || h < 1 || w < 1 || !out_conv_tc_ok(h, w, cin) || !aligned16(x) ||
+      !aligned16(wgt) || (dw && !dy))
+    return PARAGAN_ERR_INVALID_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const long long P = (long long)n * h * w;
+  const size_t plane_bytes = (size_t)P * 2 * cin * sizeof(uint16_t), ws_bytes = (size_t)96 * 2 * cin * 2;
+  const size_t scratch_n = dw ? (size_t)4 * 148 * 27 * cin : 0;
+  char* tmp = nullptr;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&tmp), plane_bytes + ws_bytes + scratch_n * 4, st) != cudaSuccess)
+    return PARAGAN_ERR_CUDA;
+  bf16* xs = reinterpret_cast<bf16*>(tmp);
+  bf16* ws = reinterpret_cast<bf16*>(tmp + plane_bytes);
+  float* scratch = reinterpret_cast<float*>(tmp + plane_bytes + ws_bytes);
+  cudaError_t e = split_planes(x, P, cin, xs, st);
+  if (e == cudaSuccess) e = split_out_weights(wgt, cin, ws, st);
+  if (e == cudaSuccess) e = out_conv_fwd_tc(xs, n, h, w, cin, ws, bias, y, st);
+  if (e == cudaSuccess && dw) e = thin_conv_wgrad(xs, dy, n, h, w, cin, 3, dw, scratch, scratch_n, st, true);
+  cudaFreeAsync(tmp, st);
+  return cuda_status(e);
 }
 
 paragan_status paragan_op_conv_wgrad(paragan_dtype dt, const void* x, const void* dy, int32_t n, int32_t h, int32_t w,

@@ -27,6 +27,7 @@
 #include "kernels.h"
 #include "optim.h"
 #include "tc_conv.h"
+#include "tc_outconv.h"
 
 namespace pg {
 
@@ -221,6 +222,8 @@ class Engine final : public EngineBase {
     attn_single_ = as == nullptr || std::atoi(as) != 0;
     const char* sp = std::getenv("PARAGAN_SUBPIXEL");
     subpix_ = kBF && (sp == nullptr || std::atoi(sp) != 0);
+    const char* tt = std::getenv("PARAGAN_THIN_TC");
+    thin_tc_ = kBF && (tt == nullptr || std::atoi(tt) != 0);
     dcgan_ = c.arch == PARAGAN_ARCH_SNDCGAN;
   }
   ~Engine() override {
@@ -1169,7 +1172,11 @@ class Engine final : public EngineBase {
       b.sums1 = A.get<double>(2 * b.cin);
       b.sums2 = A.get<double>(2 * b.cout);
     }
-    aout_ = A.get<float>((size_t)B * R_ * R_ * cl_);   // fp32 output-BN activation
+    // fp32 output-BN activation, or — tensor-core output layer (R36) — its two-term bf16 split
+    // [x1 | x2], the same bytes
+    aout_ = A.get<float>((size_t)B * R_ * R_ * cl_);
+    thin_tc_ = thin_tc_ && out_conv_tc_ok(R_, R_, cl_);
+    if (thin_tc_) oconv_ws_ = A.get<bf16>((size_t)96 * 2 * cl_);
     omean_ = A.get<float>(cl_);
     orstd_ = A.get<float>(cl_);
     osums_ = A.get<double>(2 * cl_);
@@ -1796,11 +1803,25 @@ class Engine final : public EngineBase {
     // output layer in fp32: BN -> ReLU -> conv3x3 (96 -> 3) -> tanh
     const long long M = (long long)B * R_ * R_;
     CKS(bn_forward_stats(gout_in_, M, cl_, osums_, omean_, orstd_));
-    CK((bn_apply_relu<T, float>(static_cast<const T*>(gout_in_), B, R_, R_, cl_, omean_, orstd_, nullptr, nullptr,
-                                G_.P(obn_g_), G_.P(obn_b_), aout_, false, st_)));
-    CK(timed(6, 2.0 * B * R_ * R_ * 27.0 * cl_, [&] {
-      return thin_conv_fwd(aout_, B, R_, R_, cl_, static_cast<const float*>(oconv_.wp), 3, G_.P(oconv_.b), pre_, st_);
-    }, "thin fwd"));
+    if constexpr (kBF) {
+      if (thin_tc_) {   // on the tensor cores through the bf16 splits of activation and weight (R36)
+        CK(bn_apply_relu_split(static_cast<const bf16*>(gout_in_), B, R_, R_, cl_, omean_, orstd_, G_.P(obn_g_),
+                               G_.P(obn_b_), reinterpret_cast<bf16*>(aout_), st_));
+        CK(timed(6, 2.0 * B * R_ * R_ * 27.0 * cl_, [&] {
+          PG_CUDA(split_out_weights(static_cast<const float*>(oconv_.wp), cl_, oconv_ws_, st_));
+          return out_conv_fwd_tc(aout_, B, R_, R_, cl_, oconv_ws_, G_.P(oconv_.b), pre_, st_);
+        }, "thin fwd"));
+        ++launches_;   // two launches in the timed region above
+      }
+    }
+    if (!thin_tc_) {
+      CK((bn_apply_relu<T, float>(static_cast<const T*>(gout_in_), B, R_, R_, cl_, omean_, orstd_, nullptr, nullptr,
+                                  G_.P(obn_g_), G_.P(obn_b_), aout_, false, st_)));
+      CK(timed(6, 2.0 * B * R_ * R_ * 27.0 * cl_, [&] {
+        return thin_conv_fwd(aout_, B, R_, R_, cl_, static_cast<const float*>(oconv_.wp), 3, G_.P(oconv_.b), pre_,
+                             st_);
+      }, "thin fwd"));
+    }
     CK(tanh_to_image<T>(pre_, img_, static_cast<T*>(dimg_), M, cpad_, st_));
     return PARAGAN_OK;
   }
@@ -2365,7 +2386,8 @@ class Engine final : public EngineBase {
     // tanh' and the fp32 output conv
     CK(tanh_bwd<T>(static_cast<const T*>(dimg_grad_), cpad_, img_, dpre_, M, st_));
     CK(timed(6, 2.0 * B * R_ * R_ * 27.0 * cl_, [&] {
-      return thin_conv_wgrad(aout_, dpre_, B, R_, R_, cl_, 3, G_.G(oconv_.w), scratch_f_, scratch_floats_, st_);
+      return thin_conv_wgrad(aout_, dpre_, B, R_, R_, cl_, 3, G_.G(oconv_.w), scratch_f_, scratch_floats_, st_,
+                             thin_tc_);
     }, "thin wgrad"));
     CK(col_sum<float>(dpre_, M, 3, dpart_, kMaxPartialBlocks, G_.G(oconv_.b), 0, st_));
     CK(timed(6, 2.0 * B * R_ * R_ * 27.0 * cl_, [&] {
@@ -2481,6 +2503,8 @@ class Engine final : public EngineBase {
   bool overlap_ = false, pending_d_ = false;
   int overlap_sms_ = 16, overlap_blocks_ = 3;
   bool ready_ = false, poisoned_ = false, planned_ = false, ones_ready_ = false;
+  bool thin_tc_ = false;  // G's output layer on the tensor cores via bf16 splits (R36; BF16 mode)
+  bf16* oconv_ws_ = nullptr;  // its split weight operand [96][2 cl]
   bool subpix_ = false;   // G conv1 as four phase 2x2 convs of the low-resolution input (NEXT-1)
   bool attn_single_ = true;   // single-pass fused attention forward when the score bound allows (R21)
   bool dcgan_ = false;    // SN-DCGAN (config 1) instead of BigGAN

@@ -3,6 +3,7 @@
 // thread per 8-channel group of a pixel (16-byte vectors for bf16), grids are
 // sized in multiples of the 148 SMs, reductions are warp-shuffle + shared
 // memory with fp64 cross-block accumulation in a fixed order (deterministic).
+#include <type_traits>
 #include <cuda_bf16.h>
 
 #include "common.cuh"
@@ -761,6 +762,10 @@ __global__ void __launch_bounds__(256) k_bn_bwd_apply_cs(const TI* __restrict__ 
 // stores.  (The register-staged kernels held 2 x 16 B per thread in flight at 68-90 registers,
 // ~24 KB per SM: 4.1-4.5 TB/s.)
 
+// TO = Bf16Split: the output is the two-term bf16 split of the fp32 result, y = [P][2C] with x1 = bf16(v) in
+// channels [0, C) and x2 = bf16(v - x1) in [C, 2C) (the operand of G's tensor-core output layer, R36)
+struct Bf16Split {};
+
 template <typename TI, typename TO>
 __global__ void __launch_bounds__(256) k_bn_apply_relu_bulk(const TI* __restrict__ x, long long P_total, int HW, int C,
                                                             const float* __restrict__ mean,
@@ -821,7 +826,16 @@ __global__ void __launch_bounds__(256) k_bn_apply_relu_bulk(const TI* __restrict
           const float tt = (v[j] - mu[j]) * rs[j] * ga[j] + be[j];
           v[j] = tt > 0.0f ? tt : 0.0f;
         }
-        Vec8<TO>::store(y + p * C + g * 8, v);
+        if constexpr (std::is_same<TO, Bf16Split>::value) {
+          float lo[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) lo[j] = v[j] - __bfloat162float(__float2bfloat16_rn(v[j]));
+          bf16* ys = reinterpret_cast<bf16*>(y) + p * 2 * C + g * 8;
+          Vec8<bf16>::store(ys, v);
+          Vec8<bf16>::store(ys + C, lo);
+        } else {
+          Vec8<TO>::store(y + p * C + g * 8, v);
+        }
       }
     }
     __syncthreads();   // every thread is done with buf[b]
@@ -2294,6 +2308,23 @@ template cudaError_t bn_apply_relu<bf16, float>(const bf16*, int, int, int, int,
                                                 const float*, const float*, const float*, const float*, float*, bool,
                                                 cudaStream_t);
 
+cudaError_t bn_apply_relu_split(const bf16* x, int N, int H, int W, int C, const float* mean, const float* rstd,
+                                const float* gamma, const float* beta, bf16* y2, cudaStream_t st) {
+  const int G = C / 8;
+  if (C % 8 || G > 256 || (long long)C * 2 > kBnChunkBytes ||
+      ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y2)) & 15))
+    return cudaErrorInvalidValue;
+  const int lanes = 256 / G;
+  const long long P = (long long)N * H * W;
+  const long long cmax = kBnChunkBytes / ((long long)C * 2);
+  const long long cpix = cmax >= lanes ? cmax / lanes * lanes : cmax;
+  long long blocks = (P + cpix - 1) / cpix;
+  if (blocks > 4LL * sm_cap()) blocks = 4LL * sm_cap();
+  k_bn_apply_relu_bulk<bf16, Bf16Split><<<(unsigned)blocks, lanes * G, 0, st>>>(
+      x, P, H * W, C, mean, rstd, BnAffine{nullptr, nullptr, gamma, beta}, reinterpret_cast<Bf16Split*>(y2));
+  return cudaGetLastError();
+}
+
 template <typename TI, typename TG>
 cudaError_t bn_bwd_reduce(const TI* x, const TG* dy, int N, int H, int W, int C, const float* mean, const float* rstd,
                           const float* gain, const float* bias, const float* gamma, const float* beta, bool up2,
@@ -2948,7 +2979,9 @@ __device__ __forceinline__ void cp_async_zfill(void* dst, const void* src, int b
   else
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(src), "r"(bytes_valid) : "memory");
 }
-template <int CO>
+// SPLIT: x is the two-term bf16 split [P][2C] of the fp32 activation (R36) — the same 4C bytes per pixel as
+// fp32, so the staging is unchanged and each read sums the pair, x = x1 + x2, in fp32
+template <int CO, bool SPLIT>
 __global__ void __launch_bounds__(512) k_thin_wgrad(const float* __restrict__ x, const float* __restrict__ dy, int N,
                                                     int H, int W, int C, float* __restrict__ partial) {
   extern __shared__ float4 sm4[];
@@ -2989,6 +3022,15 @@ __global__ void __launch_bounds__(512) k_thin_wgrad(const float* __restrict__ x,
   float acc[CO * 9];
 #pragma unroll
   for (int k = 0; k < CO * 9; ++k) acc[k] = 0.0f;
+  // x at staged pixel slot q (row-major over the [kWTH+2][kWTW+2] halo), channel c
+  auto xat = [&](const float* xs, int q) -> float {
+    if constexpr (SPLIT) {
+      const bf16* xb = reinterpret_cast<const bf16*>(xs) + (size_t)q * 2 * C + c;
+      return __bfloat162float(xb[0]) + __bfloat162float(xb[C]);
+    } else {
+      return xs[q * C + c];
+    }
+  };
   int buf = 0;
   if (blockIdx.x < tiles) stage(blockIdx.x, 0);
   for (int t = blockIdx.x; t < tiles; t += gridDim.x, buf ^= 1) {
@@ -3001,13 +3043,13 @@ __global__ void __launch_bounds__(512) k_thin_wgrad(const float* __restrict__ x,
     float xw[3][3];
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
-      xw[r][0] = xs[((py + r) * HC + 0) * C + c];
-      xw[r][1] = xs[((py + r) * HC + 1) * C + c];
+      xw[r][0] = xat(xs, (py + r) * HC + 0);
+      xw[r][1] = xat(xs, (py + r) * HC + 1);
     }
 #pragma unroll
     for (int px = 0; px < kWTW; ++px) {   // fully unrolled: the window slide is register renaming, not moves
 #pragma unroll
-      for (int r = 0; r < 3; ++r) xw[r][2] = xs[((py + r) * HC + px + 2) * C + c];
+      for (int r = 0; r < 3; ++r) xw[r][2] = xat(xs, (py + r) * HC + px + 2);
       const float4 g = *reinterpret_cast<const float4*>(dys + (py * kWTW + px) * 4);
       const float gv[3] = {g.x, g.y, g.z};
 #pragma unroll
@@ -3359,8 +3401,8 @@ cudaError_t thin_conv_dgrad(const float* dy, int N, int H, int W, int C, const f
   else k_thin_dgrad<3, 1><<<grid, npg * Ct, 0, st>>>(dy, N, H, W, C, w, dx);
   return cudaGetLastError();
 }
-cudaError_t thin_conv_wgrad(const float* x, const float* dy, int N, int H, int W, int C, int CO, float* dw,
-                            float* scratch, size_t scratch_floats, cudaStream_t st) {
+cudaError_t thin_conv_wgrad(const void* x, const float* dy, int N, int H, int W, int C, int CO, float* dw,
+                            float* scratch, size_t scratch_floats, cudaStream_t st, bool split) {
   if (CO != 3 || C % 4 || C > 128 || ((uintptr_t)x & 15)) return cudaErrorInvalidValue;
   const int tiles = N * ((H + kWTH - 1) / kWTH) * ((W + kWTW - 1) / kWTW);
   const size_t sm = (size_t)(2 * (kWTH + 2) * (kWTW + 2) * C + 2 * kWTH * kWTW * 4) * sizeof(float);
@@ -3371,10 +3413,69 @@ cudaError_t thin_conv_wgrad(const float* x, const float* dy, int N, int H, int W
   if (grid > tiles) grid = tiles;
   const int n = CO * 9 * C;
   while ((size_t)grid * n > scratch_floats && grid > 1) grid /= 2;
-  PG_CUDA(cudaFuncSetAttribute(k_thin_wgrad<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  k_thin_wgrad<3><<<grid, kWTH * C, sm, st>>>(x, dy, N, H, W, C, scratch);
+  const float* xf = static_cast<const float*>(x);
+  if (split) {   // (the smem size depends on C: set on every call)
+    PG_CUDA(cudaFuncSetAttribute(k_thin_wgrad<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    k_thin_wgrad<3, true><<<grid, kWTH * C, sm, st>>>(xf, dy, N, H, W, C, scratch);
+  } else {
+    PG_CUDA(cudaFuncSetAttribute(k_thin_wgrad<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    k_thin_wgrad<3, false><<<grid, kWTH * C, sm, st>>>(xf, dy, N, H, W, C, scratch);
+  }
   PG_LAUNCH_CHECK();
   k_reduce_rows_f32<<<ceil_div(n, 256), 256, 0, st>>>(scratch, grid, n, dw);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Operands of G's output layer on the tensor cores (R36; tc_outconv.cu).  x (fp32) -> [x1 | x2],
+// x1 = bf16(x), x2 = bf16(x - x1); w (fp32 [CO = 3][9][C]) -> w1 + w2 + w3 (w1 = bf16(w), w2 = bf16(w - w1),
+// w3 = bf16(w - w1 - w2)) laid out as the B operand [96][2C] over the split A = [x1 | x2]: row
+// t * 9 + term * 3 + o holds, for tap t and output o,
+//   term 0: [w1 | w1]  -> x1 w1 + x2 w1
+//   term 1: [w2 | w2]  -> x1 w2 + x2 w2
+//   term 2: [w3 | 0 ]  -> x1 w3
+// (rows 81..95 zero), so the three terms' sum drops only x2 w3 (< 2^-25 |x w|) and the split residual of x
+// (|x - x1 - x2| <= 2^-18 |x|).
+__global__ void k_split_planes(const float* __restrict__ x, long long P, int C, bf16* __restrict__ y) {
+  const long long n = P * (C / 4);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const long long p = i / (C / 4);
+    const int c = (int)(i - p * (C / 4)) * 4;
+    const float4 v = *reinterpret_cast<const float4*>(x + p * C + c);
+    const float f[4] = {v.x, v.y, v.z, v.w};
+    __nv_bfloat16 hi[4], lo[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      hi[j] = __float2bfloat16_rn(f[j]);
+      lo[j] = __float2bfloat16_rn(f[j] - __bfloat162float(hi[j]));
+    }
+    *reinterpret_cast<uint2*>(y + p * 2 * C + c) = *reinterpret_cast<const uint2*>(hi);
+    *reinterpret_cast<uint2*>(y + p * 2 * C + C + c) = *reinterpret_cast<const uint2*>(lo);
+  }
+}
+__global__ void k_split_out_weights(const float* __restrict__ w, int C, bf16* __restrict__ ws) {
+  const int n = 96 * 2 * C;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int k = i % (2 * C), row = i / (2 * C);
+    const int t = row / 9, term = (row % 9) / 3, o = row % 3, c = k < C ? k : k - C;
+    float out = 0.0f;
+    if (row < 81 && !(term == 2 && k >= C)) {
+      const float v = w[((size_t)o * 9 + t) * C + c];
+      const float w1 = __bfloat162float(__float2bfloat16_rn(v));
+      const float w2 = __bfloat162float(__float2bfloat16_rn(v - w1));
+      out = term == 0 ? w1 : term == 1 ? w2 : v - w1 - w2;
+    }
+    ws[i] = __float2bfloat16_rn(out);
+  }
+}
+
+cudaError_t split_planes(const float* x, long long P, int C, bf16* y, cudaStream_t st) {
+  if (C % 4 || ((uintptr_t)x & 15) || ((uintptr_t)y & 7)) return cudaErrorInvalidValue;
+  k_split_planes<<<grid_for(P * (C / 4), 256), 256, 0, st>>>(x, P, C, y);
+  return cudaGetLastError();
+}
+cudaError_t split_out_weights(const float* w, int C, bf16* ws, cudaStream_t st) {
+  k_split_out_weights<<<ceil_div(96 * 2 * C, 256), 256, 0, st>>>(w, C, ws);
   return cudaGetLastError();
 }
 

@@ -185,8 +185,16 @@ cudaError_t thin_conv_fwd(const float* x, int N, int H, int W, int C, const floa
 cudaError_t thin_conv_dgrad(const float* dy, int N, int H, int W, int C, const float* w, int CO, float* dx,
                             cudaStream_t st);
 // dw[CO][9][C] = sum_m dy[m][o] x[m+tap][c]  (deterministic: per-block partials in scratch, fixed-order sum)
-cudaError_t thin_conv_wgrad(const float* x, const float* dy, int N, int H, int W, int C, int CO, float* dw,
-                            float* scratch, size_t scratch_floats, cudaStream_t st);
+// split = true: x is the two-term bf16 split [m][2C] = [x1 | x2] of the activation (R36), read as x1 + x2
+cudaError_t thin_conv_wgrad(const void* x, const float* dy, int N, int H, int W, int C, int CO, float* dw,
+                            float* scratch, size_t scratch_floats, cudaStream_t st, bool split = false);
+// G's output layer on the tensor cores (R36; tc_outconv.cu): y2[p] = [bf16(x) | bf16(x - bf16(x))]
+// ([P][2C]), and the three-term bf16 split of w[3][9][C] as the B operand [96][2C] (row layout: kernels.cu)
+cudaError_t split_planes(const float* x, long long P, int C, bf16* y2, cudaStream_t st);
+cudaError_t split_out_weights(const float* w, int C, bf16* ws, cudaStream_t st);
+// output-BN apply + ReLU written as the split planes y2 [P][2C] (the fp32 result never stored)
+cudaError_t bn_apply_relu_split(const bf16* x, int N, int H, int W, int C, const float* mean, const float* rstd,
+                                const float* gamma, const float* beta, bf16* y2, cudaStream_t st);
 
 // ---------------- discriminator head + hinge loss (A7, A8), fp32
 template <typename T>

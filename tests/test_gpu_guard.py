@@ -112,3 +112,20 @@ def test_thin_fp32_layer_writes_only_its_outputs(shape):
     for b, t in ((ybuf, y), (dxbuf, dx), (wbuf, dw)):
         _check(b, fill, t.numel())
         assert not bool((t == fill).any())
+
+
+@pytest.mark.parametrize("shape", [(2, 128, 128, 96), (3, 5, 128, 16)])
+def test_out_conv_split_writes_only_its_outputs(shape):
+    """The tensor-core output layer (R36): y [M][3] fp32 written row by row from the 16-column accumulator."""
+    n, h, w, cin = shape
+    x = torch.randn(n, h, w, cin, device=DEV)
+    wt = torch.randn(3, 9, cin, device=DEV)
+    dy = torch.randn(n, h, w, 3, device=DEV)
+    fill = -12345.0
+    ybuf, y = _guarded((n, h, w, 3), torch.float32, fill)
+    wbuf, dw = _guarded((3, 9, cin), torch.float32, fill)
+    api.op_out_conv_split(x, wt, None, y, dy, dw)
+    torch.cuda.synchronize()
+    for b, t in ((ybuf, y), (wbuf, dw)):
+        _check(b, fill, t.numel())
+        assert not bool((t == fill).any())

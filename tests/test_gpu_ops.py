@@ -202,6 +202,58 @@ def test_thin_conv_f32_fwd_dgrad_wgrad(shape):
         assert np.linalg.norm(got.cpu().numpy() - want) <= 1e-5 * np.linalg.norm(want)
 
 
+def _bf16_split(a, terms):
+    """a (float64 holding fp32 values) -> [t1, t2, ...], t_k = bf16(a - t1 - ... - t_{k-1}) (R36)."""
+    out, r = [], np.asarray(a, np.float64)
+    for _ in range(terms):
+        t = torch.from_numpy(r.astype(np.float32)).to(torch.bfloat16).double().numpy()
+        out.append(t)
+        r = r - t
+    return out
+
+
+@pytest.mark.parametrize("shape", [(2, 128, 128, 96), (1, 37, 128, 32), (3, 1, 128, 8), (2, 64, 128, 16), (1, 65, 128, 128)])
+def test_out_conv_split_tensor_core_fwd_wgrad(shape):
+    """G's fp32 output layer as the BF16 engine runs it (R36): the tensor-core conv of the bf16 splits.
+    (i) Against the split's own definition, (x1 + x2)(w1 + w2) + x1 w3 in fp64: only the fp32 accumulation
+    differs (4e-6: the tensor core's fp32 sums measured 1.4e-6 at the bench shape; leaving out the x1 w3
+    term alone would add ~2^-17 = 7.6e-6, an x2 term ~2^-9).  (ii) Against the plain fp64 conv of the fp32 x and w: the split drops x2 w3 and
+    leaves |x - x1 - x2| <= 2^-18 |x| per element, so the bar is the thin fp32 kernels' own 1e-5.  The weight
+    gradient reads the same split planes (x = x1 + x2), also at 1e-5.  Shapes (W = 128, one image row per
+    tile): the bench layer, a ragged last 32-row strip (H = 37, 65), a one-row image, C = 8 / 16 (one partial
+    K chunk) and C = 128 (four chunks)."""
+    n, h, w, cin = shape
+    rng = np.random.default_rng(h * w + cin + n)
+    x = np.maximum(rng.standard_normal((n, h, w, cin)), 0).astype(np.float32)   # a ReLU output, as in G
+    wt = (rng.standard_normal((3, 9, cin)) * 0.05).astype(np.float32)
+    b = rng.standard_normal(3).astype(np.float32)
+    dy = rng.standard_normal((n, h, w, 3)).astype(np.float32)
+    xd, wd, bd, dyd = (torch.from_numpy(a).to(DEV) for a in (x, wt, b, dy))
+    y = torch.full((n, h, w, 3), float("nan"), dtype=torch.float32, device=DEV)
+    dw = torch.full((3, 9, cin), float("nan"), dtype=torch.float32, device=DEV)
+    api.op_out_conv_split(xd, wd, bd, y, dyd, dw)
+    torch.cuda.synchronize()
+    x1, x2 = _bf16_split(x, 2)
+    w1, w2, w3 = _bf16_split(wt, 3)
+
+    def conv(xa, wa, bias=None):
+        xt = torch.from_numpy(xa).permute(0, 3, 1, 2)
+        wv = torch.from_numpy(wa).reshape(3, 3, 3, cin).permute(0, 3, 1, 2)
+        return ops.conv2d(xt, wv, bias).permute(0, 2, 3, 1).numpy()
+
+    bt = torch.from_numpy(b).double()
+    want_split = conv(x1 + x2, w1 + w2, bt) + conv(x1, w3)
+    want = conv(x.astype(np.float64), wt.astype(np.float64), bt)
+    got = y.cpu().numpy()
+    assert np.linalg.norm(got - want_split) <= 4e-6 * np.linalg.norm(want_split)
+    assert np.linalg.norm(got - want) <= 1e-5 * np.linalg.norm(want)
+    xt = torch.from_numpy(x).double().permute(0, 3, 1, 2)
+    wv = torch.zeros(3, cin, 3, 3, dtype=torch.float64, requires_grad=True)
+    (gw,) = torch.autograd.grad((ops.conv2d(xt, wv, None) * torch.from_numpy(dy).double().permute(0, 3, 1, 2)).sum(), wv)
+    wantw = gw.permute(0, 2, 3, 1).reshape(3, 9, cin).numpy()
+    assert np.linalg.norm(dw.cpu().numpy() - wantw) <= 1e-5 * np.linalg.norm(wantw)
+
+
 UP2_SHAPES = [  # n, h, w, cin, cout  (low-resolution input; output 2h x 2w)
     (2, 4, 4, 64, 128),          # G block 0 geometry: 16-pixel images, 8 images per tile
     (1, 8, 8, 96, 96),

@@ -1,5 +1,5 @@
 """Times G's fp32 output-layer kernels (k_thin_fwd / _dgrad / _wgrad) at the bench shape through the op
-hooks: x [256,128,128,96] fp32, C_out = 3.  python tools/bench_thin.py [reps]"""
+hooks: x [256,128,128,96] fp32, C_out = 3; also the tensor-core split path (R36).  python tools/bench_thin.py [reps]"""
 import os
 import sys
 
@@ -23,7 +23,10 @@ def main():
     fl = 2.0 * n * h * w * 27 * c
     for name, fn in (("fwd", lambda: api.op_conv_fwd(api.F32, x, wt, b, 3, 3, y)),
                      ("dgrad", lambda: api.op_conv_dgrad(api.F32, dy, wt, c, 3, dx)),
-                     ("wgrad", lambda: api.op_conv_wgrad(api.F32, x, dy, 3, 3, dw, db=db))):
+                     ("wgrad", lambda: api.op_conv_wgrad(api.F32, x, dy, 3, 3, dw, db=db)),
+                     # R36 tensor-core path; the op also splits x (one fp32 read + bf16x2 write of x)
+                     ("split fwd (+split)", lambda: api.op_out_conv_split(x, wt, b, y)),
+                     ("split fwd+wgrad (+split)", lambda: api.op_out_conv_split(x, wt, b, y, dy, dw))):
         for _ in range(3):
             fn()
         torch.cuda.synchronize()

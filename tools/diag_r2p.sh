@@ -1,0 +1,11 @@
+cd $GRAFT_REPO_ROOT
+timeout 600 python -m pytest tests/test_gpu_ops.py -q -k "out_conv_split or thin" > gpurun_out/d17_ops.log 2>&1; tail -2 gpurun_out/d17_ops.log
+timeout 300 python -m pytest tests/test_gpu_guard.py -q -k "out_conv or thin" >> gpurun_out/d17_ops.log 2>&1; tail -1 gpurun_out/d17_ops.log
+timeout 300 python tools/bench_thin.py 10 > gpurun_out/d17_thin.log 2>&1; cat gpurun_out/d17_thin.log
+timeout 1500 python -m pytest tests/test_gpu_step.py -q > gpurun_out/d17_step.log 2>&1; tail -3 gpurun_out/d17_step.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/d17_smoke.log 2>&1; echo smoke rc=$?; tail -2 gpurun_out/d17_smoke.log
+for v in 0 1 0 1; do
+  PARAGAN_THIN_TC=$v timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/d17_bench_$v.log 2>&1
+  python -c "import json;d=json.loads(open('gpurun_out/d17_bench_$v.log').read().strip().splitlines()[-1]);print('thin_tc=$v', round(d['value'],1), d['roofline']['other_kernels_ms_per_step'], d['losses']['d'], d['losses']['g'])" >> gpurun_out/d17_summary.txt
+done
+cat gpurun_out/d17_summary.txt
