@@ -367,13 +367,17 @@ paragan_status paragan_op_conv_dgrad(paragan_dtype dt, const void* dy, int32_t n
  * (OHWI) into three bf16 terms w1 = bf16(w), w2 = bf16(w - w1), w3 = bf16(w - w1 - w2), and
  *   y[p][o] = bias[o] + sum_{tap,c} (x1 + x2)[p + tap][c] (w1 + w2)[o][tap][c] + x1[p + tap][c] w3[o][tap][c]
  * with fp32 tensor-core accumulation (y fp32 [N,H,W,3]; bias may be NULL).  When dy (fp32 [N,H,W,3]) and
- * dw (fp32 [3][9][Cin]) are both non-NULL, also dw[o][tap][c] = sum_p dy[p][o] (x1 + x2)[p + tap][c] — the
- * engine's weight gradient, read from the same split planes.  3x3 pad 1; Cin % 8 == 0, Cin <= 128, W a power
- * of two with the 128-pixel tiling of op_conv_fwd; device pointers, 16-byte aligned; the split planes are a
- * stream-ordered temporary.  PARAGAN_ERR_INVALID_ARG on a shape or alignment violation. */
+ * dw (fp32 [3][9][Cin]) are both non-NULL, also the backward pass the engine runs (one kernel): with
+ * dy1 = bf16(dy), dy2 = bf16(dy - dy1),
+ *   dw[o][tap][c] = sum_p (dy1 + dy2)[p][o] (x1 + x2)[p + tap][c]                      (written)
+ *   dx[p][c]      = sum_{o,tap} (dy1 + dy2)[p - tap][o] w1[o][tap][c] + dy1[p - tap][o] (w2 + w3)[o][tap][c]
+ * (dx fp32 [N,H,W,Cin], optional; requires dw).  3x3 pad 1;
+ * W = 128 (one image row per tensor-core tile), Cin % 8 == 0, Cin <= 128; device pointers, 16-byte
+ * aligned; the split planes and partials are stream-ordered temporaries.  PARAGAN_ERR_INVALID_ARG on a
+ * shape or alignment violation. */
 paragan_status paragan_op_out_conv_split(const float* x, int32_t n, int32_t h, int32_t w, int32_t cin,
                                          const float* wgt, const float* bias, float* y, const float* dy, float* dw,
-                                         void* stream);
+                                         float* dx, void* stream);
 
 /* Fused attention core of the non-local block (BigGAN's self-attention,
  * reading R8 — beta = softmax_rows(theta^T phi) without a 1/sqrt(d) scale, o = beta g).

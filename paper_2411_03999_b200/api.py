@@ -129,7 +129,8 @@ SYMBOLS = {
     "paragan_op_conv_wgrad": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                         C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
     "paragan_op_out_conv_split": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
-                                            C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+                                            C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                            C.c_void_p]),
     "paragan_op_conv_up2_fwd": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
                                           C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
     "paragan_op_conv_up2_dgrad": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
@@ -259,12 +260,13 @@ def op_conv_wgrad(dtype, x, dy, cout, ksz, dw, stream=None, db=None):
                                                                 _ptr(dw), _ptr(db), _stream(stream)))
 
 
-def op_out_conv_split(x, wgt, bias, y, dy=None, dw=None, stream=None):
+def op_out_conv_split(x, wgt, bias, y, dy=None, dw=None, dx=None, stream=None):
     """G's output layer as the BF16 engine runs it (R36): x fp32 [n,h,w,cin], wgt fp32 [3,9,cin] -> y fp32
-    [n,h,w,3] through the bf16 splits on the tensor cores; with dy/dw also the weight gradient."""
+    [n,h,w,3] through the bf16 splits on the tensor cores; with dy/dw (and dx) also the backward."""
     n, h, w, cin = x.shape
     _check("paragan_op_out_conv_split", lib().paragan_op_out_conv_split(_ptr(x), n, h, w, cin, _ptr(wgt), _ptr(bias),
-                                                                        _ptr(y), _ptr(dy), _ptr(dw), _stream(stream)))
+                                                                        _ptr(y), _ptr(dy), _ptr(dw), _ptr(dx),
+                                                                        _stream(stream)))
 
 
 def op_conv_up2_fwd(x, wgt, bias, cout, y, stream=None):

@@ -260,24 +260,31 @@ paragan_status paragan_op_conv_fwd_ex(const void* x, int32_t n, int32_t h, int32
 
 paragan_status paragan_op_out_conv_split(const float* x, int32_t n, int32_t h, int32_t w, int32_t cin,
                                          const float* wgt, const float* bias, float* y, const float* dy, float* dw,
-                                         void* stream) {
+                                         float* dx, void* stream) {
   if (!x || !wgt || !y || n < 1 || h < 1 || w < 1 || !out_conv_tc_ok(h, w, cin) || !aligned16(x) ||
-      !aligned16(wgt) || (dw && !dy))
+      !aligned16(wgt) || (dw && !dy) || (dx && (!dw || !aligned16(dx))))
     return PARAGAN_ERR_INVALID_ARG;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const long long P = (long long)n * h * w;
   const size_t plane_bytes = (size_t)P * 2 * cin * sizeof(uint16_t), ws_bytes = (size_t)96 * 2 * cin * 2;
-  const size_t scratch_n = dw ? (size_t)4 * 148 * 27 * cin : 0;
+  const int c16 = (cin + 15) / 16 * 16;
+  const size_t wd_bytes = (size_t)c16 * 128 * 2, dx_bytes = dx ? 0 : (size_t)P * cin * 4;
+  const size_t scratch_n = out_conv_bwd_scratch_floats(cin);
   char* tmp = nullptr;
-  if (cudaMallocAsync(reinterpret_cast<void**>(&tmp), plane_bytes + ws_bytes + scratch_n * 4, st) != cudaSuccess)
+  if (cudaMallocAsync(reinterpret_cast<void**>(&tmp), plane_bytes + ws_bytes + wd_bytes + dx_bytes + scratch_n * 4,
+                      st) != cudaSuccess)
     return PARAGAN_ERR_CUDA;
   bf16* xs = reinterpret_cast<bf16*>(tmp);
   bf16* ws = reinterpret_cast<bf16*>(tmp + plane_bytes);
-  float* scratch = reinterpret_cast<float*>(tmp + plane_bytes + ws_bytes);
+  bf16* wd = reinterpret_cast<bf16*>(tmp + plane_bytes + ws_bytes);
+  float* dxb = dx ? dx : reinterpret_cast<float*>(tmp + plane_bytes + ws_bytes + wd_bytes);
+  float* scratch = reinterpret_cast<float*>(tmp + plane_bytes + ws_bytes + wd_bytes + dx_bytes);
   cudaError_t e = split_planes(x, P, cin, xs, st);
   if (e == cudaSuccess) e = split_out_weights(wgt, cin, ws, st);
   if (e == cudaSuccess) e = out_conv_fwd_tc(xs, n, h, w, cin, ws, bias, y, st);
-  if (e == cudaSuccess && dw) e = thin_conv_wgrad(xs, dy, n, h, w, cin, 3, dw, scratch, scratch_n, st, true);
+  if (e == cudaSuccess && dw) e = split_out_weights_dgrad(wgt, cin, c16, wd, st);
+  if (e == cudaSuccess && dw)
+    e = out_conv_bwd_tc(xs, dy, n, h, w, cin, wd, dxb, dw, scratch, scratch_n, st);
   cudaFreeAsync(tmp, st);
   return cuda_status(e);
 }

@@ -1176,7 +1176,10 @@ class Engine final : public EngineBase {
     // [x1 | x2], the same bytes
     aout_ = A.get<float>((size_t)B * R_ * R_ * cl_);
     thin_tc_ = thin_tc_ && out_conv_tc_ok(R_, R_, cl_);
-    if (thin_tc_) oconv_ws_ = A.get<bf16>((size_t)96 * 2 * cl_);
+    if (thin_tc_) {
+      oconv_ws_ = A.get<bf16>((size_t)96 * 2 * cl_);
+      oconv_wd_ = A.get<bf16>((size_t)round_up(cl_, 16) * 128);
+    }
     omean_ = A.get<float>(cl_);
     orstd_ = A.get<float>(cl_);
     osums_ = A.get<double>(2 * cl_);
@@ -2385,14 +2388,24 @@ class Engine final : public EngineBase {
     const long long M = (long long)B * R_ * R_;
     // tanh' and the fp32 output conv
     CK(tanh_bwd<T>(static_cast<const T*>(dimg_grad_), cpad_, img_, dpre_, M, st_));
-    CK(timed(6, 2.0 * B * R_ * R_ * 27.0 * cl_, [&] {
-      return thin_conv_wgrad(aout_, dpre_, B, R_, R_, cl_, 3, G_.G(oconv_.w), scratch_f_, scratch_floats_, st_,
-                             thin_tc_);
-    }, "thin wgrad"));
-    CK(col_sum<float>(dpre_, M, 3, dpart_, kMaxPartialBlocks, G_.G(oconv_.b), 0, st_));
-    CK(timed(6, 2.0 * B * R_ * R_ * 27.0 * cl_, [&] {
-      return thin_conv_dgrad(dpre_, B, R_, R_, cl_, static_cast<const float*>(oconv_.wp), 3, daout_, st_);
-    }, "thin dgrad"));
+    if (thin_tc_) {   // both gradients in one tensor-core pass over the split activation (R36)
+      CK(timed(6, 2 * 2.0 * B * R_ * R_ * 27.0 * cl_, [&] {
+        PG_CUDA(split_out_weights_dgrad(static_cast<const float*>(oconv_.wp), cl_, round_up(cl_, 16), oconv_wd_,
+                                        st_));
+        return out_conv_bwd_tc(aout_, dpre_, B, R_, R_, cl_, oconv_wd_, daout_, G_.G(oconv_.w), scratch_f_,
+                               scratch_floats_, st_);
+      }, "thin bwd"));
+      launches_ += 2;   // three launches in the timed region above
+      CK(col_sum<float>(dpre_, M, 3, dpart_, kMaxPartialBlocks, G_.G(oconv_.b), 0, st_));
+    } else {
+      CK(timed(6, 2.0 * B * R_ * R_ * 27.0 * cl_, [&] {
+        return thin_conv_wgrad(aout_, dpre_, B, R_, R_, cl_, 3, G_.G(oconv_.w), scratch_f_, scratch_floats_, st_);
+      }, "thin wgrad"));
+      CK(col_sum<float>(dpre_, M, 3, dpart_, kMaxPartialBlocks, G_.G(oconv_.b), 0, st_));
+      CK(timed(6, 2.0 * B * R_ * R_ * 27.0 * cl_, [&] {
+        return thin_conv_dgrad(dpre_, B, R_, R_, cl_, static_cast<const float*>(oconv_.wp), 3, daout_, st_);
+      }, "thin dgrad"));
+    }
     // output BN backward (plain BN, learned gamma/beta)
     int ic = (dimg_idx_ + 1) % 4;
     void* cur = tmp(ic);
@@ -2505,6 +2518,7 @@ class Engine final : public EngineBase {
   bool ready_ = false, poisoned_ = false, planned_ = false, ones_ready_ = false;
   bool thin_tc_ = false;  // G's output layer on the tensor cores via bf16 splits (R36; BF16 mode)
   bf16* oconv_ws_ = nullptr;  // its split weight operand [96][2 cl]
+  bf16* oconv_wd_ = nullptr;  // the dgrad operand [round_up(cl, 16)][128]
   bool subpix_ = false;   // G conv1 as four phase 2x2 convs of the low-resolution input (NEXT-1)
   bool attn_single_ = true;   // single-pass fused attention forward when the score bound allows (R21)
   bool dcgan_ = false;    // SN-DCGAN (config 1) instead of BigGAN

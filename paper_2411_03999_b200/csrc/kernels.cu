@@ -3469,6 +3469,29 @@ __global__ void k_split_out_weights(const float* __restrict__ w, int C, bf16* __
   }
 }
 
+// dgrad operand of the same layer (tc_outconv.cu): wd[c][j], j = blk * 27 + t * 3 + o over the A~ columns
+// [dy1 | dy2 | dy1 | dy1], holds [w1 | w1 | w2 | w3][o][t][c]; j >= 108 and rows c >= C are zero
+__global__ void k_split_out_weights_dgrad(const float* __restrict__ w, int C, int C16, bf16* __restrict__ wd) {
+  const int n = C16 * 128;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int j = i % 128, c = i / 128;
+    float out = 0.0f;
+    if (j < 108 && c < C) {
+      const int blk = j / 27, m = j % 27, t = m / 3, o = m % 3;
+      const float v = w[((size_t)o * 9 + t) * C + c];
+      const float w1 = __bfloat162float(__float2bfloat16_rn(v));
+      const float w2 = __bfloat162float(__float2bfloat16_rn(v - w1));
+      out = blk <= 1 ? w1 : blk == 2 ? w2 : v - w1 - w2;
+    }
+    wd[i] = __float2bfloat16_rn(out);
+  }
+}
+
+cudaError_t split_out_weights_dgrad(const float* w, int C, int C16, bf16* wd, cudaStream_t st) {
+  k_split_out_weights_dgrad<<<ceil_div(C16 * 128, 256), 256, 0, st>>>(w, C, C16, wd);
+  return cudaGetLastError();
+}
+
 cudaError_t split_planes(const float* x, long long P, int C, bf16* y, cudaStream_t st) {
   if (C % 4 || ((uintptr_t)x & 15) || ((uintptr_t)y & 7)) return cudaErrorInvalidValue;
   k_split_planes<<<grid_for(P * (C / 4), 256), 256, 0, st>>>(x, P, C, y);

@@ -192,6 +192,8 @@ cudaError_t thin_conv_wgrad(const void* x, const float* dy, int N, int H, int W,
 // ([P][2C]), and the three-term bf16 split of w[3][9][C] as the B operand [96][2C] (row layout: kernels.cu)
 cudaError_t split_planes(const float* x, long long P, int C, bf16* y2, cudaStream_t st);
 cudaError_t split_out_weights(const float* w, int C, bf16* ws, cudaStream_t st);
+// the dgrad operand [C16][128] over the output-gradient im2col [dy1 | dy2 | dy1 | dy1] (tc_outconv.cu)
+cudaError_t split_out_weights_dgrad(const float* w, int C, int C16, bf16* wd, cudaStream_t st);
 // output-BN apply + ReLU written as the split planes y2 [P][2C] (the fp32 result never stored)
 cudaError_t bn_apply_relu_split(const bf16* x, int N, int H, int W, int C, const float* mean, const float* rstd,
                                 const float* gamma, const float* beta, bf16* y2, cudaStream_t st);

@@ -13,4 +13,12 @@ bool out_conv_tc_ok(int H, int W, int C);
 cudaError_t out_conv_fwd_tc(const void* xs, int N, int H, int W, int C, const void* ws, const float* bias, float* y,
                             cudaStream_t st);
 
+// Both gradients of the same layer in one pass (R36): dx[N][H][W][C] (fp32) = conv^T(dy, w) and
+// dw[3][9][C] (fp32, written) = sum_p dy[p][o] x[p + tap][c], from xs (the split activation above), dy
+// (fp32 [N][H][W][3]) and wd (bf16 [C16][128], split_out_weights_dgrad: the dgrad operand over
+// [dy1 | dy2 | dy1 | dy1]).  scratch >= out_conv_bwd_scratch_floats(C) (per-CTA dW partials).
+size_t out_conv_bwd_scratch_floats(int C);
+cudaError_t out_conv_bwd_tc(const void* xs, const float* dy, int N, int H, int W, int C, const void* wd, float* dx,
+                            float* dw, float* scratch, size_t scratch_floats, cudaStream_t st);
+
 }  // namespace pg

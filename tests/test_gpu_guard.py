@@ -124,8 +124,9 @@ def test_out_conv_split_writes_only_its_outputs(shape):
     fill = -12345.0
     ybuf, y = _guarded((n, h, w, 3), torch.float32, fill)
     wbuf, dw = _guarded((3, 9, cin), torch.float32, fill)
-    api.op_out_conv_split(x, wt, None, y, dy, dw)
+    dxbuf, dx = _guarded((n, h, w, cin), torch.float32, fill)
+    api.op_out_conv_split(x, wt, None, y, dy, dw, dx)
     torch.cuda.synchronize()
-    for b, t in ((ybuf, y), (wbuf, dw)):
+    for b, t in ((ybuf, y), (wbuf, dw), (dxbuf, dx)):
         _check(b, fill, t.numel())
         assert not bool((t == fill).any())

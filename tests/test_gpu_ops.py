@@ -218,8 +218,9 @@ def test_out_conv_split_tensor_core_fwd_wgrad(shape):
     (i) Against the split's own definition, (x1 + x2)(w1 + w2) + x1 w3 in fp64: only the fp32 accumulation
     differs (4e-6: the tensor core's fp32 sums measured 1.4e-6 at the bench shape; leaving out the x1 w3
     term alone would add ~2^-17 = 7.6e-6, an x2 term ~2^-9).  (ii) Against the plain fp64 conv of the fp32 x and w: the split drops x2 w3 and
-    leaves |x - x1 - x2| <= 2^-18 |x| per element, so the bar is the thin fp32 kernels' own 1e-5.  The weight
-    gradient reads the same split planes (x = x1 + x2), also at 1e-5.  Shapes (W = 128, one image row per
+    leaves |x - x1 - x2| <= 2^-18 |x| per element, so the bar is the thin fp32 kernels' own 1e-5.  The
+    backward kernel: dW from (dy1 + dy2)(x1 + x2) and dX from (dy1 + dy2) w1 + dy1 (w2 + w3), each against its
+    split definition (4e-6) and the plain fp64 gradient (1e-5).  Shapes (W = 128, one image row per
     tile): the bench layer, a ragged last 32-row strip (H = 37, 65), a one-row image, C = 8 / 16 (one partial
     K chunk) and C = 128 (four chunks)."""
     n, h, w, cin = shape
@@ -231,7 +232,8 @@ def test_out_conv_split_tensor_core_fwd_wgrad(shape):
     xd, wd, bd, dyd = (torch.from_numpy(a).to(DEV) for a in (x, wt, b, dy))
     y = torch.full((n, h, w, 3), float("nan"), dtype=torch.float32, device=DEV)
     dw = torch.full((3, 9, cin), float("nan"), dtype=torch.float32, device=DEV)
-    api.op_out_conv_split(xd, wd, bd, y, dyd, dw)
+    dx = torch.full((n, h, w, cin), float("nan"), dtype=torch.float32, device=DEV)
+    api.op_out_conv_split(xd, wd, bd, y, dyd, dw, dx)
     torch.cuda.synchronize()
     x1, x2 = _bf16_split(x, 2)
     w1, w2, w3 = _bf16_split(wt, 3)
@@ -247,11 +249,23 @@ def test_out_conv_split_tensor_core_fwd_wgrad(shape):
     got = y.cpu().numpy()
     assert np.linalg.norm(got - want_split) <= 4e-6 * np.linalg.norm(want_split)
     assert np.linalg.norm(got - want) <= 1e-5 * np.linalg.norm(want)
-    xt = torch.from_numpy(x).double().permute(0, 3, 1, 2)
-    wv = torch.zeros(3, cin, 3, 3, dtype=torch.float64, requires_grad=True)
-    (gw,) = torch.autograd.grad((ops.conv2d(xt, wv, None) * torch.from_numpy(dy).double().permute(0, 3, 1, 2)).sum(), wv)
-    wantw = gw.permute(0, 2, 3, 1).reshape(3, 9, cin).numpy()
-    assert np.linalg.norm(dw.cpu().numpy() - wantw) <= 1e-5 * np.linalg.norm(wantw)
+    def grads(xa, wa, dya):
+        xt = torch.from_numpy(np.asarray(xa, np.float64)).permute(0, 3, 1, 2).requires_grad_(True)
+        wv = torch.from_numpy(np.asarray(wa, np.float64)).reshape(3, 3, 3, cin).permute(0, 3, 1, 2).contiguous()
+        wv.requires_grad_(True)
+        gx, gw = torch.autograd.grad((ops.conv2d(xt, wv, None) * torch.from_numpy(dya).permute(0, 3, 1, 2)).sum(),
+                                     (xt, wv))
+        return gx.permute(0, 2, 3, 1).numpy(), gw.permute(0, 2, 3, 1).reshape(3, 9, cin).numpy()
+
+    dy1, dy2 = _bf16_split(dy, 2)
+    _, want_split_w = grads(x1 + x2, wt, dy1 + dy2)
+    want_split_x = grads(x, w1, dy1 + dy2)[0] + grads(x, w2 + w3, dy1)[0]
+    want_x, want_w = grads(x, wt, dy.astype(np.float64))
+    gw_, gx_ = dw.cpu().numpy(), dx.cpu().numpy()
+    assert np.linalg.norm(gw_ - want_split_w) <= 4e-6 * np.linalg.norm(want_split_w)
+    assert np.linalg.norm(gw_ - want_w) <= 1e-5 * np.linalg.norm(want_w)
+    assert np.linalg.norm(gx_ - want_split_x) <= 4e-6 * np.linalg.norm(want_split_x)
+    assert np.linalg.norm(gx_ - want_x) <= 1e-5 * np.linalg.norm(want_x)
 
 
 UP2_SHAPES = [  # n, h, w, cin, cout  (low-resolution input; output 2h x 2w)

@@ -26,7 +26,7 @@ def main():
                      ("wgrad", lambda: api.op_conv_wgrad(api.F32, x, dy, 3, 3, dw, db=db)),
                      # R36 tensor-core path; the op also splits x (one fp32 read + bf16x2 write of x)
                      ("split fwd (+split)", lambda: api.op_out_conv_split(x, wt, b, y)),
-                     ("split fwd+wgrad (+split)", lambda: api.op_out_conv_split(x, wt, b, y, dy, dw))):
+                     ("split fwd+bwd (+split)", lambda: api.op_out_conv_split(x, wt, b, y, dy, dw, dx))):
         for _ in range(3):
             fn()
         torch.cuda.synchronize()

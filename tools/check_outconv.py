@@ -22,14 +22,26 @@ def main():
         y1 = torch.full((n, h, w, 3), float("nan"), device="cuda")
         dw0 = torch.empty(3, 9, c, device="cuda")
         dw1 = torch.full((3, 9, c), float("nan"), device="cuda")
+        dx0 = torch.empty(n, h, w, c, device="cuda")
+        dx1 = torch.full((n, h, w, c), float("nan"), device="cuda")
         api.op_conv_fwd(api.F32, x, wt, b, 3, 3, y0)
         api.op_conv_wgrad(api.F32, x, dy, 3, 3, dw0)
-        api.op_out_conv_split(x, wt, b, y1, dy, dw1)
+        api.op_conv_dgrad(api.F32, dy, wt, c, 3, dx0)
+        api.op_out_conv_split(x, wt, b, y1, dy, dw1, dx1)
         torch.cuda.synchronize()
+        # fp64 weight gradient (shifted products): which of the two fp32 paths is closer
+        xp = torch.nn.functional.pad(x.double(), (0, 0, 1, 1, 1, 1))
+        dwx = torch.empty(3, 9, c, dtype=torch.float64, device="cuda")
+        for t in range(9):
+            r, s_ = divmod(t, 3)
+            dwx[:, t] = torch.einsum("nhwo,nhwc->oc", dy.double(), xp[:, r:r + h, s_:s_ + w])
+        rel = lambda a: float((a.double() - dwx).norm() / dwx.norm())
+        print(f"n={n}: dw vs fp64: simt {rel(dw0):.3e} tensor-core {rel(dw1):.3e}", flush=True)
         d = (y1 - y0).abs()
         bad = (d > 1e-3 * (1 + y0.abs())) | torch.isnan(y1)
         print(f"n={n}: y rel {float((y1 - y0).norm() / y0.norm()):.3e} max {float(d.max()):.3e} bad {int(bad.sum())}"
-              f" dw rel {float((dw1 - dw0).norm() / dw0.norm()):.3e}", flush=True)
+              f" dw rel {float((dw1 - dw0).norm() / dw0.norm()):.3e} dx rel {float((dx1 - dx0).norm() / dx0.norm()):.3e}"
+              f" dx nan {int(torch.isnan(dx1).sum())}", flush=True)
         if int(bad.sum()):
             idx = bad.nonzero()[:8].tolist()
             print("  first bad (n,h,w,o):", idx)
