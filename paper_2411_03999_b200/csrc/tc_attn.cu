@@ -24,6 +24,8 @@
 // both K-major (P^T dO, dS^T theta) and MN-major (dS phi).
 #include "tc_attn.h"
 
+#include <cstdlib>
+
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
@@ -38,14 +40,15 @@ constexpr int kT = 128;                 // query rows per tile = keys per chunk
 constexpr uint32_t kAtom = 16384;       // 128 rows x 128 B, one SW128 operand atom
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kSpan = 16.0f;          // single-pass forward when every row's score bound is within e^16 of chunk 0's max
-constexpr int kFwdKStages = 3, kFwdVStages = 2;
+constexpr int kFwdKStages = 3, kFwdVMax = 4;   // V ring: as many stages (2..4) as fit
 constexpr int kFwdThreads = 320;        // w0 TMA, w1 MMA, w2-9 softmax / epilogue
 constexpr int kSoftThreads = 256;
 constexpr int kBwdThreads = 320;        // w0 TMA, w1 MMA, w2-9 softmax / epilogue
 
+// the dynamic shared-memory base rounded up to 1024 bytes by pointer arithmetic on the shared array itself, so
+// the compiler keeps the shared address space (LDS/STS, not generic LD/ST) for every access derived from it
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
-  uintptr_t a = reinterpret_cast<uintptr_t>(p);
-  return reinterpret_cast<uint8_t*>((a + 1023) & ~uintptr_t(1023));
+  return p + ((1024u - (tc::smem_u32(p) & 1023u)) & 1023u);
 }
 
 __device__ __forceinline__ uint32_t pack2(float a, float b) {
@@ -70,30 +73,30 @@ __device__ __forceinline__ uint64_t mndesc(const void* p) {  // MN-major operand
 // ===========================================================================
 __global__ void __launch_bounds__(kFwdThreads, 1)
     k_attn_fwd(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-               const __grid_constant__ CUtensorMap tmV, const TcAttnArgs a) {
+               const __grid_constant__ CUtensorMap tmV, const TcAttnArgs a, const int nvs) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   const int C2 = a.C2;
   const uint32_t v_bytes = 2u * C2 * 128;       // two boxes [C2][64 keys]
-  uint8_t* sQ = smem;
-  uint8_t* sK = sQ + kAtom;
+  uint8_t* sQ = smem;                           // 2 buffers: the next tile's theta loads during this tile
+  uint8_t* sK = sQ + 2 * kAtom;
   uint8_t* sP = sK + kFwdKStages * kAtom;       // 2 buffers x 2 atoms
   uint8_t* sV = sP + 4 * kAtom;
-  float* red = reinterpret_cast<float*>(sV + kFwdVStages * v_bytes);   // [2 tiles][2 halves][128] row max
+  float* red = reinterpret_cast<float*>(sV + nvs * v_bytes);   // [2 tiles][2 halves][128] row max
   uint64_t* bars = reinterpret_cast<uint64_t*>(red + 2 * 2 * kT);
-  uint64_t* qfull = bars;
-  uint64_t* qempty = bars + 1;
-  uint64_t* kfull = bars + 2;
+  uint64_t* qfull = bars;        // [2]
+  uint64_t* qempty = bars + 2;   // [2]
+  uint64_t* kfull = bars + 4;
   uint64_t* kempty = kfull + kFwdKStages;
   uint64_t* vfull = kempty + kFwdKStages;
-  uint64_t* vempty = vfull + kFwdVStages;
-  uint64_t* sfull = vempty + kFwdVStages;
+  uint64_t* vempty = vfull + kFwdVMax;
+  uint64_t* sfull = vempty + kFwdVMax;
   uint64_t* sempty = sfull + 2;
   uint64_t* pfull = sempty + 2;
   uint64_t* pempty = pfull + 2;
-  uint64_t* ofull = pempty + 2;
-  uint64_t* oempty = ofull + 1;
-  uint64_t* decbar = oempty + 1;                                    // per tile: single- or two-pass decided
+  uint64_t* ofull = pempty + 2;   // [2] O double-buffered in TMEM: a tile's epilogue runs during the next tile
+  uint64_t* oempty = ofull + 2;   // [2]
+  uint64_t* decbar = oempty + 2;                                    // per tile: single- or two-pass decided
   uint32_t* dec = reinterpret_cast<uint32_t*>(decbar + 1);
   uint32_t* tmem_slot = dec + 1;
 
@@ -102,13 +105,15 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     tc::tma_prefetch(&tmQ);
     tc::tma_prefetch(&tmK);
     tc::tma_prefetch(&tmV);
-    tc::mbar_init(qfull, 1);
-    tc::mbar_init(qempty, 1);
+    for (int s = 0; s < 2; ++s) {
+      tc::mbar_init(&qfull[s], 1);
+      tc::mbar_init(&qempty[s], 1);
+    }
     for (int s = 0; s < kFwdKStages; ++s) {
       tc::mbar_init(&kfull[s], 1);
       tc::mbar_init(&kempty[s], 1);
     }
-    for (int s = 0; s < kFwdVStages; ++s) {
+    for (int s = 0; s < nvs; ++s) {
       tc::mbar_init(&vfull[s], 1);
       tc::mbar_init(&vempty[s], 1);
     }
@@ -118,8 +123,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       tc::mbar_init(&pfull[s], kSoftThreads);
       tc::mbar_init(&pempty[s], 1);
     }
-    tc::mbar_init(ofull, 1);
-    tc::mbar_init(oempty, kSoftThreads);
+    for (int s = 0; s < 2; ++s) {
+      tc::mbar_init(&ofull[s], 1);
+      tc::mbar_init(&oempty[s], kSoftThreads);
+    }
     tc::mbar_init(decbar, 1);
     tc::fence_barrier_init();
   }
@@ -127,7 +134,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
-  const uint32_t tmem = *tmem_slot;   // S buffers at columns 0 / 128, O at 256
+  const uint32_t tmem = *tmem_slot;   // S buffers at columns 0 / 128, O buffers at 256 / 256 + C2
 
   const int tiles_per_img = a.HW / kT;
   const int num_tiles = a.n * tiles_per_img;
@@ -140,9 +147,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
         const int b = tile / tiles_per_img;
         const int q0 = (tile - b * tiles_per_img) * kT;
-        tc::mbar_wait(qempty, (it & 1) ^ 1);
-        tc::mbar_expect_tx(qfull, kAtom);
-        tc::tma_load_3d(sQ, &tmQ, qfull, 0, q0, b);
+        const int qb = it & 1;
+        tc::mbar_wait(&qempty[qb], ((it >> 1) & 1) ^ 1);
+        tc::mbar_expect_tx(&qfull[qb], kAtom);
+        tc::tma_load_3d(sQ + qb * kAtom, &tmQ, &qfull[qb], 0, q0, b);
         auto load_k = [&](int c) {
           tc::mbar_wait(&kempty[ks], kph ^ 1);
           tc::mbar_expect_tx(&kfull[ks], kAtom);
@@ -155,22 +163,25 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           uint8_t* dv = sV + vs * v_bytes;
           tc::tma_load_3d(dv, &tmV, &vfull[vs], c * kT, 0, b);
           tc::tma_load_3d(dv + C2 * 128, &tmV, &vfull[vs], c * kT + 64, 0, b);
-          if (++vs == kFwdVStages) { vs = 0; vph ^= 1; }
+          if (++vs == nvs) { vs = 0; vph ^= 1; }
         };
-        // chunks 0 and 1 come first in both schedules; the rest depends on the tile's decision
+        // K(0), K(1) and V(0), V(1) come first in both schedules (the V ring is consumed in chunk order by
+        // either); the rest depends on the tile's decision
         load_k(0);
         if (NC > 1) load_k(1);
+        const int vpre = NC < 2 ? NC : 2;
+        for (int c = 0; c < vpre; ++c) load_v(c);
         tc::mbar_wait(decbar, it & 1);
         if (*reinterpret_cast<volatile uint32_t*>(dec)) {   // single pass: V(c), then K(c + 2)
           for (int c = 0; c < NC; ++c) {
-            load_v(c);
+            if (c >= vpre) load_v(c);
             if (c + 2 < NC) load_k(c + 2);
           }
         } else {                                            // two passes: the rest of pass 1, then pass 2
           for (int c = 2; c < NC; ++c) load_k(c);
           for (int c = 0; c < NC; ++c) {
             load_k(c);
-            load_v(c);
+            if (c >= vpre) load_v(c);
           }
         }
       }
@@ -184,6 +195,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       int ks = 0, vs = 0, it = 0;
       uint32_t kph = 0, vph = 0;
       uint32_t su = 0, pc = 0;   // running S-buffer use / P-buffer use counters
+      int qb = 0;                // theta buffer of the current tile
       auto issue_s = [&](bool last) {
         const int sb = su & 1;
         tc::mbar_wait(&sempty[sb], ((su >> 1) & 1) ^ 1);
@@ -191,17 +203,18 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         tc::tc_fence_after();
         if (issuer) {
           for (int k = 0; k < ksteps; ++k)
-            tc::mma_bf16(tmem + sb * kT, kdesc(sQ + k * 32), kdesc(sK + ks * kAtom + k * 32), idS, k > 0);
+            tc::mma_bf16(tmem + sb * kT, kdesc(sQ + qb * kAtom + k * 32), kdesc(sK + ks * kAtom + k * 32), idS, k > 0);
           tc::mma_commit(&kempty[ks]);
           tc::mma_commit(&sfull[sb]);
-          if (last) tc::mma_commit(qempty);
+          if (last) tc::mma_commit(&qempty[qb]);
         }
         __syncwarp();
         if (++ks == kFwdKStages) { ks = 0; kph ^= 1; }
         ++su;
       };
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
-        tc::mbar_wait(qfull, it & 1);
+        qb = it & 1;
+        tc::mbar_wait(&qfull[qb], (it >> 1) & 1);
         tc::tc_fence_after();
         issue_s(false);                                     // chunk 0 (its max decides the schedule)
         tc::mbar_wait(decbar, it & 1);
@@ -210,7 +223,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           for (int u = 1; u < NC; ++u) issue_s(false);      // rest of pass 1
           issue_s(NC == 1);                                 // pass 2 starts again at chunk 0
         }
-        tc::mbar_wait(oempty, (it & 1) ^ 1);   // the previous tile's O has been read out
+        const int ob = it & 1;
+        tc::mbar_wait(&oempty[ob], ((it >> 1) & 1) ^ 1);   // the O buffer of two tiles ago has been read out
         for (int c = 0; c < NC; ++c) {
           if (c + 1 < NC) issue_s(c + 2 == NC);
           const int pb = pc & 1;
@@ -222,16 +236,16 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           if (issuer) {
 #pragma unroll
             for (int k = 0; k < 8; ++k)
-              tc::mma_bf16(tmem + 256, kdesc(p + (k >> 2) * kAtom + (k & 3) * 32),
+              tc::mma_bf16(tmem + 256 + ob * C2, kdesc(p + (k >> 2) * kAtom + (k & 3) * 32),
                            kdesc(v + (k >> 2) * C2 * 128 + (k & 3) * 32), idO, (c | k) != 0);
             tc::mma_commit(&pempty[pb]);
             tc::mma_commit(&vempty[vs]);
           }
           __syncwarp();
-          if (++vs == kFwdVStages) { vs = 0; vph ^= 1; }
+          if (++vs == nvs) { vs = 0; vph ^= 1; }
           ++pc;
         }
-        if (issuer) tc::mma_commit(ofull);
+        if (issuer) tc::mma_commit(&ofull[ob]);
         __syncwarp();
       }
     }
@@ -242,6 +256,47 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     const int row = qd * 32 + lane;
     const uint32_t lrow = tmem + ((uint32_t)(qd * 32) << 16);
     uint32_t su = 0, pc = 0;
+    // epilogue of a finished tile, deferred into the next tile (after its chunk 0's P~ is handed to the MMA
+    // warp), so the wait for the tile's last P~ g MMA and the O stores overlap the next tile's MMAs
+    struct Pending {
+      int valid, ob, ob2ph;
+      long long grow;
+      float m, l;
+    } pend{0, 0, 0, 0, 0.0f, 0.0f};
+    auto epilogue = [&]() {
+      if (!pend.valid) return;
+      pend.valid = 0;
+      const int ob = pend.ob;
+      const float inv_l = 1.0f / pend.l;
+      tc::mbar_wait(&ofull[ob], pend.ob2ph);
+      tc::tc_fence_after();
+      bf16* op = static_cast<bf16*>(a.o) + pend.grow * C2;
+      float* op32 = a.o32 ? a.o32 + pend.grow * C2 : nullptr;
+#pragma unroll 1
+      for (int cb = h * 32; cb < C2; cb += 64) {
+        float v[32];
+        tc::tmem_ld32(lrow + 256 + ob * C2 + cb, v);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] *= inv_l;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (cb + j * 8 < C2) {
+            *reinterpret_cast<uint4*>(op + cb + j * 8) =
+                make_uint4(pack2(v[j * 8], v[j * 8 + 1]), pack2(v[j * 8 + 2], v[j * 8 + 3]),
+                           pack2(v[j * 8 + 4], v[j * 8 + 5]), pack2(v[j * 8 + 6], v[j * 8 + 7]));
+            if (op32) {
+              *reinterpret_cast<float4*>(op32 + cb + j * 8) =
+                  make_float4(v[j * 8], v[j * 8 + 1], v[j * 8 + 2], v[j * 8 + 3]);
+              *reinterpret_cast<float4*>(op32 + cb + j * 8 + 4) =
+                  make_float4(v[j * 8 + 4], v[j * 8 + 5], v[j * 8 + 6], v[j * 8 + 7]);
+            }
+          }
+        }
+      }
+      tc::tc_fence_before();
+      tc::mbar_arrive(&oempty[ob]);
+      if (h == 0) a.lse[pend.grow] = pend.m + logf(pend.l);
+    };
     int it = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
       const int b = tile / tiles_per_img;
@@ -271,8 +326,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       m = fmaxf(rb[row], rb[kT + row]);
       uint32_t ok = 0;
       if (a.phimax && NC > 1) {
-        tc::mbar_wait(qfull, it & 1);   // theta's tile (already landed: the chunk-0 MMA read it)
-        const uint8_t* qrow = sQ + row * 128;
+        tc::mbar_wait(&qfull[it & 1], (it >> 1) & 1);   // theta's tile (already landed: the chunk-0 MMA read it)
+        const uint8_t* qrow = sQ + (it & 1) * kAtom + row * 128;
         float t2 = 0.0f;
         for (int c = 0; c < a.Cq / 8; ++c) {
           const uint4 u4 = *reinterpret_cast<const uint4*>(qrow + ((c ^ (row & 7)) << 4));
@@ -346,6 +401,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                                                 pack2(w[j * 8 + 4], w[j * 8 + 5]), pack2(w[j * 8 + 6], w[j * 8 + 7])));
         tc::fence_async_smem();
         tc::mbar_arrive(&pfull[pb]);
+        if (c == 0) epilogue();   // the previous tile's
       }
       // combine the two halves' sums
       float* lb = rb + 0;   // reuse: max already consumed by both halves after this barrier
@@ -353,38 +409,15 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       lb[h * kT + row] = l;
       tc::named_bar(1, kSoftThreads);
       l = lb[row] + lb[kT + row];
-      const float inv_l = 1.0f / l;
-      // epilogue: O = (P~ g) / l -> bf16 (+ fp32); lse = m + log l
-      tc::mbar_wait(ofull, it & 1);
-      tc::tc_fence_after();
-      const long long grow = (long long)b * a.HW + q0 + row;
-      bf16* op = static_cast<bf16*>(a.o) + grow * C2;
-      float* op32 = a.o32 ? a.o32 + grow * C2 : nullptr;
-#pragma unroll 1
-      for (int cb = h * 32; cb < C2; cb += 64) {
-        float v[32];
-        tc::tmem_ld32(lrow + 256 + cb, v);
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] *= inv_l;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          if (cb + j * 8 < C2) {
-            *reinterpret_cast<uint4*>(op + cb + j * 8) =
-                make_uint4(pack2(v[j * 8], v[j * 8 + 1]), pack2(v[j * 8 + 2], v[j * 8 + 3]),
-                           pack2(v[j * 8 + 4], v[j * 8 + 5]), pack2(v[j * 8 + 6], v[j * 8 + 7]));
-            if (op32) {
-              *reinterpret_cast<float4*>(op32 + cb + j * 8) =
-                  make_float4(v[j * 8], v[j * 8 + 1], v[j * 8 + 2], v[j * 8 + 3]);
-              *reinterpret_cast<float4*>(op32 + cb + j * 8 + 4) =
-                  make_float4(v[j * 8 + 4], v[j * 8 + 5], v[j * 8 + 6], v[j * 8 + 7]);
-            }
-          }
-        }
-      }
-      tc::tc_fence_before();
-      tc::mbar_arrive(oempty);
-      if (h == 0) a.lse[grow] = m + logf(l);
+      // epilogue (O = (P~ g) / l -> bf16 (+ fp32); lse = m + log l) deferred into the next tile
+      pend.valid = 1;
+      pend.ob = it & 1;
+      pend.ob2ph = (it >> 1) & 1;
+      pend.grow = (long long)b * a.HW + q0 + row;
+      pend.m = m;
+      pend.l = l;
     }
+    epilogue();   // the last tile's
   }
   tc::tc_fence_before();
   __syncthreads();
@@ -659,10 +692,16 @@ cudaError_t map3(CUtensorMap* m, const void* base, long long d0, long long d1, l
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-size_t fwd_smem(int C2) {
-  return 1024 + (1 + kFwdKStages + 4) * kAtom + kFwdVStages * 2u * C2 * 128 + 4 * kT * sizeof(float) + 256;
-}
 constexpr size_t kSmemMax = 232448;   // 227 KB opt-in per CTA
+size_t fwd_smem(int C2, int nvs) {
+  return 1024 + (2 + kFwdKStages + 4) * kAtom + nvs * 2u * C2 * 128 + 4 * kT * sizeof(float) + 256;
+}
+int fwd_vstages(int C2) {
+  static const int cap = getenv("PARAGAN_ATTN_VSTAGES") ? atoi(getenv("PARAGAN_ATTN_VSTAGES")) : kFwdVMax;
+  int n = cap < 2 ? 2 : (cap > kFwdVMax ? kFwdVMax : cap);
+  while (n > 2 && fwd_smem(C2, n) > kSmemMax) --n;
+  return n;
+}
 // fixed part (phi, g, P^T, dS^T) + NS stages; the largest NS <= 4 that fits
 // NP (P/dS buffers) = 2 only when a 3-stage theta/dO ring still fits (measured: NP 2 with a 2-stage ring is
 // slower than NP 1 with 3 stages for D's block, 2.4 vs 2.2 ms), else 1; then the largest NS <= 4
@@ -694,11 +733,12 @@ cudaError_t tc_attn_fwd(const TcAttnArgs& a, cudaStream_t st) {
   PG_CUDA(map3(&mq, a.qkv, a.Ct, a.HW, a.n, 64, kT));
   PG_CUDA(map3(&mk, a.phi, a.Cq, a.Q, a.n, 64, kT));
   PG_CUDA(map3(&mv, a.gT, a.Q, a.C2, a.n, 64, a.C2));
-  const size_t smem = fwd_smem(a.C2);
-  PG_CUDA(cudaFuncSetAttribute(k_attn_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int nvs = fwd_vstages(a.C2);
+  const size_t smem = fwd_smem(a.C2, nvs);
   const int sms = sm_cap();
   const int tiles = a.n * (a.HW / kT);
-  k_attn_fwd<<<tiles < sms ? tiles : sms, kFwdThreads, smem, st>>>(mq, mk, mv, a);
+  PG_CUDA(cudaFuncSetAttribute(k_attn_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_attn_fwd<<<tiles < sms ? tiles : sms, kFwdThreads, smem, st>>>(mq, mk, mv, a, nvs);
   return cudaGetLastError();
 }
 

@@ -94,9 +94,10 @@ struct Wgrad3Cfg {
   static_assert(STAGES >= 2, "pipeline needs two stages");
 };
 
+// the dynamic shared-memory base rounded up to 1024 bytes by pointer arithmetic on the shared array itself, so
+// the compiler keeps the shared address space (LDS/STS, not generic LD/ST) for every access derived from it
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
-  uintptr_t a = reinterpret_cast<uintptr_t>(p);
-  return reinterpret_cast<uint8_t*>((a + 1023) & ~uintptr_t(1023));
+  return p + ((1024u - (tc::smem_u32(p) & 1023u)) & 1023u);
 }
 
 // pixel index -> (n, h, w) origin of a 128-pixel tile

@@ -52,9 +52,10 @@ constexpr int kMaxChunks = 4;             // C2 <= 256
 constexpr int kThreads = 192;             // w0 TMA, w1 MMA, w2-5 epilogue (one per TMEM lane quadrant)
 constexpr size_t kSmem = 1024 + kMaxChunks * kBChunk + kStages * kABytes + 2 * 4 * 2 * 9 * sizeof(float) + 256;
 
+// the dynamic shared-memory base rounded up to 1024 bytes by pointer arithmetic on the shared array itself, so
+// the compiler keeps the shared address space (LDS/STS, not generic LD/ST) for every access derived from it
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
-  uintptr_t a = reinterpret_cast<uintptr_t>(p);
-  return reinterpret_cast<uint8_t*>((a + 1023) & ~uintptr_t(1023));
+  return p + ((1024u - (tc::smem_u32(p) & 1023u)) & 1023u);
 }
 
 struct OcArgs {
