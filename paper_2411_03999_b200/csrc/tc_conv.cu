@@ -174,7 +174,13 @@ __device__ __forceinline__ void epilogue_loop(const TcFpropArgs& a, const CUtens
   int sb = 0;   // which of this half's two staging tiles the next 64-column group fills
   int it = 0;
   bool pending = false;
+  // BN <= 128: the two halves take alternate TILES (whole accumulators: half h always reads buffer h) rather than
+  // alternate 64-column groups of each tile, so no half idles when a tile has one or one-and-a-half groups
+  constexpr bool kSplitTiles = BN <= 128;
+  constexpr int kG0Step = kSplitTiles ? 64 : 128;
+  const int g0 = kSplitTiles ? 0 : half * 64;
   for (int tile = tile0; tile < num_tiles; tile += tile_step, ++it) {
+    if (kSplitTiles && (it & 1) != half) continue;
     const int buf = it & 1;
     const int nt = tile % a.n_tiles;
     int mt = CG == 2 ? (tile / a.n_tiles) * 2 + rank : tile / a.n_tiles;
@@ -222,14 +228,14 @@ __device__ __forceinline__ void epilogue_loop(const TcFpropArgs& a, const CUtens
     auto next_cb = [&](int cb) {   // this thread's chunk after cb: within the 64-wide group, else the next group
       const int g = cb & ~63;
       if (cb + 32 < g + 64 && cb + 32 < BN) return cb + 32;
-      return g + 128 < BN ? g + 128 : -1;
+      return g + kG0Step < BN ? g + kG0Step : -1;
     };
     uint4 scur[4] = {};
-    load_side(half * 64 < BN ? half * 64 : -1, scur);
+    load_side(g0 < BN ? g0 : -1, scur);
     tc::mbar_wait(&tfull[buf], (it >> 1) & 1);
     tc::tc_fence_after();
 #pragma unroll 1
-    for (int g = half * 64; g < BN; g += 128) {
+    for (int g = g0; g < BN; g += kG0Step) {
       uint8_t* st = stage + (half * 2 + sb) * kStageBytes;
       if (a.tma_store) {
         // the store that last used this staging tile (two groups ago) has read it; the previous
@@ -398,7 +404,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&tfull[b], 1);
-      tc::mbar_init(&tempty[b], kEpiWarps);
+      tc::mbar_init(&tempty[b], BN <= 128 ? kEpiWarps / 2 : kEpiWarps);   // one half per tile when BN <= 128
     }
     tc::fence_barrier_init();
   }
@@ -1000,7 +1006,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&tfull[b], 1);
-      tc::mbar_init(&tempty[b], kEpiWarps);
+      tc::mbar_init(&tempty[b], BN <= 128 ? kEpiWarps / 2 : kEpiWarps);   // one half per tile when BN <= 128
     }
     tc::fence_barrier_init();
   }
@@ -1142,7 +1148,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&tfull[b], 1);
-      tc::mbar_init(&tempty[b], 2 * kEpiWarps);   // both CTAs' epilogue warps (leader's copy is used)
+      tc::mbar_init(&tempty[b], (BN <= 128 ? 1 : 2) * kEpiWarps);   // both CTAs' epilogue warps (leader's copy)
     }
     tc::fence_barrier_init();
   }
