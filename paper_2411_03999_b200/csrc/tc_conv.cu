@@ -174,9 +174,9 @@ __device__ __forceinline__ void epilogue_loop(const TcFpropArgs& a, const CUtens
   int sb = 0;   // which of this half's two staging tiles the next 64-column group fills
   int it = 0;
   bool pending = false;
-  // BN <= 128: the two halves take alternate TILES (whole accumulators: half h always reads buffer h) rather than
+  // BN <= 192: the two halves take alternate TILES (whole accumulators: half h always reads buffer h) rather than
   // alternate 64-column groups of each tile, so no half idles when a tile has one or one-and-a-half groups
-  constexpr bool kSplitTiles = BN <= 128;
+  constexpr bool kSplitTiles = BN <= 192;
   constexpr int kG0Step = kSplitTiles ? 64 : 128;
   const int g0 = kSplitTiles ? 0 : half * 64;
   for (int tile = tile0; tile < num_tiles; tile += tile_step, ++it) {
@@ -404,7 +404,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&tfull[b], 1);
-      tc::mbar_init(&tempty[b], BN <= 128 ? kEpiWarps / 2 : kEpiWarps);   // one half per tile when BN <= 128
+      tc::mbar_init(&tempty[b], BN <= 192 ? kEpiWarps / 2 : kEpiWarps);   // one half per tile when BN <= 192
     }
     tc::fence_barrier_init();
   }
@@ -1006,7 +1006,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&tfull[b], 1);
-      tc::mbar_init(&tempty[b], BN <= 128 ? kEpiWarps / 2 : kEpiWarps);   // one half per tile when BN <= 128
+      tc::mbar_init(&tempty[b], BN <= 192 ? kEpiWarps / 2 : kEpiWarps);   // one half per tile when BN <= 192
     }
     tc::fence_barrier_init();
   }
@@ -1148,7 +1148,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&tfull[b], 1);
-      tc::mbar_init(&tempty[b], (BN <= 128 ? 1 : 2) * kEpiWarps);   // both CTAs' epilogue warps (leader's copy)
+      tc::mbar_init(&tempty[b], (BN <= 192 ? 1 : 2) * kEpiWarps);   // both CTAs' epilogue warps (leader's copy)
     }
     tc::fence_barrier_init();
   }
