@@ -1,0 +1,4 @@
+cd $GRAFT_REPO_ROOT
+timeout 900 python bench.py > gpurun_out/f1_bench.log 2>&1; tail -1 gpurun_out/f1_bench.log | cut -c1-600
+ROUND=r2b timeout 2400 bash tools/profile_round.sh cg2_192_1 cg2_96_0 cg2_256_2 attn_fwd attn_bwd wgrad3_96 out_conv_fwd out_conv_bwd bn_bwd_apply_bulk > gpurun_out/f1_prof.log 2>&1
+tail -12 gpurun_out/f1_prof.log
