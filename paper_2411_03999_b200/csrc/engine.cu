@@ -1120,6 +1120,7 @@ class Engine final : public EngineBase {
         b.c1.wt4 = A.get<char>((size_t)16 * b.c1.cout * b.c1.cin * 2);
       }
     }
+    if (kBF && subpix_ && !gb_.empty()) fold_jobs_d_ = A.get<FoldJob>(gb_.size());
     alloc_conv(oconv_);
     for (auto& b : db_) {
       if (b.im2col) alloc_conv(b.c1x); else alloc_conv(b.c1);
@@ -1519,6 +1520,26 @@ class Engine final : public EngineBase {
                            cudaMemcpyHostToDevice, st_));
       }
     }
+    // G's conv1 fold table (sub-pixel mode): one grouped launch per G forward
+    std::vector<FoldJob> fj;
+    if (fold_jobs_d_) {
+      int tiles = 0;
+      for (GBlock& b : gb_) {
+        const PEntry& e = G_.E[b.c1.w];
+        FoldJob j{};
+        j.w = G_.p + e.off;
+        j.inv_sigma = G_.sigma + 2 * e.job + 1;
+        j.dst0 = static_cast<bf16*>(b.c1.wp4);
+        j.dst1 = static_cast<bf16*>(b.c1.wt4);
+        j.Cout = b.c1.cout;
+        j.Cin = b.c1.cin;
+        j.tile0 = tiles;
+        tiles += ceil_div(b.c1.cout, 32) * ceil_div(b.c1.cin, 32);
+        fj.push_back(j);
+      }
+      fold_tiles_ = tiles;
+      CK(cudaMemcpyAsync(fold_jobs_d_, fj.data(), fj.size() * sizeof(FoldJob), cudaMemcpyHostToDevice, st_));
+    }
     return sync_ok();
   }
 
@@ -1535,15 +1556,7 @@ class Engine final : public EngineBase {
   // W/sigma of every G conv1 folded into the four phase kernels of the sub-pixel conv
   paragan_status fold_subpixel(bool need_dgrad) {
     if (!subpix_) return PARAGAN_OK;
-    for (GBlock& b : gb_) {
-      const PEntry& e = G_.E[b.c1.w];
-      CK(fold_up2_weights(G_.p + e.off, G_.sigma + 2 * e.job + 1, b.c1.cout, b.c1.cin,
-                          static_cast<bf16*>(b.c1.wp4), st_, 0));
-      if (need_dgrad)
-        CK(fold_up2_weights(G_.p + e.off, G_.sigma + 2 * e.job + 1, b.c1.cout, b.c1.cin,
-                            static_cast<bf16*>(b.c1.wt4), st_, 1));
-      launches_ += need_dgrad ? 2 : 1;
-    }
+    CK(fold_up2_grouped(fold_jobs_d_, (int)gb_.size(), fold_tiles_, need_dgrad, st_));
     return PARAGAN_OK;
   }
   paragan_status sn_backward_net(Net& N) {
@@ -2516,6 +2529,8 @@ class Engine final : public EngineBase {
   bool overlap_ = false, pending_d_ = false;
   int overlap_sms_ = 16, overlap_blocks_ = 3;
   bool ready_ = false, poisoned_ = false, planned_ = false, ones_ready_ = false;
+  FoldJob* fold_jobs_d_ = nullptr;   // G conv1 fold table (sub-pixel mode)
+  int fold_tiles_ = 0;
   bool thin_tc_ = false;  // G's output layer on the tensor cores via bf16 splits (R36; BF16 mode)
   bf16* oconv_ws_ = nullptr;  // its split weight operand [96][2 cl]
   bf16* oconv_wd_ = nullptr;  // the dgrad operand [round_up(cl, 16)][128]

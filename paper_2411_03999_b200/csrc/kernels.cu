@@ -3139,6 +3139,65 @@ __global__ void k_fold_up2(const float* __restrict__ w, const float* __restrict_
   }
 }
 
+// All of G's conv1 folds of one forward in one launch: 32 (o) x 32 (c) tiles; each thread reads its 9 taps
+// coalesced over c, writes the fprop layout coalesced over c and stages the 16 folded values so that the
+// dgrad layout ([Cin][16][Cout]) is written coalesced over o (the per-block kernel read it with a 9*Cin stride).
+// Same arithmetic and summation order as k_fold_up2 (bit-identical).
+__global__ void __launch_bounds__(256) k_fold_up2_grouped(const FoldJob* __restrict__ jobs, int njobs, int dgrad) {
+  __shared__ bf16 st[16][32][34];
+  int j = 0;
+  while (j + 1 < njobs && (int)blockIdx.x >= jobs[j + 1].tile0) ++j;
+  const FoldJob jb = jobs[j];
+  const int t = blockIdx.x - jb.tile0;
+  const int tc = (jb.Cin + 31) / 32;
+  const int o0 = (t / tc) * 32, c0 = (t % tc) * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const float is = jb.inv_sigma[0];
+  const int c = c0 + tx;
+  for (int oo = ty; oo < 32; oo += 8) {
+    const int o = o0 + oo;
+    if (o >= jb.Cout || c >= jb.Cin) continue;
+    float t9[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) t9[k] = jb.w[((long long)o * 9 + k) * jb.Cin + c];
+#pragma unroll
+    for (int ph = 0; ph < 4; ++ph) {
+      const int a = ph >> 1, b = ph & 1;
+#pragma unroll
+      for (int tp = 0; tp < 4; ++tp) {
+        const int p = tp >> 1, q = tp & 1;
+        const int r0 = (a == 0) ? (p == 0 ? 0 : 1) : (p == 0 ? 0 : 2);
+        const int r1 = (a == 0) ? (p == 0 ? 0 : 2) : (p == 0 ? 1 : 2);
+        const int s0 = (b == 0) ? (q == 0 ? 0 : 1) : (q == 0 ? 0 : 2);
+        const int s1 = (b == 0) ? (q == 0 ? 0 : 2) : (q == 0 ? 1 : 2);
+        float acc = 0.0f;
+#pragma unroll
+        for (int rr = 0; rr < 3; ++rr)
+#pragma unroll
+          for (int ss = 0; ss < 3; ++ss)
+            if (rr >= r0 && rr <= r1 && ss >= s0 && ss <= s1) acc += t9[rr * 3 + ss];
+        const bf16 v = __float2bfloat16_rn(acc * is);
+        jb.dst0[(((long long)ph * jb.Cout + o) * 4 + tp) * jb.Cin + c] = v;
+        st[ph * 4 + tp][oo][tx] = v;
+      }
+    }
+  }
+  if (!dgrad) return;
+  __syncthreads();
+  const int o = o0 + tx;
+  if (o >= jb.Cout) return;
+  for (int cc = ty; cc < 32; cc += 8) {
+    if (c0 + cc >= jb.Cin) break;
+#pragma unroll
+    for (int pt = 0; pt < 16; ++pt) jb.dst1[((long long)(c0 + cc) * 16 + pt) * jb.Cout + o] = st[pt][tx][cc];
+  }
+}
+
+cudaError_t fold_up2_grouped(const FoldJob* jobs_d, int njobs, int tiles, bool dgrad, cudaStream_t st) {
+  k_fold_up2_grouped<<<tiles, 256, 0, st>>>(jobs_d, njobs, dgrad ? 1 : 0);
+  return cudaGetLastError();
+}
+
 cudaError_t fold_up2_weights(const float* w, const float* inv_sigma, int Cout, int Cin, bf16* dst, cudaStream_t st,
                              int layout) {
   k_fold_up2<<<grid_for((long long)Cout * Cin, 256), 256, 0, st>>>(w, inv_sigma, Cout, Cin, dst, layout);

@@ -148,6 +148,16 @@ cudaError_t col2im3(const T* dxi, int N, int H, int W, int cx, const T* add, T* 
 // layout 0: fprop operand [phase][Cout][tap][Cin]; layout 1: dgrad operand [Cin][phase * 4 + tap][Cout]
 cudaError_t fold_up2_weights(const float* w, const float* inv_sigma, int Cout, int Cin, bf16* dst, cudaStream_t st,
                              int layout = 0);
+// every G conv1 of a forward at once (same values): job j covers tiles [tile0, tile0 + ceil(Cout/32)*ceil(Cin/32));
+// dst0 = the layout-0 operand, dst1 = the layout-1 operand (written when dgrad)
+struct FoldJob {
+  const float* w;
+  const float* inv_sigma;
+  bf16* dst0;
+  bf16* dst1;
+  int Cout, Cin, tile0, pad;
+};
+cudaError_t fold_up2_grouped(const FoldJob* jobs_d, int njobs, int tiles, bool dgrad, cudaStream_t st);
 
 // ---------------- generic fp32 SIMT kernels of the SN-DCGAN path (config 1; SURVEY Appendix B "K7")
 // strided k x k conv, NHWC, zero padding p; w OHWI [Cout][k][k][ldw] (first Cin of ldw used)
