@@ -222,11 +222,15 @@ class Engine final : public EngineBase {
     attn_single_ = as == nullptr || std::atoi(as) != 0;
     const char* sp = std::getenv("PARAGAN_SUBPIXEL");
     subpix_ = kBF && (sp == nullptr || std::atoi(sp) != 0);
+    const char* gr = std::getenv("PARAGAN_GRAPHS");
+    graphs_on_ = gr == nullptr || std::atoi(gr) != 0;
     const char* tt = std::getenv("PARAGAN_THIN_TC");
     thin_tc_ = kBF && (tt == nullptr || std::atoi(tt) != 0);
     dcgan_ = c.arch == PARAGAN_ARCH_SNDCGAN;
   }
   ~Engine() override {
+    for (auto& g : graphs_)
+      if (g.exec) cudaGraphExecDestroy(g.exec);
     if (ck_thread_.joinable()) ck_thread_.join();
     if (ck_dev_) cudaFree(ck_dev_);
     if (ck_host_) cudaFreeHost(ck_host_);
@@ -565,12 +569,94 @@ class Engine final : public EngineBase {
                         uint32_t flags) override {
     if (!ready_ || poisoned_) return PARAGAN_ERR_ORDER;
     if (!real || !real_y || !z || !fake_y || ((uintptr_t)real & 15)) return fail_arg("d_step: bad pointer");
-    // SN(G) + G forward (no grad) writes fakes into D-input rows [0, B)
-    CKS(sn_forward(G_, false));
-    CKS(fold_subpixel(false));
-    if (dcgan_) CKS(g_forward_dc(z));
-    else CKS(g_forward(z, fake_y, false));
-    return d_step_body(real, real_y, fake_y, flags);
+    return run_graphed(GraphKey{0, flags, {real, real_y, z, fake_y}}, [&]() -> paragan_status {
+      // SN(G) + G forward (no grad) writes fakes into D-input rows [0, B)
+      CKS(sn_forward(G_, false));
+      CKS(fold_subpixel(false));
+      if (dcgan_) CKS(g_forward_dc(z));
+      else CKS(g_forward(z, fake_y, false));
+      return d_step_body(real, real_y, fake_y, flags);
+    });
+  }
+
+  // ------------------------------------------------------------------ CUDA-graph step cache
+  // A D or G step issues ~250 launches.  At world_size 1 (no NCCL on the path) each distinct (step kind, flags,
+  // input pointers) is captured once into a CUDA graph and replayed afterwards: the step's device state (weights,
+  // u vectors, optimiser moments, the step counter t) lives on the device, so a replay is the same computation as
+  // the eager call; the host-side bookkeeping of the step is re-applied by hand.  Disabled while profiling, and
+  // with PARAGAN_GRAPHS=0.  A capture that fails falls back to eager execution for good.
+  struct GraphKey {
+    int kind;
+    uint32_t flags;
+    const void* p[4];
+    bool operator==(const GraphKey& o) const {
+      return kind == o.kind && flags == o.flags && p[0] == o.p[0] && p[1] == o.p[1] && p[2] == o.p[2] && p[3] == o.p[3];
+    }
+  };
+  struct HostState {   // what a step changes on the host
+    int d_since_g;
+    bool dfake_valid;
+    float dgsum, ggsum;
+  };
+  struct GraphEntry {
+    GraphKey key;
+    cudaGraphExec_t exec = nullptr;
+    uint64_t launches = 0;
+    HostState after{};
+  };
+  HostState host_state() const { return HostState{d_since_g_, dfake_valid_, D_.gsum, G_.gsum}; }
+  void set_host_state(const HostState& h) {
+    d_since_g_ = h.d_since_g;
+    dfake_valid_ = h.dfake_valid;
+    D_.gsum = h.dgsum;
+    G_.gsum = h.ggsum;
+  }
+  static constexpr size_t kMaxGraphs = 16;
+  template <class F>
+  paragan_status run_graphed(const GraphKey& k, F&& body) {
+    if (!graphs_on_ || prof_ || pending_d_ || cfg_.world_size != 1) return body();
+    for (auto& g : graphs_) {
+      if (g.key == k) {
+        // a D step's host effect depends on the count before it (++), a G step's does not (= 0)
+        HostState h = g.after;
+        if (k.kind == 0) h.d_since_g = d_since_g_ + 1;
+        if (cudaGraphLaunch(g.exec, st_) != cudaSuccess) return fail_cuda(cudaGetLastError(), "graph launch");
+        set_host_state(h);
+        launches_ += g.launches;
+        return PARAGAN_OK;
+      }
+    }
+    if (graphs_.size() >= kMaxGraphs) return body();
+    const HostState before = host_state();
+    const uint64_t l0 = launches_;
+    if (cudaStreamBeginCapture(st_, cudaStreamCaptureModeRelaxed) != cudaSuccess) {
+      cudaGetLastError();
+      graphs_on_ = false;
+      return body();
+    }
+    const paragan_status s = body();
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamEndCapture(st_, &graph);
+    cudaGraphExec_t exec = nullptr;
+    if (s == PARAGAN_OK && e == cudaSuccess) e = cudaGraphInstantiate(&exec, graph, 0);
+    if (graph) cudaGraphDestroy(graph);
+    if (s != PARAGAN_OK || e != cudaSuccess) {   // nothing ran: undo the host effects, run eagerly from now on
+      cudaGetLastError();
+      if (exec) cudaGraphExecDestroy(exec);
+      graphs_on_ = false;
+      set_host_state(before);
+      launches_ = l0;
+      if (s != PARAGAN_OK) poisoned_ = false, err_.clear();
+      return body();
+    }
+    GraphEntry g;
+    g.key = k;
+    g.exec = exec;
+    g.launches = launches_ - l0;
+    g.after = host_state();
+    graphs_.push_back(g);
+    if (cudaGraphLaunch(exec, st_) != cudaSuccess) return fail_cuda(cudaGetLastError(), "graph launch");
+    return PARAGAN_OK;
   }
   // asynchronous scheme: D on an img_buff entry instead of a fresh G forward
   paragan_status d_step_fakes(const void* real, const int32_t* real_y, const void* fakes, const int32_t* fake_y,
@@ -672,6 +758,9 @@ class Engine final : public EngineBase {
       return PARAGAN_ERR_ORDER;
     }
     if (!z || !y) return fail_arg("g_step: bad pointer");
+    return run_graphed(GraphKey{1, flags, {z, y, nullptr, nullptr}}, [&]() { return g_step_body(z, y, flags); });
+  }
+  paragan_status g_step_body(const float* z, const int32_t* y, uint32_t flags) {
     dfake_valid_ = false;
     CKS(sn_forward(G_, true));
     CKS(fold_subpixel(true));
@@ -2529,6 +2618,8 @@ class Engine final : public EngineBase {
   bool overlap_ = false, pending_d_ = false;
   int overlap_sms_ = 16, overlap_blocks_ = 3;
   bool ready_ = false, poisoned_ = false, planned_ = false, ones_ready_ = false;
+  std::vector<GraphEntry> graphs_;   // CUDA-graph step cache (run_graphed)
+  bool graphs_on_ = false;
   FoldJob* fold_jobs_d_ = nullptr;   // G conv1 fold table (sub-pixel mode)
   int fold_tiles_ = 0;
   bool thin_tc_ = false;  // G's output layer on the tensor cores via bf16 splits (R36; BF16 mode)
