@@ -285,8 +285,10 @@ class Engine final : public EngineBase {
       // A12 overlap: D's gradient all-reduce runs on its own stream and communicator (at most
       // kOverlapCTAs CTAs) while G's forward runs with kOverlapSMs SMs left free; the batch-norm / loss
       // all-reduces get a 2-CTA communicator so the two never compete for more SMs than are reserved
+      // (default: off when the CUDA-graph step cache is on — measured at 2 GPUs, graphs without the overlap
+      // 5,257-5,270 img/s vs the overlap without graphs 5,217-5,229; PARAGAN_OVERLAP=1 forces it)
       const char* ov = std::getenv("PARAGAN_OVERLAP");
-      overlap_ = (ov == nullptr || std::atoi(ov) != 0) && !cfg_.grad_comm_bf16;
+      overlap_ = (ov == nullptr ? !graphs_on_ : std::atoi(ov) != 0) && !cfg_.grad_comm_bf16;
       if (const char* e = std::getenv("PARAGAN_OVERLAP_SMS")) overlap_sms_ = std::atoi(e);
       if (const char* e = std::getenv("PARAGAN_OVERLAP_BLOCKS")) overlap_blocks_ = std::atoi(e);
       if (overlap_) {
@@ -580,11 +582,12 @@ class Engine final : public EngineBase {
   }
 
   // ------------------------------------------------------------------ CUDA-graph step cache
-  // A D or G step issues ~250 launches.  At world_size 1 (no NCCL on the path) each distinct (step kind, flags,
-  // input pointers) is captured once into a CUDA graph and replayed afterwards: the step's device state (weights,
+  // A D or G step issues ~250 launches.  Each distinct (step kind, flags, input pointers) is captured once into
+  // a CUDA graph (NCCL collectives included at world_size > 1) and replayed afterwards: the step's device state (weights,
   // u vectors, optimiser moments, the step counter t) lives on the device, so a replay is the same computation as
-  // the eager call; the host-side bookkeeping of the step is re-applied by hand.  Disabled while profiling, and
-  // with PARAGAN_GRAPHS=0.  A capture that fails falls back to eager execution for good.
+  // the eager call; the host-side bookkeeping of the step is re-applied by hand.  Disabled while profiling, with
+  // the overlapped D all-reduce (it spans two steps) and with PARAGAN_GRAPHS=0.  A capture that fails falls back
+  // to eager execution for good.
   struct GraphKey {
     int kind;
     uint32_t flags;
@@ -614,7 +617,7 @@ class Engine final : public EngineBase {
   static constexpr size_t kMaxGraphs = 16;
   template <class F>
   paragan_status run_graphed(const GraphKey& k, F&& body) {
-    if (!graphs_on_ || prof_ || pending_d_ || cfg_.world_size != 1) return body();
+    if (!graphs_on_ || prof_ || pending_d_ || overlap_) return body();
     for (auto& g : graphs_) {
       if (g.key == k) {
         // a D step's host effect depends on the count before it (++), a G step's does not (= 0)
