@@ -1613,8 +1613,9 @@ __global__ void __launch_bounds__(256) k_sn_wtu_reduce(const SnJob* __restrict__
     const int k = blk_k0[blockIdx.x] + 4 * threadIdx.x;
     if (k >= j.K) return;
     float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 8   // loads issued ahead, additions still in rc order
     for (int rc = 0; rc < j.nrc; ++rc) {
-      const float4 p = *reinterpret_cast<const float4*>(j.part + (long long)rc * j.K + k);
+      const float4 p = __ldg(reinterpret_cast<const float4*>(j.part + (long long)rc * j.K + k));
       a.x += p.x;
       a.y += p.y;
       a.z += p.z;
@@ -1626,7 +1627,8 @@ __global__ void __launch_bounds__(256) k_sn_wtu_reduce(const SnJob* __restrict__
   const int k = blk_k0[blockIdx.x] + threadIdx.x;
   if (k >= j.K) return;
   float a = 0.0f;
-  for (int rc = 0; rc < j.nrc; ++rc) a += j.part[(long long)rc * j.K + k];
+#pragma unroll 8
+  for (int rc = 0; rc < j.nrc; ++rc) a += __ldg(j.part + (long long)rc * j.K + k);
   j.t[k] = a;
 }
 // pass 2: s[r] = sum_k W[r][k] t[k] / ||t||   (block = 8 rows, one warp per row, 16-byte loads)
