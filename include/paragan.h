@@ -229,6 +229,13 @@ paragan_status paragan_apply_update(paragan_ctx* ctx, paragan_net net);
  * PARAGAN_ERR_NONFINITE when an update was skipped since the last call. */
 paragan_status paragan_sync_stats(paragan_ctx* ctx, paragan_stats* out);
 
+/* The same values without a host synchronisation: enqueues, on the context's stream, device-to-host
+ * copies of the last steps' statistics into `out` (caller-owned, page-locked host memory, valid once the
+ * stream has reached this point — e.g. after an event recorded right after the call).  Losses are already
+ * divided by world_size, as in paragan_sync_stats; `nonfinite` is the sticky flag, which only
+ * paragan_sync_stats clears.  For pipelined host loops that read step i's losses while step i + 1 runs. */
+paragan_status paragan_stats_async(paragan_ctx* ctx, paragan_stats* out);
+
 /* Copy the last generated images (bf16/fp32 NHWC as D saw them) to host NCHW fp32 [B,3,R,R]. */
 paragan_status paragan_get_fakes(paragan_ctx* ctx, float* host_nchw, size_t n);
 

@@ -103,6 +103,7 @@ SYMBOLS = {
     "paragan_allreduce_grads": (C.c_int, [C.c_void_p, C.c_int]),
     "paragan_apply_update": (C.c_int, [C.c_void_p, C.c_int]),
     "paragan_sync_stats": (C.c_int, [C.c_void_p, C.POINTER(Stats)]),
+    "paragan_stats_async": (C.c_int, [C.c_void_p, C.c_void_p]),
     "paragan_get_fakes": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t]),
     "paragan_get_dfake": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t]),
     "paragan_kernel_launches": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64)]),
@@ -483,6 +484,16 @@ class Context:
             return s
         _check("paragan_sync_stats", st, self.ctx)
         return s
+
+    def stats_async(self, buf):
+        """Enqueue the stats' device-to-host copy into `buf` (a page-locked uint8 torch tensor of at least
+        ctypes.sizeof(Stats) bytes) on the context's stream, without synchronising; read_stats(buf) once the
+        stream has passed this point."""
+        _check("paragan_stats_async", lib().paragan_stats_async(self.ctx, C.c_void_p(buf.data_ptr())), self.ctx)
+
+    @staticmethod
+    def read_stats(buf) -> Stats:
+        return Stats.from_buffer_copy(C.string_at(buf.data_ptr(), C.sizeof(Stats)))
 
     def kernel_launches(self) -> int:
         n = C.c_uint64()

@@ -171,6 +171,10 @@ paragan_status paragan_sync_stats(paragan_ctx* ctx, paragan_stats* out) {
   if (!ctx || !ctx->eng) return PARAGAN_ERR_INVALID_ARG;
   return ctx->eng->sync_stats(out);
 }
+paragan_status paragan_stats_async(paragan_ctx* ctx, paragan_stats* out) {
+  if (!ctx || !ctx->eng || !out) return PARAGAN_ERR_INVALID_ARG;
+  return ctx->eng->stats_async(out);
+}
 paragan_status paragan_get_fakes(paragan_ctx* ctx, float* host, size_t n) {
   if (!ctx || !ctx->eng) return PARAGAN_ERR_INVALID_ARG;
   return ctx->eng->get_fakes(host, n);

@@ -854,6 +854,16 @@ class Engine final : public EngineBase {
     return PARAGAN_OK;
   }
 
+  // device-side copy of the stats struct (losses scaled by 1/world_size on the device), copied out by
+  // stats_async without a host synchronisation
+  paragan_status stats_async(paragan_stats* out) override {
+    if (!ready_ || poisoned_) return PARAGAN_ERR_ORDER;
+    CKS(flush_d());
+    CK(pack_stats(D_.loss, G_.loss, D_.t_dev, G_.t_dev, nonfinite_sticky_, 1.0f / cfg_.world_size, stats_dev_, st_));
+    if (cudaMemcpyAsync(out, stats_dev_, sizeof(paragan_stats), cudaMemcpyDeviceToHost, st_) != cudaSuccess)
+      return fail_cuda(cudaGetLastError(), "stats_async copy");
+    return PARAGAN_OK;
+  }
   paragan_status sync_stats(paragan_stats* out) override {
     if (!ready_) return PARAGAN_ERR_ORDER;
     CKS(flush_d());
@@ -1213,6 +1223,7 @@ class Engine final : public EngineBase {
       }
     }
     if (kBF && subpix_ && !gb_.empty()) fold_jobs_d_ = A.get<FoldJob>(gb_.size());
+    stats_dev_ = A.get<paragan_stats>(1);
     alloc_conv(oconv_);
     for (auto& b : db_) {
       if (b.im2col) alloc_conv(b.c1x); else alloc_conv(b.c1);
@@ -2624,6 +2635,7 @@ class Engine final : public EngineBase {
   std::vector<GraphEntry> graphs_;   // CUDA-graph step cache (run_graphed)
   bool graphs_on_ = false;
   FoldJob* fold_jobs_d_ = nullptr;   // G conv1 fold table (sub-pixel mode)
+  paragan_stats* stats_dev_ = nullptr;   // stats_async staging
   int fold_tiles_ = 0;
   bool thin_tc_ = false;  // G's output layer on the tensor cores via bf16 splits (R36; BF16 mode)
   bf16* oconv_ws_ = nullptr;  // its split weight operand [96][2 cl]

@@ -27,6 +27,7 @@ class EngineBase {
   virtual paragan_status allreduce(paragan_net net) = 0;
   virtual paragan_status update(paragan_net net) = 0;
   virtual paragan_status sync_stats(paragan_stats* out) = 0;
+  virtual paragan_status stats_async(paragan_stats* out) = 0;
   virtual paragan_status get_fakes(float* host, size_t n) = 0;
   virtual paragan_status get_dfake(float* host, size_t n) = 0;
   virtual paragan_status d_step_fakes(const void* real, const int32_t* real_y, const void* fakes, const int32_t* fake_y,

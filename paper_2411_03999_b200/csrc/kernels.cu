@@ -8,6 +8,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "../../include/paragan.h"
 #include "tc_ptx.cuh"
 
 namespace pg {
@@ -3550,6 +3551,24 @@ __global__ void k_split_out_weights_dgrad(const float* __restrict__ w, int C, in
 
 cudaError_t split_out_weights_dgrad(const float* w, int C, int C16, bf16* wd, cudaStream_t st) {
   k_split_out_weights_dgrad<<<ceil_div(C16 * 128, 256), 256, 0, st>>>(w, C, C16, wd);
+  return cudaGetLastError();
+}
+
+__global__ void k_pack_stats(const float* __restrict__ ld, const float* __restrict__ lg,
+                             const long long* __restrict__ td, const long long* __restrict__ tg,
+                             const int* __restrict__ nf, float inv, paragan_stats* __restrict__ out) {
+  if (threadIdx.x != 0) return;
+  out->d_loss = ld[0] * inv;
+  out->d_real_mean = ld[1] * inv;
+  out->d_fake_mean = ld[2] * inv;
+  out->g_loss = lg[0] * inv;
+  out->nonfinite = *nf;
+  out->t_d = *td;
+  out->t_g = *tg;
+}
+cudaError_t pack_stats(const float* ld, const float* lg, const long long* td, const long long* tg, const int* nf,
+                       float inv, paragan_stats* out, cudaStream_t st) {
+  k_pack_stats<<<1, 32, 0, st>>>(ld, lg, td, tg, nf, inv, out);
   return cudaGetLastError();
 }
 

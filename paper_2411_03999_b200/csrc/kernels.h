@@ -201,6 +201,11 @@ cudaError_t thin_conv_wgrad(const void* x, const float* dy, int N, int H, int W,
 // G's output layer on the tensor cores (R36; tc_outconv.cu): y2[p] = [bf16(x) | bf16(x - bf16(x))]
 // ([P][2C]), and the three-term bf16 split of w[3][9][C] as the B operand [96][2C] (row layout: kernels.cu)
 cudaError_t split_planes(const float* x, long long P, int C, bf16* y2, cudaStream_t st);
+}  // namespace pg
+#include "../../include/paragan.h"
+namespace pg {
+cudaError_t pack_stats(const float* ld, const float* lg, const long long* td, const long long* tg, const int* nf,
+                       float inv, paragan_stats* out, cudaStream_t st);
 cudaError_t split_out_weights(const float* w, int C, bf16* ws, cudaStream_t st);
 // the dgrad operand [C16][128] over the output-gradient im2col [dy1 | dy2 | dy1 | dy1] (tc_outconv.cu)
 cudaError_t split_out_weights_dgrad(const float* w, int C, int C16, bf16* wd, cudaStream_t st);

@@ -87,3 +87,55 @@ def test_apply_update_is_the_oracle_adam_step():
     d_got, d_want = w1[:n].astype(np.float64) - w0[:n], want.numpy() - w0[:n]
     assert np.linalg.norm(d_got - d_want) / np.linalg.norm(d_want) < 1e-5
     assert np.array_equal(w1[n:], w0[n:])
+
+
+def _three_iterations(cfg, g0, d0, dbs, gb, graphs):
+    """Three D+G iterations on the same device inputs (from the second on, the CUDA-graph step cache replays
+    the captured steps); returns params, stats and the async stats of the last iteration."""
+    import ctypes
+    import os
+    old = os.environ.get("PARAGAN_GRAPHS")
+    os.environ["PARAGAN_GRAPHS"] = "1" if graphs else "0"
+    try:
+        ctx = api.Context(cfg)
+    finally:
+        if old is None:
+            del os.environ["PARAGAN_GRAPHS"]
+        else:
+            os.environ["PARAGAN_GRAPHS"] = old
+    ctx.set_params(api.NET_G, g0)
+    ctx.set_params(api.NET_D, d0)
+    tdt = torch.bfloat16 if cfg.compute == api.BF16 else torch.float32
+    real, ry, z, fy = dbs[0]
+    rp = torch.empty((cfg.local_batch, 32, 32, 8), dtype=tdt, device="cuda:0")
+    api.layout_pack(torch.from_numpy(real).cuda(), rp, cfg.compute, 8)
+    ry, z, fy = (torch.from_numpy(a).cuda() for a in (ry, z, fy))
+    zg, yg = (torch.from_numpy(a).cuda() for a in gb)
+    buf = torch.empty(ctypes.sizeof(api.Stats), dtype=torch.uint8).pin_memory()
+    for _ in range(3):
+        ctx.d_step(rp, ry, z, fy)
+        ctx.g_step(zg, yg)
+    ctx.stats_async(buf)
+    torch.cuda.synchronize()
+    sa = api.Context.read_stats(buf)
+    st = ctx.sync_stats(raise_nonfinite=False)
+    out = dict(d=ctx.get_params(api.NET_D), g=ctx.get_params(api.NET_G), launches=ctx.kernel_launches(),
+               stats=(st.d_loss, st.g_loss, st.d_real_mean, st.d_fake_mean, st.t_d, st.t_g),
+               async_stats=(sa.d_loss, sa.g_loss, sa.d_real_mean, sa.d_fake_mean, sa.t_d, sa.t_g))
+    ctx.close()
+    return out
+
+
+def test_graph_step_cache_replays_the_eager_steps_and_async_stats_match():
+    """The CUDA-graph step cache: three iterations with replayed steps are bit-identical to three
+    eager ones (weights, losses, step counters, launch count); paragan_stats_async delivers what
+    paragan_sync_stats reports."""
+    cfg = api.make_config(**MICRO, local_batch=4, compute=api.BF16)
+    ocfg = P.oracle_config(32, 4, 16, 10, 16, 4, bf16=True)
+    gs, ds, g0, d0, dbs, gb = P.make_inputs(ocfg, 4, seed=67)
+    a = _three_iterations(cfg, g0, d0, dbs, gb, graphs=True)
+    b = _three_iterations(cfg, g0, d0, dbs, gb, graphs=False)
+    assert np.array_equal(a["d"], b["d"]) and np.array_equal(a["g"], b["g"])
+    assert a["stats"] == b["stats"] and a["stats"][4:] == (3, 3)
+    assert a["launches"] == b["launches"]
+    assert a["async_stats"] == a["stats"]
