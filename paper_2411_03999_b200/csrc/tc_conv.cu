@@ -1101,14 +1101,20 @@ __global__ void __launch_bounds__(kThreads, 1)
 // ===========================================================================
 template <int BN, int MODE>
 struct Cg2Cfg {
-  static constexpr uint32_t UNIT_BYTES = MODE == 0 ? 50176 : (MODE == 1 ? 32768 : kAtomBytes);
-  static constexpr int NA = MODE == 0 ? 2 : (MODE == 1 ? 3 : 4);
+  // MODE 3: MODE 0's halo units with the whole weight resident in shared memory (this CTA's BN/2 rows of all
+  // 9 taps x 2 channel chunks, loaded once per CTA) and direct stores from the epilogue (no staging tiles):
+  // the C_in = C_out = 96 layers, where re-streaming the weights per tile was half of the per-tile TMA bytes
+  static constexpr bool RESB = MODE == 3;
+  static constexpr uint32_t UNIT_BYTES = (MODE == 0 || RESB) ? 50176 : (MODE == 1 ? 32768 : kAtomBytes);
+  static constexpr int NA = (MODE == 0 || RESB) ? 2 : (MODE == 1 ? 3 : 4);
   static constexpr uint32_t B_BYTES = (BN / 2) * 128;
-  static constexpr int STAGES_RAW = (kSmemBudget - NA * (int)UNIT_BYTES) / (int)B_BYTES;
-  static constexpr int STAGES = STAGES_RAW > 12 ? 12 : STAGES_RAW;
+  static constexpr int SBUFS = RESB ? 0 : kStageBufs;
+  static constexpr int STAGES_RAW = RESB ? 18 : (kSmemBudget - NA * (int)UNIT_BYTES) / (int)B_BYTES;
+  static constexpr int STAGES = RESB ? 18 : (STAGES_RAW > 12 ? 12 : STAGES_RAW);   // RESB: 9 taps x 2 chunks
   static_assert(STAGES >= 2, "CTA-pair conv needs a >= 2 stage B ring");
   static constexpr uint32_t TMEM_COLS = FpropCfg<BN>::TMEM_COLS;
-  static constexpr size_t SMEM = 1024 + NA * UNIT_BYTES + STAGES * B_BYTES + kStageBufs * kStageBytes + 512 + 4 * kMaxBiasSmem;
+  static constexpr size_t SMEM = 1024 + NA * UNIT_BYTES + STAGES * B_BYTES + SBUFS * kStageBytes + 512 + 4 * kMaxBiasSmem;
+  static_assert(SMEM <= 232448, "CTA-pair conv: shared memory");
 };
 
 template <int BN, int MODE>
@@ -1123,7 +1129,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sH = smem;
   uint8_t* sB = smem + NA * C::UNIT_BYTES;
   uint8_t* sO = sB + STAGES * C::B_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sO + kStageBufs * kStageBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sO + C::SBUFS * kStageBytes);
   uint64_t* empty = full + STAGES;
   uint64_t* hfull = empty + STAGES;
   uint64_t* hempty = hfull + NA;
@@ -1160,15 +1166,23 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int mpairs = (a.m_tiles + 1) / 2;
   const int num_tiles = mpairs * a.n_tiles * (a.phases > 1 ? a.phases : 1);
   const int cid = (int)tc::cluster_id_x(), ncl = (int)tc::num_clusters_x();
-  constexpr int UNITS_PER_CHUNK_FIXED = MODE == 0 ? 1 : (MODE == 1 ? 3 : 0);
-  const int units_per_chunk = MODE == 2 ? a.taps : UNITS_PER_CHUNK_FIXED;
-  const int taps_per_unit = MODE == 0 ? 9 : (MODE == 1 ? 3 : 1);
+  constexpr int M0 = C::RESB ? 0 : MODE;   // the halo geometry of MODE 3 is MODE 0's
+  constexpr int UNITS_PER_CHUNK_FIXED = M0 == 0 ? 1 : (M0 == 1 ? 3 : 0);
+  const int units_per_chunk = M0 == 2 ? a.taps : UNITS_PER_CHUNK_FIXED;
+  const int taps_per_unit = M0 == 0 ? 9 : (M0 == 1 ? 3 : 1);
   const int pad = a.ksz >> 1;
 
   if (warp == 0) {
     if (lane == 0) {
       int stage = 0, hs = 0;
       uint32_t phase = 0, hphase = 0;
+      if constexpr (C::RESB) {   // the whole weight (this CTA's half of the rows), once: stage = cc * 9 + tap
+        const uint32_t fbar = tc::map_to_rank(&full[0], 0);
+        if (is_leader) tc::mbar_expect_tx(&full[0], 2 * C::STAGES * C::B_BYTES);
+        for (int cc = 0; cc < a.c_chunks; ++cc)
+          for (int tap = 0; tap < 9; ++tap)
+            tc::tma_load_3d_cg2(sB + (cc * 9 + tap) * C::B_BYTES, &tmB, fbar, cc * 64, tap, (int)rank * (BN / 2));
+      }
       for (int tile = cid; tile < num_tiles; tile += ncl) {
         const int nt = tile % a.n_tiles;
         const int mp = tile / a.n_tiles;
@@ -1183,9 +1197,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc::mbar_wait(&hempty[hs], hphase ^ 1);
             const uint32_t hbar = tc::map_to_rank(&hfull[hs], 0);
             if (is_leader) tc::mbar_expect_tx(&hfull[hs], 2 * unit_tx);
-            if (MODE == 0) {
+            if (M0 == 0) {
               tc::tma_load_4d_cg2(sH + hs * C::UNIT_BYTES, &tmA, hbar, cc * 64, w0 - 1, h0 - 1, n0);
-            } else if (MODE == 1) {
+            } else if (M0 == 1) {
               tc::tma_load_4d_cg2(sH + hs * C::UNIT_BYTES, &tmA, hbar, cc * 64, w0 - 1 + u, h0 - 1, n0);
             } else if (a.phase_dgrad) {   // tap u = phase * 4 + p * 2 + q: dY of phase (a, b) at (i+1-a-p, j+1-b-q)
               const int ph = u >> 2, ta = ph >> 1, tb = ph & 1, p = (u >> 1) & 1, q = u & 1;
@@ -1198,7 +1212,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               const int dy = u / a.ksz - pad, dx = u % a.ksz - pad;
               tc::tma_load_4d_cg2(sH + hs * C::UNIT_BYTES, &tmA, hbar, cc * 64, w0 + dx, h0 + dy, n0);
             }
-            for (int j = 0; j < taps_per_unit; ++j) {
+            for (int j = 0; j < taps_per_unit && !C::RESB; ++j) {
               const int tap = MODE == 0 ? j : (MODE == 1 ? j * 3 + u : u);
               tc::mbar_wait(&empty[stage], phase ^ 1);
               const uint32_t fbar = tc::map_to_rank(&full[stage], 0);
@@ -1220,6 +1234,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0, hs = 0;
       uint32_t phase = 0, hphase = 0;
       int it = 0;
+      if constexpr (C::RESB) {
+        tc::mbar_wait(&full[0], 0);   // the resident weight has landed in both CTAs
+        tc::tc_fence_after();
+      }
       for (int tile = cid; tile < num_tiles; tile += ncl, ++it) {
         const int buf = it & 1;
         tc::mbar_wait(&tempty[buf], ((it >> 1) & 1) ^ 1);
@@ -1233,23 +1251,28 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc::tc_fence_after();
             const uint32_t h_base = sH0 + hs * C::UNIT_BYTES;
             for (int j = 0; j < taps_per_unit; ++j) {
-              tc::mbar_wait(&full[stage], phase);
-              tc::tc_fence_after();
+              if constexpr (!C::RESB) {
+                tc::mbar_wait(&full[stage], phase);
+                tc::tc_fence_after();
+              }
               const uint32_t row =
-                  MODE == 0 ? (uint32_t)((j / 3) * 130 + (j % 3)) : (MODE == 1 ? (uint32_t)(j * a.W) : 0u);
+                  M0 == 0 ? (uint32_t)((j / 3) * 130 + (j % 3)) : (M0 == 1 ? (uint32_t)(j * a.W) : 0u);
               // descriptors advance by 32 bytes (= 2 in the >>4 address field) per K=16 step
               const uint64_t ad0 = tc::sdesc_sw128(h_base + row * 128, 16, 1024);
-              const uint64_t bd0 = tc::sdesc_sw128(sB0 + stage * C::B_BYTES, 16, 1024);
+              const uint32_t bstage = C::RESB ? (uint32_t)(cc * 9 + j) : (uint32_t)stage;
+              const uint64_t bd0 = tc::sdesc_sw128(sB0 + bstage * C::B_BYTES, 16, 1024);
               if (issuer) {
                 tc::mma_bf16_cg2(d_tmem, ad0, bd0, idesc, acc);
                 if (ksteps > 1) tc::mma_bf16_cg2(d_tmem, ad0 + 2, bd0 + 2, idesc, 1u);
                 if (ksteps > 2) tc::mma_bf16_cg2(d_tmem, ad0 + 4, bd0 + 4, idesc, 1u);
                 if (ksteps > 3) tc::mma_bf16_cg2(d_tmem, ad0 + 6, bd0 + 6, idesc, 1u);
-                tc::mma_commit_cg2(&empty[stage], 3);
+                if constexpr (!C::RESB) tc::mma_commit_cg2(&empty[stage], 3);
               }
               __syncwarp();
               acc = 1u;
-              if (++stage == STAGES) { stage = 0; phase ^= 1; }
+              if constexpr (!C::RESB) {
+                if (++stage == STAGES) { stage = 0; phase ^= 1; }
+              }
             }
             if (issuer) tc::mma_commit_cg2(&hempty[hs], 3);
             __syncwarp();
@@ -1605,6 +1628,12 @@ cudaError_t tc_conv_fprop(const void* x, int N, int H, int W, int Cin, const voi
     if (halo_on && ksz == 3 && W % 128 == 0) {
       CUtensorMap mh;
       PG_CUDA(halo_map(&mh, x, N, H, W, Cin, 130, 3));
+      static const int resb_on = env_int("PARAGAN_RESB", 1);
+      if (resb_on && bn == 96 && Cout == 96 && a.n_tiles == 1 && a.c_chunks == 2) {
+        TcFpropArgs a3 = a;   // resident weight, direct-store epilogue
+        a3.tma_store = 0;
+        return launch_cg2_bn<96, 3>(mh, mb2, mo, a3, 390u * 128u, st, nullptr);
+      }
       return launch_cg2<0>(bn, mh, mb2, mo, a, 390u * 128u, st);
     }
     if (halo_on && ksz == 3 && W >= 16 && W <= 64 && H % (128 / W) == 0) {
