@@ -411,9 +411,11 @@ paragan_status paragan_op_attn_fwd(const void* qkv, const void* phi, const void*
     return PARAGAN_ERR_INVALID_ARG;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   void* gT = nullptr;
-  if (cudaMallocAsync(&gT, (size_t)n * (hw / 4) * c2 * 2 + (size_t)n * sizeof(float) + 256, st) != cudaSuccess)
+  if (cudaMallocAsync(&gT, (size_t)n * (hw / 4) * c2 * 2 + 2 * (size_t)n * sizeof(float) + 256, st) != cudaSuccess)
     return PARAGAN_ERR_CUDA;
   float* phimax = reinterpret_cast<float*>(static_cast<char*>(gT) + (((size_t)n * (hw / 4) * c2 * 2 + 255) & ~size_t(255)));
+  float* thetamax = phimax + n;
+  const int flat_on = getenv("PARAGAN_ATTN_FLAT") ? atoi(getenv("PARAGAN_ATTN_FLAT")) : 1;   // per call (tests toggle it)
   TcAttnArgs a{};
   a.n = n;
   a.HW = hw;
@@ -429,8 +431,10 @@ paragan_status paragan_op_attn_fwd(const void* qkv, const void* phi, const void*
   a.o32 = o32;
   a.lse = lse;
   a.phimax = phimax;
+  a.thetamax = flat_on ? thetamax : nullptr;
   cudaError_t e = attn_transpose(gp, n, a.Q, c2, gT, st);
   if (e == cudaSuccess) e = attn_phimax(phi, n, a.Q, cq, phimax, st);
+  if (e == cudaSuccess && flat_on) e = attn_thetamax(qkv, n, hw, cq, ct, thetamax, st);
   if (e == cudaSuccess) e = tc_attn_fwd(a, st);
   cudaFreeAsync(gT, st);
   return cuda_status(e);

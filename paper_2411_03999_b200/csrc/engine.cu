@@ -139,6 +139,7 @@ struct AttnL {
   void* gT = nullptr;              // pooled g transposed [n][C2][Q]
   float *o32 = nullptr, *lse = nullptr, *Dr = nullptr;
   float* phimax = nullptr;         // [n] max_j |phi_j| (enables the single-pass fused forward)
+  float* thetamax = nullptr;       // [n] max_i |theta_i| (with phimax: the flat schedule)
 };
 struct GBlock {
   int cin, cout, hin;
@@ -220,6 +221,8 @@ class Engine final : public EngineBase {
   Engine(const paragan_config& c, cudaStream_t st) : cfg_(c), st_(st) {
     const char* as = std::getenv("PARAGAN_ATTN_SINGLE");
     attn_single_ = as == nullptr || std::atoi(as) != 0;
+    const char* af = std::getenv("PARAGAN_ATTN_FLAT");
+    attn_flat_ = af == nullptr || std::atoi(af) != 0;
     const char* sp = std::getenv("PARAGAN_SUBPIXEL");
     subpix_ = kBF && (sp == nullptr || std::atoi(sp) != 0);
     const char* gr = std::getenv("PARAGAN_GRAPHS");
@@ -1319,6 +1322,7 @@ class Engine final : public EngineBase {
         at->o32 = A.get<float>((size_t)n * HW * at->C2);
         at->lse = A.get<float>((size_t)n * HW);
         at->phimax = A.get<float>((size_t)n);
+        at->thetamax = A.get<float>((size_t)n);
         at->Dr = A.get<float>((size_t)n * HW);
         dth_part_floats_ = std::max(dth_part_floats_, (size_t)((Q / 128) * n * HW * at->Cq));
       } else {
@@ -2221,6 +2225,7 @@ class Engine final : public EngineBase {
     t.lse = a.lse;
     t.Dr = a.Dr;
     t.phimax = attn_single_ ? a.phimax : nullptr;
+    t.thetamax = attn_single_ && attn_flat_ ? a.thetamax : nullptr;
     return t;
   }
   paragan_status attn_forward(Net& N, AttnL& a, const void* x, int n, void* out) {
@@ -2244,6 +2249,7 @@ class Engine final : public EngineBase {
     if (a.fused) {
       CK(attn_transpose(a.g_p, n, (int)Q, a.C2, a.gT, st_));
       CK(attn_phimax(a.phi_p, n, (int)Q, a.Cq, a.phimax, st_));
+      if (attn_flat_) CK(attn_thetamax(a.qkv, n, (int)HW, a.Cq, a.Ct, a.thetamax, st_));
       TcAttnArgs t = attn_args(a, n);
       CK(timed(5, 2.0 * n * HW * Q * (double)(a.Cq + a.C2), [&] { return tc_attn_fwd(t, st_); }, "attn fwd"));
     } else {
@@ -2640,6 +2646,7 @@ class Engine final : public EngineBase {
   bool thin_tc_ = false;  // G's output layer on the tensor cores via bf16 splits (R36; BF16 mode)
   bf16* oconv_ws_ = nullptr;  // its split weight operand [96][2 cl]
   bf16* oconv_wd_ = nullptr;  // the dgrad operand [round_up(cl, 16)][128]
+  bool attn_flat_ = true;   // attention forward: image-wide offset when the score bound allows (tc_attn.cu)
   bool subpix_ = false;   // G conv1 as four phase 2x2 convs of the low-resolution input (NEXT-1)
   bool attn_single_ = true;   // single-pass fused attention forward when the score bound allows (R21)
   bool dcgan_ = false;    // SN-DCGAN (config 1) instead of BigGAN

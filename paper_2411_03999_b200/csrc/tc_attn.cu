@@ -40,6 +40,9 @@ constexpr int kT = 128;                 // query rows per tile = keys per chunk
 constexpr uint32_t kAtom = 16384;       // 128 rows x 128 B, one SW128 operand atom
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kSpan = 16.0f;          // single-pass forward when every row's score bound is within e^16 of chunk 0's max
+constexpr float kFlat = 40.0f;          // "flat" tiles: every score of the image lies in [-U, U] with U <= 40, so the
+                                        // constant offset U (exp(S - U) in [e^-80, 1], normal in fp32 / bf16) needs
+                                        // no per-tile max and no decision round-trip
 constexpr int kFwdKStages = 3, kFwdVMax = 4;   // V ring: as many stages (2..4) as fit
 constexpr int kFwdThreads = 320;        // w0 TMA, w1 MMA, w2-9 softmax / epilogue
 constexpr int kSoftThreads = 256;
@@ -139,10 +142,17 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const int tiles_per_img = a.HW / kT;
   const int num_tiles = a.n * tiles_per_img;
   const int NC = a.Q / kT;
+  // the image-wide Cauchy-Schwarz bound U = max_i |theta_i| max_j |phi_j| (every role evaluates the same
+  // expression on the same global values, so they agree without communicating)
+  auto flat_bound = [&](int b) -> float {
+    if (!a.thetamax || !a.phimax || NC < 2) return -1.0f;
+    const float U = a.thetamax[b] * a.phimax[b] * 1.001f + 1e-3f;
+    return U <= kFlat ? U : -1.0f;   // false for NaN / inf
+  };
 
   if (warp == 0) {
     if (lane == 0) {
-      int ks = 0, vs = 0, it = 0;
+      int ks = 0, vs = 0, it = 0, dit = 0;
       uint32_t kph = 0, vph = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
         const int b = tile / tiles_per_img;
@@ -171,8 +181,13 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         if (NC > 1) load_k(1);
         const int vpre = NC < 2 ? NC : 2;
         for (int c = 0; c < vpre; ++c) load_v(c);
-        tc::mbar_wait(decbar, it & 1);
-        if (*reinterpret_cast<volatile uint32_t*>(dec)) {   // single pass: V(c), then K(c + 2)
+        bool single = true;
+        if (flat_bound(b) < 0.0f) {
+          tc::mbar_wait(decbar, dit & 1);
+          single = *reinterpret_cast<volatile uint32_t*>(dec) != 0;
+          ++dit;
+        }
+        if (single) {   // single pass: V(c), then K(c + 2)
           for (int c = 0; c < NC; ++c) {
             if (c >= vpre) load_v(c);
             if (c + 2 < NC) load_k(c + 2);
@@ -192,7 +207,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       const uint32_t idS = tc::idesc_bf16(kT, kT, false, false);
       const uint32_t idO = tc::idesc_bf16(kT, C2, false, false);
       const int ksteps = a.Cq / 16;
-      int ks = 0, vs = 0, it = 0;
+      int ks = 0, vs = 0, it = 0, dit = 0;
       uint32_t kph = 0, vph = 0;
       uint32_t su = 0, pc = 0;   // running S-buffer use / P-buffer use counters
       int qb = 0;                // theta buffer of the current tile
@@ -217,8 +232,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         tc::mbar_wait(&qfull[qb], (it >> 1) & 1);
         tc::tc_fence_after();
         issue_s(false);                                     // chunk 0 (its max decides the schedule)
-        tc::mbar_wait(decbar, it & 1);
-        const bool single = *reinterpret_cast<volatile uint32_t*>(dec) != 0;
+        bool single = true;
+        if (flat_bound(tile / tiles_per_img) < 0.0f) {
+          tc::mbar_wait(decbar, dit & 1);
+          single = *reinterpret_cast<volatile uint32_t*>(dec) != 0;
+          ++dit;
+        }
         if (!single) {
           for (int u = 1; u < NC; ++u) issue_s(false);      // rest of pass 1
           issue_s(NC == 1);                                 // pass 2 starts again at chunk 0
@@ -306,7 +325,15 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       // chunks (P~ = exp(S - m0) <= e^kSpan: no overflow, and bf16 / fp32 keep their relative precision at
       // any magnitude), so the scores are computed and exponentiated once (single pass); otherwise pass 1
       // finds the exact row max first (two passes).  Either way O = (P~ g) / l and lse = m + log l exactly.
+      // Flat images (flat_bound): the offset is the image-wide bound U itself, every chunk is loaded in the loop
+      // below and there is neither a chunk-0 max nor a decision.
       float v[32], w[32];
+      float* rb = red + (it & 1) * 2 * kT;
+      const float uflat = flat_bound(b);
+      float m = uflat;
+      uint32_t single = 1;
+      bool have0 = false;   // chunk 0's scores already in v / w
+      if (uflat < 0.0f) {
       {
         const int sb = su & 1;
         tc::mbar_wait(&sfull[sb], (su >> 1) & 1);
@@ -317,10 +344,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         tc::mbar_arrive(&sempty[sb]);
         ++su;
       }
-      float m = -INFINITY;
+      m = -INFINITY;
 #pragma unroll
       for (int j = 0; j < 32; ++j) m = fmaxf(m, fmaxf(v[j], w[j]));
-      float* rb = red + (it & 1) * 2 * kT;
       rb[h * kT + row] = m;
       tc::named_bar(1, kSoftThreads);
       m = fmaxf(rb[row], rb[kT + row]);
@@ -341,10 +367,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         const float U = sqrtf(t2) * a.phimax[b] * 1.001f + 1e-3f;
         ok = (U - m <= kSpan) ? 1u : 0u;   // false for NaN / inf
       }
-      uint32_t single;
       asm volatile("{\n\t.reg .pred p, q;\n\tsetp.ne.u32 p, %1, 0;\n\tbar.red.and.pred q, 2, %2, p;\n\t"
                    "selp.u32 %0, 1, 0, q;\n\t}"
                    : "=r"(single) : "r"(ok), "r"(kSoftThreads) : "memory");
+      have0 = single != 0;
       if (threadIdx.x == 64) {   // warp 2 lane 0 publishes the decision to the TMA and MMA warps
         *dec = single;
         tc::mbar_arrive(decbar);
@@ -368,12 +394,13 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         tc::named_bar(1, kSoftThreads);
         m = fmaxf(rb[row], rb[kT + row]);
       }
+      }   // (not flat)
       // P~ = exp(S - m) -> bf16 smem tile for the P~ g MMA; l = sum of P~ in fp32
       const float ml = m * kLog2e;
       float l = 0.0f;
       for (int c = 0; c < NC; ++c, ++pc) {
         const int pb = pc & 1;
-        if (c > 0 || !single) {   // single pass: chunk 0's scores are still in registers
+        if (c > 0 || !have0) {   // single pass after a decision: chunk 0's scores are still in registers
           const int sb = su & 1;
           tc::mbar_wait(&sfull[sb], (su >> 1) & 1);
           tc::tc_fence_after();
@@ -822,14 +849,15 @@ __global__ void k_attn_dtheta_reduce(const float* __restrict__ part, int nkb, lo
 }
 }  // namespace
 
-__global__ void k_attn_phimax(const bf16* __restrict__ phi, int Q, int Cq, float* __restrict__ out) {
+// out[b] = max over the `rows` rows of image b of the L2 norm of the row's first `cols` entries (row stride ld)
+__global__ void k_attn_phimax(const bf16* __restrict__ phi, int Q, int Cq, int ld, float* __restrict__ out) {
   __shared__ float red[8];
-  const bf16* p = phi + (long long)blockIdx.x * Q * Cq;
+  const bf16* p = phi + (long long)blockIdx.x * Q * ld;
   float mx = 0.0f;
   for (int j = threadIdx.x; j < Q; j += blockDim.x) {
     float t = 0.0f;
     for (int c = 0; c < Cq; ++c) {
-      const float x = __bfloat162float(p[(long long)j * Cq + c]);
+      const float x = __bfloat162float(p[(long long)j * ld + c]);
       t = fmaf(x, x, t);
     }
     mx = fmaxf(mx, t);
@@ -846,7 +874,11 @@ __global__ void k_attn_phimax(const bf16* __restrict__ phi, int Q, int Cq, float
 }
 
 cudaError_t attn_phimax(const void* phi, int n, int Q, int Cq, float* phimax, cudaStream_t st) {
-  k_attn_phimax<<<n, 256, 0, st>>>(static_cast<const bf16*>(phi), Q, Cq, phimax);
+  k_attn_phimax<<<n, 256, 0, st>>>(static_cast<const bf16*>(phi), Q, Cq, Cq, phimax);
+  return cudaGetLastError();
+}
+cudaError_t attn_thetamax(const void* qkv, int n, int HW, int Cq, int Ct, float* thetamax, cudaStream_t st) {
+  k_attn_phimax<<<n, 256, 0, st>>>(static_cast<const bf16*>(qkv), HW, Cq, Ct, thetamax);
   return cudaGetLastError();
 }
 

@@ -17,6 +17,8 @@ struct TcAttnArgs {
   float* lse;          // fp32 [n][HW]     row log-sum-exp of the scores (forward out, backward in)
   const float* phimax; // fp32 [n]         max_j |phi_j| per image (forward; enables the single-pass
                        //                  schedule, see k_attn_fwd), or null = always two passes
+  const float* thetamax; // fp32 [n]       max_i |theta_i| per image (forward; with phimax enables the flat
+                         //                schedule for images whose score bound is <= 40), or null
   // backward
   const void* dO;      // bf16 [n][HW][C2]
   const float* Dr;     // fp32 [n][HW]     rowsum(dO * o) = rowsum(dP * beta)
@@ -41,6 +43,8 @@ namespace pg {
 cudaError_t attn_transpose(const void* gp, int n, int Q, int C, void* gT, cudaStream_t st);
 // phimax[b] = max_j ||phi[b][j][0:Cq]||_2 (fp32; one block per image)
 cudaError_t attn_phimax(const void* phi, int n, int Q, int Cq, float* phimax, cudaStream_t st);
+// thetamax[b] = max_i |theta_i| over image b (theta = channels [0, Cq) of qkv [n][HW][Ct])
+cudaError_t attn_thetamax(const void* qkv, int n, int HW, int Cq, int Ct, float* thetamax, cudaStream_t st);
 // D[r] = sum_c dO[r][c] * o32[r][c]   (one warp per row)
 cudaError_t attn_rowdot(const void* dO, const float* o32, long long rows, int C, float* D, cudaStream_t st);
 // dqkv[r][0:Cq] = bf16( sum_{kb < nkb} part[kb][r][0:Cq] ), summed in kb order (deterministic)

@@ -58,11 +58,14 @@ CASES = [(2, 4096, 16, 48, 80), (1, 4096, 32, 96, 160), (3, 512, 16, 16, 48), (2
 
 
 @pytest.mark.parametrize("n,hw,cq,c2,ct", CASES)
-@pytest.mark.parametrize("scale", [0.5, 1.5, 6.0])
-def test_attn_fwd_bwd_vs_definition(n, hw, cq, c2, ct, scale):
-    """scale 0.5 / 1.5: every tile takes the single-pass forward (the score bound is within e^16 of chunk 0's
-    max, R21); scale 6: the scores spread over hundreds, the bound check fails and the tiles take the exact
-    two-pass forward."""
+@pytest.mark.parametrize("scale,flat", [(0.5, 1), (0.5, 0), (1.5, 1), (1.5, 0), (6.0, 1)])
+def test_attn_fwd_bwd_vs_definition(n, hw, cq, c2, ct, scale, flat, monkeypatch):
+    """scale 0.5: the image-wide score bound max|theta| max|phi| is below 40 and (flat = 1) every tile takes
+    the flat forward with that bound as its softmax offset, or (flat = 0, PARAGAN_ATTN_FLAT=0) the per-tile
+    single-pass decision; scale 1.5: every tile takes the single-pass forward (the score bound is within e^16
+    of chunk 0's max, R21); scale 6: the scores spread over hundreds, the bound check fails and the tiles take
+    the exact two-pass forward."""
+    monkeypatch.setenv("PARAGAN_ATTN_FLAT", str(flat))
     qkv, phi, gp, dO = _inputs(n, hw, cq, c2, ct, scale, seed=hw + cq + c2)
     want = _reference(qkv, phi, gp, dO, cq)
     q = hw // 4
