@@ -4,6 +4,7 @@
 #   gpurun_out/layers.md             per-layer tcgen05 conv table from CUDA events inside a bench step
 #   gpurun_out/r1_<name>.md          ncu --set full summaries of the top kernels
 export PARAGAN_ALLOW_SHORT_WARMUP=1
+export PARAGAN_GRAPHS=0   # ncu profiles eager launches (graph replays are not listed per kernel)
 CMD="python bench.py --steps 1 --warmup 1 --repeats 1 --reals uniform --no-cpu-baseline --no-e2e --no-profile"
 $CMD > gpurun_out/plain_round.log 2>&1 || exit 1
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 3000 --csv \

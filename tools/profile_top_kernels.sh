@@ -3,6 +3,7 @@
 # gpurun_out/${ROUND}_<name>.md (the .ncu-rep files are deleted unless KEEP_REP=1: gpurun returns
 # at most 64 MiB).
 export PARAGAN_ALLOW_SHORT_WARMUP=1
+export PARAGAN_GRAPHS=0   # ncu profiles eager launches (graph replays are not listed per kernel)
 CMD="python bench.py --steps 1 --warmup 1 --repeats 1 --reals uniform --no-cpu-baseline --no-e2e --no-profile"
 $CMD > gpurun_out/plain_prof.log 2>&1 || exit 1
 SPECS="cg2_192_1:k_conv_fprop_cg2<.int.192, .int.1>:4 cg2_96_0:k_conv_fprop_cg2<.int.96, .int.0>:2 cg2_256_2:k_conv_fprop_cg2<.int.256, .int.2>:6 wgrad_192:k_conv_wgrad<.int.192>:4 wgrad_256:k_conv_wgrad<.int.256>:4 thin_fwd:k_thin_fwd:1 thin_wgrad:k_thin_wgrad:0 thin_dgrad:k_thin_dgrad:0 attn_fwd:k_attn_fwd:1 attn_bwd:k_attn_bwd:0"
