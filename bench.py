@@ -479,9 +479,11 @@ def main():
                     "traffic_source": traffic.get("source"), "launches": n0, "kernel_ms_per_step": t0 / args.steps,
                     "share_of_step": (t0 / args.steps) / (ms_max / args.steps),
                     "achieved_executed": (prof[3][2] / (t0 / 1000.0)) / 1e12 if t0 > 0 else 0.0,
+                    "frac_executed": ((prof[3][2] / (t0 / 1000.0)) / 1e12) / sustained if t0 > 0 else 0.0,
                     "note": "achieved = algorithmic flops (G's conv1 over the upsampled tensor, SURVEY 8(d)) / time; "
                             "achieved_executed = flops issued to the tensor cores (sub-pixel conv1: 1/2.25 of its "
-                            "algorithmic work) / time",
+                            "algorithmic work) / time.  frac can exceed 1: the sub-pixel decomposition does 2.25x "
+                            "less work than the conv it is credited with; frac_executed is the tensor-pipe figure",
                     "wgrad": {"achieved": (f1_ / (t1 / 1000.0)) / 1e12 if t1 > 0 else 0.0,
                               "achieved_executed": (prof[4][2] / (t1 / 1000.0)) / 1e12 if t1 > 0 else 0.0,
                               "launches": n1, "ms_per_step": t1 / args.steps}}

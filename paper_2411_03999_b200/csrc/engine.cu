@@ -2249,7 +2249,11 @@ class Engine final : public EngineBase {
     if (a.fused) {
       CK(attn_transpose(a.g_p, n, (int)Q, a.C2, a.gT, st_));
       CK(attn_phimax(a.phi_p, n, (int)Q, a.Cq, a.phimax, st_));
-      if (attn_flat_) CK(attn_thetamax(a.qkv, n, (int)HW, a.Cq, a.Ct, a.thetamax, st_));
+      ++launches_;   // two kernels (max, square root)
+      if (attn_flat_) {
+        CK(attn_thetamax(a.qkv, n, (int)HW, a.Cq, a.Ct, a.thetamax, st_));
+        ++launches_;
+      }
       TcAttnArgs t = attn_args(a, n);
       CK(timed(5, 2.0 * n * HW * Q * (double)(a.Cq + a.C2), [&] { return tc_attn_fwd(t, st_); }, "attn fwd"));
     } else {

@@ -849,16 +849,26 @@ __global__ void k_attn_dtheta_reduce(const float* __restrict__ part, int nkb, lo
 }
 }  // namespace
 
-// out[b] = max over the `rows` rows of image b of the L2 norm of the row's first `cols` entries (row stride ld)
-__global__ void k_attn_phimax(const bf16* __restrict__ phi, int Q, int Cq, int ld, float* __restrict__ out) {
+// out[b] = max over the `rows` rows of image b of the L2 norm of the row's first `cols` entries (row stride ld):
+// grid (images, row slices), 16-byte loads; the slices combine through an integer atomicMax on the (non-negative)
+// squared norm's bits, which is order-independent; `out` is zeroed first, the square root taken by k_sqrt_inplace
+__global__ void k_attn_rowmaxnorm(const bf16* __restrict__ x, int rows, int cols, int ld, float* __restrict__ out) {
   __shared__ float red[8];
-  const bf16* p = phi + (long long)blockIdx.x * Q * ld;
+  const bf16* p = x + (long long)blockIdx.x * rows * ld;
+  const int per = (rows + gridDim.y - 1) / gridDim.y;
+  const int r0 = blockIdx.y * per, r1 = min(rows, r0 + per);
   float mx = 0.0f;
-  for (int j = threadIdx.x; j < Q; j += blockDim.x) {
+  for (int j = r0 + threadIdx.x; j < r1; j += blockDim.x) {
     float t = 0.0f;
-    for (int c = 0; c < Cq; ++c) {
-      const float x = __bfloat162float(p[(long long)j * ld + c]);
-      t = fmaf(x, x, t);
+    const uint4* rp = reinterpret_cast<const uint4*>(p + (long long)j * ld);
+    for (int c = 0; c < cols / 8; ++c) {
+      const uint4 u = __ldg(rp + c);
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 f = __bfloat1622float2(h[k]);
+        t = fmaf(f.x, f.x, fmaf(f.y, f.y, t));
+      }
     }
     mx = fmaxf(mx, t);
   }
@@ -869,17 +879,28 @@ __global__ void k_attn_phimax(const bf16* __restrict__ phi, int Q, int Cq, int l
   if (threadIdx.x == 0) {
     float m = 0.0f;
     for (int i = 0; i < (int)(blockDim.x >> 5); ++i) m = fmaxf(m, red[i]);
-    out[blockIdx.x] = sqrtf(m);
+    atomicMax(reinterpret_cast<int*>(out) + blockIdx.x, __float_as_int(m));
   }
+}
+__global__ void k_sqrt_inplace(float* __restrict__ v, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = sqrtf(v[i]);
+}
+cudaError_t rowmaxnorm(const void* x, int n, int rows, int cols, int ld, float* out, cudaStream_t st) {
+  if (cols % 8 || ld % 8 || (reinterpret_cast<uintptr_t>(x) & 15)) return cudaErrorInvalidValue;
+  PG_CUDA(cudaMemsetAsync(out, 0, sizeof(float) * n, st));
+  const int slices = rows >= 2048 ? 8 : 1;
+  k_attn_rowmaxnorm<<<dim3(n, slices), 256, 0, st>>>(static_cast<const bf16*>(x), rows, cols, ld, out);
+  PG_CUDA(cudaGetLastError());
+  k_sqrt_inplace<<<ceil_div(n, 256), 256, 0, st>>>(out, n);
+  return cudaGetLastError();
 }
 
 cudaError_t attn_phimax(const void* phi, int n, int Q, int Cq, float* phimax, cudaStream_t st) {
-  k_attn_phimax<<<n, 256, 0, st>>>(static_cast<const bf16*>(phi), Q, Cq, Cq, phimax);
-  return cudaGetLastError();
+  return rowmaxnorm(phi, n, Q, Cq, Cq, phimax, st);
 }
 cudaError_t attn_thetamax(const void* qkv, int n, int HW, int Cq, int Ct, float* thetamax, cudaStream_t st) {
-  k_attn_phimax<<<n, 256, 0, st>>>(static_cast<const bf16*>(qkv), HW, Cq, Ct, thetamax);
-  return cudaGetLastError();
+  return rowmaxnorm(qkv, n, HW, Cq, Ct, thetamax, st);
 }
 
 cudaError_t attn_transpose(const void* gp, int n, int Q, int C, void* gT, cudaStream_t st) {
