@@ -341,6 +341,14 @@ paragan_status paragan_op_conv_fwd_ex(const void* x, int32_t n, int32_t h, int32
                                       const float* bias, int32_t cout, int32_t ksz, const void* residual,
                                       int32_t res_mode, const void* relu_ref, int32_t relu_out, void* y,
                                       void* stream);
+/* D's block output with the 2x2 average pooling fused into the conv epilogue (the engine's path for blocks with
+ * a downsample at W <= 64): t = bf16(conv(x, wgt) + bias + residual) as op_conv_fwd_ex (res_mode 1), then
+ *   y_pool[n][h/2][w/2][Cout] = bf16(((t00 + t01) + (t10 + t11)) * 0.25),  y_relu = relu(y_pool) (optional)
+ * without t reaching memory.  BF16; W <= 64, H and W even, the 128-pixel tiling of op_conv_fwd, Cout % 16 == 0,
+ * 16-byte aligned device pointers. */
+paragan_status paragan_op_conv_fwd_pool(const void* x, int32_t n, int32_t h, int32_t w, int32_t cin, const void* wgt,
+                                        const float* bias, int32_t cout, int32_t ksz, const void* residual,
+                                        void* y_pool, void* y_relu, void* stream);
 /* dw[Cout][k*k][Cin] (fp32) = sum_p dy[p][o] * x[p + tap][c]; db[Cout] (fp32, optional, NULL to skip) =
  * sum_p dy[p][o], the bias gradient (BF16: computed by the same tcgen05 launch).
  * F32 with Cout = 3, 3x3 (G's fp32 output layer) runs the thin kernels, also in op_conv_fwd. */

@@ -129,6 +129,9 @@ SYMBOLS = {
                                          C.c_int32, C.c_void_p, C.c_void_p]),
     "paragan_op_conv_wgrad": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                         C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "paragan_op_conv_fwd_pool": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
+                                           C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                           C.c_void_p]),
     "paragan_op_out_conv_split": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
                                             C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                             C.c_void_p]),
@@ -259,6 +262,14 @@ def op_conv_wgrad(dtype, x, dy, cout, ksz, dw, stream=None, db=None):
     n, h, w, cin = x.shape
     _check("paragan_op_conv_wgrad", lib().paragan_op_conv_wgrad(dtype, _ptr(x), _ptr(dy), n, h, w, cin, cout, ksz,
                                                                 _ptr(dw), _ptr(db), _stream(stream)))
+
+
+def op_conv_fwd_pool(x, wgt, bias, cout, ksz, y_pool, residual=None, y_relu=None, stream=None):
+    """y_pool = avgpool2(bf16(conv(x) + bias + residual)) (+ relu copy), the pooling fused in the epilogue."""
+    n, h, w, cin = x.shape
+    _check("paragan_op_conv_fwd_pool", lib().paragan_op_conv_fwd_pool(_ptr(x), n, h, w, cin, _ptr(wgt), _ptr(bias), cout,
+                                                                      ksz, _ptr(residual), _ptr(y_pool), _ptr(y_relu),
+                                                                      _stream(stream)))
 
 
 def op_out_conv_split(x, wgt, bias, y, dy=None, dw=None, dx=None, stream=None):

@@ -262,6 +262,22 @@ paragan_status paragan_op_conv_fwd_ex(const void* x, int32_t n, int32_t h, int32
   return cuda_status(tc_conv_fprop(x, n, h, w, cin, wgt, cout, ksz, e, static_cast<cudaStream_t>(stream)));
 }
 
+paragan_status paragan_op_conv_fwd_pool(const void* x, int32_t n, int32_t h, int32_t w, int32_t cin, const void* wgt,
+                                        const float* bias, int32_t cout, int32_t ksz, const void* residual,
+                                        void* y_pool, void* y_relu, void* stream) {
+  if (!x || !wgt || !y_pool || n < 1 || h < 2 || w < 2 || cin < 8 || cin % 8 || cout % 16 || (ksz != 1 && ksz != 3) ||
+      !aligned16(x) || !aligned16(wgt) || !aligned16(y_pool) || (y_relu && !aligned16(y_relu)) ||
+      (residual && !aligned16(residual)) || !tc_geometry_ok(h, w))
+    return PARAGAN_ERR_INVALID_ARG;
+  TcEpilogue e;
+  e.bias = bias;
+  e.residual = residual;
+  e.res_mode = residual ? 1 : 0;
+  e.pool_out = y_pool;
+  e.pool_relu = y_relu;
+  return cuda_status(tc_conv_fprop(x, n, h, w, cin, wgt, cout, ksz, e, static_cast<cudaStream_t>(stream)));
+}
+
 paragan_status paragan_op_out_conv_split(const float* x, int32_t n, int32_t h, int32_t w, int32_t cin,
                                          const float* wgt, const float* bias, float* y, const float* dy, float* dw,
                                          float* dx, void* stream) {

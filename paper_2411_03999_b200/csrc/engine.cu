@@ -221,6 +221,8 @@ class Engine final : public EngineBase {
   Engine(const paragan_config& c, cudaStream_t st) : cfg_(c), st_(st) {
     const char* as = std::getenv("PARAGAN_ATTN_SINGLE");
     attn_single_ = as == nullptr || std::atoi(as) != 0;
+    const char* pf = std::getenv("PARAGAN_POOL_FUSE");
+    pool_fuse_ = pf == nullptr || std::atoi(pf) != 0;
     const char* af = std::getenv("PARAGAN_ATTN_FLAT");
     attn_flat_ = af == nullptr || std::atoi(af) != 0;
     const char* sp = std::getenv("PARAGAN_SUBPIXEL");
@@ -1704,8 +1706,10 @@ class Engine final : public EngineBase {
   }
 
   // ------------------------------------------------------------------ conv dispatch
+  // pool_out (BF16 engine): y is not written; the epilogue writes avgpool2(y) there (and relu of it to pool_relu)
   paragan_status conv_fwd(const void* x, int n, int H, const ConvL& c, void* y, const float* bias,
-                          const void* res, int res_mode, const float* alpha = nullptr, bool relu_out = false) {
+                          const void* res, int res_mode, const float* alpha = nullptr, bool relu_out = false,
+                          void* pool_out = nullptr, void* pool_relu = nullptr) {
     if constexpr (kBF) {
       if (!c.f32) {
         TcEpilogue e;
@@ -1714,7 +1718,9 @@ class Engine final : public EngineBase {
         e.alpha = alpha;
         e.residual = res;
         e.res_mode = res ? res_mode : 0;
-        e.out = y;
+        e.out = pool_out ? nullptr : y;
+        e.pool_out = pool_out;
+        e.pool_relu = pool_relu;
         const double fl = 2.0 * n * H * H * (double)c.cout * c.ksz * c.ksz * c.cin;
         char what[48];
         std::snprintf(what, sizeof(what), "fprop n%d %dx%d %d->%d k%d", n, H, H, c.cin, c.cout, c.ksz);
@@ -2388,7 +2394,12 @@ class Engine final : public EngineBase {
           CKS(conv_fwd(b.x, n, H, b.sc, b.s, D_.P(b.sc.b), nullptr, 0));
           skip = b.s;
         }
-        if (b.down) {
+        if (b.down && kBF && pool_fuse_ && H <= 64 && b.cout % 16 == 0) {
+          // conv2 + skip + 2x2 average pooling (+ the next block's relu) in one epilogue: the full-resolution
+          // sum never reaches HBM (bit-identical to conv2 -> avgpool2)
+          CKS(conv_fwd(b.r1, n, H, b.c2, nullptr, D_.P(b.c2.b), skip, 1, nullptr, false, b.out, next_rx));
+          rx_ready = next_rx != nullptr;
+        } else if (b.down) {
           CKS(conv_fwd(b.r1, n, H, b.c2, b.t, D_.P(b.c2.b), skip, 1));
           CK(avgpool2<T>(static_cast<const T*>(b.t), n, H, H, b.cout, b.cout, nullptr, static_cast<T*>(b.out), st_,
                          next_rx));
@@ -2650,6 +2661,7 @@ class Engine final : public EngineBase {
   bool thin_tc_ = false;  // G's output layer on the tensor cores via bf16 splits (R36; BF16 mode)
   bf16* oconv_ws_ = nullptr;  // its split weight operand [96][2 cl]
   bf16* oconv_wd_ = nullptr;  // the dgrad operand [round_up(cl, 16)][128]
+  bool pool_fuse_ = true;   // D blocks: 2x2 average pooling in conv2's epilogue (W <= 64)
   bool attn_flat_ = true;   // attention forward: image-wide offset when the score bound allows (tc_attn.cu)
   bool subpix_ = false;   // G conv1 as four phase 2x2 convs of the low-resolution input (NEXT-1)
   bool attn_single_ = true;   // single-pass fused attention forward when the score bound allows (R21)

@@ -109,6 +109,23 @@ __device__ __forceinline__ void pix_origin(int p0, int H, int W, int& n0, int& h
   w0 = r - h0 * W;
 }
 
+// the first N (multiple of 8) of v as bf16, 16-byte stores
+template <int N>
+__device__ __forceinline__ void store_row32_bf16_n(bf16* dst, const float (&v)[32]) {
+  uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int q = 0; q < N / 8; ++q) {
+    uint4 u;
+    uint32_t* w = reinterpret_cast<uint32_t*>(&u);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      __nv_bfloat162 t = __floats2bfloat162_rn(v[q * 8 + 2 * j], v[q * 8 + 2 * j + 1]);
+      w[j] = *reinterpret_cast<uint32_t*>(&t);
+    }
+    d[q] = u;
+  }
+}
+
 __device__ __forceinline__ void store_row32_bf16(bf16* dst, const float (&v)[32]) {
   uint4* d = reinterpret_cast<uint4*>(dst);
 #pragma unroll
@@ -344,7 +361,44 @@ __device__ __forceinline__ void epilogue_loop(const TcFpropArgs& a, const CUtens
 #pragma unroll
         for (int qq = 0; qq < 4; ++qq) scur[qq] = snext[qq];
       }
-      if (a.tma_store) {
+      if (a.tma_store && a.pool_out) {
+        // fused 2x2 average pooling (D blocks with a downsample): the tile holds whole row pairs, its 32 pooled
+        // pixels are contiguous in the pooled map (base m0 / 4); thread t of the half -> pooled pixel t / 4,
+        // 16 columns; same arithmetic as k_avgpool2_v on the bf16 values (bit-identical)
+        tc::named_bar(1 + half, 128);
+        const int tt = etid & 127;
+        const int pp = tt >> 2, c16 = (tt & 3) * 16;
+        const int hw2 = a.W >> 1;
+        const int r0 = (pp / hw2) * 2 * a.W + (pp % hw2) * 2;
+        const long long pm = (long long)mt * (kTileM / 4) + pp;
+        const int col = nt * BN + g + c16;
+        if ((long long)mt * kTileM + r0 + a.W + 1 < a.M + 0 && g + c16 < BN && col < a.Cout) {
+          float o[16];
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {   // two 16-byte chunks of 8 columns
+            const int ch = (c16 >> 3) + hh;
+            float q[4][8];
+            const int rr[4] = {r0, r0 + 1, r0 + a.W, r0 + a.W + 1};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const uint4 u = *reinterpret_cast<const uint4*>(st + rr[k] * 128 + ((ch ^ (rr[k] & 7)) << 4));
+              bf16x8_to_f32(u, q[k]);
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) o[hh * 8 + j] = ((q[0][j] + q[1][j]) + (q[2][j] + q[3][j])) * 0.25f;
+          }
+          float t16[32];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) t16[j] = o[j];
+          bf16* dst = reinterpret_cast<bf16*>(a.pool_out) + pm * a.ldo + col;
+          store_row32_bf16_n<16>(dst, t16);
+          if (a.pool_relu) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) t16[j] = o[j] > 0.0f ? o[j] : 0.0f;
+            store_row32_bf16_n<16>(reinterpret_cast<bf16*>(a.pool_relu) + pm * a.ldo + col, t16);
+          }
+        }
+      } else if (a.tma_store) {
         tc::fence_async_smem();
         tc::named_bar(1 + half, 128);
         if (leader) {
@@ -1614,13 +1668,20 @@ cudaError_t tc_conv_fprop(const void* x, int N, int H, int W, int Cin, const voi
   a.out_f32 = epi.out_f32;
   a.ldo = epi.ldo ? epi.ldo : Cout;
   a.relu_out = epi.relu_out;
+  a.pool_out = epi.pool_out;
+  a.pool_relu = epi.pool_relu;
   const int sms = sm_cap();
   static const int halo_on = env_int("PARAGAN_HALO", 1), tma_st = env_int("PARAGAN_TMA_STORE", 1),
                    cg2_on = env_int("PARAGAN_CG2", 1);
   CUtensorMap mo;
   a.tma_store = tma_st && !a.out_f32 && (bn % 64 == 0 || a.n_tiles == 1) && a.ldo % 8 == 0 &&
                 !((uintptr_t)epi.out & 15);
-  if (a.tma_store) PG_CUDA(out_map(&mo, epi.out, a.M, Cout, a.ldo));
+  if (a.pool_out) {   // the pooled epilogue reads the staging tiles: whole row pairs per 128-pixel tile
+    if (!a.tma_store || a.out_f32 || W > 64 || (W & 1) || (H & 1) || !tileable(H, W) || Cout % 16 ||
+        ((uintptr_t)epi.pool_out & 15) || ((uintptr_t)epi.pool_relu & 15))
+      return cudaErrorInvalidValue;
+  }
+  if (a.tma_store && !a.pool_out) PG_CUDA(out_map(&mo, epi.out, a.M, Cout, a.ldo));
   else mo = mb;   // unused
   if (cg2_on && a.tma_store && a.m_tiles >= 2) {
     CUtensorMap mb2;

@@ -18,6 +18,10 @@ struct TcEpilogue {
   int out_f32 = 0;
   int ldo = 0;                     // default Cout
   int relu_out = 0;                // ReLU applied last, before the single rounding (D's conv1 -> conv2 input)
+  // fused 2x2 average pooling (W <= 64, H and W even; tiles of whole row pairs): instead of `out` the kernel
+  // writes pool_out = avgpool2(bf16(epilogue)) [M/4][ldo] and, when set, pool_relu = relu(pool_out)
+  void* pool_out = nullptr;
+  void* pool_relu = nullptr;
 };
 
 struct TcFpropArgs {
@@ -36,6 +40,8 @@ struct TcFpropArgs {
   // convs of the low-resolution input, one per output phase (a, b); H, W, M are low-resolution and
   // the output is [N][2H][2W][Cout] written through a 5-D map {C, 2, W, 2, N*H}
   int phases;
+  void* pool_out;    // see TcEpilogue
+  void* pool_relu;
   // phase dgrad (phase_dgrad = 1): the input gradient of conv3x3(up2(x)) at low resolution,
   // dX[i][j] = sum_{phase (a,b), tap (p,q)} dY[2(i+1-a-p)+a][2(j+1-b-q)+b] Wfold_ab[p][q]^T:
   // K = 16 taps, tap u = phase * 4 + p * 2 + q read through the phase's own dY tensor map

@@ -364,3 +364,33 @@ def test_conv_up2_wgrad_integer_exact(shape):
     got = dw.cpu().numpy()
     assert np.array_equal(got, want), np.argwhere(got != want)[:5]
     assert np.array_equal(db.cpu().numpy(), dy.reshape(-1, cout).sum(0).astype(np.float32))
+
+
+POOL_SHAPES = [  # n, h, w, cin, cout, k: D's blocks 1-4 at B = 256 (W = 64 .. 8) and small ragged-batch cases
+    (256, 64, 64, 192, 192, 3), (256, 32, 32, 384, 384, 3), (256, 16, 16, 768, 768, 3), (256, 8, 8, 1536, 1536, 3),
+    (3, 16, 16, 32, 48, 3), (5, 8, 8, 64, 32, 1),
+]
+
+
+@pytest.mark.parametrize("shape", POOL_SHAPES)
+def test_conv_fwd_pool_is_conv_then_avgpool(shape):
+    """The fused pooling epilogue (D blocks with a downsample) equals the unfused path bit for bit: conv (+ bias
+    + residual, rounded to bf16) through op_conv_fwd_ex, then the 2x2 average in fp32 in the order
+    ((t00 + t01) + (t10 + t11)) * 0.25, rounded, and relu of it.  Integer-valued operands keep the conv exact."""
+    n, h, w, cin, cout, k = shape
+    g = torch.Generator(device=DEV).manual_seed(h * w + cin)
+    x = torch.randint(-2, 3, (n, h, w, cin), device=DEV, generator=g).to(torch.bfloat16)
+    wt = torch.randint(-1, 2, (cout, k * k, cin), device=DEV, generator=g).to(torch.bfloat16)
+    b = torch.randint(-3, 4, (cout,), device=DEV, generator=g).float()
+    res = torch.randint(-4, 5, (n, h, w, cout), device=DEV, generator=g).to(torch.bfloat16)
+    t = torch.empty(n, h, w, cout, dtype=torch.bfloat16, device=DEV)
+    api.op_conv_fwd_ex(x, wt, b, cout, k, t, residual=res, res_mode=1)
+    yp = torch.full((n, h // 2, w // 2, cout), float("nan"), dtype=torch.bfloat16, device=DEV)
+    yr = torch.full_like(yp, float("nan"))
+    api.op_conv_fwd_pool(x, wt, b, cout, k, yp, residual=res, y_relu=yr)
+    torch.cuda.synchronize()
+    tf = t.float()
+    want = (((tf[:, 0::2, 0::2] + tf[:, 0::2, 1::2]) + (tf[:, 1::2, 0::2] + tf[:, 1::2, 1::2])) * 0.25)
+    want = want.to(torch.bfloat16)
+    assert torch.equal(yp, want)
+    assert torch.equal(yr, torch.relu(want.float()).to(torch.bfloat16))
