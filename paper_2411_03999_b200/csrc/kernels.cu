@@ -3633,8 +3633,15 @@ __global__ void k_im2col3(const T* __restrict__ x, int N, int H, int W, int cx, 
       const int hh = h + t / 3 - 1, ww = w + t % 3 - 1;
       if (hh >= 0 && hh < H && ww >= 0 && ww < W) {
         const T* src = x + (((long long)n * H + hh) * W + ww) * cx;
+        if (cx == 8) {   // the padded image: one 16-byte load per neighbour (8 bf16 channels, 3 used)
+          float e[8];
+          Vec8<T>::load(src, e);
 #pragma unroll
-        for (int c = 0; c < 3; ++c) v[t * 3 + c] = to_f<T>(src[c]);
+          for (int c = 0; c < 3; ++c) v[t * 3 + c] = e[c];
+        } else {
+#pragma unroll
+          for (int c = 0; c < 3; ++c) v[t * 3 + c] = to_f<T>(src[c]);
+        }
       }
     }
     T* dst = out + p * 32;
