@@ -282,6 +282,7 @@ class Engine final : public EngineBase {
     paragan_status s = upload_tables();
     if (s != PARAGAN_OK) return s;
     if (fill_const(ones_buf_, maxc_, 1.0f, st_) != cudaSuccess) return fail_cuda(cudaGetLastError(), "ones");
+    if (quarter_ && fill_const(quarter_, 1, 0.25f, st_) != cudaSuccess) return fail_cuda(cudaGetLastError(), "quarter");
     if (cfg_.world_size > 1) {
       ncclUniqueId uid;
       std::memcpy(&uid, id, sizeof(uid));
@@ -1353,6 +1354,7 @@ class Engine final : public EngineBase {
     for (auto& b : gb_) maxc_ = std::max(maxc_, std::max(b.cin, b.cout));
     for (auto& b : db_) maxc_ = std::max(maxc_, std::max(b.cin_x, b.cout));
     ones_buf_ = A.get<float>(maxc_);
+    quarter_ = A.get<float>(1);
     feat_ = A.get<float>((size_t)B2 * cdl_);
     logits_ = A.get<float>(B2);
     dlogits_ = A.get<float>(B2);
@@ -1780,14 +1782,14 @@ class Engine final : public EngineBase {
   }
   // dx[n,H,H,cin_x] = alpha * dgrad(dy) (+ add)
   paragan_status conv_dgrad(const void* dy, int n, int H, const ConvL& c, void* dx, const void* add,
-                            const float* alpha = nullptr, const void* relu_ref = nullptr) {
+                            const float* alpha = nullptr, const void* relu_ref = nullptr, int add_mode = 1) {
     if constexpr (kBF) {
       if (!c.f32) {
         TcEpilogue e;
         e.alpha = alpha;
         e.relu_ref = relu_ref;
         e.residual = add;
-        e.res_mode = add ? 1 : 0;
+        e.res_mode = add ? add_mode : 0;
         e.out = dx;
         const double fl = 2.0 * n * H * H * (double)c.cout * c.ksz * c.ksz * c.cin;
         char what[48];
@@ -2463,6 +2465,7 @@ class Engine final : public EngineBase {
       const bool need_dx = (j > 0) || want_dimg;
       int isk = -1;
       void* dskip = nullptr;
+      bool dskip_half = false;   // dskip at half resolution (nearest-upsampled by the consumer's epilogue)
       if (j == 0 && b.down) {
         // s = sc(avgpool(x)) at half res; its gradient is cur (half res)
         if (want_w) {
@@ -2483,7 +2486,15 @@ class Engine final : public EngineBase {
         }
         if (need_dx) {
           isk = other(ic, it, ir1);
-          CKS(conv_dgrad(dt, n, H, b.sc, tmp(isk), nullptr));
+          if (kBF && b.down && b.sc.ksz == 1) {
+            // the 1x1 shortcut's input gradient commutes with the pool's adjoint: sc^T(up2(cur) / 4) =
+            // up2(sc^T(cur)) / 4, computed at half resolution (x 0.25 in the epilogue, exact) and added by conv1's
+            // dgrad epilogue through the half-resolution residual mode — bit-identical, 4x fewer bytes and MACs
+            CKS(conv_dgrad(cur, n, Ho, b.sc, tmp(isk), nullptr, quarter_));
+            dskip_half = true;
+          } else {
+            CKS(conv_dgrad(dt, n, H, b.sc, tmp(isk), nullptr));
+          }
           dskip = tmp(isk);
         }
       } else {
@@ -2502,7 +2513,7 @@ class Engine final : public EngineBase {
         if (k != ir1 && k != isk) { ix = k; break; }
       void* dx = tmp(ix);
       if (j > 0) {   // pre-activation block: relu'(x) mask and the skip gradient fused in the epilogue
-        CKS(conv_dgrad(dr1, n, H, b.c1, dx, dskip, nullptr, b.x));
+        CKS(conv_dgrad(dr1, n, H, b.c1, dx, dskip, nullptr, b.x, dskip_half ? 2 : 1));
       } else if (b.im2col) {
         // dgrad into the im2col buffer (no longer needed), then its adjoint (col2im) + skip gradient
         CKS(conv_dgrad(dr1, n, H, b.c1x, b.xi, nullptr));
@@ -2690,6 +2701,7 @@ class Engine final : public EngineBase {
   std::vector<ProfRec> recs_;
   std::vector<cudaEvent_t> ev_free_;
   float* ones_buf_ = nullptr;
+  float* quarter_ = nullptr;   // device 0.25 (the x2 average pool's adjoint scale as a conv epilogue alpha)
   int maxc_ = 8;
   void* tmp_attn_dqkv_ = nullptr;
   float *zin_ = nullptr, *emb_ = nullptr, *demb_g_ = nullptr, *h0f_ = nullptr, *dh0f_ = nullptr;
