@@ -162,6 +162,7 @@ struct DBlock {
   bool im2col = false;   // first layer as a K = 27 (-> 32) GEMM over an im2col of the image
   ConvL c1, c2, sc, c1x;
   void *x, *rx, *c1o, *r1, *t, *xp, *s, *out, *xi;
+  void* wp4dg = nullptr;   // conv2's input-gradient kernel folded into the four phases (pooled blocks)
 };
 
 int round8(int x) { return (x + 7) / 8 * 8; }
@@ -227,6 +228,8 @@ class Engine final : public EngineBase {
     attn_flat_ = af == nullptr || std::atoi(af) != 0;
     const char* sp = std::getenv("PARAGAN_SUBPIXEL");
     subpix_ = kBF && (sp == nullptr || std::atoi(sp) != 0);
+    const char* dgp = std::getenv("PARAGAN_DGRAD_UP2");
+    dgrad_pool_ = subpix_ && (dgp == nullptr || std::atoi(dgp) != 0);
     const char* gr = std::getenv("PARAGAN_GRAPHS");
     graphs_on_ = gr == nullptr || std::atoi(gr) != 0;
     const char* tt = std::getenv("PARAGAN_THIN_TC");
@@ -1231,11 +1234,19 @@ class Engine final : public EngineBase {
     if (kBF && subpix_ && !gb_.empty()) fold_jobs_d_ = A.get<FoldJob>(gb_.size());
     stats_dev_ = A.get<paragan_stats>(1);
     alloc_conv(oconv_);
-    for (auto& b : db_) {
+    int ndg = 0;
+    for (size_t j = 0; j < db_.size(); ++j) {
+      DBlock& b = db_[j];
       if (b.im2col) alloc_conv(b.c1x); else alloc_conv(b.c1);
       alloc_conv(b.c2);
       if (b.learn_sc) alloc_conv(b.sc);
+      b.wp4dg = nullptr;
+      if (dgrad_pool_ && j > 0 && b.down && b.c2.ksz == 3 && tc_geometry_ok(b.hout, b.hout)) {
+        b.wp4dg = A.get<char>((size_t)16 * b.cout * b.cout * 2);
+        ++ndg;
+      }
     }
+    fold_jobs_dd_ = ndg ? A.get<FoldJob>(ndg) : nullptr;
     alloc_lin(dlin_);
     demb_hat_ = A.get<float>((size_t)cfg_.n_classes * cdl_);
     for (AttnL* at : {&gattn_, &dattn_}) {
@@ -1650,6 +1661,29 @@ class Engine final : public EngineBase {
       }
       fold_tiles_ = tiles;
       CK(cudaMemcpyAsync(fold_jobs_d_, fj.data(), fj.size() * sizeof(FoldJob), cudaMemcpyHostToDevice, st_));
+    }
+    // D's pooled-block conv2 input-gradient kernels (transposed, flipped, folded)
+    std::vector<FoldJob> fd;
+    if (fold_jobs_dd_) {
+      int tiles = 0;
+      for (DBlock& b : db_) {
+        if (!b.wp4dg) continue;
+        const PEntry& e = D_.E[b.c2.w];
+        FoldJob j{};
+        j.w = D_.p + e.off;
+        j.inv_sigma = D_.sigma + 2 * e.job + 1;
+        j.dst0 = static_cast<bf16*>(b.wp4dg);
+        j.dst1 = nullptr;
+        j.Cout = b.cout;   // output channels of the input-gradient conv = conv2's input channels
+        j.Cin = b.cout;
+        j.tile0 = tiles;
+        j.tf = 1;
+        tiles += ceil_div(b.cout, 32) * ceil_div(b.cout, 32);
+        fd.push_back(j);
+      }
+      fold_tiles_dd_ = tiles;
+      fold_njobs_dd_ = (int)fd.size();
+      CK(cudaMemcpyAsync(fold_jobs_dd_, fd.data(), fd.size() * sizeof(FoldJob), cudaMemcpyHostToDevice, st_));
     }
     return sync_ok();
   }
@@ -2422,6 +2456,8 @@ class Engine final : public EngineBase {
   // ------------------------------------------------------------------ D backward (A8-A11)
   // want_w: weight grads (D step); want_dimg: gradient down to the image (G step)
   paragan_status d_backward(int n, bool want_w, bool want_dimg) {
+    if (fold_njobs_dd_)   // D's W/sigma of this step, folded for the pooled blocks' conv2 input gradient
+      CK(fold_up2_grouped(fold_jobs_dd_, fold_njobs_dd_, fold_tiles_dd_, false, st_));
     const DBlock& last = db_.back();
     const void* hlast = last.attn ? attn_out_[1] : last.out;
     void* cur = tmp(0);   // gradient w.r.t. the current block output
@@ -2442,13 +2478,17 @@ class Engine final : public EngineBase {
         ic = k;
         cur = tmp(k);
       }
-      // dt: gradient at the conv2 output (full res)
+      // dt: gradient at the conv2 output (full res) = up2(cur) / 4 behind the pool.  With the phase kernel
+      // (R37) conv2's input gradient is conv3x3^T(up2(cur)) / 4 straight from the pooled gradient, and dt is
+      // only materialised for the weight gradients
+      const bool pool_dg = b.down && j > 0 && b.learn_sc && b.sc.ksz == 1 && b.wp4dg != nullptr;
       int it;
       void* dt;
       if (b.down) {
         it = other(ic);
         dt = tmp(it);
-        CK(avgpool2_bwd<T>(static_cast<const T*>(cur), n, H, H, b.cout, nullptr, static_cast<T*>(dt), b.cout, st_));
+        if (!pool_dg || want_w)
+          CK(avgpool2_bwd<T>(static_cast<const T*>(cur), n, H, H, b.cout, nullptr, static_cast<T*>(dt), b.cout, st_));
       } else {
         it = ic;
         dt = cur;
@@ -2457,7 +2497,22 @@ class Engine final : public EngineBase {
       const int ir1 = other(ic, it);
       void* dr1 = tmp(ir1);
       // gradient at the conv1 output: dgrad(conv2) masked by relu'(c1) in the epilogue
-      CKS(conv_dgrad(dt, n, H, b.c2, dr1, nullptr, nullptr, b.r1));
+      if (pool_dg) {
+        if constexpr (kBF) {
+          TcEpilogue e;
+          e.alpha = quarter_;
+          e.relu_ref = b.r1;
+          e.out = dr1;
+          const double fl = 2.0 * n * H * H * 9.0 * b.cout * b.cout;
+          const double fx = 2.0 * n * Ho * Ho * 16.0 * b.cout * b.cout;
+          char what[48];
+          std::snprintf(what, sizeof(what), "dgrad-pool n%d %dx%d %d->%d", n, H, H, b.cout, b.cout);
+          CK(timed(0, fl, [&] { return tc_conv_fprop_up2(cur, n, Ho, Ho, b.cout, b.wp4dg, b.cout, e, st_); }, what,
+                   fx));
+        }
+      } else {
+        CKS(conv_dgrad(dt, n, H, b.c2, dr1, nullptr, nullptr, b.r1));
+      }
       if (want_w) {
         CKS(conv_wgrad(D_, b.r1, dt, n, H, b.c2, b.c2.b));
       }
@@ -2667,6 +2722,9 @@ class Engine final : public EngineBase {
   std::vector<GraphEntry> graphs_;   // CUDA-graph step cache (run_graphed)
   bool graphs_on_ = false;
   FoldJob* fold_jobs_d_ = nullptr;   // G conv1 fold table (sub-pixel mode)
+  FoldJob* fold_jobs_dd_ = nullptr;  // D pooled-block conv2 input-gradient fold table
+  int fold_tiles_dd_ = 0, fold_njobs_dd_ = 0;
+  bool dgrad_pool_ = false;          // D conv2's input gradient behind the pool through the phase kernel (R37)
   paragan_stats* stats_dev_ = nullptr;   // stats_async staging
   int fold_tiles_ = 0;
   bool thin_tc_ = false;  // G's output layer on the tensor cores via bf16 splits (R36; BF16 mode)

@@ -3189,7 +3189,8 @@ __global__ void __launch_bounds__(256) k_fold_up2_grouped(const FoldJob* __restr
     if (o >= jb.Cout || c >= jb.Cin) continue;
     float t9[9];
 #pragma unroll
-    for (int k = 0; k < 9; ++k) t9[k] = jb.w[((long long)o * 9 + k) * jb.Cin + c];
+    for (int k = 0; k < 9; ++k)
+      t9[k] = jb.tf ? jb.w[((long long)c * 9 + (8 - k)) * jb.Cout + o] : jb.w[((long long)o * 9 + k) * jb.Cin + c];
 #pragma unroll
     for (int ph = 0; ph < 4; ++ph) {
       const int a = ph >> 1, b = ph & 1;

@@ -155,7 +155,8 @@ struct FoldJob {
   const float* inv_sigma;
   bf16* dst0;
   bf16* dst1;
-  int Cout, Cin, tile0, pad;
+  int Cout, Cin, tile0;
+  int tf;   // 1: fold the input-gradient kernel of w (w is [Cin][9][Cout]; tap t reads w[c][8 - t][o])
 };
 cudaError_t fold_up2_grouped(const FoldJob* jobs_d, int njobs, int tiles, bool dgrad, cudaStream_t st);
 

@@ -209,6 +209,16 @@ __device__ __forceinline__ void epilogue_loop(const TcFpropArgs& a, const CUtens
     }
     const long long m = (long long)mt * kTileM + row;
     const bool valid = m < a.M;
+    // the ReLU-mask reference row: the output pixel itself, or in sub-pixel mode the full-resolution pixel
+    // (2i + a, 2j + b) that low-resolution pixel m writes in output phase (a, b)
+    long long rrow = m;
+    if (CG == 2 && a.phases > 1 && a.relu_ref && valid) {
+      const int hw = a.H * a.W;
+      const int n = (int)(m / hw);
+      const int r = (int)(m - (long long)n * hw);
+      const int i = r / a.W, jj = r - i * a.W;
+      rrow = ((long long)(n * 2 * a.H + 2 * i + (phase >> 1)) * (2 * a.W)) + 2 * jj + (phase & 1);
+    }
     long long rbase = 0;
     if (valid && a.residual) {
       if (a.res_mode == 2) {   // residual stored at half resolution (nearest x2 upsample)
@@ -228,7 +238,7 @@ __device__ __forceinline__ void epilogue_loop(const TcFpropArgs& a, const CUtens
     if (valid) {
       if (a.relu_ref) {
         side = reinterpret_cast<const bf16*>(a.relu_ref);
-        sbase = m * a.ldo;
+        sbase = rrow * a.ldo;
       } else if (a.residual) {
         side = reinterpret_cast<const bf16*>(a.residual);
         sbase = rbase;
@@ -331,7 +341,7 @@ __device__ __forceinline__ void epilogue_loop(const TcFpropArgs& a, const CUtens
             const bool ok = c < a.Cout;
             float t = v[j] * alpha;
             if (a.relu_ref && ok)
-              t = __bfloat162float(reinterpret_cast<const bf16*>(a.relu_ref)[m * a.ldo + c]) > 0.0f ? t : 0.0f;
+              t = __bfloat162float(reinterpret_cast<const bf16*>(a.relu_ref)[rrow * a.ldo + c]) > 0.0f ? t : 0.0f;
             if (a.bias && ok) t += bias_smem ? sbias[c] : __ldg(a.bias + c);
             if (a.residual && ok) t += __bfloat162float(reinterpret_cast<const bf16*>(a.residual)[rbase + c]);
             if (a.relu_out) t = fmaxf(t, 0.0f);
@@ -1729,7 +1739,8 @@ cudaError_t tc_conv_fprop(const void* x, int N, int H, int W, int Cin, const voi
 cudaError_t tc_conv_fprop_up2(const void* x, int N, int H, int W, int Cin, const void* wpack4, int Cout,
                               const TcEpilogue& epi, cudaStream_t st) {
   if (Cin % 8 || Cout % 8 || ((uintptr_t)x & 15) || ((uintptr_t)wpack4 & 15) || ((uintptr_t)epi.out & 15) ||
-      !tileable(H, W) || epi.residual || epi.relu_ref || epi.out_f32 || (epi.ldo && epi.ldo != Cout))
+      !tileable(H, W) || epi.residual || epi.out_f32 || (epi.ldo && epi.ldo != Cout) ||
+      ((uintptr_t)epi.relu_ref & 15))
     return cudaErrorInvalidValue;
   const int bn = pick_bn(Cout);
   TcFpropArgs a{};
@@ -1745,6 +1756,7 @@ cudaError_t tc_conv_fprop_up2(const void* x, int N, int H, int W, int Cin, const
   a.n_tiles = ceil_div(Cout, bn);
   a.bias = epi.bias;
   a.alpha = epi.alpha;
+  a.relu_ref = epi.relu_ref;   // full-resolution [N][2H][2W][Cout] (the epilogue maps each phase's pixel)
   a.out = epi.out;
   a.ldo = Cout;
   a.ldr = Cout;
