@@ -1241,7 +1241,8 @@ class Engine final : public EngineBase {
       alloc_conv(b.c2);
       if (b.learn_sc) alloc_conv(b.sc);
       b.wp4dg = nullptr;
-      if (dgrad_pool_ && j > 0 && b.down && b.c2.ksz == 3 && tc_geometry_ok(b.hout, b.hout)) {
+      if (dgrad_pool_ && b.down && b.c2.ksz == 3 && tc_geometry_ok(b.hout, b.hout) &&
+          (j == 0 || (b.learn_sc && b.sc.ksz == 1))) {
         b.wp4dg = A.get<char>((size_t)16 * b.cout * b.cout * 2);
         ++ndg;
       }
@@ -2481,7 +2482,8 @@ class Engine final : public EngineBase {
       // dt: gradient at the conv2 output (full res) = up2(cur) / 4 behind the pool.  With the phase kernel
       // (R37) conv2's input gradient is conv3x3^T(up2(cur)) / 4 straight from the pooled gradient, and dt is
       // only materialised for the weight gradients
-      const bool pool_dg = b.down && j > 0 && b.learn_sc && b.sc.ksz == 1 && b.wp4dg != nullptr;
+      // (block 0's skip gradient comes from the pooled gradient too; later blocks need the 1x1 shortcut)
+      const bool pool_dg = b.down && b.wp4dg != nullptr;
       int it;
       void* dt;
       if (b.down) {
