@@ -28,6 +28,7 @@ bn_apply_bulk|k_bn_apply_relu_bulk|4
 bn_bwd_apply_bulk|k_bn_bwd_apply_bulk|2
 bn_bwd_reduce_bulk|k_bn_bwd_reduce_bulk|2
 cg2_96_3|k_conv_fprop_cg2<.int.96, .int.3>|1
+cg2_96_2|k_conv_fprop_cg2<.int.96, .int.2>|2
 out_conv_fwd|k_out_conv_fwd|1
 out_conv_bwd|k_out_conv_bwd|0""".splitlines()
 want = sys.argv[1].split()
