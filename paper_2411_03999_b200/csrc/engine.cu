@@ -1241,8 +1241,10 @@ class Engine final : public EngineBase {
       alloc_conv(b.c2);
       if (b.learn_sc) alloc_conv(b.sc);
       b.wp4dg = nullptr;
-      if (dgrad_pool_ && b.down && b.c2.ksz == 3 && tc_geometry_ok(b.hout, b.hout) &&
-          (j == 0 || (b.learn_sc && b.sc.ksz == 1))) {
+      // (not D's first block: its 96-channel phase conv at 128^2 measured slower than the plain dgrad,
+      // 1.47 vs 1.37 ms at n = 512)
+      if (dgrad_pool_ && j > 0 && b.down && b.c2.ksz == 3 && tc_geometry_ok(b.hout, b.hout) && b.learn_sc &&
+          b.sc.ksz == 1) {
         b.wp4dg = A.get<char>((size_t)16 * b.cout * b.cout * 2);
         ++ndg;
       }
@@ -2482,7 +2484,6 @@ class Engine final : public EngineBase {
       // dt: gradient at the conv2 output (full res) = up2(cur) / 4 behind the pool.  With the phase kernel
       // (R37) conv2's input gradient is conv3x3^T(up2(cur)) / 4 straight from the pooled gradient, and dt is
       // only materialised for the weight gradients
-      // (block 0's skip gradient comes from the pooled gradient too; later blocks need the 1x1 shortcut)
       const bool pool_dg = b.down && b.wp4dg != nullptr;
       int it;
       void* dt;
