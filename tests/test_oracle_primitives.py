@@ -352,6 +352,28 @@ def test_up2_conv_phase_decomposition_is_conv_of_upsampled():
     assert sorted({r for r, _ in nz}) == [1, 2, 3, 4] and sorted({c for _, c in nz}) == [3, 4, 5, 6]
 
 
+def test_pooled_block_input_gradient_is_phase_conv_of_pooled_gradient():
+    """R37: behind a 2x2 average pool the conv's output gradient is up2(g)/4, so its input gradient equals the
+    sub-pixel phase conv of the pooled gradient g with the flipped, transposed kernel K[c][o][r][s] =
+    W[o][c][2-r][2-s], divided by 4 — checked in fp64 against autograd through avgpool2(conv2d(x, W)).  The 1x1
+    shortcut's input gradient commutes with the pool's adjoint the same way (up2(sc^T g)/4)."""
+    rng = np.random.default_rng(13)
+    x = torch.from_numpy(rng.standard_normal((2, 5, 8, 6))).requires_grad_(True)
+    w = torch.from_numpy(rng.standard_normal((4, 5, 3, 3)))
+    g = torch.from_numpy(rng.standard_normal((2, 4, 4, 3)))
+    pooled = torch.nn.functional.avg_pool2d(ops.conv2d(x, w, None), 2)
+    (want,) = torch.autograd.grad((pooled * g).sum(), x)
+    k = w.flip(2, 3).transpose(0, 1).contiguous()
+    got = ops.up2_conv3x3_phases(g, k, None) / 4.0
+    assert torch.allclose(got, want, rtol=1e-12, atol=1e-12)
+    # the 1x1 shortcut
+    x1 = torch.from_numpy(rng.standard_normal((2, 5, 8, 6))).requires_grad_(True)
+    w1 = torch.from_numpy(rng.standard_normal((4, 5, 1, 1)))
+    (want1,) = torch.autograd.grad((torch.nn.functional.avg_pool2d(ops.conv2d(x1, w1, None), 2) * g).sum(), x1)
+    got1 = ops.up2(ops.conv2d(g, w1.transpose(0, 1).contiguous(), None)) / 4.0
+    assert torch.allclose(got1, want1, rtol=1e-12, atol=1e-12)
+
+
 # ------------------------------------------------- sampled conv definitions (oracle/sampled.py)
 def test_sampled_conv_definitions_match_full_oracle():
     """oracle/sampled.py (used by the full-size GPU tests) against the full fp64 conv of ops.conv2d and
