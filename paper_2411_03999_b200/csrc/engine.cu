@@ -163,6 +163,8 @@ struct DBlock {
   ConvL c1, c2, sc, c1x;
   void *x, *rx, *c1o, *r1, *t, *xp, *s, *out, *xi;
   void* wp4dg = nullptr;   // conv2's input-gradient kernel folded into the four phases (pooled blocks)
+  void* wp4f = nullptr;    // conv2 + 2x2 pool as a 16-tap stride-2 conv, phase-major (R38; pooled blocks)
+  bool dg_phase = false;   // conv2's input gradient through wp4dg (R37); else wp4dg is only the fold's scratch
 };
 
 int round8(int x) { return (x + 7) / 8 * 8; }
@@ -230,6 +232,10 @@ class Engine final : public EngineBase {
     subpix_ = kBF && (sp == nullptr || std::atoi(sp) != 0);
     const char* dgp = std::getenv("PARAGAN_DGRAD_UP2");
     dgrad_pool_ = subpix_ && (dgp == nullptr || std::atoi(dgp) != 0);
+    const char* pfw = std::getenv("PARAGAN_POOL_FWD");
+    pool_fwd_ = dgrad_pool_ && (pfw == nullptr || std::atoi(pfw) != 0);
+    const char* pf0 = std::getenv("PARAGAN_POOL_FWD0");
+    pool_fwd0_ = pool_fwd_ && pf0 != nullptr && std::atoi(pf0) != 0;
     const char* gr = std::getenv("PARAGAN_GRAPHS");
     graphs_on_ = gr == nullptr || std::atoi(gr) != 0;
     const char* tt = std::getenv("PARAGAN_THIN_TC");
@@ -1246,6 +1252,12 @@ class Engine final : public EngineBase {
       if (dgrad_pool_ && j > 0 && b.down && b.c2.ksz == 3 && tc_geometry_ok(b.hout, b.hout) && b.learn_sc &&
           b.sc.ksz == 1) {
         b.wp4dg = A.get<char>((size_t)16 * b.cout * b.cout * 2);
+        b.wp4f = pool_fwd_ ? A.get<char>((size_t)16 * b.cout * b.cout * 2) : nullptr;
+        b.dg_phase = true;
+        ++ndg;
+      } else if (pool_fwd0_ && j == 0 && b.down && b.c2.ksz == 3 && tc_geometry_ok(b.hout, b.hout)) {
+        b.wp4dg = A.get<char>((size_t)16 * b.cout * b.cout * 2);
+        b.wp4f = A.get<char>((size_t)16 * b.cout * b.cout * 2);
         ++ndg;
       }
     }
@@ -1676,7 +1688,7 @@ class Engine final : public EngineBase {
         j.w = D_.p + e.off;
         j.inv_sigma = D_.sigma + 2 * e.job + 1;
         j.dst0 = static_cast<bf16*>(b.wp4dg);
-        j.dst1 = nullptr;
+        j.dst1 = static_cast<bf16*>(b.wp4f);   // same fold, [Cin][16][Cout] for the pooled forward (R38)
         j.Cout = b.cout;   // output channels of the input-gradient conv = conv2's input channels
         j.Cin = b.cout;
         j.tile0 = tiles;
@@ -2397,7 +2409,27 @@ class Engine final : public EngineBase {
   }
 
   // ------------------------------------------------------------------ D forward (A7)
+  // R38: out = 0.25 * up2^T(conv3x3^T_K(r1)) + b + skip at half resolution (K = conv2's flipped, transposed kernel
+  // folded per phase): conv2 + 2x2 average pool as a 16-tap stride-2 conv over the four input phases of r1
+  paragan_status pool_fwd_conv(DBlock& b, int n, const void* skip) {
+    const int H = b.hin, Ho = b.hout;
+    TcEpilogue e;
+    e.alpha = quarter_;
+    e.bias = D_.P(b.c2.b);
+    e.residual = skip;
+    e.res_mode = 1;
+    e.out = b.out;
+    const double fl = 2.0 * n * H * H * 9.0 * b.cout * b.cout;
+    const double fx = 2.0 * n * Ho * Ho * 16.0 * b.cout * b.cout;
+    char what[48];
+    std::snprintf(what, sizeof(what), "fwd-pool n%d %dx%d %d->%d", n, H, H, b.cout, b.cout);
+    CK(timed(0, fl, [&] { return tc_conv_dgrad_up2(b.r1, n, Ho, Ho, b.cout, b.wp4f, b.cout, e, st_); }, what, fx));
+    return PARAGAN_OK;
+  }
   paragan_status d_forward(int n) {
+    // D's W/sigma of this step folded for the pooled blocks: conv2's input gradient (R37, used by d_backward
+    // with the same weights) and the pooled forward (R38)
+    if (fold_njobs_dd_) CK(fold_up2_grouped(fold_jobs_dd_, fold_njobs_dd_, fold_tiles_dd_, pool_fwd_, st_));
     bool rx_ready = false;   // the previous block's pooling already wrote relu(x) into this block's rx
     for (size_t j = 0; j < db_.size(); ++j) {
       DBlock& b = db_[j];
@@ -2423,10 +2455,21 @@ class Engine final : public EngineBase {
         // skip: avgpool the image, then 1x1 conv (block 0 has no pre-activation)
         CK(avgpool2<T>(static_cast<const T*>(b.x), n, H, H, b.cin_x, b.cin_x, nullptr, static_cast<T*>(b.xp), st_));
         CKS(conv_fwd(b.xp, n, Ho, b.sc, b.s, D_.P(b.sc.b), nullptr, 0));
-        CKS(conv_fwd(b.r1, n, H, b.c2, b.t, D_.P(b.c2.b), nullptr, 0));
-        CK(avgpool2<T>(static_cast<const T*>(b.t), n, H, H, b.cout, b.cout, static_cast<const T*>(b.s),
-                       static_cast<T*>(b.out), st_, next_rx));
-        rx_ready = next_rx != nullptr;
+        if (b.wp4f) {
+          if constexpr (kBF) CKS(pool_fwd_conv(b, n, b.s));   // R38
+        } else {
+          CKS(conv_fwd(b.r1, n, H, b.c2, b.t, D_.P(b.c2.b), nullptr, 0));
+          CK(avgpool2<T>(static_cast<const T*>(b.t), n, H, H, b.cout, b.cout, static_cast<const T*>(b.s),
+                         static_cast<T*>(b.out), st_, next_rx));
+          rx_ready = next_rx != nullptr;
+        }
+      } else if (b.wp4f) {
+        // R38: avgpool(conv2(r1) + sc(x) + b) = conv2 at stride 2 folded into 16 taps over the four input phases
+        // (x 0.25 in the epilogue) + sc(avgpool(x)) + b, all at half resolution: 16 / 4 = 4 full-resolution taps
+        // of MACs instead of 9, and the 1x1 shortcut on a quarter of the pixels
+        CK(avgpool2<T>(static_cast<const T*>(b.x), n, H, H, b.cin_x, b.cin_x, nullptr, static_cast<T*>(b.xp), st_));
+        CKS(conv_fwd(b.xp, n, Ho, b.sc, b.s, D_.P(b.sc.b), nullptr, 0));
+        if constexpr (kBF) CKS(pool_fwd_conv(b, n, b.s));
       } else {
         const void* skip = b.x;
         if (b.learn_sc) {
@@ -2459,8 +2502,6 @@ class Engine final : public EngineBase {
   // ------------------------------------------------------------------ D backward (A8-A11)
   // want_w: weight grads (D step); want_dimg: gradient down to the image (G step)
   paragan_status d_backward(int n, bool want_w, bool want_dimg) {
-    if (fold_njobs_dd_)   // D's W/sigma of this step, folded for the pooled blocks' conv2 input gradient
-      CK(fold_up2_grouped(fold_jobs_dd_, fold_njobs_dd_, fold_tiles_dd_, false, st_));
     const DBlock& last = db_.back();
     const void* hlast = last.attn ? attn_out_[1] : last.out;
     void* cur = tmp(0);   // gradient w.r.t. the current block output
@@ -2484,7 +2525,7 @@ class Engine final : public EngineBase {
       // dt: gradient at the conv2 output (full res) = up2(cur) / 4 behind the pool.  With the phase kernel
       // (R37) conv2's input gradient is conv3x3^T(up2(cur)) / 4 straight from the pooled gradient, and dt is
       // only materialised for the weight gradients
-      const bool pool_dg = b.down && b.wp4dg != nullptr;
+      const bool pool_dg = b.down && b.wp4dg != nullptr && b.dg_phase;
       int it;
       void* dt;
       if (b.down) {
@@ -2540,7 +2581,10 @@ class Engine final : public EngineBase {
         }
       } else if (b.learn_sc) {
         if (want_w) {
-          CKS(conv_wgrad(D_, b.x, dt, n, H, b.sc, b.sc.b));
+          // with the pooled forward (R38) avgpool(x) is resident: sum_full (up2(cur)/4) x = sum_half cur avgpool(x),
+          // the 1x1 weight gradient on a quarter of the pixels
+          if (b.wp4f) CKS(conv_wgrad(D_, b.xp, cur, n, Ho, b.sc, b.sc.b));
+          else CKS(conv_wgrad(D_, b.x, dt, n, H, b.sc, b.sc.b));
         }
         if (need_dx) {
           isk = other(ic, it, ir1);
@@ -2728,6 +2772,8 @@ class Engine final : public EngineBase {
   FoldJob* fold_jobs_dd_ = nullptr;  // D pooled-block conv2 input-gradient fold table
   int fold_tiles_dd_ = 0, fold_njobs_dd_ = 0;
   bool dgrad_pool_ = false;          // D conv2's input gradient behind the pool through the phase kernel (R37)
+  bool pool_fwd_ = false;            // D conv2 + pool as a stride-2 phase conv at half resolution (R38)
+  bool pool_fwd0_ = false;           // ... also for D's first block (96 channels at 128^2)
   paragan_stats* stats_dev_ = nullptr;   // stats_async staging
   int fold_tiles_ = 0;
   bool thin_tc_ = false;  // G's output layer on the tensor cores via bf16 splits (R36; BF16 mode)

@@ -374,6 +374,27 @@ def test_pooled_block_input_gradient_is_phase_conv_of_pooled_gradient():
     assert torch.allclose(got1, want1, rtol=1e-12, atol=1e-12)
 
 
+def test_pooled_block_forward_is_adjoint_of_phase_conv():
+    """R38: avgpool2(conv3x3_W(x)) equals a quarter of the adjoint (up2^T conv^T) of the sub-pixel phase conv
+    with the flipped, transposed kernel K = W[o][c][2-r][2-s]^T — the 16-tap stride-2 form the pooled forward
+    runs through the phase input-gradient kernel — in fp64, the adjoint taken by autograd."""
+    rng = np.random.default_rng(17)
+    x = torch.from_numpy(rng.standard_normal((2, 5, 8, 6)))
+    w = torch.from_numpy(rng.standard_normal((4, 5, 3, 3)))
+    want = torch.nn.functional.avg_pool2d(ops.conv2d(x, w, None), 2)
+    k = w.flip(2, 3).transpose(0, 1).contiguous()   # [5][4][3][3]: maps 4 channels -> 5
+    g = torch.zeros((2, 4, 4, 3), dtype=torch.float64, requires_grad=True)
+    (got,) = torch.autograd.grad((ops.up2_conv3x3_phases(g, k, None) * x).sum(), g)
+    assert torch.allclose(got / 4.0, want, rtol=1e-12, atol=1e-12)
+    # the 1x1 shortcut's weight gradient behind the pool on the pooled input: sum_full (up2(g)/4) x = sum_half g
+    # avgpool(x)
+    gp = torch.from_numpy(rng.standard_normal((2, 4, 4, 3)))
+    w1 = torch.zeros((4, 5, 1, 1), dtype=torch.float64, requires_grad=True)
+    (want1,) = torch.autograd.grad((torch.nn.functional.avg_pool2d(ops.conv2d(x, w1, None), 2) * gp).sum(), w1)
+    got1 = torch.einsum("nohw,nchw->oc", gp, torch.nn.functional.avg_pool2d(x, 2))[:, :, None, None]
+    assert torch.allclose(got1, want1, rtol=1e-12, atol=1e-12)
+
+
 # ------------------------------------------------- sampled conv definitions (oracle/sampled.py)
 def test_sampled_conv_definitions_match_full_oracle():
     """oracle/sampled.py (used by the full-size GPU tests) against the full fp64 conv of ops.conv2d and
