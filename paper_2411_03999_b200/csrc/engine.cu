@@ -235,7 +235,7 @@ class Engine final : public EngineBase {
     const char* pfw = std::getenv("PARAGAN_POOL_FWD");
     pool_fwd_ = dgrad_pool_ && (pfw == nullptr || std::atoi(pfw) != 0);
     const char* pf0 = std::getenv("PARAGAN_POOL_FWD0");
-    pool_fwd0_ = pool_fwd_ && pf0 != nullptr && std::atoi(pf0) != 0;
+    pool_fwd0_ = pool_fwd_ && (pf0 == nullptr || std::atoi(pf0) != 0);
     const char* gr = std::getenv("PARAGAN_GRAPHS");
     graphs_on_ = gr == nullptr || std::atoi(gr) != 0;
     const char* tt = std::getenv("PARAGAN_THIN_TC");
