@@ -343,6 +343,33 @@ def test_conv_up2_dgrad_integer_exact(shape):
     assert np.array_equal(got, want_b), np.argwhere(got != want_b)[:5]
 
 
+# D's pooled blocks at small sizes: (n, full-resolution h, w, channels) — conv2 is square (C -> C)
+POOL_FWD_SHAPES = [(2, 8, 8, 96), (1, 16, 16, 192), (3, 8, 8, 64), (1, 32, 32, 128)]
+
+
+@pytest.mark.parametrize("shape", POOL_FWD_SHAPES)
+def test_pooled_forward_through_phase_dgrad_kernel_integer_exact(shape):
+    """R38: 4 * avgpool2(conv3x3_W(x)) is the phase input-gradient kernel applied to x with the
+    flipped, transposed kernel W'[c][t][o] = W[o][8 - t][c] — the launch D's pooled forward makes (the engine
+    then scales by 0.25 in the epilogue).  Against fp64 conv + 2x2 sum pooling of the oracle, bf16 rounding of
+    the exact integer result, bit for bit."""
+    n, H, W, C = shape
+    rng = np.random.default_rng(H * 41 + C)
+    x = rng.integers(-2, 3, size=(n, H, W, C)).astype(np.float32)
+    wt = rng.integers(-1, 2, size=(C, 9, C)).astype(np.float32)   # [o][t][c]
+    xt = torch.from_numpy(x).double().permute(0, 3, 1, 2)
+    wv = torch.from_numpy(wt).double().reshape(C, 3, 3, C).permute(0, 3, 1, 2)
+    want = (torch.nn.functional.avg_pool2d(ops.conv2d(xt, wv, None), 2) * 4.0).permute(0, 2, 3, 1).numpy()
+    assert np.abs(want).max() < 2 ** 24
+    wflip = np.ascontiguousarray(wt[:, ::-1, :].transpose(2, 1, 0))   # [c][t][o] = W[o][8 - t][c]
+    y = torch.full((n, H // 2, W // 2, C), float("nan"), dtype=torch.float32, device=DEV).to(torch.bfloat16)
+    api.op_conv_up2_dgrad(_bf16_np(x).to(DEV), torch.from_numpy(wflip).to(DEV), C, y)
+    torch.cuda.synchronize()
+    got = y.float().cpu().numpy()
+    want_b = torch.from_numpy(want.astype(np.float32)).to(torch.bfloat16).float().numpy()
+    assert np.array_equal(got, want_b), np.argwhere(got != want_b)[:5]
+
+
 @pytest.mark.parametrize("shape", UP2_SHAPES)
 def test_conv_up2_wgrad_integer_exact(shape):
     """Weight (and bias) gradient of conv3x3(up2(x)) from the low-resolution x through the 16 folded
