@@ -2438,8 +2438,16 @@ class Engine final : public EngineBase {
       const void* cin = b.x;
       // the next block's pre-activation relu(x) comes out of this block's pooling when nothing sits in between
       T* next_rx = (j + 1 < db_.size() && !b.attn) ? static_cast<T*>(db_[j + 1].rx) : nullptr;
+      bool xp_ready = false;   // R38 blocks: avgpool2(x) for the half-resolution shortcut
       if (j > 0) {
-        if (!rx_ready) CK(relu_copy<T>(static_cast<const T*>(b.x), static_cast<T*>(b.rx), Mi * b.cin_x, st_));
+        if (!rx_ready && b.wp4f && b.cin_x % 8 == 0) {
+          // relu(x) for conv1 and avgpool2(x) for the shortcut from one read of x (bit-identical to the two passes)
+          CK(avgpool2<T>(static_cast<const T*>(b.x), n, H, H, b.cin_x, b.cin_x, nullptr, static_cast<T*>(b.xp), st_,
+                         nullptr, static_cast<T*>(b.rx)));
+          xp_ready = true;
+        } else if (!rx_ready) {
+          CK(relu_copy<T>(static_cast<const T*>(b.x), static_cast<T*>(b.rx), Mi * b.cin_x, st_));
+        }
         cin = b.rx;
       }
       rx_ready = false;
@@ -2467,7 +2475,8 @@ class Engine final : public EngineBase {
         // R38: avgpool(conv2(r1) + sc(x) + b) = conv2 at stride 2 folded into 16 taps over the four input phases
         // (x 0.25 in the epilogue) + sc(avgpool(x)) + b, all at half resolution: 16 / 4 = 4 full-resolution taps
         // of MACs instead of 9, and the 1x1 shortcut on a quarter of the pixels
-        CK(avgpool2<T>(static_cast<const T*>(b.x), n, H, H, b.cin_x, b.cin_x, nullptr, static_cast<T*>(b.xp), st_));
+        if (!xp_ready)
+          CK(avgpool2<T>(static_cast<const T*>(b.x), n, H, H, b.cin_x, b.cin_x, nullptr, static_cast<T*>(b.xp), st_));
         CKS(conv_fwd(b.xp, n, Ho, b.sc, b.s, D_.P(b.sc.b), nullptr, 0));
         if constexpr (kBF) CKS(pool_fwd_conv(b, n, b.s));
       } else {

@@ -2085,7 +2085,7 @@ __global__ void k_relu_copy_v(const T* __restrict__ x, T* __restrict__ y, long l
 }
 template <typename T>
 __global__ void k_avgpool2_v(const T* __restrict__ x, int N, int H, int W, int C, int ldx, const T* __restrict__ add,
-                             T* __restrict__ y, T* __restrict__ y_relu) {
+                             T* __restrict__ y, T* __restrict__ y_relu, T* __restrict__ x_relu) {
   const unsigned Ho = H >> 1, Wo = W >> 1, G = C >> 3;
   const unsigned total = (unsigned)N * Ho * Wo * G;
   for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
@@ -2101,6 +2101,21 @@ __global__ void k_avgpool2_v(const T* __restrict__ x, int N, int H, int W, int C
     Vec8<T>::load(x + (b + 1) * ldx + g * 8, a1);
     Vec8<T>::load(x + (b + W) * ldx + g * 8, a2);
     Vec8<T>::load(x + (b + W + 1) * ldx + g * 8, a3);
+    if (x_relu) {   // relu(x) at full resolution from the same loads (the block's conv1 input)
+      float r[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = a0[j] > 0.0f ? a0[j] : 0.0f;
+      Vec8<T>::store(x_relu + b * ldx + g * 8, r);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = a1[j] > 0.0f ? a1[j] : 0.0f;
+      Vec8<T>::store(x_relu + (b + 1) * ldx + g * 8, r);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = a2[j] > 0.0f ? a2[j] : 0.0f;
+      Vec8<T>::store(x_relu + (b + W) * ldx + g * 8, r);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = a3[j] > 0.0f ? a3[j] : 0.0f;
+      Vec8<T>::store(x_relu + (b + W + 1) * ldx + g * 8, r);
+    }
     float ad[8];
     if (add) Vec8<T>::load(add + (long long)i * 8, ad);
 #pragma unroll
@@ -2453,7 +2468,7 @@ template cudaError_t bn_bwd_apply<bf16, float, bf16>(const bf16*, const float*, 
 #define PG_INST_T(T)                                                                                               \
   template cudaError_t relu_copy<T>(const T*, T*, long long, cudaStream_t);                                        \
   template cudaError_t relu_bwd<T>(const T*, const T*, const T*, T*, long long, cudaStream_t);                     \
-  template cudaError_t avgpool2<T>(const T*, int, int, int, int, int, const T*, T*, cudaStream_t, T*);                 \
+  template cudaError_t avgpool2<T>(const T*, int, int, int, int, int, const T*, T*, cudaStream_t, T*, T*);                 \
   template cudaError_t avgpool2_bwd<T>(const T*, int, int, int, int, const T*, T*, int, cudaStream_t);             \
   template cudaError_t up2_bwd<T>(const T*, int, int, int, int, T*, cudaStream_t);                                 \
   template cudaError_t col_sum<T>(const T*, long long, int, double*, int, float*, int, cudaStream_t);              \
@@ -2486,15 +2501,19 @@ cudaError_t relu_bwd(const T* dy, const T* ref, const T* add, T* dx, long long n
 }
 template <typename T>
 cudaError_t avgpool2(const T* x, int N, int H, int W, int C, int ldx, const T* add, T* y, cudaStream_t st,
-                     T* y_relu) {
+                     T* y_relu, T* x_relu) {
   const long long total = (long long)N * (H / 2) * (W / 2) * C;
   if (C % 8 == 0 && ldx % 8 == 0) {
-    k_avgpool2_v<T><<<grid_for(total / 8, 256), 256, 0, st>>>(x, N, H, W, C, ldx, add, y, y_relu);
+    k_avgpool2_v<T><<<grid_for(total / 8, 256), 256, 0, st>>>(x, N, H, W, C, ldx, add, y, y_relu, x_relu);
     return cudaGetLastError();
   }
   k_avgpool2<T><<<grid_for(total, 256), 256, 0, st>>>(x, N, H, W, C, ldx, add, y);
   PG_LAUNCH_CHECK();
-  if (y_relu) return relu_copy<T>(y, y_relu, total, st);
+  if (y_relu) {
+    const cudaError_t e = relu_copy<T>(y, y_relu, total, st);
+    if (e != cudaSuccess) return e;
+  }
+  if (x_relu) return relu_copy<T>(x, x_relu, (long long)N * H * W * C, st);   // (scalar path: ldx == C only)
   return cudaGetLastError();
 }
 template <typename T>

@@ -103,7 +103,8 @@ cudaError_t relu_bwd(const T* dy, const T* ref, const T* add, T* dx, long long n
 // y[N,H/2,W/2,C] = avgpool2(x) (+ add[N,H/2,W/2,C])
 template <typename T>
 cudaError_t avgpool2(const T* x, int N, int H, int W, int C, int ldx, const T* add, T* y, cudaStream_t st,
-                     T* y_relu = nullptr);   // y_relu (optional): relu(y) as well (the next D block's conv1 input)
+                     T* y_relu = nullptr,    // y_relu (optional): relu(y) as well (the next D block's conv1 input)
+                     T* x_relu = nullptr);   // x_relu (optional): relu(x) [N,H,W,ldx] from the same loads
 // dx[N,H,W,C] = 0.25 * dy[n,h/2,w/2,c]   (avgpool adjoint); optional add (same shape as dx)
 template <typename T>
 cudaError_t avgpool2_bwd(const T* dy, int N, int H, int W, int C, const T* add, T* dx, int lddx, cudaStream_t st);
